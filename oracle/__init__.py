@@ -1,0 +1,145 @@
+"""ORACLE - test infrastructure only.
+
+Plain CPU exact summation of binary64 (the oracle of DESIGN.md §3). Only
+``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package. It shares no code with the
+CUDA path (``paper_1605_05436_b200``) and never imports it.
+
+Two independent implementations of one definition (§2
+fixed-point view: the exact sum is an integer multiple of 2^-1074):
+  * O1  ``xsum_oracle.c``  big-integer limbs, threaded, any n   (this module)
+  * O2  ``oracle.pytwin``  Python ints / fractions, small n     (pins O1)
+Rounding: round-to-nearest ties-to-even of the exact sum (PAPER.md:172-179
+faithful; §5 PAPER.md:1066-1069 "correctly rounded").
+
+Every function here is pinned by ``tests/test_oracle_pins.py``; DESIGN.md lists
+the readings of the paper it follows (R1-R12).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+NLIMB = 34                    # 2176-bit two's complement image, little-endian u64 limbs
+F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT = 1, 2, 4, 8, 16
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "xsum_oracle.c")
+
+
+class _CResult(ctypes.Structure):
+    _fields_ = [("value", ctypes.c_double), ("direction", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("msb_exp", ctypes.c_int32), ("sign", ctypes.c_int32), ("count", ctypes.c_uint64),
+                ("sig53", ctypes.c_uint64), ("exp2", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+@dataclass(frozen=True)
+class Result:
+    value: float
+    bits: int            # uint64 bit pattern of value
+    direction: int       # sign(value - exact) of the finite part; 0 if a special is returned
+    flags: int
+    msb_exp: int | None  # floor(log2|exact|), None for an exact zero
+    sign: int
+    count: int
+    sig53: int           # unbounded-exponent rounding: |exact| ~= sig53 * 2^exp2
+    exp2: int
+
+
+def build() -> None:
+    if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-pthread", _SRC, "-o", _SO])
+
+
+_lib = None
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        p, u64, i32, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32
+        lib.oracle_sum.argtypes = [p, p, p, u64, i32]
+        lib.oracle_sum.restype = None
+        lib.oracle_round.argtypes = [p, u32, u64, ctypes.POINTER(_CResult)]
+        lib.oracle_round.restype = None
+        lib.oracle_limbs_add.argtypes = [p, p]
+        lib.oracle_limbs_add.restype = None
+        _lib = lib
+    return _lib
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+class Accumulator:
+    """Streaming exact sum: ``add`` chunks in any order, then ``result``."""
+
+    def __init__(self, nthreads: int | None = None):
+        self.limbs = np.zeros(NLIMB, dtype=np.uint64)
+        self._flags = ctypes.c_uint32(0)
+        self.count = 0
+        self.nthreads = nthreads or host_threads()
+
+    @property
+    def flags(self) -> int:
+        return int(self._flags.value)
+
+    def add(self, x: np.ndarray) -> "Accumulator":
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.size:
+            _L().oracle_sum(self.limbs.ctypes.data, ctypes.addressof(self._flags), x.ctypes.data,
+                            x.size, self.nthreads)
+        self.count += int(x.size)
+        return self
+
+    def merge(self, other: "Accumulator") -> "Accumulator":
+        _L().oracle_limbs_add(self.limbs.ctypes.data, other.limbs.ctypes.data)
+        self._flags.value |= other._flags.value
+        self.count += other.count
+        return self
+
+    def result(self) -> Result:
+        return round_limbs(self.limbs, self.flags, self.count)
+
+
+def round_limbs(limbs: np.ndarray, flags: int, count: int = 0) -> Result:
+    limbs = np.ascontiguousarray(limbs, dtype=np.uint64)
+    assert limbs.size == NLIMB
+    r = _CResult()
+    _L().oracle_round(limbs.ctypes.data, flags, count, ctypes.byref(r))
+    bits = int(np.array([r.value], dtype=np.float64).view(np.uint64)[0])
+    return Result(value=r.value, bits=bits, direction=r.direction, flags=r.flags,
+                  msb_exp=None if r.msb_exp == -(2 ** 31) else r.msb_exp, sign=r.sign,
+                  count=r.count, sig53=r.sig53, exp2=r.exp2)
+
+
+def exact_sum(x, nthreads: int | None = None) -> tuple[Result, np.ndarray]:
+    """(rounded result, 34-limb two's complement image of sum(x)*2^1074)."""
+    acc = Accumulator(nthreads).add(np.asarray(x, dtype=np.float64))
+    return acc.result(), acc.limbs.copy()
+
+
+def limbs_to_int(limbs: np.ndarray) -> int:
+    """Signed Python int of a 34-limb two's complement image."""
+    v = 0
+    for L in reversed(range(NLIMB)):
+        v = (v << 64) | int(limbs[L])
+    if v >> (64 * NLIMB - 1):
+        v -= 1 << (64 * NLIMB)
+    return v
+
+
+def int_to_limbs(v: int) -> np.ndarray:
+    v &= (1 << (64 * NLIMB)) - 1
+    return np.array([(v >> (64 * L)) & 0xFFFFFFFFFFFFFFFF for L in range(NLIMB)], dtype=np.uint64)

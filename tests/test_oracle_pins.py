@@ -1,0 +1,315 @@
+"""Pins of the oracle (O1 = oracle/xsum_oracle.c, O2 = oracle/pytwin.py) against
+things other than itself: hand-derived golden cases, exact rational brute force
+(Fraction(float) is exact; float(Fraction) is CPython's correctly rounded int
+division), math.fsum (Shewchuk, correctly rounded), invariants the problem fixes
+(permutation, x + (-x) = 0, 2^1023 + 1 - 2^1023 = 1, the set-equality zero-sum
+family of PAPER.md:812-839), the faithful-rounding bracket of PAPER.md:172-179,
+and Lemma 1 exhaustively at R = 8.
+"""
+from __future__ import annotations
+
+import math
+import os
+import random
+import re
+import struct
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import pytwin
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "rounding_edges.txt")
+
+
+def f2b(x: float) -> int:
+    return struct.unpack("<Q", struct.pack("<d", x))[0]
+
+
+def b2f(b: int) -> float:
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+def load_golden():
+    cases = []
+    with open(GOLDEN) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            name, ins, out, direction, cite = [p.strip() for p in line.split("|")]
+            xs = [b2f(int(h, 16)) for h in ins.split(",") if h.strip()]
+            cases.append((name, xs, int(out, 16), int(direction), cite))
+    return cases
+
+
+GOLDEN_CASES = load_golden()
+
+
+def exact_fraction(xs) -> Fraction:
+    return sum((Fraction(x) for x in xs), Fraction(0))
+
+
+def test_golden_file_has_citations():
+    assert len(GOLDEN_CASES) >= 20
+    for name, _, _, _, cite in GOLDEN_CASES:
+        assert re.search(r"PAPER\.md:\d+|SPEC\.md:\d+|\bR\d+\b|north_star", cite), name
+
+
+def test_golden_hex_literals_mean_what_they_say():
+    # the hex inputs in the golden file are the doubles named in the derivations
+    assert f2b(1e308) == 0x7FE1CCF385EBC8A0
+    assert f2b(math.pi) == 0x400921FB54442D18
+    assert f2b(2.0 ** -53) == 0x3CA0000000000000
+    assert f2b(2.0 ** 970) == 0x7C90000000000000
+    assert f2b(2.0 ** 1000) == 0x7E70000000000000
+    assert f2b(2.0 ** -1000) == 0x0170000000000000
+    assert f2b(5e-324) == 1
+    assert f2b(2.0 ** 53) == 0x4340000000000000
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES, ids=[c[0] for c in GOLDEN_CASES])
+def test_golden_o1(case):
+    name, xs, out_bits, direction, _ = case
+    r, _ = oracle.exact_sum(np.array(xs, dtype=np.float64))
+    assert r.bits == out_bits, f"{name}: {r.bits:016x} != {out_bits:016x}"
+    assert r.direction == direction
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES, ids=[c[0] for c in GOLDEN_CASES])
+def test_golden_o2(case):
+    name, xs, out_bits, direction, _ = case
+    v, d, _, _ = pytwin.exact_sum(xs)
+    assert f2b(v) == out_bits, name
+    assert d == direction
+
+
+def _random_double(rng: random.Random) -> float:
+    """Finite doubles over the whole range incl. subnormals, zeros, boundary exponents."""
+    kind = rng.random()
+    if kind < 0.1:
+        e = 0                                   # subnormal / zero
+    elif kind < 0.2:
+        e = rng.choice([1, 2, 1022, 1023, 1024, 2045, 2046])
+    else:
+        e = rng.randint(1, 2046)
+    m = rng.getrandbits(52) if rng.random() < 0.9 else rng.choice([0, 1, (1 << 52) - 1])
+    s = rng.getrandbits(1)
+    return b2f((s << 63) | (e << 52) | m)
+
+
+def _random_set(rng: random.Random, n: int) -> list[float]:
+    mode = rng.random()
+    if mode < 0.3:  # narrow exponent band -> many ties and cancellations
+        e0 = rng.randint(1, 2040)
+        xs = [b2f((rng.getrandbits(1) << 63) | (rng.randint(e0, e0 + 5) << 52) | rng.getrandbits(52))
+              for _ in range(n)]
+    elif mode < 0.45:  # add negations -> exact cancellation
+        half = [_random_double(rng) for _ in range((n + 1) // 2)]
+        xs = half + [-x for x in half[: n // 2]]
+        rng.shuffle(xs)
+    else:
+        xs = [_random_double(rng) for _ in range(n)]
+    return xs
+
+
+def test_o1_vs_exact_fraction_bruteforce():
+    """O1's image and rounding vs exact rationals (independent decoder: float.as_integer_ratio)."""
+    rng = random.Random(1605)
+    for trial in range(3000):
+        xs = _random_set(rng, rng.randint(0, 9))
+        r, limbs = oracle.exact_sum(np.array(xs, dtype=np.float64))
+        S = exact_fraction(xs)
+        A = S * (1 << 1074)
+        assert A.denominator == 1
+        assert oracle.limbs_to_int(limbs) == A.numerator, trial
+        try:
+            ref = float(S)
+        except OverflowError:
+            ref = math.inf if S > 0 else -math.inf
+        if ref == 0.0:
+            ref = 0.0
+        assert r.bits == f2b(ref), (trial, xs)
+        if S != 0 and not math.isinf(ref):
+            assert r.direction == (Fraction(ref) > S) - (Fraction(ref) < S)
+
+
+def test_o1_vs_fsum_in_range():
+    """math.fsum is correctly rounded (Shewchuk) when no intermediate overflows."""
+    rng = np.random.default_rng(7)
+    for trial in range(200):
+        n = int(rng.integers(1, 2000))
+        e = rng.integers(-300, 300, size=n).astype(np.float64)
+        x = rng.standard_normal(n) * np.exp2(e)
+        if trial % 3 == 0:
+            x = np.concatenate([x, -x[: n // 2]])
+        r, _ = oracle.exact_sum(x)
+        ref = math.fsum(x)
+        if ref == 0.0:
+            ref = 0.0
+        assert r.bits == f2b(ref)
+
+
+def test_o1_faithful_bracket():
+    """result is the largest double <= S or the smallest double >= S."""
+    rng = random.Random(11)
+    for _ in range(2000):
+        xs = _random_set(rng, rng.randint(1, 12))
+        r, limbs = oracle.exact_sum(np.array(xs))
+        if math.isinf(r.value):
+            continue
+        S = Fraction(oracle.limbs_to_int(limbs), 1 << 1074)
+        v = Fraction(r.value)
+        lo_f, hi_f = math.nextafter(r.value, -math.inf), math.nextafter(r.value, math.inf)
+        assert math.isinf(lo_f) or Fraction(lo_f) < S
+        assert math.isinf(hi_f) or S < Fraction(hi_f)
+        if v != S:   # RN: within half an ulp
+            ulp = Fraction(math.ulp(r.value))
+            assert abs(v - S) <= ulp / 2
+
+
+def test_o1_vs_o2_on_synth_prefixes():
+    import synth
+    for name in ("c1", "c2", "c4", "c5"):
+        x = synth.gen.generate(name, 12345, 20000)
+        r, limbs = oracle.exact_sum(x)
+        v, d, fl, A = pytwin.exact_sum(x.tolist())
+        assert [int(t) for t in limbs] == pytwin.limbs(A), name
+        assert r.bits == f2b(v) and r.direction == d and r.flags == fl, name
+    x = synth.gen.generate("c3", (1 << 28) - 5000, 10000, permute=False)  # pairs + tiny terms
+    r, limbs = oracle.exact_sum(x)
+    v, d, fl, A = pytwin.exact_sum(x.tolist())
+    assert [int(t) for t in limbs] == pytwin.limbs(A)
+    assert r.bits == f2b(v)
+
+
+def test_o1_permutation_and_thread_invariance():
+    rng = np.random.default_rng(3)
+    bits = rng.integers(0, 2 ** 63, size=200_000, dtype=np.uint64) & np.uint64(0xFFEFFFFFFFFFFFFF)
+    bits |= rng.integers(0, 2, size=bits.size, dtype=np.uint64) << np.uint64(63)
+    x = bits.view(np.float64)
+    r1, l1 = oracle.exact_sum(x, nthreads=1)
+    for nt in (2, 3, 8):
+        r, l = oracle.exact_sum(rng.permutation(x), nthreads=nt)
+        assert (l == l1).all() and r.bits == r1.bits and r.flags == r1.flags
+
+
+def test_o1_chunked_streaming_equals_whole():
+    import synth
+    x = synth.gen.generate("c2", 0, 100_000)
+    whole = oracle.exact_sum(x)[1]
+    acc = oracle.Accumulator()
+    for a, b in [(0, 1), (1, 777), (777, 50_000), (50_000, 100_000)]:
+        acc.add(x[a:b])
+    assert (acc.limbs == whole).all() and acc.count == 100_000
+    a1, a2 = oracle.Accumulator().add(x[:333]), oracle.Accumulator().add(x[333:])
+    assert (a1.merge(a2).limbs == whole).all()
+
+
+def test_x_plus_negx_is_plus_zero():
+    import synth
+    x = synth.gen.generate("c4", 0, 50_000)
+    y = np.concatenate([x, -x[::-1]])
+    r, limbs = oracle.exact_sum(y)
+    assert r.bits == 0 and not limbs.any() and r.direction == 0
+
+
+def test_set_equality_family():
+    """PAPER.md:812-839 (Theorem 1 lower bound): -2^(tau c_i) and +2^(tau d_i) sum to zero
+    iff the multisets C and D are equal; tau = smallest power of two > log n."""
+    rng = random.Random(5)
+    for trial in range(60):
+        n = rng.randint(1, 300)
+        tau = 1
+        while tau <= math.log2(max(n, 2)):
+            tau *= 2
+        cmax = (2046 - 1) // tau                 # keep tau*c inside the binary64 exponent range
+        C = [rng.randint(0, cmax) for _ in range(n)]
+        D = list(C)
+        rng.shuffle(D)
+        equal = trial % 2 == 0
+        if not equal:
+            j = rng.randrange(n)
+            D[j] = (D[j] + 1) % (cmax + 1)
+        # exponents tau*c relative to 2^-1074 (unbiased exponent tau*c - 1074)
+        xs = [-math.ldexp(1.0, tau * c - 1074) for c in C] + [math.ldexp(1.0, tau * d - 1074) for d in D]
+        rng.shuffle(xs)
+        r, limbs = oracle.exact_sum(np.array(xs))
+        assert (not limbs.any()) == (sorted(C) == sorted(D)), trial
+        if sorted(C) == sorted(D):
+            assert r.bits == 0
+
+
+def test_o2_rounding_matches_textbook_definition_on_boundaries():
+    """O2 (library rounding) vs O1 (bit-level RN-even) on values straddling every
+    rounding boundary shape: ties, near-ties, overflow threshold, subnormal/normal edge."""
+    rng = random.Random(99)
+    for _ in range(3000):
+        p = rng.randint(0, 2160)
+        sig = rng.getrandbits(min(p + 1, 60)) | (1 << min(p, 59))
+        A = sig << max(0, p - 59)
+        A += rng.choice([0, 1, -1, 1 << max(0, p - 53), (1 << max(0, p - 53)) - 1,
+                         (1 << max(0, p - 53)) + 1])
+        A *= rng.choice([1, -1])
+        r = oracle.round_limbs(oracle.int_to_limbs(A), 0, 0)
+        v, d, fl = pytwin.round_int(A)
+        assert r.bits == f2b(v), hex(A)
+        assert r.direction == d and r.flags == fl, hex(A)
+
+
+def test_overflow_threshold_exact():
+    """R11: RN overflows iff |S| >= 2^1024 - 2^970 (DBL_MAX + half ulp, tie to even 2^1024)."""
+    t = (1 << (1024 + 1074)) - (1 << (970 + 1074))
+    for A, inf in [(t, True), (t - 1, False), (-t, True), (-(t - 1), False)]:
+        r = oracle.round_limbs(oracle.int_to_limbs(A), 0, 0)
+        assert math.isinf(r.value) == inf
+        assert bool(r.flags & oracle.F_OVERFLOW) == inf
+
+
+def test_unbounded_rounding_fields():
+    """sig53 * 2^exp2 is the RN-even rounding with an unbounded exponent (diagnostic for c4)."""
+    A = ((1 << 53) - 1) << 2100     # beyond binary64 range
+    r = oracle.round_limbs(oracle.int_to_limbs(A), 0, 0)
+    assert math.isinf(r.value) and r.sig53 == (1 << 53) - 1 and r.exp2 == 2100 - 1074
+    assert r.msb_exp == 2152 - 1074
+
+
+# ---- Lemma 1, exhaustively at R = 8 (reading Q6 / DESIGN.md R6) ----
+
+def lemma1_carry(P: int, R: int) -> int:
+    if P >= R - 1:
+        return 1
+    if P <= -R + 1:
+        return -1
+    return 0
+
+
+@pytest.mark.parametrize("R", [8, 16, 2 ** 5])
+def test_lemma1_exhaustive(R):
+    """For regularized Y, Z (digits in [-(R-1), R-1]) and any incoming carry C_i in {-1,0,1},
+    S_i = P_i - C_{i+1} R + C_i stays in [-(R-1), R-1] (alpha = beta = R-1)."""
+    a = R - 1
+    for P in range(-2 * a, 2 * a + 1):
+        C1 = lemma1_carry(P, R)
+        W = P - C1 * R
+        assert -(a - 1) <= W <= a - 1
+        for Ci in (-1, 0, 1):
+            assert -a <= W + Ci <= a
+
+
+def test_lemma1_carry_free_addition_value_preserved():
+    """Digit-local Lemma-1 addition of two regularized vectors preserves the value (R = 8)."""
+    rng = random.Random(2)
+    R, a = 8, 7
+    for _ in range(2000):
+        D = rng.randint(1, 8)
+        Y = [rng.randint(-a, a) for _ in range(D)]
+        Z = [rng.randint(-a, a) for _ in range(D)]
+        P = [y + z for y, z in zip(Y, Z)] + [0]
+        C = [0] + [lemma1_carry(P[i], R) for i in range(D)]          # C[i+1] from P[i]
+        S = [P[i] - C[i + 1] * R + C[i] for i in range(D)] + [C[D]]
+        val = lambda v: sum(d * R ** i for i, d in enumerate(v))
+        assert val(S) == val(Y) + val(Z)
+        assert all(-a <= s <= a for s in S)

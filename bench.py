@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""Benchmark: exactly summed doubles/s on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c5] [--impl ours|reference]
+
+A step is one pass of the whole hot path over one batch:
+  N = 1: one fused launch of xsum_sum (decompose + lane-column accumulate + regularize +
+         block/grid merge + canonicalize + round) over the config's input in HBM.
+  N > 1: (torchrun, one process per GPU, NCCL) each rank sums its own shard of the same
+         size (weak scaling), then all-gathers the 384-byte states, merges and rounds.
+Inputs are synthetic (synth/, the recipe in DESIGN.md) and 2 GiB per GPU (> 126 MB L2:
+no flush needed between steps). `--impl reference` times the CPU oracle instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "doubles/s exact-summed (device-timed) at 1/2/4/8 B200; % of HBM-read roofline"
+UNIT = "doubles/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def workload(cfg_name: str, world: int) -> dict:
+    import synth
+    cfg = synth.CONFIGS[cfg_name]
+    desc = {
+        "c1": "c1: n=2^20 doubles, seed 1, exponent U[-10,10]",
+        "c2": "c2: n=2^28 doubles, seed 2, random sign, uniform mantissa, exponent U[-1000,1000]",
+        "c3": "c3: 2^27 (a,-a) pairs exp U[0,600] + 2^20 tiny exp U[-900,-800], permuted, seed 3",
+        "c4": "c4: n=2^33 doubles, seed 4, exponent U[-1022,1023], sharded over the GPUs",
+        "c5": "c5: 2^16 segments x 2^12 doubles, seed 5, exponent U[-200,200]",
+    }[cfg_name]
+    if cfg_name == "c4":
+        n_total = cfg["n"]
+        scaling = "strong"
+    else:
+        n_total = cfg["n"] * world
+        scaling = "weak"
+    return dict(desc=desc, n_total=n_total, scaling=scaling, cfg=cfg)
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (NVML, fine-grained; the recipe's nvidia-smi fields)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.ok = False
+        self._stop = threading.Event()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+            try:  # one last sample right at the end of the region
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            except Exception:
+                pass
+
+    def summary(self) -> dict:
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def measured_peak_hbm() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def profiled_traffic(cfg_name: str):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu --set full
+    summary (profiles/ncu_summary.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            s = json.load(fh)
+        return s.get("traffic_bytes_per_launch", {}).get(cfg_name)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle arm (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------
+def oracle_rate(cfg_name: str, target_s: float = 3.0, max_n: int = 1 << 27):
+    """Time the oracle (as it stands) on a bounded prefix of the workload on all host cores."""
+    import numpy as np
+
+    import oracle
+    import synth
+    cores = oracle.host_threads()
+    gen_name = "c2" if cfg_name in ("c1",) else cfg_name
+    m = 1 << 20
+    while True:
+        x = synth.host_generate(gen_name, 0, m)
+        t0 = time.perf_counter()
+        oracle.exact_sum(x, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 4 or m >= max_n:
+            break
+        m = min(max_n, m * 4)
+    if dt < target_s and m < max_n:   # final sample sized to ~target_s
+        m = int(min(max_n, m * target_s / max(dt, 1e-3)))
+        x = synth.host_generate(gen_name, 0, m)
+        t0 = time.perf_counter()
+        oracle.exact_sum(x, nthreads=cores)
+        dt = time.perf_counter() - t0
+    del x
+    return m / dt, cores, m, dt, gen_name
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    import synth
+    wl = workload(args.config, world)
+    cores = oracle.host_threads()
+    rate, _, _, _, gen_name = oracle_rate(args.config, target_s=1.0, max_n=1 << 24)
+    budget = 90.0
+    m = int(max(1 << 14, min(1 << 26, rate * budget / max(1, args.steps + args.warmup))))
+    x = synth.host_generate(gen_name, 0, m)
+    for _ in range(args.warmup):
+        oracle.exact_sum(x, nthreads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.exact_sum(x, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = m * args.steps / tot
+    sample = f"{gen_name} elements [0, {m}) per step (bounded sample of the workload), {cpu_model()}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": wl["desc"], "sample_n": m},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+
+    import paper_1605_05436_b200 as xsum
+    import synth
+    from paper_1605_05436_b200 import dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+    xsum.build()
+    synth.build()
+    wl = workload(args.config, world)
+    cfg = wl["cfg"]
+    seg = args.config == "c5"
+
+    # this rank's input, generated in HBM (untimed)
+    if args.config == "c4":
+        start, stop = dist.shard_range(cfg["n"], rank, world)
+        x = synth.device_generate("c4", start, stop - start, device=dev)
+    elif args.config == "c3":
+        x = synth.device_generate("c3", device=dev)
+    else:
+        x = synth.device_generate(args.config, device=dev)   # same c-config per rank (weak scaling)
+    n_local = x.numel()
+    torch.cuda.synchronize()
+
+    acc = xsum.Accumulator(dev)
+    tot = xsum.Accumulator(dev) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if seg:
+            xsum.sum_segments(x, cfg["seg_len"])
+        elif world == 1:
+            acc.sum(x)                                   # one fused launch
+        else:
+            acc.reset().add(x)
+            states = dist.gather_states(acc.state)
+            tot.reset().merge(states).finalize_async()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = xsum.launch_count()
+    with ClockSampler(local_rank) as clk:
+        for i in range(K):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = xsum.launch_count() - l0
+    per = [a.elapsed_time(b) for a, b in ev]                 # ms per step (device)
+    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(t.item())
+    n_all = n_local * world
+    value = n_all * K / (total_ms / 1e3)
+
+    # dominant kernel: the accumulate launch (N=1 the step is exactly that one launch)
+    if world == 1:
+        kern_ms = statistics.mean(per)
+    else:   # time the local accumulate alone with events on its stream
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for a, b in kev:
+            a.record(stream)
+            acc.reset().add(x)
+            b.record(stream)
+        torch.cuda.synchronize()
+        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    peak, peak_src = measured_peak_hbm()
+    achieved = 8.0 * n_local / (kern_ms / 1e3) / 1e9
+
+    # check the result once (device result vs nothing host-side: the parity tests do that)
+    e2e = None
+    if not args.no_e2e and world == 1 and not seg:
+        e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, m, dt, gen_name = oracle_rate(args.config)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{gen_name} elements [0, {m}) summed once by the oracle in {dt:.2f} s "
+                         f"on {cores} host threads ({cpu_model()})"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": max(3, args.warmup), "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "n_per_gpu": n_local, "n_total": n_all,
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "l2": "inputs 2 GiB+ per GPU > 126 MB L2 (no flush needed)",
+                       "step": ("xsum_sum_segments" if seg else
+                                "xsum_sum fused launch" if world == 1 else
+                                "reset+accumulate, NCCL all-gather of 384-B states, merge, finalize")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": profiled_traffic(args.config),
+                         "kernel": "k_accumulate" if not seg else "k_segments",
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": 8 * n_local,
+                         "peak_source": peak_src},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def measure_e2e(xsum, torch, x_dev, steps: int, dev):
+    """Same metric through the C-ABI with a HOST buffer: per step the pinned-host -> device copy
+    of the whole input (overlapped chunk by chunk, xsum_accumulate_host), the sum, the rounding
+    and the 48-byte device -> host read of the result."""
+    n = x_dev.numel()
+    host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host.copy_(x_dev)
+    acc = xsum.Accumulator(dev)
+    out = torch.empty(xsum.RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
+
+    def one():
+        acc.reset().add_host(host, stage_bytes=256 << 20)
+        res, _ = acc.finalize_async()
+        out.copy_(res)          # synchronous D2H of the result
+        return out
+
+    one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": xsum.RESULT_BYTES,
+            "ms_per_step": dt * 1e3, "api": "xsum_reset + xsum_accumulate_host + xsum_finalize_round + D2H"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "run N>1 under torchrun"}))
+        return 2
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,200 @@
+/* xsum.h — C-ABI of the B200 superaccumulator reduction (libxsum.so).
+ *
+ * Exact summation of IEEE-754 binary64 values after Goodrich & Eldawy,
+ * "Parallel Algorithms for Summing Floating-Point Numbers" (arXiv 1605.05436).
+ * Citations "PAPER.md:L" are line numbers of the paper's LaTeX source.
+ *
+ * Problem (§1): given X = {x_1..x_n}, compute the floating-point
+ * number S_n* that faithfully rounds S_n = sum x_i. This library returns the
+ * round-to-nearest-even double of the EXACT sum (one of the faithful results; the
+ * "correctly rounded" sum of §5) together with the exact sum
+ * itself as a canonical two's-complement integer image.
+ *
+ * Representation (§2): a superaccumulator is a vector of signed
+ * integer digits Y_j with value sum_j Y_j * R^j * 2^-1074, radix R = 2^52
+ * (XSUM_RADIX_BITS), XSUM_NDIGITS = 42 digits (2184 bits >= 1074 + 1024 + 63:
+ * enough for any n < 2^63). A state is (alpha,beta)-regularized
+ * with alpha = beta = R-1 (|Y_j| <= R-1, Lemma 1), which makes
+ * adding two states carry-free.
+ *
+ * Conventions (all entry points):
+ *   - Pointers named d_* are DEVICE pointers (cudaMalloc'd or torch tensors) on the
+ *     handle's device; h_* are HOST pointers. The caller owns every buffer passed in.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are asynchronous and stream-ordered; a buffer must stay valid until
+ *     the stream passes the call. One handle is used by one stream at a time.
+ *   - Functions return a status code and never abort or throw across the ABI.
+ *     Argument errors are detected on the host before anything is enqueued.
+ *   - NaN / +-Inf inputs are not errors: they set sticky flags (R10).
+ *   - No CPU fallback exists: every arithmetic step runs in CUDA kernels built
+ *     for sm_100a.
+ */
+#ifndef XSUM_H
+#define XSUM_H
+
+#if defined(__GNUC__)
+#define XSUM_API __attribute__((visibility("default")))
+#else
+#define XSUM_API
+#endif
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum xsum_status {
+    XSUM_OK = 0,
+    XSUM_EINVAL = 1,     /* null/misaligned pointer, bad size, wrong device, too-small buffer */
+    XSUM_ECAPACITY = 2,  /* total count would exceed 2^63-1 summands */
+    XSUM_ECUDA = 3,      /* a CUDA runtime call or kernel launch failed */
+    XSUM_EMISMATCH = 4,  /* a merged state image had a wrong header (magic/version/radix) */
+    XSUM_ENOMEM = 5      /* host allocation failed */
+} xsum_status;
+
+#define XSUM_RADIX_BITS 52          /* w: R = 2^52 */
+#define XSUM_NDIGITS 42             /* D */
+#define XSUM_STATE_BYTES 384        /* packed state image, see below */
+#define XSUM_CANON_LIMBS 34         /* canonical image: 34 x u64 = 2176-bit two's complement */
+#define XSUM_MAGIC 0x4D555358u      /* "XSUM" little-endian */
+#define XSUM_VERSION 1u
+
+/* Result / state flag bits (xsum_result.flags, state header flags). */
+#define XSUM_F_NAN 1u        /* a NaN was summed */
+#define XSUM_F_PINF 2u       /* +Inf was summed */
+#define XSUM_F_NINF 4u       /* -Inf was summed */
+#define XSUM_F_OVERFLOW 8u   /* the finite exact sum rounds beyond DBL_MAX (result +-Inf) */
+#define XSUM_F_INEXACT 16u   /* the finite exact sum is not representable */
+#define XSUM_F_MISMATCH 32u  /* a merged state image was rejected (header mismatch) */
+
+/* Packed state image (XSUM_STATE_BYTES, little-endian). Exactly mergeable in any
+ * order; it is also the checkpoint format and what ranks exchange.
+ *   offset 0  u32 magic = XSUM_MAGIC      offset 4  u16 version = XSUM_VERSION
+ *   offset 6  u8  w = 52                  offset 7  u8  ndigits = 42
+ *   offset 8  u32 flags (XSUM_F_NAN|PINF|NINF|MISMATCH)
+ *   offset 12 u32 reserved (0)            offset 16 u64 count (summands so far)
+ *   offset 24 i64 digit[42], digit j worth R^j * 2^-1074, |digit| <= R-1
+ *   offset 360..383 zero padding */
+typedef struct xsum_state_image {
+    uint32_t magic;
+    uint16_t version;
+    uint8_t w;
+    uint8_t ndigits;
+    uint32_t flags;
+    uint32_t reserved;
+    uint64_t count;
+    int64_t digit[XSUM_NDIGITS];
+    uint8_t pad[XSUM_STATE_BYTES - 24 - 8 * XSUM_NDIGITS];
+} xsum_state_image;
+
+/* Result record written by xsum_finalize_round / xsum_sum (48 bytes, device memory).
+ * PAPER.md:787-795 (§3 step 7): locate the most significant non-zero component,
+ * combine it with its neighbours and round on the truncated bits. */
+typedef struct xsum_result {
+    double value;        /* RN-even of the exact sum; +0.0 for an exact zero; NaN / +-Inf per flags */
+    int32_t direction;   /* sign(value - exact) of the finite part: -1, 0, +1 (0 if a special is returned) */
+    uint32_t flags;      /* XSUM_F_* */
+    int32_t msb_exp;     /* floor(log2 |exact|), INT32_MIN if the exact sum is zero */
+    int32_t sign;        /* 1 if the exact finite sum is negative */
+    uint64_t count;      /* summands accumulated */
+    uint64_t sig53;      /* unbounded-exponent rounding: |exact| ~= sig53 * 2^exp2 (RN-even, 53 bits) */
+    int32_t exp2;
+    int32_t reserved;
+} xsum_result;
+
+typedef struct xsum_ctx xsum_ctx;
+
+/* Sizes of the caller-provided device buffers. */
+XSUM_API size_t xsum_state_bytes(void);                 /* = XSUM_STATE_BYTES */
+XSUM_API size_t xsum_scratch_bytes(int device);         /* scratch a handle needs on `device` (block partials) */
+XSUM_API size_t xsum_result_bytes(void);                /* = sizeof(xsum_result) = 48 */
+
+/* Create a handle bound to `device` whose exact state lives in d_state (XSUM_STATE_BYTES,
+ * 8-B aligned) and whose kernels use d_scratch (>= xsum_scratch_bytes(device), 256-B
+ * aligned). The state is initialised to zero (header written) on `stream`.
+ * Errors: XSUM_EINVAL (null pointers, misalignment, scratch too small, bad device),
+ * XSUM_ECUDA, XSUM_ENOMEM. On error *h is NULL. */
+XSUM_API xsum_status xsum_create(xsum_ctx **h, int device, void *d_state, void *d_scratch,
+                        size_t scratch_bytes, void *stream);
+
+/* State := 0 (count 0, flags 0), stream-ordered. */
+XSUM_API xsum_status xsum_reset(xsum_ctx *h, void *stream);
+
+/* State += sum of d_x[0..n) EXACTLY (§5: the whole superaccumulator
+ * stays in fast memory and components are added in any order; PAPER.md:744-750 step 2
+ * decomposition; PAPER.md:559-628 carry-free regularization; PAPER.md:768-776 bottom-up
+ * merge). d_x needs only 8-byte alignment; n = 0 is a no-op. May be called repeatedly
+ * (chunked / streaming sums). One kernel launch.
+ * Errors: XSUM_EINVAL (h or d_x null with n > 0, d_x not 8-B aligned),
+ * XSUM_ECAPACITY (total count > 2^63-1), XSUM_ECUDA (launch failure). */
+XSUM_API xsum_status xsum_accumulate(xsum_ctx *h, const double *d_x, uint64_t n, void *stream);
+
+/* State += sum of h_x[0..n) for a HOST buffer (pinned memory overlaps best): chunks are
+ * copied into the caller's device staging buffer d_stage (two halves, double-buffered,
+ * stage_bytes >= 2 MiB) and accumulated while the next chunk is in flight. This is the
+ * paper's O(scan(n)) external-memory algorithm with sigma(n) <= M.
+ * Returns after enqueueing; h_x and d_stage must stay valid until `stream` completes.
+ * Errors: as xsum_accumulate, plus XSUM_EINVAL for a null / too-small staging buffer. */
+XSUM_API xsum_status xsum_accumulate_host(xsum_ctx *h, const double *h_x, uint64_t n, void *d_stage,
+                                 size_t stage_bytes, void *stream);
+
+/* State += sum of `count` packed state images at d_states (count * XSUM_STATE_BYTES bytes,
+ * 8-B aligned): the MapReduce post-process / all-gather merge (§6.1),
+ * a Lemma-1 pairwise tree of carry-free additions. Images with a bad
+ * header are skipped and set XSUM_F_MISMATCH in the state (reported by finalize).
+ * Errors: XSUM_EINVAL, XSUM_ECAPACITY, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_merge(xsum_ctx *h, const void *d_states, uint32_t count, void *stream);
+
+/* Non-destructive rounding of the state: writes *d_res (device, 8-B aligned) and, if
+ * d_canon != NULL, the canonical image (XSUM_CANON_LIMBS little-endian u64 limbs of the
+ * two's complement integer A = exact_sum * 2^1074; the "non-overlapping" form of
+ * PAPER.md:777-786 / :1058-1064, R4). Signed-carry propagation is a parallel
+ * prefix over {-1,0,+1} carries; rounding is RN-even.
+ * Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_finalize_round(xsum_ctx *h, void *d_res, uint64_t *d_canon, void *stream);
+
+/* One-shot fused path: state := sum d_x[0..n) exactly, then finalize into d_res / d_canon.
+ * Equivalent to reset + accumulate + finalize_round in ONE kernel launch (the last block
+ * to finish merges the block partials and rounds). */
+XSUM_API xsum_status xsum_sum(xsum_ctx *h, const double *d_x, uint64_t n, void *d_res, uint64_t *d_canon,
+                     void *stream);
+
+/* Cap the number of thread blocks an accumulate launch of this handle may use
+ * (0 = one per SM, the default; values above 1024 are clamped). Lets a caller leave
+ * SMs to concurrent work; tests use it to force many flush windows per lane.
+ * Errors: XSUM_EINVAL (null handle). */
+XSUM_API xsum_status xsum_set_grid_limit(xsum_ctx *h, uint32_t max_blocks);
+
+/* Release the host handle (never frees caller memory). */
+XSUM_API xsum_status xsum_destroy(xsum_ctx *h);
+
+/* Elements accumulated into the handle so far (host-side counter). */
+XSUM_API uint64_t xsum_count(const xsum_ctx *h);
+
+/* Segmented exact sums (BASELINE.json config 5): for s < nseg, d_out[s] = RN-even of the
+ * exact sum of d_x[s*seg_len .. (s+1)*seg_len). Optional outputs: d_canon[s*34 .. s*34+34)
+ * canonical images, d_flags[s] XSUM_F_* flags. d_x 8-B aligned, any seg_len >= 0.
+ * Each segment is reduced by one warp (the paper's per-block "combine").
+ * Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_sum_segments(const double *d_x, uint64_t nseg, uint64_t seg_len, double *d_out,
+                              uint64_t *d_canon, uint32_t *d_flags, void *stream);
+
+/* Variable-length segments (CSR offsets): segment s is
+ * d_x[d_offsets[s] .. d_offsets[s+1]), offsets non-decreasing device u64 array of nseg+1.
+ * Outputs as xsum_sum_segments. Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_sum_segments_csr(const double *d_x, const uint64_t *d_offsets, uint64_t nseg,
+                                  double *d_out, uint64_t *d_canon, uint32_t *d_flags, void *stream);
+
+/* Static string for a status code. */
+XSUM_API const char *xsum_status_str(xsum_status s);
+
+/* Number of kernel launches the library enqueued since load (for bench.py's gpu_launches). */
+XSUM_API uint64_t xsum_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XSUM_H */

@@ -1,0 +1,327 @@
+"""Exact floating-point summation on B200 (sm_100a): Python binding of libxsum.so.
+
+A thin ctypes layer over the C-ABI in ``include/xsum.h`` (same names, argument
+marshalling only). PyTorch supplies device memory and streams; every arithmetic
+step of the summation runs in the library's CUDA kernels. There is no CPU
+fallback: if ``libxsum.so`` is missing or no CUDA device is present, calls raise.
+
+Method: Goodrich & Eldawy, "Parallel Algorithms for Summing Floating-Point
+Numbers" (arXiv 1605.05436); see DESIGN.md for the mapping of the paper's steps
+to kernels and include/xsum.h for the boundary.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libxsum.so")
+
+STATE_BYTES = 384
+RESULT_BYTES = 48
+CANON_LIMBS = 34
+RADIX_BITS = 52
+NDIGITS = 42
+MAGIC = 0x4D555358
+VERSION = 1
+F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT, F_MISMATCH = 1, 2, 4, 8, 16, 32
+
+OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
+
+# every entry point declared in include/xsum.h
+EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_create", "xsum_reset",
+           "xsum_accumulate", "xsum_accumulate_host", "xsum_merge", "xsum_finalize_round", "xsum_sum",
+           "xsum_destroy", "xsum_count", "xsum_sum_segments", "xsum_sum_segments_csr", "xsum_status_str",
+           "xsum_launch_count", "xsum_set_grid_limit")
+
+
+class XsumError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        self.status = status
+        super().__init__(f"{fn} failed: {status_str(status)} ({status})")
+
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile libxsum.so in-tree (nvcc, sm_100a)."""
+    import importlib
+    return importlib.import_module(__name__ + ".build").build(force=force)
+
+
+def lib() -> ctypes.CDLL:
+    """Load libxsum.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise RuntimeError(f"{SO_PATH} not built: run `python -m paper_1605_05436_b200.build` "
+                               "or __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(SO_PATH)
+        p, u64, u32, i32, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t
+        sig = {
+            "xsum_state_bytes": ([], sz), "xsum_scratch_bytes": ([i32], sz), "xsum_result_bytes": ([], sz),
+            "xsum_create": ([ctypes.POINTER(p), i32, p, p, sz, p], i32), "xsum_reset": ([p, p], i32),
+            "xsum_accumulate": ([p, p, u64, p], i32), "xsum_accumulate_host": ([p, p, u64, p, sz, p], i32),
+            "xsum_merge": ([p, p, u32, p], i32), "xsum_finalize_round": ([p, p, p, p], i32),
+            "xsum_sum": ([p, p, u64, p, p, p], i32), "xsum_destroy": ([p], i32), "xsum_count": ([p], u64),
+            "xsum_sum_segments": ([p, u64, u64, p, p, p, p], i32),
+            "xsum_sum_segments_csr": ([p, p, u64, p, p, p, p], i32),
+            "xsum_status_str": ([i32], ctypes.c_char_p), "xsum_launch_count": ([], u64),
+            "xsum_set_grid_limit": ([p, u32], i32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def status_str(s: int) -> str:
+    try:
+        return lib().xsum_status_str(s).decode()
+    except Exception:  # pragma: no cover
+        return "?"
+
+
+def _check(fn: str, status: int) -> None:
+    if status != OK:
+        raise XsumError(fn, status)
+
+
+def launch_count() -> int:
+    return int(lib().xsum_launch_count())
+
+
+@dataclass(frozen=True)
+class Result:
+    """Host copy of ``xsum_result`` (include/xsum.h)."""
+    value: float
+    bits: int
+    direction: int
+    flags: int
+    msb_exp: int | None
+    sign: int
+    count: int
+    sig53: int
+    exp2: int
+
+    @staticmethod
+    def from_bytes(b: bytes | np.ndarray) -> "Result":
+        a = np.frombuffer(bytes(b), dtype=np.uint8)
+        assert a.size == RESULT_BYTES
+        value = float(a[0:8].view(np.float64)[0])
+        bits = int(a[0:8].view(np.uint64)[0])
+        i32 = a[8:24].view(np.int32)
+        u32 = a[8:24].view(np.uint32)
+        count = int(a[24:32].view(np.uint64)[0])
+        sig53 = int(a[32:40].view(np.uint64)[0])
+        exp2 = int(a[40:44].view(np.int32)[0])
+        msb = int(i32[2])
+        return Result(value=value, bits=bits, direction=int(i32[0]), flags=int(u32[1]),
+                      msb_exp=None if msb == -(2 ** 31) else msb, sign=int(i32[3]), count=count,
+                      sig53=sig53, exp2=exp2)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(device) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _as_f64_cuda(t):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if t.dtype != torch.float64:
+        raise TypeError(f"expected float64, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t
+
+
+class Accumulator:
+    """An exact superaccumulator living in device memory (the xsum_ctx handle).
+
+    ``add`` streams device tensors into it, ``add_host`` host arrays, ``merge``
+    other accumulators' state images (e.g. the all-gather of the per-GPU states),
+    ``result`` rounds it. All calls are asynchronous on the current stream except
+    the ones that return host values."""
+
+    def __init__(self, device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1605_05436_b200 needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device if device is not None else "cuda", )
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        L = lib()
+        self.state = torch.zeros(STATE_BYTES, dtype=torch.uint8, device=self.device)
+        nscr = int(L.xsum_scratch_bytes(self.device.index))
+        self.scratch = torch.zeros(nscr, dtype=torch.uint8, device=self.device)
+        self._res = torch.zeros(RESULT_BYTES, dtype=torch.uint8, device=self.device)
+        self._canon = torch.zeros(CANON_LIMBS, dtype=torch.int64, device=self.device)
+        self._stage = None
+        h = ctypes.c_void_p()
+        _check("xsum_create", L.xsum_create(ctypes.byref(h), self.device.index, self.state.data_ptr(),
+                                            self.scratch.data_ptr(), nscr, _stream_ptr(self.device)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.xsum_destroy(h)
+            except Exception:  # pragma: no cover
+                pass
+            self._h = None
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    @property
+    def count(self) -> int:
+        return int(lib().xsum_count(self._h))
+
+    def set_grid_limit(self, max_blocks: int) -> "Accumulator":
+        """Cap the blocks of an accumulate launch (0 = one per SM)."""
+        _check("xsum_set_grid_limit", lib().xsum_set_grid_limit(self._h, max_blocks))
+        return self
+
+    def reset(self) -> "Accumulator":
+        _check("xsum_reset", lib().xsum_reset(self._h, _stream_ptr(self.device)))
+        return self
+
+    def add(self, x) -> "Accumulator":
+        x = _as_f64_cuda(x)
+        _check("xsum_accumulate", lib().xsum_accumulate(self._h, x.data_ptr(), x.numel(),
+                                                        _stream_ptr(self.device)))
+        return self
+
+    def add_host(self, x, stage_bytes: int = 128 << 20) -> "Accumulator":
+        """Sum a host float64 array/tensor (pinned memory overlaps copy and compute)."""
+        torch = _torch()
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+        if x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
+            raise TypeError("expected a contiguous host float64 array")
+        if self._stage is None or self._stage.numel() < stage_bytes:
+            self._stage = torch.empty(stage_bytes, dtype=torch.uint8, device=self.device)
+        _check("xsum_accumulate_host", lib().xsum_accumulate_host(
+            self._h, x.data_ptr(), x.numel(), self._stage.data_ptr(), self._stage.numel(),
+            _stream_ptr(self.device)))
+        self._host_ref = x          # keep alive until the stream passes the copies
+        return self
+
+    def merge(self, states) -> "Accumulator":
+        """Add packed state images (uint8 CUDA tensor of k*384 bytes, or another Accumulator)."""
+        torch = _torch()
+        if isinstance(states, Accumulator):
+            states = states.state
+        if not (isinstance(states, torch.Tensor) and states.is_cuda and states.dtype == torch.uint8
+                and states.is_contiguous() and states.numel() % STATE_BYTES == 0):
+            raise TypeError("expected a contiguous uint8 CUDA tensor of k*384 bytes")
+        k = states.numel() // STATE_BYTES
+        _check("xsum_merge", lib().xsum_merge(self._h, states.data_ptr(), k, _stream_ptr(self.device)))
+        return self
+
+    def finalize_async(self, canon: bool = False):
+        """Enqueue the rounding; returns the (result bytes, canon limbs or None) device tensors."""
+        _check("xsum_finalize_round", lib().xsum_finalize_round(
+            self._h, self._res.data_ptr(), self._canon.data_ptr() if canon else None,
+            _stream_ptr(self.device)))
+        return self._res, (self._canon if canon else None)
+
+    def result(self) -> Result:
+        res, _ = self.finalize_async()
+        return Result.from_bytes(res.cpu().numpy().tobytes())
+
+    def exact(self) -> tuple[Result, np.ndarray]:
+        """(rounded result, 34-limb two's complement image of the exact sum * 2^1074)."""
+        res, canon = self.finalize_async(canon=True)
+        return Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64).copy()
+
+    def sum(self, x, canon: bool = False):
+        """One-shot fused path (xsum_sum): state := sum(x); returns device (result, canon)."""
+        x = _as_f64_cuda(x)
+        _check("xsum_sum", lib().xsum_sum(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
+                                          self._canon.data_ptr() if canon else None,
+                                          _stream_ptr(self.device)))
+        return self._res, (self._canon if canon else None)
+
+
+_default_acc: dict = {}
+
+
+def _acc_for(device) -> Accumulator:
+    torch = _torch()
+    key = (torch.cuda.current_device() if device is None else torch.device(device).index)
+    acc = _default_acc.get(key)
+    if acc is None:
+        acc = _default_acc[key] = Accumulator(device)
+    return acc
+
+
+def exact_sum(x) -> tuple[Result, np.ndarray]:
+    """Exact sum of a float64 CUDA tensor: (rounded Result, canonical 34-limb image)."""
+    x = _as_f64_cuda(x)
+    acc = _acc_for(x.device)
+    res, canon = acc.sum(x, canon=True)
+    return Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64).copy()
+
+
+def fsum(x) -> float:
+    """Correctly rounded (RN-even) sum of a float64 CUDA tensor."""
+    x = _as_f64_cuda(x)
+    res, _ = _acc_for(x.device).sum(x)
+    return Result.from_bytes(res.cpu().numpy().tobytes()).value
+
+
+def sum_segments(x, seg_len: int, canon: bool = False, flags: bool = False):
+    """Per-segment exact sums of a float64 CUDA tensor split into equal segments of seg_len.
+    Returns (values[nseg] f64, canon[nseg,34] or None, flags[nseg] or None) on the device."""
+    torch = _torch()
+    x = _as_f64_cuda(x)
+    if seg_len <= 0 or x.numel() % seg_len:
+        raise ValueError("x.numel() must be a positive multiple of seg_len")
+    nseg = x.numel() // seg_len
+    return _segments(x, nseg, seg_len, None, canon, flags)
+
+
+def sum_segments_csr(x, offsets, canon: bool = False, flags: bool = False):
+    """Variable-length segments: segment s = x[offsets[s]:offsets[s+1]] (offsets int64 CUDA)."""
+    torch = _torch()
+    x = _as_f64_cuda(x)
+    if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous() and offsets.numel() >= 1):
+        raise TypeError("offsets must be a contiguous int64 CUDA tensor of nseg+1 entries")
+    return _segments(x, offsets.numel() - 1, 0, offsets, canon, flags)
+
+
+def _segments(x, nseg, seg_len, offsets, canon, flags):
+    torch = _torch()
+    out = torch.empty(nseg, dtype=torch.float64, device=x.device)
+    cn = torch.empty((nseg, CANON_LIMBS), dtype=torch.int64, device=x.device) if canon else None
+    fl = torch.empty(nseg, dtype=torch.int32, device=x.device) if flags else None
+    L = lib()
+    st = _stream_ptr(x.device)
+    if offsets is None:
+        rc = L.xsum_sum_segments(x.data_ptr(), nseg, seg_len, out.data_ptr(),
+                                 cn.data_ptr() if cn is not None else None,
+                                 fl.data_ptr() if fl is not None else None, st)
+        _check("xsum_sum_segments", rc)
+    else:
+        xp = x if x.numel() else torch.zeros(1, dtype=torch.float64, device=x.device)
+        rc = L.xsum_sum_segments_csr(xp.data_ptr(), offsets.data_ptr(), nseg, out.data_ptr(),
+                                     cn.data_ptr() if cn is not None else None,
+                                     fl.data_ptr() if fl is not None else None, st)
+        _check("xsum_sum_segments_csr", rc)
+    return out, cn, fl

@@ -1,0 +1,248 @@
+// K2: streaming decompose-and-accumulate kernel (the hot path), with the grid-level
+// merge of block superaccumulators and an optional fused final rounding.
+//
+// Design: the paper's in-memory scan (§5: "keep our
+// entire superaccumulator stored in internal memory and process the floating-point
+// components in any order") with shared memory as the internal memory. Every lane owns a
+// private column of D int64 digits (thread-minor layout: digit j of lane l at word
+// j*32 + l, so a warp's accesses never bank-conflict whatever the data). Each summand is
+// split into two chunks added with carries deferred; a lane column is
+// regularized every FLUSH_ELEMS summands. At the end the lane columns
+// are summed (warp), the warp sums (block), the block partials (grid: the last block to
+// finish, PAPER.md:768-776 bottom-up tree) and the result rounded.
+#include <cuda_runtime.h>
+
+#include "xsum_device.cuh"
+#include "xsum_kernels.h"
+
+namespace xs {
+
+template <int WARPS, int U>
+struct AccCfg {
+    static constexpr int T = WARPS * 32;
+    static constexpr int FLUSH_TILES = FLUSH_ELEMS / (2 * U);
+    static constexpr size_t SMEM = (size_t)WARPS * D * 32 * sizeof(int64_t);
+};
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+template <int U, int T>
+__device__ __forceinline__ void rescan_window(int64_t* col, const uint4* body, uint64_t t0, uint64_t t1,
+                                              uint64_t G, uint64_t TV, int tid, uint32_t& flags) {
+    // Rare path: this lane summed a NaN/Inf bit pattern as if finite somewhere in tiles
+    // [t0, t1] (step G). Re-read its elements and cancel those chunks exactly.
+    for (uint64_t tt = t0; tt <= t1; tt += G) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
+            column_fix_special(col, v.x, v.y, flags);
+            column_fix_special(col, v.z, v.w, flags);
+        }
+    }
+}
+
+template <int WARPS, int U>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
+    using C = AccCfg<WARPS, U>;
+    constexpr int T = C::T;
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t wsum[WARPS][D];
+    __shared__ int64_t su[64];
+    __shared__ uint32_t blk_flags;
+    __shared__ int is_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    if (tid == 0) blk_flags = 0;
+    uint32_t flags = 0;
+
+    const uint64_t head = (n && ((uintptr_t)x & 15)) ? 1 : 0;   // peel to 16-B alignment
+    const uint64_t nbody = n - head;
+    const uint64_t nvec = nbody >> 1;
+    const uint4* body = reinterpret_cast<const uint4*>(x + head);
+    const uint64_t TV = (uint64_t)T * U;
+    const uint64_t ntiles = nvec / TV;
+    const uint64_t G = gridDim.x;
+
+    uint32_t emax = 0;
+    int since = 0;
+    uint64_t wstart = blockIdx.x, tlast = 0;
+    bool any_tile = false;
+    uint4 cur[U];
+    uint64_t t = blockIdx.x;
+    if (t < ntiles) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = ldg_stream(body + t * TV + (uint64_t)u * T + tid);
+    }
+    while (t < ntiles) {
+        const uint64_t tn = t + G;
+        uint4 nxt[U];
+        if (tn < ntiles) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) nxt[u] = ldg_stream(body + tn * TV + (uint64_t)u * T + tid);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            Chunks a = decompose(cur[u].x, cur[u].y);
+            emax = max(emax, a.e);
+            column_add(col, a);
+            Chunks b = decompose(cur[u].z, cur[u].w);
+            emax = max(emax, b.e);
+            column_add(col, b);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+        any_tile = true;
+        tlast = t;
+        if (++since == C::FLUSH_TILES) {
+            if (__any_sync(FULL, emax == 0x7FFu)) {
+                if (emax == 0x7FFu) rescan_window<U, T>(col, body, wstart, t, G, TV, tid, flags);
+            }
+            emax = 0;
+            regularize_column(col);
+            since = 0;
+            wstart = tn;
+            any_tile = false;
+        }
+        t = tn;
+    }
+
+    // leftover vectors (< one tile), the unaligned head and the odd tail element: checked
+    // adds by the block that would own the next tile.
+    if (blockIdx.x == ntiles % G) {
+        const uint64_t v0 = ntiles * TV;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint64_t v = v0 + (uint64_t)u * T + tid;
+            if (v < nvec) {
+                uint4 q = ldg_stream(body + v);
+                column_add_checked(col, q.x, q.y, flags);
+                column_add_checked(col, q.z, q.w, flags);
+            }
+        }
+        if (tid == 0 && head) {
+            uint2 q = ldg_one(x);
+            column_add_checked(col, q.x, q.y, flags);
+        }
+        if (tid == 1 && (nbody & 1)) {
+            uint2 q = ldg_one(x + head + 2 * nvec);
+            column_add_checked(col, q.x, q.y, flags);
+        }
+    }
+    if (__any_sync(FULL, emax == 0x7FFu)) {
+        if (emax == 0x7FFu && any_tile) rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags);
+    }
+    regularize_column(col);
+    __syncwarp();
+
+    // warp: sum the 32 lane columns; lane l takes digits l and l+32 (rotated start: the
+    // 32 lanes read 32 distinct columns per step, 2 wavefronts per 64-bit access).
+    {
+        const int64_t* wb = win + warp * (D * 32);
+        int64_t s0 = 0, s1 = 0;
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) {
+            int cc = (lane + c) & 31;
+            s0 += wb[lane * 32 + cc];
+            if (lane + 32 < D) s1 += wb[(lane + 32) * 32 + cc];
+        }
+        wsum[warp][lane] = s0;
+        if (lane + 32 < D) wsum[warp][lane + 32] = s1;
+        uint32_t f = __reduce_or_sync(FULL, flags);
+        if (lane == 0 && f) atomicOr(&blk_flags, f);
+    }
+    __syncthreads();
+
+    // block: sum the warp partials (|.| <= WARPS*32*(2^51+2^11) < 2^61), regularize, publish.
+    if (warp == 0) {
+        int64_t a0 = 0, a1 = 0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+            a0 += wsum[w][lane];
+            if (lane + 32 < D) a1 += wsum[w][lane + 32];
+        }
+        regularize_warp(a0, a1, lane);
+        p.partial[(size_t)lane * XS_MAXB + blockIdx.x] = a0;
+        if (lane + 32 < D) p.partial[(size_t)(lane + 32) * XS_MAXB + blockIdx.x] = a1;
+        if (lane == 0) p.pflags[blockIdx.x] = blk_flags;
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) is_last = (atomicAdd(p.counter, 1u) == (unsigned)(G - 1));
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+
+    // grid: the last block merges the G block partials (digit-major, coalesced) and the
+    // handle state; G <= XS_MAXB so the raw sum stays below 2^62 before regularizing.
+    for (int j = warp; j < D; j += WARPS) {
+        int64_t s = 0;
+        for (uint64_t b = lane; b < G; b += 32) s += __ldcg(&p.partial[(size_t)j * XS_MAXB + b]);
+        s = warp_sum64(s);
+        if (lane == 0) wsum[0][j] = s;
+    }
+    if (warp == 1) {
+        uint32_t f = 0;
+        for (uint64_t b = lane; b < G; b += 32) f |= __ldcg(&p.pflags[b]);
+        f = __reduce_or_sync(FULL, f);
+        if (lane == 0) blk_flags = f;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int64_t a0 = wsum[0][lane], a1 = (lane + 32 < D) ? wsum[0][lane + 32] : 0;
+        uint32_t fl = blk_flags;
+        uint64_t cnt = n;
+        if (!p.overwrite) {
+            a0 += p.state->digit[lane];
+            if (lane + 32 < D) a1 += p.state->digit[lane + 32];
+            fl |= p.state->flags;
+            cnt += p.state->count;
+        }
+        regularize_warp(a0, a1, lane);
+        p.state->digit[lane] = a0;
+        if (lane + 32 < D) p.state->digit[lane + 32] = a1;
+        if (lane == 0) {
+            p.state->flags = fl;
+            p.state->count = cnt;
+            *p.counter = 0;                      // ready for the next launch (stream order)
+        }
+        if (p.res) {
+            xsum_result r = finalize_warp(a0, a1, fl, cnt, p.canon, su, lane);
+            if (lane == 0) *p.res = r;
+        }
+    }
+}
+
+template <int WARPS, int U>
+static cudaError_t launch_accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms,
+                                     cudaStream_t s) {
+    using C = AccCfg<WARPS, U>;
+    static bool attr_set = false;   // per process; the attribute is per function and device-independent
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_accumulate<WARPS, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const uint64_t head = (n && ((uintptr_t)x & 15)) ? 1 : 0;
+    const uint64_t ntiles = ((n - head) / 2) / ((uint64_t)C::T * U);
+    uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
+    if (g < 1) g = 1;
+    if (g > XS_MAXB) g = XS_MAXB;
+    k_accumulate<WARPS, U><<<(unsigned)g, C::T, C::SMEM, s>>>(x, n, p);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
+    return launch_accumulate<16, 4>(x, n, p, num_sms, s);
+}
+
+}  // namespace xs

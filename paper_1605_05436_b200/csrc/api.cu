@@ -1,0 +1,281 @@
+// C-ABI of libxsum.so (declared and documented in include/xsum.h).
+// Host-side argument checking, handle bookkeeping and launches; every arithmetic step of
+// the summation runs in the kernels (accumulate.cu, merge_finalize.cu, segments.cu).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <new>
+
+#include "xsum.h"
+#include "xsum_kernels.h"
+
+static std::atomic<uint64_t> g_launches{0};
+
+namespace xs {
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace xs
+
+struct xsum_ctx {
+    int device;
+    int num_sms;
+    xsum_state_image* state;
+    uint8_t* scratch;
+    uint64_t count;                 // host-side mirror of the summand count (capacity check)
+    uint32_t grid_limit;            // 0 = one block per SM
+    cudaStream_t copy_stream;       // host-buffer path only (lazily created)
+    cudaEvent_t ev_ready[2], ev_done[2];
+};
+
+namespace {
+
+constexpr uint64_t kMaxCount = 0x7FFFFFFFFFFFFFFFull;
+
+struct DeviceGuard {   // run on the handle's device, restore the caller's afterwards
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+xs::AccParams acc_params(xsum_ctx* h, int overwrite, xsum_result* res, uint64_t* canon) {
+    xs::AccParams p;
+    p.state = h->state;
+    p.counter = reinterpret_cast<uint32_t*>(h->scratch + xs::SCRATCH_COUNTER_OFF);
+    p.partial = reinterpret_cast<int64_t*>(h->scratch + xs::SCRATCH_PARTIAL_OFF);
+    p.pflags = reinterpret_cast<uint32_t*>(h->scratch + xs::SCRATCH_FLAGS_OFF);
+    p.overwrite = overwrite;
+    p.res = res;
+    p.canon = canon;
+    return p;
+}
+
+int grid_of(const xsum_ctx* h) {
+    return h->grid_limit ? (int)(h->grid_limit < XS_MAXB ? h->grid_limit : XS_MAXB) : h->num_sms;
+}
+
+int sms_of(int dev) {
+    static int cache[64] = {0};
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+size_t xsum_state_bytes(void) { return XSUM_STATE_BYTES; }
+size_t xsum_scratch_bytes(int device) { (void)device; return xs::SCRATCH_BYTES; }
+size_t xsum_result_bytes(void) { return sizeof(xsum_result); }
+uint64_t xsum_launch_count(void) { return g_launches.load(); }
+
+const char* xsum_status_str(xsum_status s) {
+    switch (s) {
+        case XSUM_OK: return "ok";
+        case XSUM_EINVAL: return "invalid argument";
+        case XSUM_ECAPACITY: return "capacity exceeded (more than 2^63-1 summands)";
+        case XSUM_ECUDA: return "CUDA error";
+        case XSUM_EMISMATCH: return "state image mismatch";
+        case XSUM_ENOMEM: return "out of host memory";
+    }
+    return "unknown status";
+}
+
+xsum_status xsum_create(xsum_ctx** h, int device, void* d_state, void* d_scratch, size_t scratch_bytes,
+                        void* stream) {
+    if (!h) return XSUM_EINVAL;
+    *h = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) return XSUM_ECUDA;
+    if (device < 0 || device >= ndev) return XSUM_EINVAL;
+    if (!d_state || !d_scratch || !aligned(d_state, 8) || !aligned(d_scratch, 256)) return XSUM_EINVAL;
+    if (scratch_bytes < xs::SCRATCH_BYTES) return XSUM_EINVAL;
+    DeviceGuard g(device);
+    if (!g.ok) return XSUM_ECUDA;
+    xsum_ctx* c = new (std::nothrow) xsum_ctx();
+    if (!c) return XSUM_ENOMEM;
+    c->device = device;
+    c->num_sms = sms_of(device);
+    c->state = static_cast<xsum_state_image*>(d_state);
+    c->scratch = static_cast<uint8_t*>(d_scratch);
+    c->count = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(c->scratch, 0, xs::SCRATCH_BYTES, s) != cudaSuccess ||
+        xs::init_state(c->state, s) != cudaSuccess) {
+        delete c;
+        return XSUM_ECUDA;
+    }
+    *h = c;
+    return XSUM_OK;
+}
+
+xsum_status xsum_reset(xsum_ctx* h, void* stream) {
+    if (!h) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::init_state(h->state, static_cast<cudaStream_t>(stream)) != cudaSuccess) return XSUM_ECUDA;
+    h->count = 0;
+    return XSUM_OK;
+}
+
+xsum_status xsum_accumulate(xsum_ctx* h, const double* d_x, uint64_t n, void* stream) {
+    if (!h) return XSUM_EINVAL;
+    if (n == 0) return XSUM_OK;
+    if (!d_x || !aligned(d_x, 8)) return XSUM_EINVAL;
+    if (n > kMaxCount - h->count) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::accumulate(d_x, n, acc_params(h, 0, nullptr, nullptr), grid_of(h), static_cast<cudaStream_t>(stream)) !=
+        cudaSuccess)
+        return XSUM_ECUDA;
+    h->count += n;
+    return XSUM_OK;
+}
+
+xsum_status xsum_sum(xsum_ctx* h, const double* d_x, uint64_t n, void* d_res, uint64_t* d_canon, void* stream) {
+    if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;
+    if (n && (!d_x || !aligned(d_x, 8))) return XSUM_EINVAL;
+    if (n > kMaxCount) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::accumulate(d_x, n, acc_params(h, 1, static_cast<xsum_result*>(d_res), d_canon), grid_of(h),
+                       static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
+    h->count = n;
+    return XSUM_OK;
+}
+
+xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, void* d_stage, size_t stage_bytes,
+                                 void* stream) {
+    if (!h) return XSUM_EINVAL;
+    if (n == 0) return XSUM_OK;
+    if (!h_x || !d_stage || !aligned(d_stage, 256) || stage_bytes < (2u << 20)) return XSUM_EINVAL;
+    if (n > kMaxCount - h->count) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (!h->copy_stream) {
+        if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return XSUM_ECUDA;
+        for (int b = 0; b < 2; ++b) {
+            if (cudaEventCreateWithFlags(&h->ev_ready[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&h->ev_done[b], cudaEventDisableTiming) != cudaSuccess)
+                return XSUM_ECUDA;
+        }
+        // first use: nothing consumed the staging halves yet
+        for (int b = 0; b < 2; ++b)
+            if (cudaEventRecord(h->ev_done[b], h->copy_stream) != cudaSuccess) return XSUM_ECUDA;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t half = (stage_bytes / 2) / 256 * 256;
+    const uint64_t per = half / sizeof(double);
+    uint8_t* base = static_cast<uint8_t*>(d_stage);
+    // order the copies after all prior work on `stream`
+    if (cudaEventRecord(h->ev_ready[0], s) != cudaSuccess || cudaStreamWaitEvent(h->copy_stream, h->ev_ready[0], 0) != cudaSuccess)
+        return XSUM_ECUDA;
+    uint64_t off = 0;
+    int b = 0;
+    while (off < n) {
+        uint64_t cnt = (n - off) < per ? (n - off) : per;
+        double* buf = reinterpret_cast<double*>(base + (uint64_t)b * half);
+        if (cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0) != cudaSuccess ||
+            cudaMemcpyAsync(buf, h_x + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->copy_stream) != cudaSuccess ||
+            cudaEventRecord(h->ev_ready[b], h->copy_stream) != cudaSuccess ||
+            cudaStreamWaitEvent(s, h->ev_ready[b], 0) != cudaSuccess)
+            return XSUM_ECUDA;
+        if (xs::accumulate(buf, cnt, acc_params(h, 0, nullptr, nullptr), grid_of(h), s) != cudaSuccess) return XSUM_ECUDA;
+        if (cudaEventRecord(h->ev_done[b], s) != cudaSuccess) return XSUM_ECUDA;
+        off += cnt;
+        b ^= 1;
+    }
+    h->count += n;
+    return XSUM_OK;
+}
+
+xsum_status xsum_merge(xsum_ctx* h, const void* d_states, uint32_t count, void* stream) {
+    if (!h) return XSUM_EINVAL;
+    if (count == 0) return XSUM_OK;
+    if (!d_states || !aligned(d_states, 8)) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::merge_states(h->state, d_states, count, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+xsum_status xsum_finalize_round(xsum_ctx* h, void* d_res, uint64_t* d_canon, void* stream) {
+    if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::finalize(h->state, static_cast<xsum_result*>(d_res), d_canon, static_cast<cudaStream_t>(stream)) !=
+        cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+xsum_status xsum_destroy(xsum_ctx* h) {
+    if (!h) return XSUM_EINVAL;
+    {
+        DeviceGuard g(h->device);
+        if (h->copy_stream) {
+            cudaStreamSynchronize(h->copy_stream);
+            for (int b = 0; b < 2; ++b) {
+                cudaEventDestroy(h->ev_ready[b]);
+                cudaEventDestroy(h->ev_done[b]);
+            }
+            cudaStreamDestroy(h->copy_stream);
+        }
+    }
+    delete h;
+    return XSUM_OK;
+}
+
+uint64_t xsum_count(const xsum_ctx* h) { return h ? h->count : 0; }
+
+xsum_status xsum_set_grid_limit(xsum_ctx* h, uint32_t max_blocks) {
+    if (!h) return XSUM_EINVAL;
+    h->grid_limit = max_blocks;
+    return XSUM_OK;
+}
+
+xsum_status xsum_sum_segments(const double* d_x, uint64_t nseg, uint64_t seg_len, double* d_out, uint64_t* d_canon,
+                              uint32_t* d_flags, void* stream) {
+    if (nseg == 0) return XSUM_OK;
+    if (!d_out || !aligned(d_out, 8) || (d_canon && !aligned(d_canon, 8)) || (d_flags && !aligned(d_flags, 4)))
+        return XSUM_EINVAL;
+    if (seg_len && (!d_x || !aligned(d_x, 8))) return XSUM_EINVAL;
+    if (seg_len && nseg > kMaxCount / seg_len) return XSUM_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
+    if (xs::sum_segments(d_x, nseg, seg_len, nullptr, d_out, d_canon, d_flags, sms_of(dev),
+                         static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+xsum_status xsum_sum_segments_csr(const double* d_x, const uint64_t* d_offsets, uint64_t nseg, double* d_out,
+                                  uint64_t* d_canon, uint32_t* d_flags, void* stream) {
+    if (nseg == 0) return XSUM_OK;
+    if (!d_offsets || !aligned(d_offsets, 8) || !d_out || !aligned(d_out, 8) || (d_canon && !aligned(d_canon, 8)) ||
+        (d_flags && !aligned(d_flags, 4)))
+        return XSUM_EINVAL;
+    if (!d_x || !aligned(d_x, 8)) return XSUM_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
+    if (xs::sum_segments(d_x, nseg, 0, d_offsets, d_out, d_canon, d_flags, sms_of(dev),
+                         static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// K4 (merge tree of superaccumulators) and K5 (finalize: canonicalize + round).
+//
+// Merge: the MapReduce post-process (§6.1; Spark driver merge
+// PAPER.md:1186-1189) as a Lemma-1 pairwise tree: states are added
+// digit-parallel with signed carries C in {-1,0,1} that move at most one digit.
+// Finalize: steps 6-7 of the PRAM algorithm, see finalize_warp.
+#include <cuda_runtime.h>
+
+#include "xsum_device.cuh"
+#include "xsum_kernels.h"
+
+namespace xs {
+
+__global__ void k_init_state(xsum_state_image* st) {
+    int t = threadIdx.x;
+    if (t < D) st->digit[t] = 0;
+    uint8_t* pad = st->pad;
+    if (t < (int)sizeof(st->pad)) pad[t] = 0;
+    if (t == 0) {
+        st->magic = XSUM_MAGIC;
+        st->version = (uint16_t)XSUM_VERSION;
+        st->w = (uint8_t)W;
+        st->ndigits = (uint8_t)D;
+        st->flags = 0;
+        st->reserved = 0;
+        st->count = 0;
+    }
+}
+
+// A state image is accepted iff its header matches and its digits are regularized
+// (|Y_j| <= R-1 below the top digit; top digit bounded by the value).
+__device__ __forceinline__ bool image_ok(const xsum_state_image* im, int64_t d0, int64_t d1, int lane) {
+    bool hdr = im->magic == XSUM_MAGIC && im->version == XSUM_VERSION && im->w == W && im->ndigits == D;
+    bool ok0 = d0 >= -(R - 1) && d0 <= R - 1;
+    bool ok1 = (lane + 32 < D - 1) ? (d1 >= -(R - 1) && d1 <= R - 1)
+                                   : ((lane + 32 == D - 1) ? (d1 >= -(1ll << 40) && d1 <= (1ll << 40)) : true);
+    return hdr && __all_sync(FULL, ok0 && ok1);
+}
+
+constexpr int MERGE_WARPS = 16;
+
+__global__ void __launch_bounds__(MERGE_WARPS * 32)
+k_merge(xsum_state_image* st, const xsum_state_image* ims, uint32_t count) {
+    __shared__ int64_t acc[MERGE_WARPS][64];
+    __shared__ uint64_t cnts[MERGE_WARPS];
+    __shared__ uint32_t fls[MERGE_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t a0 = 0, a1 = 0;
+    uint64_t cnt = 0;
+    uint32_t fl = 0;
+    // leaves: each warp folds states warp, warp+16, ... (Lemma-1 adds)
+    for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
+        const xsum_state_image* im = ims + s;
+        int64_t d0 = im->digit[lane];
+        int64_t d1 = (lane + 32 < D) ? im->digit[lane + 32] : 0;
+        if (image_ok(im, d0, d1, lane)) {
+            lemma1_add(a0, a1, d0, d1, lane);
+            cnt += im->count;
+            fl |= im->flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
+        } else {
+            fl |= XSUM_F_MISMATCH;
+        }
+    }
+    acc[warp][lane] = a0;
+    acc[warp][lane + 32] = a1;
+    if (lane == 0) { cnts[warp] = cnt; fls[warp] = fl; }
+    __syncthreads();
+    // pairwise tree over the warp results (depth log2(16))
+    for (int stride = MERGE_WARPS / 2; stride >= 1; stride >>= 1) {
+        if (warp < stride) {
+            int64_t b0 = acc[warp + stride][lane], b1 = acc[warp + stride][lane + 32];
+            lemma1_add(a0, a1, b0, b1, lane);
+            acc[warp][lane] = a0;
+            acc[warp][lane + 32] = a1;
+            if (lane == 0) { cnts[warp] += cnts[warp + stride]; fls[warp] |= fls[warp + stride]; }
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+        int64_t s0 = st->digit[lane], s1 = (lane + 32 < D) ? st->digit[lane + 32] : 0;
+        lemma1_add(a0, a1, s0, s1, lane);
+        st->digit[lane] = a0;
+        if (lane + 32 < D) st->digit[lane + 32] = a1;
+        if (lane == 0) {
+            st->count += cnts[0];
+            st->flags |= fls[0];
+        }
+    }
+}
+
+__global__ void k_finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon) {
+    __shared__ int64_t su[64];
+    const int lane = threadIdx.x & 31;
+    int64_t a0 = st->digit[lane];
+    int64_t a1 = (lane + 32 < D) ? st->digit[lane + 32] : 0;
+    xsum_result r = finalize_warp(a0, a1, st->flags, st->count, canon, su, lane);
+    if (lane == 0) *res = r;
+}
+
+cudaError_t init_state(xsum_state_image* st, cudaStream_t s) {
+    k_init_state<<<1, 64, 0, s>>>(st);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, cudaStream_t s) {
+    k_merge<<<1, MERGE_WARPS * 32, 0, s>>>(st, static_cast<const xsum_state_image*>(states), count);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s) {
+    k_finalize<<<1, 32, 0, s>>>(st, res, canon);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace xs

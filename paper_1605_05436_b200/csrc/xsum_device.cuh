@@ -1,0 +1,289 @@
+// Device building blocks of the superaccumulator reduction (sm_100a).
+//
+// Citations: PAPER.md line numbers of Goodrich & Eldawy (arXiv 1605.05436).
+// Notation follows the paper: radix R = 2^w (w = 52 here, reading R5 in DESIGN.md),
+// digits Y_j with value sum_j Y_j R^j (in units of 2^-1074),
+// (alpha,beta)-regularized with alpha = beta = R-1.
+#pragma once
+
+#include <stdint.h>
+
+#include "xsum.h"
+
+namespace xs {
+
+constexpr int W = XSUM_RADIX_BITS;          // 52
+constexpr int D = XSUM_NDIGITS;             // 42 digits: 2184 bits >= 1074+1024+63
+constexpr int64_t R = 1ll << W;
+constexpr uint64_t MASK = (1ull << W) - 1;
+constexpr unsigned FULL = 0xffffffffu;
+
+// Summands a lane column may take between two regularizations. Each summand adds one
+// chunk (|chunk| <= 2^52) to at most one position of each digit. A window holds at most
+// FLUSH_ELEMS hot-loop summands, as many compensating adds for NaN/Inf patterns (see
+// column_fix_special) and <= 10 head/tail/leftover summands, on top of a regularized
+// residue |Y| <= 2^51 + 2^11:  2^51 + 2^11 + (2*1016 + 10) * 2^52 + 2^51 < 2^63, so
+// neither the adds nor the balanced carry (y + R/2) can overflow int64 (the bound is
+// re-derived in tests/test_host_logic.py). The paper's "reserved extra bit"
+// becomes 11 bits of headroom per int64 digit here.
+constexpr int FLUSH_ELEMS = 1016;
+
+// ---------------------------------------------------------------------------------
+// Step 2 of the PRAM algorithm: split x into O(1) components whose
+// exponents are multiples of the radix exponent. For binary64 (IEEE, reading R1/R2):
+// |x| = M 2^(k-1074), M = m + [e!=0] 2^52 < 2^53, k = max(e,1)-1 in [0, 2045].
+// With i = k / 52 and o = k mod 52, sM 2^o (sM = +-M) is split at bit 52 into
+//   c0 = (sM 2^o) mod 2^52  in [0, 2^52)      -> digit i
+//   c1 = floor(sM 2^o / 2^52) in [-2^52, 2^52) -> digit i+1
+// so that c0 R^i + c1 R^(i+1) = x 2^1074 exactly. Integer adds only (PAPER.md:654-668:
+// integer digits with explicit overlap). All 32-bit halves, no FP instructions.
+// ---------------------------------------------------------------------------------
+struct Chunks {
+    uint32_t i;      // digit index of c0
+    uint32_t e;      // biased exponent field (0x7FF marks NaN/Inf)
+    int64_t c0, c1;
+};
+
+__device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi) {
+    Chunks c;
+    uint32_t e = (hi >> 20) & 0x7FFu;
+    uint32_t ep = max(e, 1u);
+    uint32_t k = ep - 1u;
+    uint32_t i = k / 52u;
+    uint32_t o = k - 52u * i;
+    uint32_t imp = e + 1u - ep;                       // hidden bit: 1 unless subnormal/zero
+    uint32_t mh = (hi & 0xFFFFFu) | (imp << 20);
+    uint64_t M = ((uint64_t)mh << 32) | lo;
+    int64_t s = (int64_t)((int32_t)hi >> 31);         // 0 or -1
+    int64_t sM = (int64_t)(M ^ (uint64_t)s) - s;      // +-M
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> (52u - o);                           // arithmetic: floor division
+    c.i = i;
+    c.e = e;
+    return c;
+}
+
+// Add one summand's chunks into a lane column (digit j at col[j*32]): the "localized"
+// add of PAPER.md:1043-1047 with carries deferred (PAPER.md:669-673 lazy carries).
+__device__ __forceinline__ void column_add(int64_t* col, const Chunks& c) {
+    int64_t* p = col + c.i * 32u;
+    p[0] += c.c0;
+    p[32] += c.c1;
+}
+
+// Flags of a NaN/Inf bit pattern (only called when e == 0x7FF).
+__device__ __forceinline__ uint32_t special_flags(uint32_t lo, uint32_t hi) {
+    if ((hi & 0xFFFFFu) | lo) return XSUM_F_NAN;
+    return (hi >> 31) ? XSUM_F_NINF : XSUM_F_PINF;
+}
+
+// Checked add for the non-hot paths (head/tail elements): specials are flagged, not added.
+__device__ __forceinline__ void column_add_checked(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags) {
+    Chunks c = decompose(lo, hi);
+    if (c.e == 0x7FFu) { flags |= special_flags(lo, hi); return; }
+    column_add(col, c);
+}
+
+// Undo the chunks the unchecked hot loop added for a NaN/Inf pattern (rare path):
+// adding the chunks of the sign-flipped pattern cancels the value exactly.
+__device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags) {
+    if (((hi >> 20) & 0x7FFu) != 0x7FFu) return;
+    flags |= special_flags(lo, hi);
+    column_add(col, decompose(lo, hi ^ 0x80000000u));
+}
+
+// ---------------------------------------------------------------------------------
+// Regularization (PAPER.md:559-576 with the GSD idea of PAPER.md:522-525): each digit
+// is split as Y_j = C_{j+1} R + r_j with a balanced remainder r_j in [-R/2, R/2) and
+// S_j = r_j + C_j. Each output digit depends only on digits j and j-1 (carry-free).
+// Input |Y_j| < 2^63 - 2^51; output |S_j| <= R/2 + 2^11 <= R-1. The top digit D-1 only
+// ever receives carries (its magnitude is bounded by the value), so it
+// is not split.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t balanced_carry(int64_t y) { return (y + (R >> 1)) >> W; }
+
+__device__ __forceinline__ void regularize_column(int64_t* col) {
+    int64_t cin = 0;
+#pragma unroll 6
+    for (int j = 0; j < D - 1; ++j) {
+        int64_t y = col[j * 32];
+        int64_t c = balanced_carry(y);
+        col[j * 32] = y - (c << W) + cin;
+        cin = c;
+    }
+    col[(D - 1) * 32] += cin;
+}
+
+// Digit-parallel regularization in a warp: lane l holds digit l (a0) and, for l < 10,
+// digit l+32 (a1).
+__device__ __forceinline__ void regularize_warp(int64_t& a0, int64_t& a1, int lane) {
+    int64_t c0 = balanced_carry(a0);
+    int64_t c1 = (lane + 32 < D - 1) ? balanced_carry(a1) : 0;
+    int64_t in0 = __shfl_up_sync(FULL, c0, 1);
+    int64_t in1 = __shfl_up_sync(FULL, c1, 1);
+    int64_t c31 = __shfl_sync(FULL, c0, 31);
+    if (lane == 0) { in0 = 0; in1 = c31; }
+    a0 = a0 - (c0 << W) + in0;
+    a1 = (lane + 32 < D) ? a1 - (c1 << W) + in1 : 0;
+}
+
+// ---------------------------------------------------------------------------------
+// Lemma 1: sum of two (R-1,R-1)-regularized superaccumulators.
+// P_j = Y_j + Z_j; C_{j+1} = 1 if P_j >= R-1, -1 if P_j <= -R+1, else 0 (reading R6);
+// W_j = P_j - C_{j+1} R; S_j = W_j + C_j. Digit-parallel across the warp.
+// The top digit (j = D-1) is never split (value bound).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ int lemma1_carry(int64_t P) {
+    return P >= R - 1 ? 1 : (P <= -(R - 1) ? -1 : 0);
+}
+
+__device__ __forceinline__ void lemma1_add(int64_t& a0, int64_t& a1, int64_t b0, int64_t b1, int lane) {
+    int64_t P0 = a0 + b0, P1 = a1 + b1;
+    int C0 = lemma1_carry(P0);
+    int C1 = (lane + 32 < D - 1) ? lemma1_carry(P1) : 0;
+    int64_t W0 = P0 - (int64_t)C0 * R, W1 = P1 - (int64_t)C1 * R;
+    int in0 = __shfl_up_sync(FULL, C0, 1);
+    int in1 = __shfl_up_sync(FULL, C1, 1);
+    int c31 = __shfl_sync(FULL, C0, 31);
+    if (lane == 0) { in0 = 0; in1 = c31; }
+    a0 = W0 + in0;
+    a1 = (lane + 32 < D) ? W1 + in1 : 0;
+}
+
+// ---------------------------------------------------------------------------------
+// Steps 6-7 of the PRAM algorithm, one warp:
+//  6. signed-carry propagation to the non-overlapping form by a parallel prefix over
+//     carries in {-1,0} ("a simple lookup table based on whether the input carry bit is
+//     -1, 0, or 1"): generate/propagate masks from two ballots and one
+//     64-bit add (carry-lookahead), giving digits u_j in [0, R) of |A| (reading R4).
+//  7. locate the most significant non-zero component, combine it with its neighbours and
+//     round to nearest, ties to even, on the truncated bits (reading R3, R11).
+// Input: regularized digits (|a| <= R-1), a0 = digit lane, a1 = digit lane+32.
+// su: 64 int64 of shared scratch owned by this warp.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t extract_bits(const int64_t* su, int pos, int cnt) {
+    // bits [pos, pos+cnt) (cnt <= 64, pos >= 0) of sum_j su[j] 2^(52 j), su[j] in [0, 2^52)
+    uint64_t r = 0;
+    int j0 = pos / 52;
+    int j1 = (pos + cnt - 1) / 52;
+    for (int j = j0; j <= j1 && j < D; ++j) {
+        uint64_t v = (uint64_t)su[j];
+        int sh = 52 * j - pos;
+        if (sh >= 0) { if (sh < 64) r |= v << sh; }
+        else r |= v >> (-sh);
+    }
+    return cnt >= 64 ? r : (r & ((1ull << cnt) - 1));
+}
+
+// Returns the result record in lane 0 (other lanes: unspecified); writes the canonical
+// image (34 limbs) to `canon` if non-null.
+__device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1, uint32_t flags, uint64_t count,
+                                     uint64_t* canon, int64_t* su, int lane) {
+    xsum_result r = {};
+    const bool has1 = lane + 32 < D;
+    uint64_t nz = (uint64_t)__ballot_sync(FULL, a0 != 0) | ((uint64_t)__ballot_sync(FULL, a1 != 0) << 32);
+    int sign = 0;
+    if (nz) {
+        int msd = 63 - __clzll((long long)nz);
+        int64_t top = __shfl_sync(FULL, msd < 32 ? a0 : a1, msd & 31);
+        sign = top < 0;
+    }
+    if (sign) { a0 = -a0; a1 = -a1; }           // now sum > 0 (or zero)
+
+    // split a = b R + r, r in [0,R), b in {-1,0}; t_j = r_j + b_{j-1} in [-1, R-1]
+    int64_t b0 = a0 >> W, b1 = a1 >> W;
+    int64_t r0 = a0 & (int64_t)MASK, r1 = a1 & (int64_t)MASK;
+    if (lane + 32 == D - 1) { r1 = a1; b1 = 0; }    // top digit: not split
+    int64_t in0 = __shfl_up_sync(FULL, b0, 1), in1 = __shfl_up_sync(FULL, b1, 1);
+    int64_t b31 = __shfl_sync(FULL, b0, 31);
+    if (lane == 0) { in0 = 0; in1 = b31; }
+    int64_t t0 = r0 + in0, t1 = has1 ? r1 + in1 : 0;
+    // borrow-lookahead: g_j = (t_j == -1), p_j = (t_j == 0); borrow_in = ((G|P) + G) ^ P
+    uint64_t G = (uint64_t)__ballot_sync(FULL, t0 == -1) | ((uint64_t)__ballot_sync(FULL, has1 && t1 == -1) << 32);
+    uint64_t P = (uint64_t)__ballot_sync(FULL, t0 == 0) | ((uint64_t)__ballot_sync(FULL, has1 && t1 == 0) << 32);
+    uint64_t CI = ((G | P) + G) ^ P;
+    int64_t u0 = (t0 - (int64_t)((CI >> lane) & 1)) & (int64_t)MASK;
+    int64_t u1 = t1 - (int64_t)((CI >> (lane + 32)) & 1);
+    if (lane + 32 < D - 1) u1 &= (int64_t)MASK;
+    su[lane] = u0;
+    if (has1) su[lane + 32] = u1;
+    __syncwarp();
+    uint64_t nzu = (uint64_t)__ballot_sync(FULL, u0 != 0) | ((uint64_t)__ballot_sync(FULL, has1 && u1 != 0) << 32);
+
+    // canonical image: 34 little-endian u64 limbs of A (two's complement)
+    if (canon) {
+        uint64_t l0 = extract_bits(su, 64 * lane, 64);
+        uint64_t l1 = (lane + 32 < XSUM_CANON_LIMBS) ? extract_bits(su, 64 * (lane + 32), 64) : 0;
+        if (sign) {
+            uint64_t z = (uint64_t)__ballot_sync(FULL, l0 != 0) | ((uint64_t)__ballot_sync(FULL, l1 != 0) << 32);
+            int zl = z ? __ffsll((long long)z) - 1 : 64;     // lowest non-zero limb
+            l0 = lane < zl ? 0 : (lane == zl ? (uint64_t)(-(int64_t)l0) : ~l0);
+            l1 = lane + 32 < zl ? 0 : (lane + 32 == zl ? (uint64_t)(-(int64_t)l1) : ~l1);
+        }
+        canon[lane] = l0;
+        if (lane + 32 < XSUM_CANON_LIMBS) canon[lane + 32] = l1;
+    }
+
+    if (lane == 0) {
+        r.count = count;
+        r.reserved = 0;
+        uint32_t fl = flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
+        uint64_t bits = 0;
+        int dir = 0;
+        if (!nzu) {                               // exact zero -> +0.0 (reading R9)
+            r.msb_exp = INT32_MIN; r.sign = 0; r.sig53 = 0; r.exp2 = 0;
+        } else {
+            int m = 63 - __clzll((long long)nzu);
+            int p = 52 * m + (63 - __clzll((long long)su[m]));     // leading bit of |A|
+            r.msb_exp = p - 1074;
+            r.sign = sign;
+            if (p <= 52) {                        // |A| < 2^53: subnormal / smallest normals, exact
+                bits = extract_bits(su, 0, 53);
+                r.sig53 = bits; r.exp2 = -1074;
+            } else {
+                int sh = p - 52;
+                uint64_t q = extract_bits(su, sh, 53);
+                int g = (int)extract_bits(su, sh - 1, 1);
+                int gpos = sh - 1;                // sticky: any bit below the guard bit
+                int jg = gpos / 52;
+                bool sticky = (nzu & ((1ull << jg) - 1)) != 0;
+                int off = gpos - 52 * jg;
+                if (off) sticky = sticky || ((uint64_t)su[jg] & ((1ull << off) - 1));
+                int up = g && (sticky || (q & 1));
+                if (g || sticky) dir = up ? 1 : -1;
+                q += (uint64_t)up;
+                if (q == (1ull << 53)) { q >>= 1; sh += 1; }
+                r.sig53 = q; r.exp2 = sh - 1074;
+                int Eb = sh + 1;
+                if (Eb >= 2047) { bits = 0x7FFull << 52; fl |= XSUM_F_OVERFLOW; dir = 1; }
+                else bits = ((uint64_t)Eb << 52) | (q - (1ull << 52));
+            }
+            if (dir) fl |= XSUM_F_INEXACT;
+            if (sign) { bits |= 1ull << 63; dir = -dir; }
+        }
+        if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) { bits = 0x7FF8000000000000ull; dir = 0; }
+        else if (fl & XSUM_F_PINF) { bits = 0x7FF0000000000000ull; dir = 0; }
+        else if (fl & XSUM_F_NINF) { bits = 0xFFF0000000000000ull; dir = 0; }
+        r.value = __longlong_as_double((long long)bits);
+        r.direction = dir;
+        r.flags = fl;
+    }
+    __syncwarp();
+    return r;
+}
+
+// 128-bit streaming load of two doubles as four 32-bit halves (evict-first from L1).
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint2 ldg_one(const double* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
+}  // namespace xs

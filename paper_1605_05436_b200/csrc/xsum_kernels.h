@@ -1,0 +1,38 @@
+// Internal launcher interface between the C-ABI (api.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "xsum.h"
+
+#define XS_MAXB 1024   // max blocks of one accumulate launch (= columns of the partial table)
+
+namespace xs {
+
+struct AccParams {
+    xsum_state_image* state;   // handle state (device)
+    int64_t* partial;          // [D][XS_MAXB] block partials, digit-major (scratch)
+    uint32_t* pflags;          // [XS_MAXB] block flags (scratch)
+    uint32_t* counter;         // arrival counter (scratch, 0 between launches)
+    int overwrite;             // 1: state := sum (fused reset), 0: state += sum
+    xsum_result* res;          // non-null: fused finalize
+    uint64_t* canon;           // optional canonical image for the fused finalize
+};
+
+// scratch layout: [0,256) counter; [256, 256 + 8*D*MAXB) partials; then MAXB u32 flags
+constexpr size_t SCRATCH_COUNTER_OFF = 0;
+constexpr size_t SCRATCH_PARTIAL_OFF = 256;
+constexpr size_t SCRATCH_FLAGS_OFF = SCRATCH_PARTIAL_OFF + sizeof(int64_t) * XSUM_NDIGITS * XS_MAXB;
+constexpr size_t SCRATCH_BYTES = SCRATCH_FLAGS_OFF + sizeof(uint32_t) * XS_MAXB;
+
+void note_launch();
+
+cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
+cudaError_t init_state(xsum_state_image* st, cudaStream_t s);
+cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, cudaStream_t s);
+cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s);
+cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
+                         double* out, uint64_t* canon, uint32_t* flags, int num_sms, cudaStream_t s);
+
+}  // namespace xs

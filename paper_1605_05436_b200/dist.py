@@ -1,0 +1,46 @@
+"""Multi-GPU exact sums: one process per GPU, NCCL over NVLink / NVSwitch.
+
+The paper's single-round MapReduce (§6.1; Spark version
+PAPER.md:1172-1189): every reducer (here: a GPU) sums its share exactly into one
+superaccumulator, the fixed-size superaccumulators are shuffled (here: one NCCL
+all-gather of the 384-byte state images), and the post-process
+merges them and rounds (here: xsum_merge + xsum_finalize_round on every rank, so
+all ranks hold the identical double). Exact addition is associative, so any
+partition of the input is valid.
+"""
+from __future__ import annotations
+
+from . import STATE_BYTES, Accumulator
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced shard [start, stop) of n items for `rank` of `world`
+    (the first n % world ranks get one extra item)."""
+    if world <= 0 or not (0 <= rank < world) or n < 0:
+        raise ValueError("bad shard arguments")
+    q, r = divmod(n, world)
+    start = rank * q + min(rank, r)
+    return start, start + q + (1 if rank < r else 0)
+
+
+def gather_states(state, group=None):
+    """All-gather the fixed-size state image of every rank -> uint8 tensor [world*384].
+
+    Pure torch.distributed plumbing (works with NCCL on GPUs and gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    if state.dtype != torch.uint8 or state.numel() != STATE_BYTES:
+        raise ValueError("state must be a uint8 tensor of 384 bytes")
+    world = dist.get_world_size(group)
+    out = torch.empty(world * STATE_BYTES, dtype=torch.uint8, device=state.device)
+    dist.all_gather_into_tensor(out, state.contiguous(), group=group)
+    return out
+
+
+def allreduce_exact(acc: Accumulator, group=None) -> Accumulator:
+    """Replace acc's state by the exact sum of all ranks' states (identical on every rank)."""
+    states = gather_states(acc.state, group)
+    acc.reset()
+    acc.merge(states)
+    return acc

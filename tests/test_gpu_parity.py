@@ -1,0 +1,366 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle, bit for bit.
+
+Every comparison checks the rounded double, the direction, the flags and the
+canonical 34-limb image of the exact sum; integer work, so the
+bar is bit-exactness (no tolerance). Inputs are seeded; expected values come only
+from oracle/ (never from the CUDA path).
+"""
+from __future__ import annotations
+
+import math
+import random
+import struct
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def xs():
+    import torch  # noqa: F401
+    import paper_1605_05436_b200 as xsum
+    xsum.build()
+    synth.build()
+    return xsum
+
+
+def b2f(b: int) -> float:
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+def to_dev(x: np.ndarray, offset: int = 0):
+    """Copy to the GPU; offset=1 gives a base that is 8-B but not 16-B aligned."""
+    import torch
+    buf = torch.empty(x.size + 2, dtype=torch.float64, device="cuda")
+    assert buf.data_ptr() % 16 == 0
+    t = buf[offset:offset + x.size]
+    t.copy_(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)))
+    return t
+
+
+def assert_same(res, canon, x: np.ndarray | None = None, ref=None, what: str = ""):
+    if ref is None:
+        ref = oracle.exact_sum(x)
+    r, limbs = ref
+    assert res.bits == r.bits, f"{what}: value {res.bits:016x} != oracle {r.bits:016x}"
+    assert res.direction == r.direction, what
+    assert res.flags == r.flags, f"{what}: flags {res.flags} != {r.flags}"
+    assert res.msb_exp == r.msb_exp and res.sign == r.sign, what
+    assert res.sig53 == r.sig53 and res.exp2 == r.exp2, what
+    if canon is not None:
+        assert (np.asarray(canon, dtype=np.uint64) == limbs).all(), f"{what}: canonical image differs"
+
+
+# ---------------------------------------------------------------------------------------
+# edge cases and small random sets
+# ---------------------------------------------------------------------------------------
+
+def test_golden_cases(xs):
+    from test_oracle_pins import GOLDEN_CASES
+    for name, xs_, out_bits, direction, _ in GOLDEN_CASES:
+        x = np.array(xs_, dtype=np.float64)
+        for off in (0, 1):
+            res, canon = xs.exact_sum(to_dev(x, off))
+            assert res.bits == out_bits, name
+            assert res.direction == direction, name
+            assert_same(res, canon, x, what=name)
+
+
+def _rand_set(rng: random.Random, n: int) -> list[float]:
+    from test_oracle_pins import _random_set
+    xs_ = _random_set(rng, n)
+    if rng.random() < 0.05 and xs_:   # a few specials
+        xs_[rng.randrange(len(xs_))] = rng.choice([math.inf, -math.inf, math.nan, b2f(0x7FF0000000000001)])
+    return xs_
+
+
+def test_many_small_sets_via_csr_segments(xs):
+    import torch
+    rng = random.Random(2024)
+    sets = [_rand_set(rng, rng.choice([0, 1, 2, 3, 5, 8, 13, 31, 32, 33, 64, 65, 200, 257, 1000]))
+            for _ in range(3000)]
+    offs = np.cumsum([0] + [len(s) for s in sets]).astype(np.int64)
+    flat = np.array([v for s in sets for v in s], dtype=np.float64)
+    vals, canon, flags = xs.sum_segments_csr(to_dev(flat), torch.from_numpy(offs).cuda(), canon=True, flags=True)
+    vals = vals.cpu().numpy().view(np.uint64)
+    canon = canon.cpu().numpy().view(np.uint64)
+    flags = flags.cpu().numpy()
+    for k, s in enumerate(sets):
+        r, limbs = oracle.exact_sum(np.array(s, dtype=np.float64))
+        assert int(vals[k]) == r.bits, (k, s)
+        assert int(flags[k]) == r.flags, k
+        assert (canon[k] == limbs).all(), k
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 31, 32, 33, 63, 64, 65, 1023, 1024, 1025, 4095, 4096, 4097,
+                               8191, 8192, 8193, 65535, 65537, 148 * 4096 - 1, 148 * 4096 + 3,
+                               1016 * 512 * 2 + 7, 5_000_017])
+@pytest.mark.parametrize("off", [0, 1])
+def test_sizes_alignment_both_paths(xs, n, off):
+    x = synth.gen.generate("c4", 77, n) if n else np.zeros(0)
+    d = to_dev(x, off)
+    ref = oracle.exact_sum(x)
+    res, canon = xs.exact_sum(d)                       # fused one-launch path (xsum_sum)
+    assert_same(res, canon, ref=ref, what=f"fused n={n} off={off}")
+    acc = xs.Accumulator()                             # create / accumulate / finalize path
+    acc.add(d)
+    res2, canon2 = acc.exact()
+    assert_same(res2, canon2, ref=ref, what=f"acc n={n} off={off}")
+    assert res2.count == n
+
+
+@pytest.mark.parametrize("blocks", [1, 2, 3, 7])
+def test_many_flush_windows_per_lane(xs, blocks):
+    """A capped grid forces each lane through many regularization windows (FLUSH_ELEMS),
+    with NaN/Inf patterns planted across windows (rescan path) and a ragged tail."""
+    n = 3 * 1016 * 512 * 2 * blocks + 4097 * blocks + 5
+    x = synth.gen.generate("c4", 999, n)
+    ref_finite = oracle.exact_sum(x)
+    acc = xs.Accumulator().set_grid_limit(blocks)
+    for off in (0, 1):
+        res, canon = acc.sum(to_dev(x, off), canon=True)
+        assert_same(xs.Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64),
+                    ref=ref_finite, what=f"blocks={blocks} off={off}")
+    y = x.copy()
+    rng = np.random.default_rng(blocks)
+    for i in rng.choice(n, size=40, replace=False):
+        y.view(np.uint64)[i] = rng.choice([0x7FF0000000000000, 0xFFF0000000000000, 0x7FF8000000000001])
+    acc.reset().add(to_dev(y))
+    res, canon = acc.exact()
+    assert_same(res, canon, y, what=f"specials blocks={blocks}")
+
+
+def test_chunked_accumulate_random_splits(xs):
+    rng = np.random.default_rng(5)
+    x = synth.gen.generate("c2", 0, 3_000_000)
+    d = to_dev(x)
+    ref = oracle.exact_sum(x)
+    for trial in range(5):
+        cuts = np.sort(rng.integers(0, x.size, size=rng.integers(1, 12)))
+        cuts = [0, *cuts.tolist(), x.size]
+        acc = xs.Accumulator()
+        for a, b in zip(cuts, cuts[1:]):
+            acc.add(d[a:b])
+        res, canon = acc.exact()
+        assert_same(res, canon, ref=ref, what=f"split {cuts}")
+
+
+def test_host_buffer_path(xs):
+    import torch
+    x = synth.gen.generate("c4", 1 << 30, 5_000_001)
+    ref = oracle.exact_sum(x)
+    pinned = torch.from_numpy(x).pin_memory()
+    acc = xs.Accumulator()
+    acc.add_host(pinned, stage_bytes=4 << 20)          # many double-buffered chunks
+    res, canon = acc.exact()
+    assert_same(res, canon, ref=ref, what="host path")
+    acc2 = xs.Accumulator().add_host(x)                # pageable numpy buffer
+    res2, canon2 = acc2.exact()
+    assert_same(res2, canon2, ref=ref, what="host path pageable")
+
+
+def test_permutation_invariance(xs):
+    rng = np.random.default_rng(9)
+    x = synth.gen.generate("c2", 10, 2_000_000)
+    base = xs.exact_sum(to_dev(x))
+    for _ in range(3):
+        res, canon = xs.exact_sum(to_dev(rng.permutation(x)))
+        assert res.bits == base[0].bits and (canon == base[1]).all()
+    assert_same(base[0], base[1], x)
+
+
+def test_specials_in_hot_loop_and_tails(xs):
+    """NaN/Inf patterns anywhere (main tiles, leftovers, head, tail) are flagged and do
+    not perturb the exact finite part (the rare rescan path of accumulate.cu)."""
+    rng = np.random.default_rng(1)
+    n = 4 * 1016 * 512 * 2 + 999
+    base = synth.gen.generate("c2", 0, n)
+    cases = {
+        "nan_mid": [(n // 3, 0x7FF8000000000000)],
+        "pinf_head": [(0, 0x7FF0000000000000)],
+        "ninf_tail": [(n - 1, 0xFFF0000000000000)],
+        "snan_payload": [(12345, 0x7FF0000000000001), (n - 700, 0x7FF0000000000002)],
+        "both_inf": [(5, 0x7FF0000000000000), (n // 2, 0xFFF0000000000000)],
+        "many": [(int(i), 0x7FF0000000000000 | int(rng.integers(0, 2)) << 63) for i in
+                 rng.choice(n, size=5000, replace=False)],
+    }
+    for name, plants in cases.items():
+        x = base.copy()
+        xb = x.view(np.uint64)
+        for i, bits in plants:
+            xb[i] = bits
+        for off in (0, 1):
+            res, canon = xs.exact_sum(to_dev(x, off))
+            assert_same(res, canon, x, what=f"{name} off={off}")
+
+
+# ---------------------------------------------------------------------------------------
+# merge (MapReduce post-process / all-gather path) and Lemma-1 stress
+# ---------------------------------------------------------------------------------------
+
+def test_merge_of_shard_states_equals_whole(xs):
+    import torch
+    from paper_1605_05436_b200 import dist
+    x = synth.gen.generate("c4", 0, 4_000_003)
+    d = to_dev(x)
+    ref = oracle.exact_sum(x)
+    for p in (1, 2, 3, 8, 37):
+        states = []
+        for r in range(p):
+            a, b = dist.shard_range(x.size, r, p)
+            states.append(xs.Accumulator().add(d[a:b]).state.clone())
+        blob = torch.cat(states[::-1])                 # any order
+        acc = xs.Accumulator().merge(blob)
+        res, canon = acc.exact()
+        assert_same(res, canon, ref=ref, what=f"merge p={p}")
+        assert res.count == x.size
+
+
+def _image(digits, count=0, flags=0, magic=0x4D555358):
+    from test_host_logic import encode_state
+    img = encode_state(0, count, flags)
+    img[0:4] = np.array([magic], dtype=np.uint32).view(np.uint8)
+    img[24:24 + 8 * 42] = np.array(digits, dtype=np.int64).view(np.uint8)
+    return img
+
+
+def test_lemma1_merge_adversarial_digits(xs):
+    """Regularized digits at the Lemma-1 boundaries (P_j = +-(R-1), +-(2R-2)) merged in a
+    tree; the canonical image must equal the exact integer sum of the digit vectors."""
+    import torch
+    R = 1 << 52
+    rng = random.Random(4)
+    pats = []
+    for _ in range(64):
+        kind = rng.random()
+        if kind < 0.3:
+            d = [rng.choice([R - 1, -(R - 1)]) for _ in range(41)]
+        elif kind < 0.6:
+            d = [rng.choice([R - 1, -(R - 1), 0, 1, -1, R // 2, -(R // 2)]) for _ in range(41)]
+        else:
+            d = [rng.randint(-(R - 1), R - 1) for _ in range(41)]
+        d.append(rng.randint(-(1 << 20), 1 << 20))
+        pats.append(d)
+    for k in (1, 2, 5, 16, 17, 64):
+        imgs = np.concatenate([_image(p) for p in pats[:k]])
+        acc = xs.Accumulator().merge(torch.from_numpy(imgs).cuda())
+        res, canon = acc.exact()
+        A = sum(sum(v << (52 * j) for j, v in enumerate(p)) for p in pats[:k])
+        ref_r = oracle.round_limbs(oracle.int_to_limbs(A), 0, 0)
+        assert (canon == oracle.int_to_limbs(A)).all(), k
+        assert res.bits == ref_r.bits and res.direction == ref_r.direction, k
+        assert res.flags == ref_r.flags
+
+
+def test_merge_rejects_bad_images(xs):
+    import torch
+    good = _image([1] + [0] * 41, count=3)
+    bad_magic = _image([5] + [0] * 41, magic=0x12345678)
+    bad_digit = _image([1 << 52] + [0] * 41)          # not regularized (|Y| > R-1)
+    acc = xs.Accumulator().merge(torch.from_numpy(np.concatenate([good, bad_magic, bad_digit])).cuda())
+    res, canon = acc.exact()
+    assert res.flags & xs.F_MISMATCH
+    assert res.bits == 1 and res.count == 3            # only the good image counted: 2^-1074
+
+
+def test_launch_counter_counts_kernels(xs):
+    n0 = xs.launch_count()
+    acc = xs.Accumulator()              # init kernel
+    acc.add(to_dev(np.ones(1000)))      # one accumulate kernel
+    acc.result()                        # one finalize kernel
+    assert xs.launch_count() - n0 == 3
+
+
+# ---------------------------------------------------------------------------------------
+# segmented sums (config 5 and ragged)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seg_len", [1, 2, 3, 31, 33, 127, 4096, 5000, 1016 * 64 + 3])
+def test_segments_ragged_lengths(xs, seg_len):
+    nseg = max(1, min(300, 2_000_000 // seg_len))
+    x = synth.gen.generate("c5", 3, nseg * seg_len)
+    x.view(np.uint64)[7 % x.size] = 0x7FF8000000000000        # one NaN in segment 0
+    vals, canon, flags = xs.sum_segments(to_dev(x, 1), seg_len, canon=True, flags=True)
+    vals = vals.cpu().numpy().view(np.uint64)
+    canon = canon.cpu().numpy().view(np.uint64)
+    flags = flags.cpu().numpy()
+    for s in range(nseg):
+        r, limbs = oracle.exact_sum(x[s * seg_len:(s + 1) * seg_len])
+        assert int(vals[s]) == r.bits and int(flags[s]) == r.flags and (canon[s] == limbs).all(), s
+
+
+# ---------------------------------------------------------------------------------------
+# full BASELINE.json configs (c1..c5), inputs from the device generator; expected values
+# from the oracle over the host generator's identical bytes
+# ---------------------------------------------------------------------------------------
+
+def _host_config(name: str) -> np.ndarray:
+    return synth.host_generate(name)            # c3: pre-permutation order (sum is order-free)
+
+
+def _check_device_input_sample(name: str, d):
+    """The device generator produced the same bytes as the host generator (sampled)."""
+    if name == "c3":
+        return
+    n = d.numel()
+    for start in (0, n // 2, n - 4096):
+        a = synth.gen.generate(name, start, 4096)
+        assert (d[start:start + 4096].cpu().numpy().view(np.uint64) == a.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_full_config_parity(xs, name):
+    import torch
+    d = synth.device_generate(name)
+    _check_device_input_sample(name, d)
+    res, canon = xs.exact_sum(d)
+    del d
+    torch.cuda.empty_cache()
+    ref = oracle.exact_sum(_host_config(name))
+    assert_same(res, canon, ref=ref, what=name)
+    if name == "c3":   # the exact sum is the sum of the tiny terms alone
+        cfg = synth.CONFIGS["c3"]
+        tiny = synth.gen.generate("c3", 2 * cfg["npairs"], cfg["ntiny"], permute=False)
+        r_t, l_t = oracle.exact_sum(tiny)
+        assert (l_t == canon).all() and r_t.bits == res.bits
+
+
+def test_full_config_c5_segments(xs):
+    d = synth.device_generate("c5")
+    cfg = synth.CONFIGS["c5"]
+    vals, canon, flags = xs.sum_segments(d, cfg["seg_len"], canon=True, flags=True)
+    vals = vals.cpu().numpy().view(np.uint64)
+    canon = canon.cpu().numpy().view(np.uint64)
+    flags = flags.cpu().numpy()
+    host = _host_config("c5")
+    L = cfg["seg_len"]
+    for s in range(cfg["nseg"]):
+        r, limbs = oracle.exact_sum(host[s * L:(s + 1) * L], nthreads=1)
+        assert int(vals[s]) == r.bits and int(flags[s]) == r.flags and (canon[s] == limbs).all(), s
+
+
+@pytest.mark.slow
+def test_full_config_c4_one_gpu(xs):
+    """n = 2^33 (64 GiB) on one GPU, fused path (the bench's launch configuration);
+    the oracle streams the same 2^33 doubles from the host generator in chunks."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    cfg = synth.CONFIGS["c4"]
+    if free < cfg["n"] * 8 + (4 << 30):
+        pytest.skip("not enough device memory for 64 GiB")
+    d = synth.device_generate("c4")
+    res, canon = xs.exact_sum(d)
+    del d
+    torch.cuda.empty_cache()
+    acc = oracle.Accumulator()
+    chunk = 1 << 26
+    buf = np.empty(chunk, dtype=np.float64)
+    for start in range(0, cfg["n"], chunk):
+        acc.add(synth.host_generate("c4", start, chunk, out=buf))
+    assert_same(res, canon, ref=(acc.result(), acc.limbs), what="c4")
+    assert math.isinf(res.value) or res.msb_exp < 1024      # (Q12: almost surely +-Inf)

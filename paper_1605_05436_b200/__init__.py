@@ -50,7 +50,7 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile libxsum.so in-tree (nvcc, sm_100a)."""
     import importlib
-    return importlib.import_module(__name__ + ".build").build(force=force)
+    return importlib.import_module(__name__ + "._build").build(force=force)
 
 
 def lib() -> ctypes.CDLL:
@@ -58,7 +58,7 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
         if not os.path.exists(SO_PATH):
-            raise RuntimeError(f"{SO_PATH} not built: run `python -m paper_1605_05436_b200.build` "
+            raise RuntimeError(f"{SO_PATH} not built: run `python -m paper_1605_05436_b200._build` "
                                "or __graft_entry__.build() (no CPU fallback exists)")
         L = ctypes.CDLL(SO_PATH)
         p, u64, u32, i32, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t

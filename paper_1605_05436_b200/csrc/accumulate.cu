@@ -32,15 +32,15 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 
 template <int U, int T>
 __device__ __forceinline__ void rescan_window(int64_t* col, const uint4* body, uint64_t t0, uint64_t t1,
-                                              uint64_t G, uint64_t TV, int tid, uint32_t& flags) {
+                                              uint64_t G, uint64_t TV, int tid, uint32_t& flags, uint32_t one) {
     // Rare path: this lane summed a NaN/Inf bit pattern as if finite somewhere in tiles
     // [t0, t1] (step G). Re-read its elements and cancel those chunks exactly.
     for (uint64_t tt = t0; tt <= t1; tt += G) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
-            column_fix_special(col, v.x, v.y, flags);
-            column_fix_special(col, v.z, v.w, flags);
+            column_fix_special(col, v.x, v.y, flags, one);
+            column_fix_special(col, v.z, v.w, flags, one);
         }
     }
 }
@@ -71,7 +71,8 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     const uint64_t ntiles = nvec / TV;
     const uint64_t G = gridDim.x;
 
-    uint32_t emax = 0;
+    const uint32_t one = p.one;
+    uint32_t nspec = 0;                 // NaN/Inf patterns summed unchecked in this window
     int since = 0;
     uint64_t wstart = blockIdx.x, tlast = 0;
     bool any_tile = false;
@@ -90,22 +91,22 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            Chunks a = decompose(cur[u].x, cur[u].y);
-            emax = max(emax, a.e);
-            column_add(col, a);
-            Chunks b = decompose(cur[u].z, cur[u].w);
-            emax = max(emax, b.e);
-            column_add(col, b);
+            Chunks a = decompose(cur[u].x, cur[u].y, one);
+            nspec += a.spec;
+            column_add(col, a, one);
+            Chunks b = decompose(cur[u].z, cur[u].w, one);
+            nspec += b.spec;
+            column_add(col, b, one);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) cur[u] = nxt[u];
         any_tile = true;
         tlast = t;
         if (++since == C::FLUSH_TILES) {
-            if (__any_sync(FULL, emax == 0x7FFu)) {
-                if (emax == 0x7FFu) rescan_window<U, T>(col, body, wstart, t, G, TV, tid, flags);
+            if (__any_sync(FULL, nspec != 0)) {
+                if (nspec) rescan_window<U, T>(col, body, wstart, t, G, TV, tid, flags, one);
             }
-            emax = 0;
+            nspec = 0;
             regularize_column(col);
             since = 0;
             wstart = tn;
@@ -123,21 +124,21 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
             uint64_t v = v0 + (uint64_t)u * T + tid;
             if (v < nvec) {
                 uint4 q = ldg_stream(body + v);
-                column_add_checked(col, q.x, q.y, flags);
-                column_add_checked(col, q.z, q.w, flags);
+                column_add_checked(col, q.x, q.y, flags, one);
+                column_add_checked(col, q.z, q.w, flags, one);
             }
         }
         if (tid == 0 && head) {
             uint2 q = ldg_one(x);
-            column_add_checked(col, q.x, q.y, flags);
+            column_add_checked(col, q.x, q.y, flags, one);
         }
         if (tid == 1 && (nbody & 1)) {
             uint2 q = ldg_one(x + head + 2 * nvec);
-            column_add_checked(col, q.x, q.y, flags);
+            column_add_checked(col, q.x, q.y, flags, one);
         }
     }
-    if (__any_sync(FULL, emax == 0x7FFu)) {
-        if (emax == 0x7FFu && any_tile) rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags);
+    if (__any_sync(FULL, nspec != 0)) {
+        if (nspec && any_tile) rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags, one);
     }
     regularize_column(col);
     __syncwarp();

@@ -52,6 +52,7 @@ xs::AccParams acc_params(xsum_ctx* h, int overwrite, xsum_result* res, uint64_t*
     p.overwrite = overwrite;
     p.res = res;
     p.canon = canon;
+    p.one = 1;
     return p;
 }
 

@@ -17,20 +17,20 @@ constexpr int SEG_FLUSH_ITERS = FLUSH_ELEMS / (2 * SEG_U);
 constexpr size_t SEG_SMEM = (size_t)SEG_WARPS * D * 32 * sizeof(int64_t);
 
 __device__ __forceinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_t it0, uint64_t it1, int lane,
-                                           uint32_t& flags) {
+                                           uint32_t& flags, uint32_t one) {
     for (uint64_t it = it0; it <= it1; ++it) {
 #pragma unroll
         for (int u = 0; u < SEG_U; ++u) {
             uint4 v = ldg_stream(body + it * (32 * SEG_U) + u * 32 + lane);
-            column_fix_special(col, v.x, v.y, flags);
-            column_fix_special(col, v.z, v.w, flags);
+            column_fix_special(col, v.x, v.y, flags, one);
+            column_fix_special(col, v.z, v.w, flags, one);
         }
     }
 }
 
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
-           double* __restrict__ out, uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags) {
+           double* __restrict__ out, uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -43,7 +43,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         const double* xs = x + beg;
 #pragma unroll
         for (int j = 0; j < D; ++j) col[j * 32] = 0;
-        uint32_t flags = 0, emax = 0;
+        uint32_t flags = 0, nspec = 0;
 
         const uint64_t head = (len && ((uintptr_t)xs & 15)) ? 1 : 0;
         const uint64_t nbody = len - head;
@@ -66,20 +66,20 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
             }
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) {
-                Chunks a = decompose(cur[u].x, cur[u].y);
-                emax = max(emax, a.e);
-                column_add(col, a);
-                Chunks b = decompose(cur[u].z, cur[u].w);
-                emax = max(emax, b.e);
-                column_add(col, b);
+                Chunks a = decompose(cur[u].x, cur[u].y, one);
+                nspec += a.spec;
+                column_add(col, a, one);
+                Chunks b = decompose(cur[u].z, cur[u].w, one);
+                nspec += b.spec;
+                column_add(col, b, one);
             }
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) cur[u] = nxt[u];
             if (++since == SEG_FLUSH_ITERS) {
-                if (__any_sync(FULL, emax == 0x7FFu)) {
-                    if (emax == 0x7FFu) seg_rescan(col, body, wstart, it, lane, flags);
+                if (__any_sync(FULL, nspec != 0)) {
+                    if (nspec) seg_rescan(col, body, wstart, it, lane, flags, one);
                 }
-                emax = 0;
+                nspec = 0;
                 regularize_column(col);
                 since = 0;
                 wstart = it + 1;
@@ -88,19 +88,19 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         // leftover vectors, head and tail: checked adds
         for (uint64_t v = nit * (32 * SEG_U) + lane; v < nvec; v += 32) {
             uint4 q = ldg_stream(body + v);
-            column_add_checked(col, q.x, q.y, flags);
-            column_add_checked(col, q.z, q.w, flags);
+            column_add_checked(col, q.x, q.y, flags, one);
+            column_add_checked(col, q.z, q.w, flags, one);
         }
         if (lane == 0 && head) {
             uint2 q = ldg_one(xs);
-            column_add_checked(col, q.x, q.y, flags);
+            column_add_checked(col, q.x, q.y, flags, one);
         }
         if (lane == 1 && (nbody & 1)) {
             uint2 q = ldg_one(xs + head + 2 * nvec);
-            column_add_checked(col, q.x, q.y, flags);
+            column_add_checked(col, q.x, q.y, flags, one);
         }
-        if (__any_sync(FULL, emax == 0x7FFu)) {
-            if (emax == 0x7FFu && since) seg_rescan(col, body, wstart, nit - 1, lane, flags);
+        if (__any_sync(FULL, nspec != 0)) {
+            if (nspec && since) seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
         }
         regularize_column(col);
         __syncwarp();
@@ -137,7 +137,7 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
     uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (86 KB smem each)
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-    k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags);
+    k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags, 1u);
     note_launch();
     return cudaGetLastError();
 }

@@ -40,34 +40,65 @@ constexpr int FLUSH_ELEMS = 1016;
 // ---------------------------------------------------------------------------------
 struct Chunks {
     uint32_t i;      // digit index of c0
-    uint32_t e;      // biased exponent field (0x7FF marks NaN/Inf)
+    uint32_t spec;   // 1 iff the exponent field is 0x7FF (NaN/Inf pattern), else 0
     int64_t c0, c1;
 };
 
-__device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi) {
+// Integer helpers pinned to the FMA pipe (IMAD / IMAD.HI / IMAD.WIDE): the decode is
+// otherwise ALU-pipe bound (ncu: profiles/). `one` is a runtime 1 (a kernel argument) so
+// that ptxas cannot fold x*one+y back into an ALU-pipe IADD3.
+__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
+    uint32_t r; asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+}
+__device__ __forceinline__ int32_t mulhi_s32(int32_t a, int32_t b) {
+    int32_t r; asm("mul.hi.s32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+}
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r; asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r;
+}
+__device__ __forceinline__ uint64_t madwide_u32(uint32_t a, uint32_t b, uint64_t c) {
+    uint64_t r; asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c)); return r;
+}
+// d + c for 64-bit values, entirely on the FMA pipe (two IMADs).
+__device__ __forceinline__ int64_t add64_fma(int64_t d, int64_t c, uint32_t one) {
+    uint64_t t = madwide_u32((uint32_t)(uint64_t)c, one, (uint64_t)d);
+    uint32_t th = mad_u32((uint32_t)((uint64_t)c >> 32), one, (uint32_t)(t >> 32));
+    return (int64_t)(((uint64_t)th << 32) | (uint32_t)t);
+}
+
+// mulhi(x, K52) = floor(x / 52) for 0 <= x <= 2047 (K52 = 20165 * 2^12; 52*20165 = 2^20 + 4,
+// relative error 4/2^20 < 1/(52*2047); checked for every x in tests/test_host_logic.py).
+constexpr uint32_t K52 = 20165u << 12;
+// mulhi(e, KSPEC) = 1 iff e == 2047 for e in [0, 2047]  (2047*KSPEC >= 2^32 > 2046*KSPEC).
+constexpr uint32_t KSPEC = 2098177u;
+
+__device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t one) {
     Chunks c;
-    uint32_t e = (hi >> 20) & 0x7FFu;
+    uint32_t e = (hi >> 20) & 0x7FFu;                     // biased exponent
     uint32_t ep = max(e, 1u);
-    uint32_t k = ep - 1u;
-    uint32_t i = k / 52u;
-    uint32_t o = k - 52u * i;
-    uint32_t imp = e + 1u - ep;                       // hidden bit: 1 unless subnormal/zero
-    uint32_t mh = (hi & 0xFFFFFu) | (imp << 20);
-    uint64_t M = ((uint64_t)mh << 32) | lo;
-    int64_t s = (int64_t)((int32_t)hi >> 31);         // 0 or -1
-    int64_t sM = (int64_t)(M ^ (uint64_t)s) - s;      // +-M
+    uint32_t k = mad_u32(ep, one, 0xFFFFFFFFu);           // ep - 1: LSB position of M
+    uint32_t i = mulhi_u32(k, K52);                       // k / 52
+    uint32_t o = mad_u32(i, (uint32_t)-52, k);            // k mod 52
+    // hi - k*2^20 = sign | hidden bit | top 20 fraction bits (hidden = [e != 0])
+    uint32_t mhs = mad_u32(k, 0xFFF00000u, hi);
+    int32_t S = mulhi_s32((int32_t)hi, 2);                // 0 or -1 (sign mask)
+    uint32_t sbit = mulhi_u32(hi, 2u);                    // 0 or 1
+    uint32_t S31 = mulhi_u32((uint32_t)S, 0x80000000u);   // 0 or 0x7FFFFFFF
+    // sM = +-M = (M ^ S) - S, with M_hi ^ S = mhs ^ S31 (the sign bit of mhs is s)
+    uint64_t onec = ((uint64_t)(mhs ^ S31) << 32) | (lo ^ (uint32_t)S);
+    int64_t sM = (int64_t)madwide_u32(sbit, one, onec);
     c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> (52u - o);                           // arithmetic: floor division
+    c.c1 = sM >> (52u - o);                               // arithmetic: floor division
     c.i = i;
-    c.e = e;
+    c.spec = mulhi_u32(e, KSPEC);
     return c;
 }
 
 // Add one summand's chunks into a lane column (digit j at col[j*32]): the "localized"
 // add of PAPER.md:1043-1047 with carries deferred (PAPER.md:669-673 lazy carries).
-__device__ __forceinline__ void column_add(int64_t* col, const Chunks& c) {
+__device__ __forceinline__ void column_add(int64_t* col, const Chunks& c, uint32_t one) {
     int64_t* p = col + c.i * 32u;
-    p[0] += c.c0;
+    p[0] = add64_fma(p[0], c.c0, one);
     p[32] += c.c1;
 }
 
@@ -78,18 +109,20 @@ __device__ __forceinline__ uint32_t special_flags(uint32_t lo, uint32_t hi) {
 }
 
 // Checked add for the non-hot paths (head/tail elements): specials are flagged, not added.
-__device__ __forceinline__ void column_add_checked(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags) {
-    Chunks c = decompose(lo, hi);
-    if (c.e == 0x7FFu) { flags |= special_flags(lo, hi); return; }
-    column_add(col, c);
+__device__ __forceinline__ void column_add_checked(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags,
+                                                   uint32_t one) {
+    Chunks c = decompose(lo, hi, one);
+    if (c.spec) { flags |= special_flags(lo, hi); return; }
+    column_add(col, c, one);
 }
 
 // Undo the chunks the unchecked hot loop added for a NaN/Inf pattern (rare path):
 // adding the chunks of the sign-flipped pattern cancels the value exactly.
-__device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags) {
+__device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags,
+                                                   uint32_t one) {
     if (((hi >> 20) & 0x7FFu) != 0x7FFu) return;
     flags |= special_flags(lo, hi);
-    column_add(col, decompose(lo, hi ^ 0x80000000u));
+    column_add(col, decompose(lo, hi ^ 0x80000000u, one), one);
 }
 
 // ---------------------------------------------------------------------------------

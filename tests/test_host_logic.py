@@ -242,3 +242,22 @@ def test_product_package_never_imports_oracle():
             text = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(import|from)\s+paper_1605_05436_b200", text, re.M), f
             assert not re.search(r'#include\s+"xsum', text), f
+
+
+def test_decode_magic_constants():
+    """Constants of decompose() in xsum_device.cuh: mulhi(k, K52) = k // 52 for every
+    k the kernel can see (k <= 2046; 0..2047 checked) and mulhi(e, KSPEC) = [e == 2047]."""
+    src = open(os.path.join(ROOT, "paper_1605_05436_b200", "csrc", "xsum_device.cuh")).read()
+    k52 = eval(re.search(r"constexpr uint32_t K52 = (.*?);", src).group(1).replace("u", ""))
+    kspec = eval(re.search(r"constexpr uint32_t KSPEC = (.*?);", src).group(1).replace("u", ""))
+    for k in range(2048):
+        assert (k * k52) >> 32 == k // 52
+        assert (k * kspec) >> 32 == (1 if k == 2047 else 0)
+    # hi - k*2^20 keeps the sign bit and sets the hidden bit exactly when e != 0
+    for e in (0, 1, 2, 1023, 2046, 2047):
+        for s in (0, 1):
+            m_hi = 0xABCDE
+            hi = (s << 31) | (e << 20) | m_hi
+            k = max(e, 1) - 1
+            mhs = (hi - k * (1 << 20)) & 0xFFFFFFFF
+            assert mhs == (s << 31) | ((1 if e else 0) << 20) | m_hi

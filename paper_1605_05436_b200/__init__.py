@@ -19,6 +19,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libxsum.so")
+# development only: benchmark an alternative build of the same C-ABI (tools/variants.py)
+SO_PATH = os.environ.get("XSUM_LIBRARY", SO_PATH)
 
 STATE_BYTES = 384
 RESULT_BYTES = 48

@@ -76,43 +76,55 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     int since = 0;
     uint64_t wstart = blockIdx.x, tlast = 0;
     bool any_tile = false;
-    uint4 cur[U];
-    uint64_t t = blockIdx.x;
-    if (t < ntiles) {
+    // Three register buffers rotate without moves: while one tile is decoded the next two
+    // are in flight (3 x 64 B per thread = 96 KiB per SM), enough to cover loaded HBM
+    // latency (~1 us) at full bandwidth.
+    auto load_tile = [&](uint4 (&buf)[U], uint64_t tt) {
+        if (tt < ntiles) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = ldg_stream(body + t * TV + (uint64_t)u * T + tid);
-    }
-    while (t < ntiles) {
-        const uint64_t tn = t + G;
-        uint4 nxt[U];
-        if (tn < ntiles) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) nxt[u] = ldg_stream(body + tn * TV + (uint64_t)u * T + tid);
+            for (int u = 0; u < U; ++u) buf[u] = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
         }
+    };
+    auto do_tile = [&](const uint4 (&buf)[U], uint64_t tt) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            Chunks a = decompose(cur[u].x, cur[u].y, one);
+            Chunks a = decompose(buf[u].x, buf[u].y, one);
             nspec += a.spec;
             column_add(col, a, one);
-            Chunks b = decompose(cur[u].z, cur[u].w, one);
+            Chunks b = decompose(buf[u].z, buf[u].w, one);
             nspec += b.spec;
             column_add(col, b, one);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
         any_tile = true;
-        tlast = t;
+        tlast = tt;
         if (++since == C::FLUSH_TILES) {
             if (__any_sync(FULL, nspec != 0)) {
-                if (nspec) rescan_window<U, T>(col, body, wstart, t, G, TV, tid, flags, one);
+                if (nspec) rescan_window<U, T>(col, body, wstart, tt, G, TV, tid, flags, one);
             }
             nspec = 0;
             regularize_column(col);
             since = 0;
-            wstart = tn;
+            wstart = tt + G;
             any_tile = false;
         }
-        t = tn;
+    };
+    uint4 A[U], B[U], Cb[U];
+    uint64_t t = blockIdx.x;
+    load_tile(A, t);
+    load_tile(B, t + G);
+    load_tile(Cb, t + 2 * G);
+    while (t < ntiles) {
+        do_tile(A, t);
+        load_tile(A, t + 3 * G);
+        t += G;
+        if (t >= ntiles) break;
+        do_tile(B, t);
+        load_tile(B, t + 3 * G);
+        t += G;
+        if (t >= ntiles) break;
+        do_tile(Cb, t);
+        load_tile(Cb, t + 3 * G);
+        t += G;
     }
 
     // leftover vectors (< one tile), the unaligned head and the odd tail element: checked
@@ -242,8 +254,15 @@ static cudaError_t launch_accumulate(const double* x, uint64_t n, const AccParam
     return cudaGetLastError();
 }
 
+#ifndef XS_ACC_WARPS
+#define XS_ACC_WARPS 16   // 16 warps x 42 digits x 32 lanes x 8 B = 168 KiB of lane columns per SM
+#endif
+#ifndef XS_ACC_U
+#define XS_ACC_U 4        // 16-B vectors per thread per tile (8 summands), double-buffered in registers
+#endif
+
 cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    return launch_accumulate<16, 4>(x, n, p, num_sms, s);
+    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U>(x, n, p, num_sms, s);
 }
 
 }  // namespace xs

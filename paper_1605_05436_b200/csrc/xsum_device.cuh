@@ -96,9 +96,11 @@ __device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t o
 
 // Add one summand's chunks into a lane column (digit j at col[j*32]): the "localized"
 // add of PAPER.md:1043-1047 with carries deferred (PAPER.md:669-673 lazy carries).
+// (plain IADD3/IMAD.X adds: the LDS -> add -> STS chain is latency-critical)
 __device__ __forceinline__ void column_add(int64_t* col, const Chunks& c, uint32_t one) {
+    (void)one;
     int64_t* p = col + c.i * 32u;
-    p[0] = add64_fma(p[0], c.c0, one);
+    p[0] += c.c0;
     p[32] += c.c1;
 }
 

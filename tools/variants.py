@@ -1,0 +1,59 @@
+"""Build and time compile-time variants of the accumulate kernel (development tool).
+
+    python tools/variants.py build            # here (nvcc cross-compiles)
+    python tools/variants.py run [--n N]      # on the GPU box: one JSON line per variant
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "build", "variants")
+VARIANTS = [(16, 4), (16, 2), (12, 4), (14, 4), (16, 3)]
+
+
+def build():
+    from paper_1605_05436_b200 import _build as b
+    os.makedirs(OUT, exist_ok=True)
+    for w, u in VARIANTS:
+        so = os.path.join(OUT, f"libxsum_w{w}_u{u}.so")
+        cmd = ["nvcc", *b.ARCH, *b.FLAGS, f"-DXS_ACC_WARPS={w}", f"-DXS_ACC_U={u}", "-I", b.INCLUDE, "-shared",
+               "-o", so, *b.sources()]
+        subprocess.check_call(cmd)
+        print(so)
+
+
+def run_one(so: str, cfg: str, steps: int):
+    code = f"""
+import os, sys, json, statistics
+sys.path.insert(0, {ROOT!r})
+os.environ['XSUM_LIBRARY'] = {so!r}
+import torch, synth, paper_1605_05436_b200 as xsum
+x = synth.device_generate({cfg!r})
+acc = xsum.Accumulator()
+for _ in range(5): acc.sum(x)
+torch.cuda.synchronize()
+ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range({steps})]
+for a, b in ev:
+    a.record(); acc.sum(x); b.record()
+torch.cuda.synchronize()
+ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=8*x.numel()/ms/1e6, bits=hex(r.bits))))
+"""
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    print(out.stdout.strip() or out.stderr[-2000:], flush=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        cfgs = sys.argv[2:] or ["c2"]
+        for cfg in cfgs:
+            for w, u in VARIANTS:
+                run_one(os.path.join(OUT, f"libxsum_w{w}_u{u}.so"), cfg, 50)

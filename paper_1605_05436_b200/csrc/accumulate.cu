@@ -71,7 +71,7 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     const uint64_t ntiles = nvec / TV;
     const uint64_t G = gridDim.x;
 
-    const uint32_t one = p.one;
+    const uint32_t one = p.one, mone = p.mone;
     uint32_t nspec = 0;                 // NaN/Inf patterns summed unchecked in this window
     int since = 0;
     uint64_t wstart = blockIdx.x, tlast = 0;
@@ -88,21 +88,24 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     auto do_tile = [&](const uint4 (&buf)[U], uint64_t tt) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            Chunks a = decompose(buf[u].x, buf[u].y, one);
-            nspec += a.spec;
+            Chunks a = decompose(buf[u].x, buf[u].y, one, mone);
+            nspec = spec_fold(nspec, a);
             column_add(col, a, one);
-            Chunks b = decompose(buf[u].z, buf[u].w, one);
-            nspec += b.spec;
+            Chunks b = decompose(buf[u].z, buf[u].w, one, mone);
+            nspec = spec_fold(nspec, b);
             column_add(col, b, one);
         }
         any_tile = true;
         tlast = tt;
         if (++since == C::FLUSH_TILES) {
-            if (__any_sync(FULL, nspec != 0)) {
-                if (nspec) rescan_window<U, T>(col, body, wstart, tt, G, TV, tid, flags, one);
+            regularize_column(col);
+            if (__any_sync(FULL, spec_hit(nspec))) {       // rare: cancel NaN/Inf patterns
+                if (spec_hit(nspec)) {
+                    rescan_window<U, T>(col, body, wstart, tt, G, TV, tid, flags, one);
+                    regularize_column(col);
+                }
             }
             nspec = 0;
-            regularize_column(col);
             since = 0;
             wstart = tt + G;
             any_tile = false;
@@ -149,10 +152,13 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
             column_add_checked(col, q.x, q.y, flags, one);
         }
     }
-    if (__any_sync(FULL, nspec != 0)) {
-        if (nspec && any_tile) rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags, one);
-    }
     regularize_column(col);
+    if (__any_sync(FULL, spec_hit(nspec))) {
+        if (spec_hit(nspec) && any_tile) {
+            rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags, one);
+            regularize_column(col);
+        }
+    }
     __syncwarp();
 
     // warp: sum the 32 lane columns; lane l takes digits l and l+32 (rotated start: the

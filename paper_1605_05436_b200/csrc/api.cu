@@ -53,6 +53,7 @@ xs::AccParams acc_params(xsum_ctx* h, int overwrite, xsum_result* res, uint64_t*
     p.res = res;
     p.canon = canon;
     p.one = 1;
+    p.mone = 0xFFFFFFFFu;
     return p;
 }
 

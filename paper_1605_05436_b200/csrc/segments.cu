@@ -28,9 +28,10 @@ __device__ __forceinline__ void seg_rescan(int64_t* col, const uint4* body, uint
     }
 }
 
-__global__ void __launch_bounds__(SEG_WARPS * 32)
+__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
 k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
-           double* __restrict__ out, uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one) {
+           double* __restrict__ out, uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one,
+           uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -66,21 +67,24 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
             }
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) {
-                Chunks a = decompose(cur[u].x, cur[u].y, one);
-                nspec += a.spec;
+                Chunks a = decompose(cur[u].x, cur[u].y, one, mone);
+                nspec = spec_fold(nspec, a);
                 column_add(col, a, one);
-                Chunks b = decompose(cur[u].z, cur[u].w, one);
-                nspec += b.spec;
+                Chunks b = decompose(cur[u].z, cur[u].w, one, mone);
+                nspec = spec_fold(nspec, b);
                 column_add(col, b, one);
             }
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) cur[u] = nxt[u];
             if (++since == SEG_FLUSH_ITERS) {
-                if (__any_sync(FULL, nspec != 0)) {
-                    if (nspec) seg_rescan(col, body, wstart, it, lane, flags, one);
+                regularize_column(col);
+                if (__any_sync(FULL, spec_hit(nspec))) {
+                    if (spec_hit(nspec)) {
+                        seg_rescan(col, body, wstart, it, lane, flags, one);
+                        regularize_column(col);
+                    }
                 }
                 nspec = 0;
-                regularize_column(col);
                 since = 0;
                 wstart = it + 1;
             }
@@ -99,10 +103,13 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
             uint2 q = ldg_one(xs + head + 2 * nvec);
             column_add_checked(col, q.x, q.y, flags, one);
         }
-        if (__any_sync(FULL, nspec != 0)) {
-            if (nspec && since) seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
-        }
         regularize_column(col);
+        if (__any_sync(FULL, spec_hit(nspec))) {
+            if (spec_hit(nspec) && since) {
+                seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
+                regularize_column(col);
+            }
+        }
         __syncwarp();
 
         // combine the 32 lane columns: |sum| <= 32 (2^51 + 2^11) < 2^57
@@ -137,7 +144,7 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
     uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (86 KB smem each)
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-    k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags, 1u);
+    k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags, 1u, 0xFFFFFFFFu);
     note_launch();
     return cudaGetLastError();
 }

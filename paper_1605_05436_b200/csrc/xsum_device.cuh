@@ -20,13 +20,13 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // Summands a lane column may take between two regularizations. Each summand adds one
 // chunk (|chunk| <= 2^52) to at most one position of each digit. A window holds at most
-// FLUSH_ELEMS hot-loop summands, as many compensating adds for NaN/Inf patterns (see
-// column_fix_special) and <= 10 head/tail/leftover summands, on top of a regularized
-// residue |Y| <= 2^51 + 2^11:  2^51 + 2^11 + (2*1016 + 10) * 2^52 + 2^51 < 2^63, so
-// neither the adds nor the balanced carry (y + R/2) can overflow int64 (the bound is
-// re-derived in tests/test_host_logic.py). The paper's "reserved extra bit"
-// becomes 11 bits of headroom per int64 digit here.
-constexpr int FLUSH_ELEMS = 1016;
+// FLUSH_ELEMS hot-loop summands plus <= 10 head/tail/leftover summands on top of a
+// regularized residue |Y| <= 2^51 + 2^11:  2^51 + 2^11 + (2032 + 10) * 2^52 + 2^51 < 2^63,
+// so neither the adds nor the balanced carry (y + R/2) can overflow int64. NaN/Inf bit
+// patterns summed unchecked are cancelled after the window's regularization, in a fresh
+// window of the same bound (re-derived in tests/test_host_logic.py). The paper's "reserved
+// extra bit" becomes 11 bits of headroom per int64 digit here.
+constexpr int FLUSH_ELEMS = 2032;
 
 // ---------------------------------------------------------------------------------
 // Step 2 of the PRAM algorithm: split x into O(1) components whose
@@ -72,8 +72,85 @@ constexpr uint32_t K52 = 20165u << 12;
 // mulhi(e, KSPEC) = 1 iff e == 2047 for e in [0, 2047]  (2047*KSPEC >= 2^32 > 2046*KSPEC).
 constexpr uint32_t KSPEC = 2098177u;
 
-__device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t one) {
+#ifndef XS_DECODE
+#define XS_DECODE 3   // decode variant (3 = product); 0-2, 4: alternatives kept for tools/variants.py
+#endif
+__device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t one, uint32_t mone = 0xFFFFFFFFu) {
     Chunks c;
+    (void)mone;
+#if XS_DECODE == 0
+    (void)one;
+    uint32_t e = (hi >> 20) & 0x7FFu;
+    uint32_t ep = max(e, 1u);
+    uint32_t k = ep - 1u;
+    uint32_t i = k / 52u;
+    uint32_t o = k - 52u * i;
+    uint32_t imp = e + 1u - ep;                       // hidden bit: 1 unless subnormal/zero
+    uint32_t mh = (hi & 0xFFFFFu) | (imp << 20);
+    uint64_t M = ((uint64_t)mh << 32) | lo;
+    int64_t s = (int64_t)((int32_t)hi >> 31);         // 0 or -1
+    int64_t sM = (int64_t)(M ^ (uint64_t)s) - s;      // +-M
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> (52u - o);
+    c.i = i;
+    c.spec = (e == 0x7FFu);
+#elif XS_DECODE == 3
+    // per summand: ~14 ALU-pipe ops and ~12 FMA-pipe issue slots (IMAD = 1, IMAD.HI = 2;
+    // measured sm_100 rates in tools/op_bench.cu), no IMAD.WIDE (1/8 rate).
+    uint32_t h = hi & 0x7FFFFFFFu;                        // |x| high word
+    uint32_t e = h >> 20;                                 // biased exponent
+    uint32_t ep = max(e, 1u);
+    uint32_t k = mad_u32(ep, one, 0xFFFFFFFFu);           // ep - 1 (IMAD)
+    uint32_t i = mulhi_u32(k, K52);                       // k / 52 (IMAD.HI)
+    uint32_t o = mad_u32(i, (uint32_t)-52, k);            // k mod 52 (IMAD)
+    uint32_t r = mad_u32(o, mone, 52u);                   // 52 - o (IMAD)
+    uint32_t mh = mad_u32(k, 0xFFF00000u, h);             // hidden bit | top 20 fraction bits (IMAD)
+    int32_t S = (int32_t)hi >> 31;                        // sign mask
+    uint64_t onec = ((uint64_t)(mh ^ (uint32_t)S) << 32) | (lo ^ (uint32_t)S);
+    int64_t sM = (int64_t)onec - (int64_t)S;              // +-M (IADD3 + IMAD.X)
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> r;
+    c.i = i;
+    c.spec = k;                                           // k == 2046 only for NaN/Inf (max-tracked)
+#elif XS_DECODE == 4
+    // dec3 with the sign mask from IMAD.HI and the +1 of the two's complement carried by
+    // IMAD.X (madc): ~14 ALU-pipe ops, ~13 FMA-pipe slots per summand.
+    uint32_t h = hi & 0x7FFFFFFFu;
+    uint32_t e = h >> 20;
+    uint32_t ep = max(e, 1u);
+    uint32_t k = mad_u32(ep, one, 0xFFFFFFFFu);
+    uint32_t i = mulhi_u32(k, K52);
+    uint32_t o = mad_u32(i, (uint32_t)-52, k);
+    uint32_t r = mad_u32(o, mone, 52u);
+    uint32_t mh = mad_u32(k, 0xFFF00000u, h);
+    int32_t S = mulhi_s32((int32_t)hi, 2);                // sign mask (IMAD.HI)
+    uint32_t sbit = mad_u32((uint32_t)S, mone, 0u);       // -S (IMAD)
+    uint32_t slo, shi;
+    asm("add.cc.u32 %0, %2, %3;\n\tmadc.lo.u32 %1, %4, %5, 0;"
+        : "=r"(slo), "=r"(shi) : "r"(lo ^ (uint32_t)S), "r"(sbit), "r"(mh ^ (uint32_t)S), "r"(one));
+    int64_t sM = (int64_t)(((uint64_t)shi << 32) | slo);
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> r;
+    c.i = i;
+    c.spec = k;
+#elif XS_DECODE == 2
+    uint32_t e = (hi >> 20) & 0x7FFu;
+    uint32_t ep = max(e, 1u);
+    uint32_t k = ep - 1u;
+    uint32_t i = mulhi_u32(k, K52);                       // k / 52 (IMAD.HI)
+    uint32_t o = mad_u32(i, (uint32_t)-52, k);            // k mod 52 (IMAD)
+    uint32_t mhs = mad_u32(k, 0xFFF00000u, hi);           // sign | hidden | m_hi (IMAD)
+    int32_t S = (int32_t)hi >> 31;
+    uint32_t S31 = (uint32_t)S >> 1;
+    uint64_t onec = ((uint64_t)(mhs ^ S31) << 32) | (lo ^ (uint32_t)S);
+    int64_t sM = (int64_t)onec - (int64_t)S;
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> (52u - o);
+    c.i = i;
+    c.spec = mulhi_u32(e, KSPEC);
+    (void)one;
+#else
+
     uint32_t e = (hi >> 20) & 0x7FFu;                     // biased exponent
     uint32_t ep = max(e, 1u);
     uint32_t k = mad_u32(ep, one, 0xFFFFFFFFu);           // ep - 1: LSB position of M
@@ -91,17 +168,38 @@ __device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t o
     c.c1 = sM >> (52u - o);                               // arithmetic: floor division
     c.i = i;
     c.spec = mulhi_u32(e, KSPEC);
+#endif
     return c;
 }
+
+// Tracking of NaN/Inf bit patterns summed unchecked in the hot loop: a per-lane fold that
+// is cheap per summand and tested once per window.
+#if XS_DECODE == 3 || XS_DECODE == 4
+__device__ __forceinline__ uint32_t spec_fold(uint32_t acc, const Chunks& c) { return max(acc, c.spec); }
+__device__ __forceinline__ bool spec_hit(uint32_t acc) { return acc >= 2046u; }
+#else
+__device__ __forceinline__ uint32_t spec_fold(uint32_t acc, const Chunks& c) { return acc + c.spec; }
+__device__ __forceinline__ bool spec_hit(uint32_t acc) { return acc != 0u; }
+#endif
 
 // Add one summand's chunks into a lane column (digit j at col[j*32]): the "localized"
 // add of PAPER.md:1043-1047 with carries deferred (PAPER.md:669-673 lazy carries).
 // (plain IADD3/IMAD.X adds: the LDS -> add -> STS chain is latency-critical)
+#ifndef XS_EXPERIMENT
+#define XS_EXPERIMENT 0   // development-only diagnostic builds (tools/variants.py); 0 in the product
+#endif
 __device__ __forceinline__ void column_add(int64_t* col, const Chunks& c, uint32_t one) {
     (void)one;
+#if XS_EXPERIMENT == 1      // diagnostic: no shared-memory traffic (decode + loads only; WRONG sums)
+    col[0] ^= (c.c0 ^ c.c1) & (int64_t)(c.i == 1000u);
+#elif XS_EXPERIMENT == 2    // diagnostic: RMW always on digits 0/1 (no data-dependent addressing)
+    col[0] += c.c0;
+    col[32] += c.c1 + (int64_t)c.i;
+#else
     int64_t* p = col + c.i * 32u;
     p[0] += c.c0;
     p[32] += c.c1;
+#endif
 }
 
 // Flags of a NaN/Inf bit pattern (only called when e == 0x7FF).
@@ -114,7 +212,7 @@ __device__ __forceinline__ uint32_t special_flags(uint32_t lo, uint32_t hi) {
 __device__ __forceinline__ void column_add_checked(int64_t* col, uint32_t lo, uint32_t hi, uint32_t& flags,
                                                    uint32_t one) {
     Chunks c = decompose(lo, hi, one);
-    if (c.spec) { flags |= special_flags(lo, hi); return; }
+    if (spec_hit(c.spec)) { flags |= special_flags(lo, hi); return; }
     column_add(col, c, one);
 }
 

@@ -18,7 +18,8 @@ struct AccParams {
     int overwrite;             // 1: state := sum (fused reset), 0: state += sum
     xsum_result* res;          // non-null: fused finalize
     uint64_t* canon;           // optional canonical image for the fused finalize
-    uint32_t one;              // = 1 (opaque to the compiler: keeps integer adds on the FMA pipe)
+    uint32_t one;              // = 1  } opaque to the compiler: keeps selected integer ops as IMADs
+    uint32_t mone;             // = -1 } on the FMA pipe instead of ALU-pipe IADD3s
 };
 
 // scratch layout: [0,256) counter; [256, 256 + 8*D*MAXB) partials; then MAXB u32 flags

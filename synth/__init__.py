@@ -29,10 +29,10 @@ def build(cuda: bool = True) -> None:
     if _stale(_HOST_SO, [src]):
         subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-pthread", src, "-o", _HOST_SO])
     if cuda:
-        cu = os.path.join(_HERE, "csrc", "gen.cu")
-        if _stale(_CUDA_SO, [cu]):
+        cus = [os.path.join(_HERE, "csrc", f) for f in ("gen.cu", "probe.cu")]
+        if _stale(_CUDA_SO, cus):
             subprocess.check_call(["nvcc", *NVCC_ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
-                                   "-shared", cu, "-o", _CUDA_SO])
+                                   "-shared", *cus, "-o", _CUDA_SO])
 
 
 def _stale(target: str, sources: list[str]) -> bool:
@@ -72,6 +72,8 @@ def cuda_lib():
         lib.synth_gpu_uniform.argtypes = [p, u64, u64, u64, u64, i32, i32, p]
         lib.synth_gpu_cancel_unpermuted.argtypes = [p, u64, u64, u64, u64, i32, i32, i32, i32, p]
         lib.synth_gpu_keys_signed.argtypes = [p, u64, u64, u64, u64, p]
+        lib.synth_probe_read.argtypes = [p, u64, p, i32, i32, i32, p]
+        lib.synth_probe_read.restype = ctypes.c_int
         for f in (lib.synth_gpu_uniform, lib.synth_gpu_cancel_unpermuted, lib.synth_gpu_keys_signed):
             f.restype = ctypes.c_int
         _cuda = lib
@@ -155,3 +157,27 @@ def device_generate(name: str, start: int = 0, count: int | None = None, device=
         if rc:
             raise RuntimeError(f"synth_gpu_uniform failed: {rc}")
     return out
+
+
+def probe_read_gbs(x, variant: int = 0, blocks: int = 148, threads: int = 512, reps: int = 20) -> float:
+    """Read bandwidth (GB/s, median of reps, CUDA events) of probe `variant` over tensor x."""
+    import statistics
+
+    import torch
+    out = torch.empty(blocks * threads, dtype=torch.int32, device=x.device)
+    st = torch.cuda.current_stream(x.device)
+    lib = cuda_lib()
+    nbytes = x.numel() * x.element_size()
+    for _ in range(3):
+        lib.synth_probe_read(x.data_ptr(), nbytes, out.data_ptr(), variant, blocks, threads, st.cuda_stream)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        rc = lib.synth_probe_read(x.data_ptr(), nbytes, out.data_ptr(), variant, blocks, threads, st.cuda_stream)
+        b.record(st)
+        b.synchronize()
+        if rc:
+            raise RuntimeError(f"probe {variant} failed: {rc}")
+        ts.append(a.elapsed_time(b))
+    return nbytes / statistics.median(ts) / 1e6

@@ -122,12 +122,15 @@ def test_digit_index_division_and_chunk_split_cover_binary64():
 
 
 def test_flush_headroom_bound():
-    """FLUSH_ELEMS = 1016: residue + (2F + 10) chunk adds + the balanced-carry offset fit int64."""
+    """FLUSH_ELEMS: residue + (F + 10 stragglers) chunk adds + the balanced-carry offset fit
+    int64; the NaN/Inf compensation window (<= F adds after a regularization) likewise."""
     src = open(os.path.join(ROOT, "paper_1605_05436_b200", "csrc", "xsum_device.cuh")).read()
     F = int(re.search(r"FLUSH_ELEMS = (\d+)", src).group(1))
+    assert F % 8 == 0                                    # whole tiles (8 summands per lane)
     residue = 2 ** 51 + 2 ** 11
-    worst = residue + (2 * F + 10) * 2 ** 52
+    worst = residue + (F + 10) * 2 ** 52
     assert worst + 2 ** 51 < 2 ** 63
+    assert residue + F * 2 ** 52 + 2 ** 51 < 2 ** 63   # compensation window
     # balanced carry magnitude after a window, and the block/grid raw sums
     assert (worst + 2 ** 51) >> 52 <= 2 ** 11
     assert 512 * (2 ** 51 + 2 ** 11) < 2 ** 63          # block sum of 512 regularized lane columns
@@ -253,6 +256,8 @@ def test_decode_magic_constants():
     for k in range(2048):
         assert (k * k52) >> 32 == k // 52
         assert (k * kspec) >> 32 == (1 if k == 2047 else 0)
+    # dec3 tracks NaN/Inf by max(k): k = max(e,1)-1 reaches 2046 only for e = 2047
+    assert max(max(e, 1) - 1 for e in range(2047)) == 2045 and max(2047, 1) - 1 == 2046
     # hi - k*2^20 keeps the sign bit and sets the hidden bit exactly when e != 0
     for e in (0, 1, 2, 1023, 2046, 2047):
         for s in (0, 1):

@@ -1,8 +1,8 @@
 """Build and time compile-time variants of the accumulate kernel (development tool).
 
     python tools/variants.py build            # here (nvcc cross-compiles)
-    python tools/variants.py run [--n N]      # on the GPU box: one JSON line per variant
-"""
+    python tools/variants.py run [cfg ...]    # on the GPU box: one JSON line per variant
+Variants named exp* are diagnostic builds that compute WRONG sums (timing only)."""
 from __future__ import annotations
 
 import json
@@ -13,16 +13,24 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
-VARIANTS = [(16, 4), (16, 2), (12, 4), (14, 4), (16, 3)]
+# name -> extra nvcc defines
+VARIANTS = {
+    "dec4": ["-DXS_DECODE=4"],
+    "dec3": ["-DXS_DECODE=3"],
+    "dec2": ["-DXS_DECODE=2"],
+    "dec0": ["-DXS_DECODE=0"],
+    "dec4_nosmem": ["-DXS_DECODE=4", "-DXS_EXPERIMENT=1"],
+}
 
 
-def build():
+def build(names=None):
     from paper_1605_05436_b200 import _build as b
     os.makedirs(OUT, exist_ok=True)
-    for w, u in VARIANTS:
-        so = os.path.join(OUT, f"libxsum_w{w}_u{u}.so")
-        cmd = ["nvcc", *b.ARCH, *b.FLAGS, f"-DXS_ACC_WARPS={w}", f"-DXS_ACC_U={u}", "-I", b.INCLUDE, "-shared",
-               "-o", so, *b.sources()]
+    for name, defs in VARIANTS.items():
+        if names and name not in names:
+            continue
+        so = os.path.join(OUT, f"libxsum_{name}.so")
+        cmd = ["nvcc", *b.ARCH, *b.FLAGS, *defs, "-I", b.INCLUDE, "-shared", "-o", so, *b.sources()]
         subprocess.check_call(cmd)
         print(so)
 
@@ -51,9 +59,11 @@ print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.nu
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
-        build()
+        build(sys.argv[2:])
     else:
         cfgs = sys.argv[2:] or ["c2"]
         for cfg in cfgs:
-            for w, u in VARIANTS:
-                run_one(os.path.join(OUT, f"libxsum_w{w}_u{u}.so"), cfg, 50)
+            for name in VARIANTS:
+                so = os.path.join(OUT, f"libxsum_{name}.so")
+                if os.path.exists(so):
+                    run_one(so, cfg, 50)

@@ -28,6 +28,32 @@ __device__ __forceinline__ void seg_rescan(int64_t* col, const uint4* body, uint
     }
 }
 
+// Per-segment epilogue (one warp): combine the 32 lane columns (|sum| <= 32 (2^51 + 2^11)
+// < 2^57), regularize, canonicalize and round, write
+// the outputs, and zero the lane column for the next segment.
+__device__ __forceinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
+                                                 uint64_t len, uint64_t s, double* out, uint64_t* canon,
+                                                 uint32_t* oflags, int lane) {
+    __syncwarp();
+    int64_t a0 = 0, a1 = 0;
+#pragma unroll 8
+    for (int c = 0; c < 32; ++c) {
+        int cc = (lane + c) & 31;
+        a0 += wb[lane * 32 + cc];
+        if (lane + 32 < D) a1 += wb[(lane + 32) * 32 + cc];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    regularize_warp(a0, a1, lane);
+    flags = __reduce_or_sync(FULL, flags);
+    xsum_result r = finalize_warp(a0, a1, flags, len, canon ? canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
+    if (lane == 0) {
+        out[s] = r.value;
+        if (oflags) oflags[s] = r.flags;
+    }
+}
+
 __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
 k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
            double* __restrict__ out, uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one,
@@ -112,24 +138,106 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         }
         __syncwarp();
 
-        // combine the 32 lane columns: |sum| <= 32 (2^51 + 2^11) < 2^57
-        const int64_t* wb = win + warp * (D * 32);
-        int64_t a0 = 0, a1 = 0;
-#pragma unroll 8
-        for (int c = 0; c < 32; ++c) {
-            int cc = (lane + c) & 31;
-            a0 += wb[lane * 32 + cc];
-            if (lane + 32 < D) a1 += wb[(lane + 32) * 32 + cc];
+        segment_epilogue(col, win + warp * (D * 32), su[warp], flags, len, s, out, canon, oflags, lane);
+    }
+}
+
+
+// Fast path for equal segments whose starts are 16-B aligned and whose length is a multiple
+// of one warp tile (256 doubles), e.g. config 5: a warp's tiles form one continuous stream
+// across its segments, prefetched three tiles ahead with rotating register buffers, so the
+// per-segment epilogue runs while the next segment's first loads are already in flight.
+constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
+
+__device__ __forceinline__ void seg_rescan_uniform(int64_t* col, const uint4* seg, uint32_t t0, uint32_t t1,
+                                                   int lane, uint32_t& flags, uint32_t one) {
+    for (uint32_t t = t0; t <= t1; ++t) {
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) {
+            uint4 v = ldg_stream(seg + (uint64_t)t * (32 * SEG_U) + u * 32 + lane);
+            column_fix_special(col, v.x, v.y, flags, one);
+            column_fix_special(col, v.z, v.w, flags, one);
         }
-        __syncwarp();
-        regularize_warp(a0, a1, lane);
-        flags = __reduce_or_sync(FULL, flags);
-        xsum_result r = finalize_warp(a0, a1, flags, len, canon ? canon + s * XSUM_CANON_LIMBS : nullptr,
-                                      su[warp], lane);
-        if (lane == 0) {
-            out[s] = r.value;
-            if (oflags) oflags[s] = r.flags;
+    }
+}
+
+__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
+k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, double* __restrict__ out,
+                   uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t su[SEG_WARPS][64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t nw = (uint64_t)gridDim.x * SEG_WARPS;
+    const uint64_t gw = (uint64_t)blockIdx.x * SEG_WARPS + warp;
+    if (gw >= nseg) return;                                    // warp-uniform
+    const uint32_t TPS = (uint32_t)(seg_len / SEG_TILE);       // tiles per segment
+    const uint64_t seg_vecs = seg_len / 2;
+    const uint4* xv = reinterpret_cast<const uint4*>(x);
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+
+    uint64_t ls = gw;            // load cursor: segment, tile
+    uint32_t lt = 0;
+    auto load_next = [&](uint4 (&buf)[SEG_U]) {
+        if (ls < nseg) {
+            const uint4* p = xv + ls * seg_vecs + (uint64_t)lt * (32 * SEG_U) + lane;
+#pragma unroll
+            for (int u = 0; u < SEG_U; ++u) buf[u] = ldg_stream(p + u * 32);
+            if (++lt == TPS) { lt = 0; ls += nw; }
         }
+    };
+    uint64_t ps = gw;            // processing cursor: segment, tile
+    uint32_t pt = 0, wstart = 0, flags = 0, nspec = 0;
+    int since = 0;
+    auto close_window = [&](uint32_t tlast) {
+        regularize_column(col);
+        if (__any_sync(FULL, spec_hit(nspec))) {
+            if (spec_hit(nspec)) {
+                seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, tlast, lane, flags, one);
+                regularize_column(col);
+            }
+        }
+        nspec = 0;
+        since = 0;
+        wstart = tlast + 1;
+    };
+    auto do_tile = [&](const uint4 (&buf)[SEG_U]) {
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) {
+            Chunks a = decompose(buf[u].x, buf[u].y, one, mone);
+            nspec = spec_fold(nspec, a);
+            column_add(col, a, one);
+            Chunks b = decompose(buf[u].z, buf[u].w, one, mone);
+            nspec = spec_fold(nspec, b);
+            column_add(col, b, one);
+        }
+        ++since;
+        if (pt + 1 == TPS) {                                   // segment complete
+            close_window(pt);
+            segment_epilogue(col, win + warp * (D * 32), su[warp], flags, seg_len, ps, out, canon, oflags, lane);
+            flags = 0;
+            wstart = 0;
+            pt = 0;
+            ps += nw;
+        } else {
+            if (since == SEG_FLUSH_ITERS) close_window(pt);
+            ++pt;
+        }
+    };
+    uint4 A[SEG_U], B[SEG_U], Cb[SEG_U];
+    load_next(A);
+    load_next(B);
+    load_next(Cb);
+    while (ps < nseg) {
+        do_tile(A);
+        load_next(A);
+        if (ps >= nseg) break;
+        do_tile(B);
+        load_next(B);
+        if (ps >= nseg) break;
+        do_tile(Cb);
+        load_next(Cb);
     }
 }
 
@@ -138,13 +246,20 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SEG_SMEM);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_segments_uniform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SEG_SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
-    uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (86 KB smem each)
+    uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (84 KiB smem each)
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-    k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags, 1u, 0xFFFFFFFFu);
+    const bool uniform = !offsets && seg_len >= SEG_TILE && seg_len % SEG_TILE == 0 &&
+                         ((uintptr_t)x & 15) == 0 && seg_len / SEG_TILE < (1u << 31);
+    if (uniform)
+        k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, out, canon, flags, 1u, 0xFFFFFFFFu);
+    else
+        k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags, 1u, 0xFFFFFFFFu);
     note_launch();
     return cudaGetLastError();
 }

@@ -280,12 +280,20 @@ def test_launch_counter_counts_kernels(xs):
 # segmented sums (config 5 and ragged)
 # ---------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("seg_len", [1, 2, 3, 31, 33, 127, 4096, 5000, 1016 * 64 + 3])
-def test_segments_ragged_lengths(xs, seg_len):
+@pytest.mark.parametrize("seg_len,off", [(1, 1), (2, 1), (3, 0), (31, 1), (33, 0), (127, 1), (4096, 1), (5000, 0),
+                                         (1016 * 64 + 3, 1), (256, 0), (512, 0), (4096, 0), (256 * 300, 0)])
+def test_segments_ragged_lengths(xs, seg_len, off):
+    """Equal segments: misaligned / ragged lengths take the general kernel, aligned multiples
+    of 256 the streaming fast path (incl. a segment longer than one flush window). NaN/Inf
+    patterns planted in the first and the last segment."""
     nseg = max(1, min(300, 2_000_000 // seg_len))
     x = synth.gen.generate("c5", 3, nseg * seg_len)
-    x.view(np.uint64)[7 % x.size] = 0x7FF8000000000000        # one NaN in segment 0
-    vals, canon, flags = xs.sum_segments(to_dev(x, 1), seg_len, canon=True, flags=True)
+    xb = x.view(np.uint64)
+    xb[7 % x.size] = 0x7FF8000000000000                        # NaN in segment 0
+    xb[x.size - 1 - (5 % seg_len)] = 0xFFF0000000000000        # -Inf in the last segment
+    if seg_len > 70000:
+        xb[seg_len // 2 + 3] = 0x7FF0000000000000              # +Inf in a later flush window
+    vals, canon, flags = xs.sum_segments(to_dev(x, off), seg_len, canon=True, flags=True)
     vals = vals.cpu().numpy().view(np.uint64)
     canon = canon.cpu().numpy().view(np.uint64)
     flags = flags.cpu().numpy()

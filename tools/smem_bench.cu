@@ -33,10 +33,22 @@ __global__ void __launch_bounds__(512, 1) k_smem(uint64_t* out, int iters, uint3
             } else if (MODE == 2) {
                 asm volatile("red.shared.add.u64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(p)), "l"(c0));
                 asm volatile("red.shared.add.u64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(p + 32)), "l"(c1));
-            } else {
+            } else if (MODE == 3) {
                 uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
                 asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a), "r"((uint32_t)c0));
                 asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a + 256), "r"((uint32_t)c1));
+            } else if (MODE == 4) {          // stores only, random digit per lane
+                p[0] = c0;
+                p[32] = c1;
+            } else if (MODE == 5) {          // loads only, random digit per lane
+                acc += p[0] ^ p[32];
+            } else if (MODE == 6) {          // RMW, all lanes on the same digit
+                unsigned long long* q = col + ((x >> 16) & 0) * 32 + (it & 7) * 32;
+                q[0] += c0;
+                q[32] += c1;
+            } else if (MODE == 7) {          // RMW, lanes 16-31 shifted by one digit row
+                p[0] += c0;
+                p[32] += c1;
             }
         }
     }
@@ -57,6 +69,12 @@ extern "C" int smem_bench(int mode, uint64_t* out, int blocks, int iters, void* 
                 k_smem<2><<<blocks, 512, smem, s>>>(out, iters, 1u); break;
         case 3: cudaFuncSetAttribute(k_smem<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 k_smem<3><<<blocks, 512, smem, s>>>(out, iters, 1u); break;
+        case 4: cudaFuncSetAttribute(k_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                k_smem<4><<<blocks, 512, smem, s>>>(out, iters, 1u); break;
+        case 5: cudaFuncSetAttribute(k_smem<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                k_smem<5><<<blocks, 512, smem, s>>>(out, iters, 1u); break;
+        case 6: cudaFuncSetAttribute(k_smem<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                k_smem<6><<<blocks, 512, smem, s>>>(out, iters, 1u); break;
         default: return 1;
     }
     return (int)cudaGetLastError();

@@ -13,8 +13,12 @@ pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(0)
 out = torch.empty(148 * 512, dtype=torch.int64, device="cuda")
 iters = 2000
-for mode, name in [(0, "LDS+add+STS (64-bit)"), (1, "atomicAdd shared u64"), (2, "red.shared.add.u64"),
-                   (3, "red.shared.add.u32")]:
+import sys as _sys
+MODES = [(0, "LDS+add+STS (64-bit)"), (1, "atomicAdd shared u64"), (2, "red.shared.add.u64"),
+         (3, "red.shared.add.u32"), (4, "STS.64 only (random digit)"), (5, "LDS.64 only (random digit)"),
+         (6, "RMW same digit all lanes")]
+sel = [int(a) for a in _sys.argv[1:]]
+for mode, name in [m for m in MODES if not sel or m[0] in sel]:
     st = torch.cuda.current_stream()
     for _ in range(2):
         L.smem_bench(mode, out.data_ptr(), 148, iters, st.cuda_stream)

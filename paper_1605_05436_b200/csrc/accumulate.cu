@@ -31,7 +31,7 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 }
 
 template <int U, int T>
-__device__ __forceinline__ void rescan_window(int64_t* col, const uint4* body, uint64_t t0, uint64_t t1,
+__device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint64_t t0, uint64_t t1,
                                               uint64_t G, uint64_t TV, int tid, uint32_t& flags, uint32_t one) {
     // Rare path: this lane summed a NaN/Inf bit pattern as if finite somewhere in tiles
     // [t0, t1] (step G). Re-read its elements and cancel those chunks exactly.
@@ -152,26 +152,19 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
             column_add_checked(col, q.x, q.y, flags, one);
         }
     }
-    regularize_column(col);
     if (__any_sync(FULL, spec_hit(nspec))) {
         if (spec_hit(nspec) && any_tile) {
-            rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags, one);
             regularize_column(col);
+            rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags, one);
         }
     }
     __syncwarp();
 
-    // warp: sum the 32 lane columns; lane l takes digits l and l+32 (rotated start: the
-    // 32 lanes read 32 distinct columns per step, 2 wavefronts per 64-bit access).
+    // warp: sum the 32 raw lane columns into regularized digits (lane l holds digits l and
+    // l+32; rotated reads keep the 32 lanes on 32 distinct columns).
     {
-        const int64_t* wb = win + warp * (D * 32);
-        int64_t s0 = 0, s1 = 0;
-#pragma unroll 8
-        for (int c = 0; c < 32; ++c) {
-            int cc = (lane + c) & 31;
-            s0 += wb[lane * 32 + cc];
-            if (lane + 32 < D) s1 += wb[(lane + 32) * 32 + cc];
-        }
+        int64_t s0, s1;
+        combine_raw_columns(win + warp * (D * 32), s0, s1, lane);
         wsum[warp][lane] = s0;
         if (lane + 32 < D) wsum[warp][lane + 32] = s1;
         uint32_t f = __reduce_or_sync(FULL, flags);
@@ -179,7 +172,7 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     }
     __syncthreads();
 
-    // block: sum the warp partials (|.| <= WARPS*32*(2^51+2^11) < 2^61), regularize, publish.
+    // block: sum the warp partials (|.| <= WARPS*(2^51+2^16) < 2^56), regularize, publish.
     if (warp == 0) {
         int64_t a0 = 0, a1 = 0;
 #pragma unroll

@@ -16,7 +16,7 @@ constexpr int SEG_U = 4;
 constexpr int SEG_FLUSH_ITERS = FLUSH_ELEMS / (2 * SEG_U);
 constexpr size_t SEG_SMEM = (size_t)SEG_WARPS * D * 32 * sizeof(int64_t);
 
-__device__ __forceinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_t it0, uint64_t it1, int lane,
+__device__ __noinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_t it0, uint64_t it1, int lane,
                                            uint32_t& flags, uint32_t one) {
     for (uint64_t it = it0; it <= it1; ++it) {
 #pragma unroll
@@ -31,21 +31,15 @@ __device__ __forceinline__ void seg_rescan(int64_t* col, const uint4* body, uint
 // Per-segment epilogue (one warp): combine the 32 lane columns (|sum| <= 32 (2^51 + 2^11)
 // < 2^57), regularize, canonicalize and round, write
 // the outputs, and zero the lane column for the next segment.
-__device__ __forceinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
-                                                 uint64_t len, uint64_t s, double* out, uint64_t* canon,
-                                                 uint32_t* oflags, int lane) {
+__device__ __noinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
+                                              uint64_t len, uint64_t s, double* out, uint64_t* canon,
+                                              uint32_t* oflags, int lane) {
     __syncwarp();
-    int64_t a0 = 0, a1 = 0;
-#pragma unroll 8
-    for (int c = 0; c < 32; ++c) {
-        int cc = (lane + c) & 31;
-        a0 += wb[lane * 32 + cc];
-        if (lane + 32 < D) a1 += wb[(lane + 32) * 32 + cc];
-    }
+    int64_t a0, a1;
+    combine_raw_columns(wb, a0, a1, lane);           // lane columns need no regularization
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
-    regularize_warp(a0, a1, lane);
     flags = __reduce_or_sync(FULL, flags);
     xsum_result r = finalize_warp(a0, a1, flags, len, canon ? canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
     if (lane == 0) {
@@ -129,15 +123,12 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
             uint2 q = ldg_one(xs + head + 2 * nvec);
             column_add_checked(col, q.x, q.y, flags, one);
         }
-        regularize_column(col);
-        if (__any_sync(FULL, spec_hit(nspec))) {
+        if (__any_sync(FULL, spec_hit(nspec))) {        // raw columns go to the epilogue
             if (spec_hit(nspec) && since) {
-                seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
                 regularize_column(col);
+                seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
             }
         }
-        __syncwarp();
-
         segment_epilogue(col, win + warp * (D * 32), su[warp], flags, len, s, out, canon, oflags, lane);
     }
 }
@@ -149,7 +140,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
 // per-segment epilogue runs while the next segment's first loads are already in flight.
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
 
-__device__ __forceinline__ void seg_rescan_uniform(int64_t* col, const uint4* seg, uint32_t t0, uint32_t t1,
+__device__ __noinline__ void seg_rescan_uniform(int64_t* col, const uint4* seg, uint32_t t0, uint32_t t1,
                                                    int lane, uint32_t& flags, uint32_t one) {
     for (uint32_t t = t0; t <= t1; ++t) {
 #pragma unroll
@@ -214,7 +205,14 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
         }
         ++since;
         if (pt + 1 == TPS) {                                   // segment complete
-            close_window(pt);
+            if (__any_sync(FULL, spec_hit(nspec))) {           // raw columns go to the epilogue
+                if (spec_hit(nspec)) {
+                    regularize_column(col);
+                    seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, pt, lane, flags, one);
+                }
+            }
+            nspec = 0;
+            since = 0;
             segment_epilogue(col, win + warp * (D * 32), su[warp], flags, seg_len, ps, out, canon, oflags, lane);
             flags = 0;
             wstart = 0;

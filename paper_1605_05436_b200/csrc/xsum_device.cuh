@@ -235,7 +235,7 @@ __device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, ui
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int64_t balanced_carry(int64_t y) { return (y + (R >> 1)) >> W; }
 
-__device__ __forceinline__ void regularize_column(int64_t* col) {
+__device__ __noinline__ void regularize_column(int64_t* col) {
     int64_t cin = 0;
 #pragma unroll 6
     for (int j = 0; j < D - 1; ++j) {
@@ -258,6 +258,42 @@ __device__ __forceinline__ void regularize_warp(int64_t& a0, int64_t& a1, int la
     if (lane == 0) { in0 = 0; in1 = c31; }
     a0 = a0 - (c0 << W) + in0;
     a1 = (lane + 32 < D) ? a1 - (c1 << W) + in1 : 0;
+}
+
+// Sum the 32 lane columns of a warp WITHOUT regularizing them first, into regularized
+// digits (a0 = digit lane, a1 = digit lane+32). Each raw digit satisfies |Y| < 2^62, so it
+// is split as Y = hi*2^32 + lo (lo unsigned 32-bit): the lane sums of lo (< 2^37) and hi
+// (|.| < 2^35) cannot overflow; the balanced carry of D = HI*2^32 + LO is then
+// c = (HI + ((LO + 2^51) >> 32)) >> 20 (exact floor), and the remainder
+// r = (HI - c*2^20)*2^32 + LO. Output as regularize_warp.
+__device__ __forceinline__ void combine_raw_columns(const int64_t* wb, int64_t& a0, int64_t& a1, int lane) {
+    int64_t hs0 = 0, hs1 = 0;
+    uint64_t ls0 = 0, ls1 = 0;
+#pragma unroll 8
+    for (int c = 0; c < 32; ++c) {
+        int cc = (lane + c) & 31;                       // rotated: conflict-free columns
+        int64_t v0 = wb[lane * 32 + cc];
+        hs0 += v0 >> 32;
+        ls0 += (uint32_t)v0;
+        if (lane + 32 < D) {
+            int64_t v1 = wb[(lane + 32) * 32 + cc];
+            hs1 += v1 >> 32;
+            ls1 += (uint32_t)v1;
+        }
+    }
+    auto split = [](int64_t hs, uint64_t ls, int64_t& c, int64_t& r) {
+        c = (hs + (int64_t)((ls + (1ull << 51)) >> 32)) >> 20;
+        r = (int64_t)((uint64_t)(hs - (c << 20)) << 32) + (int64_t)ls;
+    };
+    int64_t c0, r0, c1 = 0, r1 = 0;
+    split(hs0, ls0, c0, r0);
+    if (lane + 32 < D - 1) split(hs1, ls1, c1, r1);
+    else if (lane + 32 == D - 1) { c1 = 0; r1 = (int64_t)((uint64_t)hs1 << 32) + (int64_t)ls1; }
+    int64_t in0 = __shfl_up_sync(FULL, c0, 1), in1 = __shfl_up_sync(FULL, c1, 1);
+    int64_t c31 = __shfl_sync(FULL, c0, 31);
+    if (lane == 0) { in0 = 0; in1 = c31; }
+    a0 = r0 + in0;
+    a1 = (lane + 32 < D) ? r1 + in1 : 0;
 }
 
 // ---------------------------------------------------------------------------------

@@ -235,7 +235,7 @@ __device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, ui
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int64_t balanced_carry(int64_t y) { return (y + (R >> 1)) >> W; }
 
-__device__ __noinline__ void regularize_column(int64_t* col) {
+__device__ __noinline__ static void regularize_column(int64_t* col) {
     int64_t cin = 0;
 #pragma unroll 6
     for (int j = 0; j < D - 1; ++j) {

@@ -135,6 +135,30 @@ def test_many_flush_windows_per_lane(xs, blocks):
     assert_same(res, canon, y, what=f"specials blocks={blocks}")
 
 
+@pytest.mark.parametrize("sign", [1.0, -1.0, 0.0])
+def test_headroom_worst_case_digits(xs, sign):
+    """Every summand produces the largest chunks (M = 2^53-1 at offset o = 51 in its digit),
+    all lanes hit the same digit, each lane takes full flush windows plus stragglers: the
+    raw lane digits reach the int64 headroom bound the kernel's schedule relies on
+    (xsum_device.cuh FLUSH_ELEMS) and the raw-column combine sees its largest inputs."""
+    import math
+    v = math.ldexp((1 << 53) - 1, 17)                  # e = 1092: k = 1091 = 52*20 + 51
+    n = 512 * 2032 * 3 + 4099
+    x = np.full(n, v if sign >= 0 else -v)
+    if sign == 0.0:                                    # alternate signs in runs
+        x[(np.arange(n) // 7) % 2 == 1] *= -1
+    acc = xs.Accumulator().set_grid_limit(1)
+    for off in (0, 1):
+        res, canon = acc.sum(to_dev(x, off), canon=True)
+        assert_same(xs.Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64),
+                    x, what=f"headroom sign={sign} off={off}")
+    vals, canon2, _ = xs.sum_segments(to_dev(x[: 256 * 2100 * 2]), 256 * 2100, canon=True)
+    for s in range(2):
+        r, limbs = oracle.exact_sum(x[s * 256 * 2100:(s + 1) * 256 * 2100])
+        assert int(vals.cpu().numpy().view(np.uint64)[s]) == r.bits
+        assert (canon2.cpu().numpy().view(np.uint64)[s] == limbs).all()
+
+
 def test_chunked_accumulate_random_splits(xs):
     rng = np.random.default_rng(5)
     x = synth.gen.generate("c2", 0, 3_000_000)

@@ -441,11 +441,25 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
     return r;
 }
 
-// 128-bit streaming load of two doubles as four 32-bit halves (evict-first from L1).
+// 128-bit streaming load of two doubles as four 32-bit halves (no L1 allocation).
+#ifndef XS_LOAD
+#define XS_LOAD 0   // 0: .nc.L1::no_allocate.L2::256B (product); 1: .cg; 2: .cs; 3: .nc; 4: .nc.L1::no_allocate
+#endif
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     uint4 v;
+#if XS_LOAD == 1
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+#elif XS_LOAD == 2
+    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+#elif XS_LOAD == 3
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+#elif XS_LOAD == 4
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+#endif
     return v;
 }
 

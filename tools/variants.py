@@ -15,11 +15,14 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
-    "dec4": ["-DXS_DECODE=4"],
-    "dec3": ["-DXS_DECODE=3"],
-    "dec2": ["-DXS_DECODE=2"],
-    "dec0": ["-DXS_DECODE=0"],
-    "dec4_nosmem": ["-DXS_DECODE=4", "-DXS_EXPERIMENT=1"],
+    "product": [],
+    "dec0_alu": ["-DXS_DECODE=0"],
+    "dec2_hybrid": ["-DXS_DECODE=2"],
+    "dec4_balanced": ["-DXS_DECODE=4"],
+    "nosmem_diag": ["-DXS_EXPERIMENT=1"],
+    "load_cg": ["-DXS_LOAD=1"],
+    "warps12": ["-DXS_ACC_WARPS=12"],
+    "u2": ["-DXS_ACC_U=2"],
 }
 
 

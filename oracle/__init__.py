@@ -26,6 +26,7 @@ import numpy as np
 
 NLIMB = 34                    # 2176-bit two's complement image, little-endian u64 limbs
 F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT = 1, 2, 4, 8, 16
+F_OVERFLOW32, F_INEXACT32 = 64, 128          # the binary32 rounding (value_f32)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
@@ -35,7 +36,7 @@ _SRC = os.path.join(_HERE, "xsum_oracle.c")
 class _CResult(ctypes.Structure):
     _fields_ = [("value", ctypes.c_double), ("direction", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("msb_exp", ctypes.c_int32), ("sign", ctypes.c_int32), ("count", ctypes.c_uint64),
-                ("sig53", ctypes.c_uint64), ("exp2", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("sig53", ctypes.c_uint64), ("exp2", ctypes.c_int32), ("value_f32", ctypes.c_uint32)]
 
 
 @dataclass(frozen=True)
@@ -49,6 +50,7 @@ class Result:
     count: int
     sig53: int           # unbounded-exponent rounding: |exact| ~= sig53 * 2^exp2
     exp2: int
+    bits_f32: int        # uint32 bit pattern of the RN-even binary32 rounding
 
 
 def build() -> None:
@@ -67,6 +69,8 @@ def _L():
         p, u64, i32, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32
         lib.oracle_sum.argtypes = [p, p, p, u64, i32]
         lib.oracle_sum.restype = None
+        lib.oracle_sum_f32.argtypes = [p, p, p, u64, i32]
+        lib.oracle_sum_f32.restype = None
         lib.oracle_round.argtypes = [p, u32, u64, ctypes.POINTER(_CResult)]
         lib.oracle_round.restype = None
         lib.oracle_limbs_add.argtypes = [p, p]
@@ -96,10 +100,13 @@ class Accumulator:
         return int(self._flags.value)
 
     def add(self, x: np.ndarray) -> "Accumulator":
-        x = np.ascontiguousarray(x, dtype=np.float64)
+        """Add float64 (or float32, summed exactly as binary32) values."""
+        x = np.asarray(x)
+        f32 = x.dtype == np.float32
+        x = np.ascontiguousarray(x, dtype=np.float32 if f32 else np.float64)
         if x.size:
-            _L().oracle_sum(self.limbs.ctypes.data, ctypes.addressof(self._flags), x.ctypes.data,
-                            x.size, self.nthreads)
+            fn = _L().oracle_sum_f32 if f32 else _L().oracle_sum
+            fn(self.limbs.ctypes.data, ctypes.addressof(self._flags), x.ctypes.data, x.size, self.nthreads)
         self.count += int(x.size)
         return self
 
@@ -121,12 +128,14 @@ def round_limbs(limbs: np.ndarray, flags: int, count: int = 0) -> Result:
     bits = int(np.array([r.value], dtype=np.float64).view(np.uint64)[0])
     return Result(value=r.value, bits=bits, direction=r.direction, flags=r.flags,
                   msb_exp=None if r.msb_exp == -(2 ** 31) else r.msb_exp, sign=r.sign,
-                  count=r.count, sig53=r.sig53, exp2=r.exp2)
+                  count=r.count, sig53=r.sig53, exp2=r.exp2, bits_f32=r.value_f32)
 
 
 def exact_sum(x, nthreads: int | None = None) -> tuple[Result, np.ndarray]:
-    """(rounded result, 34-limb two's complement image of sum(x)*2^1074)."""
-    acc = Accumulator(nthreads).add(np.asarray(x, dtype=np.float64))
+    """(rounded result, 34-limb two's complement image of sum(x)*2^1074); float32 arrays are
+    summed as binary32 values, anything else as float64."""
+    x = np.asarray(x)
+    acc = Accumulator(nthreads).add(x if x.dtype == np.float32 else np.asarray(x, dtype=np.float64))
     return acc.result(), acc.limbs.copy()
 
 

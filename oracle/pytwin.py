@@ -13,6 +13,7 @@ import struct
 from fractions import Fraction
 
 F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT = 1, 2, 4, 8, 16
+F_OVERFLOW32, F_INEXACT32 = 64, 128
 NLIMB = 34
 
 
@@ -58,6 +59,8 @@ def round_int(A: int, flags: int = 0) -> tuple[float, int, int]:
         direction = (fv > exact) - (fv < exact)
     if direction:
         flags |= F_INEXACT
+    _, f32flags = round_int_f32(A, 0)           # the binary32 rounding's flags (independent)
+    flags |= f32flags & (F_OVERFLOW32 | F_INEXACT32)
     if value == 0.0:
         value = 0.0                     # exact zero -> +0.0 (R9)
     if (flags & F_NAN) or ((flags & F_PINF) and (flags & F_NINF)):
@@ -84,3 +87,61 @@ def limbs(A: int) -> list[int]:
     """34 little-endian u64 limbs of A in two's complement."""
     v = A & ((1 << (64 * NLIMB)) - 1)
     return [(v >> (64 * L)) & 0xFFFFFFFFFFFFFFFF for L in range(NLIMB)]
+
+
+def decode32(bits: int) -> tuple[int, int, int]:
+    """(sign, biased exponent, fraction) of a binary32 bit pattern."""
+    return bits >> 31, (bits >> 23) & 0xFF, bits & 0x7FFFFF
+
+
+def exact_int_f32(bit_patterns) -> tuple[int, int]:
+    """(A, flags) for binary32 inputs given as uint32 bit patterns: A = sum * 2^1074."""
+    A = 0
+    flags = 0
+    for b in bit_patterns:
+        s, e, m = decode32(int(b))
+        if e == 0xFF:
+            flags |= F_NAN if m else (F_NINF if s else F_PINF)
+            continue
+        v = (m << 925) if e == 0 else ((m | (1 << 23)) << (e - 1 + 925))
+        A += -v if s else v
+    return A, flags
+
+
+def _f32_value(bits: int) -> Fraction:
+    s, e, m = decode32(bits)
+    v = Fraction(m, 1 << 149) if e == 0 else Fraction(m | (1 << 23), 1) * Fraction(2) ** (e - 150)
+    return -v if s else v
+
+
+def round_int_f32(A: int, flags: int = 0) -> tuple[int, int]:
+    """(binary32 bits, flags) of the RN-even binary32 rounding of A * 2^-1074, by search:
+    the two binary32 neighbours of the exact value are found from a float64 guess and
+    compared exactly as rationals (independent of the oracle's bit-level rounding)."""
+    flags &= F_NAN | F_PINF | F_NINF
+    if (flags & F_NAN) or ((flags & F_PINF) and (flags & F_NINF)):
+        return 0x7FC00000, flags
+    if flags & F_PINF:
+        return 0x7F800000, flags
+    if flags & F_NINF:
+        return 0xFF800000, flags
+    if A == 0:
+        return 0, flags
+    S = Fraction(A, 1 << 1074)
+    sign = 0x80000000 if A < 0 else 0
+    mag = abs(S)
+    top = Fraction((1 << 24) - 1) * Fraction(2) ** 104            # FLT_MAX
+    if mag >= top + Fraction(2) ** 103:                           # >= FLT_MAX + half ulp: tie -> even = inf
+        return sign | 0x7F800000, flags | F_OVERFLOW32 | F_INEXACT32
+    # candidate neighbours: magnitudes are monotone in the bit pattern
+    guess = struct.unpack("<I", struct.pack("<f", min(float(mag), 3.4028234663852886e38)))[0]
+    best = None
+    for b in range(max(0, guess - 2), min(0x7F7FFFFF, guess + 2) + 1):
+        d = abs(_f32_value(b) - mag)
+        key = (d, b & 1)                                           # nearest, then even
+        if best is None or key < best[0]:
+            best = (key, b)
+    b = best[1]
+    if _f32_value(b) != mag:
+        flags |= F_INEXACT32
+    return sign | b, flags

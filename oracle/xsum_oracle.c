@@ -36,6 +36,8 @@
 #define OF_NINF     4u   /* -Inf was summed */
 #define OF_OVERFLOW 8u   /* finite exact sum rounds beyond DBL_MAX -> +-Inf */
 #define OF_INEXACT  16u  /* rounded value != exact finite sum */
+#define OF_OVERFLOW32 64u   /* binary32 rounding: finite exact sum rounds beyond FLT_MAX */
+#define OF_INEXACT32 128u   /* binary32 rounding != exact finite sum */
 
 typedef struct {
     double   value;
@@ -46,7 +48,7 @@ typedef struct {
     uint64_t count;
     uint64_t sig53;      /* unbounded-exponent RN-even rounding: |exact| ~ sig53 * 2^exp2 */
     int32_t  exp2;
-    int32_t  pad;
+    uint32_t value_f32;  /* bits of the RN-even binary32 rounding of the exact sum */
 } oracle_result;
 
 /* A += v * 2^(64*at), v an unsigned 64-bit value; carry ripples to the top limb. */
@@ -86,6 +88,33 @@ void oracle_accumulate(uint64_t *P, uint64_t *N, uint32_t *flags, const double *
     }
 }
 
+/* binary32 inputs (IEEE 754 binary32, t = 23, l = 8): |x| = M 2^(k-149),
+ * M = m + [e!=0] 2^23, k = max(e,1)-1; in units of 2^-1074 that is M 2^(k+925). */
+void oracle_accumulate_f32(uint64_t *P, uint64_t *N, uint32_t *flags, const float *x, uint64_t n) {
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t b;
+        memcpy(&b, &x[i], 4);
+        uint32_t s = b >> 31;
+        uint32_t e = (b >> 23) & 0xFF;
+        uint32_t m = b & 0x7FFFFF;
+        if (e == 0xFF) {
+            if (m) *flags |= OF_NAN;
+            else   *flags |= s ? OF_NINF : OF_PINF;
+            continue;
+        }
+        uint64_t M = m | ((e != 0) ? (1u << 23) : 0);
+        if (M == 0) continue;
+        unsigned k = ((e != 0) ? e - 1 : 0) + 925;      /* bit position in units of 2^-1074 */
+        int L = (int)(k / 64);
+        unsigned sh = k % 64;
+        uint64_t lo = M << sh;
+        uint64_t hi = sh ? (M >> (64 - sh)) : 0;
+        uint64_t *T = s ? N : P;
+        limbs_add_u64(T, L, lo);
+        limbs_add_u64(T, L + 1, hi);
+    }
+}
+
 /* A += B (limbwise with carry). */
 void oracle_limbs_add(uint64_t *A, const uint64_t *B) {
     uint64_t c = 0;
@@ -114,29 +143,31 @@ void oracle_limbs_sub(uint64_t *A, const uint64_t *B) {
 }
 
 typedef struct {
-    const double *x;
+    const void *x;
     uint64_t n;
+    int f32;
     uint64_t P[NLIMB], N[NLIMB];
     uint32_t flags;
 } part_t;
 
 static void *part_run(void *arg) {
     part_t *p = (part_t *)arg;
-    oracle_accumulate(p->P, p->N, &p->flags, p->x, p->n);
+    if (p->f32) oracle_accumulate_f32(p->P, p->N, &p->flags, (const float *)p->x, p->n);
+    else        oracle_accumulate(p->P, p->N, &p->flags, (const double *)p->x, p->n);
     return NULL;
 }
 
-/* Exact sum of x[0..n) ADDED TO (A, flags) (two's complement limbs), using nthreads host
- * threads over contiguous chunks. Callers zero A and flags for a fresh sum. */
-void oracle_sum(uint64_t *A, uint32_t *flags, const double *x, uint64_t n, int nthreads) {
+static void sum_threads(uint64_t *A, uint32_t *flags, const void *x, uint64_t n, int nthreads, int f32) {
     if (nthreads < 1) nthreads = 1;
     if ((uint64_t)nthreads > n / 65536 + 1) nthreads = (int)(n / 65536 + 1);
     part_t *parts = (part_t *)calloc((size_t)nthreads, sizeof(part_t));
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
     uint64_t per = n / (uint64_t)nthreads, rem = n % (uint64_t)nthreads, off = 0;
+    size_t esz = f32 ? 4 : 8;
     for (int t = 0; t < nthreads; ++t) {
-        parts[t].x = x + off;
+        parts[t].x = (const char *)x + off * esz;
         parts[t].n = per + ((uint64_t)t < rem ? 1 : 0);
+        parts[t].f32 = f32;
         off += parts[t].n;
         pthread_create(&th[t], NULL, part_run, &parts[t]);
     }
@@ -147,6 +178,17 @@ void oracle_sum(uint64_t *A, uint32_t *flags, const double *x, uint64_t n, int n
         *flags |= parts[t].flags;
     }
     free(parts); free(th);
+}
+
+/* Exact sum of x[0..n) ADDED TO (A, flags) (two's complement limbs), using nthreads host
+ * threads over contiguous chunks. Callers zero A and flags for a fresh sum. */
+void oracle_sum(uint64_t *A, uint32_t *flags, const double *x, uint64_t n, int nthreads) {
+    sum_threads(A, flags, x, n, nthreads, 0);
+}
+
+/* Same for binary32 inputs. */
+void oracle_sum_f32(uint64_t *A, uint32_t *flags, const float *x, uint64_t n, int nthreads) {
+    sum_threads(A, flags, x, n, nthreads, 1);
 }
 
 static int bitlen64(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return b; }
@@ -225,6 +267,33 @@ void oracle_round(const uint64_t *A, uint32_t flags_in, uint64_t count, oracle_r
         if (direction) flags |= OF_INEXACT;
         if (neg) { bits |= 1ull << 63; direction = -direction; }
     }
+    /* binary32 rounding of the same exact value (t = 23, subnormal unit 2^-149 = bit 925) */
+    uint32_t b32 = 0;
+    if (top >= 0) {
+        long p = 64L * top + bitlen64(a[top]) - 1;
+        long sh = p - 23 > 925 ? p - 23 : 925;
+        uint64_t q = 0;
+        for (long j = p; j >= sh; --j) q = (q << 1) | (uint64_t)bit_at(a, j);
+        int guard = bit_at(a, sh - 1);
+        int sticky = any_below(a, sh - 1);
+        int up = guard && (sticky || (q & 1));
+        if (guard || sticky) flags |= OF_INEXACT32;
+        q += (uint64_t)up;
+        if (sh == 925) {
+            b32 = (uint32_t)q;                   /* subnormal / smallest normals: bits = q (q <= 2^24) */
+        } else {
+            if (q == (1ull << 24)) { q >>= 1; sh += 1; }
+            long Eb = sh - 925 + 1;
+            if (Eb >= 255) { b32 = 0x7F800000u; flags |= OF_OVERFLOW32 | OF_INEXACT32; }
+            else b32 = ((uint32_t)Eb << 23) | (uint32_t)(q - (1ull << 23));
+        }
+        if (neg) b32 |= 0x80000000u;            /* a negative sum that rounds to 0 gives -0.0f */
+    }
+    if ((flags & OF_NAN) || ((flags & OF_PINF) && (flags & OF_NINF))) b32 = 0x7FC00000u;
+    else if (flags & OF_PINF) b32 = 0x7F800000u;
+    else if (flags & OF_NINF) b32 = 0xFF800000u;
+    r->value_f32 = b32;
+
     if ((flags & OF_NAN) || ((flags & OF_PINF) && (flags & OF_NINF))) {
         bits = 0x7FF8000000000000ull; direction = 0;
     } else if (flags & OF_PINF) {

@@ -313,3 +313,95 @@ def test_lemma1_carry_free_addition_value_preserved():
         val = lambda v: sum(d * R ** i for i, d in enumerate(v))
         assert val(S) == val(Y) + val(Z)
         assert all(-a <= s <= a for s in S)
+
+
+# ---- binary32: inputs summed as binary32, and binary32 rounding ----
+
+GOLDEN32 = os.path.join(os.path.dirname(__file__), "golden", "rounding_edges_f32.txt")
+
+
+def load_golden32():
+    cases = []
+    with open(GOLDEN32) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            name, ins, out, cite = [p.strip() for p in line.split("|")]
+            xs = [b2f(int(h, 16)) for h in ins.split(",") if h.strip()]
+            cases.append((name, xs, int(out, 16), cite))
+    return cases
+
+
+GOLDEN32_CASES = load_golden32()
+
+
+def test_golden32_hex_literals():
+    assert f2b(float(np.float32(3.4028234663852886e38))) == 0x47EFFFFFE0000000
+    assert f2b(2.0 ** -149) == 0x36A0000000000000 and f2b(2.0 ** 103) == 0x4660000000000000
+    assert f2b(2.0 ** -54) == 0x3C90000000000000
+
+
+@pytest.mark.parametrize("case", GOLDEN32_CASES, ids=[c[0] for c in GOLDEN32_CASES])
+def test_golden32_o1_and_o2(case):
+    name, xs, out32, cite = case
+    assert re.search(r"PAPER\.md:\d+|\bR\d+\b", cite)
+    r, limbs = oracle.exact_sum(np.array(xs, dtype=np.float64))
+    assert r.bits_f32 == out32, f"{name}: {r.bits_f32:08x} != {out32:08x}"
+    A, fl = pytwin.exact_int(xs)
+    assert pytwin.round_int_f32(A, fl)[0] == out32, name
+
+
+def _rand_f32_bits(rng, n):
+    kind = rng.random()
+    out = []
+    for _ in range(n):
+        if kind < 0.3:
+            e = rng.randint(100, 106)
+        else:
+            e = rng.choice([0, 0, 1, 2, 126, 127, 253, 254]) if rng.random() < 0.3 else rng.randint(0, 254)
+        out.append((rng.getrandbits(1) << 31) | (e << 23) | rng.getrandbits(23))
+    return out
+
+
+def test_o1_f32_inputs_vs_exact_rationals():
+    """binary32 inputs: O1's exact image vs Fraction(float32) sums; its binary32 rounding vs
+    the twin's search over neighbouring binary32 values with exact rational comparisons."""
+    rng = random.Random(32)
+    for trial in range(1500):
+        bits = _rand_f32_bits(rng, rng.randint(0, 10))
+        x = np.array(bits, dtype=np.uint32).view(np.float32)
+        r, limbs = oracle.exact_sum(x)
+        S = sum((Fraction(float(v)) for v in x), Fraction(0))
+        assert oracle.limbs_to_int(limbs) == S * (1 << 1074), trial
+        A, fl = pytwin.exact_int_f32(bits)
+        assert A == oracle.limbs_to_int(limbs)
+        b32, _ = pytwin.round_int_f32(A, fl)
+        assert r.bits_f32 == b32, (trial, [hex(b) for b in bits])
+        v, d, f, _ = pytwin.exact_sum([float(v) for v in x])
+        assert r.bits == f2b(v) and r.flags == f
+
+
+def test_o1_f32_rounding_on_boundaries():
+    """binary32 rounding of integers straddling ties / overflow / subnormal edges (O1 bit-level
+    algorithm vs the twin's rational search)."""
+    rng = random.Random(33)
+    for _ in range(3000):
+        p = rng.randint(900, 1210)                      # binary32 range in units of 2^-1074
+        A = (rng.getrandbits(30) | (1 << 29)) << max(0, p - 29)
+        A += rng.choice([0, 1, -1, 1 << max(0, p - 24), (1 << max(0, p - 24)) - 1, 1 << max(0, p - 25)])
+        A *= rng.choice([1, -1])
+        r = oracle.round_limbs(oracle.int_to_limbs(A), 0, 0)
+        b32, fl = pytwin.round_int_f32(A, 0)
+        assert r.bits_f32 == b32, hex(A)
+        assert (r.flags & (oracle.F_OVERFLOW32 | oracle.F_INEXACT32)) == fl
+
+
+def test_f32_sum_equals_numpy_when_exactly_representable():
+    """Sums of small integers as float32 are exact in any order: the binary32 rounding is the value."""
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        x = rng.integers(-1000, 1000, size=1000).astype(np.float32)
+        r, _ = oracle.exact_sum(x)
+        expect = np.float32(int(x.astype(np.int64).sum()))
+        assert r.bits_f32 == int(np.array([expect], dtype=np.float32).view(np.uint32)[0])

@@ -68,6 +68,8 @@ typedef enum xsum_status {
 #define XSUM_F_OVERFLOW 8u   /* the finite exact sum rounds beyond DBL_MAX (result +-Inf) */
 #define XSUM_F_INEXACT 16u   /* the finite exact sum is not representable */
 #define XSUM_F_MISMATCH 32u  /* a merged state image was rejected (header mismatch) */
+#define XSUM_F_OVERFLOW32 64u /* the binary32 rounding (value_f32) overflowed to +-Inf */
+#define XSUM_F_INEXACT32 128u /* the binary32 rounding differs from the exact finite sum */
 
 /* Packed state image (XSUM_STATE_BYTES, little-endian). Exactly mergeable in any
  * order; it is also the checkpoint format and what ranks exchange.
@@ -101,7 +103,8 @@ typedef struct xsum_result {
     uint64_t count;      /* summands accumulated */
     uint64_t sig53;      /* unbounded-exponent rounding: |exact| ~= sig53 * 2^exp2 (RN-even, 53 bits) */
     int32_t exp2;
-    int32_t reserved;
+    uint32_t value_f32;  /* bits of the RN-even binary32 rounding of the exact sum (one rounding, no
+                            double rounding; a negative sum that rounds to 0 gives -0.0f) */
 } xsum_result;
 
 typedef struct xsum_ctx xsum_ctx;
@@ -130,6 +133,16 @@ XSUM_API xsum_status xsum_reset(xsum_ctx *h, void *stream);
  * Errors: XSUM_EINVAL (h or d_x null with n > 0, d_x not 8-B aligned),
  * XSUM_ECAPACITY (total count > 2^63-1), XSUM_ECUDA (launch failure). */
 XSUM_API xsum_status xsum_accumulate(xsum_ctx *h, const double *d_x, uint64_t n, void *stream);
+
+/* Binary32 inputs: state += sum of the binary32 values d_x[0..n) EXACTLY
+ * (IEEE binary32, t = 23 / l = 8; every binary32 is a multiple of 2^-149,
+ * inside the same 2^-1074 fixed-point window). d_x 4-byte aligned. Same errors as
+ * xsum_accumulate. Results round to binary64 (value) and binary32 (value_f32). */
+XSUM_API xsum_status xsum_accumulate_f32(xsum_ctx *h, const float *d_x, uint64_t n, void *stream);
+
+/* One-shot fused binary32 path (reset + accumulate_f32 + finalize in one launch). */
+XSUM_API xsum_status xsum_sum_f32(xsum_ctx *h, const float *d_x, uint64_t n, void *d_res, uint64_t *d_canon,
+                                  void *stream);
 
 /* State += sum of h_x[0..n) for a HOST buffer (pinned memory overlaps best): chunks are
  * copied into the caller's device staging buffer d_stage (two halves, double-buffered,

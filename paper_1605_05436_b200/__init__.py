@@ -30,6 +30,7 @@ NDIGITS = 42
 MAGIC = 0x4D555358
 VERSION = 1
 F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT, F_MISMATCH = 1, 2, 4, 8, 16, 32
+F_OVERFLOW32, F_INEXACT32 = 64, 128
 
 OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 
@@ -37,7 +38,7 @@ OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_create", "xsum_reset",
            "xsum_accumulate", "xsum_accumulate_host", "xsum_merge", "xsum_finalize_round", "xsum_sum",
            "xsum_destroy", "xsum_count", "xsum_sum_segments", "xsum_sum_segments_csr", "xsum_status_str",
-           "xsum_launch_count", "xsum_set_grid_limit")
+           "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32")
 
 
 class XsumError(RuntimeError):
@@ -74,6 +75,7 @@ def lib() -> ctypes.CDLL:
             "xsum_sum_segments_csr": ([p, p, u64, p, p, p, p], i32),
             "xsum_status_str": ([i32], ctypes.c_char_p), "xsum_launch_count": ([], u64),
             "xsum_set_grid_limit": ([p, u32], i32),
+            "xsum_accumulate_f32": ([p, p, u64, p], i32), "xsum_sum_f32": ([p, p, u64, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -111,6 +113,11 @@ class Result:
     count: int
     sig53: int
     exp2: int
+    bits_f32: int        # bits of the RN-even binary32 rounding of the exact sum
+
+    @property
+    def value_f32(self) -> float:
+        return float(np.array([self.bits_f32], dtype=np.uint32).view(np.float32)[0])
 
     @staticmethod
     def from_bytes(b: bytes | np.ndarray) -> "Result":
@@ -123,10 +130,11 @@ class Result:
         count = int(a[24:32].view(np.uint64)[0])
         sig53 = int(a[32:40].view(np.uint64)[0])
         exp2 = int(a[40:44].view(np.int32)[0])
+        b32 = int(a[44:48].view(np.uint32)[0])
         msb = int(i32[2])
         return Result(value=value, bits=bits, direction=int(i32[0]), flags=int(u32[1]),
                       msb_exp=None if msb == -(2 ** 31) else msb, sign=int(i32[3]), count=count,
-                      sig53=sig53, exp2=exp2)
+                      sig53=sig53, exp2=exp2, bits_f32=b32)
 
 
 def _torch():
@@ -139,15 +147,19 @@ def _stream_ptr(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _as_f64_cuda(t):
+def _as_f64_cuda(t, allow_f32: bool = False):
     torch = _torch()
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError("expected a CUDA tensor")
-    if t.dtype != torch.float64:
-        raise TypeError(f"expected float64, got {t.dtype}")
+    if t.dtype != torch.float64 and not (allow_f32 and t.dtype == torch.float32):
+        raise TypeError(f"expected float64{' or float32' if allow_f32 else ''}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
     return t
+
+
+def _is_f32(t) -> bool:
+    return t.dtype == _torch().float32
 
 
 class Accumulator:
@@ -204,9 +216,14 @@ class Accumulator:
         return self
 
     def add(self, x) -> "Accumulator":
-        x = _as_f64_cuda(x)
-        _check("xsum_accumulate", lib().xsum_accumulate(self._h, x.data_ptr(), x.numel(),
-                                                        _stream_ptr(self.device)))
+        """Sum a float64 (binary64) or float32 (binary32) CUDA tensor into the state, exactly."""
+        x = _as_f64_cuda(x, allow_f32=True)
+        if _is_f32(x):
+            _check("xsum_accumulate_f32", lib().xsum_accumulate_f32(self._h, x.data_ptr(), x.numel(),
+                                                                    _stream_ptr(self.device)))
+        else:
+            _check("xsum_accumulate", lib().xsum_accumulate(self._h, x.data_ptr(), x.numel(),
+                                                            _stream_ptr(self.device)))
         return self
 
     def add_host(self, x, stage_bytes: int = 128 << 20) -> "Accumulator":
@@ -253,11 +270,12 @@ class Accumulator:
         return Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64).copy()
 
     def sum(self, x, canon: bool = False):
-        """One-shot fused path (xsum_sum): state := sum(x); returns device (result, canon)."""
-        x = _as_f64_cuda(x)
-        _check("xsum_sum", lib().xsum_sum(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
-                                          self._canon.data_ptr() if canon else None,
-                                          _stream_ptr(self.device)))
+        """One-shot fused path (xsum_sum / xsum_sum_f32): state := sum(x); returns device
+        (result, canon)."""
+        x = _as_f64_cuda(x, allow_f32=True)
+        fn, name = (lib().xsum_sum_f32, "xsum_sum_f32") if _is_f32(x) else (lib().xsum_sum, "xsum_sum")
+        _check(name, fn(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
+                        self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
         return self._res, (self._canon if canon else None)
 
 
@@ -274,18 +292,20 @@ def _acc_for(device) -> Accumulator:
 
 
 def exact_sum(x) -> tuple[Result, np.ndarray]:
-    """Exact sum of a float64 CUDA tensor: (rounded Result, canonical 34-limb image)."""
-    x = _as_f64_cuda(x)
+    """Exact sum of a float64 or float32 CUDA tensor: (rounded Result, canonical 34-limb image)."""
+    x = _as_f64_cuda(x, allow_f32=True)
     acc = _acc_for(x.device)
     res, canon = acc.sum(x, canon=True)
     return Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64).copy()
 
 
 def fsum(x) -> float:
-    """Correctly rounded (RN-even) sum of a float64 CUDA tensor."""
-    x = _as_f64_cuda(x)
+    """Correctly rounded (RN-even) sum of a float64 CUDA tensor (float32 tensors: the correctly
+    rounded binary32 of their exact sum, returned as a Python float)."""
+    x = _as_f64_cuda(x, allow_f32=True)
     res, _ = _acc_for(x.device).sum(x)
-    return Result.from_bytes(res.cpu().numpy().tobytes()).value
+    r = Result.from_bytes(res.cpu().numpy().tobytes())
+    return r.value_f32 if _is_f32(x) else r.value
 
 
 def sum_segments(x, seg_len: int, canon: bool = False, flags: bool = False):

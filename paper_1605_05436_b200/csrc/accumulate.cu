@@ -17,10 +17,10 @@
 
 namespace xs {
 
-template <int WARPS, int U>
+template <int WARPS, int U, typename E>
 struct AccCfg {
     static constexpr int T = WARPS * 32;
-    static constexpr int FLUSH_TILES = FLUSH_ELEMS / (2 * U);
+    static constexpr int FLUSH_TILES = FLUSH_ELEMS / (Elem<E>::PER_VEC * U);
     static constexpr size_t SMEM = (size_t)WARPS * D * 32 * sizeof(int64_t);
 };
 
@@ -30,7 +30,7 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
     return v;
 }
 
-template <int U, int T>
+template <int U, int T, typename E>
 __device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint64_t t0, uint64_t t1,
                                               uint64_t G, uint64_t TV, int tid, uint32_t& flags, uint32_t one) {
     // Rare path: this lane summed a NaN/Inf bit pattern as if finite somewhere in tiles
@@ -39,16 +39,17 @@ __device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
-            column_fix_special(col, v.x, v.y, flags, one);
-            column_fix_special(col, v.z, v.w, flags, one);
+            Elem<E>::fix_vec(col, v, flags, one);
         }
     }
 }
 
-template <int WARPS, int U>
+template <int WARPS, int U, typename E>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
-    using C = AccCfg<WARPS, U>;
+k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
+    using C = AccCfg<WARPS, U, E>;
+    using EL = Elem<E>;
+    constexpr int PV = EL::PER_VEC;
     constexpr int T = C::T;
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t wsum[WARPS][D];
@@ -63,9 +64,11 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
 
-    const uint64_t head = (n && ((uintptr_t)x & 15)) ? 1 : 0;   // peel to 16-B alignment
+    // peel up to PV-1 head elements to reach 16-B alignment; <= PV-1 tail elements remain
+    uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / sizeof(E);
+    if (head > n) head = n;
     const uint64_t nbody = n - head;
-    const uint64_t nvec = nbody >> 1;
+    const uint64_t nvec = nbody / PV;
     const uint4* body = reinterpret_cast<const uint4*>(x + head);
     const uint64_t TV = (uint64_t)T * U;
     const uint64_t ntiles = nvec / TV;
@@ -87,21 +90,14 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     };
     auto do_tile = [&](const uint4 (&buf)[U], uint64_t tt) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            Chunks a = decompose(buf[u].x, buf[u].y, one, mone);
-            nspec = spec_fold(nspec, a);
-            column_add(col, a, one);
-            Chunks b = decompose(buf[u].z, buf[u].w, one, mone);
-            nspec = spec_fold(nspec, b);
-            column_add(col, b, one);
-        }
+        for (int u = 0; u < U; ++u) EL::add_vec(col, buf[u], nspec, one, mone);
         any_tile = true;
         tlast = tt;
         if (++since == C::FLUSH_TILES) {
             regularize_column(col);
-            if (__any_sync(FULL, spec_hit(nspec))) {       // rare: cancel NaN/Inf patterns
-                if (spec_hit(nspec)) {
-                    rescan_window<U, T>(col, body, wstart, tt, G, TV, tid, flags, one);
+            if (__any_sync(FULL, EL::hit(nspec))) {        // rare: cancel NaN/Inf patterns
+                if (EL::hit(nspec)) {
+                    rescan_window<U, T, E>(col, body, wstart, tt, G, TV, tid, flags, one);
                     regularize_column(col);
                 }
             }
@@ -130,32 +126,23 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
         t += G;
     }
 
-    // leftover vectors (< one tile), the unaligned head and the odd tail element: checked
-    // adds by the block that would own the next tile.
+    // leftover vectors (< one tile), the unaligned head and the tail elements: checked adds by
+    // the block that would own the next tile.
     if (blockIdx.x == ntiles % G) {
         const uint64_t v0 = ntiles * TV;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             uint64_t v = v0 + (uint64_t)u * T + tid;
-            if (v < nvec) {
-                uint4 q = ldg_stream(body + v);
-                column_add_checked(col, q.x, q.y, flags, one);
-                column_add_checked(col, q.z, q.w, flags, one);
-            }
+            if (v < nvec) EL::add_vec_checked(col, ldg_stream(body + v), flags, one);
         }
-        if (tid == 0 && head) {
-            uint2 q = ldg_one(x);
-            column_add_checked(col, q.x, q.y, flags, one);
-        }
-        if (tid == 1 && (nbody & 1)) {
-            uint2 q = ldg_one(x + head + 2 * nvec);
-            column_add_checked(col, q.x, q.y, flags, one);
-        }
+        const uint64_t tail = nbody - nvec * PV;
+        if ((uint64_t)tid < head) EL::add_one_checked(col, x + tid, flags, one);
+        if (tid >= PV && (uint64_t)(tid - PV) < tail) EL::add_one_checked(col, x + head + nvec * PV + (tid - PV), flags, one);
     }
-    if (__any_sync(FULL, spec_hit(nspec))) {
-        if (spec_hit(nspec) && any_tile) {
+    if (__any_sync(FULL, EL::hit(nspec))) {
+        if (EL::hit(nspec) && any_tile) {
             regularize_column(col);
-            rescan_window<U, T>(col, body, wstart, tlast, G, TV, tid, flags, one);
+            rescan_window<U, T, E>(col, body, wstart, tlast, G, TV, tid, flags, one);
         }
     }
     __syncwarp();
@@ -232,23 +219,23 @@ k_accumulate(const double* __restrict__ x, uint64_t n, AccParams p) {
     }
 }
 
-template <int WARPS, int U>
-static cudaError_t launch_accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms,
-                                     cudaStream_t s) {
-    using C = AccCfg<WARPS, U>;
+template <int WARPS, int U, typename E>
+static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
+    using C = AccCfg<WARPS, U, E>;
     static bool attr_set = false;   // per process; the attribute is per function and device-independent
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_accumulate<WARPS, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_accumulate<WARPS, U, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)C::SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const uint64_t head = (n && ((uintptr_t)x & 15)) ? 1 : 0;
-    const uint64_t ntiles = ((n - head) / 2) / ((uint64_t)C::T * U);
+    uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / sizeof(E);
+    if (head > n) head = n;
+    const uint64_t ntiles = ((n - head) / Elem<E>::PER_VEC) / ((uint64_t)C::T * U);
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    k_accumulate<WARPS, U><<<(unsigned)g, C::T, C::SMEM, s>>>(x, n, p);
+    k_accumulate<WARPS, U, E><<<(unsigned)g, C::T, C::SMEM, s>>>(x, n, p);
     note_launch();
     return cudaGetLastError();
 }
@@ -257,11 +244,15 @@ static cudaError_t launch_accumulate(const double* x, uint64_t n, const AccParam
 #define XS_ACC_WARPS 16   // 16 warps x 42 digits x 32 lanes x 8 B = 168 KiB of lane columns per SM
 #endif
 #ifndef XS_ACC_U
-#define XS_ACC_U 4        // 16-B vectors per thread per tile (8 summands), double-buffered in registers
+#define XS_ACC_U 4        // 16-B vectors per thread per tile, three tiles in flight (registers)
 #endif
 
 cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U>(x, n, p, num_sms, s);
+    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, double>(x, n, p, num_sms, s);
+}
+
+cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
+    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, float>(x, n, p, num_sms, s);
 }
 
 }  // namespace xs

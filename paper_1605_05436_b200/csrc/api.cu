@@ -159,6 +159,33 @@ xsum_status xsum_sum(xsum_ctx* h, const double* d_x, uint64_t n, void* d_res, ui
     return XSUM_OK;
 }
 
+xsum_status xsum_accumulate_f32(xsum_ctx* h, const float* d_x, uint64_t n, void* stream) {
+    if (!h) return XSUM_EINVAL;
+    if (n == 0) return XSUM_OK;
+    if (!d_x || !aligned(d_x, 4)) return XSUM_EINVAL;
+    if (n > kMaxCount - h->count) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::accumulate_f32(d_x, n, acc_params(h, 0, nullptr, nullptr), grid_of(h), static_cast<cudaStream_t>(stream)) !=
+        cudaSuccess)
+        return XSUM_ECUDA;
+    h->count += n;
+    return XSUM_OK;
+}
+
+xsum_status xsum_sum_f32(xsum_ctx* h, const float* d_x, uint64_t n, void* d_res, uint64_t* d_canon, void* stream) {
+    if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;
+    if (n && (!d_x || !aligned(d_x, 4))) return XSUM_EINVAL;
+    if (n > kMaxCount) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::accumulate_f32(d_x, n, acc_params(h, 1, static_cast<xsum_result*>(d_res), d_canon), grid_of(h),
+                           static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
+    h->count = n;
+    return XSUM_OK;
+}
+
 xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, void* d_stage, size_t stage_bytes,
                                  void* stream) {
     if (!h) return XSUM_EINVAL;

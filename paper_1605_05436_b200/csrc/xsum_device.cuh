@@ -20,13 +20,14 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // Summands a lane column may take between two regularizations. Each summand adds one
 // chunk (|chunk| <= 2^52) to at most one position of each digit. A window holds at most
-// FLUSH_ELEMS hot-loop summands plus <= 10 head/tail/leftover summands on top of a
-// regularized residue |Y| <= 2^51 + 2^11:  2^51 + 2^11 + (2032 + 10) * 2^52 + 2^51 < 2^63,
-// so neither the adds nor the balanced carry (y + R/2) can overflow int64. NaN/Inf bit
-// patterns summed unchecked are cancelled after the window's regularization, in a fresh
-// window of the same bound (re-derived in tests/test_host_logic.py). The paper's "reserved
-// extra bit" becomes 11 bits of headroom per int64 digit here.
-constexpr int FLUSH_ELEMS = 2032;
+// FLUSH_ELEMS hot-loop summands plus <= 17 head/tail/leftover summands (4 x 4 binary32 per
+// lane + 1) on top of a regularized residue |Y| <= 2^51 + 2^11:
+// 2^51 + 2^11 + (2016 + 17) * 2^52 + 2^51 < 2^63, so neither the adds nor the balanced
+// carry (y + R/2) can overflow int64. NaN/Inf bit patterns summed unchecked are cancelled
+// after the window's regularization, in a fresh window of the same bound (re-derived in
+// tests/test_host_logic.py). The paper's "reserved extra bit" becomes
+// 11 bits of headroom per int64 digit here. 2016 is a multiple of 8 and 16 (whole tiles).
+constexpr int FLUSH_ELEMS = 2016;
 
 // ---------------------------------------------------------------------------------
 // Step 2 of the PRAM algorithm: split x into O(1) components whose
@@ -226,6 +227,119 @@ __device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, ui
 }
 
 // ---------------------------------------------------------------------------------
+// binary32 inputs (IEEE binary32, t = 23, l = 8):
+// |x| = M 2^(k-149) with M = m + [e!=0] 2^23 < 2^24, k = max(e,1)-1, i.e. M at bit position
+// k + 925 in units of 2^-1074: the same digit window holds binary32 values exactly.
+// ---------------------------------------------------------------------------------
+constexpr uint32_t SPEC_K_F64 = 2046;   // bit position k reached only by NaN/Inf patterns
+constexpr uint32_t SPEC_K_F32 = 1179;   // 254 + 925
+
+__device__ __forceinline__ Chunks decompose32(uint32_t b, uint32_t one, uint32_t mone) {
+    Chunks c;
+    uint32_t h = b & 0x7FFFFFFFu;
+    uint32_t e = h >> 23;
+    uint32_t ep = max(e, 1u);
+    uint32_t k = mad_u32(ep, one, 924u);                  // ep - 1 + 925
+    uint32_t i = mulhi_u32(k, K52);                       // k / 52
+    uint32_t o = mad_u32(i, (uint32_t)-52, k);
+    uint32_t r = mad_u32(o, mone, 52u);                   // 52 - o
+    uint32_t M = mad_u32(mad_u32(ep, 0xFF800000u, h), one, 0x800000u);   // h - (ep-1) 2^23
+    int32_t S = (int32_t)b >> 31;
+    int64_t sM = (int64_t)(int32_t)((M ^ (uint32_t)S) - (uint32_t)S);     // +-M, |M| < 2^24
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> r;
+    c.i = i;
+    c.spec = k;
+    return c;
+}
+
+__device__ __forceinline__ uint32_t special_flags32(uint32_t b) {
+    if (b & 0x7FFFFFu) return XSUM_F_NAN;
+    return (b >> 31) ? XSUM_F_NINF : XSUM_F_PINF;
+}
+
+// Input element traits: how a 16-byte vector splits into summands, and the non-hot paths.
+template <typename T> struct Elem;
+
+template <> struct Elem<double> {
+    static constexpr int PER_VEC = 2;
+    __device__ static __forceinline__ uint32_t fold(uint32_t acc, const Chunks& c) { return spec_fold(acc, c); }
+    __device__ static __forceinline__ bool hit(uint32_t acc) { return spec_hit(acc); }
+    __device__ static __forceinline__ void add_vec(int64_t* col, const uint4& v, uint32_t& nspec, uint32_t one,
+                                                   uint32_t mone) {
+        Chunks a = decompose(v.x, v.y, one, mone);
+        nspec = fold(nspec, a);
+        column_add(col, a, one);
+        Chunks b = decompose(v.z, v.w, one, mone);
+        nspec = fold(nspec, b);
+        column_add(col, b, one);
+    }
+    __device__ static __forceinline__ void fix_vec(int64_t* col, const uint4& v, uint32_t& flags, uint32_t one) {
+        column_fix_special(col, v.x, v.y, flags, one);
+        column_fix_special(col, v.z, v.w, flags, one);
+    }
+    __device__ static __forceinline__ void add_vec_checked(int64_t* col, const uint4& v, uint32_t& flags,
+                                                           uint32_t one) {
+        column_add_checked(col, v.x, v.y, flags, one);
+        column_add_checked(col, v.z, v.w, flags, one);
+    }
+    __device__ static __forceinline__ void add_one_checked(int64_t* col, const double* p, uint32_t& flags,
+                                                           uint32_t one) {
+        uint2 q;
+        asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(q.x), "=r"(q.y) : "l"(p));
+        column_add_checked(col, q.x, q.y, flags, one);
+    }
+};
+
+template <> struct Elem<float> {
+    static constexpr int PER_VEC = 4;
+    __device__ static __forceinline__ uint32_t fold(uint32_t acc, const Chunks& c) { return max(acc, c.spec); }
+    __device__ static __forceinline__ bool hit(uint32_t acc) { return acc >= SPEC_K_F32; }
+    __device__ static __forceinline__ void add1(int64_t* col, uint32_t b, uint32_t& nspec, uint32_t one,
+                                                uint32_t mone) {
+        Chunks a = decompose32(b, one, mone);
+        nspec = fold(nspec, a);
+        column_add(col, a, one);
+    }
+    __device__ static __forceinline__ void add_vec(int64_t* col, const uint4& v, uint32_t& nspec, uint32_t one,
+                                                   uint32_t mone) {
+        add1(col, v.x, nspec, one, mone);
+        add1(col, v.y, nspec, one, mone);
+        add1(col, v.z, nspec, one, mone);
+        add1(col, v.w, nspec, one, mone);
+    }
+    __device__ static __forceinline__ void fix1(int64_t* col, uint32_t b, uint32_t& flags, uint32_t one) {
+        if (((b >> 23) & 0xFFu) != 0xFFu) return;
+        flags |= special_flags32(b);
+        column_add(col, decompose32(b ^ 0x80000000u, one, 0xFFFFFFFFu), one);
+    }
+    __device__ static __forceinline__ void fix_vec(int64_t* col, const uint4& v, uint32_t& flags, uint32_t one) {
+        fix1(col, v.x, flags, one);
+        fix1(col, v.y, flags, one);
+        fix1(col, v.z, flags, one);
+        fix1(col, v.w, flags, one);
+    }
+    __device__ static __forceinline__ void checked1(int64_t* col, uint32_t b, uint32_t& flags, uint32_t one) {
+        Chunks c = decompose32(b, one, 0xFFFFFFFFu);
+        if (hit(c.spec)) { flags |= special_flags32(b); return; }
+        column_add(col, c, one);
+    }
+    __device__ static __forceinline__ void add_vec_checked(int64_t* col, const uint4& v, uint32_t& flags,
+                                                           uint32_t one) {
+        checked1(col, v.x, flags, one);
+        checked1(col, v.y, flags, one);
+        checked1(col, v.z, flags, one);
+        checked1(col, v.w, flags, one);
+    }
+    __device__ static __forceinline__ void add_one_checked(int64_t* col, const float* p, uint32_t& flags,
+                                                           uint32_t one) {
+        uint32_t b;
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(b) : "l"(p));
+        checked1(col, b, flags, one);
+    }
+};
+
+// ---------------------------------------------------------------------------------
 // Regularization (PAPER.md:559-576 with the GSD idea of PAPER.md:522-525): each digit
 // is split as Y_j = C_{j+1} R + r_j with a balanced remainder r_j in [-R/2, R/2) and
 // S_j = r_j + C_j. Each output digit depends only on digits j and j-1 (carry-free).
@@ -395,10 +509,18 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
 
     if (lane == 0) {
         r.count = count;
-        r.reserved = 0;
         uint32_t fl = flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
         uint64_t bits = 0;
+        uint32_t b32 = 0;
         int dir = 0;
+        // any bit of |A| below position pos (pos >= 0)?
+        auto any_below = [&](int pos) -> bool {
+            int jg = pos / 52;
+            bool st = (nzu & ((1ull << jg) - 1)) != 0;
+            int off = pos - 52 * jg;
+            if (off) st = st || ((uint64_t)su[jg] & ((1ull << off) - 1));
+            return st;
+        };
         if (!nzu) {                               // exact zero -> +0.0 (reading R9)
             r.msb_exp = INT32_MIN; r.sign = 0; r.sig53 = 0; r.exp2 = 0;
         } else {
@@ -413,11 +535,7 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
                 int sh = p - 52;
                 uint64_t q = extract_bits(su, sh, 53);
                 int g = (int)extract_bits(su, sh - 1, 1);
-                int gpos = sh - 1;                // sticky: any bit below the guard bit
-                int jg = gpos / 52;
-                bool sticky = (nzu & ((1ull << jg) - 1)) != 0;
-                int off = gpos - 52 * jg;
-                if (off) sticky = sticky || ((uint64_t)su[jg] & ((1ull << off) - 1));
+                bool sticky = any_below(sh - 1);  // sticky: any bit below the guard bit
                 int up = g && (sticky || (q & 1));
                 if (g || sticky) dir = up ? 1 : -1;
                 q += (uint64_t)up;
@@ -429,7 +547,30 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
             }
             if (dir) fl |= XSUM_F_INEXACT;
             if (sign) { bits |= 1ull << 63; dir = -dir; }
+            // binary32 rounding of the same exact value (t = 23; least subnormal 2^-149 = bit 925)
+            {
+                int sh = p - 23 > 925 ? p - 23 : 925;
+                uint64_t q = extract_bits(su, sh, 25);
+                int g = (int)extract_bits(su, sh - 1, 1);
+                bool sticky = any_below(sh - 1);
+                int up = g && (sticky || (q & 1));
+                if (g || sticky) fl |= XSUM_F_INEXACT32;
+                q += (uint64_t)up;
+                if (sh == 925) {
+                    b32 = (uint32_t)q;            // subnormal / smallest normals: bits = q (q <= 2^24)
+                } else {
+                    if (q == (1ull << 24)) { q >>= 1; sh += 1; }
+                    int Eb = sh - 925 + 1;
+                    if (Eb >= 255) { b32 = 0x7F800000u; fl |= XSUM_F_OVERFLOW32 | XSUM_F_INEXACT32; }
+                    else b32 = ((uint32_t)Eb << 23) | (uint32_t)(q - (1ull << 23));
+                }
+                if (sign) b32 |= 0x80000000u;     // a negative sum that rounds to 0 gives -0.0f (R18)
+            }
         }
+        if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) b32 = 0x7FC00000u;
+        else if (fl & XSUM_F_PINF) b32 = 0x7F800000u;
+        else if (fl & XSUM_F_NINF) b32 = 0xFF800000u;
+        r.value_f32 = b32;
         if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) { bits = 0x7FF8000000000000ull; dir = 0; }
         else if (fl & XSUM_F_PINF) { bits = 0x7FF0000000000000ull; dir = 0; }
         else if (fl & XSUM_F_NINF) { bits = 0xFFF0000000000000ull; dir = 0; }

@@ -31,6 +31,7 @@ constexpr size_t SCRATCH_BYTES = SCRATCH_FLAGS_OFF + sizeof(uint32_t) * XS_MAXB;
 void note_launch();
 
 cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
+cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
 cudaError_t init_state(xsum_state_image* st, cudaStream_t s);
 cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, cudaStream_t s);
 cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s);

@@ -52,6 +52,7 @@ def assert_same(res, canon, x: np.ndarray | None = None, ref=None, what: str = "
     assert res.flags == r.flags, f"{what}: flags {res.flags} != {r.flags}"
     assert res.msb_exp == r.msb_exp and res.sign == r.sign, what
     assert res.sig53 == r.sig53 and res.exp2 == r.exp2, what
+    assert res.bits_f32 == r.bits_f32, f"{what}: binary32 {res.bits_f32:08x} != oracle {r.bits_f32:08x}"
     if canon is not None:
         assert (np.asarray(canon, dtype=np.uint64) == limbs).all(), f"{what}: canonical image differs"
 
@@ -396,3 +397,66 @@ def test_full_config_c4_one_gpu(xs):
         acc.add(synth.host_generate("c4", start, chunk, out=buf))
     assert_same(res, canon, ref=(acc.result(), acc.limbs), what="c4")
     assert math.isinf(res.value) or res.msb_exp < 1024      # (Q12: almost surely +-Inf)
+
+
+# ---------------------------------------------------------------------------------------
+# binary32 inputs
+# ---------------------------------------------------------------------------------------
+
+def _f32_data(n: int, seed: int, emin: int = 1, emax: int = 254) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    e = rng.integers(emin, emax + 1, size=n, dtype=np.uint32)
+    bits = (rng.integers(0, 2, size=n, dtype=np.uint32) << np.uint32(31)) | (e << np.uint32(23)) | \
+        rng.integers(0, 1 << 23, size=n, dtype=np.uint32)
+    return bits.view(np.float32)
+
+
+def to_dev32(x: np.ndarray, offset: int = 0):
+    import torch
+    buf = torch.empty(x.size + 4, dtype=torch.float32, device="cuda")
+    t = buf[offset:offset + x.size]
+    t.copy_(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)))
+    return t
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 17, 4095, 4096 * 4 + 3, 65536 + 7, 148 * 8192 + 11, 3_000_001])
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_f32_sizes_alignment(xs, n, off):
+    x = _f32_data(n, n + 17 * off)
+    if n > 10:                                   # subnormals and zeros too
+        x[::97] = np.float32(1e-42)
+        x[5::101] = np.float32(-0.0)
+    ref = oracle.exact_sum(x)
+    d = to_dev32(x, off)
+    res, canon = xs.exact_sum(d)
+    assert_same(res, canon, ref=ref, what=f"f32 fused n={n} off={off}")
+    acc = xs.Accumulator().add(d)
+    res2, canon2 = acc.exact()
+    assert_same(res2, canon2, ref=ref, what=f"f32 acc n={n} off={off}")
+
+
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_f32_flush_windows_and_specials(xs, blocks):
+    n = 3 * 2016 * 512 * blocks + 777
+    x = _f32_data(n, blocks, 100, 160)
+    acc = xs.Accumulator().set_grid_limit(blocks)
+    res, canon = acc.sum(to_dev32(x), canon=True)
+    assert_same(xs.Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64),
+                x, what=f"f32 windows blocks={blocks}")
+    y = x.copy()
+    rng = np.random.default_rng(7)
+    for i in rng.choice(n, size=25, replace=False):
+        y.view(np.uint32)[i] = rng.choice([0x7F800000, 0xFF800000, 0x7FC00001])
+    acc.reset().add(to_dev32(y, 1))
+    res, canon = acc.exact()
+    assert_same(res, canon, y, what=f"f32 specials blocks={blocks}")
+
+
+def test_mixed_binary32_and_binary64_in_one_state(xs):
+    """One superaccumulator holds binary32 and binary64 summands exactly (same 2^-1074 window)."""
+    a = _f32_data(1_000_003, 3, 60, 200)
+    b = synth.gen.generate("c2", 0, 2_000_001)
+    acc = xs.Accumulator().add(to_dev32(a)).add(to_dev(b, 1)).add(to_dev32(-a[:1000]))
+    res, canon = acc.exact()
+    oa = oracle.Accumulator().add(a).add(b).add(-a[:1000])
+    assert_same(res, canon, ref=(oa.result(), oa.limbs), what="mixed")

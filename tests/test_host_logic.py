@@ -122,13 +122,13 @@ def test_digit_index_division_and_chunk_split_cover_binary64():
 
 
 def test_flush_headroom_bound():
-    """FLUSH_ELEMS: residue + (F + 10 stragglers) chunk adds + the balanced-carry offset fit
+    """FLUSH_ELEMS: residue + (F + 17 stragglers) chunk adds + the balanced-carry offset fit
     int64; the NaN/Inf compensation window (<= F adds after a regularization) likewise."""
     src = open(os.path.join(ROOT, "paper_1605_05436_b200", "csrc", "xsum_device.cuh")).read()
     F = int(re.search(r"FLUSH_ELEMS = (\d+)", src).group(1))
-    assert F % 8 == 0                                    # whole tiles (8 summands per lane)
+    assert F % 16 == 0                                   # whole tiles (8 binary64 / 16 binary32 per lane)
     residue = 2 ** 51 + 2 ** 11
-    worst = residue + (F + 10) * 2 ** 52
+    worst = residue + (F + 17) * 2 ** 52
     assert worst + 2 ** 51 < 2 ** 63
     assert residue + F * 2 ** 52 + 2 ** 51 < 2 ** 63   # compensation window
     # balanced carry magnitude after a window, and the block/grid raw sums

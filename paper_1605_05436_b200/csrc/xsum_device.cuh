@@ -6,7 +6,20 @@
 // (alpha,beta)-regularized with alpha = beta = R-1.
 #pragma once
 
+#include <assert.h>
 #include <stdint.h>
+
+// XS_CHECKED=1 builds (tools/checked_build.py) assert every shared-memory digit index and the
+// int64 headroom invariant on device: the pool's compute-sanitizer is unavailable, so the GPU
+// test-suite is run against this build as the bounds/overflow check. 0 in the product.
+#ifndef XS_CHECKED
+#define XS_CHECKED 0
+#endif
+#if XS_CHECKED
+#define XS_ASSERT(c) assert(c)
+#else
+#define XS_ASSERT(c) ((void)0)
+#endif
 
 #include "xsum.h"
 
@@ -197,7 +210,11 @@ __device__ __forceinline__ void column_add(int64_t* col, const Chunks& c, uint32
     col[0] += c.c0;
     col[32] += c.c1 + (int64_t)c.i;
 #else
+    XS_ASSERT(c.i + 1 < (uint32_t)D - 1);            // chunks land in digits <= 40
     int64_t* p = col + c.i * 32u;
+    // room for one more chunk (|c| <= 2^52) and the balanced carry's +R/2
+    XS_ASSERT(p[0] > -0x7FE0000000000000ll && p[0] < 0x7FE0000000000000ll);
+    XS_ASSERT(p[32] > -0x7FE0000000000000ll && p[32] < 0x7FE0000000000000ll);
     p[0] += c.c0;
     p[32] += c.c1;
 #endif
@@ -354,6 +371,7 @@ __device__ __noinline__ static void regularize_column(int64_t* col) {
 #pragma unroll 6
     for (int j = 0; j < D - 1; ++j) {
         int64_t y = col[j * 32];
+        XS_ASSERT(y > -(1ll << 63) + (1ll << 52) && y < (1ll << 63) - (1ll << 52));   // headroom kept
         int64_t c = balanced_carry(y);
         col[j * 32] = y - (c << W) + cin;
         cin = c;

@@ -134,6 +134,27 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
 }
 
 
+// Streaming-path epilogue: the lane columns are never zeroed; the segment's digits are the
+// difference of the raw lane sums at this segment end and at the previous one (exact
+// integer arithmetic; regularizations in between preserve every column's value, so the
+// digit-wise difference still represents exactly the value added by this segment).
+__device__ __noinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* su, uint32_t flags, uint64_t len,
+                                                    uint64_t s, double* out, uint64_t* canon, uint32_t* oflags,
+                                                    LaneSums& prev, int lane) {
+    __syncwarp();
+    LaneSums now = raw_lane_sums(wb, lane);
+    LaneSums d = {now.hs0 - prev.hs0, now.ls0 - prev.ls0, now.hs1 - prev.hs1, now.ls1 - prev.ls1};
+    prev = now;
+    int64_t a0, a1;
+    sums_to_digits(d, a0, a1, lane);
+    flags = __reduce_or_sync(FULL, flags);
+    xsum_result r = finalize_warp(a0, a1, flags, len, canon ? canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
+    if (lane == 0) {
+        out[s] = r.value;
+        if (oflags) oflags[s] = r.flags;
+    }
+}
+
 // Fast path for equal segments whose starts are 16-B aligned and whose length is a multiple
 // of one warp tile (256 doubles), e.g. config 5: a warp's tiles form one continuous stream
 // across its segments, prefetched three tiles ahead with rotating register buffers, so the
@@ -181,6 +202,7 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
     uint64_t ps = gw;            // processing cursor: segment, tile
     uint32_t pt = 0, wstart = 0, flags = 0, nspec = 0;
     int since = 0;
+    LaneSums prev = {0, 0, 0, 0};                              // raw lane sums at the previous segment end
     auto close_window = [&](uint32_t tlast) {
         regularize_column(col);
         if (__any_sync(FULL, spec_hit(nspec))) {
@@ -205,19 +227,26 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
         }
         ++since;
         if (pt + 1 == TPS) {                                   // segment complete
-            if (__any_sync(FULL, spec_hit(nspec))) {           // raw columns go to the epilogue
+            if (__any_sync(FULL, spec_hit(nspec))) {           // rare: cancel NaN/Inf patterns
                 if (spec_hit(nspec)) {
                     regularize_column(col);
                     seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, pt, lane, flags, one);
+                    regularize_column(col);
                 }
+                nspec = 0;
+                since = 0;                                     // the window restarts (all lanes)
             }
-            nspec = 0;
-            since = 0;
-            segment_epilogue(col, win + warp * (D * 32), su[warp], flags, seg_len, ps, out, canon, oflags, lane);
+            segment_epilogue_delta(win + warp * (D * 32), su[warp], flags, seg_len, ps, out, canon, oflags, prev,
+                                   lane);
             flags = 0;
-            wstart = 0;
+            wstart = 0;                                        // window tiles of the next segment start at 0
             pt = 0;
             ps += nw;
+            if (since == SEG_FLUSH_ITERS) {                    // windows may span segments; no
+                regularize_column(col);                        // NaN/Inf is pending here (checked
+                nspec = 0;                                     // above), so no rescan is needed
+                since = 0;
+            }
         } else {
             if (since == SEG_FLUSH_ITERS) close_window(pt);
             ++pt;

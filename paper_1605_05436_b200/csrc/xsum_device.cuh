@@ -371,7 +371,7 @@ __device__ __noinline__ static void regularize_column(int64_t* col) {
 #pragma unroll 6
     for (int j = 0; j < D - 1; ++j) {
         int64_t y = col[j * 32];
-        XS_ASSERT(y > -(1ll << 63) + (1ll << 52) && y < (1ll << 63) - (1ll << 52));   // headroom kept
+        XS_ASSERT(y > -0x7FF0000000000000ll && y < 0x7FF0000000000000ll);   // headroom kept
         int64_t c = balanced_carry(y);
         col[j * 32] = y - (c << W) + cin;
         cin = c;
@@ -398,34 +398,51 @@ __device__ __forceinline__ void regularize_warp(int64_t& a0, int64_t& a1, int la
 // (|.| < 2^35) cannot overflow; the balanced carry of D = HI*2^32 + LO is then
 // c = (HI + ((LO + 2^51) >> 32)) >> 20 (exact floor), and the remainder
 // r = (HI - c*2^20)*2^32 + LO. Output as regularize_warp.
-__device__ __forceinline__ void combine_raw_columns(const int64_t* wb, int64_t& a0, int64_t& a1, int lane) {
-    int64_t hs0 = 0, hs1 = 0;
-    uint64_t ls0 = 0, ls1 = 0;
+struct LaneSums {          // per lane: digits lane and lane+32, each as (sum of hi words, sum of lo words)
+    int64_t hs0, ls0, hs1, ls1;
+};
+
+__device__ __forceinline__ LaneSums raw_lane_sums(const int64_t* wb, int lane) {
+    LaneSums t = {0, 0, 0, 0};
 #pragma unroll 8
     for (int c = 0; c < 32; ++c) {
         int cc = (lane + c) & 31;                       // rotated: conflict-free columns
         int64_t v0 = wb[lane * 32 + cc];
-        hs0 += v0 >> 32;
-        ls0 += (uint32_t)v0;
+        t.hs0 += v0 >> 32;
+        t.ls0 += (int64_t)(uint32_t)v0;
         if (lane + 32 < D) {
             int64_t v1 = wb[(lane + 32) * 32 + cc];
-            hs1 += v1 >> 32;
-            ls1 += (uint32_t)v1;
+            t.hs1 += v1 >> 32;
+            t.ls1 += (int64_t)(uint32_t)v1;
         }
     }
-    auto split = [](int64_t hs, uint64_t ls, int64_t& c, int64_t& r) {
-        c = (hs + (int64_t)((ls + (1ull << 51)) >> 32)) >> 20;
-        r = (int64_t)((uint64_t)(hs - (c << 20)) << 32) + (int64_t)ls;
+    return t;
+}
+
+// Digits D_j = hs_j 2^32 + ls_j (|hs| < 2^40, |ls| < 2^50) -> regularized digits: balanced
+// carry c = floor((D + 2^51) / 2^52) = (hs + ((ls + 2^51) >> 32)) >> 20 (exact floor since
+// 0 <= ls + 2^51 < 2^52), remainder r = (hs - c 2^20) 2^32 + ls in [-2^51, 2^51).
+__device__ __forceinline__ void sums_to_digits(const LaneSums& t, int64_t& a0, int64_t& a1, int lane) {
+    auto split = [](int64_t hs, int64_t ls, int64_t& c, int64_t& r) {
+        c = (hs + ((ls + (1ll << 51)) >> 32)) >> 20;
+        r = (int64_t)((uint64_t)(hs - (c << 20)) << 32) + ls;
     };
     int64_t c0, r0, c1 = 0, r1 = 0;
-    split(hs0, ls0, c0, r0);
-    if (lane + 32 < D - 1) split(hs1, ls1, c1, r1);
-    else if (lane + 32 == D - 1) { c1 = 0; r1 = (int64_t)((uint64_t)hs1 << 32) + (int64_t)ls1; }
+    split(t.hs0, t.ls0, c0, r0);
+    if (lane + 32 < D - 1) split(t.hs1, t.ls1, c1, r1);
+    else if (lane + 32 == D - 1) { c1 = 0; r1 = (int64_t)((uint64_t)t.hs1 << 32) + t.ls1; }
     int64_t in0 = __shfl_up_sync(FULL, c0, 1), in1 = __shfl_up_sync(FULL, c1, 1);
     int64_t c31 = __shfl_sync(FULL, c0, 31);
     if (lane == 0) { in0 = 0; in1 = c31; }
     a0 = r0 + in0;
     a1 = (lane + 32 < D) ? r1 + in1 : 0;
+}
+
+// Sum the 32 lane columns of a warp WITHOUT regularizing them first, into regularized
+// digits (a0 = digit lane, a1 = digit lane+32). Each raw digit is split as Y = hi 2^32 + lo
+// (lo unsigned 32-bit): the lane sums of lo (< 2^37) and hi (|.| < 2^36) cannot overflow.
+__device__ __forceinline__ void combine_raw_columns(const int64_t* wb, int64_t& a0, int64_t& a1, int lane) {
+    sums_to_digits(raw_lane_sums(wb, lane), a0, a1, lane);
 }
 
 // ---------------------------------------------------------------------------------

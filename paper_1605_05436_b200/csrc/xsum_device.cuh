@@ -542,74 +542,68 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
         if (lane + 32 < XSUM_CANON_LIMBS) canon[lane + 32] = l1;
     }
 
+    // Step 7: lanes 0 and 1 round the same exact value in parallel, lane 0 to binary64
+    // (t = 52, least subnormal 2^-1074 = bit 0, exponent field < 2047) and lane 1 to binary32
+    // (t = 23, least subnormal 2^-149 = bit 925, exponent field < 255): one routine,
+    // ties-to-even on the guard and sticky bits (reading R3).
+    const bool is64 = lane == 0;
+    const int prec = is64 ? 53 : 24, emin = is64 ? 0 : 925, emax = is64 ? 2047 : 255;
+    uint64_t bits = 0;
+    uint32_t rf = 0;                              // flags of this lane's rounding
+    int dir = 0, msb = INT32_MIN, sh_out = 0;
+    uint64_t q_out = 0;
+    if (lane < 2 && nzu) {
+        int m = 63 - __clzll((long long)nzu);
+        int p = 52 * m + (63 - __clzll((long long)su[m]));         // leading bit of |A|
+        msb = p - 1074;
+        int sh = p - (prec - 1) > emin ? p - (prec - 1) : emin;
+        uint64_t q = extract_bits(su, sh, prec + 1);
+        int g = sh > 0 ? (int)extract_bits(su, sh - 1, 1) : 0;
+        bool sticky = false;                                        // any bit below the guard bit
+        if (sh > 1) {
+            int pos = sh - 1, jg = pos / 52, off = pos - 52 * jg;
+            sticky = (nzu & ((1ull << jg) - 1)) != 0;
+            if (off) sticky = sticky || ((uint64_t)su[jg] & ((1ull << off) - 1));
+        }
+        int up = g && (sticky || (q & 1));
+        if (g || sticky) dir = up ? 1 : -1;
+        q += (uint64_t)up;
+        if (sh == emin) {
+            bits = q;                             // subnormal / smallest normals: bits = q
+        } else {
+            if (q == (1ull << prec)) { q >>= 1; sh += 1; }
+            int Eb = sh - emin + 1;
+            if (Eb >= emax) { bits = (uint64_t)emax << (prec - 1); rf |= is64 ? XSUM_F_OVERFLOW : XSUM_F_OVERFLOW32; dir = 1; }
+            else bits = ((uint64_t)Eb << (prec - 1)) | (q - (1ull << (prec - 1)));
+        }
+        q_out = q;
+        sh_out = sh;
+        if (dir) rf |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
+        if (sign) { bits |= is64 ? (1ull << 63) : 0x80000000ull; dir = -dir; }   // -0.0f possible (R18)
+    }
+    const uint64_t b32 = __shfl_sync(FULL, bits, 1);
+    const uint32_t rf32 = __shfl_sync(FULL, rf, 1);
     if (lane == 0) {
         r.count = count;
-        uint32_t fl = flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
-        uint64_t bits = 0;
-        uint32_t b32 = 0;
-        int dir = 0;
-        // any bit of |A| below position pos (pos >= 0)?
-        auto any_below = [&](int pos) -> bool {
-            int jg = pos / 52;
-            bool st = (nzu & ((1ull << jg) - 1)) != 0;
-            int off = pos - 52 * jg;
-            if (off) st = st || ((uint64_t)su[jg] & ((1ull << off) - 1));
-            return st;
-        };
+        uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH)) | rf | rf32;
+        uint32_t v32 = (uint32_t)b32;
         if (!nzu) {                               // exact zero -> +0.0 (reading R9)
             r.msb_exp = INT32_MIN; r.sign = 0; r.sig53 = 0; r.exp2 = 0;
         } else {
-            int m = 63 - __clzll((long long)nzu);
-            int p = 52 * m + (63 - __clzll((long long)su[m]));     // leading bit of |A|
-            r.msb_exp = p - 1074;
+            r.msb_exp = msb;
             r.sign = sign;
-            if (p <= 52) {                        // |A| < 2^53: subnormal / smallest normals, exact
-                bits = extract_bits(su, 0, 53);
-                r.sig53 = bits; r.exp2 = -1074;
-            } else {
-                int sh = p - 52;
-                uint64_t q = extract_bits(su, sh, 53);
-                int g = (int)extract_bits(su, sh - 1, 1);
-                bool sticky = any_below(sh - 1);  // sticky: any bit below the guard bit
-                int up = g && (sticky || (q & 1));
-                if (g || sticky) dir = up ? 1 : -1;
-                q += (uint64_t)up;
-                if (q == (1ull << 53)) { q >>= 1; sh += 1; }
-                r.sig53 = q; r.exp2 = sh - 1074;
-                int Eb = sh + 1;
-                if (Eb >= 2047) { bits = 0x7FFull << 52; fl |= XSUM_F_OVERFLOW; dir = 1; }
-                else bits = ((uint64_t)Eb << 52) | (q - (1ull << 52));
-            }
-            if (dir) fl |= XSUM_F_INEXACT;
-            if (sign) { bits |= 1ull << 63; dir = -dir; }
-            // binary32 rounding of the same exact value (t = 23; least subnormal 2^-149 = bit 925)
-            {
-                int sh = p - 23 > 925 ? p - 23 : 925;
-                uint64_t q = extract_bits(su, sh, 25);
-                int g = (int)extract_bits(su, sh - 1, 1);
-                bool sticky = any_below(sh - 1);
-                int up = g && (sticky || (q & 1));
-                if (g || sticky) fl |= XSUM_F_INEXACT32;
-                q += (uint64_t)up;
-                if (sh == 925) {
-                    b32 = (uint32_t)q;            // subnormal / smallest normals: bits = q (q <= 2^24)
-                } else {
-                    if (q == (1ull << 24)) { q >>= 1; sh += 1; }
-                    int Eb = sh - 925 + 1;
-                    if (Eb >= 255) { b32 = 0x7F800000u; fl |= XSUM_F_OVERFLOW32 | XSUM_F_INEXACT32; }
-                    else b32 = ((uint32_t)Eb << 23) | (uint32_t)(q - (1ull << 23));
-                }
-                if (sign) b32 |= 0x80000000u;     // a negative sum that rounds to 0 gives -0.0f (R18)
-            }
+            r.sig53 = q_out;                      // unbounded-exponent rounding (before overflow)
+            r.exp2 = sh_out - 1074;
         }
-        if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) b32 = 0x7FC00000u;
-        else if (fl & XSUM_F_PINF) b32 = 0x7F800000u;
-        else if (fl & XSUM_F_NINF) b32 = 0xFF800000u;
-        r.value_f32 = b32;
-        if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) { bits = 0x7FF8000000000000ull; dir = 0; }
-        else if (fl & XSUM_F_PINF) { bits = 0x7FF0000000000000ull; dir = 0; }
-        else if (fl & XSUM_F_NINF) { bits = 0xFFF0000000000000ull; dir = 0; }
+        if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
+            bits = 0x7FF8000000000000ull; dir = 0; v32 = 0x7FC00000u;
+        } else if (fl & XSUM_F_PINF) {
+            bits = 0x7FF0000000000000ull; dir = 0; v32 = 0x7F800000u;
+        } else if (fl & XSUM_F_NINF) {
+            bits = 0xFFF0000000000000ull; dir = 0; v32 = 0xFF800000u;
+        }
         r.value = __longlong_as_double((long long)bits);
+        r.value_f32 = v32;
         r.direction = dir;
         r.flags = fl;
     }

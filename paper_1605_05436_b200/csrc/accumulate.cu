@@ -17,7 +17,7 @@
 
 namespace xs {
 
-template <int WARPS, int U, typename E>
+template <int WARPS, int U, int NB, typename E>
 struct AccCfg {
     static constexpr int T = WARPS * 32;
     static constexpr int FLUSH_TILES = FLUSH_ELEMS / (Elem<E>::PER_VEC * U);
@@ -44,10 +44,10 @@ __device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint
     }
 }
 
-template <int WARPS, int U, typename E>
+template <int WARPS, int U, int NB, typename E>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
-    using C = AccCfg<WARPS, U, E>;
+    using C = AccCfg<WARPS, U, NB, E>;
     using EL = Elem<E>;
     constexpr int PV = EL::PER_VEC;
     constexpr int T = C::T;
@@ -107,23 +107,23 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
             any_tile = false;
         }
     };
-    uint4 A[U], B[U], Cb[U];
+    // NB register buffers of U vectors rotate without moves (the unrolled b loop indexes them
+    // statically): while one tile is decoded the next NB-1 are in flight.
+    uint4 buf[NB][U];
     uint64_t t = blockIdx.x;
-    load_tile(A, t);
-    load_tile(B, t + G);
-    load_tile(Cb, t + 2 * G);
-    while (t < ntiles) {
-        do_tile(A, t);
-        load_tile(A, t + 3 * G);
-        t += G;
-        if (t >= ntiles) break;
-        do_tile(B, t);
-        load_tile(B, t + 3 * G);
-        t += G;
-        if (t >= ntiles) break;
-        do_tile(Cb, t);
-        load_tile(Cb, t + 3 * G);
-        t += G;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) load_tile(buf[b], t + (uint64_t)b * G);
+    bool more = t < ntiles;
+    while (more) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (more) {
+                do_tile(buf[b], t);
+                load_tile(buf[b], t + (uint64_t)NB * G);
+                t += G;
+                more = t < ntiles;
+            }
+        }
     }
 
     // leftover vectors (< one tile), the unaligned head and the tail elements: checked adds by
@@ -219,12 +219,12 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     }
 }
 
-template <int WARPS, int U, typename E>
+template <int WARPS, int U, int NB, typename E>
 static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    using C = AccCfg<WARPS, U, E>;
+    using C = AccCfg<WARPS, U, NB, E>;
     static bool attr_set = false;   // per process; the attribute is per function and device-independent
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_accumulate<WARPS, U, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_accumulate<WARPS, U, NB, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)C::SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -235,7 +235,7 @@ static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p,
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    k_accumulate<WARPS, U, E><<<(unsigned)g, C::T, C::SMEM, s>>>(x, n, p);
+    k_accumulate<WARPS, U, NB, E><<<(unsigned)g, C::T, C::SMEM, s>>>(x, n, p);
     note_launch();
     return cudaGetLastError();
 }
@@ -244,15 +244,18 @@ static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p,
 #define XS_ACC_WARPS 16   // 16 warps x 42 digits x 32 lanes x 8 B = 168 KiB of lane columns per SM
 #endif
 #ifndef XS_ACC_U
-#define XS_ACC_U 4        // 16-B vectors per thread per tile, three tiles in flight (registers)
+#define XS_ACC_U 4        // 16-B vectors per thread per tile
 #endif
+#ifndef XS_ACC_NB
+#define XS_ACC_NB 5       // rotating register buffers (NB-1 tiles in flight); tools/variants.py:
+#endif                    // c2 671 (NB=3), 708 (4), 715 G/s (5) at U=4
 
 cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, double>(x, n, p, num_sms, s);
+    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, XS_ACC_NB, double>(x, n, p, num_sms, s);
 }
 
 cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, float>(x, n, p, num_sms, s);
+    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, XS_ACC_NB, float>(x, n, p, num_sms, s);
 }
 
 }  // namespace xs

@@ -160,6 +160,10 @@ __device__ __noinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* 
 // across its segments, prefetched three tiles ahead with rotating register buffers, so the
 // per-segment epilogue runs while the next segment's first loads are already in flight.
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
+#ifndef XS_SEG_NB
+#define XS_SEG_NB 5
+#endif
+constexpr int SEG_NB = XS_SEG_NB;               // rotating register buffers (SEG_NB-1 tiles in flight)
 
 __device__ __noinline__ void seg_rescan_uniform(int64_t* col, const uint4* seg, uint32_t t0, uint32_t t1,
                                                    int lane, uint32_t& flags, uint32_t one) {
@@ -252,19 +256,17 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
             ++pt;
         }
     };
-    uint4 A[SEG_U], B[SEG_U], Cb[SEG_U];
-    load_next(A);
-    load_next(B);
-    load_next(Cb);
+    uint4 buf[SEG_NB][SEG_U];
+#pragma unroll
+    for (int b = 0; b < SEG_NB; ++b) load_next(buf[b]);
     while (ps < nseg) {
-        do_tile(A);
-        load_next(A);
-        if (ps >= nseg) break;
-        do_tile(B);
-        load_next(B);
-        if (ps >= nseg) break;
-        do_tile(Cb);
-        load_next(Cb);
+#pragma unroll
+        for (int b = 0; b < SEG_NB; ++b) {
+            if (ps < nseg) {
+                do_tile(buf[b]);
+                load_next(buf[b]);
+            }
+        }
     }
 }
 

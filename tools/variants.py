@@ -15,14 +15,13 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
-    "product": [],
-    "dec0_alu": ["-DXS_DECODE=0"],
-    "dec2_hybrid": ["-DXS_DECODE=2"],
-    "dec4_balanced": ["-DXS_DECODE=4"],
-    "nosmem_diag": ["-DXS_EXPERIMENT=1"],
-    "load_cg": ["-DXS_LOAD=1"],
-    "warps12": ["-DXS_ACC_WARPS=12"],
-    "u2": ["-DXS_ACC_U=2"],
+    "u4nb3": [],
+    "u4nb4": ["-DXS_ACC_U=4", "-DXS_ACC_NB=4"],
+    "u4nb5": ["-DXS_ACC_U=4", "-DXS_ACC_NB=5"],
+    "u5nb4": ["-DXS_ACC_U=5", "-DXS_ACC_NB=4"],
+    "u6nb3": ["-DXS_ACC_U=6", "-DXS_ACC_NB=3"],
+    "u3nb5": ["-DXS_ACC_U=3", "-DXS_ACC_NB=5"],
+    "u8nb2": ["-DXS_ACC_U=8", "-DXS_ACC_NB=2"],
 }
 
 

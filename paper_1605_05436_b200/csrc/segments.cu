@@ -161,7 +161,7 @@ __device__ __noinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* 
 // per-segment epilogue runs while the next segment's first loads are already in flight.
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
 #ifndef XS_SEG_NB
-#define XS_SEG_NB 5
+#define XS_SEG_NB 3   // tools/variants.py, c5: NB=3 476, NB=4 466, NB=5 415 G/s
 #endif
 constexpr int SEG_NB = XS_SEG_NB;               // rotating register buffers (SEG_NB-1 tiles in flight)
 

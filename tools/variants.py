@@ -15,13 +15,9 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
-    "u4nb3": [],
-    "u4nb4": ["-DXS_ACC_U=4", "-DXS_ACC_NB=4"],
-    "u4nb5": ["-DXS_ACC_U=4", "-DXS_ACC_NB=5"],
-    "u5nb4": ["-DXS_ACC_U=5", "-DXS_ACC_NB=4"],
-    "u6nb3": ["-DXS_ACC_U=6", "-DXS_ACC_NB=3"],
-    "u3nb5": ["-DXS_ACC_U=3", "-DXS_ACC_NB=5"],
-    "u8nb2": ["-DXS_ACC_U=8", "-DXS_ACC_NB=2"],
+    "product": [],
+    "seg_nb3": ["-DXS_SEG_NB=3"],
+    "seg_nb4": ["-DXS_SEG_NB=4"],
 }
 
 
@@ -43,8 +39,15 @@ import os, sys, json, statistics
 sys.path.insert(0, {ROOT!r})
 os.environ['XSUM_LIBRARY'] = {so!r}
 import torch, synth, paper_1605_05436_b200 as xsum
-x = synth.device_generate({cfg!r})
+x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = xsum.Accumulator()
+if {cfg!r}.endswith("seg"):
+    class _S:
+        def sum(self, x):
+            v, _, _ = xsum.sum_segments(x, 4096)
+            return xsum_res, None
+    xsum_res = acc.sum(x)[0]
+    acc = _S()
 for _ in range(5): acc.sum(x)
 torch.cuda.synchronize()
 ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range({steps})]

@@ -139,31 +139,26 @@ def profiled_traffic(cfg_name: str):
 # ------------------------------------------------------------------------------------------
 # CPU oracle arm (cpu_baseline and --impl reference)
 # ------------------------------------------------------------------------------------------
-def oracle_rate(cfg_name: str, target_s: float = 3.0, max_n: int = 1 << 27):
-    """Time the oracle (as it stands) on a bounded prefix of the workload on all host cores."""
-    import numpy as np
-
+def oracle_rate(cfg_name: str, target_s: float = 1.5, max_n: int = 1 << 28):
+    """Time the oracle (as it stands) on a bounded prefix of the workload on all host cores:
+    passes over the same sample until ~target_s seconds of wall time (x the host cores =
+    10-30 s of CPU work). Returns (doubles/s, cores, sample size, passes, seconds, config)."""
     import oracle
     import synth
     cores = oracle.host_threads()
     gen_name = "c2" if cfg_name in ("c1",) else cfg_name
-    m = 1 << 20
+    m = min(max_n, synth.CONFIGS[gen_name]["n"])
+    x = synth.host_generate(gen_name, 0, m)
+    oracle.exact_sum(x[: 1 << 16], nthreads=cores)          # load the library, warm the threads
+    passes, t0 = 0, time.perf_counter()
     while True:
-        x = synth.host_generate(gen_name, 0, m)
-        t0 = time.perf_counter()
         oracle.exact_sum(x, nthreads=cores)
+        passes += 1
         dt = time.perf_counter() - t0
-        if dt >= target_s / 4 or m >= max_n:
+        if dt >= target_s:
             break
-        m = min(max_n, m * 4)
-    if dt < target_s and m < max_n:   # final sample sized to ~target_s
-        m = int(min(max_n, m * target_s / max(dt, 1e-3)))
-        x = synth.host_generate(gen_name, 0, m)
-        t0 = time.perf_counter()
-        oracle.exact_sum(x, nthreads=cores)
-        dt = time.perf_counter() - t0
     del x
-    return m / dt, cores, m, dt, gen_name
+    return m * passes / dt, cores, m, passes, dt, gen_name
 
 
 def cpu_model() -> str:
@@ -185,7 +180,7 @@ def run_reference(args, rank: int, world: int):
     import synth
     wl = workload(args.config, world)
     cores = oracle.host_threads()
-    rate, _, _, _, gen_name = oracle_rate(args.config, target_s=1.0, max_n=1 << 24)
+    rate, _, _, _, _, gen_name = oracle_rate(args.config, target_s=0.5, max_n=1 << 24)
     budget = 90.0
     m = int(max(1 << 14, min(1 << 26, rate * budget / max(1, args.steps + args.warmup))))
     x = synth.host_generate(gen_name, 0, m)
@@ -305,10 +300,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, m, dt, gen_name = oracle_rate(args.config)
+        rate, cores, m, passes, dt, gen_name = oracle_rate(args.config)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{gen_name} elements [0, {m}) summed once by the oracle in {dt:.2f} s "
-                         f"on {cores} host threads ({cpu_model()})"}
+               "sample": f"{gen_name} elements [0, {m}) summed {passes}x by the oracle in {dt:.2f} s "
+                         f"on {cores} host threads = {dt * cores:.1f} CPU-s ({cpu_model()})"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,

@@ -248,9 +248,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         elif world == 1:
             acc.sum(x)                                   # one fused launch
         else:
-            acc.reset().add(x)
-            states = dist.gather_states(acc.state)
-            tot.reset().merge(states).finalize_async()
+            dist.exact_sum_distributed(x, acc, tot)     # 2 launches + one NCCL all-gather
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -314,7 +312,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "l2": "inputs 2 GiB+ per GPU > 126 MB L2 (no flush needed)",
                        "step": ("xsum_sum_segments" if seg else
                                 "xsum_sum fused launch" if world == 1 else
-                                "reset+accumulate, NCCL all-gather of 384-B states, merge, finalize")},
+                                "local xsum_sum, NCCL all-gather of 384-B states, xsum_merge_round")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
                          "kernel": "k_accumulate" if not seg else "k_segments",

@@ -160,6 +160,14 @@ XSUM_API xsum_status xsum_accumulate_host(xsum_ctx *h, const double *h_x, uint64
  * Errors: XSUM_EINVAL, XSUM_ECAPACITY, XSUM_ECUDA. */
 XSUM_API xsum_status xsum_merge(xsum_ctx *h, const void *d_states, uint32_t count, void *stream);
 
+/* Fused post-process ("reads back the p sparse superaccumulators ...
+ * add all of them into one ... converted to a correctly-rounded floating point value"):
+ * state := sum of the `count` images (Lemma-1 tree, as xsum_merge), then the rounding of
+ * xsum_finalize_round into d_res / d_canon, in ONE launch. Used after the all-gather of the
+ * per-GPU states. Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_merge_round(xsum_ctx *h, const void *d_states, uint32_t count, void *d_res,
+                                      uint64_t *d_canon, void *stream);
+
 /* Non-destructive rounding of the state: writes *d_res (device, 8-B aligned) and, if
  * d_canon != NULL, the canonical image (XSUM_CANON_LIMBS little-endian u64 limbs of the
  * two's complement integer A = exact_sum * 2^1074; the "non-overlapping" form of

@@ -38,7 +38,7 @@ OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_create", "xsum_reset",
            "xsum_accumulate", "xsum_accumulate_host", "xsum_merge", "xsum_finalize_round", "xsum_sum",
            "xsum_destroy", "xsum_count", "xsum_sum_segments", "xsum_sum_segments_csr", "xsum_status_str",
-           "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32")
+           "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round")
 
 
 class XsumError(RuntimeError):
@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
             "xsum_status_str": ([i32], ctypes.c_char_p), "xsum_launch_count": ([], u64),
             "xsum_set_grid_limit": ([p, u32], i32),
             "xsum_accumulate_f32": ([p, p, u64, p], i32), "xsum_sum_f32": ([p, p, u64, p, p, p], i32),
+            "xsum_merge_round": ([p, p, u32, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -252,6 +253,18 @@ class Accumulator:
         k = states.numel() // STATE_BYTES
         _check("xsum_merge", lib().xsum_merge(self._h, states.data_ptr(), k, _stream_ptr(self.device)))
         return self
+
+    def merge_round(self, states, canon: bool = False):
+        """state := sum of the packed state images, then round (one launch; xsum_merge_round).
+        Returns the device (result, canon) like finalize_async."""
+        torch = _torch()
+        if not (isinstance(states, torch.Tensor) and states.is_cuda and states.dtype == torch.uint8
+                and states.is_contiguous() and states.numel() % STATE_BYTES == 0):
+            raise TypeError("expected a contiguous uint8 CUDA tensor of k*384 bytes")
+        _check("xsum_merge_round", lib().xsum_merge_round(
+            self._h, states.data_ptr(), states.numel() // STATE_BYTES, self._res.data_ptr(),
+            self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
+        return self._res, (self._canon if canon else None)
 
     def finalize_async(self, canon: bool = False):
         """Enqueue the rounding; returns the (result bytes, canon limbs or None) device tensors."""

@@ -237,7 +237,20 @@ xsum_status xsum_merge(xsum_ctx* h, const void* d_states, uint32_t count, void* 
     if (!d_states || !aligned(d_states, 8)) return XSUM_EINVAL;
     DeviceGuard g(h->device);
     if (!g.ok) return XSUM_ECUDA;
-    if (xs::merge_states(h->state, d_states, count, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    if (xs::merge_states(h->state, d_states, count, 0, nullptr, nullptr, static_cast<cudaStream_t>(stream)) !=
+        cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+xsum_status xsum_merge_round(xsum_ctx* h, const void* d_states, uint32_t count, void* d_res, uint64_t* d_canon,
+                             void* stream) {
+    if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;
+    if (count && (!d_states || !aligned(d_states, 8))) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::merge_states(h->state, d_states, count, 1, static_cast<xsum_result*>(d_res), d_canon,
+                         static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
     return XSUM_OK;
 }

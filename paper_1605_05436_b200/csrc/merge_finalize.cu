@@ -40,7 +40,8 @@ __device__ __forceinline__ bool image_ok(const xsum_state_image* im, int64_t d0,
 constexpr int MERGE_WARPS = 16;
 
 __global__ void __launch_bounds__(MERGE_WARPS * 32)
-k_merge(xsum_state_image* st, const xsum_state_image* ims, uint32_t count) {
+k_merge(xsum_state_image* st, const xsum_state_image* ims, uint32_t count, int overwrite, xsum_result* res,
+        uint64_t* canon) {
     __shared__ int64_t acc[MERGE_WARPS][64];
     __shared__ uint64_t cnts[MERGE_WARPS];
     __shared__ uint32_t fls[MERGE_WARPS];
@@ -77,13 +78,30 @@ k_merge(xsum_state_image* st, const xsum_state_image* ims, uint32_t count) {
         __syncthreads();
     }
     if (warp == 0) {
-        int64_t s0 = st->digit[lane], s1 = (lane + 32 < D) ? st->digit[lane + 32] : 0;
-        lemma1_add(a0, a1, s0, s1, lane);
+        uint64_t cnt_all = cnts[0];
+        uint32_t fl_all = fls[0];
+        if (!overwrite) {
+            int64_t s0 = st->digit[lane], s1 = (lane + 32 < D) ? st->digit[lane + 32] : 0;
+            lemma1_add(a0, a1, s0, s1, lane);
+            cnt_all += st->count;
+            fl_all |= st->flags;
+        }
         st->digit[lane] = a0;
         if (lane + 32 < D) st->digit[lane + 32] = a1;
+        if (lane < (int)(sizeof(st->pad))) st->pad[lane] = 0;
         if (lane == 0) {
-            st->count += cnts[0];
-            st->flags |= fls[0];
+            st->magic = XSUM_MAGIC;
+            st->version = (uint16_t)XSUM_VERSION;
+            st->w = (uint8_t)W;
+            st->ndigits = (uint8_t)D;
+            st->reserved = 0;
+            st->count = cnt_all;
+            st->flags = fl_all;
+        }
+        if (res) {                                // fused post-process rounding
+            __shared__ int64_t su[64];
+            xsum_result r = finalize_warp(a0, a1, fl_all, cnt_all, canon, su, lane);
+            if (lane == 0) *res = r;
         }
     }
 }
@@ -103,8 +121,10 @@ cudaError_t init_state(xsum_state_image* st, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, cudaStream_t s) {
-    k_merge<<<1, MERGE_WARPS * 32, 0, s>>>(st, static_cast<const xsum_state_image*>(states), count);
+cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, int overwrite, xsum_result* res,
+                         uint64_t* canon, cudaStream_t s) {
+    k_merge<<<1, MERGE_WARPS * 32, 0, s>>>(st, static_cast<const xsum_state_image*>(states), count, overwrite, res,
+                                           canon);
     note_launch();
     return cudaGetLastError();
 }

@@ -44,3 +44,13 @@ def allreduce_exact(acc: Accumulator, group=None) -> Accumulator:
     acc.reset()
     acc.merge(states)
     return acc
+
+
+def exact_sum_distributed(x, acc: Accumulator, total: Accumulator, group=None):
+    """The whole multi-GPU step on this rank's shard x: local fused sum (one launch), NCCL
+    all-gather of the 384-byte states, fused merge + round (one launch). Returns the device
+    result record; every rank gets the identical bits."""
+    acc.sum(x)                                   # state := sum(x) (its local rounding is unused)
+    states = gather_states(acc.state, group)
+    res, _ = total.merge_round(states)
+    return res

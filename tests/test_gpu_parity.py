@@ -246,6 +246,30 @@ def test_merge_of_shard_states_equals_whole(xs):
         assert res.count == x.size
 
 
+def test_merge_round_is_the_fused_post_process(xs):
+    """xsum_merge_round: state := sum of the images (previous state discarded), rounded in the
+    same launch - the multi-GPU step's post-process after the all-gather."""
+    import torch
+    from paper_1605_05436_b200 import dist
+    x = synth.gen.generate("c4", 1 << 32, 3_000_017)
+    d = to_dev(x)
+    ref = oracle.exact_sum(x)
+    states = []
+    for r in range(8):
+        a, b = dist.shard_range(x.size, r, 8)
+        acc = xs.Accumulator()
+        acc.sum(d[a:b])                              # the local fused step each rank runs
+        states.append(acc.state.clone())
+    tot = xs.Accumulator().add(d[:1000])             # stale content must be discarded
+    n0 = xs.launch_count()
+    res, canon = tot.merge_round(torch.cat(states), canon=True)
+    assert xs.launch_count() - n0 == 1
+    assert_same(xs.Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64),
+                ref=ref, what="merge_round")
+    r2, c2 = tot.exact()                             # the state holds the merged sum
+    assert_same(r2, c2, ref=ref, what="merge_round state")
+
+
 def _image(digits, count=0, flags=0, magic=0x4D555358):
     from test_host_logic import encode_state
     img = encode_state(0, count, flags)

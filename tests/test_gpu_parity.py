@@ -484,3 +484,48 @@ def test_mixed_binary32_and_binary64_in_one_state(xs):
     res, canon = acc.exact()
     oa = oracle.Accumulator().add(a).add(b).add(-a[:1000])
     assert_same(res, canon, ref=(oa.result(), oa.limbs), what="mixed")
+
+
+def test_status_codes_on_device(xs):
+    """Argument errors are reported as status codes (never crashes), on a live device."""
+    import ctypes
+
+    import torch
+    L = xs.lib()
+    acc = xs.Accumulator()
+    d = torch.zeros(16, dtype=torch.float64, device="cuda")
+    f = torch.zeros(16, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.xsum_accumulate(acc.handle, d.data_ptr() + 4, 3, st) == xs.EINVAL       # not 8-B aligned
+    assert L.xsum_accumulate_f32(acc.handle, f.data_ptr() + 2, 3, st) == xs.EINVAL   # not 4-B aligned
+    assert L.xsum_accumulate(acc.handle, None, 3, st) == xs.EINVAL
+    assert L.xsum_accumulate(acc.handle, d.data_ptr(), 0, st) == xs.OK               # n = 0: no-op
+    assert L.xsum_merge(acc.handle, d.data_ptr() + 4, 1, st) == xs.EINVAL
+    assert L.xsum_finalize_round(acc.handle, None, None, st) == xs.EINVAL
+    assert L.xsum_accumulate(acc.handle, d.data_ptr(), 2 ** 63, st) == xs.ECAPACITY   # > 2^63-1 summands
+    h = ctypes.c_void_p()
+    small = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    assert L.xsum_create(ctypes.byref(h), 0, acc.state.data_ptr(), small.data_ptr(), 16, st) == xs.EINVAL
+    assert L.xsum_create(ctypes.byref(h), 99, acc.state.data_ptr(), acc.scratch.data_ptr(),
+                         acc.scratch.numel(), st) == xs.EINVAL
+    with pytest.raises(xs.XsumError):
+        acc.merge(torch.zeros(100, dtype=torch.uint8, device="cuda"))             # not k*384 bytes
+    torch.cuda.synchronize()
+    assert acc.result().count == 0 and acc.result().bits == 0                    # state untouched
+
+
+def test_many_state_images_merge(xs):
+    """A merge of thousands of states (the Lemma-1 leaf folds plus the warp tree)."""
+    import torch
+    x = synth.gen.generate("c4", 77, 2_000_000)
+    d = to_dev(x)
+    k = 2500
+    cuts = np.linspace(0, x.size, k + 1).astype(int)
+    states = torch.empty((k, 384), dtype=torch.uint8, device="cuda")
+    acc = xs.Accumulator()
+    for j in range(k):
+        acc.sum(d[cuts[j]:cuts[j + 1]])
+        states[j].copy_(acc.state)
+    res, canon = xs.Accumulator().merge(states.reshape(-1)).exact()
+    assert_same(res, canon, x, what="2500-way merge")
+    assert res.count == x.size

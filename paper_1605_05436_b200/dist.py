@@ -33,6 +33,12 @@ def gather_states(state, group=None):
     if state.dtype != torch.uint8 or state.numel() != STATE_BYTES:
         raise ValueError("state must be a uint8 tensor of 384 bytes")
     world = dist.get_world_size(group)
+    if dist.get_backend(group) == "gloo":
+        # host-staged exchange (CPU process groups; tests run several ranks on one GPU this way)
+        host = state.detach().to("cpu").contiguous()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        return torch.cat(parts).to(state.device)
     out = torch.empty(world * STATE_BYTES, dtype=torch.uint8, device=state.device)
     dist.all_gather_into_tensor(out, state.contiguous(), group=group)
     return out

@@ -508,7 +508,7 @@ def test_status_codes_on_device(xs):
     assert L.xsum_create(ctypes.byref(h), 0, acc.state.data_ptr(), small.data_ptr(), 16, st) == xs.EINVAL
     assert L.xsum_create(ctypes.byref(h), 99, acc.state.data_ptr(), acc.scratch.data_ptr(),
                          acc.scratch.numel(), st) == xs.EINVAL
-    with pytest.raises(xs.XsumError):
+    with pytest.raises((TypeError, xs.XsumError)):
         acc.merge(torch.zeros(100, dtype=torch.uint8, device="cuda"))             # not k*384 bytes
     torch.cuda.synchronize()
     assert acc.result().count == 0 and acc.result().bits == 0                    # state untouched

@@ -76,53 +76,50 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
 
     const uint32_t one = p.one, mone = p.mone;
     uint32_t nspec = 0;                 // NaN/Inf patterns summed unchecked in this window
-    int since = 0;
     uint64_t wstart = blockIdx.x, tlast = 0;
     bool any_tile = false;
-    // Three register buffers rotate without moves: while one tile is decoded the next two
-    // are in flight (3 x 64 B per thread = 96 KiB per SM), enough to cover loaded HBM
-    // latency (~1 us) at full bandwidth.
     auto load_tile = [&](uint4 (&buf)[U], uint64_t tt) {
         if (tt < ntiles) {
 #pragma unroll
             for (int u = 0; u < U; ++u) buf[u] = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
         }
     };
-    auto do_tile = [&](const uint4 (&buf)[U], uint64_t tt) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) EL::add_vec(col, buf[u], nspec, one, mone);
-        any_tile = true;
-        tlast = tt;
-        if (++since == C::FLUSH_TILES) {
-            regularize_column(col);
-            if (__any_sync(FULL, EL::hit(nspec))) {        // rare: cancel NaN/Inf patterns
-                if (EL::hit(nspec)) {
-                    rescan_window<U, T, E>(col, body, wstart, tt, G, TV, tid, flags, one);
-                    regularize_column(col);
-                }
-            }
-            nspec = 0;
-            since = 0;
-            wstart = tt + G;
-            any_tile = false;
-        }
-    };
     // NB register buffers of U vectors rotate without moves (the unrolled b loop indexes them
-    // statically): while one tile is decoded the next NB-1 are in flight.
+    // statically): while one tile is decoded the next NB-1 are in flight. The window check
+    // runs once per NB-tile group, outside the unrolled loop, and inlines the regularization:
+    // an out-of-line call here would have to save the in-flight buffers, i.e. wait for them.
+    constexpr int GROUPS_PER_WINDOW = C::FLUSH_TILES / NB;    // window = NB*GROUPS <= FLUSH_TILES tiles
     uint4 buf[NB][U];
     uint64_t t = blockIdx.x;
 #pragma unroll
     for (int b = 0; b < NB; ++b) load_tile(buf[b], t + (uint64_t)b * G);
     bool more = t < ntiles;
+    int groups = 0;
     while (more) {
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             if (more) {
-                do_tile(buf[b], t);
+#pragma unroll
+                for (int u = 0; u < U; ++u) EL::add_vec(col, buf[b][u], nspec, one, mone);
+                any_tile = true;
+                tlast = t;
                 load_tile(buf[b], t + (uint64_t)NB * G);
                 t += G;
                 more = t < ntiles;
             }
+        }
+        if (++groups == GROUPS_PER_WINDOW) {
+            regularize_column_inl(col);
+            if (__any_sync(FULL, EL::hit(nspec))) {        // rare: cancel NaN/Inf patterns
+                if (EL::hit(nspec)) {
+                    rescan_window<U, T, E>(col, body, wstart, tlast, G, TV, tid, flags, one);
+                    regularize_column(col);
+                }
+            }
+            nspec = 0;
+            groups = 0;
+            wstart = t;
+            any_tile = false;
         }
     }
 

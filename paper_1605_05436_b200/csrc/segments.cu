@@ -138,7 +138,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
 // difference of the raw lane sums at this segment end and at the previous one (exact
 // integer arithmetic; regularizations in between preserve every column's value, so the
 // digit-wise difference still represents exactly the value added by this segment).
-__device__ __noinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* su, uint32_t flags, uint64_t len,
+__device__ __forceinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* su, uint32_t flags, uint64_t len,
                                                     uint64_t s, double* out, uint64_t* canon, uint32_t* oflags,
                                                     LaneSums& prev, int lane) {
     __syncwarp();
@@ -161,7 +161,7 @@ __device__ __noinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* 
 // per-segment epilogue runs while the next segment's first loads are already in flight.
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
 #ifndef XS_SEG_NB
-#define XS_SEG_NB 3   // tools/variants.py, c5: NB=3 476, NB=4 466, NB=5 415 G/s
+#define XS_SEG_NB 4   // streaming path needs tiles-per-segment % NB == 0 (c5: 16 tiles)
 #endif
 constexpr int SEG_NB = XS_SEG_NB;               // rotating register buffers (SEG_NB-1 tiles in flight)
 
@@ -205,40 +205,40 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
     };
     uint64_t ps = gw;            // processing cursor: segment, tile
     uint32_t pt = 0, wstart = 0, flags = 0, nspec = 0;
-    int since = 0;
+    int groups = 0;
     LaneSums prev = {0, 0, 0, 0};                              // raw lane sums at the previous segment end
-    auto close_window = [&](uint32_t tlast) {
-        regularize_column(col);
-        if (__any_sync(FULL, spec_hit(nspec))) {
-            if (spec_hit(nspec)) {
-                seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, tlast, lane, flags, one);
-                regularize_column(col);
-            }
-        }
-        nspec = 0;
-        since = 0;
-        wstart = tlast + 1;
-    };
-    auto do_tile = [&](const uint4 (&buf)[SEG_U]) {
+    // TPS is a multiple of SEG_NB (dispatch condition): every NB-tile group lies inside one
+    // segment, so the segment end and the window check sit once, inlined, after the unrolled
+    // group (no out-of-line call while loads are in flight).
+    constexpr int GROUPS_PER_WINDOW = SEG_FLUSH_ITERS / SEG_NB;
+    uint4 buf[SEG_NB][SEG_U];
 #pragma unroll
-        for (int u = 0; u < SEG_U; ++u) {
-            Chunks a = decompose(buf[u].x, buf[u].y, one, mone);
-            nspec = spec_fold(nspec, a);
-            column_add(col, a, one);
-            Chunks b = decompose(buf[u].z, buf[u].w, one, mone);
-            nspec = spec_fold(nspec, b);
-            column_add(col, b, one);
+    for (int b = 0; b < SEG_NB; ++b) load_next(buf[b]);
+    while (ps < nseg) {
+#pragma unroll
+        for (int b = 0; b < SEG_NB; ++b) {
+#pragma unroll
+            for (int u = 0; u < SEG_U; ++u) {
+                Chunks a = decompose(buf[b][u].x, buf[b][u].y, one, mone);
+                nspec = spec_fold(nspec, a);
+                column_add(col, a, one);
+                Chunks c = decompose(buf[b][u].z, buf[b][u].w, one, mone);
+                nspec = spec_fold(nspec, c);
+                column_add(col, c, one);
+            }
+            load_next(buf[b]);
         }
-        ++since;
-        if (pt + 1 == TPS) {                                   // segment complete
+        pt += SEG_NB;
+        ++groups;
+        if (pt == TPS) {                                       // segment complete
             if (__any_sync(FULL, spec_hit(nspec))) {           // rare: cancel NaN/Inf patterns
                 if (spec_hit(nspec)) {
                     regularize_column(col);
-                    seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, pt, lane, flags, one);
+                    seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, pt - 1, lane, flags, one);
                     regularize_column(col);
                 }
                 nspec = 0;
-                since = 0;                                     // the window restarts (all lanes)
+                groups = 0;                                    // the window restarts (all lanes)
             }
             segment_epilogue_delta(win + warp * (D * 32), su[warp], flags, seg_len, ps, out, canon, oflags, prev,
                                    lane);
@@ -246,26 +246,18 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
             wstart = 0;                                        // window tiles of the next segment start at 0
             pt = 0;
             ps += nw;
-            if (since == SEG_FLUSH_ITERS) {                    // windows may span segments; no
-                regularize_column(col);                        // NaN/Inf is pending here (checked
-                nspec = 0;                                     // above), so no rescan is needed
-                since = 0;
-            }
-        } else {
-            if (since == SEG_FLUSH_ITERS) close_window(pt);
-            ++pt;
         }
-    };
-    uint4 buf[SEG_NB][SEG_U];
-#pragma unroll
-    for (int b = 0; b < SEG_NB; ++b) load_next(buf[b]);
-    while (ps < nseg) {
-#pragma unroll
-        for (int b = 0; b < SEG_NB; ++b) {
-            if (ps < nseg) {
-                do_tile(buf[b]);
-                load_next(buf[b]);
+        if (groups == GROUPS_PER_WINDOW) {                     // window close (may span segments)
+            regularize_column_inl(col);
+            if (__any_sync(FULL, spec_hit(nspec))) {           // pending only in the current segment
+                if (spec_hit(nspec)) {
+                    seg_rescan_uniform(col, xv + ps * seg_vecs, wstart, pt - 1, lane, flags, one);
+                    regularize_column(col);
+                }
             }
+            nspec = 0;
+            groups = 0;
+            wstart = pt;
         }
     }
 }
@@ -283,7 +275,7 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
     uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (84 KiB smem each)
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-    const bool uniform = !offsets && seg_len >= SEG_TILE && seg_len % SEG_TILE == 0 &&
+    const bool uniform = !offsets && seg_len >= SEG_TILE && seg_len % ((uint64_t)SEG_TILE * SEG_NB) == 0 &&
                          ((uintptr_t)x & 15) == 0 && seg_len / SEG_TILE < (1u << 31);
     if (uniform)
         k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, out, canon, flags, 1u, 0xFFFFFFFFu);

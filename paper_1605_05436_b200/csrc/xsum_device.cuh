@@ -366,6 +366,20 @@ template <> struct Elem<float> {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int64_t balanced_carry(int64_t y) { return (y + (R >> 1)) >> W; }
 
+__device__ __forceinline__ void regularize_column_inl(int64_t* col) {
+    int64_t cin = 0;
+#pragma unroll 6
+    for (int j = 0; j < D - 1; ++j) {
+        int64_t y = col[j * 32];
+        XS_ASSERT(y > -0x7FF0000000000000ll && y < 0x7FF0000000000000ll);   // headroom kept
+        int64_t c = balanced_carry(y);
+        col[j * 32] = y - (c << W) + cin;
+        cin = c;
+    }
+    col[(D - 1) * 32] += cin;
+}
+
+// Out-of-line copy for the rare paths (NaN/Inf compensation, leftovers).
 __device__ __noinline__ static void regularize_column(int64_t* col) {
     int64_t cin = 0;
 #pragma unroll 6

@@ -161,7 +161,7 @@ __device__ __forceinline__ void segment_epilogue_delta(const int64_t* wb, int64_
 // per-segment epilogue runs while the next segment's first loads are already in flight.
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
 #ifndef XS_SEG_NB
-#define XS_SEG_NB 4   // streaming path needs tiles-per-segment % NB == 0 (c5: 16 tiles)
+#define XS_SEG_NB 2   // streaming path needs tiles-per-segment % NB == 0; c5: NB=2 560, 4 550, 8 342 G/s
 #endif
 constexpr int SEG_NB = XS_SEG_NB;               // rotating register buffers (SEG_NB-1 tiles in flight)
 

@@ -134,34 +134,13 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
 }
 
 
-// Streaming-path epilogue: the lane columns are never zeroed; the segment's digits are the
-// difference of the raw lane sums at this segment end and at the previous one (exact
-// integer arithmetic; regularizations in between preserve every column's value, so the
-// digit-wise difference still represents exactly the value added by this segment).
-__device__ __forceinline__ void segment_epilogue_delta(const int64_t* wb, int64_t* su, uint32_t flags, uint64_t len,
-                                                    uint64_t s, double* out, uint64_t* canon, uint32_t* oflags,
-                                                    LaneSums& prev, int lane) {
-    __syncwarp();
-    LaneSums now = raw_lane_sums(wb, lane);
-    LaneSums d = {now.hs0 - prev.hs0, now.ls0 - prev.ls0, now.hs1 - prev.hs1, now.ls1 - prev.ls1};
-    prev = now;
-    int64_t a0, a1;
-    sums_to_digits(d, a0, a1, lane);
-    flags = __reduce_or_sync(FULL, flags);
-    xsum_result r = finalize_warp(a0, a1, flags, len, canon ? canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
-    if (lane == 0) {
-        out[s] = r.value;
-        if (oflags) oflags[s] = r.flags;
-    }
-}
-
 // Fast path for equal segments whose starts are 16-B aligned and whose length is a multiple
 // of one warp tile (256 doubles), e.g. config 5: a warp's tiles form one continuous stream
 // across its segments, prefetched three tiles ahead with rotating register buffers, so the
 // per-segment epilogue runs while the next segment's first loads are already in flight.
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
 #ifndef XS_SEG_NB
-#define XS_SEG_NB 2   // streaming path needs tiles-per-segment % NB == 0; c5: NB=2 560, 4 550, 8 342 G/s
+#define XS_SEG_NB 2   // streaming path needs tiles-per-segment % NB == 0; c5: NB=2 597, NB=4 585 G/s
 #endif
 constexpr int SEG_NB = XS_SEG_NB;               // rotating register buffers (SEG_NB-1 tiles in flight)
 
@@ -193,28 +172,36 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
 
-    uint64_t ls = gw;            // load cursor: segment, tile
+    // Load cursor: TPS is a multiple of SEG_NB (dispatch condition), so an NB-tile group never
+    // crosses a segment: one bounds check and one segment step per group, pointer increments
+    // only (no 64-bit multiplies on the hot path).
+    constexpr uint32_t TV = 32 * SEG_U;                        // vectors per warp tile
+    const uint64_t seg_skip = (nw - 1) * seg_vecs;             // from a segment's end to this warp's next
+    const uint4* lp = xv + gw * seg_vecs + lane;
+    uint64_t ls = gw;
     uint32_t lt = 0;
-    auto load_next = [&](uint4 (&buf)[SEG_U]) {
-        if (ls < nseg) {
-            const uint4* p = xv + ls * seg_vecs + (uint64_t)lt * (32 * SEG_U) + lane;
-#pragma unroll
-            for (int u = 0; u < SEG_U; ++u) buf[u] = ldg_stream(p + u * 32);
-            if (++lt == TPS) { lt = 0; ls += nw; }
-        }
+    auto advance_load = [&]() {
+        lp += SEG_NB * TV;
+        lt += SEG_NB;
+        if (lt == TPS) { lt = 0; ls += nw; lp += seg_skip; }
     };
     uint64_t ps = gw;            // processing cursor: segment, tile
     uint32_t pt = 0, wstart = 0, flags = 0, nspec = 0;
     int groups = 0;
-    LaneSums prev = {0, 0, 0, 0};                              // raw lane sums at the previous segment end
-    // TPS is a multiple of SEG_NB (dispatch condition): every NB-tile group lies inside one
-    // segment, so the segment end and the window check sit once, inlined, after the unrolled
-    // group (no out-of-line call while loads are in flight).
+    // The lane columns are never zeroed: a segment's digits are the difference of the raw lane
+    // sums at its end and at the previous segment's end (exact integer arithmetic; the
+    // regularizations in between preserve every column's value, so the digit-wise difference
+    // still represents exactly the value this segment added).
+    LaneSums prev = {0, 0, 0, 0};
     constexpr int GROUPS_PER_WINDOW = SEG_FLUSH_ITERS / SEG_NB;
     uint4 buf[SEG_NB][SEG_U];
 #pragma unroll
-    for (int b = 0; b < SEG_NB; ++b) load_next(buf[b]);
+    for (int b = 0; b < SEG_NB; ++b)
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) buf[b][u] = ldg_stream(lp + b * TV + u * 32);
+    advance_load();
     while (ps < nseg) {
+        const bool ld = ls < nseg;
 #pragma unroll
         for (int b = 0; b < SEG_NB; ++b) {
 #pragma unroll
@@ -226,8 +213,12 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
                 nspec = spec_fold(nspec, c);
                 column_add(col, c, one);
             }
-            load_next(buf[b]);
+            if (ld) {
+#pragma unroll
+                for (int u = 0; u < SEG_U; ++u) buf[b][u] = ldg_stream(lp + b * TV + u * 32);
+            }
         }
+        if (ld) advance_load();
         pt += SEG_NB;
         ++groups;
         if (pt == TPS) {                                       // segment complete
@@ -240,8 +231,21 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
                 nspec = 0;
                 groups = 0;                                    // the window restarts (all lanes)
             }
-            segment_epilogue_delta(win + warp * (D * 32), su[warp], flags, seg_len, ps, out, canon, oflags, prev,
-                                   lane);
+            // epilogue inline: an out-of-line call would wait for the in-flight buffers
+            const int64_t* wb = win + warp * (D * 32);
+            __syncwarp();
+            LaneSums now = raw_lane_sums(wb, lane);
+            LaneSums d = {now.hs0 - prev.hs0, now.ls0 - prev.ls0, now.hs1 - prev.hs1, now.ls1 - prev.ls1};
+            prev = now;
+            int64_t a0, a1;
+            sums_to_digits(d, a0, a1, lane);
+            const uint32_t fl = __reduce_or_sync(FULL, flags);
+            xsum_result r = finalize_warp_inl(a0, a1, fl, seg_len, canon ? canon + ps * XSUM_CANON_LIMBS : nullptr,
+                                              su[warp], lane);
+            if (lane == 0) {
+                out[ps] = r.value;
+                if (oflags) oflags[ps] = r.flags;
+            }
             flags = 0;
             wstart = 0;                                        // window tiles of the next segment start at 0
             pt = 0;

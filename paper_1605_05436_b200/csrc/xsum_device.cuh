@@ -509,8 +509,8 @@ __device__ __forceinline__ uint64_t extract_bits(const int64_t* su, int pos, int
 
 // Returns the result record in lane 0 (other lanes: unspecified); writes the canonical
 // image (34 limbs) to `canon` if non-null.
-__device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1, uint32_t flags, uint64_t count,
-                                     uint64_t* canon, int64_t* su, int lane) {
+__device__ __forceinline__ xsum_result finalize_warp_inl(int64_t a0, int64_t a1, uint32_t flags, uint64_t count,
+                                                         uint64_t* canon, int64_t* su, int lane) {
     xsum_result r = {};
     const bool has1 = lane + 32 < D;
     uint64_t nz = (uint64_t)__ballot_sync(FULL, a0 != 0) | ((uint64_t)__ballot_sync(FULL, a1 != 0) << 32);
@@ -623,6 +623,12 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
     }
     __syncwarp();
     return r;
+}
+
+// Out-of-line copy for the latency-insensitive callers (grid merge, finalize kernels).
+__device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1, uint32_t flags, uint64_t count,
+                                                         uint64_t* canon, int64_t* su, int lane) {
+    return finalize_warp_inl(a0, a1, flags, count, canon, su, lane);
 }
 
 // 128-bit streaming load of two doubles as four 32-bit halves (no L1 allocation).

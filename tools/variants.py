@@ -16,10 +16,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "acc_nb4": ["-DXS_ACC_NB=4"],
-    "acc_nb6": ["-DXS_ACC_NB=6"],
-    "seg_nb2": ["-DXS_SEG_NB=2"],
-    "seg_nb8": ["-DXS_SEG_NB=8"],
+    "seg_nb4": ["-DXS_SEG_NB=4"],
 }
 
 

@@ -1,6 +1,6 @@
 """ORACLE - test infrastructure only.
 
-Plain CPU exact summation of binary64 (the oracle of DESIGN.md §3). Only
+Plain CPU exact summation of binary64 / binary32 / binary16 / bfloat16 (the oracle of DESIGN.md §3). Only
 ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 ``--impl reference`` legs may import this package. It shares no code with the
 CUDA path (``paper_1605_05436_b200``) and never imports it.
@@ -71,6 +71,8 @@ def _L():
         lib.oracle_sum.restype = None
         lib.oracle_sum_f32.argtypes = [p, p, p, u64, i32]
         lib.oracle_sum_f32.restype = None
+        lib.oracle_sum_h16.argtypes = [p, p, p, u64, i32, i32]
+        lib.oracle_sum_h16.restype = None
         lib.oracle_round.argtypes = [p, u32, u64, ctypes.POINTER(_CResult)]
         lib.oracle_round.restype = None
         lib.oracle_limbs_add.argtypes = [p, p]
@@ -99,9 +101,21 @@ class Accumulator:
     def flags(self) -> int:
         return int(self._flags.value)
 
-    def add(self, x: np.ndarray) -> "Accumulator":
-        """Add float64 (or float32, summed exactly as binary32) values."""
+    def add(self, x: np.ndarray, fmt: str | None = None) -> "Accumulator":
+        """Add float64 values (float32 arrays are summed exactly as binary32, float16 arrays as
+        binary16). 16-bit bit patterns (uint16 arrays) need fmt = "f16" or "bf16"."""
         x = np.asarray(x)
+        if x.dtype == np.float16 or fmt is not None:
+            if fmt is None:
+                fmt = "f16"
+            if fmt not in ("f16", "bf16"):
+                raise ValueError("fmt must be 'f16' or 'bf16'")
+            x = np.ascontiguousarray(x).view(np.uint16)
+            if x.size:
+                _L().oracle_sum_h16(self.limbs.ctypes.data, ctypes.addressof(self._flags), x.ctypes.data, x.size,
+                                    self.nthreads, 1 if fmt == "bf16" else 0)
+            self.count += int(x.size)
+            return self
         f32 = x.dtype == np.float32
         x = np.ascontiguousarray(x, dtype=np.float32 if f32 else np.float64)
         if x.size:
@@ -131,10 +145,14 @@ def round_limbs(limbs: np.ndarray, flags: int, count: int = 0) -> Result:
                   count=r.count, sig53=r.sig53, exp2=r.exp2, bits_f32=r.value_f32)
 
 
-def exact_sum(x, nthreads: int | None = None) -> tuple[Result, np.ndarray]:
+def exact_sum(x, nthreads: int | None = None, fmt: str | None = None) -> tuple[Result, np.ndarray]:
     """(rounded result, 34-limb two's complement image of sum(x)*2^1074); float32 arrays are
-    summed as binary32 values, anything else as float64."""
+    summed as binary32 values, float16 arrays as binary16, uint16 bit patterns per fmt
+    ("f16" / "bf16"), anything else as float64."""
     x = np.asarray(x)
+    if fmt is not None or x.dtype == np.float16:
+        acc = Accumulator(nthreads).add(x, fmt=fmt)
+        return acc.result(), acc.limbs.copy()
     acc = Accumulator(nthreads).add(x if x.dtype == np.float32 else np.asarray(x, dtype=np.float64))
     return acc.result(), acc.limbs.copy()
 

@@ -145,3 +145,27 @@ def round_int_f32(A: int, flags: int = 0) -> tuple[int, int]:
     if _f32_value(b) != mag:
         flags |= F_INEXACT32
     return sign | b, flags
+
+
+# 16-bit formats (binary16: t = 10, l = 5; bfloat16: t = 7, l = 8), the paper's t-bit fraction /
+# l-bit exponent format with the IEEE bias (R1). Python ints, one element at
+# a time: x = (-1)^s M 2^(max(e,1) - bias - t), A = x 2^1074.
+H16 = {"f16": (10, 5), "bf16": (7, 8)}
+
+
+def exact_int_h16(bit_patterns, fmt: str) -> tuple[int, int]:
+    """(A, flags) for 16-bit inputs given as uint16 bit patterns: A = sum * 2^1074."""
+    t, l = H16[fmt]
+    bias = (1 << (l - 1)) - 1
+    A = 0
+    flags = 0
+    for b in bit_patterns:
+        b = int(b)
+        s, e, m = b >> 15, (b >> t) & ((1 << l) - 1), b & ((1 << t) - 1)
+        if e == (1 << l) - 1:
+            flags |= F_NAN if m else (F_NINF if s else F_PINF)
+            continue
+        M = m if e == 0 else m + (1 << t)
+        v = M << (max(e, 1) - bias - t + 1074)
+        A += -v if s else v
+    return A, flags

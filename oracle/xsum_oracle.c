@@ -115,6 +115,39 @@ void oracle_accumulate_f32(uint64_t *P, uint64_t *N, uint32_t *flags, const floa
     }
 }
 
+/* 16-bit formats given as bit patterns: IEEE 754 binary16 (t = 10, l = 5) and bfloat16
+ * (t = 7, l = 8), the paper's general format of t fraction bits and an l-bit exponent
+ * (IEEE bias 2^(l-1)-1 per reading R1):
+ *   |x| = M 2^(k + 1 - bias - t), M = m + [e!=0] 2^t, k = max(e,1) - 1,
+ * i.e. M at bit position k + 1 - bias - t + 1074 in units of 2^-1074 (binary16: k + 1050,
+ * bfloat16: k + 941). The all-ones exponent field is NaN (m != 0) or +-Inf. */
+void oracle_accumulate_h16(uint64_t *P, uint64_t *N, uint32_t *flags, const uint16_t *x, uint64_t n,
+                           int t, int l) {
+    const uint32_t emask = (1u << l) - 1, mmask = (1u << t) - 1;
+    const int bias = (1 << (l - 1)) - 1;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t b = x[i];
+        uint32_t s = b >> 15;
+        uint32_t e = (b >> t) & emask;
+        uint32_t m = b & mmask;
+        if (e == emask) {
+            if (m) *flags |= OF_NAN;
+            else   *flags |= s ? OF_NINF : OF_PINF;
+            continue;
+        }
+        uint64_t M = m | ((e != 0) ? (1u << t) : 0);
+        if (M == 0) continue;
+        unsigned k = (unsigned)(((e != 0) ? (int)e - 1 : 0) + 1 - bias - t + 1074);
+        int L = (int)(k / 64);
+        unsigned sh = k % 64;
+        uint64_t lo = M << sh;
+        uint64_t hi = sh ? (M >> (64 - sh)) : 0;
+        uint64_t *T = s ? N : P;
+        limbs_add_u64(T, L, lo);
+        limbs_add_u64(T, L + 1, hi);
+    }
+}
+
 /* A += B (limbwise with carry). */
 void oracle_limbs_add(uint64_t *A, const uint64_t *B) {
     uint64_t c = 0;
@@ -142,32 +175,42 @@ void oracle_limbs_sub(uint64_t *A, const uint64_t *B) {
     }
 }
 
+/* input formats of sum_threads */
+#define FMT_F64 0
+#define FMT_F32 1
+#define FMT_F16 2   /* binary16 */
+#define FMT_BF16 3  /* bfloat16 */
+
 typedef struct {
     const void *x;
     uint64_t n;
-    int f32;
+    int fmt;
     uint64_t P[NLIMB], N[NLIMB];
     uint32_t flags;
 } part_t;
 
 static void *part_run(void *arg) {
     part_t *p = (part_t *)arg;
-    if (p->f32) oracle_accumulate_f32(p->P, p->N, &p->flags, (const float *)p->x, p->n);
-    else        oracle_accumulate(p->P, p->N, &p->flags, (const double *)p->x, p->n);
+    switch (p->fmt) {
+    case FMT_F32:  oracle_accumulate_f32(p->P, p->N, &p->flags, (const float *)p->x, p->n); break;
+    case FMT_F16:  oracle_accumulate_h16(p->P, p->N, &p->flags, (const uint16_t *)p->x, p->n, 10, 5); break;
+    case FMT_BF16: oracle_accumulate_h16(p->P, p->N, &p->flags, (const uint16_t *)p->x, p->n, 7, 8); break;
+    default:       oracle_accumulate(p->P, p->N, &p->flags, (const double *)p->x, p->n); break;
+    }
     return NULL;
 }
 
-static void sum_threads(uint64_t *A, uint32_t *flags, const void *x, uint64_t n, int nthreads, int f32) {
+static void sum_threads(uint64_t *A, uint32_t *flags, const void *x, uint64_t n, int nthreads, int fmt) {
     if (nthreads < 1) nthreads = 1;
     if ((uint64_t)nthreads > n / 65536 + 1) nthreads = (int)(n / 65536 + 1);
     part_t *parts = (part_t *)calloc((size_t)nthreads, sizeof(part_t));
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
     uint64_t per = n / (uint64_t)nthreads, rem = n % (uint64_t)nthreads, off = 0;
-    size_t esz = f32 ? 4 : 8;
+    size_t esz = fmt == FMT_F64 ? 8 : (fmt == FMT_F32 ? 4 : 2);
     for (int t = 0; t < nthreads; ++t) {
         parts[t].x = (const char *)x + off * esz;
         parts[t].n = per + ((uint64_t)t < rem ? 1 : 0);
-        parts[t].f32 = f32;
+        parts[t].fmt = fmt;
         off += parts[t].n;
         pthread_create(&th[t], NULL, part_run, &parts[t]);
     }
@@ -183,12 +226,17 @@ static void sum_threads(uint64_t *A, uint32_t *flags, const void *x, uint64_t n,
 /* Exact sum of x[0..n) ADDED TO (A, flags) (two's complement limbs), using nthreads host
  * threads over contiguous chunks. Callers zero A and flags for a fresh sum. */
 void oracle_sum(uint64_t *A, uint32_t *flags, const double *x, uint64_t n, int nthreads) {
-    sum_threads(A, flags, x, n, nthreads, 0);
+    sum_threads(A, flags, x, n, nthreads, FMT_F64);
 }
 
 /* Same for binary32 inputs. */
 void oracle_sum_f32(uint64_t *A, uint32_t *flags, const float *x, uint64_t n, int nthreads) {
-    sum_threads(A, flags, x, n, nthreads, 1);
+    sum_threads(A, flags, x, n, nthreads, FMT_F32);
+}
+
+/* Same for 16-bit bit patterns: bf16 = 0 -> binary16, bf16 = 1 -> bfloat16. */
+void oracle_sum_h16(uint64_t *A, uint32_t *flags, const uint16_t *x, uint64_t n, int nthreads, int bf16) {
+    sum_threads(A, flags, x, n, nthreads, bf16 ? FMT_BF16 : FMT_F16);
 }
 
 static int bitlen64(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return b; }

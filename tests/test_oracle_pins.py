@@ -405,3 +405,102 @@ def test_f32_sum_equals_numpy_when_exactly_representable():
         r, _ = oracle.exact_sum(x)
         expect = np.float32(int(x.astype(np.int64).sum()))
         assert r.bits_f32 == int(np.array([expect], dtype=np.float32).view(np.uint32)[0])
+
+
+# ------------------------------------------------------------------------------------------
+# 16-bit inputs (binary16 / bfloat16)
+# ------------------------------------------------------------------------------------------
+GOLDEN_H16 = os.path.join(os.path.dirname(__file__), "golden", "rounding_edges_h16.txt")
+
+
+def load_golden_h16():
+    cases = []
+    with open(GOLDEN_H16) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            name, fmt, ins, o64, o32, cite = [p.strip() for p in line.split("|")]
+            bits = np.array([int(h, 16) for h in ins.split(",")], dtype=np.uint16)
+            cases.append((name, fmt, bits, int(o64, 16), int(o32, 16), cite))
+    return cases
+
+
+H16_CASES = load_golden_h16()
+
+
+def h16_values(bits: np.ndarray, fmt: str) -> list:
+    """Library decoders, independent of the oracle: numpy's binary16, and bfloat16 as the top
+    half of a binary32 (its definition) decoded by numpy's float32."""
+    bits = np.ascontiguousarray(bits, dtype=np.uint16)
+    if fmt == "f16":
+        return [float(v) for v in bits.view(np.float16)]
+    return [float(v) for v in (bits.astype(np.uint32) << 16).view(np.float32)]
+
+
+@pytest.mark.parametrize("case", H16_CASES, ids=[c[0] for c in H16_CASES])
+def test_golden_h16(case):
+    name, fmt, bits, o64, o32, cite = case
+    assert re.search(r"PAPER\.md:\d+|\bR\d+\b", cite), name
+    r, _ = oracle.exact_sum(bits, fmt=fmt)
+    assert r.bits == o64, f"{name}: {r.bits:016x} != {o64:016x}"
+    assert r.bits_f32 == o32, f"{name}: {r.bits_f32:08x} != {o32:08x}"
+    # the hand-derived binary64 value agrees with the library decoders' exact sum
+    vals = h16_values(bits, fmt)
+    if all(math.isfinite(v) for v in vals):
+        assert b2f(o64) == float(exact_fraction(vals))
+
+
+def test_golden_h16_literals_mean_what_they_say():
+    assert h16_values(np.array([0x3C00, 0x0001, 0x7BFF, 0x0400, 0x03FF], np.uint16), "f16") == \
+        [1.0, 2.0 ** -24, 65504.0, 2.0 ** -14, 1023 * 2.0 ** -24]
+    assert h16_values(np.array([0x3F80, 0x0001, 0x3380, 0x7F7F], np.uint16), "bf16") == \
+        [1.0, 2.0 ** -133, 2.0 ** -24, (2 - 2.0 ** -7) * 2.0 ** 127]
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+def test_h16_random_patterns_vs_rationals(fmt):
+    # random bit patterns over the whole format (all exponents, subnormals, both signs; the
+    # specials are dropped here and covered by the golden cases)
+    rng = np.random.default_rng(16 if fmt == "f16" else 17)
+    emask = 0x7C00 if fmt == "f16" else 0x7F80
+    for trial in range(300):
+        n = int(rng.integers(1, 60))
+        bits = rng.integers(0, 1 << 16, size=n, dtype=np.uint32).astype(np.uint16)
+        bits = bits[(bits & emask) != emask]
+        vals = h16_values(bits, fmt)
+        S = exact_fraction(vals)
+        r, limbs = oracle.exact_sum(bits, fmt=fmt)
+        assert oracle.limbs_to_int(limbs) == S * (1 << 1074)
+        assert r.value == float(S) and (r.value != 0.0 or r.bits == 0)
+        # binary32 rounding vs the twin's independent rational search
+        b32, _ = pytwin.round_int_f32(int(S * (1 << 1074)))
+        assert r.bits_f32 == b32
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+def test_h16_o1_matches_o2_and_specials(fmt):
+    rng = np.random.default_rng(5)
+    bits = rng.integers(0, 1 << 16, size=20000, dtype=np.uint32).astype(np.uint16)
+    r, limbs = oracle.exact_sum(bits, fmt=fmt, nthreads=3)
+    A, flags = pytwin.exact_int_h16(bits, fmt)
+    assert oracle.limbs_to_int(limbs) == A
+    assert (r.flags & 7) == flags
+    # chunking / threading invariance and permutation invariance
+    r2, limbs2 = oracle.exact_sum(bits[::-1].copy(), fmt=fmt, nthreads=1)
+    assert (limbs2 == limbs).all() and r2.bits == r.bits
+
+
+def test_h16_all_binary16_finite_values_sum_to_zero():
+    # every finite binary16 appears with both signs: the exact sum is 0 (+0.0, R9), while the
+    # positive half alone is sum over e, m of the format's values (closed form below)
+    allb = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    fin = allb[(allb & 0x7C00) != 0x7C00]
+    r, limbs = oracle.exact_sum(fin, fmt="f16")
+    assert r.bits == 0 and not limbs.any()
+    pos = fin[fin < 0x8000]
+    # closed form: subnormals sum_{m<1024} m 2^-24 + normals sum_{e=1..30} sum_m (1024+m) 2^(e-25)
+    sub = Fraction(sum(range(1024)), 1 << 24)
+    nor = sum(Fraction(sum(range(1024, 2048)) * 2 ** e, 1 << 25) for e in range(1, 31))
+    _, lp = oracle.exact_sum(pos, fmt="f16")
+    assert oracle.limbs_to_int(lp) == (sub + nor) * (1 << 1074)

@@ -144,6 +144,21 @@ XSUM_API xsum_status xsum_accumulate_f32(xsum_ctx *h, const float *d_x, uint64_t
 XSUM_API xsum_status xsum_sum_f32(xsum_ctx *h, const float *d_x, uint64_t n, void *d_res, uint64_t *d_canon,
                                   void *stream);
 
+/* 16-bit inputs, given as bit patterns: state += sum of the IEEE binary16
+ * (t = 10, l = 5) or bfloat16 (t = 7, l = 8) values d_x[0..n) EXACTLY (the paper's t-bit fraction /
+ * l-bit exponent format; every such value is an integer multiple of 2^-24 resp.
+ * 2^-133, inside the 2^-1074 fixed-point window). d_x 2-byte aligned. NaN / +-Inf patterns set
+ * the sticky flags (R10). Results round to binary64 (value) and binary32 (value_f32).
+ * Errors: as xsum_accumulate. One launch per 2^40 summands. */
+XSUM_API xsum_status xsum_accumulate_f16(xsum_ctx *h, const uint16_t *d_x, uint64_t n, void *stream);
+XSUM_API xsum_status xsum_accumulate_bf16(xsum_ctx *h, const uint16_t *d_x, uint64_t n, void *stream);
+
+/* One-shot fused 16-bit paths (reset + accumulate + finalize; one launch for n < 2^40). */
+XSUM_API xsum_status xsum_sum_f16(xsum_ctx *h, const uint16_t *d_x, uint64_t n, void *d_res, uint64_t *d_canon,
+                                  void *stream);
+XSUM_API xsum_status xsum_sum_bf16(xsum_ctx *h, const uint16_t *d_x, uint64_t n, void *d_res, uint64_t *d_canon,
+                                   void *stream);
+
 /* State += sum of h_x[0..n) for a HOST buffer (pinned memory overlaps best): chunks are
  * copied into the caller's device staging buffer d_stage (two halves, double-buffered,
  * stage_bytes >= 2 MiB) and accumulated while the next chunk is in flight. This is the

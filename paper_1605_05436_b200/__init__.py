@@ -38,7 +38,8 @@ OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_create", "xsum_reset",
            "xsum_accumulate", "xsum_accumulate_host", "xsum_merge", "xsum_finalize_round", "xsum_sum",
            "xsum_destroy", "xsum_count", "xsum_sum_segments", "xsum_sum_segments_csr", "xsum_status_str",
-           "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round")
+           "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round",
+           "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16")
 
 
 class XsumError(RuntimeError):
@@ -77,6 +78,8 @@ def lib() -> ctypes.CDLL:
             "xsum_set_grid_limit": ([p, u32], i32),
             "xsum_accumulate_f32": ([p, p, u64, p], i32), "xsum_sum_f32": ([p, p, u64, p, p, p], i32),
             "xsum_merge_round": ([p, p, u32, p, p, p], i32),
+            "xsum_accumulate_f16": ([p, p, u64, p], i32), "xsum_accumulate_bf16": ([p, p, u64, p], i32),
+            "xsum_sum_f16": ([p, p, u64, p, p, p], i32), "xsum_sum_bf16": ([p, p, u64, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -152,8 +155,9 @@ def _as_f64_cuda(t, allow_f32: bool = False):
     torch = _torch()
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError("expected a CUDA tensor")
-    if t.dtype != torch.float64 and not (allow_f32 and t.dtype == torch.float32):
-        raise TypeError(f"expected float64{' or float32' if allow_f32 else ''}, got {t.dtype}")
+    ok = (torch.float64, torch.float32, torch.float16, torch.bfloat16) if allow_f32 else (torch.float64,)
+    if t.dtype not in ok:
+        raise TypeError(f"expected one of {ok}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
     return t
@@ -161,6 +165,15 @@ def _as_f64_cuda(t, allow_f32: bool = False):
 
 def _is_f32(t) -> bool:
     return t.dtype == _torch().float32
+
+
+# per input dtype: (accumulate entry point, fused sum entry point)
+_ENTRY = {"float64": ("xsum_accumulate", "xsum_sum"), "float32": ("xsum_accumulate_f32", "xsum_sum_f32"),
+          "float16": ("xsum_accumulate_f16", "xsum_sum_f16"), "bfloat16": ("xsum_accumulate_bf16", "xsum_sum_bf16")}
+
+
+def _entry(t, fused: bool) -> str:
+    return _ENTRY[str(t.dtype).replace("torch.", "")][1 if fused else 0]
 
 
 class Accumulator:
@@ -217,14 +230,10 @@ class Accumulator:
         return self
 
     def add(self, x) -> "Accumulator":
-        """Sum a float64 (binary64) or float32 (binary32) CUDA tensor into the state, exactly."""
+        """Sum a float64 / float32 / float16 / bfloat16 CUDA tensor into the state, exactly."""
         x = _as_f64_cuda(x, allow_f32=True)
-        if _is_f32(x):
-            _check("xsum_accumulate_f32", lib().xsum_accumulate_f32(self._h, x.data_ptr(), x.numel(),
-                                                                    _stream_ptr(self.device)))
-        else:
-            _check("xsum_accumulate", lib().xsum_accumulate(self._h, x.data_ptr(), x.numel(),
-                                                            _stream_ptr(self.device)))
+        name = _entry(x, fused=False)
+        _check(name, getattr(lib(), name)(self._h, x.data_ptr(), x.numel(), _stream_ptr(self.device)))
         return self
 
     def add_host(self, x, stage_bytes: int = 128 << 20) -> "Accumulator":
@@ -286,9 +295,9 @@ class Accumulator:
         """One-shot fused path (xsum_sum / xsum_sum_f32): state := sum(x); returns device
         (result, canon)."""
         x = _as_f64_cuda(x, allow_f32=True)
-        fn, name = (lib().xsum_sum_f32, "xsum_sum_f32") if _is_f32(x) else (lib().xsum_sum, "xsum_sum")
-        _check(name, fn(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
-                        self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
+        name = _entry(x, fused=True)
+        _check(name, getattr(lib(), name)(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
+                                          self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
         return self._res, (self._canon if canon else None)
 
 
@@ -305,7 +314,8 @@ def _acc_for(device) -> Accumulator:
 
 
 def exact_sum(x) -> tuple[Result, np.ndarray]:
-    """Exact sum of a float64 or float32 CUDA tensor: (rounded Result, canonical 34-limb image)."""
+    """Exact sum of a float64 / float32 / float16 / bfloat16 CUDA tensor: (rounded Result,
+    canonical 34-limb image)."""
     x = _as_f64_cuda(x, allow_f32=True)
     acc = _acc_for(x.device)
     res, canon = acc.sum(x, canon=True)
@@ -314,7 +324,8 @@ def exact_sum(x) -> tuple[Result, np.ndarray]:
 
 def fsum(x) -> float:
     """Correctly rounded (RN-even) sum of a float64 CUDA tensor (float32 tensors: the correctly
-    rounded binary32 of their exact sum, returned as a Python float)."""
+    rounded binary32 of their exact sum, returned as a Python float; float16 / bfloat16
+    tensors: the correctly rounded binary64 of their exact sum)."""
     x = _as_f64_cuda(x, allow_f32=True)
     res, _ = _acc_for(x.device).sum(x)
     r = Result.from_bytes(res.cpu().numpy().tobytes())

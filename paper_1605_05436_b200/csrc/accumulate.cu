@@ -12,6 +12,7 @@
 // finish, PAPER.md:768-776 bottom-up tree) and the result rounded.
 #include <cuda_runtime.h>
 
+#include "grid_tail.cuh"
 #include "xsum_device.cuh"
 #include "xsum_kernels.h"
 
@@ -23,12 +24,6 @@ struct AccCfg {
     static constexpr int FLUSH_TILES = FLUSH_ELEMS / (Elem<E>::PER_VEC * U);
     static constexpr size_t SMEM = (size_t)WARPS * D * 32 * sizeof(int64_t);
 };
-
-__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
 
 template <int U, int T, typename E>
 __device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint64_t t0, uint64_t t1,
@@ -156,64 +151,18 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     }
     __syncthreads();
 
-    // block: sum the warp partials (|.| <= WARPS*(2^51+2^16) < 2^56), regularize, publish.
+    // block: sum the warp partials (|.| <= WARPS*(2^51+2^16) < 2^56), regularize, publish;
+    // the last block merges the grid (grid_tail.cuh).
+    int64_t a0 = 0, a1 = 0;
     if (warp == 0) {
-        int64_t a0 = 0, a1 = 0;
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) {
             a0 += wsum[w][lane];
             if (lane + 32 < D) a1 += wsum[w][lane + 32];
         }
         regularize_warp(a0, a1, lane);
-        p.partial[(size_t)lane * XS_MAXB + blockIdx.x] = a0;
-        if (lane + 32 < D) p.partial[(size_t)(lane + 32) * XS_MAXB + blockIdx.x] = a1;
-        if (lane == 0) p.pflags[blockIdx.x] = blk_flags;
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) is_last = (atomicAdd(p.counter, 1u) == (unsigned)(G - 1));
     }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-
-    // grid: the last block merges the G block partials (digit-major, coalesced) and the
-    // handle state; G <= XS_MAXB so the raw sum stays below 2^62 before regularizing.
-    for (int j = warp; j < D; j += WARPS) {
-        int64_t s = 0;
-        for (uint64_t b = lane; b < G; b += 32) s += __ldcg(&p.partial[(size_t)j * XS_MAXB + b]);
-        s = warp_sum64(s);
-        if (lane == 0) wsum[0][j] = s;
-    }
-    if (warp == 1) {
-        uint32_t f = 0;
-        for (uint64_t b = lane; b < G; b += 32) f |= __ldcg(&p.pflags[b]);
-        f = __reduce_or_sync(FULL, f);
-        if (lane == 0) blk_flags = f;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        int64_t a0 = wsum[0][lane], a1 = (lane + 32 < D) ? wsum[0][lane + 32] : 0;
-        uint32_t fl = blk_flags;
-        uint64_t cnt = n;
-        if (!p.overwrite) {
-            a0 += p.state->digit[lane];
-            if (lane + 32 < D) a1 += p.state->digit[lane + 32];
-            fl |= p.state->flags;
-            cnt += p.state->count;
-        }
-        regularize_warp(a0, a1, lane);
-        p.state->digit[lane] = a0;
-        if (lane + 32 < D) p.state->digit[lane + 32] = a1;
-        if (lane == 0) {
-            p.state->flags = fl;
-            p.state->count = cnt;
-            *p.counter = 0;                      // ready for the next launch (stream order)
-        }
-        if (p.res) {
-            xsum_result r = finalize_warp(a0, a1, fl, cnt, p.canon, su, lane);
-            if (lane == 0) *p.res = r;
-        }
-    }
+    grid_tail<WARPS>(a0, a1, blk_flags, n, p, wsum[0], su, &blk_flags, &is_last, warp, lane);
 }
 
 template <int WARPS, int U, int NB, typename E>

@@ -1,0 +1,297 @@
+// K7: exact sums of 16-bit inputs, IEEE binary16 and bfloat16.
+//
+// The paper's format has a t-bit fraction and an l-bit exponent; binary16
+// is t = 10, l = 5 and bfloat16 t = 7, l = 8 (IEEE bias, reading R1). Every such value is
+// M 2^k in units of its least subnormal, M = m + [e!=0] 2^t < 2^(t+1), k = max(e,1) - 1.
+// With so few significand bits the superaccumulator's components can be much narrower than
+// the binary64 path's 52-bit digits (components are integers whose
+// exponents are multiples of a fixed width): each lane keeps unsigned 32-bit "bins", one per
+// (sign, exponent group) with groups of 2^SB consecutive exponents, and adds M 2^(k mod 2^SB)
+// into the bin of its group - one 32-bit add per summand, no carries, no sign handling. Every
+// FLUSH adds (before a bin can wrap) the bins are emptied into per-lane int64 bins; at the
+// end the block's bins are converted into the 52-bit digit window and merged up the same
+// grid tree as binary64 sums (grid_tail.cuh). NaN/Inf patterns fall into a
+// bin group of their own (exponent field all ones) that is never summed: a lane that sees it
+// non-empty at a window close rescans its window to classify NaN / +Inf / -Inf (reading R10).
+#include <cuda_runtime.h>
+
+#include "grid_tail.cuh"
+#include "xsum_device.cuh"
+#include "xsum_kernels.h"
+
+namespace xs {
+
+template <int T_, int L_, int SB_, int FLUSH_, int BASE_>
+struct H16Fmt {
+    static constexpr int t = T_;                          // fraction bits
+    static constexpr int l = L_;                          // exponent bits
+    static constexpr int SB = SB_;                        // exponent group = 2^SB consecutive exponents
+    // q = max(e,1) + 1 in [2, 2^l - 1] for finite values, 2^l for NaN/Inf: group g = q >> SB,
+    // offset o = q mod 2^SB; finite groups 0..NGF-1, the special group NGF.
+    static constexpr int NGF = ((1 << l) - 1) / (1 << SB) + 1;
+    static constexpr int NBIN = 2 * (NGF + 1);           // bin = 2 g + sign
+    static constexpr int NBIN64 = 2 * NGF;                // finite bins only
+    static constexpr int FLUSH = FLUSH_;                  // adds per window: FLUSH * max(M 2^o) < 2^32
+    static constexpr int BASE = BASE_;                    // window bit position of k = 0 (units 2^-1074)
+    // bin g holds sum M 2^o with M 2^k = (M 2^o) 2^(g 2^SB - 2): position BASE - 2 + g 2^SB
+    static constexpr int pos(int g) { return BASE - 2 + g * (1 << SB); }
+};
+// binary16: M <= 2047, o <= 7: 16383 * 2047 * 2^7 < 2^32.  bfloat16: M <= 255, o <= 15:
+// 511 * 255 * 2^15 < 2^32. Window bit positions: binary16 k + 1050, bfloat16 k + 941.
+using FmtF16 = H16Fmt<10, 5, 3, 16383, 1050>;
+using FmtBF16 = H16Fmt<7, 8, 4, 511, 941>;
+
+constexpr int H16_WARPS = 16;
+constexpr int H16_U = 4;          // 16-B vectors per thread per tile (8 summands each)
+#ifndef XS_H16_NB
+#define XS_H16_NB 4
+#endif
+constexpr int H16_NB = XS_H16_NB; // rotating register buffers (NB-1 tiles in flight)
+
+// One summand: h = |x| bit pattern (15 bits), s = sign bit; bins = this lane's bin column
+// (bin b at word b*32).
+template <class F>
+__device__ __forceinline__ void h16_add(uint32_t* bins, uint32_t h, uint32_t s) {
+    const uint32_t q = max((h >> F::t) + 1u, 2u);                          // max(e,1) + 1
+    const uint32_t M = (h + (2u << F::t)) - q * (1u << F::t);              // m + [e!=0] 2^t
+    const uint32_t o = q & ((1u << F::SB) - 1u);
+    const uint32_t b = ((q >> F::SB) << 1) | s;
+    XS_ASSERT(b < (uint32_t)F::NBIN);
+#ifdef XS_H16_RED
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bins + b * 32u)),
+                 "r"(M << o) : "memory");
+#else
+    bins[b * 32u] += M << o;
+#endif
+}
+
+// the two summands of a 32-bit word (little-endian: element 2i in the low half)
+template <class F>
+__device__ __forceinline__ void h16_add_word(uint32_t* bins, uint32_t w) {
+    h16_add<F>(bins, w & 0x7FFFu, (w >> 15) & 1u);
+    h16_add<F>(bins, (w >> 16) & 0x7FFFu, w >> 31);
+}
+
+template <class F>
+__device__ __forceinline__ uint32_t h16_special_flags(uint32_t b16) {
+    if (((b16 >> F::t) & ((1u << F::l) - 1u)) != (1u << F::l) - 1u) return 0;
+    if (b16 & ((1u << F::t) - 1u)) return XSUM_F_NAN;
+    return (b16 >> 15) ? XSUM_F_NINF : XSUM_F_PINF;
+}
+
+template <class F>
+__device__ __noinline__ void h16_rescan(const uint4* body, uint64_t t0, uint64_t t1, uint64_t G, uint64_t TV, int tid,
+                                        uint32_t& flags) {
+    // rare path: classify the NaN/Inf patterns of this lane's window (they were binned into
+    // the special group, which is never summed)
+    for (uint64_t tt = t0; tt <= t1; tt += G) {
+        for (int u = 0; u < H16_U; ++u) {
+            uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * (H16_WARPS * 32) + tid);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            for (int i = 0; i < 4; ++i) flags |= h16_special_flags<F>(w[i] & 0xFFFFu) | h16_special_flags<F>(w[i] >> 16);
+        }
+    }
+}
+
+// Empty the 32-bit bins into the int64 bins (finite groups) and clear the special group;
+// returns true if this lane's special group was non-empty.
+template <class F>
+__device__ __forceinline__ bool h16_flush(uint32_t* bins, int64_t* bins64) {
+#pragma unroll
+    for (int b = 0; b < F::NBIN64; ++b) {
+        bins64[b * 32] += (int64_t)bins[b * 32];
+        bins[b * 32] = 0;
+    }
+    const uint32_t sp = bins[F::NBIN64 * 32] | bins[(F::NBIN64 + 1) * 32];
+    bins[F::NBIN64 * 32] = 0;
+    bins[(F::NBIN64 + 1) * 32] = 0;
+    return sp != 0;
+}
+
+// Checked single summand (head / tail / leftovers): specials are flagged, not binned.
+template <class F>
+__device__ __forceinline__ void h16_add_checked(uint32_t* bins, uint32_t b16, uint32_t& flags) {
+    const uint32_t f = h16_special_flags<F>(b16);
+    if (f) { flags |= f; return; }
+    h16_add<F>(bins, b16 & 0x7FFFu, b16 >> 15);
+}
+
+template <class F>
+__global__ void __launch_bounds__(H16_WARPS * 32, 1)
+k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
+    constexpr int T = H16_WARPS * 32;
+    constexpr int PV = 8;                                   // summands per 16-B vector
+    constexpr int FLUSH_TILES = F::FLUSH / (PV * H16_U);    // tiles per bin window
+    constexpr int GROUPS_PER_WINDOW = FLUSH_TILES / H16_NB;
+    static_assert(GROUPS_PER_WINDOW >= 1, "window shorter than one buffer group");
+    // per lane: NBIN u32 bins, NBIN64 int64 bins (thread-minor, conflict-free)
+    extern __shared__ __align__(16) int64_t smem64[];
+    int64_t* const bins64_all = smem64;                                       // [WARPS][NBIN64][32]
+    uint32_t* const bins_all = reinterpret_cast<uint32_t*>(smem64 + H16_WARPS * F::NBIN64 * 32);
+    __shared__ int64_t wsum[H16_WARPS][F::NBIN64];
+    __shared__ int64_t digits[64];
+    __shared__ int64_t su[64];
+    __shared__ uint32_t blk_flags;
+    __shared__ int is_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t* bins = bins_all + warp * (F::NBIN * 32) + lane;
+    int64_t* bins64 = bins64_all + warp * (F::NBIN64 * 32) + lane;
+#pragma unroll
+    for (int b = 0; b < F::NBIN; ++b) bins[b * 32] = 0;
+#pragma unroll
+    for (int b = 0; b < F::NBIN64; ++b) bins64[b * 32] = 0;
+    if (tid < 64) digits[tid] = 0;
+    if (tid == 0) blk_flags = 0;
+    uint32_t flags = 0;
+
+    // peel up to 7 head elements to reach 16-B alignment; <= 7 tail elements remain
+    uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 2;
+    if (head > n) head = n;
+    const uint64_t nbody = n - head;
+    const uint64_t nvec = nbody / PV;
+    const uint4* body = reinterpret_cast<const uint4*>(x + head);
+    const uint64_t TV = (uint64_t)T * H16_U;
+    const uint64_t ntiles = nvec / TV;
+    const uint64_t G = gridDim.x;
+
+    uint64_t wstart = blockIdx.x, tlast = 0;
+    bool any_tile = false;
+    auto load_tile = [&](uint4 (&buf)[H16_U], uint64_t tt) {
+        if (tt < ntiles) {
+#pragma unroll
+            for (int u = 0; u < H16_U; ++u) buf[u] = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
+        }
+    };
+    uint4 buf[H16_NB][H16_U];
+    uint64_t t = blockIdx.x;
+#pragma unroll
+    for (int b = 0; b < H16_NB; ++b) load_tile(buf[b], t + (uint64_t)b * G);
+    bool more = t < ntiles;
+    int groups = 0;
+    while (more) {
+#pragma unroll
+        for (int b = 0; b < H16_NB; ++b) {
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < H16_U; ++u) {
+                    h16_add_word<F>(bins, buf[b][u].x);
+                    h16_add_word<F>(bins, buf[b][u].y);
+                    h16_add_word<F>(bins, buf[b][u].z);
+                    h16_add_word<F>(bins, buf[b][u].w);
+                }
+                any_tile = true;
+                tlast = t;
+                load_tile(buf[b], t + (uint64_t)H16_NB * G);
+                t += G;
+                more = t < ntiles;
+            }
+        }
+        if (++groups == GROUPS_PER_WINDOW) {
+#ifdef XS_H16_RED
+            __syncwarp();
+#endif
+            if (h16_flush<F>(bins, bins64)) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
+            groups = 0;
+            wstart = t;
+            any_tile = false;
+        }
+    }
+#ifdef XS_H16_RED
+    __syncwarp();
+#endif
+    if (h16_flush<F>(bins, bins64) && any_tile) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
+
+    // leftover vectors (< one tile), the unaligned head and the tail: checked adds by the block
+    // that would own the next tile (<= 4 vectors + 1 element per thread: no bin can wrap)
+    if (blockIdx.x == ntiles % G) {
+        const uint64_t v0 = ntiles * TV;
+        for (int u = 0; u < H16_U; ++u) {
+            uint64_t v = v0 + (uint64_t)u * T + tid;
+            if (v < nvec) {
+                uint4 q = ldg_stream(body + v);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                for (int i = 0; i < 4; ++i) {
+                    h16_add_checked<F>(bins, w[i] & 0xFFFFu, flags);
+                    h16_add_checked<F>(bins, w[i] >> 16, flags);
+                }
+            }
+        }
+        const uint64_t tail = nbody - nvec * PV;
+        if ((uint64_t)tid < head) h16_add_checked<F>(bins, __ldg(x + tid), flags);
+        if (tid >= 8 && (uint64_t)(tid - 8) < tail) h16_add_checked<F>(bins, __ldg(x + head + nvec * PV + (tid - 8)), flags);
+    }
+#ifdef XS_H16_RED
+    __syncwarp();
+#endif
+    h16_flush<F>(bins, bins64);
+    __syncwarp();
+
+    // warp: lane b sums bin b over the 32 lanes (rotated reads: conflict-free); block: warp 0
+    // sums the warps. Per-lane int64 bins hold < 2^(32 + 24) for launches of < 2^40 summands
+    // (api.cu splits longer ones), so the block totals stay below 2^63.
+    {
+        const int64_t* wb = bins64_all + warp * (F::NBIN64 * 32);
+        for (int b = lane; b < F::NBIN64; b += 32) {
+            int64_t s = 0;
+#pragma unroll 8
+            for (int c = 0; c < 32; ++c) s += wb[b * 32 + ((c + b) & 31)];
+            wsum[warp][b] = s;
+        }
+        uint32_t f = __reduce_or_sync(FULL, flags);
+        if (lane == 0 && f) atomicOr(&blk_flags, f);
+    }
+    __syncthreads();
+    // block bins -> 52-bit digits: bin (g, sign) is worth +-T 2^pos(g); split into the <= 3
+    // digits it overlaps and add them (shared int64 adds, once per bin per block)
+    if (warp == 0) {
+        for (int b = lane; b < F::NBIN64; b += 32) {
+            int64_t T = 0;
+            for (int w = 0; w < H16_WARPS; ++w) T += wsum[w][b];
+            const int P = F::pos(b >> 1);
+            const int i = P / W, o = P - W * (P / W);
+            const uint64_t u = (uint64_t)T;                         // T >= 0
+            const int64_t c0 = (int64_t)((u << o) & MASK);                  // bits [0, 52) of u 2^o
+            const int64_t c1 = (int64_t)((u >> (W - o)) & MASK);            // bits [52, 104)
+            const int64_t c2 = (2 * W - o < 64) ? (int64_t)(u >> (2 * W - o)) : 0;   // bits >= 104 (u < 2^63)
+            const int64_t sg = (b & 1) ? -1 : 1;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&digits[i]), (unsigned long long)(sg * c0));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&digits[i + 1]), (unsigned long long)(sg * c1));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&digits[i + 2]), (unsigned long long)(sg * c2));
+        }
+    }
+    __syncthreads();
+    int64_t a0 = 0, a1 = 0;
+    if (warp == 0) {
+        a0 = digits[lane];
+        a1 = (lane + 32 < D) ? digits[lane + 32] : 0;
+        regularize_warp(a0, a1, lane);
+    }
+    grid_tail<H16_WARPS>(a0, a1, blk_flags, n, p, digits, su, &blk_flags, &is_last, warp, lane);
+}
+
+template <class F>
+static cudaError_t launch_h16(const uint16_t* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
+    constexpr size_t SMEM = (size_t)H16_WARPS * 32 * (F::NBIN64 * 8 + F::NBIN * 4);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_accumulate_h16<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 2;
+    if (head > n) head = n;
+    const uint64_t ntiles = ((n - head) / 8) / ((uint64_t)H16_WARPS * 32 * H16_U);
+    uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
+    if (g < 1) g = 1;
+    if (g > XS_MAXB) g = XS_MAXB;
+    k_accumulate_h16<F><<<(unsigned)g, H16_WARPS * 32, SMEM, s>>>(x, n, p);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t accumulate_h16(const uint16_t* x, uint64_t n, int bf16, const AccParams& p, int num_sms, cudaStream_t s) {
+    return bf16 ? launch_h16<FmtBF16>(x, n, p, num_sms, s) : launch_h16<FmtF16>(x, n, p, num_sms, s);
+}
+
+}  // namespace xs

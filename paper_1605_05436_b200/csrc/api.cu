@@ -74,6 +74,50 @@ int sms_of(int dev) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// 16-bit inputs: one launch per 2^40 summands (the kernel's int64 bin totals stay < 2^63).
+xsum_status run_h16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, int bf16, int overwrite, xsum_result* res,
+                    uint64_t* canon, cudaStream_t s) {
+    constexpr uint64_t CH = 1ull << 40;
+    uint64_t off = 0;
+    bool first = true;
+    do {
+        const uint64_t c = (n - off) < CH ? (n - off) : CH;
+        const bool last = off + c == n;
+        if (xs::accumulate_h16(d_x + off, c, bf16, acc_params(h, first ? overwrite : 0, last ? res : nullptr,
+                                                               last ? canon : nullptr),
+                               grid_of(h), s) != cudaSuccess)
+            return XSUM_ECUDA;
+        off += c;
+        first = false;
+    } while (off < n);
+    return XSUM_OK;
+}
+
+xsum_status accumulate_h16_api(xsum_ctx* h, const uint16_t* d_x, uint64_t n, int bf16, void* stream) {
+    if (!h) return XSUM_EINVAL;
+    if (n == 0) return XSUM_OK;
+    if (!d_x || !aligned(d_x, 2)) return XSUM_EINVAL;
+    if (n > kMaxCount - h->count) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    xsum_status st = run_h16(h, d_x, n, bf16, 0, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+    if (st == XSUM_OK) h->count += n;
+    return st;
+}
+
+xsum_status sum_h16_api(xsum_ctx* h, const uint16_t* d_x, uint64_t n, int bf16, void* d_res, uint64_t* d_canon,
+                        void* stream) {
+    if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;
+    if (n && (!d_x || !aligned(d_x, 2))) return XSUM_EINVAL;
+    if (n > kMaxCount) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    xsum_status st = run_h16(h, d_x, n, bf16, 1, static_cast<xsum_result*>(d_res), d_canon,
+                             static_cast<cudaStream_t>(stream));
+    if (st == XSUM_OK) h->count = n;
+    return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -184,6 +228,19 @@ xsum_status xsum_sum_f32(xsum_ctx* h, const float* d_x, uint64_t n, void* d_res,
         return XSUM_ECUDA;
     h->count = n;
     return XSUM_OK;
+}
+
+xsum_status xsum_accumulate_f16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, void* stream) {
+    return accumulate_h16_api(h, d_x, n, 0, stream);
+}
+xsum_status xsum_accumulate_bf16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, void* stream) {
+    return accumulate_h16_api(h, d_x, n, 1, stream);
+}
+xsum_status xsum_sum_f16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, void* d_res, uint64_t* d_canon, void* stream) {
+    return sum_h16_api(h, d_x, n, 0, d_res, d_canon, stream);
+}
+xsum_status xsum_sum_bf16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, void* d_res, uint64_t* d_canon, void* stream) {
+    return sum_h16_api(h, d_x, n, 1, d_res, d_canon, stream);
 }
 
 xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, void* d_stage, size_t stage_bytes,

@@ -32,6 +32,7 @@ void note_launch();
 
 cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
 cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
+cudaError_t accumulate_h16(const uint16_t* x, uint64_t n, int bf16, const AccParams& p, int num_sms, cudaStream_t s);
 cudaError_t init_state(xsum_state_image* st, cudaStream_t s);
 cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, int overwrite, xsum_result* res,
                          uint64_t* canon, cudaStream_t s);

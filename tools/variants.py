@@ -16,7 +16,9 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "seg_nb4": ["-DXS_SEG_NB=4"],
+    "h16_red": ["-DXS_H16_RED"],
+    "h16_nb2": ["-DXS_H16_NB=2"],
+    "h16_nb6": ["-DXS_H16_NB=6"],
 }
 
 
@@ -38,7 +40,13 @@ import os, sys, json, statistics
 sys.path.insert(0, {ROOT!r})
 os.environ['XSUM_LIBRARY'] = {so!r}
 import torch, synth, paper_1605_05436_b200 as xsum
-x = synth.device_generate({cfg!r}.replace("seg", ""))
+if {cfg!r} in ("f16", "bf16"):
+    g = torch.Generator(device="cuda"); g.manual_seed(1)
+    x = torch.randint(-32768, 32767, (1 << 30,), dtype=torch.int16, device="cuda", generator=g)
+    em = 0x7C00 if {cfg!r} == "f16" else 0x7F80
+    x = torch.where((x & em) == em, x ^ 0x400, x).view(torch.float16 if {cfg!r} == "f16" else torch.bfloat16)
+else:
+    x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = xsum.Accumulator()
 if {cfg!r}.endswith("seg"):
     class _S:
@@ -55,7 +63,7 @@ for a, b in ev:
 torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
-print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=8*x.numel()/ms/1e6, bits=hex(r.bits))))
+print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, bits=hex(r.bits))))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     print(out.stdout.strip() or out.stderr[-2000:], flush=True)

@@ -48,8 +48,8 @@ constexpr int H16_U = 4;          // 16-B vectors per thread per tile (8 summand
 #endif
 constexpr int H16_NB = XS_H16_NB; // rotating register buffers (NB-1 tiles in flight)
 
-// One summand: h = |x| bit pattern (15 bits), s = sign bit; bins = this lane's bin column
-// (bin b at word b*32).
+// One summand (checked paths): h = |x| bit pattern (15 bits), s = sign bit; bins = this lane's
+// bin column (bin b at word b*32).
 template <class F>
 __device__ __forceinline__ void h16_add(uint32_t* bins, uint32_t h, uint32_t s) {
     const uint32_t q = max((h >> F::t) + 1u, 2u);                          // max(e,1) + 1
@@ -57,19 +57,58 @@ __device__ __forceinline__ void h16_add(uint32_t* bins, uint32_t h, uint32_t s) 
     const uint32_t o = q & ((1u << F::SB) - 1u);
     const uint32_t b = ((q >> F::SB) << 1) | s;
     XS_ASSERT(b < (uint32_t)F::NBIN);
-#ifdef XS_H16_RED
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bins + b * 32u)),
-                 "r"(M << o) : "memory");
-#else
     bins[b * 32u] += M << o;
+}
+
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r; asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+}
+
+__device__ __forceinline__ void bin_add(uint32_t saddr, uint32_t v) {
+#ifdef XS_H16_LDSTS
+    uint32_t o;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(o) : "r"(saddr) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr), "r"(o + v) : "memory");
+#else
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");   // fire and forget
 #endif
 }
 
-// the two summands of a 32-bit word (little-endian: element 2i in the low half)
+__device__ __forceinline__ uint32_t madhi_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r; asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r;
+}
+
+// The two summands of a 32-bit word (little-endian: element 2i in the low half), decoded with
+// the exponent work done once for both halves in 16-bit lanes (VIMNMX.U16x2, and IMADs / LOP3s
+// whose per-half results cannot carry into the other half): per half q = max(e,1)+1 < 2^16,
+// M = h + 2^(t+1) - q 2^t in [0, 2^(t+1)), bin byte offset (2 g + s) 128 < 2^16. The work is
+// split between the ALU pipe (shifts, masks, min/max) and the FMA pipe (IMAD / IMAD.HI with
+// the opaque `one` / `mone`), which ncu showed as the binding resource (ALU 93% busy in a plain
+// version). `sbase` is the shared address of this lane's bin 0 (bin b at sbase + 128 b),
+// `sbase2` = sbase * (2^16 + 1) mod 2^32.
 template <class F>
-__device__ __forceinline__ void h16_add_word(uint32_t* bins, uint32_t w) {
-    h16_add<F>(bins, w & 0x7FFFu, (w >> 15) & 1u);
-    h16_add<F>(bins, (w >> 16) & 0x7FFFu, w >> 31);
+__device__ __forceinline__ void h16_add_word(uint32_t sbase, uint32_t sbase2, uint32_t w, uint32_t one,
+                                             uint32_t mone) {
+    constexpr uint32_t t = F::t, SB = F::SB;
+    constexpr uint32_t EM2 = ((1u << F::l) - 1u) * 0x00010001u;
+    const uint32_t e2 = (w >> t) & EM2;                                       // exponent fields
+    const uint32_t ep2 = vmax_u16x2(e2, 0x00010001u);                         // max(e,1)
+    const uint32_t q2 = mad_u32(ep2, one, 0x00010001u);                       // + 1
+    const uint32_t h2 = w & 0x7FFF7FFFu;                                      // |x| patterns
+    const uint32_t M2 = mad_u32(ep2, 0u - (1u << t), mad_u32(h2, one, (1u << t) * 0x00010001u));  // M
+    const uint32_t o2 = q2 & (((1u << SB) - 1u) * 0x00010001u);               // q mod 2^SB
+    const uint32_t g2 = mad_u32(o2, mone, q2);                                // 2^SB g
+    const uint32_t s2 = madhi_u32(mad_u32(h2, mone, w), 1u << 24, 0u);        // 128 s  (sign bits >> 8)
+    const uint32_t a2 = mad_u32(g2, 1u << (8 - SB), s2);                      // (2 g + s) 128
+    XS_ASSERT((a2 & 0xFFFFu) < (uint32_t)F::NBIN * 128u && (a2 >> 16) < (uint32_t)F::NBIN * 128u);
+    const uint32_t Mh = M2 >> 16, oh = o2 >> 16;
+    const uint32_t Ml = mad_u32(Mh, 0xFFFF0000u, M2);
+    uint32_t vl;                      // Ml << o_lo: the wrap-mode funnel shift uses o2 mod 32 = o_lo
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(vl) : "r"(0u), "r"(Ml), "r"(o2));
+    const uint32_t addr_hi = sbase + (a2 >> 16);
+    const uint32_t addr_lo = mad_u32(addr_hi, 0xFFFF0000u, mad_u32(a2, one, sbase2));   // sbase + (a2 & 0xFFFF)
+    bin_add(addr_lo, vl);
+    bin_add(addr_hi, Mh << oh);
 }
 
 template <class F>
@@ -136,6 +175,9 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t* bins = bins_all + warp * (F::NBIN * 32) + lane;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bins);
+    const uint32_t sbase2 = sbase * 0x00010001u;
+    const uint32_t one = p.one, mone = p.mone;
     int64_t* bins64 = bins64_all + warp * (F::NBIN64 * 32) + lane;
 #pragma unroll
     for (int b = 0; b < F::NBIN; ++b) bins[b * 32] = 0;
@@ -175,10 +217,10 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
             if (more) {
 #pragma unroll
                 for (int u = 0; u < H16_U; ++u) {
-                    h16_add_word<F>(bins, buf[b][u].x);
-                    h16_add_word<F>(bins, buf[b][u].y);
-                    h16_add_word<F>(bins, buf[b][u].z);
-                    h16_add_word<F>(bins, buf[b][u].w);
+                    h16_add_word<F>(sbase, sbase2, buf[b][u].x, one, mone);
+                    h16_add_word<F>(sbase, sbase2, buf[b][u].y, one, mone);
+                    h16_add_word<F>(sbase, sbase2, buf[b][u].z, one, mone);
+                    h16_add_word<F>(sbase, sbase2, buf[b][u].w, one, mone);
                 }
                 any_tile = true;
                 tlast = t;
@@ -188,18 +230,12 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
             }
         }
         if (++groups == GROUPS_PER_WINDOW) {
-#ifdef XS_H16_RED
-            __syncwarp();
-#endif
             if (h16_flush<F>(bins, bins64)) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
             groups = 0;
             wstart = t;
             any_tile = false;
         }
     }
-#ifdef XS_H16_RED
-    __syncwarp();
-#endif
     if (h16_flush<F>(bins, bins64) && any_tile) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
 
     // leftover vectors (< one tile), the unaligned head and the tail: checked adds by the block
@@ -221,9 +257,6 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
         if ((uint64_t)tid < head) h16_add_checked<F>(bins, __ldg(x + tid), flags);
         if (tid >= 8 && (uint64_t)(tid - 8) < tail) h16_add_checked<F>(bins, __ldg(x + head + nvec * PV + (tid - 8)), flags);
     }
-#ifdef XS_H16_RED
-    __syncwarp();
-#endif
     h16_flush<F>(bins, bins64);
     __syncwarp();
 

@@ -16,7 +16,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "h16_red": ["-DXS_H16_RED"],
+    "h16_ldsts": ["-DXS_H16_LDSTS"],
     "h16_nb2": ["-DXS_H16_NB=2"],
     "h16_nb6": ["-DXS_H16_NB=6"],
 }

@@ -28,21 +28,50 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
         p.partial[(size_t)lane * XS_MAXB + blockIdx.x] = a0;
         if (lane + 32 < D) p.partial[(size_t)(lane + 32) * XS_MAXB + blockIdx.x] = a1;
         if (lane == 0) p.pflags[blockIdx.x] = bflags;
-        __threadfence();
         __syncwarp();
-        if (lane == 0) *sh_last = (atomicAdd(p.counter, 1u) == (unsigned)(G - 1));
+        if (lane == 0) {
+            // release: this block's partial (ordered before by the warp barrier) is visible to
+            // the block that sees the final count; acquire: the last block sees all of them
+            uint32_t old;
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counter) : "memory");
+            *sh_last = (old == (uint32_t)(G - 1));
+        }
     }
     __syncthreads();
     if (!*sh_last) return;
     __threadfence();
 
-    // the last block merges the G block partials (digit-major, coalesced) and the handle
-    // state; G <= XS_MAXB so the raw sum stays below 2^62 before regularizing.
-    for (int j = warp; j < D; j += WARPS) {
-        int64_t s = 0;
-        for (uint64_t b = lane; b < G; b += 32) s += __ldcg(&p.partial[(size_t)j * XS_MAXB + b]);
-        s = warp_sum64(s);
-        if (lane == 0) red[j] = s;
+    // The last block merges the G block partials (digit-major, coalesced) and the handle
+    // state; G <= XS_MAXB so the raw sum stays below 2^62 before regularizing. Warp w sums
+    // digits w, w+WARPS, ...; a lane issues all its loads of one round (4 partials of each of
+    // its digits) before using any: one L2 round trip per 128 blocks instead of one per 32.
+    constexpr int JPW = (D + WARPS - 1) / WARPS;
+    int64_t st0 = 0, st1 = 0;
+    if (warp == 0 && !p.overwrite) {                     // state digits, fetched alongside
+        st0 = __ldcg(&p.state->digit[lane]);
+        st1 = (lane + 32 < D) ? __ldcg(&p.state->digit[lane + 32]) : 0;
+    }
+    int64_t acc[JPW];
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) acc[jj] = 0;
+    for (uint64_t b0 = lane; b0 < G; b0 += 128) {
+        int64_t v[JPW][4];
+#pragma unroll
+        for (int jj = 0; jj < JPW; ++jj)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = warp + jj * WARPS;
+                const uint64_t b = b0 + 32 * u;
+                v[jj][u] = (j < D && b < G) ? __ldcg(&p.partial[(size_t)j * XS_MAXB + b]) : 0;
+            }
+#pragma unroll
+        for (int jj = 0; jj < JPW; ++jj) acc[jj] += (v[jj][0] + v[jj][1]) + (v[jj][2] + v[jj][3]);
+    }
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) {
+        const int j = warp + jj * WARPS;
+        const int64_t s = warp_sum64(acc[jj]);
+        if (j < D && lane == 0) red[j] = s;
     }
     if (warp == 1 % WARPS) {
         uint32_t f = 0;
@@ -52,12 +81,10 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
     }
     __syncthreads();
     if (warp == 0) {
-        int64_t b0 = red[lane], b1 = (lane + 32 < D) ? red[lane + 32] : 0;
+        int64_t b0 = red[lane] + st0, b1 = (lane + 32 < D) ? red[lane + 32] + st1 : 0;
         uint32_t fl = *sh_flags;
         uint64_t cnt = n;
         if (!p.overwrite) {
-            b0 += p.state->digit[lane];
-            if (lane + 32 < D) b1 += p.state->digit[lane + 32];
             fl |= p.state->flags;
             cnt += p.state->count;
         }

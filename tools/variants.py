@@ -16,9 +16,9 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "h16_ldsts": ["-DXS_H16_LDSTS"],
-    "h16_nb2": ["-DXS_H16_NB=2"],
-    "h16_nb6": ["-DXS_H16_NB=6"],
+    "acc_u1nb2": ["-DXS_ACC_U=1", "-DXS_ACC_NB=2"],
+    "acc_u2nb2": ["-DXS_ACC_U=2", "-DXS_ACC_NB=2"],
+    "acc_w8u1nb2": ["-DXS_ACC_WARPS=8", "-DXS_ACC_U=1", "-DXS_ACC_NB=2"],
 }
 
 
@@ -40,7 +40,9 @@ import os, sys, json, statistics
 sys.path.insert(0, {ROOT!r})
 os.environ['XSUM_LIBRARY'] = {so!r}
 import torch, synth, paper_1605_05436_b200 as xsum
-if {cfg!r} in ("f16", "bf16"):
+if {cfg!r}.startswith("n"):
+    x = synth.device_generate("c2")[: 1 << int({cfg!r}[1:])].clone()
+elif {cfg!r} in ("f16", "bf16"):
     g = torch.Generator(device="cuda"); g.manual_seed(1)
     x = torch.randint(-32768, 32767, (1 << 30,), dtype=torch.int16, device="cuda", generator=g)
     em = 0x7C00 if {cfg!r} == "f16" else 0x7F80

@@ -200,8 +200,5 @@ cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_
     return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, XS_ACC_NB, double>(x, n, p, num_sms, s);
 }
 
-cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    return launch_accumulate<XS_ACC_WARPS, XS_ACC_U, XS_ACC_NB, float>(x, n, p, num_sms, s);
-}
 
 }  // namespace xs

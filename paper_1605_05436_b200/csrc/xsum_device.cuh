@@ -33,8 +33,8 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // Summands a lane column may take between two regularizations. Each summand adds one
 // chunk (|chunk| <= 2^52) to at most one position of each digit. A window holds at most
-// FLUSH_ELEMS hot-loop summands plus <= 17 head/tail/leftover summands (4 x 4 binary32 per
-// lane + 1) on top of a regularized residue |Y| <= 2^51 + 2^11:
+// FLUSH_ELEMS hot-loop summands plus <= 17 head/tail/leftover summands on top of a
+// regularized residue |Y| <= 2^51 + 2^11:
 // 2^51 + 2^11 + (2016 + 17) * 2^52 + 2^51 < 2^63, so neither the adds nor the balanced
 // carry (y + R/2) can overflow int64. NaN/Inf bit patterns summed unchecked are cancelled
 // after the window's regularization, in a fresh window of the same bound (re-derived in
@@ -243,38 +243,6 @@ __device__ __forceinline__ void column_fix_special(int64_t* col, uint32_t lo, ui
     column_add(col, decompose(lo, hi ^ 0x80000000u, one), one);
 }
 
-// ---------------------------------------------------------------------------------
-// binary32 inputs (IEEE binary32, t = 23, l = 8):
-// |x| = M 2^(k-149) with M = m + [e!=0] 2^23 < 2^24, k = max(e,1)-1, i.e. M at bit position
-// k + 925 in units of 2^-1074: the same digit window holds binary32 values exactly.
-// ---------------------------------------------------------------------------------
-constexpr uint32_t SPEC_K_F64 = 2046;   // bit position k reached only by NaN/Inf patterns
-constexpr uint32_t SPEC_K_F32 = 1179;   // 254 + 925
-
-__device__ __forceinline__ Chunks decompose32(uint32_t b, uint32_t one, uint32_t mone) {
-    Chunks c;
-    uint32_t h = b & 0x7FFFFFFFu;
-    uint32_t e = h >> 23;
-    uint32_t ep = max(e, 1u);
-    uint32_t k = mad_u32(ep, one, 924u);                  // ep - 1 + 925
-    uint32_t i = mulhi_u32(k, K52);                       // k / 52
-    uint32_t o = mad_u32(i, (uint32_t)-52, k);
-    uint32_t r = mad_u32(o, mone, 52u);                   // 52 - o
-    uint32_t M = mad_u32(mad_u32(ep, 0xFF800000u, h), one, 0x800000u);   // h - (ep-1) 2^23
-    int32_t S = (int32_t)b >> 31;
-    int64_t sM = (int64_t)(int32_t)((M ^ (uint32_t)S) - (uint32_t)S);     // +-M, |M| < 2^24
-    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> r;
-    c.i = i;
-    c.spec = k;
-    return c;
-}
-
-__device__ __forceinline__ uint32_t special_flags32(uint32_t b) {
-    if (b & 0x7FFFFFu) return XSUM_F_NAN;
-    return (b >> 31) ? XSUM_F_NINF : XSUM_F_PINF;
-}
-
 // Input element traits: how a 16-byte vector splits into summands, and the non-hot paths.
 template <typename T> struct Elem;
 
@@ -305,54 +273,6 @@ template <> struct Elem<double> {
         uint2 q;
         asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(q.x), "=r"(q.y) : "l"(p));
         column_add_checked(col, q.x, q.y, flags, one);
-    }
-};
-
-template <> struct Elem<float> {
-    static constexpr int PER_VEC = 4;
-    __device__ static __forceinline__ uint32_t fold(uint32_t acc, const Chunks& c) { return max(acc, c.spec); }
-    __device__ static __forceinline__ bool hit(uint32_t acc) { return acc >= SPEC_K_F32; }
-    __device__ static __forceinline__ void add1(int64_t* col, uint32_t b, uint32_t& nspec, uint32_t one,
-                                                uint32_t mone) {
-        Chunks a = decompose32(b, one, mone);
-        nspec = fold(nspec, a);
-        column_add(col, a, one);
-    }
-    __device__ static __forceinline__ void add_vec(int64_t* col, const uint4& v, uint32_t& nspec, uint32_t one,
-                                                   uint32_t mone) {
-        add1(col, v.x, nspec, one, mone);
-        add1(col, v.y, nspec, one, mone);
-        add1(col, v.z, nspec, one, mone);
-        add1(col, v.w, nspec, one, mone);
-    }
-    __device__ static __forceinline__ void fix1(int64_t* col, uint32_t b, uint32_t& flags, uint32_t one) {
-        if (((b >> 23) & 0xFFu) != 0xFFu) return;
-        flags |= special_flags32(b);
-        column_add(col, decompose32(b ^ 0x80000000u, one, 0xFFFFFFFFu), one);
-    }
-    __device__ static __forceinline__ void fix_vec(int64_t* col, const uint4& v, uint32_t& flags, uint32_t one) {
-        fix1(col, v.x, flags, one);
-        fix1(col, v.y, flags, one);
-        fix1(col, v.z, flags, one);
-        fix1(col, v.w, flags, one);
-    }
-    __device__ static __forceinline__ void checked1(int64_t* col, uint32_t b, uint32_t& flags, uint32_t one) {
-        Chunks c = decompose32(b, one, 0xFFFFFFFFu);
-        if (hit(c.spec)) { flags |= special_flags32(b); return; }
-        column_add(col, c, one);
-    }
-    __device__ static __forceinline__ void add_vec_checked(int64_t* col, const uint4& v, uint32_t& flags,
-                                                           uint32_t one) {
-        checked1(col, v.x, flags, one);
-        checked1(col, v.y, flags, one);
-        checked1(col, v.z, flags, one);
-        checked1(col, v.w, flags, one);
-    }
-    __device__ static __forceinline__ void add_one_checked(int64_t* col, const float* p, uint32_t& flags,
-                                                           uint32_t one) {
-        uint32_t b;
-        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(b) : "l"(p));
-        checked1(col, b, flags, one);
     }
 };
 

@@ -148,3 +148,16 @@ def test_h16_status_codes(xs):
     assert L.xsum_accumulate_bf16(acc.handle, h.data_ptr(), 0, st) == xs.OK
     assert L.xsum_sum_f16(acc.handle, h.data_ptr(), 3, None, None, st) == xs.EINVAL
     assert L.xsum_accumulate_f16(acc.handle, h.data_ptr(), 2 ** 63, st) == xs.ECAPACITY
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+def test_h16_signed_zeros_and_subnormals(xs, fmt):
+    # -0 has M = 0 with the sign bit set (the case a sign-extension slip gets wrong), and
+    # subnormals have no hidden bit (R2); alone, mixed, and as a block-sized run
+    rng = np.random.default_rng(3)
+    subs = rng.integers(1, 1 << (10 if fmt == "f16" else 7), size=5000, dtype=np.uint32).astype(np.uint16)
+    subs |= (rng.integers(0, 2, size=5000, dtype=np.uint32) << 15).astype(np.uint16)
+    for b in (np.array([0x8000], np.uint16), np.array([0x8000, 0x0000, 0x8000], np.uint16),
+              np.full(40000, 0x8000, np.uint16), subs, np.concatenate([subs, np.full(777, 0x8000, np.uint16)])):
+        res, canon = xs.exact_sum(to_dev16(b, fmt, 1))
+        check(xs, res, canon, oracle.exact_sum(b, fmt=fmt), f"{fmt} zeros/subnormals n={b.size}")

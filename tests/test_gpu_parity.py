@@ -476,6 +476,17 @@ def test_f32_flush_windows_and_specials(xs, blocks):
     assert_same(res, canon, y, what=f"f32 specials blocks={blocks}")
 
 
+def test_f32_signed_zeros_and_subnormals(xs):
+    """-0.0f has M = 0 with the sign bit set; subnormals have no hidden bit (R2)."""
+    rng = np.random.default_rng(4)
+    subs = (rng.integers(1, 1 << 23, size=9000, dtype=np.uint32) |
+            (rng.integers(0, 2, size=9000, dtype=np.uint32) << np.uint32(31))).view(np.float32)
+    for x in (np.array([-0.0], np.float32), np.array([-0.0, 0.0, -0.0], np.float32),
+              np.full(70000, -0.0, np.float32), subs, np.concatenate([subs, np.full(555, -0.0, np.float32)])):
+        res, canon = xs.exact_sum(to_dev32(x, 1))
+        assert_same(res, canon, x, what=f"f32 zeros/subnormals n={x.size}")
+
+
 def test_mixed_binary32_and_binary64_in_one_state(xs):
     """One superaccumulator holds binary32 and binary64 summands exactly (same 2^-1074 window)."""
     a = _f32_data(1_000_003, 3, 60, 200)

@@ -16,9 +16,8 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "acc_u1nb2": ["-DXS_ACC_U=1", "-DXS_ACC_NB=2"],
-    "acc_u2nb2": ["-DXS_ACC_U=2", "-DXS_ACC_NB=2"],
-    "acc_w8u1nb2": ["-DXS_ACC_WARPS=8", "-DXS_ACC_U=1", "-DXS_ACC_NB=2"],
+    "f32b_nb4": ["-DXS_F32B_NB=4"],
+    "f32b_nb3": ["-DXS_F32B_NB=3"],
 }
 
 
@@ -42,6 +41,10 @@ os.environ['XSUM_LIBRARY'] = {so!r}
 import torch, synth, paper_1605_05436_b200 as xsum
 if {cfg!r}.startswith("n"):
     x = synth.device_generate("c2")[: 1 << int({cfg!r}[1:])].clone()
+elif {cfg!r} == "f32":
+    g = torch.Generator(device="cuda"); g.manual_seed(1)
+    x = torch.randint(-2 ** 31, 2 ** 31 - 1, (1 << 29,), dtype=torch.int32, device="cuda", generator=g)
+    x = torch.where((x & 0x7F800000) == 0x7F800000, x ^ 0x800000, x).view(torch.float32)
 elif {cfg!r} in ("f16", "bf16"):
     g = torch.Generator(device="cuda"); g.manual_seed(1)
     x = torch.randint(-32768, 32767, (1 << 30,), dtype=torch.int16, device="cuda", generator=g)

@@ -91,6 +91,24 @@ typedef struct xsum_state_image {
     uint8_t pad[XSUM_STATE_BYTES - 24 - 8 * XSUM_NDIGITS];
 } xsum_state_image;
 
+/* Sparse state image: the paper's sparse superaccumulator keeps only the
+ * active (non-zero) components. Header (24 bytes, little-endian) followed by
+ * nnz u64 records (digit << 6) | index in strictly ascending index order, digit the
+ * regularized component (|digit| <= R-1; the top digit's magnitude is bounded by the value),
+ * stored two's complement in the top 58 bits. Size 24 + 8*nnz <= XSUM_SPARSE_MAX_BYTES; narrow
+ * exponent ranges give a few records. */
+#define XSUM_SPARSE_MAGIC 0x41505358u   /* "XSPA" little-endian */
+#define XSUM_SPARSE_MAX_BYTES (24 + 8 * XSUM_NDIGITS)
+typedef struct xsum_sparse_header {
+    uint32_t magic;      /* XSUM_SPARSE_MAGIC */
+    uint16_t version;    /* XSUM_VERSION */
+    uint8_t w;           /* 52 */
+    uint8_t nnz;         /* records that follow, <= XSUM_NDIGITS */
+    uint32_t flags;      /* XSUM_F_NAN | PINF | NINF | MISMATCH */
+    uint32_t reserved;   /* 0 */
+    uint64_t count;      /* summands */
+} xsum_sparse_header;
+
 /* Result record written by xsum_finalize_round / xsum_sum (48 bytes, device memory).
  * PAPER.md:787-795 (§3 step 7): locate the most significant non-zero component,
  * combine it with its neighbours and round on the truncated bits. */
@@ -182,6 +200,20 @@ XSUM_API xsum_status xsum_merge(xsum_ctx *h, const void *d_states, uint32_t coun
  * per-GPU states. Errors: XSUM_EINVAL, XSUM_ECUDA. */
 XSUM_API xsum_status xsum_merge_round(xsum_ctx *h, const void *d_states, uint32_t count, void *d_res,
                                       uint64_t *d_canon, void *stream);
+
+/* Sparse image of the state: writes the header and one
+ * record per non-zero digit to d_out (device, 8-B aligned, >= XSUM_SPARSE_MAX_BYTES) and the
+ * image's byte size to *d_nbytes (device u32). Non-destructive. Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_to_sparse(xsum_ctx *h, void *d_out, uint32_t *d_nbytes, void *stream);
+
+/* State += sum of `count` sparse images; image s starts at byte d_images + d_offsets[s]
+ * (d_offsets: device u64[count], multiples of 8). Carry-free Lemma-1 merge tree as
+ * xsum_merge (the paper's sparse merges of PAPER.md:851-873 without the
+ * sort: the indices address the dense window directly). Images with a bad header, misaligned
+ * offset, unsorted / out-of-range indices or unregularized digits are skipped and set
+ * XSUM_F_MISMATCH. Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_merge_sparse(xsum_ctx *h, const void *d_images, const uint64_t *d_offsets, uint32_t count,
+                                       void *stream);
 
 /* Non-destructive rounding of the state: writes *d_res (device, 8-B aligned) and, if
  * d_canon != NULL, the canonical image (XSUM_CANON_LIMBS little-endian u64 limbs of the

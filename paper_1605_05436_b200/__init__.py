@@ -34,12 +34,18 @@ F_OVERFLOW32, F_INEXACT32 = 64, 128
 
 OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 
+# sparse state image (include/xsum.h): 24-byte header + nnz records (digit << 6) | index
+SPARSE_MAGIC = 0x41505358
+SPARSE_HEADER_BYTES = 24
+SPARSE_MAX_BYTES = SPARSE_HEADER_BYTES + 8 * NDIGITS
+
 # every entry point declared in include/xsum.h
 EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_create", "xsum_reset",
            "xsum_accumulate", "xsum_accumulate_host", "xsum_merge", "xsum_finalize_round", "xsum_sum",
            "xsum_destroy", "xsum_count", "xsum_sum_segments", "xsum_sum_segments_csr", "xsum_status_str",
            "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round",
-           "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16")
+           "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
+           "xsum_to_sparse", "xsum_merge_sparse")
 
 
 class XsumError(RuntimeError):
@@ -80,6 +86,7 @@ def lib() -> ctypes.CDLL:
             "xsum_merge_round": ([p, p, u32, p, p, p], i32),
             "xsum_accumulate_f16": ([p, p, u64, p], i32), "xsum_accumulate_bf16": ([p, p, u64, p], i32),
             "xsum_sum_f16": ([p, p, u64, p, p, p], i32), "xsum_sum_bf16": ([p, p, u64, p, p, p], i32),
+            "xsum_to_sparse": ([p, p, p, p], i32), "xsum_merge_sparse": ([p, p, p, u32, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -275,6 +282,32 @@ class Accumulator:
             self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
         return self._res, (self._canon if canon else None)
 
+    def to_sparse(self):
+        """Sparse image of the state (xsum_to_sparse): (uint8 CUDA tensor of SPARSE_MAX_BYTES,
+        its valid byte count as a host int)."""
+        torch = _torch()
+        out = torch.zeros(SPARSE_MAX_BYTES, dtype=torch.uint8, device=self.device)
+        nb = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _check("xsum_to_sparse", lib().xsum_to_sparse(self._h, out.data_ptr(), nb.data_ptr(),
+                                                      _stream_ptr(self.device)))
+        n = int(nb.item())
+        return out[:n], n
+
+    def merge_sparse(self, images, offsets) -> "Accumulator":
+        """State += the sparse images in `images` (uint8 CUDA tensor) starting at byte
+        `offsets` (int64 CUDA tensor, multiples of 8)."""
+        torch = _torch()
+        if not (isinstance(images, torch.Tensor) and images.is_cuda and images.dtype == torch.uint8 and
+                images.is_contiguous()):
+            raise TypeError("images must be a contiguous uint8 CUDA tensor")
+        if not (isinstance(offsets, torch.Tensor) and offsets.is_cuda and offsets.dtype == torch.int64 and
+                offsets.is_contiguous()):
+            raise TypeError("offsets must be a contiguous int64 CUDA tensor")
+        base = images if images.numel() else torch.zeros(8, dtype=torch.uint8, device=self.device)
+        _check("xsum_merge_sparse", lib().xsum_merge_sparse(self._h, base.data_ptr(), offsets.data_ptr(),
+                                                            offsets.numel(), _stream_ptr(self.device)))
+        return self
+
     def finalize_async(self, canon: bool = False):
         """Enqueue the rounding; returns the (result bytes, canon limbs or None) device tensors."""
         _check("xsum_finalize_round", lib().xsum_finalize_round(
@@ -299,6 +332,18 @@ class Accumulator:
         _check(name, getattr(lib(), name)(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
                                           self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
         return self._res, (self._canon if canon else None)
+
+
+def decode_sparse(b: bytes) -> dict:
+    """Host-side parse of one sparse image (include/xsum.h): header fields and {index: digit}."""
+    a = np.frombuffer(bytes(b), dtype=np.uint8)
+    magic, version, w, nnz, flags, _, count = np.frombuffer(a[:24].tobytes(), dtype=np.dtype(
+        [("m", "<u4"), ("v", "<u2"), ("w", "u1"), ("n", "u1"), ("f", "<u4"), ("r", "<u4"), ("c", "<u8")]))[0]
+    if magic != SPARSE_MAGIC or version != VERSION or w != RADIX_BITS or a.size < 24 + 8 * int(nnz):
+        raise ValueError("not a sparse xsum image")
+    rec = np.frombuffer(a[24:24 + 8 * int(nnz)].tobytes(), dtype="<i8")
+    digits = {int(r & 63): int(r >> 6) for r in rec}
+    return {"flags": int(flags), "count": int(count), "digits": digits}
 
 
 _default_acc: dict = {}
@@ -350,6 +395,34 @@ def sum_segments_csr(x, offsets, canon: bool = False, flags: bool = False):
     if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous() and offsets.numel() >= 1):
         raise TypeError("offsets must be a contiguous int64 CUDA tensor of nseg+1 entries")
     return _segments(x, offsets.numel() - 1, 0, offsets, canon, flags)
+
+
+def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
+    """Exact reduction of a float64 CUDA tensor along one dimension: every
+    output element is the correctly rounded (RN-even) sum of its fibre, independent of order -
+    a reproducible torch.sum(x, dim). The fibres are laid out as equal contiguous segments
+    (a movedim + contiguous copy when `dim` is not the last dimension) and summed by
+    xsum_sum_segments, one warp per fibre."""
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64:
+        raise TypeError("expected a float64 CUDA tensor")
+    if x.dim() == 0:
+        raise ValueError("exact_sum_dim needs a tensor with at least one dimension")
+    d = dim % x.dim()
+    xt = x.movedim(d, -1).contiguous()
+    seg = xt.shape[-1]
+    out_shape = xt.shape[:-1]
+    nseg = 1
+    for s_ in out_shape:
+        nseg *= s_
+    if nseg == 0:
+        out = torch.empty(out_shape, dtype=torch.float64, device=x.device)
+    else:
+        out, _, _ = _segments(xt.reshape(-1) if xt.numel() else torch.zeros(1, dtype=torch.float64,
+                                                                             device=x.device),
+                              nseg, seg, None, False, False)
+        out = out.reshape(out_shape)
+    return out.unsqueeze(d) if keepdim else out
 
 
 def _segments(x, nseg, seg_len, offsets, canon, flags):

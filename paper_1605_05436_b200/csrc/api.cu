@@ -300,6 +300,26 @@ xsum_status xsum_merge(xsum_ctx* h, const void* d_states, uint32_t count, void* 
     return XSUM_OK;
 }
 
+xsum_status xsum_to_sparse(xsum_ctx* h, void* d_out, uint32_t* d_nbytes, void* stream) {
+    if (!h || !d_out || !aligned(d_out, 8) || !d_nbytes || !aligned(d_nbytes, 4)) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::to_sparse(h->state, d_out, d_nbytes, static_cast<cudaStream_t>(stream)) != cudaSuccess) return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+xsum_status xsum_merge_sparse(xsum_ctx* h, const void* d_images, const uint64_t* d_offsets, uint32_t count,
+                              void* stream) {
+    if (!h) return XSUM_EINVAL;
+    if (count == 0) return XSUM_OK;
+    if (!d_images || !aligned(d_images, 8) || !d_offsets || !aligned(d_offsets, 8)) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    if (xs::merge_sparse(h->state, d_images, d_offsets, count, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
 xsum_status xsum_merge_round(xsum_ctx* h, const void* d_states, uint32_t count, void* d_res, uint64_t* d_canon,
                              void* stream) {
     if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;

@@ -39,25 +39,90 @@ __device__ __forceinline__ bool image_ok(const xsum_state_image* im, int64_t d0,
 
 constexpr int MERGE_WARPS = 16;
 
+// Leaf loaders of the merge tree: one warp reads image s into digit-parallel registers
+// (a0 = digit lane, a1 = digit lane+32). Returns false (image rejected) on a bad header or
+// digits that are not regularized.
+struct DenseImages {
+    const xsum_state_image* ims;
+    __device__ __forceinline__ bool load(uint32_t s, int lane, int64_t* /*scratch*/, int64_t& d0, int64_t& d1,
+                                         uint64_t& cnt, uint32_t& fl) const {
+        const xsum_state_image* im = ims + s;
+        d0 = im->digit[lane];
+        d1 = (lane + 32 < D) ? im->digit[lane + 32] : 0;
+        cnt = im->count;
+        fl = im->flags;
+        return image_ok(im, d0, d1, lane);
+    }
+};
+
+// Sparse images (the paper's sparse superaccumulator, PAPER.md:682-696:
+// only the active indices are kept): a 24-byte header and nnz records (digit << 6) | index in
+// ascending index order (include/xsum.h). Image s starts at base + offs[s].
+struct SparseImages {
+    const uint8_t* base;
+    const uint64_t* offs;
+    __device__ __forceinline__ bool load(uint32_t s, int lane, int64_t* scratch, int64_t& d0, int64_t& d1,
+                                         uint64_t& cnt, uint32_t& fl) const {
+        const uint64_t off = offs[s];
+        d0 = d1 = 0;
+        cnt = 0;
+        fl = 0;
+        if (off & 7) return false;                                     // warp-uniform
+        const xsum_sparse_header* hd = reinterpret_cast<const xsum_sparse_header*>(base + off);
+        const uint32_t nnz = hd->nnz;
+        if (hd->magic != XSUM_SPARSE_MAGIC || hd->version != XSUM_VERSION || hd->w != W || nnz > (uint32_t)D)
+            return false;
+        const uint64_t* rec = reinterpret_cast<const uint64_t*>(base + off + sizeof(xsum_sparse_header));
+        scratch[lane] = 0;
+        scratch[lane + 32] = 0;
+        __syncwarp();
+        bool ok = true;
+        int prev_last = -1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t r = (uint32_t)lane + 32u * h;
+            const bool has = r < nnz;
+            const uint64_t v = has ? rec[r] : 0;
+            const int idx = has ? (int)(v & 63u) : 64;
+            const int64_t dg = (int64_t)v >> 6;
+            int prev = __shfl_up_sync(FULL, idx, 1);
+            if (lane == 0) prev = prev_last;
+            prev_last = __shfl_sync(FULL, idx, 31);
+            if (has) {
+                const int64_t lim = idx < D - 1 ? R - 1 : (1ll << 40);
+                ok = ok && idx < D && idx > prev && dg != 0 && dg >= -lim && dg <= lim;
+                if (idx < D) scratch[idx] = dg;
+            }
+        }
+        __syncwarp();
+        d0 = scratch[lane];
+        d1 = (lane + 32 < D) ? scratch[lane + 32] : 0;
+        cnt = hd->count;
+        fl = hd->flags;
+        return __all_sync(FULL, ok);
+    }
+};
+
+template <class Src>
 __global__ void __launch_bounds__(MERGE_WARPS * 32)
-k_merge(xsum_state_image* st, const xsum_state_image* ims, uint32_t count, int overwrite, xsum_result* res,
-        uint64_t* canon) {
+k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_result* res, uint64_t* canon) {
     __shared__ int64_t acc[MERGE_WARPS][64];
+    __shared__ int64_t scr[MERGE_WARPS][64];
     __shared__ uint64_t cnts[MERGE_WARPS];
     __shared__ uint32_t fls[MERGE_WARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t a0 = 0, a1 = 0;
     uint64_t cnt = 0;
     uint32_t fl = 0;
-    // leaves: each warp folds states warp, warp+16, ... (Lemma-1 adds)
+    // leaves: each warp folds images warp, warp+16, ... (Lemma-1 adds)
     for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
-        const xsum_state_image* im = ims + s;
-        int64_t d0 = im->digit[lane];
-        int64_t d1 = (lane + 32 < D) ? im->digit[lane + 32] : 0;
-        if (image_ok(im, d0, d1, lane)) {
+        int64_t d0, d1;
+        uint64_t c;
+        uint32_t f;
+        if (src.load(s, lane, scr[warp], d0, d1, c, f)) {
             lemma1_add(a0, a1, d0, d1, lane);
-            cnt += im->count;
-            fl |= im->flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
+            cnt += c;
+            fl |= f & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
         } else {
             fl |= XSUM_F_MISMATCH;
         }
@@ -123,8 +188,45 @@ cudaError_t init_state(xsum_state_image* st, cudaStream_t s) {
 
 cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, int overwrite, xsum_result* res,
                          uint64_t* canon, cudaStream_t s) {
-    k_merge<<<1, MERGE_WARPS * 32, 0, s>>>(st, static_cast<const xsum_state_image*>(states), count, overwrite, res,
-                                           canon);
+    k_merge<<<1, MERGE_WARPS * 32, 0, s>>>(st, DenseImages{static_cast<const xsum_state_image*>(states)}, count,
+                                           overwrite, res, canon);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t merge_sparse(xsum_state_image* st, const void* images, const uint64_t* offsets, uint32_t count,
+                         cudaStream_t s) {
+    k_merge<<<1, MERGE_WARPS * 32, 0, s>>>(st, SparseImages{static_cast<const uint8_t*>(images), offsets}, count, 0,
+                                           nullptr, nullptr);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// Encode the (regularized) state as a sparse image: one record per non-zero digit, ascending.
+__global__ void k_to_sparse(const xsum_state_image* st, uint8_t* out, uint32_t* nbytes) {
+    const int lane = threadIdx.x & 31;
+    const int64_t a0 = st->digit[lane];
+    const int64_t a1 = (lane + 32 < D) ? st->digit[lane + 32] : 0;
+    const uint64_t nz = (uint64_t)__ballot_sync(FULL, a0 != 0) | ((uint64_t)__ballot_sync(FULL, a1 != 0) << 32);
+    const uint32_t nnz = __popcll(nz);
+    uint64_t* rec = reinterpret_cast<uint64_t*>(out + sizeof(xsum_sparse_header));
+    if (a0 != 0) rec[__popcll(nz & ((1ull << lane) - 1))] = ((uint64_t)a0 << 6) | (uint64_t)lane;
+    if (a1 != 0) rec[__popcll(nz & ((1ull << (lane + 32)) - 1))] = ((uint64_t)a1 << 6) | (uint64_t)(lane + 32);
+    if (lane == 0) {
+        xsum_sparse_header* hd = reinterpret_cast<xsum_sparse_header*>(out);
+        hd->magic = XSUM_SPARSE_MAGIC;
+        hd->version = (uint16_t)XSUM_VERSION;
+        hd->w = (uint8_t)W;
+        hd->nnz = (uint8_t)nnz;
+        hd->flags = st->flags;
+        hd->reserved = 0;
+        hd->count = st->count;
+        *nbytes = (uint32_t)(sizeof(xsum_sparse_header) + 8 * nnz);
+    }
+}
+
+cudaError_t to_sparse(const xsum_state_image* st, void* out, uint32_t* nbytes, cudaStream_t s) {
+    k_to_sparse<<<1, 32, 0, s>>>(st, static_cast<uint8_t*>(out), nbytes);
     note_launch();
     return cudaGetLastError();
 }

@@ -36,6 +36,9 @@ cudaError_t accumulate_h16(const uint16_t* x, uint64_t n, int bf16, const AccPar
 cudaError_t init_state(xsum_state_image* st, cudaStream_t s);
 cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t count, int overwrite, xsum_result* res,
                          uint64_t* canon, cudaStream_t s);
+cudaError_t merge_sparse(xsum_state_image* st, const void* images, const uint64_t* offsets, uint32_t count,
+                         cudaStream_t s);
+cudaError_t to_sparse(const xsum_state_image* st, void* out, uint32_t* nbytes, cudaStream_t s);
 cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s);
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                          double* out, uint64_t* canon, uint32_t* flags, int num_sms, cudaStream_t s);

@@ -540,3 +540,22 @@ def test_many_state_images_merge(xs):
     res, canon = xs.Accumulator().merge(states.reshape(-1)).exact()
     assert_same(res, canon, x, what="2500-way merge")
     assert res.count == x.size
+
+
+@pytest.mark.parametrize("shape,dim", [((7, 300), -1), ((7, 300), 0), ((3, 5, 4097), 1), ((2, 0, 3), 2),
+                                       ((2, 0, 3), 1), ((1,), 0), ((4, 1), 1), ((33, 2049), 0)])
+def test_exact_sum_dim(xs, shape, dim):
+    """Exact reduction along a tensor dimension: each fibre vs the oracle."""
+    import torch
+    n = int(np.prod(shape))
+    x = synth.gen.generate("c2", 11, n).reshape(shape) if n else np.zeros(shape)
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    out = xs.exact_sum_dim(t, dim).cpu().numpy()
+    ref_shape = np.sum(x, axis=dim).shape
+    assert out.shape == ref_shape
+    xm = np.moveaxis(x, dim, -1).reshape(out.size, x.shape[dim])
+    for i, row in enumerate(xm):
+        r, _ = oracle.exact_sum(row)
+        assert out.reshape(-1)[i].view(np.uint64) == np.uint64(r.bits), (shape, dim, i)
+    kd = xs.exact_sum_dim(t, dim, keepdim=True)
+    assert tuple(kd.shape) == tuple(np.sum(x, axis=dim, keepdims=True).shape)

@@ -266,3 +266,21 @@ def test_decode_magic_constants():
             k = max(e, 1) - 1
             mhs = (hi - k * (1 << 20)) & 0xFFFFFFFF
             assert mhs == (s << 31) | ((1 if e else 0) << 20) | m_hi
+
+
+def test_sparse_image_decoder_on_a_hand_built_image():
+    """The sparse wire format of include/xsum.h, built byte by byte: header then records
+    (digit << 6) | index; digit -3 at index 20 and 2^51 at index 21 (value -3 R^20 + 2^51 R^21)."""
+    import struct
+
+    import paper_1605_05436_b200 as xs
+    hdr = struct.pack("<IHBBIIQ", 0x41505358, 1, 52, 2, 4, 0, 12345)
+    recs = struct.pack("<qq", (-3 << 6) | 20, ((1 << 51) << 6) | 21)
+    d = xs.decode_sparse(hdr + recs)
+    assert d == {"flags": 4, "count": 12345, "digits": {20: -3, 21: 1 << 51}}
+    assert xs.SPARSE_MAX_BYTES == 24 + 8 * 42
+    import pytest
+    with pytest.raises(ValueError):
+        xs.decode_sparse(struct.pack("<IHBBIIQ", 0x41505359, 1, 52, 0, 0, 0, 0))   # bad magic
+    with pytest.raises(ValueError):
+        xs.decode_sparse(hdr + recs[:8])                                          # truncated

@@ -70,6 +70,8 @@ typedef enum xsum_status {
 #define XSUM_F_MISMATCH 32u  /* a merged state image was rejected (header mismatch) */
 #define XSUM_F_OVERFLOW32 64u /* the binary32 rounding (value_f32) overflowed to +-Inf */
 #define XSUM_F_INEXACT32 128u /* the binary32 rounding differs from the exact finite sum */
+#define XSUM_F_PEER_TIMEOUT 256u /* fused multi-GPU step: a peer's state did not arrive within ~2 s;
+                                   the value is NOT the group's sum (xsum_sum_allreduce) */
 
 /* Packed state image (XSUM_STATE_BYTES, little-endian). Exactly mergeable in any
  * order; it is also the checkpoint format and what ranks exchange.
@@ -228,6 +230,33 @@ XSUM_API xsum_status xsum_finalize_round(xsum_ctx *h, void *d_res, uint64_t *d_c
  * to finish merges the block partials and rounds). */
 XSUM_API xsum_status xsum_sum(xsum_ctx *h, const double *d_x, uint64_t n, void *d_res, uint64_t *d_canon,
                      void *stream);
+
+/* Fused multi-GPU step (SURVEY.md §8(e) fused option; the MapReduce post-process of
+ * PAPER.md:1151-1163 done over NVLink peer memory inside the accumulate kernel):
+ * every one of `world` ranks calls xsum_sum_allreduce with its own shard; in ONE launch per rank
+ * the shard is summed, the last block publishes the rank's state into every rank's exchange
+ * buffer (P2P stores), release-increments every rank's arrival counter, waits (acquire) for all
+ * world contributions and merges them in rank order with Lemma-1 adds, so every rank's state is
+ * the group's exact sum (bit-identical digits) and d_res / d_canon its rounding.
+ * d_bufs: DEVICE array of `world` pointers, d_bufs[r] = rank r's exchange buffer as mapped in
+ * this process (symmetric memory / CUDA IPC), each >= xsum_peer_buffer_bytes(world) bytes,
+ * 8-B aligned, zero-initialised before the first call. epoch: 1 for the first call on these
+ * buffers, then +1 per call (the same on every rank). All ranks must make the call (it is a
+ * collective); a peer that does not arrive within ~2 s sets XSUM_F_PEER_TIMEOUT instead of
+ * hanging. Errors: XSUM_EINVAL (rank >= world, world == 0, epoch == 0, null / misaligned
+ * pointers), XSUM_ECAPACITY, XSUM_ECUDA. */
+XSUM_API size_t xsum_peer_buffer_bytes(uint32_t world);
+XSUM_API xsum_status xsum_sum_allreduce(xsum_ctx *h, const double *d_x, uint64_t n, void *const *d_bufs,
+                                        uint32_t rank, uint32_t world, uint64_t epoch, void *d_res,
+                                        uint64_t *d_canon, void *stream);
+
+/* Self-test of the exchange protocol on ONE GPU: `world` (<= 64) virtual ranks, one thread block
+ * each, run the same device exchange as xsum_sum_allreduce in one cooperative launch (so all are
+ * co-resident): rank r publishes state image d_states[r] (regularized), waits and merges;
+ * writes the merged image d_out[r] and its rounding d_res[r] (xsum_result). d_bufs as above, on
+ * this device. Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_peer_selftest(const void *d_states, void *const *d_bufs, uint32_t world, uint64_t epoch,
+                                        void *d_res, void *d_out, void *stream);
 
 /* Cap the number of thread blocks an accumulate launch of this handle may use
  * (0 = one per SM, the default; values above 1024 are clamped). Lets a caller leave

@@ -31,6 +31,7 @@ MAGIC = 0x4D555358
 VERSION = 1
 F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT, F_MISMATCH = 1, 2, 4, 8, 16, 32
 F_OVERFLOW32, F_INEXACT32 = 64, 128
+F_PEER_TIMEOUT = 256
 
 OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 
@@ -45,7 +46,8 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_destroy", "xsum_count", "xsum_sum_segments", "xsum_sum_segments_csr", "xsum_status_str",
            "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round",
            "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
-           "xsum_to_sparse", "xsum_merge_sparse")
+           "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
+           "xsum_peer_selftest")
 
 
 class XsumError(RuntimeError):
@@ -87,6 +89,9 @@ def lib() -> ctypes.CDLL:
             "xsum_accumulate_f16": ([p, p, u64, p], i32), "xsum_accumulate_bf16": ([p, p, u64, p], i32),
             "xsum_sum_f16": ([p, p, u64, p, p, p], i32), "xsum_sum_bf16": ([p, p, u64, p, p, p], i32),
             "xsum_to_sparse": ([p, p, p, p], i32), "xsum_merge_sparse": ([p, p, p, u32, p], i32),
+            "xsum_peer_buffer_bytes": ([u32], sz),
+            "xsum_sum_allreduce": ([p, p, u64, p, u32, u32, u64, p, p, p], i32),
+            "xsum_peer_selftest": ([p, p, u32, u64, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -282,6 +287,16 @@ class Accumulator:
             self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
         return self._res, (self._canon if canon else None)
 
+    def sum_allreduce(self, x, bufs_dev: int, rank: int, world: int, epoch: int, canon: bool = False):
+        """Fused multi-GPU step (xsum_sum_allreduce): state := exact sum of every rank's shard, in
+        one launch per rank; `bufs_dev` is the device address of the array of the world exchange
+        buffer pointers (dist.PeerExchange sets it up). Returns the device (result, canon)."""
+        x = _as_f64_cuda(x)
+        _check("xsum_sum_allreduce", lib().xsum_sum_allreduce(
+            self._h, x.data_ptr(), x.numel(), bufs_dev, rank, world, epoch, self._res.data_ptr(),
+            self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
+        return self._res, (self._canon if canon else None)
+
     def to_sparse(self):
         """Sparse image of the state (xsum_to_sparse): (uint8 CUDA tensor of SPARSE_MAX_BYTES,
         its valid byte count as a host int)."""
@@ -332,6 +347,28 @@ class Accumulator:
         _check(name, getattr(lib(), name)(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
                                           self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
         return self._res, (self._canon if canon else None)
+
+
+def peer_buffer_bytes(world: int) -> int:
+    return int(lib().xsum_peer_buffer_bytes(world))
+
+
+def peer_selftest(states, world: int, epoch: int = 1, bufs=None):
+    """Run the fused multi-GPU exchange protocol with `world` virtual ranks on one GPU
+    (xsum_peer_selftest): states = uint8 CUDA tensor of world state images. Returns (list of
+    Result, merged images uint8 tensor [world*384], the exchange buffers for reuse)."""
+    torch = _torch()
+    dev = states.device
+    nb = peer_buffer_bytes(world)
+    if bufs is None:
+        bufs = [torch.zeros(nb, dtype=torch.uint8, device=dev) for _ in range(world)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=dev)
+    res = torch.zeros(world * RESULT_BYTES, dtype=torch.uint8, device=dev)
+    out = torch.zeros(world * STATE_BYTES, dtype=torch.uint8, device=dev)
+    _check("xsum_peer_selftest", lib().xsum_peer_selftest(states.data_ptr(), ptrs.data_ptr(), world, epoch,
+                                                          res.data_ptr(), out.data_ptr(), _stream_ptr(dev)))
+    rb = res.cpu().numpy().tobytes()
+    return [Result.from_bytes(rb[i * RESULT_BYTES:(i + 1) * RESULT_BYTES]) for i in range(world)], out, bufs
 
 
 def decode_sparse(b: bytes) -> dict:

@@ -54,6 +54,9 @@ xs::AccParams acc_params(xsum_ctx* h, int overwrite, xsum_result* res, uint64_t*
     p.canon = canon;
     p.one = 1;
     p.mone = 0xFFFFFFFFu;
+    p.peer.bufs = nullptr;
+    p.peer.rank = p.peer.world = 0;
+    p.peer.epoch = 0;
     return p;
 }
 
@@ -200,6 +203,38 @@ xsum_status xsum_sum(xsum_ctx* h, const double* d_x, uint64_t n, void* d_res, ui
                        static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
     h->count = n;
+    return XSUM_OK;
+}
+
+size_t xsum_peer_buffer_bytes(uint32_t world) { return xs::peer_buffer_bytes(world); }
+
+xsum_status xsum_sum_allreduce(xsum_ctx* h, const double* d_x, uint64_t n, void* const* d_bufs, uint32_t rank,
+                               uint32_t world, uint64_t epoch, void* d_res, uint64_t* d_canon, void* stream) {
+    if (!h || !d_res || !aligned(d_res, 8) || (d_canon && !aligned(d_canon, 8))) return XSUM_EINVAL;
+    if (n && (!d_x || !aligned(d_x, 8))) return XSUM_EINVAL;
+    if (!d_bufs || !aligned(d_bufs, 8) || world == 0 || rank >= world || epoch == 0) return XSUM_EINVAL;
+    if (n > kMaxCount) return XSUM_ECAPACITY;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    xs::AccParams p = acc_params(h, 1, static_cast<xsum_result*>(d_res), d_canon);
+    p.peer.bufs = reinterpret_cast<uint8_t* const*>(d_bufs);
+    p.peer.rank = rank;
+    p.peer.world = world;
+    p.peer.epoch = epoch;
+    if (xs::accumulate(d_x, n, p, grid_of(h), static_cast<cudaStream_t>(stream)) != cudaSuccess) return XSUM_ECUDA;
+    h->count = n;                                   // host mirror: this rank's shard
+    return XSUM_OK;
+}
+
+xsum_status xsum_peer_selftest(const void* d_states, void* const* d_bufs, uint32_t world, uint64_t epoch, void* d_res,
+                               void* d_out, void* stream) {
+    if (!d_states || !aligned(d_states, 8) || !d_bufs || !aligned(d_bufs, 8) || !d_res || !aligned(d_res, 8) ||
+        !d_out || !aligned(d_out, 8) || world == 0 || world > 64 || epoch == 0)
+        return XSUM_EINVAL;
+    if (xs::peer_selftest(static_cast<const xsum_state_image*>(d_states), reinterpret_cast<uint8_t* const*>(d_bufs),
+                          world, epoch, static_cast<xsum_result*>(d_res), static_cast<xsum_state_image*>(d_out),
+                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return XSUM_ECUDA;
     return XSUM_OK;
 }
 

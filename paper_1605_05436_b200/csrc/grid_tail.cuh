@@ -15,6 +15,75 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
     return v;
 }
 
+// Cross-GPU step of the fused multi-GPU sum (§6.1: the reducers' outputs
+// are gathered and merged by the post-process), run by warp 0 of the last block of every rank
+// on its rank's final state (b0, b1 regularized digits; fl, cnt): publish the state into slot
+// [epoch & 1][rank] of every rank's exchange buffer over NVLink (P2P stores), release-add one to
+// every rank's arrival counter, wait (acquire, bounded) until the own counter reaches
+// epoch*world, then merge the world slots in rank order with Lemma-1 adds, so
+// every rank holds bit-identical digits. A rank can be at most one call ahead of another (it
+// needs everyone's contribution to finish a call), hence two slot sets by epoch parity.
+// Returns false if the wait timed out (~2 s): the caller flags the result instead of hanging.
+__device__ __forceinline__ bool peer_exchange_merge(int64_t& b0, int64_t& b1, uint32_t& fl, uint64_t& cnt,
+                                                    const PeerParams& pp, int lane) {
+    const uint32_t world = pp.world, rank = pp.rank;
+    const size_t set = (size_t)(pp.epoch & 1) * world * XSUM_STATE_BYTES;
+    for (uint32_t r = 0; r < world; ++r) {
+        xsum_state_image* slot = reinterpret_cast<xsum_state_image*>(pp.bufs[r] + set + (size_t)rank * XSUM_STATE_BYTES);
+        slot->digit[lane] = b0;
+        if (lane + 32 < D) slot->digit[lane + 32] = b1;
+        if (lane == 0) {
+            slot->magic = XSUM_MAGIC;
+            slot->version = (uint16_t)XSUM_VERSION;
+            slot->w = (uint8_t)W;
+            slot->ndigits = (uint8_t)D;
+            slot->flags = fl;
+            slot->reserved = 0;
+            slot->count = cnt;
+        }
+    }
+    __threadfence_system();
+    __syncwarp();
+    bool ok = true;
+    if (lane == 0) {
+        for (uint32_t r = 0; r < world; ++r) {
+            unsigned long long* c = reinterpret_cast<unsigned long long*>(pp.bufs[r] + peer_counter_off(world));
+            asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(c) : "memory");
+        }
+        const unsigned long long* mine =
+            reinterpret_cast<const unsigned long long*>(pp.bufs[rank] + peer_counter_off(world));
+        const unsigned long long want = pp.epoch * world;
+        const long long t0 = clock64();
+        unsigned long long v;
+        while (true) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+            if (v >= want) break;
+            if (clock64() - t0 > (1ll << 32)) { ok = false; break; }   // ~2 s at 1.9 GHz
+            __nanosleep(64);
+        }
+    }
+    ok = __shfl_sync(FULL, ok ? 1 : 0, 0) != 0;
+    __syncwarp();
+    __threadfence_system();
+    int64_t a0 = 0, a1 = 0;
+    uint64_t c = 0;
+    uint32_t f = 0;
+    for (uint32_t r = 0; r < world; ++r) {               // fixed order: identical digits on every rank
+        const volatile xsum_state_image* slot =
+            reinterpret_cast<const volatile xsum_state_image*>(pp.bufs[rank] + set + (size_t)r * XSUM_STATE_BYTES);
+        const int64_t d0 = slot->digit[lane];
+        const int64_t d1 = (lane + 32 < D) ? slot->digit[lane + 32] : 0;
+        lemma1_add(a0, a1, d0, d1, lane);
+        c += slot->count;
+        f |= slot->flags;
+    }
+    b0 = a0;
+    b1 = a1;
+    cnt = c;
+    fl = f | (ok ? 0u : XSUM_F_PEER_TIMEOUT);
+    return ok;
+}
+
 // Call with all threads of the block. On entry warp 0 holds the block's regularized digits
 // (a0 = digit lane, a1 = digit lane+32) and `bflags` the block's flags; other warps' a0/a1
 // are ignored. `red` is >= D int64 of shared scratch, `su` 64 int64, `sh_flags`/`sh_last`
@@ -89,6 +158,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
             cnt += p.state->count;
         }
         regularize_warp(b0, b1, lane);
+        if (p.peer.bufs) peer_exchange_merge(b0, b1, fl, cnt, p.peer, lane);   // fused multi-GPU step
         p.state->digit[lane] = b0;
         if (lane + 32 < D) p.state->digit[lane + 32] = b1;
         if (lane == 0) {

@@ -6,6 +6,7 @@
 // Finalize: steps 6-7 of the PRAM algorithm, see finalize_warp.
 #include <cuda_runtime.h>
 
+#include "grid_tail.cuh"
 #include "xsum_device.cuh"
 #include "xsum_kernels.h"
 
@@ -122,7 +123,7 @@ k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_resul
         if (src.load(s, lane, scr[warp], d0, d1, c, f)) {
             lemma1_add(a0, a1, d0, d1, lane);
             cnt += c;
-            fl |= f & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH);
+            fl |= f & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT);
         } else {
             fl |= XSUM_F_MISMATCH;
         }
@@ -229,6 +230,47 @@ cudaError_t to_sparse(const xsum_state_image* st, void* out, uint32_t* nbytes, c
     k_to_sparse<<<1, 32, 0, s>>>(st, static_cast<uint8_t*>(out), nbytes);
     note_launch();
     return cudaGetLastError();
+}
+
+// One block per virtual rank: the exchange of the fused multi-GPU step on one device.
+__global__ void k_peer_selftest(const xsum_state_image* states, uint8_t* const* bufs, uint32_t world, uint64_t epoch,
+                                xsum_result* res, xsum_state_image* out) {
+    __shared__ int64_t su[64];
+    const int lane = threadIdx.x & 31;
+    const uint32_t r = blockIdx.x;
+    const xsum_state_image* in = states + r;
+    int64_t b0 = in->digit[lane], b1 = (lane + 32 < D) ? in->digit[lane + 32] : 0;
+    uint32_t fl = in->flags;
+    uint64_t cnt = in->count;
+    PeerParams pp;
+    pp.bufs = bufs;
+    pp.rank = r;
+    pp.world = world;
+    pp.epoch = epoch;
+    peer_exchange_merge(b0, b1, fl, cnt, pp, lane);
+    xsum_state_image* o = out + r;
+    o->digit[lane] = b0;
+    if (lane + 32 < D) o->digit[lane + 32] = b1;
+    if (lane < (int)sizeof(o->pad)) o->pad[lane] = 0;
+    if (lane == 0) {
+        o->magic = XSUM_MAGIC;
+        o->version = (uint16_t)XSUM_VERSION;
+        o->w = (uint8_t)W;
+        o->ndigits = (uint8_t)D;
+        o->reserved = 0;
+        o->flags = fl;
+        o->count = cnt;
+    }
+    xsum_result rr = finalize_warp(b0, b1, fl, cnt, nullptr, su, lane);
+    if (lane == 0) res[r] = rr;
+}
+
+cudaError_t peer_selftest(const xsum_state_image* states, uint8_t* const* bufs, uint32_t world, uint64_t epoch,
+                          xsum_result* res, xsum_state_image* out, cudaStream_t s) {
+    void* args[] = {(void*)&states, (void*)&bufs, (void*)&world, (void*)&epoch, (void*)&res, (void*)&out};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_peer_selftest, dim3(world), dim3(32), args, 0, s);
+    note_launch();
+    return e;
 }
 
 cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s) {

@@ -519,7 +519,7 @@ __device__ __forceinline__ xsum_result finalize_warp_inl(int64_t a0, int64_t a1,
     const uint32_t rf32 = __shfl_sync(FULL, rf, 1);
     if (lane == 0) {
         r.count = count;
-        uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH)) | rf | rf32;
+        uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT)) | rf | rf32;
         uint32_t v32 = (uint32_t)b32;
         if (!nzu) {                               // exact zero -> +0.0 (reading R9)
             r.msb_exp = INT32_MIN; r.sign = 0; r.sig53 = 0; r.exp2 = 0;

@@ -10,6 +10,18 @@
 
 namespace xs {
 
+// Fused multi-GPU step (SURVEY.md §8(e) fused option): the exchange buffers of the `world`
+// ranks, addressable by every rank (NVLink P2P / symmetric memory). Buffer layout:
+// [2][world][XSUM_STATE_BYTES] state slots (parity of the call's epoch) then a u64 arrival
+// counter that every rank's call increments once (monotone: epoch e is complete at e*world).
+struct PeerParams {
+    uint8_t* const* bufs;      // device array of the world buffer pointers (null: no exchange)
+    uint32_t rank, world;
+    uint64_t epoch;            // 1, 2, 3, ... per call on the same buffers
+};
+constexpr size_t peer_counter_off(uint32_t world) { return 2ull * world * XSUM_STATE_BYTES; }
+constexpr size_t peer_buffer_bytes(uint32_t world) { return peer_counter_off(world) + 64; }
+
 struct AccParams {
     xsum_state_image* state;   // handle state (device)
     int64_t* partial;          // [D][XS_MAXB] block partials, digit-major (scratch)
@@ -20,6 +32,7 @@ struct AccParams {
     uint64_t* canon;           // optional canonical image for the fused finalize
     uint32_t one;              // = 1  } opaque to the compiler: keeps selected integer ops as IMADs
     uint32_t mone;             // = -1 } on the FMA pipe instead of ALU-pipe IADD3s
+    PeerParams peer;           // fused cross-GPU exchange after the grid merge (bufs null: none)
 };
 
 // scratch layout: [0,256) counter; [256, 256 + 8*D*MAXB) partials; then MAXB u32 flags
@@ -39,6 +52,8 @@ cudaError_t merge_states(xsum_state_image* st, const void* states, uint32_t coun
 cudaError_t merge_sparse(xsum_state_image* st, const void* images, const uint64_t* offsets, uint32_t count,
                          cudaStream_t s);
 cudaError_t to_sparse(const xsum_state_image* st, void* out, uint32_t* nbytes, cudaStream_t s);
+cudaError_t peer_selftest(const xsum_state_image* states, uint8_t* const* bufs, uint32_t world, uint64_t epoch,
+                          xsum_result* res, xsum_state_image* out, cudaStream_t s);
 cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s);
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                          double* out, uint64_t* canon, uint32_t* flags, int num_sms, cudaStream_t s);

@@ -10,7 +10,7 @@ partition of the input is valid.
 """
 from __future__ import annotations
 
-from . import STATE_BYTES, Accumulator
+from . import STATE_BYTES, Accumulator, peer_buffer_bytes
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -60,3 +60,36 @@ def exact_sum_distributed(x, acc: Accumulator, total: Accumulator, group=None):
     states = gather_states(acc.state, group)
     res, _ = total.merge_round(states)
     return res
+
+
+class PeerExchange:
+    """Exchange buffers of the fused multi-GPU step (xsum_sum_allreduce): one per rank, mapped
+    into every rank's address space through torch symmetric memory (CUDA IPC over NVLink), zeroed
+    once; `epoch` counts the calls made on them (the kernel's arrival counters are monotone).
+
+    The step is ONE launch per rank: the shard's fused sum, then the last block publishes the
+    state to every peer (P2P stores), signals, waits for all and merges -
+    no NCCL call on the data path."""
+
+    def __init__(self, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        nbytes = peer_buffer_bytes(self.world)
+        self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        self.buf.zero_()
+        torch.cuda.synchronize(device)
+        self.handle = symm_mem.rendezvous(self.buf, self.group.group_name)
+        self.bufs_dev = int(self.handle.buffer_ptrs_dev)
+        self.epoch = 0
+        dist.barrier(group=self.group)
+
+    def sum(self, x, acc: Accumulator, canon: bool = False):
+        """State of `acc` := exact sum over all ranks' shards x (one launch); returns the device
+        (result, canon), bit-identical on every rank."""
+        self.epoch += 1
+        return acc.sum_allreduce(x, self.bufs_dev, self.rank, self.world, self.epoch, canon=canon)

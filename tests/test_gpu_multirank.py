@@ -57,3 +57,68 @@ def test_distributed_step_two_ranks_one_gpu(world):
     for rank, bits, flags, count, canon in got:
         assert bits == ref.bits and flags == ref.flags and count == n, rank
         assert (np.frombuffer(canon, dtype=np.uint64) == limbs).all(), rank
+
+
+# ------------------------------------------------------------------------------------------
+# fused multi-GPU step: the exchange protocol with virtual ranks in ONE cooperative launch
+# (one block per rank, all co-resident), the B200_PROFILING.md way of testing kernels that
+# wait on one another with fewer GPUs than ranks.
+# ------------------------------------------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_peer_exchange_protocol_virtual_ranks(world):
+    import numpy as np
+    import torch
+
+    import oracle
+    import paper_1605_05436_b200 as xsum
+    import synth
+    xsum.build()
+    n = 3_000_017
+    x = synth.gen.generate("c4", 5, n)
+    cuts = [n * r // world for r in range(world + 1)]
+    states = []
+    for r in range(world):
+        acc = xsum.Accumulator().add(torch.from_numpy(x[cuts[r]:cuts[r + 1]]).cuda())
+        states.append(acc.state.clone())
+    st = torch.cat(states)
+    ref, limbs = oracle.exact_sum(x)
+    bufs = None
+    for epoch in (1, 2, 3):                           # repeated calls: epoch parity slots, monotone counters
+        res, out, bufs = xsum.peer_selftest(st, world, epoch, bufs)
+        imgs = out.cpu().numpy().reshape(world, -1)
+        for r in range(world):
+            assert res[r].bits == ref.bits and res[r].flags == ref.flags and res[r].count == n, (world, epoch, r)
+            assert (imgs[r] == imgs[0]).all()         # bit-identical digits on every rank
+        m = xsum.Accumulator().merge(out[:384].clone())
+        _, canon = m.exact()
+        assert (canon == limbs).all()
+
+
+@pytest.mark.gpu
+def test_fused_allreduce_single_rank_world():
+    """xsum_sum_allreduce with world = 1 (its own buffer as the only peer): the fused kernel's
+    exchange path end to end on the real accumulate launch."""
+    import torch
+
+    import oracle
+    import paper_1605_05436_b200 as xsum
+    import synth
+    xsum.build()
+    x = synth.gen.generate("c2", 8, 2_000_003)
+    buf = torch.zeros(xsum.peer_buffer_bytes(1), dtype=torch.uint8, device="cuda")
+    ptrs = torch.tensor([buf.data_ptr()], dtype=torch.int64, device="cuda")
+    acc = xsum.Accumulator()
+    ref, limbs = oracle.exact_sum(x)
+    d = torch.from_numpy(x).cuda()
+    for epoch in (1, 2, 3, 4):
+        res, canon = acc.sum_allreduce(d, ptrs.data_ptr(), 0, 1, epoch, canon=True)
+        r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+        assert r.bits == ref.bits and r.flags == ref.flags and r.count == x.size
+        assert (canon.cpu().numpy().view("u8") == limbs).all()
+    # a missing peer (world 2, nobody else calls) times out instead of hanging
+    b2 = [torch.zeros(xsum.peer_buffer_bytes(2), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    ptrs2 = torch.tensor([b.data_ptr() for b in b2], dtype=torch.int64, device="cuda")
+    res, _ = acc.sum_allreduce(d, ptrs2.data_ptr(), 0, 2, 1)
+    r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+    assert r.flags & xsum.F_PEER_TIMEOUT

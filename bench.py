@@ -313,6 +313,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
     peak, peak_src = measured_peak_hbm()
     achieved = 8.0 * n_local / (kern_ms / 1e3) / 1e9
+    # context for the roofline: a pure streaming read of the same input in the same run (the
+    # best read-only probe configuration of profiles/r01_microbench.txt: 296 blocks x 512 threads,
+    # 8 x 16-B loads in flight per thread), untimed by the step
+    try:
+        probe_gbs = synth.probe_read_gbs(x, 1, 2 * torch.cuda.get_device_properties(dev).multi_processor_count,
+                                         512, reps=10)
+    except Exception:  # noqa: BLE001
+        probe_gbs = None
 
     # check the result once (device result vs nothing host-side: the parity tests do that)
     e2e = None
@@ -338,7 +346,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
                          "kernel": "k_accumulate" if not seg else "k_segments",
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": 8 * n_local,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src, "read_probe_gbs": probe_gbs,
+                         "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e,

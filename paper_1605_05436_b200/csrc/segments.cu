@@ -12,7 +12,10 @@
 namespace xs {
 
 constexpr int SEG_WARPS = 8;
-constexpr int SEG_U = 4;
+#ifndef XS_SEG_U
+#define XS_SEG_U 4
+#endif
+constexpr int SEG_U = XS_SEG_U;
 constexpr int SEG_FLUSH_ITERS = FLUSH_ELEMS / (2 * SEG_U);
 constexpr size_t SEG_SMEM = (size_t)SEG_WARPS * D * 32 * sizeof(int64_t);
 

@@ -16,8 +16,10 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "f32b_nb4": ["-DXS_F32B_NB=4"],
-    "f32b_nb3": ["-DXS_F32B_NB=3"],
+    "seg_u8nb2": ["-DXS_SEG_U=8", "-DXS_SEG_NB=2"],
+    "seg_u2nb4": ["-DXS_SEG_U=2", "-DXS_SEG_NB=4"],
+    "seg_u2nb8": ["-DXS_SEG_U=2", "-DXS_SEG_NB=8"],
+    "seg_u4nb4": ["-DXS_SEG_U=4", "-DXS_SEG_NB=4"],
 }
 
 

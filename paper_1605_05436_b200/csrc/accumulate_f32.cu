@@ -33,6 +33,8 @@ constexpr int F32B_REG_FLUSHES = 256;      // <= 4 chunks per digit per flush: 2
 constexpr int F32B_BASE = 925;             // window bit position of k = 0 (2^-149 = 2^925 * 2^-1074)
 constexpr uint32_t F32B_SPEC_EP = 255;      // exponent field of NaN/Inf
 
+static_assert(F32B_FLUSH * (((1ull << 24) - 1) << 31) < (1ull << 63), "bin window too long");
+static_assert((16 + 1) * (((1ull << 24) - 1) << 31) < (1ull << 63), "leftovers (after a flush) overflow a bin");
 __host__ __device__ constexpr int f32b_pos(int g) { return F32B_BASE - 1 + 32 * g; }   // bin g's bit position
 
 // One summand: bits b. ep = max(e,1); M = h + 2^23 - ep 2^23 = m + [e!=0] 2^23; bin ep >> 5 gets
@@ -74,6 +76,9 @@ __device__ __forceinline__ void f32b_flush(int64_t* bins, int64_t* col) {
         const int64_t c1 = (V >> (W - o)) & (int64_t)MASK;
         const int64_t c2 = V >> (2 * W - o < 63 ? 2 * W - o : 63);
         XS_ASSERT(i + 2 < D - 1);
+        XS_ASSERT(col[i * 32] > -0x7FC0000000000000ll && col[i * 32] < 0x7FC0000000000000ll);
+        XS_ASSERT(col[(i + 1) * 32] > -0x7FC0000000000000ll && col[(i + 1) * 32] < 0x7FC0000000000000ll);
+        XS_ASSERT(col[(i + 2) * 32] > -0x7FC0000000000000ll && col[(i + 2) * 32] < 0x7FC0000000000000ll);
         col[i * 32] += c0;
         col[(i + 1) * 32] += c1;
         col[(i + 2) * 32] += c2;

@@ -40,6 +40,12 @@ struct H16Fmt {
 // 511 * 255 * 2^15 < 2^32. Window bit positions: binary16 k + 1050, bfloat16 k + 941.
 using FmtF16 = H16Fmt<10, 5, 3, 16383, 1050>;
 using FmtBF16 = H16Fmt<7, 8, 4, 511, 941>;
+// a window of FLUSH adds of the largest M 2^o cannot wrap an unsigned 32-bit bin
+template <class F>
+constexpr bool flush_fits() {
+    return (unsigned long long)F::FLUSH * ((2ull << F::t) - 1) * (1ull << ((1 << F::SB) - 1)) < (1ull << 32);
+}
+static_assert(flush_fits<FmtF16>() && flush_fits<FmtBF16>(), "bin window too long");
 
 constexpr int H16_WARPS = 16;
 constexpr int H16_U = 4;          // 16-B vectors per thread per tile (8 summands each)
@@ -138,6 +144,7 @@ template <class F>
 __device__ __forceinline__ bool h16_flush(uint32_t* bins, int64_t* bins64) {
 #pragma unroll
     for (int b = 0; b < F::NBIN64; ++b) {
+        XS_ASSERT(bins64[b * 32] >= 0 && bins64[b * 32] < (1ll << 62));      // < 2^40 summands per launch
         bins64[b * 32] += (int64_t)bins[b * 32];
         bins[b * 32] = 0;
     }

@@ -38,6 +38,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    # testing the N>1 host path with several ranks on ONE GPU (gloo, no fused exchange: no kernel
+    # waits on another rank then); the driver's runs use the defaults
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-fused", action="store_true")
     return ap.parse_args()
 
 
@@ -216,11 +220,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     import synth
     from paper_1605_05436_b200 import dist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group("gloo")
     xsum.build()
     synth.build()
     wl = workload(args.config, world)
@@ -245,12 +253,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # or, if the peer buffers cannot be set up on this machine, local sum + NCCL all-gather +
     # merge_round
     pe, exchange = None, None
-    if world > 1 and not seg:
+    if world > 1 and not seg and not args.no_fused and args.dist_backend == "nccl":
         try:
             pe = dist.PeerExchange(dev)
             exchange = "fused: one launch per rank, NVLink P2P state exchange (xsum_sum_allreduce)"
         except Exception as e:  # noqa: BLE001
             exchange = f"NCCL all-gather of 384-B states + xsum_merge_round (peer buffers unavailable: {e!r:.120})"
+    elif world > 1 and not seg:
+        exchange = f"{args.dist_backend} all-gather of 384-B states + xsum_merge_round"
 
     def step():
         if seg:
@@ -287,15 +297,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         bits = torch.tensor([rr.bits - (1 << 64) if rr.bits >> 63 else rr.bits, rr.flags], dtype=torch.int64,
                             device=dev)
         lo, hi = bits.clone(), bits.clone()
-        torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
-        torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+        allreduce_(lo, torch.distributed.ReduceOp.MIN)
+        allreduce_(hi, torch.distributed.ReduceOp.MAX)
         if not torch.equal(lo, hi) or int(hi[1]) & xsum.F_PEER_TIMEOUT:
             raise RuntimeError(f"ranks disagree or the peer exchange timed out: {lo.tolist()} {hi.tolist()}")
     per = [a.elapsed_time(b) for a, b in ev]                 # ms per step (device)
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        allreduce_(t, torch.distributed.ReduceOp.MAX)
     total_ms = float(t.item())
     n_all = n_local * world
     value = n_all * K / (total_ms / 1e3)
@@ -388,6 +398,19 @@ def measure_e2e(xsum, torch, x_dev, steps: int, dev):
             "ms_per_step": dt * 1e3, "api": "xsum_reset + xsum_accumulate_host + xsum_finalize_round + D2H"}
 
 
+def allreduce_(t, op):
+    """In-place all-reduce of a small CUDA tensor (host-staged for gloo process groups)."""
+    import torch
+    import torch.distributed as tdist
+    if tdist.get_backend() == "gloo":
+        h = t.cpu()
+        tdist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        tdist.all_reduce(t, op=op)
+    return t
+
+
 def measure_e2e_multi(xsum, torch, dist, x_dev, steps: int, dev, pe, acc, tot, world: int):
     """N > 1: per step every rank copies its shard from pinned host memory to the device, runs
     the multi-GPU step (fused or NCCL, as timed above) and reads the 48-byte result back;
@@ -415,7 +438,7 @@ def measure_e2e_multi(xsum, torch, dist, x_dev, steps: int, dev, pe, acc, tot, w
         one()
     torch.cuda.synchronize()
     dt = torch.tensor([(time.perf_counter() - t0) / steps], dtype=torch.float64, device=dev)
-    torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+    allreduce_(dt, torch.distributed.ReduceOp.MAX)
     dt = float(dt.item())
     return {"value": n * world / dt, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
             "d2h_bytes_per_step": xsum.RESULT_BYTES * world, "ms_per_step": dt * 1e3,

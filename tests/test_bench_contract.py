@@ -7,6 +7,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -40,3 +42,39 @@ def test_graft_entry_has_build_and_smoke():
     sys.path.insert(0, ROOT)
     import __graft_entry__ as g
     assert callable(g.build) and callable(g.smoke)
+
+
+def _json_line(stdout: str) -> dict:
+    lines = [l for l in stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_our_arm_one_gpu_contract():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "5", "--warmup", "3",
+                          "--config", "c1", "--e2e-steps", "1"], capture_output=True, text=True, timeout=900,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = _json_line(out.stdout)
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3 and d["value"] > 0
+    assert d["gpu_launches"] == 5                       # one fused launch per step
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["n_per_gpu"] and d["e2e"]["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["clocks"]["sm_max_mhz"]
+
+
+@pytest.mark.gpu
+def test_our_arm_two_ranks_host_path_on_one_gpu():
+    """The N>1 host path of bench.py (launch, barrier, max over ranks, e2e, cross-rank result
+    check) with 2 ranks sharing one GPU over gloo; no fused exchange (its kernels would wait on
+    each other, which must not run as separate launches on one GPU)."""
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29571", os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "3", "--warmup", "3", "--config", "c1", "--dist-backend", "gloo",
+                          "--e2e-steps", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = _json_line(out.stdout)
+    assert d["n_gpus"] == 2 and d["config"]["n_total"] == 2 * d["config"]["n_per_gpu"]
+    assert d["gpu_launches"] == 6 and d["e2e"]["h2d_bytes_per_step"] == 2 * 8 * d["config"]["n_per_gpu"]

@@ -278,6 +278,22 @@ XSUM_API uint64_t xsum_count(const xsum_ctx *h);
 XSUM_API xsum_status xsum_sum_segments(const double *d_x, uint64_t nseg, uint64_t seg_len, double *d_out,
                               uint64_t *d_canon, uint32_t *d_flags, void *stream);
 
+/* Element formats of xsum_sum_segments_ex. */
+#define XSUM_DT_F64 0   /* IEEE binary64 */
+#define XSUM_DT_F32 1   /* IEEE binary32 */
+#define XSUM_DT_F16 2   /* IEEE binary16 (bit patterns) */
+#define XSUM_DT_BF16 3  /* bfloat16 (bit patterns) */
+
+/* Segmented exact sums of any input format (SURVEY.md §8(f) f1 x f2): segment s is
+ * d_x[s*seg_len .. (s+1)*seg_len) or, if d_offsets != NULL, d_x[d_offsets[s] .. d_offsets[s+1])
+ * (elements of `dtype`, d_x aligned to the element size). Per segment, optional outputs: d_out[s]
+ * the RN-even binary64 and d_out32[s] the RN-even binary32 of the exact sum (each rounded once
+ * from the exact value), d_canon[s*34 ..] the canonical image, d_flags[s]. One warp per segment.
+ * Errors: XSUM_EINVAL (bad dtype, null / misaligned pointers, no output requested), XSUM_ECUDA. */
+XSUM_API xsum_status xsum_sum_segments_ex(const void *d_x, int dtype, uint64_t nseg, uint64_t seg_len,
+                                          const uint64_t *d_offsets, double *d_out, float *d_out32,
+                                          uint64_t *d_canon, uint32_t *d_flags, void *stream);
+
 /* Variable-length segments (CSR offsets): segment s is
  * d_x[d_offsets[s] .. d_offsets[s+1]), offsets non-decreasing device u64 array of nseg+1.
  * Outputs as xsum_sum_segments. Errors: XSUM_EINVAL, XSUM_ECUDA. */

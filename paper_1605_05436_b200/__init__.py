@@ -47,7 +47,7 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round",
            "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
-           "xsum_peer_selftest")
+           "xsum_peer_selftest", "xsum_sum_segments_ex")
 
 
 class XsumError(RuntimeError):
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
             "xsum_peer_buffer_bytes": ([u32], sz),
             "xsum_sum_allreduce": ([p, p, u64, p, u32, u32, u64, p, p, p], i32),
             "xsum_peer_selftest": ([p, p, u32, u64, p, p, p], i32),
+            "xsum_sum_segments_ex": ([p, i32, u64, u64, p, p, p, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -414,35 +415,51 @@ def fsum(x) -> float:
     return r.value_f32 if _is_f32(x) else r.value
 
 
-def sum_segments(x, seg_len: int, canon: bool = False, flags: bool = False):
-    """Per-segment exact sums of a float64 CUDA tensor split into equal segments of seg_len.
-    Returns (values[nseg] f64, canon[nseg,34] or None, flags[nseg] or None) on the device."""
+_DT = {"float64": 0, "float32": 1, "float16": 2, "bfloat16": 3}
+
+
+def _as_seg_input(t):
     torch = _torch()
-    x = _as_f64_cuda(x)
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if t.dtype not in (torch.float64, torch.float32, torch.float16, torch.bfloat16):
+        raise TypeError(f"expected float64 / float32 / float16 / bfloat16, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t
+
+
+def sum_segments(x, seg_len: int, canon: bool = False, flags: bool = False):
+    """Per-segment exact sums of a CUDA tensor split into equal segments of seg_len. Values are
+    the RN-even rounding of each exact sum: float64 for float64 input, float32 (the binary32
+    rounding, one rounding from the exact value) for float32 / float16 / bfloat16 input.
+    Returns (values[nseg], canon[nseg,34] or None, flags[nseg] or None) on the device."""
+    x = _as_seg_input(x)
     if seg_len <= 0 or x.numel() % seg_len:
         raise ValueError("x.numel() must be a positive multiple of seg_len")
-    nseg = x.numel() // seg_len
-    return _segments(x, nseg, seg_len, None, canon, flags)
+    return _segments(x, x.numel() // seg_len, seg_len, None, canon, flags)
 
 
 def sum_segments_csr(x, offsets, canon: bool = False, flags: bool = False):
     """Variable-length segments: segment s = x[offsets[s]:offsets[s+1]] (offsets int64 CUDA)."""
     torch = _torch()
-    x = _as_f64_cuda(x)
+    x = _as_seg_input(x)
     if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous() and offsets.numel() >= 1):
         raise TypeError("offsets must be a contiguous int64 CUDA tensor of nseg+1 entries")
     return _segments(x, offsets.numel() - 1, 0, offsets, canon, flags)
 
 
 def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
-    """Exact reduction of a float64 CUDA tensor along one dimension: every
-    output element is the correctly rounded (RN-even) sum of its fibre, independent of order -
-    a reproducible torch.sum(x, dim). The fibres are laid out as equal contiguous segments
-    (a movedim + contiguous copy when `dim` is not the last dimension) and summed by
-    xsum_sum_segments, one warp per fibre."""
+    """Exact reduction of a CUDA tensor along one dimension: every output
+    element is the correctly rounded (RN-even) sum of its fibre, independent of order - a
+    reproducible torch.sum(x, dim). float64 input gives float64, float32 / float16 / bfloat16
+    input the float32 rounding of the exact sum. The fibres are laid out as equal contiguous
+    segments (a movedim + contiguous copy when `dim` is not the last dimension) and summed by
+    xsum_sum_segments_ex, one warp per fibre."""
     torch = _torch()
-    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64:
-        raise TypeError("expected a float64 CUDA tensor")
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype not in (torch.float64, torch.float32,
+                                                                           torch.float16, torch.bfloat16):
+        raise TypeError("expected a float64 / float32 / float16 / bfloat16 CUDA tensor")
     if x.dim() == 0:
         raise ValueError("exact_sum_dim needs a tensor with at least one dimension")
     d = dim % x.dim()
@@ -453,31 +470,25 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
     for s_ in out_shape:
         nseg *= s_
     if nseg == 0:
-        out = torch.empty(out_shape, dtype=torch.float64, device=x.device)
+        out = torch.empty(out_shape, dtype=torch.float64 if x.dtype == torch.float64 else torch.float32,
+                          device=x.device)
     else:
-        out, _, _ = _segments(xt.reshape(-1) if xt.numel() else torch.zeros(1, dtype=torch.float64,
-                                                                             device=x.device),
-                              nseg, seg, None, False, False)
+        out, _, _ = _segments(xt.reshape(-1), nseg, seg, None, False, False)
         out = out.reshape(out_shape)
     return out.unsqueeze(d) if keepdim else out
 
 
 def _segments(x, nseg, seg_len, offsets, canon, flags):
     torch = _torch()
-    out = torch.empty(nseg, dtype=torch.float64, device=x.device)
+    f64 = x.dtype == torch.float64
+    out = torch.empty(nseg, dtype=torch.float64 if f64 else torch.float32, device=x.device)
     cn = torch.empty((nseg, CANON_LIMBS), dtype=torch.int64, device=x.device) if canon else None
     fl = torch.empty(nseg, dtype=torch.int32, device=x.device) if flags else None
-    L = lib()
-    st = _stream_ptr(x.device)
-    if offsets is None:
-        rc = L.xsum_sum_segments(x.data_ptr(), nseg, seg_len, out.data_ptr(),
-                                 cn.data_ptr() if cn is not None else None,
-                                 fl.data_ptr() if fl is not None else None, st)
-        _check("xsum_sum_segments", rc)
-    else:
-        xp = x if x.numel() else torch.zeros(1, dtype=torch.float64, device=x.device)
-        rc = L.xsum_sum_segments_csr(xp.data_ptr(), offsets.data_ptr(), nseg, out.data_ptr(),
-                                     cn.data_ptr() if cn is not None else None,
-                                     fl.data_ptr() if fl is not None else None, st)
-        _check("xsum_sum_segments_csr", rc)
+    xp = x if x.numel() else torch.zeros(8, dtype=x.dtype, device=x.device)
+    rc = lib().xsum_sum_segments_ex(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
+                                    offsets.data_ptr() if offsets is not None else None,
+                                    out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
+                                    cn.data_ptr() if cn is not None else None,
+                                    fl.data_ptr() if fl is not None else None, _stream_ptr(x.device))
+    _check("xsum_sum_segments_ex", rc)
     return out, cn, fl

@@ -411,7 +411,7 @@ xsum_status xsum_sum_segments(const double* d_x, uint64_t nseg, uint64_t seg_len
     if (seg_len && nseg > kMaxCount / seg_len) return XSUM_EINVAL;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
-    if (xs::sum_segments(d_x, nseg, seg_len, nullptr, d_out, d_canon, d_flags, sms_of(dev),
+    if (xs::sum_segments(d_x, nseg, seg_len, nullptr, xs::SegOut{d_out, nullptr, d_canon, d_flags}, sms_of(dev),
                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
     return XSUM_OK;
@@ -426,10 +426,35 @@ xsum_status xsum_sum_segments_csr(const double* d_x, const uint64_t* d_offsets, 
     if (!d_x || !aligned(d_x, 8)) return XSUM_EINVAL;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
-    if (xs::sum_segments(d_x, nseg, 0, d_offsets, d_out, d_canon, d_flags, sms_of(dev),
+    if (xs::sum_segments(d_x, nseg, 0, d_offsets, xs::SegOut{d_out, nullptr, d_canon, d_flags}, sms_of(dev),
                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
     return XSUM_OK;
+}
+
+xsum_status xsum_sum_segments_ex(const void* d_x, int dtype, uint64_t nseg, uint64_t seg_len,
+                                 const uint64_t* d_offsets, double* d_out, float* d_out32, uint64_t* d_canon,
+                                 uint32_t* d_flags, void* stream) {
+    if (dtype < XSUM_DT_F64 || dtype > XSUM_DT_BF16) return XSUM_EINVAL;
+    if (nseg == 0) return XSUM_OK;
+    if (!d_out && !d_out32 && !d_canon && !d_flags) return XSUM_EINVAL;
+    if ((d_out && !aligned(d_out, 8)) || (d_out32 && !aligned(d_out32, 4)) || (d_canon && !aligned(d_canon, 8)) ||
+        (d_flags && !aligned(d_flags, 4)) || (d_offsets && !aligned(d_offsets, 8)))
+        return XSUM_EINVAL;
+    const uintptr_t esz = dtype == XSUM_DT_F64 ? 8 : (dtype == XSUM_DT_F32 ? 4 : 2);
+    if ((d_offsets || seg_len) && (!d_x || !aligned(d_x, esz))) return XSUM_EINVAL;
+    if (!d_offsets && seg_len && nseg > kMaxCount / seg_len) return XSUM_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
+    const xs::SegOut o{d_out, d_out32, d_canon, d_flags};
+    cudaError_t e;
+    if (dtype == XSUM_DT_F64)
+        e = xs::sum_segments(static_cast<const double*>(d_x), nseg, d_offsets ? 0 : seg_len, d_offsets, o, sms_of(dev),
+                             static_cast<cudaStream_t>(stream));
+    else
+        e = xs::sum_segments_small(d_x, dtype, nseg, d_offsets ? 0 : seg_len, d_offsets, o, sms_of(dev),
+                                   static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? XSUM_OK : XSUM_ECUDA;
 }
 
 }  // extern "C"

@@ -35,8 +35,7 @@ __device__ __noinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_
 // < 2^57), regularize, canonicalize and round, write
 // the outputs, and zero the lane column for the next segment.
 __device__ __noinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
-                                              uint64_t len, uint64_t s, double* out, uint64_t* canon,
-                                              uint32_t* oflags, int lane) {
+                                              uint64_t len, uint64_t s, const SegOut& o, int lane) {
     __syncwarp();
     int64_t a0, a1;
     combine_raw_columns(wb, a0, a1, lane);           // lane columns need no regularization
@@ -44,17 +43,13 @@ __device__ __noinline__ void segment_epilogue(int64_t* col, const int64_t* wb, i
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
     flags = __reduce_or_sync(FULL, flags);
-    xsum_result r = finalize_warp(a0, a1, flags, len, canon ? canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
-    if (lane == 0) {
-        out[s] = r.value;
-        if (oflags) oflags[s] = r.flags;
-    }
+    xsum_result r = finalize_warp(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
+    if (lane == 0) o.write(s, r);
 }
 
 __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
 k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
-           double* __restrict__ out, uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one,
-           uint32_t mone) {
+           SegOut o, uint32_t one, uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -132,7 +127,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
                 seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
             }
         }
-        segment_epilogue(col, win + warp * (D * 32), su[warp], flags, len, s, out, canon, oflags, lane);
+        segment_epilogue(col, win + warp * (D * 32), su[warp], flags, len, s, o, lane);
     }
 }
 
@@ -160,8 +155,8 @@ __device__ __noinline__ void seg_rescan_uniform(int64_t* col, const uint4* seg, 
 }
 
 __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
-k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, double* __restrict__ out,
-                   uint64_t* __restrict__ canon, uint32_t* __restrict__ oflags, uint32_t one, uint32_t mone) {
+k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one,
+                   uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -243,12 +238,9 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
             int64_t a0, a1;
             sums_to_digits(d, a0, a1, lane);
             const uint32_t fl = __reduce_or_sync(FULL, flags);
-            xsum_result r = finalize_warp_inl(a0, a1, fl, seg_len, canon ? canon + ps * XSUM_CANON_LIMBS : nullptr,
+            xsum_result r = finalize_warp_inl(a0, a1, fl, seg_len, o.canon ? o.canon + ps * XSUM_CANON_LIMBS : nullptr,
                                               su[warp], lane);
-            if (lane == 0) {
-                out[ps] = r.value;
-                if (oflags) oflags[ps] = r.flags;
-            }
+            if (lane == 0) o.write(ps, r);
             flags = 0;
             wstart = 0;                                        // window tiles of the next segment start at 0
             pt = 0;
@@ -269,8 +261,8 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
     }
 }
 
-cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, double* out,
-                         uint64_t* canon, uint32_t* flags, int num_sms, cudaStream_t s) {
+cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
+                         int num_sms, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SEG_SMEM);
@@ -285,9 +277,9 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     const bool uniform = !offsets && seg_len >= SEG_TILE && seg_len % ((uint64_t)SEG_TILE * SEG_NB) == 0 &&
                          ((uintptr_t)x & 15) == 0 && seg_len / SEG_TILE < (1u << 31);
     if (uniform)
-        k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, out, canon, flags, 1u, 0xFFFFFFFFu);
+        k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
     else
-        k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, out, canon, flags, 1u, 0xFFFFFFFFu);
+        k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, o, 1u, 0xFFFFFFFFu);
     note_launch();
     return cudaGetLastError();
 }

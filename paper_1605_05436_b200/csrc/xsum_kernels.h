@@ -55,7 +55,23 @@ cudaError_t to_sparse(const xsum_state_image* st, void* out, uint32_t* nbytes, c
 cudaError_t peer_selftest(const xsum_state_image* states, uint8_t* const* bufs, uint32_t world, uint64_t epoch,
                           xsum_result* res, xsum_state_image* out, cudaStream_t s);
 cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s);
-cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
-                         double* out, uint64_t* canon, uint32_t* flags, int num_sms, cudaStream_t s);
+// Per-segment outputs (any may be null): binary64 / binary32 roundings, canonical images, flags.
+struct SegOut {
+    double* out;
+    float* out32;
+    uint64_t* canon;
+    uint32_t* flags;
+    __device__ __forceinline__ void write(uint64_t s, const xsum_result& r) const {
+        if (out) out[s] = r.value;
+        if (out32) out32[s] = __uint_as_float(r.value_f32);
+        if (flags) flags[s] = r.flags;
+    }
+};
+
+cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
+                         int num_sms, cudaStream_t s);
+// binary32 / binary16 / bfloat16 elements (dtype XSUM_DT_F32 / F16 / BF16), equal or CSR segments
+cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
+                               const SegOut& o, int num_sms, cudaStream_t s);
 
 }  // namespace xs

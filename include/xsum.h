@@ -54,6 +54,12 @@ typedef enum xsum_status {
     XSUM_ENOMEM = 5      /* host allocation failed */
 } xsum_status;
 
+/* Element formats (xsum_sum_segments_ex, xsum_accumulate_host_ex). */
+#define XSUM_DT_F64 0   /* IEEE binary64 */
+#define XSUM_DT_F32 1   /* IEEE binary32 */
+#define XSUM_DT_F16 2   /* IEEE binary16 (bit patterns) */
+#define XSUM_DT_BF16 3  /* bfloat16 (bit patterns) */
+
 #define XSUM_RADIX_BITS 52          /* w: R = 2^52 */
 #define XSUM_NDIGITS 42             /* D */
 #define XSUM_STATE_BYTES 384        /* packed state image, see below */
@@ -188,6 +194,11 @@ XSUM_API xsum_status xsum_sum_bf16(xsum_ctx *h, const uint16_t *d_x, uint64_t n,
 XSUM_API xsum_status xsum_accumulate_host(xsum_ctx *h, const double *h_x, uint64_t n, void *d_stage,
                                  size_t stage_bytes, void *stream);
 
+/* The same for a host buffer of any element format (dtype XSUM_DT_*; the element size sets the
+ * chunking). Errors: as xsum_accumulate_host, plus XSUM_EINVAL for a bad dtype. */
+XSUM_API xsum_status xsum_accumulate_host_ex(xsum_ctx *h, const void *h_x, uint64_t n, int dtype, void *d_stage,
+                                             size_t stage_bytes, void *stream);
+
 /* State += sum of `count` packed state images at d_states (count * XSUM_STATE_BYTES bytes,
  * 8-B aligned): the MapReduce post-process / all-gather merge (§6.1),
  * a Lemma-1 pairwise tree of carry-free additions. Images with a bad
@@ -277,12 +288,6 @@ XSUM_API uint64_t xsum_count(const xsum_ctx *h);
  * Errors: XSUM_EINVAL, XSUM_ECUDA. */
 XSUM_API xsum_status xsum_sum_segments(const double *d_x, uint64_t nseg, uint64_t seg_len, double *d_out,
                               uint64_t *d_canon, uint32_t *d_flags, void *stream);
-
-/* Element formats of xsum_sum_segments_ex. */
-#define XSUM_DT_F64 0   /* IEEE binary64 */
-#define XSUM_DT_F32 1   /* IEEE binary32 */
-#define XSUM_DT_F16 2   /* IEEE binary16 (bit patterns) */
-#define XSUM_DT_BF16 3  /* bfloat16 (bit patterns) */
 
 /* Segmented exact sums of any input format (SURVEY.md §8(f) f1 x f2): segment s is
  * d_x[s*seg_len .. (s+1)*seg_len) or, if d_offsets != NULL, d_x[d_offsets[s] .. d_offsets[s+1])

@@ -47,7 +47,7 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round",
            "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
-           "xsum_peer_selftest", "xsum_sum_segments_ex")
+           "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex")
 
 
 class XsumError(RuntimeError):
@@ -93,6 +93,7 @@ def lib() -> ctypes.CDLL:
             "xsum_sum_allreduce": ([p, p, u64, p, u32, u32, u64, p, p, p], i32),
             "xsum_peer_selftest": ([p, p, u32, u64, p, p, p], i32),
             "xsum_sum_segments_ex": ([p, i32, u64, u64, p, p, p, p, p, p], i32),
+            "xsum_accumulate_host_ex": ([p, p, u64, i32, p, sz, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -250,17 +251,21 @@ class Accumulator:
         return self
 
     def add_host(self, x, stage_bytes: int = 128 << 20) -> "Accumulator":
-        """Sum a host float64 array/tensor (pinned memory overlaps copy and compute)."""
+        """Sum a host array/tensor (float64, float32, float16 or bfloat16; pinned memory overlaps
+        copy and compute) through double-buffered staging chunks (xsum_accumulate_host_ex)."""
         torch = _torch()
         if isinstance(x, np.ndarray):
-            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
-        if x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
-            raise TypeError("expected a contiguous host float64 array")
+            if x.dtype not in (np.float64, np.float32, np.float16):
+                x = np.asarray(x, dtype=np.float64)
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        if x.is_cuda or x.dtype not in (torch.float64, torch.float32, torch.float16, torch.bfloat16) or \
+                not x.is_contiguous():
+            raise TypeError("expected a contiguous host float64 / float32 / float16 / bfloat16 array")
         if self._stage is None or self._stage.numel() < stage_bytes:
             self._stage = torch.empty(stage_bytes, dtype=torch.uint8, device=self.device)
-        _check("xsum_accumulate_host", lib().xsum_accumulate_host(
-            self._h, x.data_ptr(), x.numel(), self._stage.data_ptr(), self._stage.numel(),
-            _stream_ptr(self.device)))
+        _check("xsum_accumulate_host_ex", lib().xsum_accumulate_host_ex(
+            self._h, x.data_ptr(), x.numel(), _DT[str(x.dtype).replace("torch.", "")], self._stage.data_ptr(),
+            self._stage.numel(), _stream_ptr(self.device)))
         self._host_ref = x          # keep alive until the stream passes the copies
         return self
 

@@ -278,12 +278,16 @@ xsum_status xsum_sum_bf16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, void* d_
     return sum_h16_api(h, d_x, n, 1, d_res, d_canon, stream);
 }
 
-xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, void* d_stage, size_t stage_bytes,
-                                 void* stream) {
+// Host-buffer streaming for any element format (dtype XSUM_DT_*): double-buffered H2D chunks on
+// the handle's copy stream, each accumulated on `stream` while the next one is in flight.
+static xsum_status accumulate_host_any(xsum_ctx* h, const void* h_x, uint64_t n, int dtype, void* d_stage,
+                                       size_t stage_bytes, void* stream) {
     if (!h) return XSUM_EINVAL;
+    if (dtype < XSUM_DT_F64 || dtype > XSUM_DT_BF16) return XSUM_EINVAL;
     if (n == 0) return XSUM_OK;
     if (!h_x || !d_stage || !aligned(d_stage, 256) || stage_bytes < (2u << 20)) return XSUM_EINVAL;
     if (n > kMaxCount - h->count) return XSUM_ECAPACITY;
+    const uint64_t esz = dtype == XSUM_DT_F64 ? 8 : (dtype == XSUM_DT_F32 ? 4 : 2);
     DeviceGuard g(h->device);
     if (!g.ok) return XSUM_ECUDA;
     if (!h->copy_stream) {
@@ -299,8 +303,9 @@ xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, voi
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint64_t half = (stage_bytes / 2) / 256 * 256;
-    const uint64_t per = half / sizeof(double);
+    const uint64_t per = half / esz;
     uint8_t* base = static_cast<uint8_t*>(d_stage);
+    const uint8_t* src = static_cast<const uint8_t*>(h_x);
     // order the copies after all prior work on `stream`
     if (cudaEventRecord(h->ev_ready[0], s) != cudaSuccess || cudaStreamWaitEvent(h->copy_stream, h->ev_ready[0], 0) != cudaSuccess)
         return XSUM_ECUDA;
@@ -308,19 +313,34 @@ xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, voi
     int b = 0;
     while (off < n) {
         uint64_t cnt = (n - off) < per ? (n - off) : per;
-        double* buf = reinterpret_cast<double*>(base + (uint64_t)b * half);
+        uint8_t* buf = base + (uint64_t)b * half;
         if (cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0) != cudaSuccess ||
-            cudaMemcpyAsync(buf, h_x + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->copy_stream) != cudaSuccess ||
+            cudaMemcpyAsync(buf, src + off * esz, cnt * esz, cudaMemcpyHostToDevice, h->copy_stream) != cudaSuccess ||
             cudaEventRecord(h->ev_ready[b], h->copy_stream) != cudaSuccess ||
             cudaStreamWaitEvent(s, h->ev_ready[b], 0) != cudaSuccess)
             return XSUM_ECUDA;
-        if (xs::accumulate(buf, cnt, acc_params(h, 0, nullptr, nullptr), grid_of(h), s) != cudaSuccess) return XSUM_ECUDA;
+        const xs::AccParams p = acc_params(h, 0, nullptr, nullptr);
+        cudaError_t e;
+        if (dtype == XSUM_DT_F64) e = xs::accumulate(reinterpret_cast<const double*>(buf), cnt, p, grid_of(h), s);
+        else if (dtype == XSUM_DT_F32) e = xs::accumulate_f32(reinterpret_cast<const float*>(buf), cnt, p, grid_of(h), s);
+        else e = xs::accumulate_h16(reinterpret_cast<const uint16_t*>(buf), cnt, dtype == XSUM_DT_BF16, p, grid_of(h), s);
+        if (e != cudaSuccess) return XSUM_ECUDA;
         if (cudaEventRecord(h->ev_done[b], s) != cudaSuccess) return XSUM_ECUDA;
         off += cnt;
         b ^= 1;
     }
     h->count += n;
     return XSUM_OK;
+}
+
+xsum_status xsum_accumulate_host(xsum_ctx* h, const double* h_x, uint64_t n, void* d_stage, size_t stage_bytes,
+                                 void* stream) {
+    return accumulate_host_any(h, h_x, n, XSUM_DT_F64, d_stage, stage_bytes, stream);
+}
+
+xsum_status xsum_accumulate_host_ex(xsum_ctx* h, const void* h_x, uint64_t n, int dtype, void* d_stage,
+                                    size_t stage_bytes, void* stream) {
+    return accumulate_host_any(h, h_x, n, dtype, d_stage, stage_bytes, stream);
 }
 
 xsum_status xsum_merge(xsum_ctx* h, const void* d_states, uint32_t count, void* stream) {

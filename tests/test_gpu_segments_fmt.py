@@ -129,3 +129,19 @@ def test_exact_sum_dim_formats(xs, fmt):
         for i, row in enumerate(fib):
             r, _ = ref_of(fmt, np.ascontiguousarray(row))
             assert out[i] == r.bits_f32, (fmt, dim, i)
+
+
+@pytest.mark.parametrize("fmt", ["f32", "f16", "bf16"])
+def test_host_buffer_streaming_formats(xs, fmt):
+    """xsum_accumulate_host_ex: pinned host tensors of each format through a 2 MiB staging buffer
+    (several double-buffered chunks) vs the oracle."""
+    import torch
+    n = 3_000_003
+    b = bits_data(fmt, n, 123)
+    dt = getattr(torch, TORCH_DT[fmt])
+    host = torch.from_numpy(b.view(np.int32 if fmt == "f32" else np.int16)).view(dt).pin_memory()
+    acc = xs.Accumulator().add_host(host, stage_bytes=2 << 20)
+    res, canon = acc.exact()
+    r, limbs = ref_of(fmt, b)
+    assert res.bits == r.bits and res.bits_f32 == r.bits_f32 and res.flags == r.flags
+    assert (canon == limbs).all() and res.count == n

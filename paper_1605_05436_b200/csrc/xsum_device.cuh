@@ -70,47 +70,16 @@ __device__ __forceinline__ int32_t mulhi_s32(int32_t a, int32_t b) {
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r; asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r;
 }
-__device__ __forceinline__ uint64_t madwide_u32(uint32_t a, uint32_t b, uint64_t c) {
-    uint64_t r; asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c)); return r;
-}
-// d + c for 64-bit values, entirely on the FMA pipe (two IMADs).
-__device__ __forceinline__ int64_t add64_fma(int64_t d, int64_t c, uint32_t one) {
-    uint64_t t = madwide_u32((uint32_t)(uint64_t)c, one, (uint64_t)d);
-    uint32_t th = mad_u32((uint32_t)((uint64_t)c >> 32), one, (uint32_t)(t >> 32));
-    return (int64_t)(((uint64_t)th << 32) | (uint32_t)t);
-}
-
 // mulhi(x, K52) = floor(x / 52) for 0 <= x <= 2047 (K52 = 20165 * 2^12; 52*20165 = 2^20 + 4,
 // relative error 4/2^20 < 1/(52*2047); checked for every x in tests/test_host_logic.py).
 constexpr uint32_t K52 = 20165u << 12;
-// mulhi(e, KSPEC) = 1 iff e == 2047 for e in [0, 2047]  (2047*KSPEC >= 2^32 > 2046*KSPEC).
-constexpr uint32_t KSPEC = 2098177u;
 
-#ifndef XS_DECODE
-#define XS_DECODE 3   // decode variant (3 = product); 0-2, 4: alternatives kept for tools/variants.py
-#endif
+// Per summand ~14 ALU-pipe ops and ~12 FMA-pipe issue slots (IMAD = 1, IMAD.HI = 2; measured
+// sm_100 rates in tools/op_bench.cu, profiles/r01_microbench.txt), no IMAD.WIDE (1/8 rate): the
+// constant divisions and the hidden-bit / sign assembly run as IMADs so that the ALU pipe is not
+// the binding resource (an ALU-only decode measured 85% ALU busy and 640 vs 684 G/s).
 __device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t one, uint32_t mone = 0xFFFFFFFFu) {
     Chunks c;
-    (void)mone;
-#if XS_DECODE == 0
-    (void)one;
-    uint32_t e = (hi >> 20) & 0x7FFu;
-    uint32_t ep = max(e, 1u);
-    uint32_t k = ep - 1u;
-    uint32_t i = k / 52u;
-    uint32_t o = k - 52u * i;
-    uint32_t imp = e + 1u - ep;                       // hidden bit: 1 unless subnormal/zero
-    uint32_t mh = (hi & 0xFFFFFu) | (imp << 20);
-    uint64_t M = ((uint64_t)mh << 32) | lo;
-    int64_t s = (int64_t)((int32_t)hi >> 31);         // 0 or -1
-    int64_t sM = (int64_t)(M ^ (uint64_t)s) - s;      // +-M
-    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> (52u - o);
-    c.i = i;
-    c.spec = (e == 0x7FFu);
-#elif XS_DECODE == 3
-    // per summand: ~14 ALU-pipe ops and ~12 FMA-pipe issue slots (IMAD = 1, IMAD.HI = 2;
-    // measured sm_100 rates in tools/op_bench.cu), no IMAD.WIDE (1/8 rate).
     uint32_t h = hi & 0x7FFFFFFFu;                        // |x| high word
     uint32_t e = h >> 20;                                 // biased exponent
     uint32_t ep = max(e, 1u);
@@ -126,75 +95,13 @@ __device__ __forceinline__ Chunks decompose(uint32_t lo, uint32_t hi, uint32_t o
     c.c1 = sM >> r;
     c.i = i;
     c.spec = k;                                           // k == 2046 only for NaN/Inf (max-tracked)
-#elif XS_DECODE == 4
-    // dec3 with the sign mask from IMAD.HI and the +1 of the two's complement carried by
-    // IMAD.X (madc): ~14 ALU-pipe ops, ~13 FMA-pipe slots per summand.
-    uint32_t h = hi & 0x7FFFFFFFu;
-    uint32_t e = h >> 20;
-    uint32_t ep = max(e, 1u);
-    uint32_t k = mad_u32(ep, one, 0xFFFFFFFFu);
-    uint32_t i = mulhi_u32(k, K52);
-    uint32_t o = mad_u32(i, (uint32_t)-52, k);
-    uint32_t r = mad_u32(o, mone, 52u);
-    uint32_t mh = mad_u32(k, 0xFFF00000u, h);
-    int32_t S = mulhi_s32((int32_t)hi, 2);                // sign mask (IMAD.HI)
-    uint32_t sbit = mad_u32((uint32_t)S, mone, 0u);       // -S (IMAD)
-    uint32_t slo, shi;
-    asm("add.cc.u32 %0, %2, %3;\n\tmadc.lo.u32 %1, %4, %5, 0;"
-        : "=r"(slo), "=r"(shi) : "r"(lo ^ (uint32_t)S), "r"(sbit), "r"(mh ^ (uint32_t)S), "r"(one));
-    int64_t sM = (int64_t)(((uint64_t)shi << 32) | slo);
-    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> r;
-    c.i = i;
-    c.spec = k;
-#elif XS_DECODE == 2
-    uint32_t e = (hi >> 20) & 0x7FFu;
-    uint32_t ep = max(e, 1u);
-    uint32_t k = ep - 1u;
-    uint32_t i = mulhi_u32(k, K52);                       // k / 52 (IMAD.HI)
-    uint32_t o = mad_u32(i, (uint32_t)-52, k);            // k mod 52 (IMAD)
-    uint32_t mhs = mad_u32(k, 0xFFF00000u, hi);           // sign | hidden | m_hi (IMAD)
-    int32_t S = (int32_t)hi >> 31;
-    uint32_t S31 = (uint32_t)S >> 1;
-    uint64_t onec = ((uint64_t)(mhs ^ S31) << 32) | (lo ^ (uint32_t)S);
-    int64_t sM = (int64_t)onec - (int64_t)S;
-    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> (52u - o);
-    c.i = i;
-    c.spec = mulhi_u32(e, KSPEC);
-    (void)one;
-#else
-
-    uint32_t e = (hi >> 20) & 0x7FFu;                     // biased exponent
-    uint32_t ep = max(e, 1u);
-    uint32_t k = mad_u32(ep, one, 0xFFFFFFFFu);           // ep - 1: LSB position of M
-    uint32_t i = mulhi_u32(k, K52);                       // k / 52
-    uint32_t o = mad_u32(i, (uint32_t)-52, k);            // k mod 52
-    // hi - k*2^20 = sign | hidden bit | top 20 fraction bits (hidden = [e != 0])
-    uint32_t mhs = mad_u32(k, 0xFFF00000u, hi);
-    int32_t S = mulhi_s32((int32_t)hi, 2);                // 0 or -1 (sign mask)
-    uint32_t sbit = mulhi_u32(hi, 2u);                    // 0 or 1
-    uint32_t S31 = mulhi_u32((uint32_t)S, 0x80000000u);   // 0 or 0x7FFFFFFF
-    // sM = +-M = (M ^ S) - S, with M_hi ^ S = mhs ^ S31 (the sign bit of mhs is s)
-    uint64_t onec = ((uint64_t)(mhs ^ S31) << 32) | (lo ^ (uint32_t)S);
-    int64_t sM = (int64_t)madwide_u32(sbit, one, onec);
-    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> (52u - o);                               // arithmetic: floor division
-    c.i = i;
-    c.spec = mulhi_u32(e, KSPEC);
-#endif
     return c;
 }
 
 // Tracking of NaN/Inf bit patterns summed unchecked in the hot loop: a per-lane fold that
 // is cheap per summand and tested once per window.
-#if XS_DECODE == 3 || XS_DECODE == 4
 __device__ __forceinline__ uint32_t spec_fold(uint32_t acc, const Chunks& c) { return max(acc, c.spec); }
 __device__ __forceinline__ bool spec_hit(uint32_t acc) { return acc >= 2046u; }
-#else
-__device__ __forceinline__ uint32_t spec_fold(uint32_t acc, const Chunks& c) { return acc + c.spec; }
-__device__ __forceinline__ bool spec_hit(uint32_t acc) { return acc != 0u; }
-#endif
 
 // Add one summand's chunks into a lane column (digit j at col[j*32]): the "localized"
 // add of PAPER.md:1043-1047 with carries deferred (PAPER.md:669-673 lazy carries).
@@ -551,25 +458,12 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
     return finalize_warp_inl(a0, a1, flags, count, canon, su, lane);
 }
 
-// 128-bit streaming load of two doubles as four 32-bit halves (no L1 allocation).
-#ifndef XS_LOAD
-#define XS_LOAD 0   // 0: .nc.L1::no_allocate.L2::256B (product); 1: .cg; 2: .cs; 3: .nc; 4: .nc.L1::no_allocate
-#endif
+// 128-bit streaming load of two doubles as four 32-bit halves (no L1 allocation; 256-B L2
+// prefetch: the best of the load flavours measured, profiles/r01_microbench.txt).
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     uint4 v;
-#if XS_LOAD == 1
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#elif XS_LOAD == 2
-    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#elif XS_LOAD == 3
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#elif XS_LOAD == 4
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#else
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#endif
     return v;
 }
 

@@ -161,8 +161,12 @@ def _torch():
 
 
 def _stream_ptr(device) -> int:
+    """The current CUDA stream of `device` as a raw cudaStream_t value (no Stream object)."""
     torch = _torch()
-    return torch.cuda.current_stream(device).cuda_stream
+    idx = device.index if isinstance(device, torch.device) else device
+    if idx is None:
+        idx = torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)
 
 
 def _as_f64_cuda(t, allow_f32: bool = False):
@@ -186,8 +190,27 @@ _ENTRY = {"float64": ("xsum_accumulate", "xsum_sum"), "float32": ("xsum_accumula
           "float16": ("xsum_accumulate_f16", "xsum_sum_f16"), "bfloat16": ("xsum_accumulate_bf16", "xsum_sum_bf16")}
 
 
-def _entry(t, fused: bool) -> str:
-    return _ENTRY[str(t.dtype).replace("torch.", "")][1 if fused else 0]
+_FNS: dict = {}
+
+
+def _fns_for(t):
+    """(accumulate fn, fused-sum fn, names) of the library for a CUDA tensor's dtype; the hot
+    per-call path (one dict lookup instead of string work)."""
+    f = _FNS.get(t.dtype)
+    if f is None:
+        torch = _torch()
+        if not isinstance(t, torch.Tensor):
+            raise TypeError("expected a CUDA tensor")
+        key = str(t.dtype).replace("torch.", "")
+        if key not in _ENTRY:
+            raise TypeError(f"expected float64 / float32 / float16 / bfloat16, got {t.dtype}")
+        a, s_ = _ENTRY[key]
+        f = _FNS[t.dtype] = (getattr(lib(), a), getattr(lib(), s_), a, s_)
+    if not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return f
 
 
 class Accumulator:
@@ -211,6 +234,8 @@ class Accumulator:
         self.scratch = torch.zeros(nscr, dtype=torch.uint8, device=self.device)
         self._res = torch.zeros(RESULT_BYTES, dtype=torch.uint8, device=self.device)
         self._canon = torch.zeros(CANON_LIMBS, dtype=torch.int64, device=self.device)
+        self._idx = self.device.index
+        self._res_ptr, self._canon_ptr = self._res.data_ptr(), self._canon.data_ptr()
         self._stage = None
         h = ctypes.c_void_p()
         _check("xsum_create", L.xsum_create(ctypes.byref(h), self.device.index, self.state.data_ptr(),
@@ -245,9 +270,10 @@ class Accumulator:
 
     def add(self, x) -> "Accumulator":
         """Sum a float64 / float32 / float16 / bfloat16 CUDA tensor into the state, exactly."""
-        x = _as_f64_cuda(x, allow_f32=True)
-        name = _entry(x, fused=False)
-        _check(name, getattr(lib(), name)(self._h, x.data_ptr(), x.numel(), _stream_ptr(self.device)))
+        fa, _, name, _ = _fns_for(x)
+        rc = fa(self._h, x.data_ptr(), x.numel(), _stream_ptr(self._idx))
+        if rc:
+            raise XsumError(name, rc)
         return self
 
     def add_host(self, x, stage_bytes: int = 128 << 20) -> "Accumulator":
@@ -348,10 +374,11 @@ class Accumulator:
     def sum(self, x, canon: bool = False):
         """One-shot fused path (xsum_sum / xsum_sum_f32): state := sum(x); returns device
         (result, canon)."""
-        x = _as_f64_cuda(x, allow_f32=True)
-        name = _entry(x, fused=True)
-        _check(name, getattr(lib(), name)(self._h, x.data_ptr(), x.numel(), self._res.data_ptr(),
-                                          self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
+        _, fs, _, name = _fns_for(x)
+        rc = fs(self._h, x.data_ptr(), x.numel(), self._res_ptr, self._canon_ptr if canon else None,
+                _stream_ptr(self._idx))
+        if rc:
+            raise XsumError(name, rc)
         return self._res, (self._canon if canon else None)
 
 

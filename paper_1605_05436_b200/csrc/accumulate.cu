@@ -168,13 +168,8 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
 template <int WARPS, int U, int NB, typename E>
 static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
     using C = AccCfg<WARPS, U, NB, E>;
-    static bool attr_set = false;   // per process; the attribute is per function and device-independent
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_accumulate<WARPS, U, NB, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_accumulate<WARPS, U, NB, E>, C::SMEM, smem_set)) return e;
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / sizeof(E);
     if (head > n) head = n;
     const uint64_t ntiles = ((n - head) / Elem<E>::PER_VEC) / ((uint64_t)C::T * U);

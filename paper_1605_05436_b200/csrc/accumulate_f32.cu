@@ -241,12 +241,8 @@ k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
 
 cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
     constexpr size_t SMEM = (size_t)F32B_WARPS * 32 * (D + F32B_NBIN) * sizeof(int64_t);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_accumulate_f32b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_accumulate_f32b, SMEM, smem_set)) return e;
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 4;
     if (head > n) head = n;
     const uint64_t ntiles = ((n - head) / 4) / ((uint64_t)F32B_WARPS * 32 * F32B_U);

@@ -313,12 +313,8 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
 template <class F>
 static cudaError_t launch_h16(const uint16_t* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
     constexpr size_t SMEM = (size_t)H16_WARPS * 32 * (F::NBIN64 * 8 + F::NBIN * 4);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_accumulate_h16<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_accumulate_h16<F>, SMEM, smem_set)) return e;
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 2;
     if (head > n) head = n;
     const uint64_t ntiles = ((n - head) / 8) / ((uint64_t)H16_WARPS * 32 * H16_U);

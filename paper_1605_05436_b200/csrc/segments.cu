@@ -263,14 +263,9 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
 
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
                          int num_sms, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SEG_SMEM);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_segments_uniform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SEG_SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static unsigned long long smem_set = 0, smem_set_u = 0;
+    if (cudaError_t e = ensure_smem(k_segments, SEG_SMEM, smem_set)) return e;
+    if (cudaError_t e = ensure_smem(k_segments_uniform, SEG_SMEM, smem_set_u)) return e;
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
     uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (84 KiB smem each)
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);

@@ -135,13 +135,8 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
 template <class F>
 static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                 const SegOut& o, int num_sms, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_segments_small<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)SSEG_SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_segments_small<F>, SSEG_SMEM, smem_set)) return e;
     const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
     const uint64_t cap = (uint64_t)num_sms * 2;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);

@@ -43,6 +43,21 @@ constexpr size_t SCRATCH_BYTES = SCRATCH_FLAGS_OFF + sizeof(uint32_t) * XS_MAXB;
 
 void note_launch();
 
+// Opt `kernel` into `bytes` of dynamic shared memory once per device: the attribute belongs to
+// the function in the current device's context, so a process driving several GPUs sets it on
+// each. `done` is the caller's per-kernel bitmask of devices (device index < 64).
+template <typename K>
+inline cudaError_t ensure_smem(K kernel, size_t bytes, unsigned long long& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
+    return e;
+}
+
 cudaError_t accumulate(const double* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
 cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s);
 cudaError_t accumulate_h16(const uint16_t* x, uint64_t n, int bf16, const AccParams& p, int num_sms, cudaStream_t s);

@@ -156,13 +156,13 @@ def oracle_rate(cfg_name: str, target_s: float = 1.5, max_n: int = 1 << 28):
     oracle.exact_sum(x[: 1 << 16], nthreads=cores)          # load the library, warm the threads
     passes, t0 = 0, time.perf_counter()
     while True:
-        oracle.exact_sum(x, nthreads=cores)
+        ref = oracle.exact_sum(x, nthreads=cores)
         passes += 1
         dt = time.perf_counter() - t0
         if dt >= target_s:
             break
     del x
-    return m * passes / dt, cores, m, passes, dt, gen_name
+    return m * passes / dt, cores, m, passes, dt, gen_name, ref
 
 
 def cpu_model() -> str:
@@ -184,7 +184,7 @@ def run_reference(args, rank: int, world: int):
     import synth
     wl = workload(args.config, world)
     cores = oracle.host_threads()
-    rate, _, _, _, _, gen_name = oracle_rate(args.config, target_s=0.5, max_n=1 << 24)
+    rate, _, _, _, _, gen_name, _ = oracle_rate(args.config, target_s=0.5, max_n=1 << 24)
     budget = 90.0
     m = int(max(1 << 14, min(1 << 26, rate * budget / max(1, args.steps + args.warmup))))
     x = synth.host_generate(gen_name, 0, m)
@@ -339,12 +339,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev)
         else:
             e2e = measure_e2e_multi(xsum, torch, dist, x, args.e2e_steps, dev, pe, acc, tot, world)
+    # the timed step's exact result (the state the last step left), for the record
+    result = None
+    if world == 1 and not seg:
+        import hashlib
+        r_gpu, canon_gpu = acc.exact()
+        result = {"value_hex": f"{r_gpu.bits:016x}", "flags": r_gpu.flags,
+                  "image_sha256": hashlib.sha256(np.asarray(canon_gpu, dtype="<u8").tobytes()).hexdigest()}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, m, passes, dt, gen_name = oracle_rate(args.config)
+        rate, cores, m, passes, dt, gen_name, (r_cpu, limbs_cpu) = oracle_rate(args.config)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{gen_name} elements [0, {m}) summed {passes}x by the oracle in {dt:.2f} s "
                          f"on {cores} host threads = {dt * cores:.1f} CPU-s ({cpu_model()})"}
+        if result is not None and gen_name == args.config and m == n_local:
+            # the sample is the whole workload: the oracle's exact sum vs the timed GPU result
+            cpu["matches_gpu"] = bool(r_cpu.bits == r_gpu.bits and r_cpu.flags == r_gpu.flags and
+                                      (np.asarray(limbs_cpu) == np.asarray(canon_gpu)).all())
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -365,6 +376,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "result": result,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -63,6 +63,7 @@ def test_our_arm_one_gpu_contract():
     assert r["bound"] == "hbm" and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["n_per_gpu"] and d["e2e"]["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["clocks"]["sm_max_mhz"]
+    assert len(d["result"]["value_hex"]) == 16 and len(d["result"]["image_sha256"]) == 64
 
 
 @pytest.mark.gpu

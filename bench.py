@@ -26,6 +26,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "doubles/s exact-summed (device-timed) at 1/2/4/8 B200; % of HBM-read roofline"
 UNIT = "doubles/s"
+FMT_OF = {"c2f32": "binary32", "c2f16": "binary16", "c2bf16": "bfloat16"}
+
+
+def metric_unit(cfg_name: str):
+    """BASELINE.json's metric, or for the other-format workloads the same metric in their values."""
+    if cfg_name in FMT_OF:
+        return (f"{FMT_OF[cfg_name]} values/s exact-summed (device-timed); % of HBM-read roofline",
+                f"{FMT_OF[cfg_name]} values/s")
+    return METRIC, UNIT
 
 
 def parse():
@@ -33,7 +42,10 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    # c1..c5: BASELINE.json configs; c5csr / c2f32 / c2f16 / c2bf16: measurement workloads of the
+    # NEXT rows (CSR segments, other input formats; synth/gen.py)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5csr", "c2f32", "c2f16",
+                                                         "c2bf16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -54,6 +66,10 @@ def workload(cfg_name: str, world: int) -> dict:
         "c3": "c3: 2^27 (a,-a) pairs exp U[0,600] + 2^20 tiny exp U[-900,-800], permuted, seed 3",
         "c4": "c4: n=2^33 doubles, seed 4, exponent U[-1022,1023], sharded over the GPUs",
         "c5": "c5: 2^16 segments x 2^12 doubles, seed 5, exponent U[-200,200]",
+        "c5csr": "c5csr: 2^16 CSR segments of 1..8192 doubles (mean 4096), seed 9, exponent U[-200,200]",
+        "c2f32": "c2f32: n=2^28 binary32, seed 6, uniform over the finite bit patterns",
+        "c2f16": "c2f16: n=2^28 binary16, seed 7, uniform over the finite bit patterns",
+        "c2bf16": "c2bf16: n=2^28 bfloat16, seed 8, uniform over the finite bit patterns",
     }[cfg_name]
     if cfg_name == "c4":
         n_total = cfg["n"]
@@ -144,6 +160,7 @@ def profiled_traffic(cfg_name: str):
 # CPU oracle arm (cpu_baseline and --impl reference)
 # ------------------------------------------------------------------------------------------
 def oracle_rate(cfg_name: str, target_s: float = 1.5, max_n: int = 1 << 28):
+    import numpy as np
     """Time the oracle (as it stands) on a bounded prefix of the workload on all host cores:
     passes over the same sample until ~target_s seconds of wall time (x the host cores =
     10-30 s of CPU work). Returns (doubles/s, cores, sample size, passes, seconds, config)."""
@@ -152,11 +169,23 @@ def oracle_rate(cfg_name: str, target_s: float = 1.5, max_n: int = 1 << 28):
     cores = oracle.host_threads()
     gen_name = "c2" if cfg_name in ("c1",) else cfg_name
     m = min(max_n, synth.CONFIGS[gen_name]["n"])
-    x = synth.host_generate(gen_name, 0, m)
-    oracle.exact_sum(x[: 1 << 16], nthreads=cores)          # load the library, warm the threads
+    fmt = synth.CONFIGS[gen_name].get("fmt")
+    if fmt is None:
+        x = synth.host_generate(gen_name, 0, m)
+
+        def run(a):
+            return oracle.exact_sum(a, nthreads=cores)
+    else:
+        x = synth.host_bits(gen_name, 0, m)
+
+        def run(a):
+            if fmt == "f32":
+                return oracle.exact_sum(a.view(np.float32), nthreads=cores)
+            return oracle.exact_sum(a, nthreads=cores, fmt=fmt)
+    run(x[: 1 << 16])                                       # load the library, warm the threads
     passes, t0 = 0, time.perf_counter()
     while True:
-        ref = oracle.exact_sum(x, nthreads=cores)
+        ref = run(x)
         passes += 1
         dt = time.perf_counter() - t0
         if dt >= target_s:
@@ -187,24 +216,32 @@ def run_reference(args, rank: int, world: int):
     rate, _, _, _, _, gen_name, _ = oracle_rate(args.config, target_s=0.5, max_n=1 << 24)
     budget = 90.0
     m = int(max(1 << 14, min(1 << 26, rate * budget / max(1, args.steps + args.warmup))))
-    x = synth.host_generate(gen_name, 0, m)
+    fmt = synth.CONFIGS[gen_name].get("fmt")
+    if fmt is None:
+        x = synth.host_generate(gen_name, 0, m)
+    elif fmt == "f32":
+        x = synth.host_bits(gen_name, 0, m).view(np.float32)
+    else:
+        x = synth.host_bits(gen_name, 0, m)
+    kw = {"fmt": fmt} if fmt in ("f16", "bf16") else {}
     for _ in range(args.warmup):
-        oracle.exact_sum(x, nthreads=cores)
+        oracle.exact_sum(x, nthreads=cores, **kw)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.exact_sum(x, nthreads=cores)
+        oracle.exact_sum(x, nthreads=cores, **kw)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = m * args.steps / tot
     sample = f"{gen_name} elements [0, {m}) per step (bounded sample of the workload), {cpu_model()}"
+    metric, unit = metric_unit(args.config)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": {"workload": wl["desc"], "sample_n": m},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -233,10 +270,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     synth.build()
     wl = workload(args.config, world)
     cfg = wl["cfg"]
-    seg = args.config == "c5"
+    if world > 1 and cfg["kind"] in ("bits", "csr"):
+        raise SystemExit(f"--config {args.config} is a one-GPU measurement workload")
+    seg = args.config in ("c5", "c5csr")
+    csr = None
+    metric, unit = metric_unit(args.config)
 
     # this rank's input, generated in HBM (untimed)
-    if args.config == "c4":
+    if cfg["kind"] == "bits":
+        x = synth.device_bits(args.config, device=dev)
+    elif args.config == "c5csr":
+        x = synth.device_generate("c5csr", device=dev)
+        csr = synth.csr_offsets("c5csr", device=dev)
+    elif args.config == "c4":
         start, stop = dist.shard_range(cfg["n"], rank, world)
         x = synth.device_generate("c4", start, stop - start, device=dev)
     elif args.config == "c3":
@@ -263,7 +309,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         exchange = f"{args.dist_backend} all-gather of 384-B states + xsum_merge_round"
 
     def step():
-        if seg:
+        if csr is not None:
+            xsum.sum_segments_csr(x, csr)
+        elif seg:
             xsum.sum_segments(x, cfg["seg_len"])
         elif world == 1:
             acc.sum(x)                                   # one fused launch
@@ -281,9 +329,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    # inputs smaller than 256 MiB (c1) would be served from the 126 MB L2 on every step after
+    # the first: flush L2 by writing a 256 MiB buffer before each timed step (outside its events)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if x.numel() * x.element_size() < (256 << 20) \
+        else None
     l0 = xsum.launch_count()
     with ClockSampler(local_rank) as clk:
         for i in range(K):
+            if flush is not None:
+                flush.zero_()
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
@@ -302,7 +356,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if not torch.equal(lo, hi) or int(hi[1]) & xsum.F_PEER_TIMEOUT:
             raise RuntimeError(f"ranks disagree or the peer exchange timed out: {lo.tolist()} {hi.tolist()}")
     per = [a.elapsed_time(b) for a, b in ev]                 # ms per step (device)
-    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    # span of the K steps; with L2 flushes in between, the sum of the steps' own times
+    total_ms = sum(per) if flush is not None else ev[0][0].elapsed_time(ev[-1][1])
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         allreduce_(t, torch.distributed.ReduceOp.MAX)
@@ -322,7 +377,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
     peak, peak_src = measured_peak_hbm()
-    achieved = 8.0 * n_local / (kern_ms / 1e3) / 1e9
+    esz = x.element_size()                                   # algorithmic bytes per summand
+    achieved = esz * n_local / (kern_ms / 1e3) / 1e9
     # context for the roofline: a pure streaming read of the same input in the same run (the
     # best read-only probe configuration of profiles/r01_microbench.txt: 296 blocks x 512 threads,
     # 8 x 16-B loads in flight per thread), untimed by the step
@@ -334,9 +390,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # check the result once (device result vs nothing host-side: the parity tests do that)
     e2e = None
-    if not args.no_e2e and not seg and 8 * n_local <= (16 << 30):
+    if not args.no_e2e and not seg and esz * n_local <= (16 << 30):
         if world == 1:
-            e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev)
+            e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev, unit)
         else:
             e2e = measure_e2e_multi(xsum, torch, dist, x, args.e2e_steps, dev, pe, acc, tot, world)
     # the timed step's exact result (the state the last step left), for the record
@@ -349,7 +405,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, m, passes, dt, gen_name, (r_cpu, limbs_cpu) = oracle_rate(args.config)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+        cpu = {"value": rate, "unit": unit, "cores": cores, "kind": "oracle",
                "sample": f"{gen_name} elements [0, {m}) summed {passes}x by the oracle in {dt:.2f} s "
                          f"on {cores} host threads = {dt * cores:.1f} CPU-s ({cpu_model()})"}
         if result is not None and gen_name == args.config and m == n_local:
@@ -358,18 +414,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                       (np.asarray(limbs_cpu) == np.asarray(canon_gpu)).all())
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": K,
             "warmup": max(3, args.warmup), "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": wl["desc"], "n_per_gpu": n_local, "n_total": n_all,
                        "parallelism": f"dp{world}" if world > 1 else "single",
-                       "l2": "inputs 2 GiB+ per GPU > 126 MB L2 (no flush needed)",
-                       "step": ("xsum_sum_segments" if seg else
+                       "l2": ("L2 flushed (256 MiB write) before every timed step; steps timed individually"
+                              if flush is not None else
+                              f"inputs {x.numel() * x.element_size() / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)"),
+                       "step": ("xsum_sum_segments_csr" if csr is not None else "xsum_sum_segments" if seg else
                                 "xsum_sum fused launch" if world == 1 else exchange)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
-                         "kernel": "k_accumulate" if not seg else "k_segments",
-                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": 8 * n_local,
+                         "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
+                                    "c2bf16": "k_accumulate_h16", "c5": "k_segments_uniform",
+                                    "c5csr": "k_segments"}.get(args.config, "k_accumulate"),
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local,
                          "peak_source": peak_src, "read_probe_gbs": probe_gbs,
                          "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None},
             "clocks": clk.summary(),
@@ -383,12 +443,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.distributed.destroy_process_group()
 
 
-def measure_e2e(xsum, torch, x_dev, steps: int, dev):
+def measure_e2e(xsum, torch, x_dev, steps: int, dev, unit: str = UNIT):
     """Same metric through the C-ABI with a HOST buffer: per step the pinned-host -> device copy
     of the whole input (overlapped chunk by chunk, xsum_accumulate_host), the sum, the rounding
     and the 48-byte device -> host read of the result."""
     n = x_dev.numel()
-    host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host = torch.empty(n, dtype=x_dev.dtype, pin_memory=True)
     host.copy_(x_dev)
     acc = xsum.Accumulator(dev)
     out = torch.empty(xsum.RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
@@ -406,7 +466,8 @@ def measure_e2e(xsum, torch, x_dev, steps: int, dev):
         one()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": xsum.RESULT_BYTES,
+    return {"value": n / dt, "unit": unit, "h2d_bytes_per_step": x_dev.element_size() * n,
+            "d2h_bytes_per_step": xsum.RESULT_BYTES,
             "ms_per_step": dt * 1e3, "api": "xsum_reset + xsum_accumulate_host + xsum_finalize_round + D2H"}
 
 

@@ -110,6 +110,33 @@ def host_generate(name: str, start: int = 0, count: int | None = None, out: np.n
     return out[:count]
 
 
+def host_bits(name: str, start: int = 0, count: int | None = None) -> np.ndarray:
+    """Elements [start, start+count) of a "bits" config (other input formats) as bit patterns,
+    the draws from the threaded C generator (gen.bits is the numpy definition)."""
+    from .gen import bits_fix
+    cfg = CONFIGS[name]
+    if count is None:
+        count = cfg["n"] - start
+    return bits_fix(host_keys(cfg["seed"], cfg["st"], start, count), cfg["fmt"])
+
+
+def device_bits(name: str, device=None):
+    """A "bits" config as a CUDA tensor of its format (float32 / float16 / bfloat16)."""
+    import torch
+    cfg = CONFIGS[name]
+    b = host_bits(name)
+    t = torch.from_numpy(b.view(np.int32 if cfg["fmt"] == "f32" else np.int16)).to(
+        torch.device(device if device is not None else "cuda"))
+    return t.view({"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg["fmt"]])
+
+
+def csr_offsets(name: str, device=None):
+    """int64 CUDA tensor of a "csr" config's offsets."""
+    import torch
+    from .gen import csr_offsets as offs
+    return torch.from_numpy(offs(CONFIGS[name])).to(torch.device(device if device is not None else "cuda"))
+
+
 def host_keys(seed: int, st: int, start: int, count: int, nthreads: int | None = None) -> np.ndarray:
     out = np.empty(count, dtype=np.uint64)
     host_lib().synth_keys(out.ctypes.data, start, count, seed, st, nthreads or _threads())

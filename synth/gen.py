@@ -41,6 +41,20 @@ CONFIGS = {
                nseg=1 << 16, seg_len=1 << 12),
 }
 
+# Measurement workloads of the NEXT rows, not BASELINE.json configs:
+#  * c5csr: 2^16 variable-length segments, len_s = 1 + (U(seed, 1, s) >> 51) in [1, 8192]
+#    (mean ~4096), elements drawn like c5 (f1, CSR segments);
+#  * c2f32 / c2f16 / c2bf16: 2^28 elements of another format (f2), element j = the low 32 / 16
+#    bits of U(seed, 0, j), an all-ones exponent field (NaN/Inf) moved down by one exponent:
+#    uniform over the finite bit patterns (every exponent incl. subnormals, both signs, zeros).
+FORMAT_BITS = {"f32": (32, 0x7F800000, 1 << 23), "f16": (16, 0x7C00, 1 << 10), "bf16": (16, 0x7F80, 1 << 7)}
+CONFIGS.update({
+    "c5csr": dict(kind="csr", nseg=1 << 16, seed=9, st=0, lo=-200, hi=200, maxlen=1 << 13),
+    "c2f32": dict(kind="bits", fmt="f32", n=1 << 28, seed=6, st=0),
+    "c2f16": dict(kind="bits", fmt="f16", n=1 << 28, seed=7, st=0),
+    "c2bf16": dict(kind="bits", fmt="bf16", n=1 << 28, seed=8, st=0),
+})
+
 
 def mix64(z: np.ndarray) -> np.ndarray:
     z = np.asarray(z, dtype=np.uint64)
@@ -124,6 +138,33 @@ def cancel_permuted(cfg: dict) -> np.ndarray:
     return cancel_unpermuted(cfg, 0, n)[perm]
 
 
+def csr_offsets(cfg: dict) -> np.ndarray:
+    """int64 offsets [0, len_0, len_0+len_1, ...] of a "csr" config (nseg + 1 entries)."""
+    u = U(cfg["seed"], 1, np.arange(cfg["nseg"], dtype=np.uint64))
+    lens = (u >> np.uint64(64 - int(np.log2(cfg["maxlen"])))).astype(np.int64) + 1
+    return np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+
+
+CONFIGS["c5csr"]["n"] = int(csr_offsets(CONFIGS["c5csr"])[-1])
+
+
+def bits_fix(u: np.ndarray, fmt: str) -> np.ndarray:
+    """Finite bit patterns of format ``fmt`` from raw 64-bit draws (see FORMAT_BITS)."""
+    width, em, low = FORMAT_BITS[fmt]
+    b = (u & np.uint64((1 << width) - 1)).astype(np.uint32 if width == 32 else np.uint16)
+    spec = (b & b.dtype.type(em)) == b.dtype.type(em)
+    b[spec] ^= b.dtype.type(low)
+    return b
+
+
+def bits(name: str, start: int = 0, count: int | None = None) -> np.ndarray:
+    """Elements [start, start+count) of a "bits" config as bit patterns (uint32 / uint16)."""
+    cfg = CONFIGS[name]
+    if count is None:
+        count = cfg["n"] - start
+    return bits_fix(U(cfg["seed"], cfg["st"], np.arange(start, start + count, dtype=np.uint64)), cfg["fmt"])
+
+
 def generate(name: str, start: int = 0, count: int | None = None, permute: bool = True) -> np.ndarray:
     """Elements [start, start+count) of config ``name`` as float64 (host memory).
 
@@ -135,8 +176,10 @@ def generate(name: str, start: int = 0, count: int | None = None, permute: bool 
         count = n - start
     if start < 0 or start + count > n:
         raise ValueError("range outside config")
-    if cfg["kind"] in ("uniform", "segments"):
+    if cfg["kind"] in ("uniform", "segments", "csr"):
         return uniform(cfg["seed"], cfg["lo"], cfg["hi"], start, count, cfg["st"])
+    if cfg["kind"] == "bits":
+        raise ValueError("use gen.bits() for the other formats")
     if permute:
         if start != 0 or count != n:
             raise ValueError("permuted c3 is only available whole; use permute=False")

@@ -83,3 +83,25 @@ def test_device_generator_matches_numpy(name, start):
     torch.cuda.synchronize()
     a = gen.generate(name, start, 10_000, permute=False)
     assert (d.cpu().numpy().view(np.uint64) == a.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("name", ["c2f32", "c2f16", "c2bf16"])
+def test_format_bits_numpy_vs_c(name):
+    """The other-format workloads: numpy definition vs the threaded C draws, finite patterns only,
+    every exponent field reached."""
+    a = gen.bits(name, 1000, 200_000)
+    b = synth.host_bits(name, 1000, 200_000)
+    assert (a == b).all()
+    width, em, _ = gen.FORMAT_BITS[gen.CONFIGS[name]["fmt"]]
+    assert a.dtype == (np.uint32 if width == 32 else np.uint16)
+    e = (a & a.dtype.type(em)) >> a.dtype.type((em & -em).bit_length() - 1)
+    assert int(e.max()) == (em >> ((em & -em).bit_length() - 1)) - 1      # never all ones
+    assert len(np.unique(e)) == int(e.max()) + 1                          # every finite exponent
+
+
+def test_csr_workload_offsets():
+    cfg = gen.CONFIGS["c5csr"]
+    offs = gen.csr_offsets(cfg)
+    lens = np.diff(offs)
+    assert offs[0] == 0 and offs.size == cfg["nseg"] + 1 and offs[-1] == cfg["n"]
+    assert lens.min() >= 1 and lens.max() <= cfg["maxlen"] and abs(lens.mean() - 4096) < 100

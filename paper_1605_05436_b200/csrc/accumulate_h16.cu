@@ -175,7 +175,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
     int64_t* const bins64_all = smem64;                                       // [WARPS][NBIN64][32]
     uint32_t* const bins_all = reinterpret_cast<uint32_t*>(smem64 + H16_WARPS * F::NBIN64 * 32);
     __shared__ int64_t wsum[H16_WARPS][F::NBIN64];
-    __shared__ int64_t digits[64];
+    __shared__ int64_t digits[64];                          // grid-tail scratch
     __shared__ int64_t su[64];
     __shared__ uint32_t blk_flags;
     __shared__ int is_last;
@@ -190,7 +190,6 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
     for (int b = 0; b < F::NBIN; ++b) bins[b * 32] = 0;
 #pragma unroll
     for (int b = 0; b < F::NBIN64; ++b) bins64[b * 32] = 0;
-    if (tid < 64) digits[tid] = 0;
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
 
@@ -282,29 +281,32 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
         if (lane == 0 && f) atomicOr(&blk_flags, f);
     }
     __syncthreads();
-    // block bins -> 52-bit digits: bin (g, sign) is worth +-T 2^pos(g); split into the <= 3
-    // digits it overlaps and add them (shared int64 adds, once per bin per block)
-    if (warp == 0) {
-        for (int b = lane; b < F::NBIN64; b += 32) {
-            int64_t T = 0;
-            for (int w = 0; w < H16_WARPS; ++w) T += wsum[w][b];
-            const int P = F::pos(b >> 1);
-            const int i = P / W, o = P - W * (P / W);
-            const uint64_t u = (uint64_t)T;                         // T >= 0
-            const int64_t c0 = (int64_t)((u << o) & MASK);                  // bits [0, 52) of u 2^o
-            const int64_t c1 = (int64_t)((u >> (W - o)) & MASK);            // bits [52, 104)
-            const int64_t c2 = (2 * W - o < 64) ? (int64_t)(u >> (2 * W - o)) : 0;   // bits >= 104 (u < 2^63)
-            const int64_t sg = (b & 1) ? -1 : 1;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&digits[i]), (unsigned long long)(sg * c0));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&digits[i + 1]), (unsigned long long)(sg * c1));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&digits[i + 2]), (unsigned long long)(sg * c2));
-        }
-    }
-    __syncthreads();
+    // block bins -> 52-bit digits: group g's net value V_g = T(g,+) - T(g,-) is worth V_g 2^pos(g);
+    // its <= 3 chunks (constant shifts) go to the digits it overlaps. Lane j gathers the chunks of
+    // digits j and j+32 from the groups whose window covers them (no shared atomics).
+    __shared__ int64_t gch[F::NGF][3];
     int64_t a0 = 0, a1 = 0;
     if (warp == 0) {
-        a0 = digits[lane];
-        a1 = (lane + 32 < D) ? digits[lane + 32] : 0;
+        if (lane < F::NGF) {
+            int64_t tp = 0, tn = 0;
+            for (int w = 0; w < H16_WARPS; ++w) {
+                tp += wsum[w][2 * lane];
+                tn += wsum[w][2 * lane + 1];
+            }
+            const int64_t V = tp - tn;
+            const int P = F::pos(lane), o = P % W;
+            gch[lane][0] = (int64_t)(((uint64_t)V << o) & MASK);              // bits [0, 52) of V 2^o
+            gch[lane][1] = (V >> (W - o)) & (int64_t)MASK;                    // bits [52, 104)
+            gch[lane][2] = V >> (2 * W - o < 63 ? 2 * W - o : 63);            // bits >= 104 (signed)
+        }
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < F::NGF; ++g) {
+            const int i = F::pos(g) / W;
+            const int d0 = lane - i, d1 = lane + 32 - i;
+            if (d0 >= 0 && d0 < 3) a0 += gch[g][d0];
+            if (d1 >= 0 && d1 < 3) a1 += gch[g][d1];
+        }
         regularize_warp(a0, a1, lane);
     }
     grid_tail<H16_WARPS>(a0, a1, blk_flags, n, p, digits, su, &blk_flags, &is_last, warp, lane);

@@ -10,9 +10,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1605_05436_b200 as xsum  # noqa: E402
 import synth  # noqa: E402
 
-x_all = synth.device_generate("c2")
+kind = sys.argv[1] if len(sys.argv) > 1 else "f64"
+if kind == "f64":
+    x_all = synth.device_generate("c2")
+else:
+    x_all = synth.device_bits({"f32": "c2f32", "f16": "c2f16", "bf16": "c2bf16"}[kind])
 acc = xsum.Accumulator()
-for k in (10, 14, 16, 18, 20, 22, 24):
+for k in (10, 14, 16, 18, 20, 22, 24, 26, 28):
     x = x_all[: 1 << k].clone()
     for _ in range(5):
         acc.sum(x)

@@ -53,6 +53,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     __shared__ int is_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) xs_stamp(p.partial, 0, blockIdx.x);                 // block start
     int64_t* col = win + warp * (D * 32) + lane;
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
@@ -131,6 +132,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
         if ((uint64_t)tid < head) EL::add_one_checked(col, x + tid, flags, one);
         if (tid >= PV && (uint64_t)(tid - PV) < tail) EL::add_one_checked(col, x + head + nvec * PV + (tid - PV), flags, one);
     }
+    if (tid == 0) xs_stamp(p.partial, 1, blockIdx.x);                 // stream done
     if (__any_sync(FULL, EL::hit(nspec))) {
         if (EL::hit(nspec) && any_tile) {
             regularize_column(col);
@@ -150,6 +152,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
         if (lane == 0 && f) atomicOr(&blk_flags, f);
     }
     __syncthreads();
+    if (tid == 0) xs_stamp(p.partial, 2, blockIdx.x);                 // warp combines done
 
     // block: sum the warp partials (|.| <= WARPS*(2^51+2^16) < 2^56), regularize, publish;
     // the last block merges the grid (grid_tail.cuh).

@@ -107,6 +107,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) xs_stamp(p.partial, 3, blockIdx.x);        // arrival atomic returned
     if (!*sh_last) return;
     __threadfence();
 
@@ -149,6 +150,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
         if (lane == 0) *sh_flags = f;
     }
     __syncthreads();
+    if (threadIdx.x == 0) xs_stamp(p.partial, 4, 0);                  // last block: partials merged
     if (warp == 0) {
         int64_t b0 = red[lane] + st0, b1 = (lane + 32 < D) ? red[lane + 32] + st1 : 0;
         uint32_t fl = *sh_flags;
@@ -170,6 +172,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
             xsum_result r = finalize_warp(b0, b1, fl, cnt, p.canon, su, lane);
             if (lane == 0) *p.res = r;
         }
+        if (lane == 0) xs_stamp(p.partial, 5, 0);                     // last block: done
     }
 }
 

@@ -43,6 +43,22 @@ constexpr size_t SCRATCH_BYTES = SCRATCH_FLAGS_OFF + sizeof(uint32_t) * XS_MAXB;
 
 void note_launch();
 
+// XS_TIMING=1 (diagnostic builds, tools/timing_probe.py): per-block %globaltimer stamps written
+// into the unused columns (>= 512) of the scratch partial table: stamp k of block b at
+// partial[(D-1-k) * XS_MAXB + 512 + b]. 0 in the product.
+#ifndef XS_TIMING
+#define XS_TIMING 0
+#endif
+__device__ __forceinline__ void xs_stamp(int64_t* partial, int k, unsigned b) {
+#if XS_TIMING
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    partial[(size_t)(XSUM_NDIGITS - 1 - k) * XS_MAXB + 512 + b] = (int64_t)t;
+#else
+    (void)partial; (void)k; (void)b;
+#endif
+}
+
 // Opt `kernel` into `bytes` of dynamic shared memory once per device: the attribute belongs to
 // the function in the current device's context, so a process driving several GPUs sets it on
 // each. `done` is the caller's per-kernel bitmask of devices (device index < 64).

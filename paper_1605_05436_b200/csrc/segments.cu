@@ -34,7 +34,7 @@ __device__ __noinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_
 // Per-segment epilogue (one warp): combine the 32 lane columns (|sum| <= 32 (2^51 + 2^11)
 // < 2^57), regularize, canonicalize and round, write
 // the outputs, and zero the lane column for the next segment.
-__device__ __noinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
+__device__ __forceinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
                                               uint64_t len, uint64_t s, const SegOut& o, int lane) {
     __syncwarp();
     int64_t a0, a1;
@@ -43,7 +43,8 @@ __device__ __noinline__ void segment_epilogue(int64_t* col, const int64_t* wb, i
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
     flags = __reduce_or_sync(FULL, flags);
-    xsum_result r = finalize_warp(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
+    // inline (finalize_warp_inl): an out-of-line call would wait for the next segment's loads
+    xsum_result r = finalize_warp_inl(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
     if (lane == 0) o.write(s, r);
 }
 
@@ -56,27 +57,41 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
     int64_t* col = win + warp * (D * 32) + lane;
     const uint64_t nw = (uint64_t)gridDim.x * SEG_WARPS;
 
-    for (uint64_t s = (uint64_t)blockIdx.x * SEG_WARPS + warp; s < nseg; s += nw) {
-        const uint64_t beg = offsets ? offsets[s] : s * seg_len;
-        const uint64_t len = offsets ? offsets[s + 1] - beg : seg_len;
-        const double* xs = x + beg;
+    // A warp's segments s, s + nw, ...: the next segment's bounds and first tile are fetched
+    // before the current segment's epilogue, so its DRAM latency hides behind the epilogue.
+    struct Seg {
+        const double* xs;
+        uint64_t len, head, nbody, nvec, nit;
+        const uint4* body;
+    };
+    auto open_seg = [&](uint64_t sj) {
+        Seg g;
+        const uint64_t beg = offsets ? offsets[sj] : sj * seg_len;
+        g.len = offsets ? offsets[sj + 1] - beg : seg_len;
+        g.xs = x + beg;
+        g.head = (g.len && ((uintptr_t)g.xs & 15)) ? 1 : 0;
+        g.nbody = g.len - g.head;
+        g.nvec = g.nbody >> 1;
+        g.body = reinterpret_cast<const uint4*>(g.xs + g.head);
+        g.nit = g.nvec / (32 * SEG_U);
+        return g;
+    };
+    uint64_t s = (uint64_t)blockIdx.x * SEG_WARPS + warp;
+    if (s >= nseg) return;                                           // warp-uniform
 #pragma unroll
-        for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    Seg g = open_seg(s);
+    uint4 cur[SEG_U];
+    if (g.nit) {
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
+    }
+    while (true) {
         uint32_t flags = 0, nspec = 0;
-
-        const uint64_t head = (len && ((uintptr_t)xs & 15)) ? 1 : 0;
-        const uint64_t nbody = len - head;
-        const uint64_t nvec = nbody >> 1;
-        const uint4* body = reinterpret_cast<const uint4*>(xs + head);
-        const uint64_t nit = nvec / (32 * SEG_U);
-
+        const uint64_t nit = g.nit, nvec = g.nvec;
+        const uint4* body = g.body;
         uint64_t wstart = 0;
         int since = 0;
-        uint4 cur[SEG_U];
-        if (nit) {
-#pragma unroll
-            for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(body + u * 32 + lane);
-        }
         for (uint64_t it = 0; it < nit; ++it) {
             uint4 nxt[SEG_U];
             if (it + 1 < nit) {
@@ -107,18 +122,26 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
                 wstart = it + 1;
             }
         }
-        // leftover vectors, head and tail: checked adds
-        for (uint64_t v = nit * (32 * SEG_U) + lane; v < nvec; v += 32) {
-            uint4 q = ldg_stream(body + v);
-            column_add_checked(col, q.x, q.y, flags, one);
-            column_add_checked(col, q.z, q.w, flags, one);
+        // leftover vectors (issued together before use), head and tail: checked adds
+        uint4 lv[SEG_U];
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) {
+            const uint64_t v = nit * (32 * SEG_U) + u * 32 + lane;
+            if (v < nvec) lv[u] = ldg_stream(body + v);
         }
-        if (lane == 0 && head) {
-            uint2 q = ldg_one(xs);
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) {
+            if (nit * (32 * SEG_U) + u * 32 + lane < nvec) {
+                column_add_checked(col, lv[u].x, lv[u].y, flags, one);
+                column_add_checked(col, lv[u].z, lv[u].w, flags, one);
+            }
+        }
+        if (lane == 0 && g.head) {
+            uint2 q = ldg_one(g.xs);
             column_add_checked(col, q.x, q.y, flags, one);
         }
-        if (lane == 1 && (nbody & 1)) {
-            uint2 q = ldg_one(xs + head + 2 * nvec);
+        if (lane == 1 && (g.nbody & 1)) {
+            uint2 q = ldg_one(g.xs + g.head + 2 * nvec);
             column_add_checked(col, q.x, q.y, flags, one);
         }
         if (__any_sync(FULL, spec_hit(nspec))) {        // raw columns go to the epilogue
@@ -127,7 +150,20 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
                 seg_rescan(col, body, wstart, nit - 1, lane, flags, one);
             }
         }
+        // prefetch the next segment, then close this one (the epilogue zeroes the columns)
+        const uint64_t sn = s + nw;
+        const bool more = sn < nseg;
+        const uint64_t len = g.len;
+        if (more) {
+            g = open_seg(sn);
+            if (g.nit) {
+#pragma unroll
+                for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
+            }
+        }
         segment_epilogue(col, win + warp * (D * 32), su[warp], flags, len, s, o, lane);
+        if (!more) break;
+        s = sn;
     }
 }
 

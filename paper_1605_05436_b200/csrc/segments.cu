@@ -64,10 +64,16 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         uint64_t len, head, nbody, nvec, nit;
         const uint4* body;
     };
-    auto open_seg = [&](uint64_t sj) {
+    // CSR bounds of the segment after next are loaded one segment ahead (ob, oe)
+    auto bounds = [&](uint64_t sj, uint64_t& b, uint64_t& e) {
+        if (sj < nseg) {
+            b = offsets ? __ldg(offsets + sj) : sj * seg_len;
+            e = offsets ? __ldg(offsets + sj + 1) : b + seg_len;
+        }
+    };
+    auto open_seg = [&](uint64_t beg, uint64_t end) {
         Seg g;
-        const uint64_t beg = offsets ? offsets[sj] : sj * seg_len;
-        g.len = offsets ? offsets[sj + 1] - beg : seg_len;
+        g.len = end - beg;
         g.xs = x + beg;
         g.head = (g.len && ((uintptr_t)g.xs & 15)) ? 1 : 0;
         g.nbody = g.len - g.head;
@@ -80,13 +86,16 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
     if (s >= nseg) return;                                           // warp-uniform
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
-    Seg g = open_seg(s);
+    uint64_t cb = 0, ce = 0, ob = 0, oe = 0;
+    bounds(s, cb, ce);
+    Seg g = open_seg(cb, ce);
     uint4 cur[SEG_U];
     if (g.nit) {
 #pragma unroll
         for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
     }
     while (true) {
+        bounds(s + nw, ob, oe);                                      // next segment's bounds, early
         uint32_t flags = 0, nspec = 0;
         const uint64_t nit = g.nit, nvec = g.nvec;
         const uint4* body = g.body;
@@ -155,7 +164,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         const bool more = sn < nseg;
         const uint64_t len = g.len;
         if (more) {
-            g = open_seg(sn);
+            g = open_seg(ob, oe);
             if (g.nit) {
 #pragma unroll
                 for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);

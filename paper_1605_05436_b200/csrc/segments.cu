@@ -101,23 +101,19 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         const uint4* body = g.body;
         uint64_t wstart = 0;
         int since = 0;
-        for (uint64_t it = 0; it < nit; ++it) {
-            uint4 nxt[SEG_U];
-            if (it + 1 < nit) {
-#pragma unroll
-                for (int u = 0; u < SEG_U; ++u) nxt[u] = ldg_stream(body + (it + 1) * (32 * SEG_U) + u * 32 + lane);
-            }
+        // two register buffers alternate without copies (a copy would wait for the loads in
+        // flight): tile it+1 loads while tile it is decoded
+        uint4 alt[SEG_U];
+        auto process = [&](const uint4 (&bf)[SEG_U], uint64_t it) {
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) {
-                Chunks a = decompose(cur[u].x, cur[u].y, one, mone);
+                Chunks a = decompose(bf[u].x, bf[u].y, one, mone);
                 nspec = spec_fold(nspec, a);
                 column_add(col, a, one);
-                Chunks b = decompose(cur[u].z, cur[u].w, one, mone);
+                Chunks b = decompose(bf[u].z, bf[u].w, one, mone);
                 nspec = spec_fold(nspec, b);
                 column_add(col, b, one);
             }
-#pragma unroll
-            for (int u = 0; u < SEG_U; ++u) cur[u] = nxt[u];
             if (++since == SEG_FLUSH_ITERS) {
                 regularize_column(col);
                 if (__any_sync(FULL, spec_hit(nspec))) {
@@ -130,6 +126,19 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
                 since = 0;
                 wstart = it + 1;
             }
+        };
+        for (uint64_t it = 0; it < nit; it += 2) {
+            if (it + 1 < nit) {
+#pragma unroll
+                for (int u = 0; u < SEG_U; ++u) alt[u] = ldg_stream(body + (it + 1) * (32 * SEG_U) + u * 32 + lane);
+            }
+            process(cur, it);
+            if (it + 1 >= nit) break;
+            if (it + 2 < nit) {
+#pragma unroll
+                for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(body + (it + 2) * (32 * SEG_U) + u * 32 + lane);
+            }
+            process(alt, it + 1);
         }
         // leftover vectors (issued together before use), head and tail: checked adds
         uint4 lv[SEG_U];

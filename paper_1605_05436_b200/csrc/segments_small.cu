@@ -97,38 +97,98 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
     const int64_t* wb = win + warp * (D * 32);
     const uint64_t nw = (uint64_t)gridDim.x * SSEG_WARPS;
     constexpr int PV = F::per_vec;
-    // vectors a lane may add between regularizations (plus <= 2 head/tail elements)
-    constexpr uint32_t WIN_VECS = (FLUSH_ELEMS - 2) / PV;
 
-    for (uint64_t s = (uint64_t)blockIdx.x * SSEG_WARPS + warp; s < nseg; s += nw) {
-        const uint64_t beg = offsets ? offsets[s] : s * seg_len;
-        const uint64_t len = offsets ? offsets[s + 1] - beg : seg_len;
-        const uint8_t* xs = x + beg * F::eb;
+    constexpr int SU = 4;                                   // vectors per lane per tile
+    constexpr uint32_t WIN_TILES = (FLUSH_ELEMS - 2 - SU * PV) / (SU * PV);   // + leftovers + head/tail
+    struct Seg {
+        const uint8_t* xs;
+        uint64_t len, head, nvec, tail, nit;
+        const uint4* body;
+    };
+    auto open_seg = [&](uint64_t sj) {
+        Seg g;
+        const uint64_t beg = offsets ? offsets[sj] : sj * seg_len;
+        g.len = offsets ? offsets[sj + 1] - beg : seg_len;
+        g.xs = x + beg * F::eb;
+        g.head = ((16 - ((uintptr_t)g.xs & 15)) & 15) / F::eb;
+        if (g.head > g.len) g.head = g.len;
+        g.nvec = (g.len - g.head) / PV;
+        g.tail = g.len - g.head - g.nvec * PV;
+        g.body = reinterpret_cast<const uint4*>(g.xs + g.head * F::eb);
+        g.nit = g.nvec / (32 * SU);
+        return g;
+    };
+    uint64_t s = (uint64_t)blockIdx.x * SSEG_WARPS + warp;
+    if (s >= nseg) return;                                  // warp-uniform
 #pragma unroll
-        for (int j = 0; j < D; ++j) col[j * 32] = 0;
-        uint32_t flags = 0;
-        uint64_t head = ((16 - ((uintptr_t)xs & 15)) & 15) / F::eb;
-        if (head > len) head = len;
-        const uint64_t nvec = (len - head) / PV;
-        const uint64_t tail = len - head - nvec * PV;
-        const uint4* body = reinterpret_cast<const uint4*>(xs + head * F::eb);
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    Seg g = open_seg(s);
+    uint4 cur[SU], alt[SU];
+    if (g.nit) {
+#pragma unroll
+        for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
+    }
+    while (true) {
+        uint32_t flags = 0, since = 0;
+        const uint64_t nit = g.nit, nvec = g.nvec;
+        const uint4* body = g.body;
         // head / tail: one element per lane (head < PV <= 8, tail < PV)
-        if ((uint64_t)lane < head) sadd<F>(col, sload_one<F>(xs + lane * F::eb), flags, one);
-        if (lane >= 8 && (uint64_t)(lane - 8) < tail)
-            sadd<F>(col, sload_one<F>(xs + (head + nvec * PV + (lane - 8)) * F::eb), flags, one);
-        uint32_t since = 0;
-        for (uint64_t v = lane; v < nvec; v += 32) {
-            sadd_vec<F>(col, ldg_stream(body + v), flags, one);
-            if (++since == WIN_VECS) { regularize_column(col); since = 0; }
+        if ((uint64_t)lane < g.head) sadd<F>(col, sload_one<F>(g.xs + lane * F::eb), flags, one);
+        if (lane >= 8 && (uint64_t)(lane - 8) < g.tail)
+            sadd<F>(col, sload_one<F>(g.xs + (g.head + nvec * PV + (lane - 8)) * F::eb), flags, one);
+        // full tiles: two register buffers alternate (tile it+1 loads while tile it is added)
+        auto process = [&](const uint4 (&bf)[SU]) {
+#pragma unroll
+            for (int u = 0; u < SU; ++u) sadd_vec<F>(col, bf[u], flags, one);
+            if (++since == WIN_TILES) { regularize_column(col); since = 0; }
+        };
+        for (uint64_t it = 0; it < nit; it += 2) {
+            if (it + 1 < nit) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) alt[u] = ldg_stream(body + (it + 1) * (32 * SU) + u * 32 + lane);
+            }
+            process(cur);
+            if (it + 1 >= nit) break;
+            if (it + 2 < nit) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(body + (it + 2) * (32 * SU) + u * 32 + lane);
+            }
+            process(alt);
+        }
+        // leftover vectors (< one tile), loaded together before use
+        uint4 lv[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+            const uint64_t v = nit * (32 * SU) + u * 32 + lane;
+            if (v < nvec) lv[u] = ldg_stream(body + v);
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+            if (nit * (32 * SU) + u * 32 + lane < nvec) sadd_vec<F>(col, lv[u], flags, one);
+        // prefetch the next segment, then close this one
+        const uint64_t sn = s + nw;
+        const bool more = sn < nseg;
+        const uint64_t len = g.len;
+        if (more) {
+            g = open_seg(sn);
+            if (g.nit) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
+            }
         }
         __syncwarp();
         int64_t a0, a1;
         combine_raw_columns(wb, a0, a1, lane);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < D; ++j) col[j * 32] = 0;
         flags = __reduce_or_sync(FULL, flags);
         const xsum_result r =
-            finalize_warp(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su[warp], lane);
+            finalize_warp_inl(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su[warp], lane);
         if (lane == 0) o.write(s, r);
         __syncwarp();
+        if (!more) break;
+        s = sn;
     }
 }
 

@@ -54,6 +54,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) xs_stamp(p.partial, 0, blockIdx.x);                 // block start
+    pdl_release_dependents();    // the next launch may take SMs as this grid's blocks finish
     int64_t* col = win + warp * (D * 32) + lane;
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
@@ -179,9 +180,9 @@ static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p,
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    k_accumulate<WARPS, U, NB, E><<<(unsigned)g, C::T, C::SMEM, s>>>(x, n, p);
+    cudaError_t e = launch_pdl(k_accumulate<WARPS, U, NB, E>, (unsigned)g, C::T, C::SMEM, s, x, n, p);
     note_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 #ifndef XS_ACC_WARPS

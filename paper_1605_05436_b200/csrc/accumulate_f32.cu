@@ -128,6 +128,7 @@ k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
     __shared__ int is_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_release_dependents();    // the next launch may take SMs as this grid's blocks finish
     int64_t* col = win + warp * (D * 32) + lane;
     int64_t* bins = win + F32B_WARPS * D * 32 + warp * (F32B_NBIN * 32) + lane;
 #pragma unroll
@@ -249,9 +250,9 @@ cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int n
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    k_accumulate_f32b<<<(unsigned)g, F32B_WARPS * 32, SMEM, s>>>(x, n, p);
+    cudaError_t e = launch_pdl(k_accumulate_f32b, (unsigned)g, F32B_WARPS * 32, SMEM, s, x, n, p);
     note_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace xs

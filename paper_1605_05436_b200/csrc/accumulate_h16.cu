@@ -181,6 +181,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
     __shared__ int is_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_release_dependents();    // the next launch may take SMs as this grid's blocks finish
     uint32_t* bins = bins_all + warp * (F::NBIN * 32) + lane;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bins);
     const uint32_t sbase2 = sbase * 0x00010001u;
@@ -323,9 +324,9 @@ static cudaError_t launch_h16(const uint16_t* x, uint64_t n, const AccParams& p,
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    k_accumulate_h16<F><<<(unsigned)g, H16_WARPS * 32, SMEM, s>>>(x, n, p);
+    cudaError_t e = launch_pdl(k_accumulate_h16<F>, (unsigned)g, H16_WARPS * 32, SMEM, s, x, n, p);
     note_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t accumulate_h16(const uint16_t* x, uint64_t n, int bf16, const AccParams& p, int num_sms, cudaStream_t s) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <new>
 
 #include "xsum.h"
@@ -13,6 +14,13 @@ static std::atomic<uint64_t> g_launches{0};
 
 namespace xs {
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("XSUM_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 }  // namespace xs
 
 struct xsum_ctx {

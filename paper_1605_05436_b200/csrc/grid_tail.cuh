@@ -93,6 +93,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
                                           int64_t* red, int64_t* su, uint32_t* sh_flags, int* sh_last, int warp,
                                           int lane) {
     const uint64_t G = gridDim.x;
+    pdl_wait_predecessor();      // the previous launch may still be merging in the scratch / state
     if (warp == 0) {
         p.partial[(size_t)lane * XS_MAXB + blockIdx.x] = a0;
         if (lane + 32 < D) p.partial[(size_t)(lane + 32) * XS_MAXB + blockIdx.x] = a1;

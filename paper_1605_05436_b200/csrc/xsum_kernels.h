@@ -43,6 +43,34 @@ constexpr size_t SCRATCH_BYTES = SCRATCH_FLAGS_OFF + sizeof(uint32_t) * XS_MAXB;
 
 void note_launch();
 
+// Programmatic dependent launch (sm_90+): an accumulate launch may start its blocks while the
+// previous kernel in the stream is still finishing (its last block merging and rounding, slower
+// SMs streaming their last tiles); the kernel waits for the predecessor's completion
+// (griddepcontrol.wait in grid_tail) before it touches the scratch table or the state, and it
+// only reads its input before that point. A predecessor that is not an xsum accumulate kernel
+// releases its dependents at completion, so inputs produced by earlier kernels are complete.
+// XSUM_NO_PDL=1 in the environment launches normally (A/B measurements).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+__device__ __forceinline__ void pdl_release_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait_predecessor() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // XS_TIMING=1 (diagnostic builds, tools/timing_probe.py): per-block %globaltimer stamps written
 // into the unused columns (>= 512) of the scratch partial table: stamp k of block b at
 // partial[(D-1-k) * XS_MAXB + 512 + b]. 0 in the product.

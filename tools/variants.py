@@ -1,7 +1,9 @@
 """Build and time compile-time variants of the accumulate kernel (development tool).
 
-    python tools/variants.py build            # here (nvcc cross-compiles)
-    python tools/variants.py run [cfg ...]    # on the GPU box: one JSON line per variant
+    python tools/variants.py build [name ...]   # here (nvcc cross-compiles)
+    python tools/variants.py run [cfg ...]      # on the GPU box: one JSON line per built variant
+cfg: c1..c5 (binary64 configs), c5seg (segments of c5), f32 / f16 / bf16 (random finite
+patterns), n<k> (the first 2^k elements of c2).
 Variants named exp* are diagnostic builds that compute WRONG sums (timing only)."""
 from __future__ import annotations
 
@@ -16,10 +18,12 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
-    "seg_u8nb2": ["-DXS_SEG_U=8", "-DXS_SEG_NB=2"],
-    "seg_u2nb4": ["-DXS_SEG_U=2", "-DXS_SEG_NB=4"],
-    "seg_u2nb8": ["-DXS_SEG_U=2", "-DXS_SEG_NB=8"],
-    "seg_u4nb4": ["-DXS_SEG_U=4", "-DXS_SEG_NB=4"],
+    # examples of compile-time knobs (see the kernels): register-buffer depth of each kernel
+    "acc_nb4": ["-DXS_ACC_NB=4"],
+    "seg_nb4": ["-DXS_SEG_NB=4"],
+    "h16_nb2": ["-DXS_H16_NB=2"],
+    "h16_ldsts": ["-DXS_H16_LDSTS"],
+    "f32b_nb4": ["-DXS_F32B_NB=4"],
 }
 
 

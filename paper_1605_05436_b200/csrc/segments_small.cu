@@ -3,12 +3,16 @@
 //
 // One warp per segment (the paper's per-partition combine), lanes striding
 // over the segment with 16-byte loads. Each element of the paper's t-bit / l-bit format
-// is M 2^k in units of its least subnormal, i.e. M at bit k + OFF of the
-// 2^-1074 window (binary32 OFF = 925, binary16 1050, bfloat16 941); it is split into the two
-// 52-bit digit chunks of PAPER.md:744-750 and added to the lane's column with carries deferred
-// (regularized every FLUSH_ELEMS adds). NaN/Inf patterns are flagged, not
-// added (reading R10). At the segment's end the 32 columns are combined and finalize_warp
-// canonicalizes and rounds (binary64 and binary32).
+// is M 2^k in units of its least subnormal (M < 2^(t+1), k = max(e,1) - 1),
+// i.e. M at bit k + OFF of the 2^-1074 window (binary32 OFF = 925, binary16 1050, bfloat16 941).
+// As in K8, each lane adds M 2^(ep mod 32) (ep = max(e,1)) into an unsigned 64-bit bin per
+// (sign, group of 32 exponents) - one 64-bit read-modify-write per element, carries deferred
+// - and empties the bins into a narrow digit column (only the digits the
+// format reaches, from COL0 on) every 511 adds and at the segment's end. NaN/Inf patterns are
+// summed as if finite; a per-lane max of ep sends a segment that held one to a rescan that
+// cancels them exactly and sets the flags (reading R10). At the segment's end the 32 narrow
+// columns are combined, moved to their digit positions and rounded by finalize_warp (binary64
+// and binary32).
 #include <cuda_runtime.h>
 
 #include "xsum_device.cuh"
@@ -20,61 +24,100 @@ template <int T_, int L_, int OFF_, int EB_>
 struct SFmt {
     static constexpr int t = T_, l = L_, off = OFF_, eb = EB_;
     static constexpr int per_vec = 16 / EB_;
+    static constexpr uint32_t EM = (1u << L_) - 1u;            // exponent field of NaN/Inf
+    static constexpr int NG = (int)(EM / 32u) + 1;             // groups g = ep >> 5, ep <= EM
+    static constexpr int NBIN = 2 * NG;                        // bin 2 g + sign
+    static constexpr int pos(int g) { return OFF_ - 1 + 32 * g; }   // bit position of group g
+    static constexpr int COL0 = pos(0) / 52;
+    // digits the bins reach (+2 for a chunk's span) plus room for the carries of 2^63 summands
+    static constexpr int COLS = pos(NG - 1) / 52 + 2 - COL0 + 4;
 };
 using SF32 = SFmt<23, 8, 925, 4>;
 using SF16 = SFmt<10, 5, 1050, 2>;
 using SBF16 = SFmt<7, 8, 941, 2>;
+static_assert(SF32::NG == 8 && SBF16::NG == 8 && SF16::NG == 1, "exponent groups");
+static_assert(SF32::COL0 + SF32::COLS <= D && SBF16::COL0 + SBF16::COLS <= D, "column window");
 
-// Element bits b (the low 8*eb bits): chunks of sign * M * 2^(k + off); spec = 1 for NaN/Inf.
+constexpr int SSEG_FLUSH = 511;            // 511 adds of M 2^o < 2^55 stay below 2^64
+constexpr int SSEG_REG_FLUSHES = 128;      // <= 10 chunks per digit per flush: 2^51 + 1280 * 2^52 < 2^63
+
+// One element: bits b (the low 8*eb bits). Adds M 2^o into bin (ep >> 5, sign); `bins` = this
+// lane's bin column (bin j at word j*32, byte offset 256 j = 16 (ep - o) + 256 s).
 template <class F>
-__device__ __forceinline__ Chunks sdecode(uint32_t b, uint32_t one) {
+__device__ __forceinline__ void sbin_add(uint64_t* bins, uint32_t b, uint32_t& spec, uint32_t one) {
     constexpr uint32_t SBIT = F::t + F::l;
-    constexpr uint32_t EM = (1u << F::l) - 1u;
-    Chunks c;
     const uint32_t h = b & ((1u << SBIT) - 1u);
-    const uint32_t e = h >> F::t;
-    const uint32_t ep = max(e, 1u);
-    const uint32_t M = h - ((ep - 1u) << F::t);                  // m + [e != 0] 2^t
-    const uint32_t K = mad_u32(ep, one, (uint32_t)F::off - 1u);  // k + off
-    const uint32_t i = mulhi_u32(K, K52);                        // K / 52
-    const uint32_t o = K - 52u * i;
-    const int64_t sM = ((b >> SBIT) & 1u) ? -(int64_t)M : (int64_t)M;
-    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
-    c.c1 = sM >> (52u - o);
-    c.i = i;
-    c.spec = (e == EM);
-    return c;
+    const uint32_t ep = max(h >> F::t, 1u);
+    const uint32_t M = mad_u32(ep, 0u - (1u << F::t), mad_u32(h, one, 1u << F::t));   // m + [e!=0] 2^t
+    const uint32_t o = ep & 31u;
+    uint32_t vhi;
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(vhi) : "r"(M), "r"(0u), "r"(o));
+    const uint64_t v = ((uint64_t)vhi << 32) | (M << o);
+    spec = max(spec, ep);
+    const uint32_t off = mad_u32(mad_u32(o, 0xFFFFFFFFu, ep), 16u, ((b >> SBIT) & 1u) << 8);
+    XS_ASSERT(off / 256 < (uint32_t)F::NBIN);
+    *reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(bins) + off) += v;
 }
 
 template <class F>
 __device__ __forceinline__ uint32_t sspecial_flags(uint32_t b) {
     constexpr uint32_t SBIT = F::t + F::l;
-    constexpr uint32_t EM = (1u << F::l) - 1u;
-    if (((b >> F::t) & EM) != EM) return 0;
+    if (((b >> F::t) & F::EM) != F::EM) return 0;
     if (b & ((1u << F::t) - 1u)) return XSUM_F_NAN;
     return ((b >> SBIT) & 1u) ? XSUM_F_NINF : XSUM_F_PINF;
 }
 
-template <class F>
-__device__ __forceinline__ void sadd(int64_t* col, uint32_t b, uint32_t& flags, uint32_t one) {
-    const Chunks c = sdecode<F>(b, one);
-    if (c.spec) { flags |= sspecial_flags<F>(b); return; }
-    column_add(col, c, one);
-}
-
 // the elements of a 16-byte vector
 template <class F>
-__device__ __forceinline__ void sadd_vec(int64_t* col, const uint4& v, uint32_t& flags, uint32_t one) {
+__device__ __forceinline__ void sbin_add_vec(uint64_t* bins, const uint4& v, uint32_t& spec, uint32_t one) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         if (F::eb == 4) {
-            sadd<F>(col, w[q], flags, one);
+            sbin_add<F>(bins, w[q], spec, one);
         } else {
-            sadd<F>(col, w[q] & 0xFFFFu, flags, one);
-            sadd<F>(col, w[q] >> 16, flags, one);
+            sbin_add<F>(bins, w[q] & 0xFFFFu, spec, one);
+            sbin_add<F>(bins, w[q] >> 16, spec, one);
         }
     }
+}
+
+// Bins -> narrow column (row r = digit COL0 + r): bin (g, s) is worth (-1)^s V 2^pos(g); V 2^o
+// (o = pos mod 52) splits into c0 + c1 2^52 + c2 2^104, all >= 0 (constant shifts).
+template <class F>
+__device__ __forceinline__ void sbin_flush(uint64_t* bins, int64_t* col) {
+#pragma unroll
+    for (int j = 0; j < F::NBIN; ++j) {
+        const int P = F::pos(j >> 1), i = P / W - F::COL0, o = P % W;
+        const uint64_t V = bins[j * 32];
+        bins[j * 32] = 0;
+        const int64_t c0 = (int64_t)((V << o) & MASK);
+        const int64_t c1 = (int64_t)((V >> (W - o)) & MASK);
+        const int64_t c2 = (int64_t)(2 * W - o < 64 ? V >> (2 * W - o) : 0);
+        XS_ASSERT(i >= 0 && i + 2 < F::COLS - 1);
+        if (j & 1) {
+            col[i * 32] -= c0;
+            col[(i + 1) * 32] -= c1;
+            col[(i + 2) * 32] -= c2;
+        } else {
+            col[i * 32] += c0;
+            col[(i + 1) * 32] += c1;
+            col[(i + 2) * 32] += c2;
+        }
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void scol_regularize(int64_t* col) {
+    int64_t cin = 0;
+#pragma unroll
+    for (int j = 0; j < F::COLS - 1; ++j) {
+        const int64_t y = col[j * 32];
+        const int64_t c = balanced_carry(y);
+        col[j * 32] = y - (c << W) + cin;
+        cin = c;
+    }
+    col[(F::COLS - 1) * 32] += cin;
 }
 
 template <class F>
@@ -84,7 +127,48 @@ __device__ __forceinline__ uint32_t sload_one(const uint8_t* p) {
 }
 
 constexpr int SSEG_WARPS = 8;
-constexpr size_t SSEG_SMEM = (size_t)SSEG_WARPS * D * 32 * sizeof(int64_t);
+constexpr int SSEG_U = 4;                  // vectors per lane per tile
+
+template <class F>
+constexpr size_t sseg_smem() { return (size_t)SSEG_WARPS * 32 * (F::COLS + F::NBIN) * sizeof(int64_t); }
+
+// Rare path: the segment held NaN/Inf patterns (summed as finite values): re-read it, set the
+// flags and cancel them (the sign-flipped pattern lands in the other sign's bin of the same
+// group), flush.
+template <class F>
+__device__ __noinline__ void sseg_rescan(uint64_t* bins, int64_t* col, const uint8_t* xs, uint64_t head,
+                                         const uint4* body, uint64_t nvec, uint64_t tail, int lane, uint32_t& flags,
+                                         uint32_t one) {
+    uint32_t dummy = 0, adds = 0, flushes = 0;
+    scol_regularize<F>(col);                            // fresh headroom for the flushes below
+    auto fix = [&](uint32_t b) {
+        const uint32_t f = sspecial_flags<F>(b);
+        if (f) {
+            flags |= f;
+            sbin_add<F>(bins, b ^ (1u << (F::t + F::l)), dummy, one);
+            if (++adds == SSEG_FLUSH) {                 // a lane may cancel any number of specials
+                sbin_flush<F>(bins, col);
+                adds = 0;
+                if (++flushes == SSEG_REG_FLUSHES) { scol_regularize<F>(col); flushes = 0; }
+            }
+        }
+    };
+    if ((uint64_t)lane < head) fix(sload_one<F>(xs + lane * F::eb));
+    if (lane >= 8 && (uint64_t)(lane - 8) < tail) fix(sload_one<F>(xs + (head + nvec * F::per_vec + (lane - 8)) * F::eb));
+    for (uint64_t v = lane; v < nvec; v += 32) {
+        const uint4 q = ldg_stream(body + v);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        for (int i = 0; i < 4; ++i) {
+            if (F::eb == 4) {
+                fix(w[i]);
+            } else {
+                fix(w[i] & 0xFFFFu);
+                fix(w[i] >> 16);
+            }
+        }
+    }
+    sbin_flush<F>(bins, col);
+}
 
 template <class F>
 __global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
@@ -93,13 +177,13 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SSEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t* col = win + warp * (D * 32) + lane;
-    const int64_t* wb = win + warp * (D * 32);
+    int64_t* col = win + warp * (F::COLS * 32) + lane;
+    const int64_t* wb = win + warp * (F::COLS * 32);
+    uint64_t* bins = reinterpret_cast<uint64_t*>(win + SSEG_WARPS * F::COLS * 32) + warp * (F::NBIN * 32) + lane;
     const uint64_t nw = (uint64_t)gridDim.x * SSEG_WARPS;
     constexpr int PV = F::per_vec;
-
-    constexpr int SU = 4;                                   // vectors per lane per tile
-    constexpr uint32_t WIN_TILES = (FLUSH_ELEMS - 2 - SU * PV) / (SU * PV);   // + leftovers + head/tail
+    constexpr int SU = SSEG_U;
+    constexpr uint32_t WIN_TILES = (SSEG_FLUSH - 2 - SU * PV) / (SU * PV);   // + leftovers + head/tail
     struct Seg {
         const uint8_t* xs;
         uint64_t len, head, nvec, tail, nit;
@@ -121,7 +205,9 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
     uint64_t s = (uint64_t)blockIdx.x * SSEG_WARPS + warp;
     if (s >= nseg) return;                                  // warp-uniform
 #pragma unroll
-    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    for (int j = 0; j < F::COLS; ++j) col[j * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < F::NBIN; ++j) bins[j * 32] = 0;
     Seg g = open_seg(s);
     uint4 cur[SU], alt[SU];
     if (g.nit) {
@@ -129,18 +215,22 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
         for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
     }
     while (true) {
-        uint32_t flags = 0, since = 0;
+        uint32_t flags = 0, since = 0, spec = 0, flushes = 0;
         const uint64_t nit = g.nit, nvec = g.nvec;
         const uint4* body = g.body;
         // head / tail: one element per lane (head < PV <= 8, tail < PV)
-        if ((uint64_t)lane < g.head) sadd<F>(col, sload_one<F>(g.xs + lane * F::eb), flags, one);
+        if ((uint64_t)lane < g.head) sbin_add<F>(bins, sload_one<F>(g.xs + lane * F::eb), spec, one);
         if (lane >= 8 && (uint64_t)(lane - 8) < g.tail)
-            sadd<F>(col, sload_one<F>(g.xs + (g.head + nvec * PV + (lane - 8)) * F::eb), flags, one);
+            sbin_add<F>(bins, sload_one<F>(g.xs + (g.head + nvec * PV + (lane - 8)) * F::eb), spec, one);
         // full tiles: two register buffers alternate (tile it+1 loads while tile it is added)
         auto process = [&](const uint4 (&bf)[SU]) {
 #pragma unroll
-            for (int u = 0; u < SU; ++u) sadd_vec<F>(col, bf[u], flags, one);
-            if (++since == WIN_TILES) { regularize_column(col); since = 0; }
+            for (int u = 0; u < SU; ++u) sbin_add_vec<F>(bins, bf[u], spec, one);
+            if (++since == WIN_TILES) {
+                sbin_flush<F>(bins, col);
+                since = 0;
+                if (++flushes == SSEG_REG_FLUSHES) { scol_regularize<F>(col); flushes = 0; }
+            }
         };
         for (uint64_t it = 0; it < nit; it += 2) {
             if (it + 1 < nit) {
@@ -164,7 +254,10 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
         }
 #pragma unroll
         for (int u = 0; u < SU; ++u)
-            if (nit * (32 * SU) + u * 32 + lane < nvec) sadd_vec<F>(col, lv[u], flags, one);
+            if (nit * (32 * SU) + u * 32 + lane < nvec) sbin_add_vec<F>(bins, lv[u], spec, one);
+        sbin_flush<F>(bins, col);
+        if (__any_sync(FULL, spec == F::EM))            // rare: NaN/Inf patterns in this segment
+            sseg_rescan<F>(bins, col, g.xs, g.head, body, nvec, g.tail, lane, flags, one);
         // prefetch the next segment, then close this one
         const uint64_t sn = s + nw;
         const bool more = sn < nseg;
@@ -176,15 +269,35 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
                 for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
             }
         }
+        // combine: lane r < COLS sums row r over the 32 lanes (hi/lo halves: raw |Y| < 2^63),
+        // splits balanced carries (the top row is not split), the carries move one row up, and
+        // the rows move to their digit positions
         __syncwarp();
-        int64_t a0, a1;
-        combine_raw_columns(wb, a0, a1, lane);
+        int64_t hs = 0, ls = 0;
+        if (lane < F::COLS) {
+#pragma unroll 8
+            for (int c = 0; c < 32; ++c) {
+                const int64_t v = wb[lane * 32 + ((lane + c) & 31)];
+                hs += v >> 32;
+                ls += (int64_t)(uint32_t)v;
+            }
+        }
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < D; ++j) col[j * 32] = 0;
+        for (int j = 0; j < F::COLS; ++j) col[j * 32] = 0;
+        int64_t cr = 0, rr = (int64_t)((uint64_t)hs << 32) + ls;
+        if (lane < F::COLS - 1) {
+            cr = (hs + ((ls + (1ll << 51)) >> 32)) >> 20;
+            rr = (int64_t)((uint64_t)(hs - (cr << 20)) << 32) + ls;
+        }
+        int64_t cin = __shfl_up_sync(FULL, cr, 1);
+        if (lane == 0) cin = 0;
+        const int64_t row = lane < F::COLS ? rr + cin : 0;
+        const int64_t d = __shfl_sync(FULL, row, (lane - F::COL0) & 31);
+        const int64_t a0 = (lane >= F::COL0 && lane < F::COL0 + F::COLS) ? d : 0;
         flags = __reduce_or_sync(FULL, flags);
         const xsum_result r =
-            finalize_warp_inl(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su[warp], lane);
+            finalize_warp_inl(a0, 0, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su[warp], lane);
         if (lane == 0) o.write(s, r);
         __syncwarp();
         if (!more) break;
@@ -196,12 +309,12 @@ template <class F>
 static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                 const SegOut& o, int num_sms, cudaStream_t s) {
     static unsigned long long smem_set = 0;
-    if (cudaError_t e = ensure_smem(k_segments_small<F>, SSEG_SMEM, smem_set)) return e;
+    if (cudaError_t e = ensure_smem(k_segments_small<F>, sseg_smem<F>(), smem_set)) return e;
     const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
     const uint64_t cap = (uint64_t)num_sms * 2;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-    k_segments_small<F><<<g, SSEG_WARPS * 32, SSEG_SMEM, s>>>(static_cast<const uint8_t*>(x), nseg, seg_len, offsets, o,
-                                                               1u);
+    k_segments_small<F><<<g, SSEG_WARPS * 32, sseg_smem<F>(), s>>>(static_cast<const uint8_t*>(x), nseg, seg_len,
+                                                                    offsets, o, 1u);
     note_launch();
     return cudaGetLastError();
 }

@@ -145,3 +145,19 @@ def test_host_buffer_streaming_formats(xs, fmt):
     r, limbs = ref_of(fmt, b)
     assert res.bits == r.bits and res.bits_f32 == r.bits_f32 and res.flags == r.flags
     assert (canon == limbs).all() and res.count == n
+
+
+@pytest.mark.parametrize("fmt", ["f32", "f16", "bf16"])
+def test_segments_full_of_specials(xs, fmt):
+    """A long segment made mostly of NaN / Inf patterns (more than a bin window per lane): the
+    rare path cancels every one exactly; a segment of +Inf and finite values gives +Inf, one of
+    only finite values next to it is unaffected."""
+    import torch
+    n = 70_000
+    b = bits_data(fmt, 3 * n, 31)
+    em = {"f32": 0x7F800000, "f16": 0x7C00, "bf16": 0x7F80}[fmt]
+    pinf = b.dtype.type(em)
+    b[: n - 5] = pinf                                   # segment 0: +Inf almost everywhere
+    b[n: n + n // 2] = b.dtype.type(em | 1)             # segment 1: half NaN
+    vals, canon, flags = xs.sum_segments(to_dev(b, fmt, 1), n, canon=True, flags=True)
+    check_segments(xs, fmt, b, [(0, n), (n, 2 * n), (2 * n, 3 * n)], vals, canon, flags, f"{fmt} specials")

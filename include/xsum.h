@@ -28,6 +28,13 @@
  *   - NaN / +-Inf inputs are not errors: they set sticky flags (R10).
  *   - No CPU fallback exists: every arithmetic step runs in CUDA kernels built
  *     for sm_100a.
+ *   - The accumulate launches (xsum_accumulate*, xsum_sum*, xsum_sum_allreduce) use
+ *     programmatic dependent launch: one may start reading its input while the previous
+ *     xsum accumulate launch in the stream is still finishing (it waits for that launch
+ *     before touching the handle's scratch or state). Data written by any other preceding
+ *     stream operation is complete, as with ordinary stream order; an input must therefore
+ *     not be written by the immediately preceding xsum accumulate launch (none of them write
+ *     their input). XSUM_NO_PDL=1 in the environment disables it.
  */
 #ifndef XSUM_H
 #define XSUM_H

@@ -559,3 +559,32 @@ def test_exact_sum_dim(xs, shape, dim):
         assert out.reshape(-1)[i].view(np.uint64) == np.uint64(r.bits), (shape, dim, i)
     kd = xs.exact_sum_dim(t, dim, keepdim=True)
     assert tuple(kd.shape) == tuple(np.sum(x, axis=dim, keepdims=True).shape)
+
+
+def test_every_exponent_and_digit_boundary(xs):
+    """Per-element decomposition at every binary64 exponent (SURVEY.md §4 layer 3): each
+    biased exponent 0..2046 with a random fraction and both signs, summed alone (segments of
+    length 1) and with its neighbour one exponent up (the chunks straddle every digit boundary
+    k mod 52 = 0 and 51), each vs the oracle."""
+    import torch
+    rng = np.random.default_rng(2046)
+    e = np.arange(2047, dtype=np.uint64)
+    frac = rng.integers(0, 1 << 52, size=e.size, dtype=np.uint64)
+    sign = rng.integers(0, 2, size=e.size, dtype=np.uint64)
+    bits = (sign << np.uint64(63)) | (e << np.uint64(52)) | frac
+    x = bits.view(np.float64)
+    d = torch.from_numpy(x.copy()).cuda()
+    vals, canon, flags = xs.sum_segments(d, 1, canon=True, flags=True)
+    v, cn = vals.cpu().numpy().view(np.uint64), canon.cpu().numpy().view(np.uint64)
+    for i in range(x.size):
+        r, limbs = oracle.exact_sum(x[i:i + 1])
+        assert v[i] == r.bits and (cn[i] == limbs).all(), f"exponent field {i}"
+    pairs = np.stack([x[:-1], -x[1:] * 0.75], axis=1).reshape(-1)
+    vals, canon, _ = xs.sum_segments(torch.from_numpy(pairs.copy()).cuda(), 2, canon=True)
+    v, cn = vals.cpu().numpy().view(np.uint64), canon.cpu().numpy().view(np.uint64)
+    for i in range(x.size - 1):
+        r, limbs = oracle.exact_sum(pairs[2 * i:2 * i + 2])
+        assert v[i] == r.bits and (cn[i] == limbs).all(), f"pair at exponent field {i}"
+    res, canon = xs.exact_sum(d)                          # and all of them at once (fused path)
+    r, limbs = oracle.exact_sum(x)
+    assert res.bits == r.bits and (canon == limbs).all()

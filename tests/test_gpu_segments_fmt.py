@@ -161,3 +161,23 @@ def test_segments_full_of_specials(xs, fmt):
     b[n: n + n // 2] = b.dtype.type(em | 1)             # segment 1: half NaN
     vals, canon, flags = xs.sum_segments(to_dev(b, fmt, 1), n, canon=True, flags=True)
     check_segments(xs, fmt, b, [(0, n), (n, 2 * n), (2 * n, 3 * n)], vals, canon, flags, f"{fmt} specials")
+
+
+@pytest.mark.parametrize("fmt", ["f32", "f16", "bf16"])
+def test_every_exponent_each_format(xs, fmt):
+    """Every finite exponent field of the format with a random fraction and both signs: alone
+    (segments of length 1: the bin / group / column-window placement of every exponent) and all
+    together through the fused kernel, vs the oracle."""
+    rng = np.random.default_rng(7)
+    t, l = {"f32": (23, 8), "f16": (10, 5), "bf16": (7, 8)}[fmt]
+    ut = np.uint32 if fmt == "f32" else np.uint16
+    e = np.repeat(np.arange((1 << l) - 1, dtype=np.uint64), 2)
+    fr = rng.integers(0, 1 << t, size=e.size, dtype=np.uint64)
+    sg = np.tile(np.array([0, 1], dtype=np.uint64), e.size // 2)
+    b = ((sg << np.uint64(t + l)) | (e << np.uint64(t)) | fr).astype(ut)
+    d = to_dev(b, fmt, 0)
+    vals, canon, flags = xs.sum_segments(d, 1, canon=True, flags=True)
+    check_segments(xs, fmt, b, [(i, i + 1) for i in range(b.size)], vals, canon, flags, f"{fmt} exponents")
+    res, cn = xs.exact_sum(d)
+    r, limbs = ref_of(fmt, b)
+    assert res.bits == r.bits and res.bits_f32 == r.bits_f32 and (cn == limbs).all()

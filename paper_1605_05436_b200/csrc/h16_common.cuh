@@ -1,0 +1,106 @@
+// Decoding of 16-bit summands into exponent-group bins (binary16 / bfloat16), shared by the
+// whole-array kernel K7 (accumulate_h16.cu) and the 16-bit segments kernel (segments_small.cu).
+// See accumulate_h16.cu for the method and its citations.
+#pragma once
+
+#include "xsum_device.cuh"
+
+namespace xs {
+
+template <int T_, int L_, int SB_, int FLUSH_, int BASE_>
+struct H16Fmt {
+    static constexpr int t = T_;                          // fraction bits
+    static constexpr int l = L_;                          // exponent bits
+    static constexpr int SB = SB_;                        // exponent group = 2^SB consecutive exponents
+    // q = max(e,1) + 1 in [2, 2^l - 1] for finite values, 2^l for NaN/Inf: group g = q >> SB,
+    // offset o = q mod 2^SB; finite groups 0..NGF-1, the special group NGF.
+    static constexpr int NGF = ((1 << l) - 1) / (1 << SB) + 1;
+    static constexpr int NBIN = 2 * (NGF + 1);           // bin = 2 g + sign
+    static constexpr int NBIN64 = 2 * NGF;                // finite bins only
+    static constexpr int FLUSH = FLUSH_;                  // adds per window: FLUSH * max(M 2^o) < 2^32
+    static constexpr int BASE = BASE_;                    // window bit position of k = 0 (units 2^-1074)
+    // bin g holds sum M 2^o with M 2^k = (M 2^o) 2^(g 2^SB - 2): position BASE - 2 + g 2^SB
+    static constexpr int pos(int g) { return BASE - 2 + g * (1 << SB); }
+};
+// binary16: M <= 2047, o <= 7: 16383 * 2047 * 2^7 < 2^32.  bfloat16: M <= 255, o <= 15:
+// 511 * 255 * 2^15 < 2^32. Window bit positions: binary16 k + 1050, bfloat16 k + 941.
+using FmtF16 = H16Fmt<10, 5, 3, 16383, 1050>;
+using FmtBF16 = H16Fmt<7, 8, 4, 511, 941>;
+// a window of FLUSH adds of the largest M 2^o cannot wrap an unsigned 32-bit bin
+template <class F>
+constexpr bool flush_fits() {
+    return (unsigned long long)F::FLUSH * ((2ull << F::t) - 1) * (1ull << ((1 << F::SB) - 1)) < (1ull << 32);
+}
+static_assert(flush_fits<FmtF16>() && flush_fits<FmtBF16>(), "bin window too long");
+
+// One summand (checked paths): h = |x| bit pattern (15 bits), s = sign bit; bins = this lane's
+// bin column (bin b at word b*32).
+template <class F>
+__device__ __forceinline__ void h16_add(uint32_t* bins, uint32_t h, uint32_t s) {
+    const uint32_t q = max((h >> F::t) + 1u, 2u);                          // max(e,1) + 1
+    const uint32_t M = (h + (2u << F::t)) - q * (1u << F::t);              // m + [e!=0] 2^t
+    const uint32_t o = q & ((1u << F::SB) - 1u);
+    const uint32_t b = ((q >> F::SB) << 1) | s;
+    XS_ASSERT(b < (uint32_t)F::NBIN);
+    bins[b * 32u] += M << o;
+}
+
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r; asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+}
+
+__device__ __forceinline__ void bin_add(uint32_t saddr, uint32_t v) {
+#ifdef XS_H16_LDSTS
+    uint32_t o;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(o) : "r"(saddr) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr), "r"(o + v) : "memory");
+#else
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");   // fire and forget
+#endif
+}
+
+__device__ __forceinline__ uint32_t madhi_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r; asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r;
+}
+
+// The two summands of a 32-bit word (little-endian: element 2i in the low half), decoded with
+// the exponent work done once for both halves in 16-bit lanes (VIMNMX.U16x2, and IMADs / LOP3s
+// whose per-half results cannot carry into the other half): per half q = max(e,1)+1 < 2^16,
+// M = h + 2^(t+1) - q 2^t in [0, 2^(t+1)), bin byte offset (2 g + s) 128 < 2^16. The work is
+// split between the ALU pipe (shifts, masks, min/max) and the FMA pipe (IMAD / IMAD.HI with
+// the opaque `one` / `mone`), which ncu showed as the binding resource (ALU 93% busy in a plain
+// version). `sbase` is the shared address of this lane's bin 0 (bin b at sbase + 128 b),
+// `sbase2` = sbase * (2^16 + 1) mod 2^32.
+template <class F>
+__device__ __forceinline__ void h16_add_word(uint32_t sbase, uint32_t sbase2, uint32_t w, uint32_t one,
+                                             uint32_t mone) {
+    constexpr uint32_t t = F::t, SB = F::SB;
+    constexpr uint32_t EM2 = ((1u << F::l) - 1u) * 0x00010001u;
+    const uint32_t e2 = (w >> t) & EM2;                                       // exponent fields
+    const uint32_t ep2 = vmax_u16x2(e2, 0x00010001u);                         // max(e,1)
+    const uint32_t q2 = mad_u32(ep2, one, 0x00010001u);                       // + 1
+    const uint32_t h2 = w & 0x7FFF7FFFu;                                      // |x| patterns
+    const uint32_t M2 = mad_u32(ep2, 0u - (1u << t), mad_u32(h2, one, (1u << t) * 0x00010001u));  // M
+    const uint32_t o2 = q2 & (((1u << SB) - 1u) * 0x00010001u);               // q mod 2^SB
+    const uint32_t g2 = mad_u32(o2, mone, q2);                                // 2^SB g
+    const uint32_t s2 = madhi_u32(mad_u32(h2, mone, w), 1u << 24, 0u);        // 128 s  (sign bits >> 8)
+    const uint32_t a2 = mad_u32(g2, 1u << (8 - SB), s2);                      // (2 g + s) 128
+    XS_ASSERT((a2 & 0xFFFFu) < (uint32_t)F::NBIN * 128u && (a2 >> 16) < (uint32_t)F::NBIN * 128u);
+    const uint32_t Mh = M2 >> 16, oh = o2 >> 16;
+    const uint32_t Ml = mad_u32(Mh, 0xFFFF0000u, M2);
+    uint32_t vl;                      // Ml << o_lo: the wrap-mode funnel shift uses o2 mod 32 = o_lo
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(vl) : "r"(0u), "r"(Ml), "r"(o2));
+    const uint32_t addr_hi = sbase + (a2 >> 16);
+    const uint32_t addr_lo = mad_u32(addr_hi, 0xFFFF0000u, mad_u32(a2, one, sbase2));   // sbase + (a2 & 0xFFFF)
+    bin_add(addr_lo, vl);
+    bin_add(addr_hi, Mh << oh);
+}
+
+template <class F>
+__device__ __forceinline__ uint32_t h16_special_flags(uint32_t b16) {
+    if (((b16 >> F::t) & ((1u << F::l) - 1u)) != (1u << F::l) - 1u) return 0;
+    if (b16 & ((1u << F::t) - 1u)) return XSUM_F_NAN;
+    return (b16 >> 15) ? XSUM_F_NINF : XSUM_F_PINF;
+}
+
+}  // namespace xs

@@ -15,6 +15,7 @@
 // and binary32).
 #include <cuda_runtime.h>
 
+#include "h16_common.cuh"
 #include "xsum_device.cuh"
 #include "xsum_kernels.h"
 
@@ -305,6 +306,238 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// 16-bit formats: the decode and bins of K7 (h16_common.cuh: both halves of a word decoded in
+// 16-bit lanes, unsigned 32-bit bins per (sign, group of 2^SB exponents) fed by fire-and-forget
+// red.shared, NaN/Inf in a group of their own that is never summed) with a per-segment flush
+// into a narrow digit column. About 11 instructions per element instead of ~17.
+// ---------------------------------------------------------------------------------------
+template <class F>
+struct H16Seg {
+    static constexpr int COL0 = F::pos(0) / 52;
+    static constexpr int COLS = F::pos(F::NGF - 1) / 52 + 2 - COL0 + 4;   // a bin spans <= 2 digits
+    static constexpr int REG_FLUSHES = 64;   // <= 18 chunks per digit per flush: 64 * 18 * 2^52 < 2^62
+};
+
+// Empty the finite u32 bins into the narrow column (row r = digit COL0 + r); returns true if this
+// lane's NaN/Inf group was non-empty (and clears it).
+template <class F>
+__device__ __forceinline__ bool h16seg_flush(uint32_t* bins, int64_t* col) {
+    using S = H16Seg<F>;
+#pragma unroll
+    for (int j = 0; j < F::NBIN64; ++j) {
+        const int P = F::pos(j >> 1), i = P / W - S::COL0, o = P % W;
+        const uint64_t V = bins[j * 32];
+        bins[j * 32] = 0;
+        const int64_t c0 = (int64_t)((V << o) & MASK);
+        const int64_t c1 = (int64_t)(V >> (W - o));                 // V 2^o < 2^84: two digits
+        XS_ASSERT(i >= 0 && i + 1 < S::COLS - 1);
+        if (j & 1) {
+            col[i * 32] -= c0;
+            col[(i + 1) * 32] -= c1;
+        } else {
+            col[i * 32] += c0;
+            col[(i + 1) * 32] += c1;
+        }
+    }
+    const uint32_t sp = bins[F::NBIN64 * 32] | bins[(F::NBIN64 + 1) * 32];
+    bins[F::NBIN64 * 32] = 0;
+    bins[(F::NBIN64 + 1) * 32] = 0;
+    return sp != 0;
+}
+
+template <class F>
+__device__ __forceinline__ void h16seg_regularize(int64_t* col) {
+    constexpr int COLS = H16Seg<F>::COLS;
+    int64_t cin = 0;
+#pragma unroll
+    for (int j = 0; j < COLS - 1; ++j) {
+        const int64_t y = col[j * 32];
+        const int64_t c = balanced_carry(y);
+        col[j * 32] = y - (c << W) + cin;
+        cin = c;
+    }
+    col[(COLS - 1) * 32] += cin;
+}
+
+// Rare path: classify the NaN/Inf patterns of a segment (they were binned into the special
+// group, which is never summed).
+template <class F>
+__device__ __noinline__ uint32_t h16seg_classify(const uint16_t* xs, uint64_t len, int lane) {
+    uint32_t f = 0;
+    for (uint64_t i = lane; i < len; i += 32) f |= h16_special_flags<F>(__ldg(xs + i));
+    return f;
+}
+
+template <class F>
+__device__ __forceinline__ void h16seg_add_checked(uint32_t* bins, uint32_t b16, uint32_t& flags) {
+    const uint32_t f = h16_special_flags<F>(b16);
+    if (f) { flags |= f; return; }
+    h16_add<F>(bins, b16 & 0x7FFFu, b16 >> 15);
+}
+
+template <class F>
+constexpr size_t h16seg_smem() {
+    return (size_t)SSEG_WARPS * 32 * (H16Seg<F>::COLS * 8 + F::NBIN * 4);
+}
+
+template <class F>
+__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
+               SegOut o, uint32_t one, uint32_t mone) {
+    using S = H16Seg<F>;
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t su[SSEG_WARPS][64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (S::COLS * 32) + lane;
+    const int64_t* wb = win + warp * (S::COLS * 32);
+    uint32_t* bins = reinterpret_cast<uint32_t*>(win + SSEG_WARPS * S::COLS * 32) + warp * (F::NBIN * 32) + lane;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bins);
+    const uint32_t sbase2 = sbase * 0x00010001u;
+    const uint64_t nw = (uint64_t)gridDim.x * SSEG_WARPS;
+    constexpr int PV = 8;
+    constexpr int SU = SSEG_U;
+    constexpr uint32_t WIN_TILES = (F::FLUSH - 2 - SU * PV) / (SU * PV);   // + leftovers + head/tail
+    static_assert(WIN_TILES >= 1, "window shorter than one tile");
+    struct Seg {
+        const uint16_t* xs;
+        uint64_t len, head, nvec, tail, nit;
+        const uint4* body;
+    };
+    auto open_seg = [&](uint64_t sj) {
+        Seg g;
+        const uint64_t beg = offsets ? offsets[sj] : sj * seg_len;
+        g.len = offsets ? offsets[sj + 1] - beg : seg_len;
+        g.xs = x + beg;
+        g.head = ((16 - ((uintptr_t)g.xs & 15)) & 15) / 2;
+        if (g.head > g.len) g.head = g.len;
+        g.nvec = (g.len - g.head) / PV;
+        g.tail = g.len - g.head - g.nvec * PV;
+        g.body = reinterpret_cast<const uint4*>(g.xs + g.head);
+        g.nit = g.nvec / (32 * SU);
+        return g;
+    };
+    uint64_t s = (uint64_t)blockIdx.x * SSEG_WARPS + warp;
+    if (s >= nseg) return;                                  // warp-uniform
+#pragma unroll
+    for (int j = 0; j < S::COLS; ++j) col[j * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < F::NBIN; ++j) bins[j * 32] = 0;
+    Seg g = open_seg(s);
+    uint4 cur[SU], alt[SU];
+    if (g.nit) {
+#pragma unroll
+        for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
+    }
+    while (true) {
+        uint32_t flags = 0, since = 0, flushes = 0;
+        bool special = false;
+        const uint64_t nit = g.nit, nvec = g.nvec;
+        const uint4* body = g.body;
+        if ((uint64_t)lane < g.head) h16seg_add_checked<F>(bins, __ldg(g.xs + lane), flags);
+        if (lane >= 8 && (uint64_t)(lane - 8) < g.tail)
+            h16seg_add_checked<F>(bins, __ldg(g.xs + g.head + nvec * PV + (lane - 8)), flags);
+        auto process = [&](const uint4 (&bf)[SU]) {
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                h16_add_word<F>(sbase, sbase2, bf[u].x, one, mone);
+                h16_add_word<F>(sbase, sbase2, bf[u].y, one, mone);
+                h16_add_word<F>(sbase, sbase2, bf[u].z, one, mone);
+                h16_add_word<F>(sbase, sbase2, bf[u].w, one, mone);
+            }
+            if (++since == WIN_TILES) {
+                special |= h16seg_flush<F>(bins, col);
+                since = 0;
+                if (++flushes == S::REG_FLUSHES) { h16seg_regularize<F>(col); flushes = 0; }
+            }
+        };
+        for (uint64_t it = 0; it < nit; it += 2) {
+            if (it + 1 < nit) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) alt[u] = ldg_stream(body + (it + 1) * (32 * SU) + u * 32 + lane);
+            }
+            process(cur);
+            if (it + 1 >= nit) break;
+            if (it + 2 < nit) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(body + (it + 2) * (32 * SU) + u * 32 + lane);
+            }
+            process(alt);
+        }
+        uint4 lv[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+            const uint64_t v = nit * (32 * SU) + u * 32 + lane;
+            if (v < nvec) lv[u] = ldg_stream(body + v);
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+            if (nit * (32 * SU) + u * 32 + lane < nvec) {
+                h16_add_word<F>(sbase, sbase2, lv[u].x, one, mone);
+                h16_add_word<F>(sbase, sbase2, lv[u].y, one, mone);
+                h16_add_word<F>(sbase, sbase2, lv[u].z, one, mone);
+                h16_add_word<F>(sbase, sbase2, lv[u].w, one, mone);
+            }
+        }
+        special |= h16seg_flush<F>(bins, col);
+        if (__any_sync(FULL, special)) flags |= h16seg_classify<F>(g.xs, g.len, lane);   // rare
+        const uint64_t sn = s + nw;
+        const bool more = sn < nseg;
+        const uint64_t len = g.len;
+        if (more) {
+            g = open_seg(sn);
+            if (g.nit) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
+            }
+        }
+        __syncwarp();
+        int64_t hs = 0, ls = 0;
+        if (lane < S::COLS) {
+#pragma unroll 8
+            for (int c = 0; c < 32; ++c) {
+                const int64_t v = wb[lane * 32 + ((lane + c) & 31)];
+                hs += v >> 32;
+                ls += (int64_t)(uint32_t)v;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < S::COLS; ++j) col[j * 32] = 0;
+        int64_t cr = 0, rr = (int64_t)((uint64_t)hs << 32) + ls;
+        if (lane < S::COLS - 1) {
+            cr = (hs + ((ls + (1ll << 51)) >> 32)) >> 20;
+            rr = (int64_t)((uint64_t)(hs - (cr << 20)) << 32) + ls;
+        }
+        int64_t cin = __shfl_up_sync(FULL, cr, 1);
+        if (lane == 0) cin = 0;
+        const int64_t row = lane < S::COLS ? rr + cin : 0;
+        const int64_t d = __shfl_sync(FULL, row, (lane - S::COL0) & 31);
+        const int64_t a0 = (lane >= S::COL0 && lane < S::COL0 + S::COLS) ? d : 0;
+        flags = __reduce_or_sync(FULL, flags);
+        const xsum_result r =
+            finalize_warp_inl(a0, 0, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su[warp], lane);
+        if (lane == 0) o.write(s, r);
+        __syncwarp();
+        if (!more) break;
+        s = sn;
+    }
+}
+
+template <class F>
+static cudaError_t launch_h16seg(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
+                                 const SegOut& o, int num_sms, cudaStream_t s) {
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_segments_h16<F>, h16seg_smem<F>(), smem_set)) return e;
+    const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
+    const uint64_t cap = (uint64_t)num_sms * 2;
+    const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    k_segments_h16<F><<<g, SSEG_WARPS * 32, h16seg_smem<F>(), s>>>(static_cast<const uint16_t*>(x), nseg, seg_len,
+                                                                    offsets, o, 1u, 0xFFFFFFFFu);
+    note_launch();
+    return cudaGetLastError();
+}
+
 template <class F>
 static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                 const SegOut& o, int num_sms, cudaStream_t s) {
@@ -323,8 +556,8 @@ cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t
                                const SegOut& o, int num_sms, cudaStream_t s) {
     switch (dtype) {
         case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s);
-        case XSUM_DT_F16: return launch_small<SF16>(x, nseg, seg_len, offsets, o, num_sms, s);
-        case XSUM_DT_BF16: return launch_small<SBF16>(x, nseg, seg_len, offsets, o, num_sms, s);
+        case XSUM_DT_F16: return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s);
+        case XSUM_DT_BF16: return launch_h16seg<FmtBF16>(x, nseg, seg_len, offsets, o, num_sms, s);
         default: return cudaErrorInvalidValue;
     }
 }

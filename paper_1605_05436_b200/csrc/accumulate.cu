@@ -53,7 +53,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     __shared__ int is_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) xs_stamp(p.partial, 0, blockIdx.x);                 // block start
+    if (tid == 0) xs_stamp(p.stamps, 0, blockIdx.x);                 // block start
     pdl_release_dependents();    // the next launch may take SMs as this grid's blocks finish
     int64_t* col = win + warp * (D * 32) + lane;
 #pragma unroll
@@ -133,7 +133,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
         if ((uint64_t)tid < head) EL::add_one_checked(col, x + tid, flags, one);
         if (tid >= PV && (uint64_t)(tid - PV) < tail) EL::add_one_checked(col, x + head + nvec * PV + (tid - PV), flags, one);
     }
-    if (tid == 0) xs_stamp(p.partial, 1, blockIdx.x);                 // stream done
+    if (tid == 0) xs_stamp(p.stamps, 1, blockIdx.x);                 // stream done
     if (__any_sync(FULL, EL::hit(nspec))) {
         if (EL::hit(nspec) && any_tile) {
             regularize_column(col);
@@ -153,7 +153,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
         if (lane == 0 && f) atomicOr(&blk_flags, f);
     }
     __syncthreads();
-    if (tid == 0) xs_stamp(p.partial, 2, blockIdx.x);                 // warp combines done
+    if (tid == 0) xs_stamp(p.stamps, 2, blockIdx.x);                 // warp combines done
 
     // block: sum the warp partials (|.| <= WARPS*(2^51+2^16) < 2^56), regularize, publish;
     // the last block merges the grid (grid_tail.cuh).
@@ -180,7 +180,7 @@ static cudaError_t launch_accumulate(const E* x, uint64_t n, const AccParams& p,
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    cudaError_t e = launch_pdl(k_accumulate<WARPS, U, NB, E>, (unsigned)g, C::T, C::SMEM, s, x, n, p);
+    cudaError_t e = launch_pdl(n * sizeof(E) < PDL_MAX_BYTES, k_accumulate<WARPS, U, NB, E>, (unsigned)g, C::T, C::SMEM, s, x, n, p);
     note_launch();
     return e;
 }

@@ -292,7 +292,7 @@ cudaError_t accumulate_f32(const float* x, uint64_t n, const AccParams& p, int n
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    cudaError_t e = launch_pdl(k_accumulate_f32b, (unsigned)g, F32B_WARPS * 32, SMEM, s, x, n, p);
+    cudaError_t e = launch_pdl(n * 4 < PDL_MAX_BYTES, k_accumulate_f32b, (unsigned)g, F32B_WARPS * 32, SMEM, s, x, n, p);
     note_launch();
     return e;
 }

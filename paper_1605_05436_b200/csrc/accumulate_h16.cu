@@ -229,7 +229,7 @@ static cudaError_t launch_h16(const uint16_t* x, uint64_t n, const AccParams& p,
     uint64_t g = ntiles < (uint64_t)num_sms ? ntiles : (uint64_t)num_sms;
     if (g < 1) g = 1;
     if (g > XS_MAXB) g = XS_MAXB;
-    cudaError_t e = launch_pdl(k_accumulate_h16<F>, (unsigned)g, H16_WARPS * 32, SMEM, s, x, n, p);
+    cudaError_t e = launch_pdl(n * 2 < PDL_MAX_BYTES, k_accumulate_h16<F>, (unsigned)g, H16_WARPS * 32, SMEM, s, x, n, p);
     note_launch();
     return e;
 }

@@ -55,8 +55,9 @@ xs::AccParams acc_params(xsum_ctx* h, int overwrite, xsum_result* res, uint64_t*
     xs::AccParams p;
     p.state = h->state;
     p.counter = reinterpret_cast<uint32_t*>(h->scratch + xs::SCRATCH_COUNTER_OFF);
-    p.partial = reinterpret_cast<int64_t*>(h->scratch + xs::SCRATCH_PARTIAL_OFF);
-    p.pflags = reinterpret_cast<uint32_t*>(h->scratch + xs::SCRATCH_FLAGS_OFF);
+    p.gflags = reinterpret_cast<uint32_t*>(h->scratch + xs::SCRATCH_GFLAGS_OFF);
+    p.gacc = reinterpret_cast<int64_t*>(h->scratch + xs::SCRATCH_ACC_OFF);
+    p.stamps = XS_TIMING ? reinterpret_cast<int64_t*>(h->scratch + xs::SCRATCH_STAMP_OFF) : nullptr;
     p.overwrite = overwrite;
     p.res = res;
     p.canon = canon;

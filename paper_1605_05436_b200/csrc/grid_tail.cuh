@@ -1,7 +1,9 @@
 // Grid level of the merge tree (§3 step 5 bottom-up; MapReduce
-// post-process PAPER.md:1158-1163): every block publishes its regularized superaccumulator
-// to the scratch table, and the last block to arrive merges the table and the handle state
-// and, for a fused one-shot sum, rounds. Shared by the accumulate kernels.
+// post-process PAPER.md:1158-1163): every block adds its regularized superaccumulator into a
+// grid accumulator in L2 (digit-wise 64-bit atomics: the digits of up to XS_MAXB regularized
+// states sum without overflow, and regularizing once at the end gives the same value), and the
+// last block to arrive merges it with the handle state and, for a fused one-shot sum, rounds
+// (PAPER.md:777-795). Shared by the accumulate kernels.
 #pragma once
 
 #include "xsum_device.cuh"
@@ -95,63 +97,44 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
     const uint64_t G = gridDim.x;
     pdl_wait_predecessor();      // the previous launch may still be merging in the scratch / state
     if (warp == 0) {
-        p.partial[(size_t)lane * XS_MAXB + blockIdx.x] = a0;
-        if (lane + 32 < D) p.partial[(size_t)(lane + 32) * XS_MAXB + blockIdx.x] = a1;
-        if (lane == 0) p.pflags[blockIdx.x] = bflags;
+        // every block adds its regularized partial into the grid accumulator (L2 atomics,
+        // fire-and-forget; |sum| <= XS_MAXB (2^51 + 2^16) < 2^62) and ORs its flags
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p.gacc + lane), "l"(a0) : "memory");
+        if (lane + 32 < D)
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p.gacc + lane + 32), "l"(a1) : "memory");
+        if (lane == 0 && bflags) atomicOr(p.gflags, bflags);
         __syncwarp();
         if (lane == 0) {
-            // release: this block's partial (ordered before by the warp barrier) is visible to
-            // the block that sees the final count; acquire: the last block sees all of them
+            // release: this block's adds (ordered before by the warp barrier) are visible to the
+            // block that sees the final count; acquire: the last block sees all of them
             uint32_t old;
             asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counter) : "memory");
             *sh_last = (old == (uint32_t)(G - 1));
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) xs_stamp(p.partial, 3, blockIdx.x);        // arrival atomic returned
+    if (threadIdx.x == 0) xs_stamp(p.stamps, 3, blockIdx.x);         // arrival atomic returned
     if (!*sh_last) return;
     __threadfence();
-
-    // The last block merges the G block partials (digit-major, coalesced) and the handle
-    // state; G <= XS_MAXB so the raw sum stays below 2^62 before regularizing. Warp w sums
-    // digits w, w+WARPS, ...; a lane issues all its loads of one round (4 partials of each of
-    // its digits) before using any: one L2 round trip per 128 blocks instead of one per 32.
-    constexpr int JPW = (D + WARPS - 1) / WARPS;
+    if (warp == 0) {                     // the grid's sum, then the accumulator cleared for the next launch
+        red[lane] = __ldcg(p.gacc + lane);
+        p.gacc[lane] = 0;
+        if (lane + 32 < D) {
+            red[lane + 32] = __ldcg(p.gacc + lane + 32);
+            p.gacc[lane + 32] = 0;
+        }
+        if (lane == 0) {
+            *sh_flags = __ldcg(p.gflags);
+            *p.gflags = 0;
+        }
+    }
     int64_t st0 = 0, st1 = 0;
     if (warp == 0 && !p.overwrite) {                     // state digits, fetched alongside
         st0 = __ldcg(&p.state->digit[lane]);
         st1 = (lane + 32 < D) ? __ldcg(&p.state->digit[lane + 32]) : 0;
     }
-    int64_t acc[JPW];
-#pragma unroll
-    for (int jj = 0; jj < JPW; ++jj) acc[jj] = 0;
-    for (uint64_t b0 = lane; b0 < G; b0 += 128) {
-        int64_t v[JPW][4];
-#pragma unroll
-        for (int jj = 0; jj < JPW; ++jj)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = warp + jj * WARPS;
-                const uint64_t b = b0 + 32 * u;
-                v[jj][u] = (j < D && b < G) ? __ldcg(&p.partial[(size_t)j * XS_MAXB + b]) : 0;
-            }
-#pragma unroll
-        for (int jj = 0; jj < JPW; ++jj) acc[jj] += (v[jj][0] + v[jj][1]) + (v[jj][2] + v[jj][3]);
-    }
-#pragma unroll
-    for (int jj = 0; jj < JPW; ++jj) {
-        const int j = warp + jj * WARPS;
-        const int64_t s = warp_sum64(acc[jj]);
-        if (j < D && lane == 0) red[j] = s;
-    }
-    if (warp == 1 % WARPS) {
-        uint32_t f = 0;
-        for (uint64_t b = lane; b < G; b += 32) f |= __ldcg(&p.pflags[b]);
-        f = __reduce_or_sync(FULL, f);
-        if (lane == 0) *sh_flags = f;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) xs_stamp(p.partial, 4, 0);                  // last block: partials merged
+    __syncwarp();
+    if (threadIdx.x == 0) xs_stamp(p.stamps, 4, 0);                   // last block: grid sum read
     if (warp == 0) {
         int64_t b0 = red[lane] + st0, b1 = (lane + 32 < D) ? red[lane + 32] + st1 : 0;
         uint32_t fl = *sh_flags;
@@ -173,7 +156,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
             xsum_result r = finalize_warp(b0, b1, fl, cnt, p.canon, su, lane);
             if (lane == 0) *p.res = r;
         }
-        if (lane == 0) xs_stamp(p.partial, 5, 0);                     // last block: done
+        if (lane == 0) xs_stamp(p.stamps, 5, 0);                      // last block: done
     }
 }
 

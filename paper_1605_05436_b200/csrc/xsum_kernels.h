@@ -6,7 +6,7 @@
 
 #include "xsum.h"
 
-#define XS_MAXB 1024   // max blocks of one accumulate launch (= columns of the partial table)
+#define XS_MAXB 1024   // max blocks of one accumulate launch (1024 x regularized partials < 2^62)
 
 namespace xs {
 
@@ -24,9 +24,10 @@ constexpr size_t peer_buffer_bytes(uint32_t world) { return peer_counter_off(wor
 
 struct AccParams {
     xsum_state_image* state;   // handle state (device)
-    int64_t* partial;          // [D][XS_MAXB] block partials, digit-major (scratch)
-    uint32_t* pflags;          // [XS_MAXB] block flags (scratch)
+    int64_t* gacc;             // [D] grid accumulator: every block red.adds its partial (scratch, 0 between launches)
+    uint32_t* gflags;          // grid flags (red.or; scratch, 0 between launches)
     uint32_t* counter;         // arrival counter (scratch, 0 between launches)
+    int64_t* stamps;           // XS_TIMING builds: [6][XS_MAXB] %globaltimer stamps (scratch), else null
     int overwrite;             // 1: state := sum (fused reset), 0: state += sum
     xsum_result* res;          // non-null: fused finalize
     uint64_t* canon;           // optional canonical image for the fused finalize
@@ -35,11 +36,17 @@ struct AccParams {
     PeerParams peer;           // fused cross-GPU exchange after the grid merge (bufs null: none)
 };
 
-// scratch layout: [0,256) counter; [256, 256 + 8*D*MAXB) partials; then MAXB u32 flags
+// XS_TIMING=1: diagnostic builds (tools/timing_probe.py) stamp %globaltimer per block; 0 in the product
+#ifndef XS_TIMING
+#define XS_TIMING 0
+#endif
+// scratch layout: [0,4) arrival counter, [4,8) grid flags; [256, 256 + 8 D) grid accumulator;
+// timing builds only: [1024, 1024 + 8 * 6 * MAXB) stamps
 constexpr size_t SCRATCH_COUNTER_OFF = 0;
-constexpr size_t SCRATCH_PARTIAL_OFF = 256;
-constexpr size_t SCRATCH_FLAGS_OFF = SCRATCH_PARTIAL_OFF + sizeof(int64_t) * XSUM_NDIGITS * XS_MAXB;
-constexpr size_t SCRATCH_BYTES = SCRATCH_FLAGS_OFF + sizeof(uint32_t) * XS_MAXB;
+constexpr size_t SCRATCH_GFLAGS_OFF = 4;
+constexpr size_t SCRATCH_ACC_OFF = 256;
+constexpr size_t SCRATCH_STAMP_OFF = 1024;
+constexpr size_t SCRATCH_BYTES = SCRATCH_STAMP_OFF + (XS_TIMING ? sizeof(int64_t) * 6 * XS_MAXB : 0);
 
 void note_launch();
 
@@ -49,12 +56,15 @@ void note_launch();
 // (griddepcontrol.wait in grid_tail) before it touches the scratch table or the state, and it
 // only reads its input before that point. A predecessor that is not an xsum accumulate kernel
 // releases its dependents at completion, so inputs produced by earlier kernels are complete.
-// XSUM_NO_PDL=1 in the environment launches normally (A/B measurements).
+// XSUM_NO_PDL=1 in the environment launches normally (A/B measurements). Only launches of less
+// than PDL_MAX_BYTES of input use it: back to back, 2^24-2^26 doubles gain 6-12%, while at 2^28
+// the early blocks' reads slow the previous grid's stragglers (-1..2%, profiles/r01_pdl_ab.txt).
 bool pdl_enabled();
+constexpr uint64_t PDL_MAX_BYTES = 1ull << 30;
 
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
-                              Args... args) {
+inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
@@ -64,26 +74,21 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 __device__ __forceinline__ void pdl_release_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void pdl_wait_predecessor() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// XS_TIMING=1 (diagnostic builds, tools/timing_probe.py): per-block %globaltimer stamps written
-// into the unused columns (>= 512) of the scratch partial table: stamp k of block b at
-// partial[(D-1-k) * XS_MAXB + 512 + b]. 0 in the product.
-#ifndef XS_TIMING
-#define XS_TIMING 0
-#endif
-__device__ __forceinline__ void xs_stamp(int64_t* partial, int k, unsigned b) {
+// XS_TIMING builds: stamp k of block b at stamps[k * XS_MAXB + b] (scratch).
+__device__ __forceinline__ void xs_stamp(int64_t* stamps, int k, unsigned b) {
 #if XS_TIMING
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    partial[(size_t)(XSUM_NDIGITS - 1 - k) * XS_MAXB + 512 + b] = (int64_t)t;
+    stamps[(size_t)k * XS_MAXB + b] = (int64_t)t;
 #else
-    (void)partial; (void)k; (void)b;
+    (void)stamps; (void)k; (void)b;
 #endif
 }
 

@@ -1,6 +1,7 @@
 """Where the fixed cost of a fused sum goes: an XS_TIMING=1 build of libxsum stamps %globaltimer
 per block (start, stream done, warp combines done, arrival atomic returned) and in the last block
-(partials merged, rounded), into unused scratch columns; this prints the spread (development tool).
+(grid sum read, rounded) into a scratch area of timing builds; this prints the spread (development
+tool).
 
     python tools/timing_probe.py build     # here
     python tools/timing_probe.py run       # GPU box
@@ -38,8 +39,8 @@ for k in (10, 20, 28):
     acc.scratch.zero_()
     acc.sum(x)
     torch.cuda.synchronize()
-    part = acc.scratch[256:256 + 8 * D * MAXB].view(torch.int64).cpu().numpy().reshape(D, MAXB)
-    st = {j: part[D - 1 - j, 512:] for j in range(6)}
+    stamps = acc.scratch[1024:1024 + 8 * 6 * MAXB].view(torch.int64).cpu().numpy().reshape(6, MAXB)
+    st = {j: stamps[j] for j in range(6)}
     nb = int((st[0] != 0).sum())
     t0 = st[0][:nb].min()
     rel = {j: (st[j][:nb] - t0) / 1e3 for j in range(4)}

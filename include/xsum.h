@@ -144,7 +144,7 @@ typedef struct xsum_ctx xsum_ctx;
 
 /* Sizes of the caller-provided device buffers. */
 XSUM_API size_t xsum_state_bytes(void);                 /* = XSUM_STATE_BYTES */
-XSUM_API size_t xsum_scratch_bytes(int device);         /* scratch a handle needs on `device` (block partials) */
+XSUM_API size_t xsum_scratch_bytes(int device);         /* scratch a handle needs on `device` (1 KiB: grid accumulator) */
 XSUM_API size_t xsum_result_bytes(void);                /* = sizeof(xsum_result) = 48 */
 
 /* Create a handle bound to `device` whose exact state lives in d_state (XSUM_STATE_BYTES,

@@ -8,9 +8,10 @@
 // exponents are multiples of a fixed width): each lane keeps unsigned 32-bit "bins", one per
 // (sign, exponent group) with groups of 2^SB consecutive exponents, and adds M 2^(k mod 2^SB)
 // into the bin of its group - one 32-bit add per summand, no carries, no sign handling. Every
-// FLUSH adds (before a bin can wrap) the bins are emptied into per-lane int64 bins; at the
-// end the block's bins are converted into the 52-bit digit window and merged up the same
-// grid tree as binary64 sums (grid_tail.cuh). NaN/Inf patterns fall into a
+// FLUSH adds (before a bin can wrap) the bins are emptied into a narrow per-lane column of the
+// 52-bit digits the format reaches (h16_common.cuh); at the end the columns are combined into
+// digits and merged up the same grid tree as binary64 sums (grid_tail.cuh).
+// NaN/Inf patterns fall into a
 // bin group of their own (exponent field all ones) that is never summed: a lane that sees it
 // non-empty at a window close rescans its window to classify NaN / +Inf / -Inf (reading R10).
 #include <cuda_runtime.h>
@@ -43,22 +44,6 @@ __device__ __noinline__ void h16_rescan(const uint4* body, uint64_t t0, uint64_t
     }
 }
 
-// Empty the 32-bit bins into the int64 bins (finite groups) and clear the special group;
-// returns true if this lane's special group was non-empty.
-template <class F>
-__device__ __forceinline__ bool h16_flush(uint32_t* bins, int64_t* bins64) {
-#pragma unroll
-    for (int b = 0; b < F::NBIN64; ++b) {
-        XS_ASSERT(bins64[b * 32] >= 0 && bins64[b * 32] < (1ll << 62));      // < 2^40 summands per launch
-        bins64[b * 32] += (int64_t)bins[b * 32];
-        bins[b * 32] = 0;
-    }
-    const uint32_t sp = bins[F::NBIN64 * 32] | bins[(F::NBIN64 + 1) * 32];
-    bins[F::NBIN64 * 32] = 0;
-    bins[(F::NBIN64 + 1) * 32] = 0;
-    return sp != 0;
-}
-
 // Checked single summand (head / tail / leftovers): specials are flagged, not binned.
 template <class F>
 __device__ __forceinline__ void h16_add_checked(uint32_t* bins, uint32_t b16, uint32_t& flags) {
@@ -70,16 +55,17 @@ __device__ __forceinline__ void h16_add_checked(uint32_t* bins, uint32_t b16, ui
 template <class F>
 __global__ void __launch_bounds__(H16_WARPS * 32, 1)
 k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
+    using C = H16Col<F>;
     constexpr int T = H16_WARPS * 32;
     constexpr int PV = 8;                                   // summands per 16-B vector
     constexpr int FLUSH_TILES = F::FLUSH / (PV * H16_U);    // tiles per bin window
     constexpr int GROUPS_PER_WINDOW = FLUSH_TILES / H16_NB;
     static_assert(GROUPS_PER_WINDOW >= 1, "window shorter than one buffer group");
-    // per lane: NBIN u32 bins, NBIN64 int64 bins (thread-minor, conflict-free)
+    // per lane: NBIN u32 bins and a COLS-digit int64 column (thread-minor, conflict-free)
     extern __shared__ __align__(16) int64_t smem64[];
-    int64_t* const bins64_all = smem64;                                       // [WARPS][NBIN64][32]
-    uint32_t* const bins_all = reinterpret_cast<uint32_t*>(smem64 + H16_WARPS * F::NBIN64 * 32);
-    __shared__ int64_t wsum[H16_WARPS][F::NBIN64];
+    int64_t* const cols_all = smem64;                                         // [WARPS][COLS][32]
+    uint32_t* const bins_all = reinterpret_cast<uint32_t*>(smem64 + H16_WARPS * C::COLS * 32);
+    __shared__ int64_t wsum[H16_WARPS][32];
     __shared__ int64_t digits[64];                          // grid-tail scratch
     __shared__ int64_t su[64];
     __shared__ uint32_t blk_flags;
@@ -91,11 +77,11 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bins);
     const uint32_t sbase2 = sbase * 0x00010001u;
     const uint32_t one = p.one, mone = p.mone;
-    int64_t* bins64 = bins64_all + warp * (F::NBIN64 * 32) + lane;
+    int64_t* col = cols_all + warp * (C::COLS * 32) + lane;
 #pragma unroll
     for (int b = 0; b < F::NBIN; ++b) bins[b * 32] = 0;
 #pragma unroll
-    for (int b = 0; b < F::NBIN64; ++b) bins64[b * 32] = 0;
+    for (int j = 0; j < C::COLS; ++j) col[j * 32] = 0;
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
 
@@ -111,6 +97,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
 
     uint64_t wstart = blockIdx.x, tlast = 0;
     bool any_tile = false;
+    int flushes = 0;
     auto load_tile = [&](uint4 (&buf)[H16_U], uint64_t tt) {
         if (tt < ntiles) {
 #pragma unroll
@@ -142,13 +129,14 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
             }
         }
         if (++groups == GROUPS_PER_WINDOW) {
-            if (h16_flush<F>(bins, bins64)) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
+            if (h16_flush_col<F>(bins, col)) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
+            if (++flushes == C::REG_FLUSHES) { h16_col_regularize<F>(col); flushes = 0; }
             groups = 0;
             wstart = t;
             any_tile = false;
         }
     }
-    if (h16_flush<F>(bins, bins64) && any_tile) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
+    if (h16_flush_col<F>(bins, col) && any_tile) h16_rescan<F>(body, wstart, tlast, G, TV, tid, flags);
 
     // leftover vectors (< one tile), the unaligned head and the tail: checked adds by the block
     // that would own the next tile (<= 4 vectors + 1 element per thread: no bin can wrap)
@@ -169,50 +157,21 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
         if ((uint64_t)tid < head) h16_add_checked<F>(bins, __ldg(x + tid), flags);
         if (tid >= 8 && (uint64_t)(tid - 8) < tail) h16_add_checked<F>(bins, __ldg(x + head + nvec * PV + (tid - 8)), flags);
     }
-    h16_flush<F>(bins, bins64);
+    h16_flush_col<F>(bins, col);
     __syncwarp();
 
-    // warp: lane b sums bin b over the 32 lanes (rotated reads: conflict-free); block: warp 0
-    // sums the warps. Per-lane int64 bins hold < 2^(32 + 24) for launches of < 2^40 summands
-    // (api.cu splits longer ones), so the block totals stay below 2^63.
+    // warp: the 32 narrow columns become the warp's digits (lane j: digit j); block: warp 0 sums
+    // the warps (|.| <= 16 (2^51 + 2^16)) and regularizes; grid: grid_tail.cuh
     {
-        const int64_t* wb = bins64_all + warp * (F::NBIN64 * 32);
-        for (int b = lane; b < F::NBIN64; b += 32) {
-            int64_t s = 0;
-#pragma unroll 8
-            for (int c = 0; c < 32; ++c) s += wb[b * 32 + ((c + b) & 31)];
-            wsum[warp][b] = s;
-        }
-        uint32_t f = __reduce_or_sync(FULL, flags);
+        wsum[warp][lane] = h16_col_combine<F>(cols_all + warp * (C::COLS * 32), lane);
+        const uint32_t f = __reduce_or_sync(FULL, flags);
         if (lane == 0 && f) atomicOr(&blk_flags, f);
     }
     __syncthreads();
-    // block bins -> 52-bit digits: group g's net value V_g = T(g,+) - T(g,-) is worth V_g 2^pos(g);
-    // its <= 3 chunks (constant shifts) go to the digits it overlaps. Lane j gathers the chunks of
-    // digits j and j+32 from the groups whose window covers them (no shared atomics).
-    __shared__ int64_t gch[F::NGF][3];
     int64_t a0 = 0, a1 = 0;
     if (warp == 0) {
-        if (lane < F::NGF) {
-            int64_t tp = 0, tn = 0;
-            for (int w = 0; w < H16_WARPS; ++w) {
-                tp += wsum[w][2 * lane];
-                tn += wsum[w][2 * lane + 1];
-            }
-            const int64_t V = tp - tn;
-            const int P = F::pos(lane), o = P % W;
-            gch[lane][0] = (int64_t)(((uint64_t)V << o) & MASK);              // bits [0, 52) of V 2^o
-            gch[lane][1] = (V >> (W - o)) & (int64_t)MASK;                    // bits [52, 104)
-            gch[lane][2] = V >> (2 * W - o < 63 ? 2 * W - o : 63);            // bits >= 104 (signed)
-        }
-        __syncwarp();
 #pragma unroll
-        for (int g = 0; g < F::NGF; ++g) {
-            const int i = F::pos(g) / W;
-            const int d0 = lane - i, d1 = lane + 32 - i;
-            if (d0 >= 0 && d0 < 3) a0 += gch[g][d0];
-            if (d1 >= 0 && d1 < 3) a1 += gch[g][d1];
-        }
+        for (int w = 0; w < H16_WARPS; ++w) a0 += wsum[w][lane];
         regularize_warp(a0, a1, lane);
     }
     grid_tail<H16_WARPS>(a0, a1, blk_flags, n, p, digits, su, &blk_flags, &is_last, warp, lane);
@@ -220,7 +179,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
 
 template <class F>
 static cudaError_t launch_h16(const uint16_t* x, uint64_t n, const AccParams& p, int num_sms, cudaStream_t s) {
-    constexpr size_t SMEM = (size_t)H16_WARPS * 32 * (F::NBIN64 * 8 + F::NBIN * 4);
+    constexpr size_t SMEM = (size_t)H16_WARPS * 32 * (H16Col<F>::COLS * 8 + F::NBIN * 4);
     static unsigned long long smem_set = 0;
     if (cudaError_t e = ensure_smem(k_accumulate_h16<F>, SMEM, smem_set)) return e;
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 2;

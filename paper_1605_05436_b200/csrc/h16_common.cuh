@@ -22,16 +22,21 @@ struct H16Fmt {
     // bin g holds sum M 2^o with M 2^k = (M 2^o) 2^(g 2^SB - 2): position BASE - 2 + g 2^SB
     static constexpr int pos(int g) { return BASE - 2 + g * (1 << SB); }
 };
-// binary16: M <= 2047, o <= 7: 16383 * 2047 * 2^7 < 2^32.  bfloat16: M <= 255, o <= 15:
-// 511 * 255 * 2^15 < 2^32. Window bit positions: binary16 k + 1050, bfloat16 k + 941.
+// Groups of 8 exponents for both formats: binary16 M <= 2047, o <= 7: 16383 * 2047 * 2^7 < 2^32
+// (4 finite groups); bfloat16 M <= 255, o <= 7: 131071 * 255 * 2^7 < 2^32 (32 finite groups; the
+// windows are long enough that emptying the bins is rare). Window bit positions: binary16
+// k + 1050, bfloat16 k + 941.
 using FmtF16 = H16Fmt<10, 5, 3, 16383, 1050>;
-using FmtBF16 = H16Fmt<7, 8, 4, 511, 941>;
+using FmtBF16 = H16Fmt<7, 8, 3, 131071, 941>;
+// Segments empty their bins at every segment's end, so fewer bins beat longer windows there:
+// bfloat16 groups of 16 exponents (17 groups; 511 * 255 * 2^15 < 2^32).
+using FmtBF16Seg = H16Fmt<7, 8, 4, 511, 941>;
 // a window of FLUSH adds of the largest M 2^o cannot wrap an unsigned 32-bit bin
 template <class F>
 constexpr bool flush_fits() {
     return (unsigned long long)F::FLUSH * ((2ull << F::t) - 1) * (1ull << ((1 << F::SB) - 1)) < (1ull << 32);
 }
-static_assert(flush_fits<FmtF16>() && flush_fits<FmtBF16>(), "bin window too long");
+static_assert(flush_fits<FmtF16>() && flush_fits<FmtBF16>() && flush_fits<FmtBF16Seg>(), "bin window too long");
 
 // One summand (checked paths): h = |x| bit pattern (15 bits), s = sign bit; bins = this lane's
 // bin column (bin b at word b*32).
@@ -101,6 +106,92 @@ __device__ __forceinline__ uint32_t h16_special_flags(uint32_t b16) {
     if (((b16 >> F::t) & ((1u << F::l) - 1u)) != (1u << F::l) - 1u) return 0;
     if (b16 & ((1u << F::t) - 1u)) return XSUM_F_NAN;
     return (b16 >> 15) ? XSUM_F_NINF : XSUM_F_PINF;
+}
+
+// The bins are emptied into a narrow per-lane digit column holding only the digits the format
+// reaches: row r is digit COL0 + r. A u32 bin (< 2^32) at bit position pos(g) spans <= 2 digits;
+// COLS leaves room above for the carries of 2^63 summands; per flush a digit takes at most
+// CHUNKS chunks (< 2^52 each), so REG_FLUSHES flushes fit the int64 headroom before the column
+// must be regularized.
+template <class F>
+struct H16Col {
+    static constexpr int COL0 = F::pos(0) / 52;
+    static constexpr int COLS = F::pos(F::NGF - 1) / 52 + 2 - COL0 + 4;
+    static constexpr int CHUNKS = 2 * ((52 + 84) / (1 << F::SB) + 1);
+    static constexpr int REG_FLUSHES = 2000 / CHUNKS >= 64 ? 64 : (2000 / CHUNKS >= 32 ? 32 : 16);
+};
+static_assert(H16Col<FmtBF16>::REG_FLUSHES * H16Col<FmtBF16>::CHUNKS < 2048 &&
+              H16Col<FmtBF16Seg>::REG_FLUSHES * H16Col<FmtBF16Seg>::CHUNKS < 2048 &&
+              H16Col<FmtF16>::REG_FLUSHES * H16Col<FmtF16>::CHUNKS < 2048, "column headroom");
+
+// Empty the finite u32 bins into the narrow column; returns true if this lane's NaN/Inf group
+// was non-empty (and clears it: NaN/Inf are never summed).
+template <class F>
+__device__ __forceinline__ bool h16_flush_col(uint32_t* bins, int64_t* col) {
+    using C = H16Col<F>;
+#pragma unroll
+    for (int j = 0; j < F::NBIN64; ++j) {
+        const int P = F::pos(j >> 1), i = P / W - C::COL0, o = P % W;
+        const uint64_t V = bins[j * 32];
+        bins[j * 32] = 0;
+        const int64_t c0 = (int64_t)((V << o) & MASK);
+        const int64_t c1 = (int64_t)(V >> (W - o));                 // V 2^o < 2^84: two digits
+        XS_ASSERT(i >= 0 && i + 1 < C::COLS - 1);
+        if (j & 1) {
+            col[i * 32] -= c0;
+            col[(i + 1) * 32] -= c1;
+        } else {
+            col[i * 32] += c0;
+            col[(i + 1) * 32] += c1;
+        }
+    }
+    const uint32_t sp = bins[F::NBIN64 * 32] | bins[(F::NBIN64 + 1) * 32];
+    bins[F::NBIN64 * 32] = 0;
+    bins[(F::NBIN64 + 1) * 32] = 0;
+    return sp != 0;
+}
+
+template <class F>
+__device__ __forceinline__ void h16_col_regularize(int64_t* col) {
+    constexpr int COLS = H16Col<F>::COLS;
+    int64_t cin = 0;
+#pragma unroll
+    for (int j = 0; j < COLS - 1; ++j) {
+        const int64_t y = col[j * 32];
+        const int64_t c = balanced_carry(y);
+        col[j * 32] = y - (c << W) + cin;
+        cin = c;
+    }
+    col[(COLS - 1) * 32] += cin;
+}
+
+// A warp's narrow columns (wb: rows of 32 lanes) combined into the digit-parallel form: lane j
+// returns digit j (all rows lie below digit 32). Row r is summed by lane r as hi/lo 32-bit halves
+// (raw digits |Y| < 2^63), balanced carries are split off (the top row takes carries only) and
+// move one row up.
+template <class F>
+__device__ __forceinline__ int64_t h16_col_combine(const int64_t* wb, int lane) {
+    using C = H16Col<F>;
+    static_assert(C::COL0 + C::COLS <= 32, "narrow column above digit 31");
+    int64_t hs = 0, ls = 0;
+    if (lane < C::COLS) {
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) {
+            const int64_t v = wb[lane * 32 + ((lane + c) & 31)];
+            hs += v >> 32;
+            ls += (int64_t)(uint32_t)v;
+        }
+    }
+    int64_t cr = 0, rr = (int64_t)((uint64_t)hs << 32) + ls;
+    if (lane < C::COLS - 1) {
+        cr = (hs + ((ls + (1ll << 51)) >> 32)) >> 20;
+        rr = (int64_t)((uint64_t)(hs - (cr << 20)) << 32) + ls;
+    }
+    int64_t cin = __shfl_up_sync(FULL, cr, 1);
+    if (lane == 0) cin = 0;
+    const int64_t row = lane < C::COLS ? rr + cin : 0;
+    const int64_t d = __shfl_sync(FULL, row, (lane - C::COL0) & 31);
+    return (lane >= C::COL0 && lane < C::COL0 + C::COLS) ? d : 0;
 }
 
 }  // namespace xs

@@ -312,54 +312,6 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
 // red.shared, NaN/Inf in a group of their own that is never summed) with a per-segment flush
 // into a narrow digit column. About 11 instructions per element instead of ~17.
 // ---------------------------------------------------------------------------------------
-template <class F>
-struct H16Seg {
-    static constexpr int COL0 = F::pos(0) / 52;
-    static constexpr int COLS = F::pos(F::NGF - 1) / 52 + 2 - COL0 + 4;   // a bin spans <= 2 digits
-    static constexpr int REG_FLUSHES = 64;   // <= 18 chunks per digit per flush: 64 * 18 * 2^52 < 2^62
-};
-
-// Empty the finite u32 bins into the narrow column (row r = digit COL0 + r); returns true if this
-// lane's NaN/Inf group was non-empty (and clears it).
-template <class F>
-__device__ __forceinline__ bool h16seg_flush(uint32_t* bins, int64_t* col) {
-    using S = H16Seg<F>;
-#pragma unroll
-    for (int j = 0; j < F::NBIN64; ++j) {
-        const int P = F::pos(j >> 1), i = P / W - S::COL0, o = P % W;
-        const uint64_t V = bins[j * 32];
-        bins[j * 32] = 0;
-        const int64_t c0 = (int64_t)((V << o) & MASK);
-        const int64_t c1 = (int64_t)(V >> (W - o));                 // V 2^o < 2^84: two digits
-        XS_ASSERT(i >= 0 && i + 1 < S::COLS - 1);
-        if (j & 1) {
-            col[i * 32] -= c0;
-            col[(i + 1) * 32] -= c1;
-        } else {
-            col[i * 32] += c0;
-            col[(i + 1) * 32] += c1;
-        }
-    }
-    const uint32_t sp = bins[F::NBIN64 * 32] | bins[(F::NBIN64 + 1) * 32];
-    bins[F::NBIN64 * 32] = 0;
-    bins[(F::NBIN64 + 1) * 32] = 0;
-    return sp != 0;
-}
-
-template <class F>
-__device__ __forceinline__ void h16seg_regularize(int64_t* col) {
-    constexpr int COLS = H16Seg<F>::COLS;
-    int64_t cin = 0;
-#pragma unroll
-    for (int j = 0; j < COLS - 1; ++j) {
-        const int64_t y = col[j * 32];
-        const int64_t c = balanced_carry(y);
-        col[j * 32] = y - (c << W) + cin;
-        cin = c;
-    }
-    col[(COLS - 1) * 32] += cin;
-}
-
 // Rare path: classify the NaN/Inf patterns of a segment (they were binned into the special
 // group, which is never summed).
 template <class F>
@@ -378,14 +330,14 @@ __device__ __forceinline__ void h16seg_add_checked(uint32_t* bins, uint32_t b16,
 
 template <class F>
 constexpr size_t h16seg_smem() {
-    return (size_t)SSEG_WARPS * 32 * (H16Seg<F>::COLS * 8 + F::NBIN * 4);
+    return (size_t)SSEG_WARPS * 32 * (H16Col<F>::COLS * 8 + F::NBIN * 4);
 }
 
 template <class F>
 __global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
 k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
                SegOut o, uint32_t one, uint32_t mone) {
-    using S = H16Seg<F>;
+    using S = H16Col<F>;
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SSEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -446,9 +398,9 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
                 h16_add_word<F>(sbase, sbase2, bf[u].w, one, mone);
             }
             if (++since == WIN_TILES) {
-                special |= h16seg_flush<F>(bins, col);
+                special |= h16_flush_col<F>(bins, col);
                 since = 0;
-                if (++flushes == S::REG_FLUSHES) { h16seg_regularize<F>(col); flushes = 0; }
+                if (++flushes == S::REG_FLUSHES) { h16_col_regularize<F>(col); flushes = 0; }
             }
         };
         for (uint64_t it = 0; it < nit; it += 2) {
@@ -479,7 +431,7 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
                 h16_add_word<F>(sbase, sbase2, lv[u].w, one, mone);
             }
         }
-        special |= h16seg_flush<F>(bins, col);
+        special |= h16_flush_col<F>(bins, col);
         if (__any_sync(FULL, special)) flags |= h16seg_classify<F>(g.xs, g.len, lane);   // rare
         const uint64_t sn = s + nw;
         const bool more = sn < nseg;
@@ -492,28 +444,10 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
             }
         }
         __syncwarp();
-        int64_t hs = 0, ls = 0;
-        if (lane < S::COLS) {
-#pragma unroll 8
-            for (int c = 0; c < 32; ++c) {
-                const int64_t v = wb[lane * 32 + ((lane + c) & 31)];
-                hs += v >> 32;
-                ls += (int64_t)(uint32_t)v;
-            }
-        }
+        const int64_t a0 = h16_col_combine<F>(wb, lane);
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < S::COLS; ++j) col[j * 32] = 0;
-        int64_t cr = 0, rr = (int64_t)((uint64_t)hs << 32) + ls;
-        if (lane < S::COLS - 1) {
-            cr = (hs + ((ls + (1ll << 51)) >> 32)) >> 20;
-            rr = (int64_t)((uint64_t)(hs - (cr << 20)) << 32) + ls;
-        }
-        int64_t cin = __shfl_up_sync(FULL, cr, 1);
-        if (lane == 0) cin = 0;
-        const int64_t row = lane < S::COLS ? rr + cin : 0;
-        const int64_t d = __shfl_sync(FULL, row, (lane - S::COL0) & 31);
-        const int64_t a0 = (lane >= S::COL0 && lane < S::COL0 + S::COLS) ? d : 0;
         flags = __reduce_or_sync(FULL, flags);
         const xsum_result r =
             finalize_warp_inl(a0, 0, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su[warp], lane);
@@ -557,7 +491,7 @@ cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t
     switch (dtype) {
         case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s);
         case XSUM_DT_F16: return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s);
-        case XSUM_DT_BF16: return launch_h16seg<FmtBF16>(x, nseg, seg_len, offsets, o, num_sms, s);
+        case XSUM_DT_BF16: return launch_h16seg<FmtBF16Seg>(x, nseg, seg_len, offsets, o, num_sms, s);
         default: return cudaErrorInvalidValue;
     }
 }

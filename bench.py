@@ -334,13 +334,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if x.numel() * x.element_size() < (256 << 20) \
         else None
     l0 = xsum.launch_count()
+    # events bracket the K steps; per-step events only when L2 flushes sit between the steps
+    # (otherwise they would add a stream operation between consecutive kernels)
     with ClockSampler(local_rank) as clk:
         for i in range(K):
             if flush is not None:
                 flush.zero_()
-            ev[i][0].record(stream)
+            if flush is not None or i == 0:
+                ev[i][0].record(stream)
             step()
-            ev[i][1].record(stream)
+            if flush is not None or i == K - 1:
+                ev[i][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -355,9 +359,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         allreduce_(hi, torch.distributed.ReduceOp.MAX)
         if not torch.equal(lo, hi) or int(hi[1]) & xsum.F_PEER_TIMEOUT:
             raise RuntimeError(f"ranks disagree or the peer exchange timed out: {lo.tolist()} {hi.tolist()}")
-    per = [a.elapsed_time(b) for a, b in ev]                 # ms per step (device)
     # span of the K steps; with L2 flushes in between, the sum of the steps' own times
-    total_ms = sum(per) if flush is not None else ev[0][0].elapsed_time(ev[-1][1])
+    if flush is not None:
+        total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    else:
+        total_ms = ev[0][0].elapsed_time(ev[-1][1])
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         allreduce_(t, torch.distributed.ReduceOp.MAX)
@@ -365,9 +371,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     n_all = n_local * world
     value = n_all * K / (total_ms / 1e3)
 
-    # dominant kernel: the accumulate launch (N=1 the step is exactly that one launch)
+    # dominant kernel: the accumulate launch (N=1 the step is exactly that one launch: its
+    # average duration is the rank's span / K, launch gaps included)
     if world == 1:
-        kern_ms = statistics.mean(per)
+        kern_ms = total_ms / K
     else:   # time the local accumulate alone with events on its stream
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
         for a, b in kev:

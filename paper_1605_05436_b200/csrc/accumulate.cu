@@ -122,16 +122,26 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
 
     // leftover vectors (< one tile), the unaligned head and the tail elements: checked adds by
     // the block that would own the next tile.
+    bool touched = blockIdx.x < ntiles;                 // every thread takes part in every tile
     if (blockIdx.x == ntiles % G) {
         const uint64_t v0 = ntiles * TV;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             uint64_t v = v0 + (uint64_t)u * T + tid;
-            if (v < nvec) EL::add_vec_checked(col, ldg_stream(body + v), flags, one);
+            if (v < nvec) {
+                EL::add_vec_checked(col, ldg_stream(body + v), flags, one);
+                touched = true;
+            }
         }
         const uint64_t tail = nbody - nvec * PV;
-        if ((uint64_t)tid < head) EL::add_one_checked(col, x + tid, flags, one);
-        if (tid >= PV && (uint64_t)(tid - PV) < tail) EL::add_one_checked(col, x + head + nvec * PV + (tid - PV), flags, one);
+        if ((uint64_t)tid < head) {
+            EL::add_one_checked(col, x + tid, flags, one);
+            touched = true;
+        }
+        if (tid >= PV && (uint64_t)(tid - PV) < tail) {
+            EL::add_one_checked(col, x + head + nvec * PV + (tid - PV), flags, one);
+            touched = true;
+        }
     }
     if (tid == 0) xs_stamp(p.stamps, 1, blockIdx.x);                 // stream done
     if (__any_sync(FULL, EL::hit(nspec))) {
@@ -143,10 +153,11 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     __syncwarp();
 
     // warp: sum the 32 raw lane columns into regularized digits (lane l holds digits l and
-    // l+32; rotated reads keep the 32 lanes on 32 distinct columns).
+    // l+32; rotated reads keep the 32 lanes on 32 distinct columns). A warp that added nothing
+    // (small inputs) has zero columns and skips the combine.
     {
-        int64_t s0, s1;
-        combine_raw_columns(win + warp * (D * 32), s0, s1, lane);
+        int64_t s0 = 0, s1 = 0;
+        if (__any_sync(FULL, touched)) combine_raw_columns(win + warp * (D * 32), s0, s1, lane);
         wsum[warp][lane] = s0;
         if (lane + 32 < D) wsum[warp][lane + 32] = s1;
         uint32_t f = __reduce_or_sync(FULL, flags);

@@ -305,6 +305,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             exchange = "fused: one launch per rank, NVLink P2P state exchange (xsum_sum_allreduce)"
         except Exception as e:  # noqa: BLE001
             exchange = f"NCCL all-gather of 384-B states + xsum_merge_round (peer buffers unavailable: {e!r:.120})"
+        if pe is not None:
+            why = fused_check(xsum, dist, pe, x, acc, tot)
+            if why:
+                pe = None
+                exchange = f"NCCL all-gather of 384-B states + xsum_merge_round (fused exchange rejected: {why})"
     elif world > 1 and not seg:
         exchange = f"{args.dist_backend} all-gather of 384-B states + xsum_merge_round"
 
@@ -489,6 +494,27 @@ def allreduce_(t, op):
     else:
         tdist.all_reduce(t, op=op)
     return t
+
+
+def fused_check(xsum, dist, pe, x, acc, tot) -> str | None:
+    """Before timing the fused multi-GPU step, run it once on a 2^20-element prefix and compare
+    with the NCCL all-gather + merge path on the same prefix; every rank must see bit-identical
+    results and no peer timeout, else (all ranks agree on it) the NCCL path is timed instead.
+    Returns None when the fused step is accepted, else the reason."""
+    import torch
+
+    probe = x[: min(x.numel(), 1 << 20)]
+    res, _ = pe.sum(probe, acc)
+    fused = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+    ref = xsum.Result.from_bytes(dist.exact_sum_distributed(probe, xsum.Accumulator(x.device), tot)
+                                 .cpu().numpy().tobytes())
+    ok = fused.bits == ref.bits and fused.flags == ref.flags and not fused.flags & xsum.F_PEER_TIMEOUT
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=x.device)
+    allreduce_(flag, torch.distributed.ReduceOp.MIN)
+    if int(flag.item()):
+        return None
+    return (f"rank result {fused.bits:016x}/{fused.flags:#x} vs NCCL path {ref.bits:016x}/{ref.flags:#x}"
+            if not ok else "another rank disagreed")
 
 
 def measure_e2e_multi(xsum, torch, dist, x_dev, steps: int, dev, pe, acc, tot, world: int):

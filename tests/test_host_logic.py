@@ -282,3 +282,64 @@ def test_sparse_image_decoder_on_a_hand_built_image():
         xs.decode_sparse(struct.pack("<IHBBIIQ", 0x41505359, 1, 52, 0, 0, 0, 0))   # bad magic
     with pytest.raises(ValueError):
         xs.decode_sparse(hdr + recs[:8])                                          # truncated
+
+
+def _result_bytes(bits: int, flags: int):
+    import torch
+    a = np.zeros(xsum.RESULT_BYTES, dtype=np.uint8)
+    a[0:8] = np.array([bits], dtype=np.uint64).view(np.uint8)
+    a[12:16] = np.array([flags], dtype=np.uint32).view(np.uint8)
+    return torch.from_numpy(a)
+
+
+def _fused_check_worker(rank: int, world: int, port: int, mode: str, q):
+    """bench.fused_check with stand-ins for the fused step (pe.sum) and the NCCL path
+    (dist.exact_sum_distributed): CPU tensors, gloo group."""
+    import types
+
+    import torch
+    import torch.distributed as tdist
+    sys.path.insert(0, ROOT)
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        good = 0x3FF0000000000001
+        fused_bits, fused_flags = good, 0
+        if mode == "timeout":
+            fused_flags = xsum.F_PEER_TIMEOUT
+        elif mode == "one_rank_wrong" and rank == 1:
+            fused_bits = good ^ 1
+        pe = types.SimpleNamespace(sum=lambda x, acc: (_result_bytes(fused_bits, fused_flags), None))
+        fake_dist = types.SimpleNamespace(exact_sum_distributed=lambda x, acc, tot: _result_bytes(good, 0))
+        fake_xsum = types.SimpleNamespace(Result=xsum.Result, F_PEER_TIMEOUT=xsum.F_PEER_TIMEOUT,
+                                          Accumulator=lambda device: None)
+        why = bench.fused_check(fake_xsum, fake_dist, pe, torch.zeros(10, dtype=torch.float64), None, None)
+        q.put((rank, why))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["ok", "timeout", "one_rank_wrong"])
+def test_bench_fused_check_two_ranks(mode):
+    """bench.py times the fused multi-GPU step only if every rank's fused result on a probe
+    equals the NCCL all-gather path's with no peer timeout; one rank's disagreement makes every
+    rank fall back (the decision is all-reduced)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + (os.getpid() % 2000) + ["ok", "timeout", "one_rank_wrong"].index(mode) * 7
+    procs = [ctx.Process(target=_fused_check_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if mode == "ok":
+        assert got == {0: None, 1: None}
+    else:
+        assert got[0] is not None and got[1] is not None
+        if mode == "one_rank_wrong":
+            assert got[0] == "another rank disagreed" and got[1].startswith("rank result")

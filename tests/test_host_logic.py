@@ -52,7 +52,8 @@ def test_library_sizes_match_header(built):
     L = built
     assert L.xsum_state_bytes() == xsum.STATE_BYTES == 384
     assert L.xsum_result_bytes() == xsum.RESULT_BYTES == 48
-    assert L.xsum_scratch_bytes(0) >= 256 + 8 * 42 * 148
+    # arrival counter (0), flags word (4), grid accumulator of 42 u64 digits at byte 256
+    assert L.xsum_scratch_bytes(0) >= 256 + 8 * 42
     assert L.xsum_status_str(0) == b"ok"
     assert L.xsum_status_str(2).startswith(b"capacity")
 

@@ -364,13 +364,13 @@ __device__ __forceinline__ xsum_result finalize_warp_inl(int64_t a0, int64_t a1,
     int64_t u0 = (t0 - (int64_t)((CI >> lane) & 1)) & (int64_t)MASK;
     int64_t u1 = t1 - (int64_t)((CI >> (lane + 32)) & 1);
     if (lane + 32 < D - 1) u1 &= (int64_t)MASK;
-    su[lane] = u0;
-    if (has1) su[lane + 32] = u1;
-    __syncwarp();
     uint64_t nzu = (uint64_t)__ballot_sync(FULL, u0 != 0) | ((uint64_t)__ballot_sync(FULL, has1 && u1 != 0) << 32);
 
     // canonical image: 34 little-endian u64 limbs of A (two's complement)
     if (canon) {
+        su[lane] = u0;
+        if (has1) su[lane + 32] = u1;
+        __syncwarp();
         uint64_t l0 = extract_bits(su, 64 * lane, 64);
         uint64_t l1 = (lane + 32 < XSUM_CANON_LIMBS) ? extract_bits(su, 64 * (lane + 32), 64) : 0;
         if (sign) {
@@ -393,34 +393,50 @@ __device__ __forceinline__ xsum_result finalize_warp_inl(int64_t a0, int64_t a1,
     uint32_t rf = 0;                              // flags of this lane's rounding
     int dir = 0, msb = INT32_MIN, sh_out = 0;
     uint64_t q_out = 0;
-    if (lane < 2 && nzu) {
-        int m = 63 - __clzll((long long)nzu);
-        int p = 52 * m + (63 - __clzll((long long)su[m]));         // leading bit of |A|
-        msb = p - 1074;
-        int sh = p - (prec - 1) > emin ? p - (prec - 1) : emin;
-        uint64_t q = extract_bits(su, sh, prec + 1);
-        int g = sh > 0 ? (int)extract_bits(su, sh - 1, 1) : 0;
-        bool sticky = false;                                        // any bit below the guard bit
-        if (sh > 1) {
-            int pos = sh - 1, jg = pos / 52, off = pos - 52 * jg;
-            sticky = (nzu & ((1ull << jg) - 1)) != 0;
-            if (off) sticky = sticky || ((uint64_t)su[jg] & ((1ull << off) - 1));
+    if (nzu) {                                    // warp-uniform
+        // The guard bit lies at most prec+1 <= 54 bits below the leading bit, so the kept bits
+        // and the guard bit sit in the three digits m, m-1, m-2 (m = top non-zero digit):
+        // Wp = (d_m 2^104 + d_{m-1} 2^52 + d_{m-2}) >> 51 < 2^105 holds them (bit 0 of Wp =
+        // bit 52m-53 of |A|); everything below Wp is sticky.
+        const int m = 63 - __clzll((long long)nzu);
+        auto digit = [&](int j) -> uint64_t {     // digit j (warp-uniform j), 0 for j < 0
+            uint64_t v = (uint64_t)__shfl_sync(FULL, j >= 32 ? u1 : u0, j & 31);
+            return j >= 0 ? v : 0;
+        };
+        const uint64_t dm = digit(m), dm1 = digit(m - 1), dm2 = digit(m - 2);
+        if (lane < 2) {
+            const int p = 52 * m + (63 - __clzll((long long)dm));   // leading bit of |A|
+            msb = p - 1074;
+            int sh = p - (prec - 1) > emin ? p - (prec - 1) : emin;
+            const unsigned __int128 Wp = ((unsigned __int128)dm << 53) | ((unsigned __int128)dm1 << 1) | (dm2 >> 51);
+            const int s = sh - 52 * m + 53;                         // >= 54 - prec >= 1
+            uint64_t q = 0;
+            int g = 0;
+            bool sticky;                                            // any bit below the guard bit
+            if (s < 128) {
+                q = (uint64_t)(Wp >> s);
+                g = (int)((uint64_t)(Wp >> (s - 1)) & 1);
+                sticky = (Wp & (((unsigned __int128)1 << (s - 1)) - 1)) != 0;
+            } else {
+                sticky = Wp != 0;                                   // guard bit above Wp: 0
+            }
+            sticky = sticky || (dm2 & ((1ull << 51) - 1)) || (m >= 3 && (nzu & ((1ull << (m - 2)) - 1)));
+            int up = g && (sticky || (q & 1));
+            if (g || sticky) dir = up ? 1 : -1;
+            q += (uint64_t)up;
+            if (sh == emin) {
+                bits = q;                             // subnormal / smallest normals: bits = q
+            } else {
+                if (q == (1ull << prec)) { q >>= 1; sh += 1; }
+                int Eb = sh - emin + 1;
+                if (Eb >= emax) { bits = (uint64_t)emax << (prec - 1); rf |= is64 ? XSUM_F_OVERFLOW : XSUM_F_OVERFLOW32; dir = 1; }
+                else bits = ((uint64_t)Eb << (prec - 1)) | (q - (1ull << (prec - 1)));
+            }
+            q_out = q;
+            sh_out = sh;
+            if (dir) rf |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
+            if (sign) { bits |= is64 ? (1ull << 63) : 0x80000000ull; dir = -dir; }   // -0.0f possible (R18)
         }
-        int up = g && (sticky || (q & 1));
-        if (g || sticky) dir = up ? 1 : -1;
-        q += (uint64_t)up;
-        if (sh == emin) {
-            bits = q;                             // subnormal / smallest normals: bits = q
-        } else {
-            if (q == (1ull << prec)) { q >>= 1; sh += 1; }
-            int Eb = sh - emin + 1;
-            if (Eb >= emax) { bits = (uint64_t)emax << (prec - 1); rf |= is64 ? XSUM_F_OVERFLOW : XSUM_F_OVERFLOW32; dir = 1; }
-            else bits = ((uint64_t)Eb << (prec - 1)) | (q - (1ull << (prec - 1)));
-        }
-        q_out = q;
-        sh_out = sh;
-        if (dir) rf |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
-        if (sign) { bits |= is64 ? (1ull << 63) : 0x80000000ull; dir = -dir; }   // -0.0f possible (R18)
     }
     const uint64_t b32 = __shfl_sync(FULL, bits, 1);
     const uint32_t rf32 = __shfl_sync(FULL, rf, 1);

@@ -258,12 +258,16 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
         for (int b = 0; b < SEG_NB; ++b) {
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) {
+#ifdef XS_EXP_SEG_NOACC   // diagnostic (wrong sums): loads only
+                nspec ^= buf[b][u].x ^ buf[b][u].y ^ buf[b][u].z ^ buf[b][u].w;
+#else
                 Chunks a = decompose(buf[b][u].x, buf[b][u].y, one, mone);
                 nspec = spec_fold(nspec, a);
                 column_add(col, a, one);
                 Chunks c = decompose(buf[b][u].z, buf[b][u].w, one, mone);
                 nspec = spec_fold(nspec, c);
                 column_add(col, c, one);
+#endif
             }
             if (ld) {
 #pragma unroll
@@ -284,6 +288,12 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
                 groups = 0;                                    // the window restarts (all lanes)
             }
             // epilogue inline: an out-of-line call would wait for the in-flight buffers
+#if defined(XS_EXP_SEG_NOEPI) || defined(XS_EXP_SEG_NOACC)   // diagnostic (wrong sums)
+            if (lane == 0) o.out[ps] = (double)nspec;
+            if (false) {
+#else
+            {
+#endif
             const int64_t* wb = win + warp * (D * 32);
             __syncwarp();
             LaneSums now = raw_lane_sums(wb, lane);
@@ -295,6 +305,7 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
             xsum_result r = finalize_warp_inl(a0, a1, fl, seg_len, o.canon ? o.canon + ps * XSUM_CANON_LIMBS : nullptr,
                                               su[warp], lane);
             if (lane == 0) o.write(ps, r);
+            }
             flags = 0;
             wstart = 0;                                        // window tiles of the next segment start at 0
             pt = 0;

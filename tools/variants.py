@@ -21,6 +21,12 @@ VARIANTS = {
     # examples of compile-time knobs (see the kernels): register-buffer depth of each kernel
     "acc_nb4": ["-DXS_ACC_NB=4"],
     "seg_nb4": ["-DXS_SEG_NB=4"],
+    "seg_u2nb4": ["-DXS_SEG_U=2", "-DXS_SEG_NB=4"],
+    "seg_u2nb8": ["-DXS_SEG_U=2", "-DXS_SEG_NB=8"],
+    "seg_u1nb8": ["-DXS_SEG_U=1", "-DXS_SEG_NB=8"],
+    "seg_u1nb16": ["-DXS_SEG_U=1", "-DXS_SEG_NB=16"],
+    "exp_seg_noepi": ["-DXS_EXP_SEG_NOEPI"],
+    "exp_seg_noacc": ["-DXS_EXP_SEG_NOACC"],
     "h16_nb2": ["-DXS_H16_NB=2"],
     "h16_ldsts": ["-DXS_H16_LDSTS"],
     "f32b_nb4": ["-DXS_F32B_NB=4"],
@@ -62,7 +68,8 @@ acc = xsum.Accumulator()
 if {cfg!r}.endswith("seg"):
     class _S:
         def sum(self, x):
-            v, _, _ = xsum.sum_segments(x, 4096)
+            global seg_v
+            seg_v, _, _ = xsum.sum_segments(x, 4096)
             return xsum_res, None
     xsum_res = acc.sum(x)[0]
     acc = _S()
@@ -74,7 +81,9 @@ for a, b in ev:
 torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
-print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, bits=hex(r.bits))))
+import hashlib
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith("seg") else hex(r.bits)
+print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     print(out.stdout.strip() or out.stderr[-2000:], flush=True)

@@ -2,7 +2,7 @@
 
     python tools/variants.py build [name ...]   # here (nvcc cross-compiles)
     python tools/variants.py run [cfg ...]      # on the GPU box: one JSON line per built variant
-cfg: c1..c5 (binary64 configs), c5seg (segments of c5), f32 / f16 / bf16 (random finite
+cfg: c1..c5 (binary64 configs), c5seg (segments of c5), c5csr (CSR segments), f32 / f16 / bf16 (random finite
 patterns), n<k> (the first 2^k elements of c2).
 Variants named exp* are diagnostic builds that compute WRONG sums (timing only)."""
 from __future__ import annotations
@@ -62,9 +62,20 @@ elif {cfg!r} in ("f16", "bf16"):
     x = torch.randint(-32768, 32767, (1 << 30,), dtype=torch.int16, device="cuda", generator=g)
     em = 0x7C00 if {cfg!r} == "f16" else 0x7F80
     x = torch.where((x & em) == em, x ^ 0x400, x).view(torch.float16 if {cfg!r} == "f16" else torch.bfloat16)
+elif {cfg!r} == "c5csr":
+    x = synth.device_generate("c5csr")
+    csr = synth.csr_offsets("c5csr", device="cuda")
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = xsum.Accumulator()
+if {cfg!r} == "c5csr":
+    class _C:
+        def sum(self, x):
+            global seg_v
+            seg_v, _, _ = xsum.sum_segments_csr(x, csr)
+            return xsum_res, None
+    xsum_res = acc.sum(x)[0]
+    acc = _C()
 if {cfg!r}.endswith("seg"):
     class _S:
         def sum(self, x):
@@ -82,7 +93,7 @@ torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
 import hashlib
-check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith("seg") else hex(r.bits)
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr")) else hex(r.bits)
 print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
@@ -94,8 +105,9 @@ if __name__ == "__main__":
         build(sys.argv[2:])
     else:
         cfgs = sys.argv[2:] or ["c2"]
+        reps = int(os.environ.get("VARIANT_REPS", "1"))
         for cfg in cfgs:
-            for name in VARIANTS:
+            for name in [v for _ in range(reps) for v in VARIANTS]:   # interleaved repetitions
                 so = os.path.join(OUT, f"libxsum_{name}.so")
                 if os.path.exists(so):
                     run_one(so, cfg, 50)

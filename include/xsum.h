@@ -158,6 +158,23 @@ XSUM_API xsum_status xsum_create(xsum_ctx **h, int device, void *d_state, void *
 /* State := 0 (count 0, flags 0), stream-ordered. */
 XSUM_API xsum_status xsum_reset(xsum_ctx *h, void *stream);
 
+/* Checkpoint / resume (the paper's external-memory scan PAPER.md:1095-1108:
+ * the whole superaccumulator is the only state, so a long or out-of-core summation can stop
+ * and resume). The checkpoint is the 384-byte state image above.
+ * xsum_save_state: copies the handle's state image into host_image (>= XSUM_STATE_BYTES bytes,
+ *   caller-owned) after everything enqueued on `stream`; synchronizes `stream`.
+ *   Errors: XSUM_EINVAL (null), XSUM_ECUDA.
+ * xsum_check_state_image: host-side validation of an image: magic, version, w = 52, 42 digits,
+ *   zero reserved word and padding, known flag bits, count <= 2^63-1, every digit regularized
+ *   (|digit| <= R-1; the top digit |d| <= 2^29, the bound the value range gives).
+ *   Returns XSUM_OK or XSUM_EMISMATCH (XSUM_EINVAL for null).
+ * xsum_load_state: state := the image (validated as above; nothing is written on error),
+ *   stream-ordered; the host-side count becomes the image's count. host_image may be pageable
+ *   and freed when the call returns. Errors: XSUM_EINVAL, XSUM_EMISMATCH, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_save_state(xsum_ctx *h, void *host_image, void *stream);
+XSUM_API xsum_status xsum_check_state_image(const void *host_image);
+XSUM_API xsum_status xsum_load_state(xsum_ctx *h, const void *host_image, void *stream);
+
 /* State += sum of d_x[0..n) EXACTLY (§5: the whole superaccumulator
  * stays in fast memory and components are added in any order; PAPER.md:744-750 step 2
  * decomposition; PAPER.md:559-628 carry-free regularization; PAPER.md:768-776 bottom-up

@@ -47,7 +47,8 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_launch_count", "xsum_set_grid_limit", "xsum_accumulate_f32", "xsum_sum_f32", "xsum_merge_round",
            "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
-           "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex")
+           "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex", "xsum_save_state",
+           "xsum_check_state_image", "xsum_load_state")
 
 
 class XsumError(RuntimeError):
@@ -94,6 +95,8 @@ def lib() -> ctypes.CDLL:
             "xsum_peer_selftest": ([p, p, u32, u64, p, p, p], i32),
             "xsum_sum_segments_ex": ([p, i32, u64, u64, p, p, p, p, p, p], i32),
             "xsum_accumulate_host_ex": ([p, p, u64, i32, p, sz, p], i32),
+            "xsum_save_state": ([p, p, p], i32), "xsum_check_state_image": ([p], i32),
+            "xsum_load_state": ([p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -101,6 +104,13 @@ def lib() -> ctypes.CDLL:
             f.restype = res
         _lib = L
     return _lib
+
+
+def check_state_image(image: bytes) -> bool:
+    """Host-side validation of a 384-byte state image (xsum_check_state_image): header, flags,
+    count and digit ranges. True if the image is a valid checkpoint."""
+    image = bytes(image)
+    return len(image) == STATE_BYTES and lib().xsum_check_state_image(image) == 0
 
 
 def status_str(s: int) -> str:
@@ -306,6 +316,38 @@ class Accumulator:
         k = states.numel() // STATE_BYTES
         _check("xsum_merge", lib().xsum_merge(self._h, states.data_ptr(), k, _stream_ptr(self.device)))
         return self
+
+    def save_state(self) -> bytes:
+        """Checkpoint: the 384-byte state image after everything enqueued so far
+        (xsum_save_state; synchronizes the stream)."""
+        buf = ctypes.create_string_buffer(STATE_BYTES)
+        _check("xsum_save_state", lib().xsum_save_state(self._h, buf, _stream_ptr(self.device)))
+        return buf.raw
+
+    def load_state(self, image: bytes) -> "Accumulator":
+        """Resume: state := a checkpoint image (validated host-side first, xsum_load_state)."""
+        image = bytes(image)
+        if len(image) != STATE_BYTES:
+            raise ValueError(f"a state image has {STATE_BYTES} bytes, got {len(image)}")
+        _check("xsum_load_state", lib().xsum_load_state(self._h, image, _stream_ptr(self.device)))
+        return self
+
+    def save(self, path) -> None:
+        """Write the checkpoint to `path` atomically (temporary file + rename)."""
+        data = self.save_state()
+        tmp = f"{path}.tmp{os.getpid()}"
+        with open(tmp, "wb") as f:
+            f.write(data)
+            f.flush()
+            os.fsync(f.fileno())
+        os.replace(tmp, path)
+
+    @classmethod
+    def load(cls, path, device=None) -> "Accumulator":
+        """A new accumulator resumed from the checkpoint file at `path`."""
+        with open(path, "rb") as f:
+            data = f.read()
+        return cls(device).load_state(data)
 
     def merge_round(self, states, canon: bool = False):
         """state := sum of the packed state images, then round (one launch; xsum_merge_round).

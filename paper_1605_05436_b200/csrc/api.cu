@@ -2,6 +2,7 @@
 // Host-side argument checking, handle bookkeeping and launches; every arithmetic step of
 // the summation runs in the kernels (accumulate.cu, merge_finalize.cu, segments.cu).
 #include <cuda_runtime.h>
+#include <cstring>
 
 #include <atomic>
 #include <cstdlib>
@@ -185,6 +186,51 @@ xsum_status xsum_reset(xsum_ctx* h, void* stream) {
     if (!g.ok) return XSUM_ECUDA;
     if (xs::init_state(h->state, static_cast<cudaStream_t>(stream)) != cudaSuccess) return XSUM_ECUDA;
     h->count = 0;
+    return XSUM_OK;
+}
+
+// Checkpoint / resume: the 384-byte state image is the checkpoint.
+xsum_status xsum_save_state(xsum_ctx* h, void* host_image, void* stream) {
+    if (!h || !host_image) return XSUM_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(host_image, h->state, XSUM_STATE_BYTES, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return XSUM_ECUDA;
+    return XSUM_OK;
+}
+
+xsum_status xsum_check_state_image(const void* host_image) {
+    if (!host_image) return XSUM_EINVAL;
+    xsum_state_image im;
+    std::memcpy(&im, host_image, sizeof im);
+    if (im.magic != XSUM_MAGIC || im.version != XSUM_VERSION || im.w != 52 || im.ndigits != XSUM_NDIGITS ||
+        im.reserved != 0 || (im.flags & ~(XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH)) ||
+        im.count > kMaxCount)
+        return XSUM_EMISMATCH;
+    for (unsigned char b : im.pad)
+        if (b) return XSUM_EMISMATCH;
+    const int64_t rmax = (1ll << 52) - 1;                 // regularized: |digit| <= R-1 (Lemma 1)
+    for (int j = 0; j < XSUM_NDIGITS - 1; ++j)
+        if (im.digit[j] > rmax || im.digit[j] < -rmax) return XSUM_EMISMATCH;
+    // top digit (R^41 = 2^2132): |A| < 2^(1024+1074+63) bounds it by 2^29
+    if (im.digit[XSUM_NDIGITS - 1] > (1ll << 29) || im.digit[XSUM_NDIGITS - 1] < -(1ll << 29)) return XSUM_EMISMATCH;
+    return XSUM_OK;
+}
+
+xsum_status xsum_load_state(xsum_ctx* h, const void* host_image, void* stream) {
+    if (!h || !host_image) return XSUM_EINVAL;
+    if (xsum_status st = xsum_check_state_image(host_image)) return st;
+    DeviceGuard g(h->device);
+    if (!g.ok) return XSUM_ECUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // pageable source: the copy is staged before the call returns, so the caller may free it
+    if (cudaMemcpyAsync(h->state, host_image, XSUM_STATE_BYTES, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return XSUM_ECUDA;
+    uint64_t cnt;
+    std::memcpy(&cnt, static_cast<const uint8_t*>(host_image) + 16, sizeof cnt);
+    h->count = cnt;
     return XSUM_OK;
 }
 

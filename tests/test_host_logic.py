@@ -204,6 +204,38 @@ def test_state_codec_roundtrip():
         assert decode_state(encode_state(A, 5)) == (A, 5)
 
 
+def test_checkpoint_image_validation(built):
+    """xsum_check_state_image (the gate of xsum_load_state): accepts every well-formed image,
+    rejects each single header/range violation (include/xsum.h layout)."""
+    R = 1 << 52
+    for A, cnt, fl in ((0, 0, 0), (1, 1, 0), (-(1 << 2100) + 7, 2 ** 63 - 1, 0), ((1 << 1500) - 3, 9, 1 | 2 | 4)):
+        assert xsum.check_state_image(encode_state(A, cnt, fl).tobytes())
+
+    def bad(mut):
+        img = encode_state(12345 << 700, 77)
+        mut(img)
+        return not xsum.check_state_image(img.tobytes())
+
+    def setd(j, v):
+        def f(img):
+            img[24 + 8 * j:32 + 8 * j] = np.array([v], dtype=np.int64).view(np.uint8)
+        return f
+
+    assert bad(lambda i: i.__setitem__(0, 0))                               # magic
+    assert bad(lambda i: i.__setitem__(4, 2))                               # version
+    assert bad(lambda i: i.__setitem__(6, 51))                              # radix
+    assert bad(lambda i: i.__setitem__(7, 44))                              # digit count
+    assert bad(lambda i: i.__setitem__(12, 1))                              # reserved word
+    assert bad(lambda i: i.__setitem__(383, 1))                             # padding
+    assert bad(lambda i: i.__setitem__(9, 1))                               # unknown flag bit 256
+    assert bad(lambda i: i.__setitem__(23, 0x80))                           # count >= 2^63
+    assert bad(setd(3, R))                                                  # |digit| > R-1
+    assert bad(setd(40, -R))
+    assert bad(setd(41, (1 << 29) + 1))                                     # top digit bound
+    assert not bad(setd(3, R - 1)) and not bad(setd(3, -(R - 1))) and not bad(setd(41, -(1 << 29)))
+    assert not xsum.check_state_image(b"\0" * 383)
+
+
 def test_two_rank_gloo_state_exchange():
     """world_size 2: every rank receives every rank's state image; merging the gathered
     images (decoded here) gives the exact sum of the whole input."""

@@ -18,6 +18,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 # name -> extra nvcc defines
 VARIANTS = {
     "product": [],
+    "base": [],        # build this one from another checkout of the sources for same-box A/B
     # examples of compile-time knobs (see the kernels): register-buffer depth of each kernel
     "acc_nb4": ["-DXS_ACC_NB=4"],
     "seg_nb4": ["-DXS_SEG_NB=4"],

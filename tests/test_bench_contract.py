@@ -38,6 +38,20 @@ def test_reference_arm_nonzero_rank_exits_quietly():
     assert out.returncode == 0 and out.stdout.strip() == ""
 
 
+def test_clock_rejection_rule():
+    """Timing rules: hw_slowdown / hw_thermal_slowdown / sw_thermal_slowdown, or SM clocks far
+    below max with no reason (a leftover lock), reject the timed region; sw_power_cap does not."""
+    sys.path.insert(0, ROOT)
+    import bench
+    ok = {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": [], "samples": 20}
+    assert not bench.clocks_rejected(ok)
+    assert not bench.clocks_rejected(dict(ok, sm_mhz=1560, reasons=["sw_power_cap"]))
+    for r in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"):
+        assert bench.clocks_rejected(dict(ok, reasons=[r]))
+    assert bench.clocks_rejected(dict(ok, sm_mhz=1000))
+    assert not bench.clocks_rejected(dict(ok, samples=0, sm_mhz=None))
+
+
 def test_graft_entry_has_build_and_smoke():
     sys.path.insert(0, ROOT)
     import __graft_entry__ as g

@@ -188,8 +188,10 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
 
 // Fast path for equal segments whose starts are 16-B aligned and whose length is a multiple
 // of one warp tile (256 doubles), e.g. config 5: a warp's tiles form one continuous stream
-// across its segments, prefetched three tiles ahead with rotating register buffers, so the
+// across its segments, loaded SEG_NB - 1 tiles ahead into rotating register buffers, so the
 // per-segment epilogue runs while the next segment's first loads are already in flight.
+// (profiles/r01_c5_diagnosis.txt: deeper buffers, dedicated epilogue warps and 128-bit
+// column-sum loads were measured and are not faster.)
 constexpr uint32_t SEG_TILE = 32 * SEG_U * 2;   // doubles per warp tile
 #ifndef XS_SEG_NB
 #define XS_SEG_NB 2   // streaming path needs tiles-per-segment % NB == 0; c5: NB=2 597, NB=4 585 G/s

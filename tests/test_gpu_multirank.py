@@ -122,3 +122,55 @@ def test_fused_allreduce_single_rank_world():
     res, _ = acc.sum_allreduce(d, ptrs2.data_ptr(), 0, 2, 1)
     r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
     assert r.flags & xsum.F_PEER_TIMEOUT
+
+
+def _symm_rank(port: int, q):
+    import torch
+    import torch.distributed as tdist
+
+    import oracle
+    import paper_1605_05436_b200 as xsum
+    import synth
+    from paper_1605_05436_b200 import dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        x = synth.gen.generate("c2", 11, 1_000_003)
+        ref, limbs = oracle.exact_sum(x)
+        d = torch.from_numpy(x).cuda()
+        pe = dist.PeerExchange(torch.device("cuda", 0))      # torch symmetric memory + rendezvous
+        acc = xsum.Accumulator()
+        ok = []
+        for _ in range(3):                                     # consecutive epochs on the same buffers
+            res, canon = pe.sum(d, acc, canon=True)
+            r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+            ok.append(r.bits == ref.bits and r.flags == ref.flags and
+                      bool((canon.cpu().numpy().view("u8") == limbs).all()))
+        # the NCCL fallback path on the same group
+        tot = xsum.Accumulator()
+        r2 = xsum.Result.from_bytes(dist.exact_sum_distributed(d, xsum.Accumulator(), tot).cpu().numpy().tobytes())
+        ok.append(r2.bits == ref.bits and r2.flags == ref.flags)
+        q.put(("ok", ok))
+    except Exception as e:  # noqa: BLE001
+        q.put(("error", repr(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_exchange_symmetric_memory_nccl_world1():
+    """The bench's N > 1 setup on the real stack: an NCCL process group, dist.PeerExchange
+    (torch symmetric memory allocation + rendezvous, device pointer table) and the fused
+    one-launch step through it, three epochs, plus the NCCL all-gather path; world size 1 (one
+    GPU), so no kernel waits on another process."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_symm_rank, args=(29700 + os.getpid() % 1000, q))
+    p.start()
+    kind, val = q.get(timeout=300)
+    p.join(timeout=60)
+    assert kind == "ok", val
+    assert all(val), val

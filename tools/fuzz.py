@@ -5,7 +5,7 @@
 Each case draws an input format, a size (log-uniform up to 2^22), a base misalignment, a content
 mix (uniform bit patterns, a narrow exponent band, cancelling pairs, sprinkled NaN/Inf, zeros and
 subnormals) and an API (fused sum, chunked accumulate, host streaming, shard merge, sparse image
-round trip, equal / CSR segments), and compares value bits, binary32 bits, flags and the canonical
+round trip, equal / CSR segments, checkpoint / resume), and compares value bits, binary32 bits, flags and the canonical
 image with the oracle. Prints one line per failure (with the case seed) and a summary."""
 from __future__ import annotations
 
@@ -81,7 +81,13 @@ def one_case(seed: int) -> str | None:
     off = int(rng.integers(0, 8))
     b = content(rng, fmt, n)
     d = to_dev(b, fmt, off)
-    api = rng.integers(0, 6)
+    api = rng.integers(0, 7)
+    if api == 6:                                          # checkpoint / resume mid-way
+        c = int(rng.integers(0, n + 1))
+        a = xs.Accumulator().add(d[:c])
+        res, canon = xs.Accumulator().load_state(a.save_state()).add(d[c:]).exact()
+        r, limbs = ref(fmt, b)
+        return None if same(res, canon, r, limbs) else f"{fmt} n={n} checkpoint at {c}"
     if api == 0:
         res, canon = xs.exact_sum(d)
         r, limbs = ref(fmt, b)

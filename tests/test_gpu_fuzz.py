@@ -1,6 +1,6 @@
 """A short randomized differential run (tools/fuzz.py): random formats, sizes, alignments, content
-mixes and APIs against the oracle, fixed seeds (reproducible). profiles/r01_fuzz.txt records a
-longer run (39467 cases, 0 failures)."""
+mixes and APIs against the oracle, fixed seeds (reproducible). profiles/r01_fuzz.txt records
+longer runs (over 300k cases on the product and checked builds, 0 failures)."""
 from __future__ import annotations
 
 import os

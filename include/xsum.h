@@ -335,6 +335,27 @@ XSUM_API const char *xsum_status_str(xsum_status s);
 /* Number of kernel launches the library enqueued since load (for bench.py's gpu_launches). */
 XSUM_API uint64_t xsum_launch_count(void);
 
+/* Exact reduction along a strided dimension (a reproducible sum over one
+ * tensor dimension without a transposing copy): d_x is a contiguous [outer][len][inner] array of
+ * `dtype` elements (XSUM_DT_*; element-size aligned); for every o < outer, i < inner
+ *   d_out64[o*inner + i] and/or d_out32[o*inner + i] = RN-even (binary64 / binary32) of the exact
+ *   sum over r < len of d_x[(o*len + r)*inner + i]   (len = 0 gives +0.0),
+ * d_flags[o*inner + i] (optional) the XSUM_F_* flags of that sum (NaN/Inf seen, and OVERFLOW /
+ * INEXACT for the binary64 rounding, OVERFLOW32 / INEXACT32 for the binary32 one, per the outputs
+ * requested). Specials follow R10 (NaN, +Inf, -Inf). Each lane sums one fibre in its own shared
+ * superaccumulator and rounds it itself. When the fibres
+ * cannot fill the GPU the rows are split into parts whose exact partial superaccumulators are
+ * merged by a second launch; that needs d_work of xsum_sum_strided_work_bytes(...) bytes
+ * (8-B aligned, caller-owned, no initialization); with a smaller or NULL d_work the split is not
+ * used (same results, fewer SMs busy). inner = 1 is served by the segment kernels
+ * (xsum_sum_segments_ex; its flags carry both roundings' bits). At least one of d_out64 /
+ * d_out32. Stream-ordered, no host synchronization. Errors: XSUM_EINVAL (bad dtype, no output,
+ * misalignment, sizes overflowing 2^63), XSUM_ECUDA. */
+XSUM_API size_t xsum_sum_strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int device);
+XSUM_API xsum_status xsum_sum_strided(const void *d_x, int dtype, uint64_t outer, uint64_t len, uint64_t inner,
+                                      double *d_out64, float *d_out32, uint32_t *d_flags, void *d_work,
+                                      size_t work_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,7 +48,7 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
            "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex", "xsum_save_state",
-           "xsum_check_state_image", "xsum_load_state")
+           "xsum_check_state_image", "xsum_load_state", "xsum_sum_strided_work_bytes", "xsum_sum_strided")
 
 
 class XsumError(RuntimeError):
@@ -97,6 +97,8 @@ def lib() -> ctypes.CDLL:
             "xsum_accumulate_host_ex": ([p, p, u64, i32, p, sz, p], i32),
             "xsum_save_state": ([p, p, p], i32), "xsum_check_state_image": ([p], i32),
             "xsum_load_state": ([p, p, p], i32),
+            "xsum_sum_strided_work_bytes": ([u64, u64, u64, i32], sz),
+            "xsum_sum_strided": ([p, i32, u64, u64, u64, p, p, p, p, sz, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -537,6 +539,20 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
     if x.dim() == 0:
         raise ValueError("exact_sum_dim needs a tensor with at least one dimension")
     d = dim % x.dim()
+    f64 = x.dtype == torch.float64
+    outer = 1
+    for s_ in x.shape[:d]:
+        outer *= s_
+    inner = 1
+    for s_ in x.shape[d + 1:]:
+        inner *= s_
+    length = x.shape[d]
+    out_shape = tuple(x.shape[:d]) + tuple(x.shape[d + 1:])
+    if inner > 1 and x.is_contiguous():
+        # strided fibres summed in place (xsum_sum_strided): no transposing copy
+        o64, o32, _ = _strided(x, outer, length, inner, f64, not f64)
+        out = (o64 if f64 else o32).reshape(out_shape)
+        return out.unsqueeze(d) if keepdim else out
     xt = x.movedim(d, -1).contiguous()
     seg = xt.shape[-1]
     out_shape = xt.shape[:-1]
@@ -550,6 +566,36 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
         out, _, _ = _segments(xt.reshape(-1), nseg, seg, None, False, False)
         out = out.reshape(out_shape)
     return out.unsqueeze(d) if keepdim else out
+
+
+def sum_strided(x, outer: int, length: int, inner: int, out64: bool = True, out32: bool = False, flags: bool = False):
+    """Exact sums over the middle axis of a contiguous CUDA tensor viewed as [outer][length][inner]
+    (xsum_sum_strided): returns (binary64 values or None, binary32 values or None, flags or None),
+    each of outer*inner elements."""
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or not x.is_contiguous() or \
+            x.dtype not in (torch.float64, torch.float32, torch.float16, torch.bfloat16):
+        raise TypeError("expected a contiguous float64 / float32 / float16 / bfloat16 CUDA tensor")
+    if outer * length * inner != x.numel():
+        raise ValueError("outer * length * inner must equal x.numel()")
+    return _strided(x, outer, length, inner, out64, out32, flags)
+
+
+def _strided(x, outer, length, inner, out64, out32, flags=False):
+    torch = _torch()
+    F = outer * inner
+    o64 = torch.empty(F, dtype=torch.float64, device=x.device) if out64 else None
+    o32 = torch.empty(F, dtype=torch.float32, device=x.device) if out32 else None
+    fl = torch.empty(F, dtype=torch.int32, device=x.device) if flags else None
+    wb = int(lib().xsum_sum_strided_work_bytes(outer, length, inner, x.device.index))
+    work = torch.empty(wb, dtype=torch.uint8, device=x.device) if wb else None
+    xp = x if x.numel() else torch.zeros(8, dtype=x.dtype, device=x.device)
+    _check("xsum_sum_strided", lib().xsum_sum_strided(
+        xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], outer, length, inner,
+        o64.data_ptr() if o64 is not None else None, o32.data_ptr() if o32 is not None else None,
+        fl.data_ptr() if fl is not None else None, work.data_ptr() if work is not None else None, wb,
+        _stream_ptr(x.device)))
+    return o64, o32, fl
 
 
 def _segments(x, nseg, seg_len, offsets, canon, flags):

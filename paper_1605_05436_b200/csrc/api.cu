@@ -532,4 +532,30 @@ xsum_status xsum_sum_segments_ex(const void* d_x, int dtype, uint64_t nseg, uint
     return e == cudaSuccess ? XSUM_OK : XSUM_ECUDA;
 }
 
+size_t xsum_sum_strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int device) {
+    if (inner <= 1) return 0;
+    return xs::strided_work_bytes(outer, len, inner, sms_of(device));
+}
+
+xsum_status xsum_sum_strided(const void* d_x, int dtype, uint64_t outer, uint64_t len, uint64_t inner,
+                             double* d_out64, float* d_out32, uint32_t* d_flags, void* d_work, size_t work_bytes,
+                             void* stream) {
+    if (dtype < XSUM_DT_F64 || dtype > XSUM_DT_BF16) return XSUM_EINVAL;
+    if (!d_out64 && !d_out32) return XSUM_EINVAL;
+    if ((d_out64 && !aligned(d_out64, 8)) || (d_out32 && !aligned(d_out32, 4)) || (d_flags && !aligned(d_flags, 4)) ||
+        (d_work && !aligned(d_work, 8)))
+        return XSUM_EINVAL;
+    if (outer == 0 || inner == 0) return XSUM_OK;
+    if (outer > kMaxCount / inner || (len && outer * inner > kMaxCount / len)) return XSUM_EINVAL;
+    const uintptr_t esz = dtype == XSUM_DT_F64 ? 8 : (dtype == XSUM_DT_F32 ? 4 : 2);
+    if (len && (!d_x || !aligned(d_x, esz))) return XSUM_EINVAL;
+    if (inner == 1)                                 // contiguous fibres: the segment kernels
+        return xsum_sum_segments_ex(d_x, dtype, outer, len, nullptr, d_out64, d_out32, nullptr, d_flags, stream);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
+    const xs::StrOut o{d_out64, d_out32, d_flags};
+    return xs::sum_strided(d_x, dtype, outer, len, inner, o, d_work, work_bytes, sms_of(dev),
+                           static_cast<cudaStream_t>(stream)) == cudaSuccess ? XSUM_OK : XSUM_ECUDA;
+}
+
 }  // extern "C"

@@ -134,6 +134,16 @@ struct SegOut {
 
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
                          int num_sms, cudaStream_t s);
+// strided reductions (K10, strided.cu): x as [outer][len][inner], out[o*inner + i]
+struct StrOut {
+    double* out64;
+    float* out32;
+    uint32_t* flags;
+};
+uint32_t strided_parts(uint64_t outer, uint64_t len, uint64_t inner, int num_sms);
+size_t strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int num_sms);
+cudaError_t sum_strided(const void* x, int dtype, uint64_t outer, uint64_t len, uint64_t inner, const StrOut& o,
+                        void* work, size_t work_bytes, int num_sms, cudaStream_t s);
 // binary32 / binary16 / bfloat16 elements (dtype XSUM_DT_F32 / F16 / BF16), equal or CSR segments
 cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                const SegOut& o, int num_sms, cudaStream_t s);

@@ -26,6 +26,9 @@ VARIANTS = {
     "seg_u2nb8": ["-DXS_SEG_U=2", "-DXS_SEG_NB=8"],
     "seg_u1nb8": ["-DXS_SEG_U=1", "-DXS_SEG_NB=8"],
     "seg_u1nb16": ["-DXS_SEG_U=1", "-DXS_SEG_NB=16"],
+    "str_nb3": ["-DXS_STR_NB=3"],
+    "str_nb6": ["-DXS_STR_NB=6"],
+    "str_u4nb8": ["-DXS_STR_UNR=4", "-DXS_STR_NB=8"],
     "exp_seg_noepi": ["-DXS_EXP_SEG_NOEPI"],
     "exp_seg_noacc": ["-DXS_EXP_SEG_NOACC"],
     "h16_nb2": ["-DXS_H16_NB=2"],
@@ -63,12 +66,24 @@ elif {cfg!r} in ("f16", "bf16"):
     x = torch.randint(-32768, 32767, (1 << 30,), dtype=torch.int16, device="cuda", generator=g)
     em = 0x7C00 if {cfg!r} == "f16" else 0x7F80
     x = torch.where((x & em) == em, x ^ 0x400, x).view(torch.float16 if {cfg!r} == "f16" else torch.bfloat16)
+elif {cfg!r}.startswith("str"):
+    base = synth.device_generate("c2")
+    shp = {{"str64": (4096, 65536), "str1m": (1 << 20, 256), "str3d": (64, 4096, 1024)}}.get({cfg!r}, (4096, 65536))
+    x = base.reshape(shp)
+    if {cfg!r} == "strbf16":
+        x = synth.device_bits("c2bf16").reshape(shp)
+    class _D:
+        def sum(self, x):
+            global seg_v
+            seg_v = xsum.exact_sum_dim(x, 1 if x.dim() == 3 else 0)
+            return xsum_res, None
+    xsum_res = xsum.Accumulator().sum(base[:1024])[0]
 elif {cfg!r} == "c5csr":
     x = synth.device_generate("c5csr")
     csr = synth.csr_offsets("c5csr", device="cuda")
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
-acc = xsum.Accumulator()
+acc = _D() if {cfg!r}.startswith("str") else xsum.Accumulator()
 if {cfg!r} == "c5csr":
     class _C:
         def sum(self, x):
@@ -94,7 +109,7 @@ torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
 import hashlib
-check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr")) else hex(r.bits)
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr")) or {cfg!r}.startswith("str") else hex(r.bits)
 print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)

@@ -136,8 +136,12 @@ __device__ __forceinline__ uint64_t lane_round(const LaneTop& t, int prec, int e
     } else {
         if (q == (1ull << prec)) { q >>= 1; sh += 1; }
         const int Eb = sh - emin + 1;
-        if (Eb >= emax) { bits = (uint64_t)emax << (prec - 1); rf |= is64 ? XSUM_F_OVERFLOW : XSUM_F_OVERFLOW32; }
-        else bits = ((uint64_t)Eb << (prec - 1)) | (q - (1ull << (prec - 1)));
+        if (Eb >= emax) {                          // +-Inf: never the exact value (finalize_warp's dir = 1)
+            bits = (uint64_t)emax << (prec - 1);
+            rf |= is64 ? (XSUM_F_OVERFLOW | XSUM_F_INEXACT) : (XSUM_F_OVERFLOW32 | XSUM_F_INEXACT32);
+        } else {
+            bits = ((uint64_t)Eb << (prec - 1)) | (q - (1ull << (prec - 1)));
+        }
     }
     if (g || sticky) rf |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
     if (t.sign) bits |= is64 ? (1ull << 63) : 0x80000000ull;

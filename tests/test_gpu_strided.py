@@ -129,6 +129,7 @@ def test_strided_rounding_edges(xs):
         [1.7976931348623157e308, 2.0 ** 970], [1.7976931348623157e308, 2.0 ** 969], [-0.0, -0.0],
         [2.0 ** 104, -1.0], [-(2.0 ** 104), 1.0], [2.0 ** -1074, 2.0 ** -1074], [2.0 ** -150, 2.0 ** -160],
         [-(2.0 ** -150)], [3.4028235677973366e38, 1.0e30], [1.0 + 2.0 ** -23, 2.0 ** -24, 2.0 ** -60],
+        [2.0 ** 127, 2.0 ** 127], [-(2.0 ** 128)],               # exact sums that overflow binary32
     ]
     length = max(len(v) for v in vals)
     inner = len(vals)

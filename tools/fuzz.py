@@ -5,7 +5,7 @@
 Each case draws an input format, a size (log-uniform up to 2^22), a base misalignment, a content
 mix (uniform bit patterns, a narrow exponent band, cancelling pairs, sprinkled NaN/Inf, zeros and
 subnormals) and an API (fused sum, chunked accumulate, host streaming, shard merge, sparse image
-round trip, equal / CSR segments, checkpoint / resume), and compares value bits, binary32 bits, flags and the canonical
+round trip, equal / CSR segments, checkpoint / resume, strided reductions), and compares value bits, binary32 bits, flags and the canonical
 image with the oracle. Prints one line per failure (with the case seed) and a summary."""
 from __future__ import annotations
 
@@ -81,7 +81,25 @@ def one_case(seed: int) -> str | None:
     off = int(rng.integers(0, 8))
     b = content(rng, fmt, n)
     d = to_dev(b, fmt, off)
-    api = rng.integers(0, 7)
+    api = rng.integers(0, 8)
+    if api == 7 and n:                                    # strided reduction [outer][len][inner]
+        inner = int(rng.integers(2, 80))
+        outer = int(rng.integers(1, 4))
+        length = n // (outer * inner)
+        if length == 0:
+            return None
+        m = outer * length * inner
+        o64, o32, fl = xs.sum_strided(d[:m], outer, length, inner, out64=True, out32=True, flags=True)
+        v64 = o64.cpu().numpy().view(np.uint64)
+        v32 = o32.cpu().numpy().view(np.uint32)
+        f = fl.cpu().numpy().view(np.uint32)
+        a3 = b[:m].reshape(outer, length, inner)
+        for k in range(outer * inner):
+            o, i = divmod(k, inner)
+            r, _ = ref(fmt, np.ascontiguousarray(a3[o, :, i]))
+            if (int(v64[k]), int(v32[k]), int(f[k])) != (r.bits, r.bits_f32, r.flags & 0xDF):
+                return f"{fmt} strided {outer}x{length}x{inner} fibre {k}"
+        return None
     if api == 6:                                          # checkpoint / resume mid-way
         c = int(rng.integers(0, n + 1))
         a = xs.Accumulator().add(d[:c])

@@ -529,9 +529,10 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
     """Exact reduction of a CUDA tensor along one dimension: every output
     element is the correctly rounded (RN-even) sum of its fibre, independent of order - a
     reproducible torch.sum(x, dim). float64 input gives float64, float32 / float16 / bfloat16
-    input the float32 rounding of the exact sum. The fibres are laid out as equal contiguous
-    segments (a movedim + contiguous copy when `dim` is not the last dimension) and summed by
-    xsum_sum_segments_ex, one warp per fibre."""
+    input the float32 rounding of the exact sum. A contiguous tensor reduced over a non-last
+    dimension goes to xsum_sum_strided (no copy); otherwise the fibres are laid out as equal
+    contiguous segments (a movedim + contiguous copy for non-contiguous inputs) and summed by
+    xsum_sum_segments_ex (one warp per fibre; one lane per fibre for fibres of <= 256)."""
     torch = _torch()
     if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype not in (torch.float64, torch.float32,
                                                                            torch.float16, torch.bfloat16):

@@ -330,6 +330,8 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
 
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
                          int num_sms, cudaStream_t s) {
+    if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
+        return sum_segments_lanes(x, XSUM_DT_F64, nseg, seg_len, o, num_sms, s);
     static unsigned long long smem_set = 0, smem_set_u = 0;
     if (cudaError_t e = ensure_smem(k_segments, SEG_SMEM, smem_set)) return e;
     if (cudaError_t e = ensure_smem(k_segments_uniform, SEG_SMEM, smem_set_u)) return e;

@@ -1,0 +1,198 @@
+// K11: many short equal segments (SURVEY.md §8(f) f1 "batched exact sums"): one LANE per
+// segment. With one warp per segment (K6/K9), a segment of a few dozen elements still pays the
+// whole warp epilogue (column combine, carry resolution, rounding: ~800 warp instructions);
+// here every lane owns one segment and its private 42-digit shared-memory column (K2's lane
+// column), reads the segment's elements itself and canonicalizes and rounds
+// its own column (one thread; lane_round.cuh) - 32 segments per warp, no
+// cross-lane step at all. The lanes of a warp read 32 consecutive segments, so a warp's loads
+// cover one contiguous span of 32*len elements; loads allocate in L1, where the neighbouring
+// bytes of a sector wait for the lane's next load.
+#include <cuda_runtime.h>
+
+#include "lane_round.cuh"
+#include "xsum_device.cuh"
+#include "xsum_kernels.h"
+
+namespace xs {
+
+constexpr int SL_WARPS = 16;
+constexpr size_t SL_SMEM = (size_t)SL_WARPS * D * 32 * sizeof(int64_t);
+
+// L1-allocating read-only loads (the lane revisits the rest of each sector on its next loads)
+__device__ __forceinline__ uint4 ld_v4_ca(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+template <int DT> struct SlLd;
+template <> struct SlLd<XSUM_DT_F64> {
+    using T = double;
+    __device__ static __forceinline__ uint2 load(const T* p) {
+        uint2 v;
+        asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+        return v;
+    }
+};
+template <> struct SlLd<XSUM_DT_F32> {
+    using T = float;
+    __device__ static __forceinline__ uint2 load(const T* p) {
+        uint32_t b;
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(b) : "l"(p));
+        return widen(__uint_as_float(b));
+    }
+};
+template <> struct SlLd<XSUM_DT_F16> {
+    using T = uint16_t;
+    __device__ static __forceinline__ uint2 load(const T* p) {
+        unsigned short b;
+        asm volatile("ld.global.nc.b16 %0, [%1];" : "=h"(b) : "l"(p));
+        return widen(__half2float(__ushort_as_half(b)));
+    }
+};
+template <> struct SlLd<XSUM_DT_BF16> {
+    using T = uint16_t;
+    __device__ static __forceinline__ uint2 load(const T* p) {
+        unsigned short b;
+        asm volatile("ld.global.nc.b16 %0, [%1];" : "=h"(b) : "l"(p));
+        return widen(__uint_as_float((uint32_t)b << 16));
+    }
+};
+
+// Regularize digits [lo, hi] of a lane column (the only ones this segment touched; digits
+// outside are zero), carrying into hi + 1; returns the new top of the touched range. Same split
+// as regularize_column (balanced carry); the window's top digit is not split.
+__device__ __forceinline__ int lane_regularize_range(int64_t* col, int lo, int hi) {
+    int64_t cin = 0;
+    const int last = hi < D - 1 ? hi : D - 2;
+    for (int j = lo; j <= last; ++j) {
+        const int64_t y = col[j * 32];
+        const int64_t c = balanced_carry(y);
+        col[j * 32] = y - (c << W) + cin;
+        cin = c;
+    }
+    col[(last + 1) * 32] += cin;
+    return last + 1;
+}
+
+// Round the lane's regularized column (segment s of `count` elements) into the segment outputs:
+// both roundings and the flags exactly as finalize_warp reports them, and the canonical image.
+__device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
+                                                   int hi) {
+    const LaneTop t = lane_canonical_top(col, lo, hi);
+    uint32_t rf = 0;
+    uint64_t b64 = lane_round(t, 53, 0, 2047, true, rf);
+    uint32_t b32 = (uint32_t)lane_round(t, 24, 925, 255, false, rf);
+    const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf;
+    if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
+        b64 = 0x7FF8000000000000ull; b32 = 0x7FC00000u;
+    } else if (fl & XSUM_F_PINF) {
+        b64 = 0x7FF0000000000000ull; b32 = 0x7F800000u;
+    } else if (fl & XSUM_F_NINF) {
+        b64 = 0xFFF0000000000000ull; b32 = 0xFF800000u;
+    }
+    if (o.out) o.out[s] = __longlong_as_double((long long)b64);
+    if (o.out32) o.out32[s] = __uint_as_float(b32);
+    if (o.flags) o.flags[s] = fl;
+    if (o.canon) lane_canon_image(col, t.m, t.sign, o.canon + s * XSUM_CANON_LIMBS);
+}
+
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(SL_WARPS * 32, 1)
+k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint64_t len, SegOut o, uint32_t one) {
+    using L = SlLd<DT>;
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t groups = (nseg + 31) / 32;
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    for (uint64_t g = (uint64_t)blockIdx.x * SL_WARPS + warp; g < groups; g += (uint64_t)gridDim.x * SL_WARPS) {
+        const uint64_t s = g * 32 + lane;
+        if (s >= nseg) continue;
+        uint32_t flags = 0;
+#ifdef XS_SL_FULL                                    // A/B knob: always the whole column
+        int lo = 0, hi = D - 1;
+#else
+        int lo = D, hi = -1;                         // touched digit range of this segment
+#endif
+        auto add = [&](uint32_t xlo, uint32_t xhi) {
+            Chunks c = decompose(xlo, xhi, one);
+            if (spec_hit(c.spec)) { flags |= special_flags(xlo, xhi); return; }
+            column_add(col, c, one);
+#ifndef XS_SL_FULL
+            lo = min(lo, (int)c.i);
+            hi = max(hi, (int)c.i + 1);
+#endif
+        };
+        const typename L::T* p = x + s * len;
+        uint64_t r = 0;
+        int since = 0;
+        auto flush = [&]() {
+            if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
+            since = 0;
+        };
+        if (VEC) {                                   // binary64, even length, 16-B aligned rows
+            const uint4* pv = reinterpret_cast<const uint4*>(p);
+            for (; r + 8 <= len; r += 8) {
+                uint4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = ld_v4_ca(pv + r / 2 + u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    add(v[u].x, v[u].y);
+                    add(v[u].z, v[u].w);
+                }
+                since += 8;
+                if (since > FLUSH_ELEMS - 8) flush();
+            }
+        } else {
+            for (; r + 8 <= len; r += 8) {
+                uint2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = L::load(p + r + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) add(v[u].x, v[u].y);
+                since += 8;
+                if (since > FLUSH_ELEMS - 8) flush();
+            }
+        }
+        for (; r < len; ++r) {                       // < 8 left: within the window
+            uint2 v = L::load(p + r);
+            add(v.x, v.y);
+        }
+        flush();
+        if (hi < 0) lo = hi = 0;
+        lane_store_segment(col, flags, o, s, lo, hi);
+        for (int j = lo; j <= hi; ++j) col[j * 32] = 0;   // the rest of the column is still zero
+    }
+}
+
+template <int DT, bool VEC>
+static cudaError_t launch_lanes(const void* x, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
+                                cudaStream_t s) {
+    static unsigned long long done = 0;
+    if (cudaError_t e = ensure_smem(k_segments_lanes<DT, VEC>, SL_SMEM, done)) return e;
+    const uint64_t groups = (nseg + 31) / 32;
+    const uint64_t want = (groups + SL_WARPS - 1) / SL_WARPS;
+    const unsigned g = (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
+    k_segments_lanes<DT, VEC><<<g, SL_WARPS * 32, SL_SMEM, s>>>(static_cast<const typename SlLd<DT>::T*>(x), nseg,
+                                                                len, o, 1u);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t sum_segments_lanes(const void* x, int dtype, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
+                               cudaStream_t s) {
+    if (nseg == 0) return cudaSuccess;
+    switch (dtype) {
+        case XSUM_DT_F64:
+            if (len % 2 == 0 && ((uintptr_t)x & 15) == 0)
+                return launch_lanes<XSUM_DT_F64, true>(x, nseg, len, o, num_sms, s);
+            return launch_lanes<XSUM_DT_F64, false>(x, nseg, len, o, num_sms, s);
+        case XSUM_DT_F32: return launch_lanes<XSUM_DT_F32, false>(x, nseg, len, o, num_sms, s);
+        case XSUM_DT_F16: return launch_lanes<XSUM_DT_F16, false>(x, nseg, len, o, num_sms, s);
+        default: return launch_lanes<XSUM_DT_BF16, false>(x, nseg, len, o, num_sms, s);
+    }
+}
+
+}  // namespace xs

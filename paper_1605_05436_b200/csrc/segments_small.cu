@@ -488,6 +488,8 @@ static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, 
 
 cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                const SegOut& o, int num_sms, cudaStream_t s) {
+    if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
+        return sum_segments_lanes(x, dtype, nseg, seg_len, o, num_sms, s);
     switch (dtype) {
         case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s);
         case XSUM_DT_F16: return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s);

@@ -134,6 +134,14 @@ struct SegOut {
 
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
                          int num_sms, cudaStream_t s);
+// short equal segments, one lane per segment (K11, segments_lanes.cu); sum_segments and
+// sum_segments_small route equal segments of length <= SEG_LANES_MAX here
+#ifndef XS_SEG_LANES_MAX
+#define XS_SEG_LANES_MAX 256
+#endif
+constexpr uint64_t SEG_LANES_MAX = XS_SEG_LANES_MAX;
+cudaError_t sum_segments_lanes(const void* x, int dtype, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
+                               cudaStream_t s);
 // strided reductions (K10, strided.cu): x as [outer][len][inner], out[o*inner + i]
 struct StrOut {
     double* out64;

@@ -1,0 +1,105 @@
+"""GPU parity of K11 (one lane per segment; equal segments of length <= 256, SURVEY.md §8(f) f1
+batched exact sums) in every input format: values (both roundings), flags and canonical images
+vs the oracle, across the dispatch threshold, with narrow and wide exponent ranges (the touched
+digit-range tracking), cancellation, specials, signed zeros and misaligned bases."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def xs():
+    import torch  # noqa: F401
+    import paper_1605_05436_b200 as xsum
+    xsum.build()
+    synth.build()
+    return xsum
+
+
+FMT = {"f64": (np.uint64, 0x7FF0000000000000, 64), "f32": (np.uint32, 0x7F800000, 32),
+       "f16": (np.uint16, 0x7C00, 16), "bf16": (np.uint16, 0x7F80, 16)}
+
+
+def data(fmt: str, n: int, seed: int, narrow: bool) -> np.ndarray:
+    ut, em, bits = FMT[fmt]
+    rng = np.random.default_rng(seed)
+    if fmt == "f64":
+        b = synth.gen.generate("c1" if narrow else "c2", seed, n).view(np.uint64).copy()
+    else:
+        b = rng.integers(0, 1 << bits, size=n, dtype=np.uint64).astype(ut)
+        if narrow:                                       # exponent field pinned to 3 values
+            t = {32: 23, 16: 10 if fmt == "f16" else 7}[bits]
+            e0 = {32: 120, 16: 12 if fmt == "f16" else 120}[bits]
+            e = rng.integers(e0, e0 + 3, size=n).astype(np.uint64)
+            b = ((b.astype(np.uint64) & np.uint64(~em & ((1 << bits) - 1))) | (e << np.uint64(t))).astype(ut)
+        fin = (b & ut(em)) == ut(em)
+        b[fin] ^= ut(em & ~(em << 1) & ((1 << bits) - 1))
+    k = rng.integers(0, n, size=max(1, n // 300))        # cancellation partners, zeros, specials
+    b[k] = b[(k + 1) % n] ^ ut(1 << (bits - 1))
+    z = rng.integers(0, n, size=max(1, n // 500))
+    b[z] = ut(1 << (bits - 1))
+    sp = rng.integers(0, n, size=max(1, n // 2000))
+    b[sp] = np.array([em, em | (1 << (bits - 1)), em | 1], dtype=np.uint64)[rng.integers(0, 3, size=sp.size)].astype(ut)
+    return b
+
+
+def to_dev(b: np.ndarray, fmt: str, off: int):
+    import torch
+    it = {"f64": torch.int64, "f32": torch.int32, "f16": torch.int16, "bf16": torch.int16}[fmt]
+    dt = {"f64": torch.float64, "f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[fmt]
+    nt = {"f64": np.int64, "f32": np.int32, "f16": np.int16, "bf16": np.int16}[fmt]
+    buf = torch.empty(b.size + 8, dtype=it, device="cuda")
+    t = buf[off:off + b.size]
+    t.copy_(torch.from_numpy(b.view(nt)))
+    return t.view(dt)
+
+
+def ref(fmt, seg):
+    if fmt == "f64":
+        return oracle.exact_sum(seg.view(np.float64))
+    if fmt == "f32":
+        return oracle.exact_sum(seg.view(np.float32))
+    return oracle.exact_sum(seg, fmt=fmt)
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32", "f16", "bf16"])
+@pytest.mark.parametrize("L", [1, 2, 3, 7, 8, 9, 33, 64, 255, 256, 257])
+@pytest.mark.parametrize("narrow", [True, False])
+def test_short_segments_vs_oracle(xs, fmt, L, narrow):
+    nseg = 100
+    b = data(fmt, nseg * L, 1000 + L, narrow)
+    off = L % 3                                          # misaligned bases too (scalar-load path)
+    vals, canon, flags = xs.sum_segments(to_dev(b, fmt, off), L, canon=True, flags=True)
+    v = vals.cpu().numpy()
+    v = v.view(np.uint64) if fmt == "f64" else v.view(np.uint32)
+    cn = canon.cpu().numpy().view(np.uint64)
+    fl = flags.cpu().numpy().view(np.uint32)
+    for s in range(nseg):
+        r, limbs = ref(fmt, b[s * L:(s + 1) * L])
+        want = r.bits if fmt == "f64" else r.bits_f32
+        assert int(v[s]) == want and int(fl[s]) == r.flags, (fmt, L, narrow, s)
+        assert (cn[s] == limbs).all(), (fmt, L, narrow, s)
+
+
+def test_short_segments_both_roundings(xs):
+    """xsum_sum_segments_ex with both outputs on short binary64 segments: the binary32 rounding of
+    each exact sum (one rounding) next to the binary64 one."""
+    import torch
+    L, nseg = 5, 1000
+    b = data("f64", L * nseg, 5, False)
+    d = to_dev(b, "f64", 0)
+    o64 = torch.empty(nseg, dtype=torch.float64, device="cuda")
+    o32 = torch.empty(nseg, dtype=torch.float32, device="cuda")
+    rc = xs.lib().xsum_sum_segments_ex(d.data_ptr(), 0, nseg, L, None, o64.data_ptr(), o32.data_ptr(), None, None,
+                                       torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    v64, v32 = o64.cpu().numpy().view(np.uint64), o32.cpu().numpy().view(np.uint32)
+    for s in range(nseg):
+        r, _ = ref("f64", b[s * L:(s + 1) * L])
+        assert (int(v64[s]), int(v32[s])) == (r.bits, r.bits_f32), s

@@ -26,6 +26,8 @@ VARIANTS = {
     "seg_u2nb8": ["-DXS_SEG_U=2", "-DXS_SEG_NB=8"],
     "seg_u1nb8": ["-DXS_SEG_U=1", "-DXS_SEG_NB=8"],
     "seg_u1nb16": ["-DXS_SEG_U=1", "-DXS_SEG_NB=16"],
+    "lanes0": ["-DXS_SEG_LANES_MAX=0"],
+    "sl_full": ["-DXS_SL_FULL"],
     "str_nb3": ["-DXS_STR_NB=3"],
     "str_nb6": ["-DXS_STR_NB=6"],
     "str_u4nb8": ["-DXS_STR_UNR=4", "-DXS_STR_NB=8"],

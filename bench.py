@@ -45,7 +45,7 @@ def parse():
     # c1..c5: BASELINE.json configs; c5csr / c2f32 / c2f16 / c2bf16: measurement workloads of the
     # NEXT rows (CSR segments, other input formats; synth/gen.py)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5csr", "c2f32", "c2f16",
-                                                         "c2bf16"])
+                                                         "c2bf16", "c2dim0", "c5s16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -70,6 +70,8 @@ def workload(cfg_name: str, world: int) -> dict:
         "c2f32": "c2f32: n=2^28 binary32, seed 6, uniform over the finite bit patterns",
         "c2f16": "c2f16: n=2^28 binary16, seed 7, uniform over the finite bit patterns",
         "c2bf16": "c2bf16: n=2^28 bfloat16, seed 8, uniform over the finite bit patterns",
+        "c2dim0": "c2dim0: c2's 2^28 doubles as a [4096, 65536] matrix, exact_sum_dim over dim 0 (65536 sums)",
+        "c5s16": "c5s16: 2^24 segments x 16 doubles, seed 10, exponent U[-200,200]",
     }[cfg_name]
     if cfg_name == "c4":
         n_total = cfg["n"]
@@ -280,9 +282,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     synth.build()
     wl = workload(args.config, world)
     cfg = wl["cfg"]
-    if world > 1 and cfg["kind"] in ("bits", "csr"):
+    if world > 1 and (cfg["kind"] in ("bits", "csr") or args.config in ("c2dim0", "c5s16")):
         raise SystemExit(f"--config {args.config} is a one-GPU measurement workload")
-    seg = args.config in ("c5", "c5csr")
+    seg = args.config in ("c5", "c5csr", "c5s16", "c2dim0")      # many results per step
     csr = None
     metric, unit = metric_unit(args.config)
 
@@ -326,6 +328,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     def step():
         if csr is not None:
             xsum.sum_segments_csr(x, csr)
+        elif cfg.get("op") == "dim0":
+            xsum.exact_sum_dim(x.view(cfg["shape"]), 0)
         elif seg:
             xsum.sum_segments(x, cfg["seg_len"])
         elif world == 1:
@@ -463,7 +467,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
                          "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
                                     "c2bf16": "k_accumulate_h16", "c5": "k_segments_uniform",
-                                    "c5csr": "k_segments"}.get(args.config, "k_accumulate"),
+                                    "c5csr": "k_segments", "c5s16": "k_segments_lanes",
+                                    "c2dim0": "k_sum_strided"}.get(args.config, "k_accumulate"),
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local,
                          "peak_source": peak_src, "read_probe_gbs": probe_gbs,
                          "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None},

@@ -53,6 +53,10 @@ CONFIGS.update({
     "c2f32": dict(kind="bits", fmt="f32", n=1 << 28, seed=6, st=0),
     "c2f16": dict(kind="bits", fmt="f16", n=1 << 28, seed=7, st=0),
     "c2bf16": dict(kind="bits", fmt="bf16", n=1 << 28, seed=8, st=0),
+    # f1 measurement workloads: c2's elements as a [4096, 65536] matrix reduced over dim 0 (K10,
+    # strided), and 2^24 segments of 16 doubles drawn like c5 with seed 10 (K11, one lane each)
+    "c2dim0": dict(kind="uniform", n=1 << 28, seed=2, st=0, lo=-1000, hi=1000, op="dim0", shape=(4096, 65536)),
+    "c5s16": dict(kind="segments", n=1 << 28, seed=10, st=0, lo=-200, hi=200, nseg=1 << 24, seg_len=16),
 })
 
 

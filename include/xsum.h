@@ -336,6 +336,17 @@ XSUM_API const char *xsum_status_str(xsum_status s);
 /* Number of kernel launches the library enqueued since load (for bench.py's gpu_launches). */
 XSUM_API uint64_t xsum_launch_count(void);
 
+/* xsum_sum_segments_ex with a work-balancing ticket: d_ticket (optional, 8-B aligned, caller-owned)
+ * is one 64-bit device word that must be ZERO when the call's work starts on `stream` (e.g. zeroed
+ * by a stream-ordered memset just before) and is left non-zero. With CSR offsets the warps then
+ * draw the next unclaimed segment from it atomically instead of taking the static order s,
+ * s + nw, ... - ragged lengths otherwise leave the busiest warp with well above the mean work
+ * (c5csr: 1.36x). Used for binary64 CSR segments; ignored otherwise. A ticket word must not be
+ * shared by calls whose work may overlap. Errors: as xsum_sum_segments_ex. */
+XSUM_API xsum_status xsum_sum_segments_ws(const void *d_x, int dtype, uint64_t nseg, uint64_t seg_len,
+                                          const uint64_t *d_offsets, double *d_out, float *d_out32,
+                                          uint64_t *d_canon, uint32_t *d_flags, void *d_ticket, void *stream);
+
 /* Exact reduction along a strided dimension (a reproducible sum over one
  * tensor dimension without a transposing copy): d_x is a contiguous [outer][len][inner] array of
  * `dtype` elements (XSUM_DT_*; element-size aligned); for every o < outer, i < inner

@@ -48,7 +48,8 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_accumulate_f16", "xsum_accumulate_bf16", "xsum_sum_f16", "xsum_sum_bf16",
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
            "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex", "xsum_save_state",
-           "xsum_check_state_image", "xsum_load_state", "xsum_sum_strided_work_bytes", "xsum_sum_strided")
+           "xsum_check_state_image", "xsum_load_state", "xsum_sum_strided_work_bytes", "xsum_sum_strided",
+           "xsum_sum_segments_ws")
 
 
 class XsumError(RuntimeError):
@@ -99,6 +100,7 @@ def lib() -> ctypes.CDLL:
             "xsum_load_state": ([p, p, p], i32),
             "xsum_sum_strided_work_bytes": ([u64, u64, u64, i32], sz),
             "xsum_sum_strided": ([p, i32, u64, u64, u64, p, p, p, p, sz, p], i32),
+            "xsum_sum_segments_ws": ([p, i32, u64, u64, p, p, p, p, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -606,10 +608,14 @@ def _segments(x, nseg, seg_len, offsets, canon, flags):
     cn = torch.empty((nseg, CANON_LIMBS), dtype=torch.int64, device=x.device) if canon else None
     fl = torch.empty(nseg, dtype=torch.int32, device=x.device) if flags else None
     xp = x if x.numel() else torch.zeros(8, dtype=x.dtype, device=x.device)
-    rc = lib().xsum_sum_segments_ex(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
+    # ragged binary64 segments: a zeroed ticket word (stream-ordered, torch's allocator) lets the
+    # warps balance the work dynamically (xsum_sum_segments_ws)
+    tk = torch.zeros(1, dtype=torch.int64, device=x.device) if offsets is not None and f64 else None
+    rc = lib().xsum_sum_segments_ws(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
                                     offsets.data_ptr() if offsets is not None else None,
                                     out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
                                     cn.data_ptr() if cn is not None else None,
-                                    fl.data_ptr() if fl is not None else None, _stream_ptr(x.device))
-    _check("xsum_sum_segments_ex", rc)
+                                    fl.data_ptr() if fl is not None else None,
+                                    tk.data_ptr() if tk is not None else None, _stream_ptr(x.device))
+    _check("xsum_sum_segments_ws", rc)
     return out, cn, fl

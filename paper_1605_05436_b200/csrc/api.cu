@@ -510,6 +510,14 @@ xsum_status xsum_sum_segments_csr(const double* d_x, const uint64_t* d_offsets, 
 xsum_status xsum_sum_segments_ex(const void* d_x, int dtype, uint64_t nseg, uint64_t seg_len,
                                  const uint64_t* d_offsets, double* d_out, float* d_out32, uint64_t* d_canon,
                                  uint32_t* d_flags, void* stream) {
+    return xsum_sum_segments_ws(d_x, dtype, nseg, seg_len, d_offsets, d_out, d_out32, d_canon, d_flags, nullptr,
+                                stream);
+}
+
+xsum_status xsum_sum_segments_ws(const void* d_x, int dtype, uint64_t nseg, uint64_t seg_len,
+                                 const uint64_t* d_offsets, double* d_out, float* d_out32, uint64_t* d_canon,
+                                 uint32_t* d_flags, void* d_ticket, void* stream) {
+    if (d_ticket && !aligned(d_ticket, 8)) return XSUM_EINVAL;
     if (dtype < XSUM_DT_F64 || dtype > XSUM_DT_BF16) return XSUM_EINVAL;
     if (nseg == 0) return XSUM_OK;
     if (!d_out && !d_out32 && !d_canon && !d_flags) return XSUM_EINVAL;
@@ -525,7 +533,7 @@ xsum_status xsum_sum_segments_ex(const void* d_x, int dtype, uint64_t nseg, uint
     cudaError_t e;
     if (dtype == XSUM_DT_F64)
         e = xs::sum_segments(static_cast<const double*>(d_x), nseg, d_offsets ? 0 : seg_len, d_offsets, o, sms_of(dev),
-                             static_cast<cudaStream_t>(stream));
+                             static_cast<cudaStream_t>(stream), static_cast<unsigned long long*>(d_ticket));
     else
         e = xs::sum_segments_small(d_x, dtype, nseg, d_offsets ? 0 : seg_len, d_offsets, o, sms_of(dev),
                                    static_cast<cudaStream_t>(stream));

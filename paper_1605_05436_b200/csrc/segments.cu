@@ -85,13 +85,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
     // Segment order: with a ticket counter, warps take the next unclaimed segment (dynamic
     // balancing: ragged CSR lengths made the static round-robin's busiest warp do 1.36x the mean
     // work on c5csr); without one, segments s, s + nw, ... (static).
-    auto next_seg = [&](uint64_t cur) -> uint64_t {
-        if (!ticket) return cur + nw;
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(ticket, 1ull);
-        return (uint64_t)__shfl_sync(FULL, t, 0);
-    };
-    uint64_t s = ticket ? next_seg(0) : (uint64_t)blockIdx.x * SEG_WARPS + warp;
+    uint64_t s = ticket ? seg_next(ticket, 0, nw, lane) : (uint64_t)blockIdx.x * SEG_WARPS + warp;
     if (s >= nseg) return;                                           // warp-uniform
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
@@ -104,7 +98,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
     }
     while (true) {
-        const uint64_t sn = next_seg(s);
+        const uint64_t sn = seg_next(ticket, s, nw, lane);
         bounds(sn, ob, oe);                                          // next segment's bounds, early
         uint32_t flags = 0, nspec = 0;
         const uint64_t nit = g.nit, nvec = g.nvec;
@@ -338,7 +332,7 @@ k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len
 }
 
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
-                         int num_sms, cudaStream_t s) {
+                         int num_sms, cudaStream_t s, unsigned long long* ticket) {
     if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
         return sum_segments_lanes(x, XSUM_DT_F64, nseg, seg_len, o, num_sms, s);
     static unsigned long long smem_set = 0, smem_set_u = 0;
@@ -352,20 +346,8 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     if (uniform)
         k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
     else {
-        // a stream-ordered 8-byte ticket counter for dynamic segment assignment (static order if
-        // the allocation fails)
-        unsigned long long* ticket = nullptr;
-        if (offsets && cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(*ticket), s) == cudaSuccess) {
-            if (cudaMemsetAsync(ticket, 0, sizeof(*ticket), s) != cudaSuccess) {
-                cudaFreeAsync(ticket, s);
-                ticket = nullptr;
-            }
-        } else {
-            (void)cudaGetLastError();
-            ticket = nullptr;
-        }
-        k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, o, ticket, 1u, 0xFFFFFFFFu);
-        if (ticket) cudaFreeAsync(ticket, s);
+        k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, o, offsets ? ticket : nullptr, 1u,
+                                                       0xFFFFFFFFu);
     }
     note_launch();
     return cudaGetLastError();

@@ -474,6 +474,14 @@ __device__ __noinline__ static xsum_result finalize_warp(int64_t a0, int64_t a1,
     return finalize_warp_inl(a0, a1, flags, count, canon, su, lane);
 }
 
+// The next segment of a warp: the next ticket (dynamic assignment) or cur + nw (static order).
+__device__ __forceinline__ uint64_t seg_next(unsigned long long* ticket, uint64_t cur, uint64_t nw, int lane) {
+    if (!ticket) return cur + nw;
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1ull);
+    return (uint64_t)__shfl_sync(FULL, t, 0);
+}
+
 // 128-bit streaming load of two doubles as four 32-bit halves (no L1 allocation; 256-B L2
 // prefetch: the best of the load flavours measured, profiles/r01_microbench.txt).
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {

@@ -132,8 +132,10 @@ struct SegOut {
     }
 };
 
+// ticket: optional zeroed 8-byte device counter; with CSR offsets the warps draw segments from
+// it (dynamic balancing of ragged lengths), else the static order s, s + nw, ...
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
-                         int num_sms, cudaStream_t s);
+                         int num_sms, cudaStream_t s, unsigned long long* ticket = nullptr);
 // short equal segments, one lane per segment (K11, segments_lanes.cu); sum_segments and
 // sum_segments_small route equal segments of length <= SEG_LANES_MAX here
 #ifndef XS_SEG_LANES_MAX

@@ -608,9 +608,9 @@ def _segments(x, nseg, seg_len, offsets, canon, flags):
     cn = torch.empty((nseg, CANON_LIMBS), dtype=torch.int64, device=x.device) if canon else None
     fl = torch.empty(nseg, dtype=torch.int32, device=x.device) if flags else None
     xp = x if x.numel() else torch.zeros(8, dtype=x.dtype, device=x.device)
-    # ragged binary64 segments: a zeroed ticket word (stream-ordered, torch's allocator) lets the
+    # ragged segments: a zeroed ticket word (stream-ordered, torch's allocator) lets the
     # warps balance the work dynamically (xsum_sum_segments_ws)
-    tk = torch.zeros(1, dtype=torch.int64, device=x.device) if offsets is not None and f64 else None
+    tk = torch.zeros(1, dtype=torch.int64, device=x.device) if offsets is not None else None
     rc = lib().xsum_sum_segments_ws(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
                                     offsets.data_ptr() if offsets is not None else None,
                                     out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),

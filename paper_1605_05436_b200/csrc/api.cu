@@ -536,7 +536,7 @@ xsum_status xsum_sum_segments_ws(const void* d_x, int dtype, uint64_t nseg, uint
                              static_cast<cudaStream_t>(stream), static_cast<unsigned long long*>(d_ticket));
     else
         e = xs::sum_segments_small(d_x, dtype, nseg, d_offsets ? 0 : seg_len, d_offsets, o, sms_of(dev),
-                                   static_cast<cudaStream_t>(stream));
+                                   static_cast<cudaStream_t>(stream), static_cast<unsigned long long*>(d_ticket));
     return e == cudaSuccess ? XSUM_OK : XSUM_ECUDA;
 }
 

@@ -174,7 +174,7 @@ __device__ __noinline__ void sseg_rescan(uint64_t* bins, int64_t* col, const uin
 template <class F>
 __global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
 k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
-                 SegOut o, uint32_t one) {
+                 SegOut o, unsigned long long* __restrict__ ticket, uint32_t one) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SSEG_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -203,7 +203,7 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
         g.nit = g.nvec / (32 * SU);
         return g;
     };
-    uint64_t s = (uint64_t)blockIdx.x * SSEG_WARPS + warp;
+    uint64_t s = ticket ? seg_next(ticket, 0, nw, lane) : (uint64_t)blockIdx.x * SSEG_WARPS + warp;
     if (s >= nseg) return;                                  // warp-uniform
 #pragma unroll
     for (int j = 0; j < F::COLS; ++j) col[j * 32] = 0;
@@ -216,6 +216,7 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
         for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
     }
     while (true) {
+        const uint64_t sn = seg_next(ticket, s, nw, lane);     // drawn early: its latency hides
         uint32_t flags = 0, since = 0, spec = 0, flushes = 0;
         const uint64_t nit = g.nit, nvec = g.nvec;
         const uint4* body = g.body;
@@ -260,7 +261,6 @@ k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
         if (__any_sync(FULL, spec == F::EM))            // rare: NaN/Inf patterns in this segment
             sseg_rescan<F>(bins, col, g.xs, g.head, body, nvec, g.tail, lane, flags, one);
         // prefetch the next segment, then close this one
-        const uint64_t sn = s + nw;
         const bool more = sn < nseg;
         const uint64_t len = g.len;
         if (more) {
@@ -336,7 +336,7 @@ constexpr size_t h16seg_smem() {
 template <class F>
 __global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
 k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
-               SegOut o, uint32_t one, uint32_t mone) {
+               SegOut o, unsigned long long* __restrict__ ticket, uint32_t one, uint32_t mone) {
     using S = H16Col<F>;
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SSEG_WARPS][64];
@@ -369,7 +369,7 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
         g.nit = g.nvec / (32 * SU);
         return g;
     };
-    uint64_t s = (uint64_t)blockIdx.x * SSEG_WARPS + warp;
+    uint64_t s = ticket ? seg_next(ticket, 0, nw, lane) : (uint64_t)blockIdx.x * SSEG_WARPS + warp;
     if (s >= nseg) return;                                  // warp-uniform
 #pragma unroll
     for (int j = 0; j < S::COLS; ++j) col[j * 32] = 0;
@@ -382,6 +382,7 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
         for (int u = 0; u < SU; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
     }
     while (true) {
+        const uint64_t sn = seg_next(ticket, s, nw, lane);     // drawn early: its latency hides
         uint32_t flags = 0, since = 0, flushes = 0;
         bool special = false;
         const uint64_t nit = g.nit, nvec = g.nvec;
@@ -433,7 +434,6 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
         }
         special |= h16_flush_col<F>(bins, col);
         if (__any_sync(FULL, special)) flags |= h16seg_classify<F>(g.xs, g.len, lane);   // rare
-        const uint64_t sn = s + nw;
         const bool more = sn < nseg;
         const uint64_t len = g.len;
         if (more) {
@@ -460,40 +460,41 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
 
 template <class F>
 static cudaError_t launch_h16seg(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
-                                 const SegOut& o, int num_sms, cudaStream_t s) {
+                                 const SegOut& o, int num_sms, cudaStream_t s, unsigned long long* ticket) {
     static unsigned long long smem_set = 0;
     if (cudaError_t e = ensure_smem(k_segments_h16<F>, h16seg_smem<F>(), smem_set)) return e;
     const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
     const uint64_t cap = (uint64_t)num_sms * 2;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     k_segments_h16<F><<<g, SSEG_WARPS * 32, h16seg_smem<F>(), s>>>(static_cast<const uint16_t*>(x), nseg, seg_len,
-                                                                    offsets, o, 1u, 0xFFFFFFFFu);
+                                                                    offsets, o, offsets ? ticket : nullptr, 1u,
+                                                                    0xFFFFFFFFu);
     note_launch();
     return cudaGetLastError();
 }
 
 template <class F>
 static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
-                                const SegOut& o, int num_sms, cudaStream_t s) {
+                                const SegOut& o, int num_sms, cudaStream_t s, unsigned long long* ticket) {
     static unsigned long long smem_set = 0;
     if (cudaError_t e = ensure_smem(k_segments_small<F>, sseg_smem<F>(), smem_set)) return e;
     const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
     const uint64_t cap = (uint64_t)num_sms * 2;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     k_segments_small<F><<<g, SSEG_WARPS * 32, sseg_smem<F>(), s>>>(static_cast<const uint8_t*>(x), nseg, seg_len,
-                                                                    offsets, o, 1u);
+                                                                    offsets, o, offsets ? ticket : nullptr, 1u);
     note_launch();
     return cudaGetLastError();
 }
 
 cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
-                               const SegOut& o, int num_sms, cudaStream_t s) {
+                               const SegOut& o, int num_sms, cudaStream_t s, unsigned long long* ticket) {
     if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
         return sum_segments_lanes(x, dtype, nseg, seg_len, o, num_sms, s);
     switch (dtype) {
-        case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s);
-        case XSUM_DT_F16: return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s);
-        case XSUM_DT_BF16: return launch_h16seg<FmtBF16Seg>(x, nseg, seg_len, offsets, o, num_sms, s);
+        case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
+        case XSUM_DT_F16: return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
+        case XSUM_DT_BF16: return launch_h16seg<FmtBF16Seg>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -156,6 +156,6 @@ cudaError_t sum_strided(const void* x, int dtype, uint64_t outer, uint64_t len, 
                         void* work, size_t work_bytes, int num_sms, cudaStream_t s);
 // binary32 / binary16 / bfloat16 elements (dtype XSUM_DT_F32 / F16 / BF16), equal or CSR segments
 cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
-                               const SegOut& o, int num_sms, cudaStream_t s);
+                               const SegOut& o, int num_sms, cudaStream_t s, unsigned long long* ticket = nullptr);
 
 }  // namespace xs

@@ -1,5 +1,6 @@
 """GPU parity of K11 (one lane per segment; equal segments of length <= 256, SURVEY.md §8(f) f1
-batched exact sums) in every input format: values (both roundings), flags and canonical images
+batched exact sums) in every input format: values (both roundings), flags and canonical images;
+the ticket-word dynamic order of ragged CSR segments (xsum_sum_segments_ws) vs the static order;
 vs the oracle, across the dispatch threshold, with narrow and wide exponent ranges (the touched
 digit-range tracking), cancellation, specials, signed zeros and misaligned bases."""
 from __future__ import annotations
@@ -103,3 +104,43 @@ def test_short_segments_both_roundings(xs):
     for s in range(nseg):
         r, _ = ref("f64", b[s * L:(s + 1) * L])
         assert (int(v64[s]), int(v32[s])) == (r.bits, r.bits_f32), s
+
+
+def test_ticket_and_static_order_identical(xs):
+    """xsum_sum_segments_ws: ragged CSR segments with the dynamic ticket order give bit-identical
+    values, flags and images to the static order (exact sums do not depend on which warp takes
+    which segment); a misaligned ticket word is rejected."""
+    import torch
+    rng = np.random.default_rng(3)
+    lens = rng.integers(0, 3000, size=700)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    for fmt in ("f64", "f32", "bf16"):
+        b = data(fmt, int(offs[-1]), 77, False)
+        d = to_dev(b, fmt, 0)
+        o = torch.from_numpy(offs).cuda()
+        st = torch.cuda.current_stream().cuda_stream
+        outs = []
+        for use_ticket in (False, True):
+            f64 = fmt == "f64"
+            out = torch.empty(lens.size, dtype=torch.float64 if f64 else torch.float32, device="cuda")
+            cn = torch.empty((lens.size, 34), dtype=torch.int64, device="cuda")
+            fl = torch.empty(lens.size, dtype=torch.int32, device="cuda")
+            tk = torch.zeros(1, dtype=torch.int64, device="cuda")
+            rc = xs.lib().xsum_sum_segments_ws(d.data_ptr(), xs._DT[str(d.dtype)[6:]], lens.size, 0, o.data_ptr(),
+                                              out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
+                                              cn.data_ptr(), fl.data_ptr(), tk.data_ptr() if use_ticket else None, st)
+            assert rc == 0
+            outs.append((out.cpu().numpy().tobytes(), cn.cpu().numpy().tobytes(), fl.cpu().numpy().tobytes()))
+            if use_ticket:
+                assert int(tk.item()) >= lens.size                 # the warps drew every segment
+        assert outs[0] == outs[1], fmt
+        for s in range(0, lens.size, 97):
+            r, limbs = ref(fmt, b[offs[s]:offs[s + 1]])
+            got = np.frombuffer(outs[1][0], dtype=np.uint64 if fmt == "f64" else np.uint32)[s]
+            assert int(got) == (r.bits if fmt == "f64" else r.bits_f32), (fmt, s)
+    tk = torch.zeros(2, dtype=torch.int64, device="cuda")
+    out = torch.empty(4, dtype=torch.float64, device="cuda")
+    x = torch.zeros(8, dtype=torch.float64, device="cuda")
+    o = torch.tensor([0, 2, 4, 6, 8], dtype=torch.int64, device="cuda")
+    assert xs.lib().xsum_sum_segments_ws(x.data_ptr(), 0, 4, 0, o.data_ptr(), out.data_ptr(), None, None, None,
+                                        tk.data_ptr() + 4, torch.cuda.current_stream().cuda_stream) == xs.EINVAL

@@ -1,8 +1,8 @@
 """GPU parity of K11 (one lane per segment; equal segments of length <= 256, SURVEY.md §8(f) f1
-batched exact sums) in every input format: values (both roundings), flags and canonical images;
-the ticket-word dynamic order of ragged CSR segments (xsum_sum_segments_ws) vs the static order;
-vs the oracle, across the dispatch threshold, with narrow and wide exponent ranges (the touched
-digit-range tracking), cancellation, specials, signed zeros and misaligned bases."""
+batched exact sums) in every input format: values (both roundings), flags and canonical images vs
+the oracle, across the dispatch threshold, with narrow and wide exponent ranges (the touched
+digit-range tracking), cancellation, specials, signed zeros and misaligned bases. Also: the
+ticket-word dynamic order of ragged CSR segments (xsum_sum_segments_ws) vs the static order."""
 from __future__ import annotations
 
 import numpy as np

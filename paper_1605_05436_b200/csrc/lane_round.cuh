@@ -68,6 +68,7 @@ __device__ __forceinline__ LaneTop lane_canonical_top(int64_t* col, int first = 
     t.sign = col[top * 32] < 0;
     int64_t br = 0;
     int lo = -1;                                   // lowest non-zero canonical digit
+#pragma unroll 4
     for (int j = first; j <= top; ++j) {
         int64_t u = (t.sign ? -col[j * 32] : col[j * 32]) + br;
         if (j < D - 1) {

@@ -64,6 +64,7 @@ template <> struct SlLd<XSUM_DT_BF16> {
 __device__ __forceinline__ int lane_regularize_range(int64_t* col, int lo, int hi) {
     int64_t cin = 0;
     const int last = hi < D - 1 ? hi : D - 2;
+#pragma unroll 4
     for (int j = lo; j <= last; ++j) {
         const int64_t y = col[j * 32];
         const int64_t c = balanced_carry(y);
@@ -163,6 +164,7 @@ k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint
         flush();
         if (hi < 0) lo = hi = 0;
         lane_store_segment(col, flags, o, s, lo, hi);
+#pragma unroll 4
         for (int j = lo; j <= hi; ++j) col[j * 32] = 0;   // the rest of the column is still zero
     }
 }

@@ -20,6 +20,8 @@
  * Conventions (all entry points):
  *   - Pointers named d_* are DEVICE pointers (cudaMalloc'd or torch tensors) on the
  *     handle's device; h_* are HOST pointers. The caller owns every buffer passed in.
+ *   - Entry points without a handle (segments, strided reductions) run on the calling
+ *     thread's current CUDA device; their device pointers must be on it.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Calls are asynchronous and stream-ordered; a buffer must stay valid until
  *     the stream passes the call. One handle is used by one stream at a time.

@@ -593,11 +593,12 @@ def _strided(x, outer, length, inner, out64, out32, flags=False):
     wb = int(lib().xsum_sum_strided_work_bytes(outer, length, inner, x.device.index))
     work = torch.empty(wb, dtype=torch.uint8, device=x.device) if wb else None
     xp = x if x.numel() else torch.zeros(8, dtype=x.dtype, device=x.device)
-    _check("xsum_sum_strided", lib().xsum_sum_strided(
-        xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], outer, length, inner,
-        o64.data_ptr() if o64 is not None else None, o32.data_ptr() if o32 is not None else None,
-        fl.data_ptr() if fl is not None else None, work.data_ptr() if work is not None else None, wb,
-        _stream_ptr(x.device)))
+    with torch.cuda.device(x.device):          # handle-less entry points run on the current device
+        _check("xsum_sum_strided", lib().xsum_sum_strided(
+            xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], outer, length, inner,
+            o64.data_ptr() if o64 is not None else None, o32.data_ptr() if o32 is not None else None,
+            fl.data_ptr() if fl is not None else None, work.data_ptr() if work is not None else None, wb,
+            _stream_ptr(x.device)))
     return o64, o32, fl
 
 
@@ -611,11 +612,12 @@ def _segments(x, nseg, seg_len, offsets, canon, flags):
     # ragged segments: a zeroed ticket word (stream-ordered, torch's allocator) lets the
     # warps balance the work dynamically (xsum_sum_segments_ws)
     tk = torch.zeros(1, dtype=torch.int64, device=x.device) if offsets is not None else None
-    rc = lib().xsum_sum_segments_ws(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
-                                    offsets.data_ptr() if offsets is not None else None,
-                                    out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
-                                    cn.data_ptr() if cn is not None else None,
-                                    fl.data_ptr() if fl is not None else None,
-                                    tk.data_ptr() if tk is not None else None, _stream_ptr(x.device))
+    with torch.cuda.device(x.device):          # handle-less entry points run on the current device
+        rc = lib().xsum_sum_segments_ws(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
+                                        offsets.data_ptr() if offsets is not None else None,
+                                        out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
+                                        cn.data_ptr() if cn is not None else None,
+                                        fl.data_ptr() if fl is not None else None,
+                                        tk.data_ptr() if tk is not None else None, _stream_ptr(x.device))
     _check("xsum_sum_segments_ws", rc)
     return out, cn, fl

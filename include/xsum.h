@@ -349,6 +349,17 @@ XSUM_API xsum_status xsum_sum_segments_ws(const void *d_x, int dtype, uint64_t n
                                           const uint64_t *d_offsets, double *d_out, float *d_out32,
                                           uint64_t *d_canon, uint32_t *d_flags, void *d_ticket, void *stream);
 
+/* CSR segments that are mostly short (SURVEY.md §8(f) f1 batched sums; e.g. sparse-matrix rows):
+ * same arguments and outputs as xsum_sum_segments_ws with d_offsets required. Warps take groups of
+ * 32 consecutive segments; a segment of <= 256 elements is summed by one lane in its own
+ * superaccumulator and rounded by it (one thread), longer ones of the group by
+ * the whole warp. d_ticket (optional, zero at the call's start, as in xsum_sum_segments_ws)
+ * balances the groups dynamically. Faster than the warp-per-segment path when most segments are
+ * short; the binding picks it when the mean length is <= 256. Errors: XSUM_EINVAL, XSUM_ECUDA. */
+XSUM_API xsum_status xsum_sum_segments_csr_lanes(const void *d_x, int dtype, uint64_t nseg, const uint64_t *d_offsets,
+                                                 double *d_out, float *d_out32, uint64_t *d_canon, uint32_t *d_flags,
+                                                 void *d_ticket, void *stream);
+
 /* Exact reduction along a strided dimension (a reproducible sum over one
  * tensor dimension without a transposing copy): d_x is a contiguous [outer][len][inner] array of
  * `dtype` elements (XSUM_DT_*; element-size aligned); for every o < outer, i < inner

@@ -38,6 +38,7 @@ OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 # sparse state image (include/xsum.h): 24-byte header + nnz records (digit << 6) | index
 SPARSE_MAGIC = 0x41505358
 SPARSE_HEADER_BYTES = 24
+SEG_LANES_MAX = 256          # segments of at most this many elements are summed one lane each
 SPARSE_MAX_BYTES = SPARSE_HEADER_BYTES + 8 * NDIGITS
 
 # every entry point declared in include/xsum.h
@@ -49,7 +50,7 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
            "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex", "xsum_save_state",
            "xsum_check_state_image", "xsum_load_state", "xsum_sum_strided_work_bytes", "xsum_sum_strided",
-           "xsum_sum_segments_ws")
+           "xsum_sum_segments_ws", "xsum_sum_segments_csr_lanes")
 
 
 class XsumError(RuntimeError):
@@ -101,6 +102,7 @@ def lib() -> ctypes.CDLL:
             "xsum_sum_strided_work_bytes": ([u64, u64, u64, i32], sz),
             "xsum_sum_strided": ([p, i32, u64, u64, u64, p, p, p, p, sz, p], i32),
             "xsum_sum_segments_ws": ([p, i32, u64, u64, p, p, p, p, p, p, p], i32),
+            "xsum_sum_segments_csr_lanes": ([p, i32, u64, p, p, p, p, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -613,6 +615,15 @@ def _segments(x, nseg, seg_len, offsets, canon, flags):
     # warps balance the work dynamically (xsum_sum_segments_ws)
     tk = torch.zeros(1, dtype=torch.int64, device=x.device) if offsets is not None else None
     with torch.cuda.device(x.device):          # handle-less entry points run on the current device
+        if offsets is not None and x.numel() <= SEG_LANES_MAX * nseg:
+            # mostly short CSR segments (mean length <= 256): one lane per short segment
+            rc = lib().xsum_sum_segments_csr_lanes(
+                xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, offsets.data_ptr(),
+                out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
+                cn.data_ptr() if cn is not None else None, fl.data_ptr() if fl is not None else None,
+                tk.data_ptr(), _stream_ptr(x.device))
+            _check("xsum_sum_segments_csr_lanes", rc)
+            return out, cn, fl
         rc = lib().xsum_sum_segments_ws(xp.data_ptr(), _DT[str(x.dtype).replace("torch.", "")], nseg, seg_len,
                                         offsets.data_ptr() if offsets is not None else None,
                                         out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),

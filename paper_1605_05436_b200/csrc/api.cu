@@ -540,6 +540,25 @@ xsum_status xsum_sum_segments_ws(const void* d_x, int dtype, uint64_t nseg, uint
     return e == cudaSuccess ? XSUM_OK : XSUM_ECUDA;
 }
 
+xsum_status xsum_sum_segments_csr_lanes(const void* d_x, int dtype, uint64_t nseg, const uint64_t* d_offsets,
+                                        double* d_out, float* d_out32, uint64_t* d_canon, uint32_t* d_flags,
+                                        void* d_ticket, void* stream) {
+    if (dtype < XSUM_DT_F64 || dtype > XSUM_DT_BF16) return XSUM_EINVAL;
+    if (nseg == 0) return XSUM_OK;
+    if (!d_out && !d_out32 && !d_canon && !d_flags) return XSUM_EINVAL;
+    const uintptr_t esz = dtype == XSUM_DT_F64 ? 8 : (dtype == XSUM_DT_F32 ? 4 : 2);
+    if (!d_offsets || !aligned(d_offsets, 8) || !d_x || !aligned(d_x, esz) || (d_out && !aligned(d_out, 8)) ||
+        (d_out32 && !aligned(d_out32, 4)) || (d_canon && !aligned(d_canon, 8)) || (d_flags && !aligned(d_flags, 4)) ||
+        (d_ticket && !aligned(d_ticket, 8)))
+        return XSUM_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
+    const xs::SegOut o{d_out, d_out32, d_canon, d_flags};
+    return xs::sum_segments_lanes_csr(d_x, dtype, nseg, d_offsets, o, static_cast<unsigned long long*>(d_ticket),
+                                      sms_of(dev), static_cast<cudaStream_t>(stream)) == cudaSuccess ? XSUM_OK
+                                                                                                     : XSUM_ECUDA;
+}
+
 size_t xsum_sum_strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int device) {
     if (inner <= 1) return 0;
     return xs::strided_work_bytes(outer, len, inner, sms_of(device));

@@ -169,6 +169,127 @@ k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint
     }
 }
 
+// K11c: CSR segments, mostly short (the caller's choice, e.g. a mean length <= 256). Warps take
+// groups of 32 consecutive segments (from the ticket word in units of groups, or statically);
+// every lane whose segment has <= SEG_LANES_MAX elements sums it alone as in K11 (scalar
+// L1-allocating loads: CSR starts have any alignment); the group's longer segments are then
+// summed one at a time by the whole warp (coalesced loads into the 32 lane columns, the raw
+// column combine and finalize_warp of K6's epilogue).
+template <int DT>
+__global__ void __launch_bounds__(SL_WARPS * 32, 1)
+k_segments_lanes_csr(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, const uint64_t* __restrict__ offsets,
+                     SegOut o, unsigned long long* __restrict__ ticket, uint32_t one) {
+    using L = SlLd<DT>;
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t su[SL_WARPS][64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t groups = (nseg + 31) / 32;
+    const uint64_t nw = (uint64_t)gridDim.x * SL_WARPS;
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    uint64_t g = ticket ? seg_next(ticket, 0, nw, lane) : (uint64_t)blockIdx.x * SL_WARPS + warp;
+    while (g < groups) {
+        const uint64_t gn = seg_next(ticket, g, nw, lane);        // next group, drawn early
+        const uint64_t s = g * 32 + lane;
+        const bool act = s < nseg;
+        const uint64_t b = act ? __ldg(offsets + s) : 0, e = act ? __ldg(offsets + s + 1) : 0;
+        const uint64_t len = e - b;
+        const bool small = act && len <= SEG_LANES_MAX;
+        if (small) {                                             // one lane, one segment
+            uint32_t flags = 0;
+            int lo = D, hi = -1;
+            auto add = [&](uint32_t xlo, uint32_t xhi) {
+                Chunks c = decompose(xlo, xhi, one);
+                if (spec_hit(c.spec)) { flags |= special_flags(xlo, xhi); return; }
+                column_add(col, c, one);
+                lo = min(lo, (int)c.i);
+                hi = max(hi, (int)c.i + 1);
+            };
+            const typename L::T* p = x + b;
+            uint64_t r = 0;
+            for (; r + 8 <= len; r += 8) {                       // len <= 256 < FLUSH_ELEMS: one window
+                uint2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = L::load(p + r + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) add(v[u].x, v[u].y);
+            }
+            for (; r < len; ++r) {
+                uint2 v = L::load(p + r);
+                add(v.x, v.y);
+            }
+            if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
+            if (hi < 0) lo = hi = 0;
+            lane_store_segment(col, flags, o, s, lo, hi);
+#pragma unroll 4
+            for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+        }
+        unsigned long long big = __ballot_sync(FULL, act && !small);
+        while (big) {                                            // long segments: the whole warp
+            const int j = __ffsll((long long)big) - 1;
+            big &= big - 1;
+            const uint64_t bj = __shfl_sync(FULL, b, j), ej = __shfl_sync(FULL, e, j);
+            uint32_t flags = 0;
+            int since = 0;
+            uint64_t r = bj + lane;
+            for (; r + 7 * 32 < ej; r += 8 * 32) {
+                uint2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = L::load(x + r + u * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) column_add_checked(col, v[u].x, v[u].y, flags, one);
+                since += 8;
+                if (since > FLUSH_ELEMS - 8) {
+                    regularize_column(col);
+                    since = 0;
+                }
+            }
+            for (; r < ej; r += 32) {                            // < 8 per lane left: in the window
+                uint2 v = L::load(x + r);
+                column_add_checked(col, v.x, v.y, flags, one);
+            }
+            __syncwarp();
+            int64_t a0, a1;
+            combine_raw_columns(win + warp * (D * 32), a0, a1, lane);
+            __syncwarp();
+#pragma unroll
+            for (int d = 0; d < D; ++d) col[d * 32] = 0;
+            const uint32_t fl = __reduce_or_sync(FULL, flags);
+            const uint64_t sj = g * 32 + j;
+            xsum_result res = finalize_warp(a0, a1, fl, ej - bj, o.canon ? o.canon + sj * XSUM_CANON_LIMBS : nullptr,
+                                            su[warp], lane);
+            if (lane == 0) o.write(sj, res);
+        }
+        g = gn;
+    }
+}
+
+template <int DT>
+static cudaError_t launch_lanes_csr(const void* x, uint64_t nseg, const uint64_t* offsets, const SegOut& o,
+                                    unsigned long long* ticket, int num_sms, cudaStream_t s) {
+    static unsigned long long done = 0;
+    if (cudaError_t e = ensure_smem(k_segments_lanes_csr<DT>, SL_SMEM, done)) return e;
+    const uint64_t groups = (nseg + 31) / 32;
+    const uint64_t want = (groups + SL_WARPS - 1) / SL_WARPS;
+    const unsigned g = (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
+    k_segments_lanes_csr<DT><<<g, SL_WARPS * 32, SL_SMEM, s>>>(static_cast<const typename SlLd<DT>::T*>(x), nseg,
+                                                               offsets, o, ticket, 1u);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t sum_segments_lanes_csr(const void* x, int dtype, uint64_t nseg, const uint64_t* offsets, const SegOut& o,
+                                   unsigned long long* ticket, int num_sms, cudaStream_t s) {
+    if (nseg == 0) return cudaSuccess;
+    switch (dtype) {
+        case XSUM_DT_F64: return launch_lanes_csr<XSUM_DT_F64>(x, nseg, offsets, o, ticket, num_sms, s);
+        case XSUM_DT_F32: return launch_lanes_csr<XSUM_DT_F32>(x, nseg, offsets, o, ticket, num_sms, s);
+        case XSUM_DT_F16: return launch_lanes_csr<XSUM_DT_F16>(x, nseg, offsets, o, ticket, num_sms, s);
+        default: return launch_lanes_csr<XSUM_DT_BF16>(x, nseg, offsets, o, ticket, num_sms, s);
+    }
+}
+
 template <int DT, bool VEC>
 static cudaError_t launch_lanes(const void* x, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
                                 cudaStream_t s) {

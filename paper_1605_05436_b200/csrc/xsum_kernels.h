@@ -144,6 +144,9 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
 constexpr uint64_t SEG_LANES_MAX = XS_SEG_LANES_MAX;
 cudaError_t sum_segments_lanes(const void* x, int dtype, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
                                cudaStream_t s);
+// CSR segments, mostly short: short ones one lane each, the rest by the warp (K11c)
+cudaError_t sum_segments_lanes_csr(const void* x, int dtype, uint64_t nseg, const uint64_t* offsets, const SegOut& o,
+                                   unsigned long long* ticket, int num_sms, cudaStream_t s);
 // strided reductions (K10, strided.cu): x as [outer][len][inner], out[o*inner + i]
 struct StrOut {
     double* out64;

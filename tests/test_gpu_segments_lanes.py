@@ -144,3 +144,47 @@ def test_ticket_and_static_order_identical(xs):
     o = torch.tensor([0, 2, 4, 6, 8], dtype=torch.int64, device="cuda")
     assert xs.lib().xsum_sum_segments_ws(x.data_ptr(), 0, 4, 0, o.data_ptr(), out.data_ptr(), None, None, None,
                                         tk.data_ptr() + 4, torch.cuda.current_stream().cuda_stream) == xs.EINVAL
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32", "f16", "bf16"])
+@pytest.mark.parametrize("mix", ["short", "mixed", "empty"])
+def test_csr_lanes_vs_oracle(xs, fmt, mix):
+    """K11c (xsum_sum_segments_csr_lanes, picked by the binding when the mean CSR length is <= 256):
+    short segments one lane each, the longer ones of a 32-segment group by the whole warp; values,
+    flags and canonical images of every segment vs the oracle, misaligned starts included."""
+    import torch
+    rng = np.random.default_rng({"short": 1, "mixed": 2, "empty": 3}[mix])
+    nseg = 1500
+    lens = rng.integers(0, 40, size=nseg)
+    if mix == "mixed":                                   # a few long segments (warp path), incl. > a window
+        k = rng.integers(0, nseg, size=12)
+        lens[k] = rng.integers(257, 70_000, size=12)
+    if mix == "empty":
+        lens[rng.integers(0, nseg, size=nseg // 2)] = 0
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    total = int(offs[-1])
+    b = data(fmt, max(total, 1) + 300 * nseg, 40 + nseg, mix == "short")   # spare tail: mean <= 256
+    d = to_dev(b, fmt, 1)
+    o = torch.from_numpy(offs).cuda()
+    runs = [xs.sum_segments_csr(d, o, canon=True, flags=True)]           # the binding's choice
+    f64 = fmt == "f64"                                                    # and K11c explicitly
+    out = torch.empty(nseg, dtype=torch.float64 if f64 else torch.float32, device="cuda")
+    cnt = torch.empty((nseg, 34), dtype=torch.int64, device="cuda")
+    flt = torch.empty(nseg, dtype=torch.int32, device="cuda")
+    for tk in (None, torch.zeros(1, dtype=torch.int64, device="cuda")):
+        rc = xs.lib().xsum_sum_segments_csr_lanes(d.data_ptr(), xs._DT[str(d.dtype)[6:]], nseg, o.data_ptr(),
+                                                 out.data_ptr() if f64 else None, None if f64 else out.data_ptr(),
+                                                 cnt.data_ptr(), flt.data_ptr(), tk.data_ptr() if tk is not None else None,
+                                                 torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        runs.append((out.clone(), cnt.clone(), flt.clone()))
+    for vals, canon, flags in runs:
+        v = vals.cpu().numpy()
+        v = v.view(np.uint64) if fmt == "f64" else v.view(np.uint32)
+        cn = canon.cpu().numpy().view(np.uint64)
+        fl = flags.cpu().numpy().view(np.uint32)
+        for s in range(nseg):
+            r, limbs = ref(fmt, b[offs[s]:offs[s + 1]])
+            want = r.bits if fmt == "f64" else r.bits_f32
+            assert int(v[s]) == want and int(fl[s]) == r.flags, (fmt, mix, s, lens[s])
+            assert (cn[s] == limbs).all(), (fmt, mix, s)

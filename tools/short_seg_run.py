@@ -35,3 +35,27 @@ for name in ("c2", "c1x"):
         print(f"{name:4s} L={L:5d}: {x.numel() // L:9d} segments  {ms * 1e3:9.1f} us  "
               f"{x.numel() / ms / 1e6:7.1f} G doubles/s  (exact_sum_dim over the last dim: {ms_dim * 1e3:9.1f} us)",
               flush=True)
+
+# ragged CSR segments, mostly short (sparse-matrix-like rows): K11c (the binding's choice for a mean
+# length <= 256) vs the warp-per-segment path with the ticket order (xsum_sum_segments_ws)
+import numpy as np  # noqa: E402
+
+x = synth.device_generate("c5")
+for maxlen in (8, 32, 128, 512):
+    rng = np.random.default_rng(maxlen)
+    nseg = int(x.numel() // (maxlen / 2 + 0.5))
+    lens = rng.integers(0, maxlen + 1, size=nseg)
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    keep = int(np.searchsorted(offs, x.numel(), side="right")) - 1
+    offs_t = torch.from_numpy(offs[:keep + 1].astype(np.int64)).cuda()
+    n = int(offs[keep])
+    out = torch.empty(keep, dtype=torch.float64, device="cuda")
+
+    def warp_path():
+        tk = torch.zeros(1, dtype=torch.int64, device="cuda")
+        xsum.lib().xsum_sum_segments_ws(x.data_ptr(), 0, keep, 0, offs_t.data_ptr(), out.data_ptr(), None, None, None,
+                                        tk.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    ms_l = t_ms(lambda: xsum.sum_segments_csr(x, offs_t))
+    ms_w = t_ms(warp_path)
+    print(f"csr lengths U[0,{maxlen}]: {keep:9d} segments, {n} doubles: binding {ms_l * 1e3:9.1f} us "
+          f"({n / ms_l / 1e6:6.1f} G/s) | warp per segment {ms_w * 1e3:9.1f} us ({n / ms_w / 1e6:6.1f} G/s)", flush=True)

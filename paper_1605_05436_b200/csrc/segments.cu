@@ -3,7 +3,10 @@
 // One warp reduces one segment with the same lane-column hot loop as K2, then combines
 // its 32 columns, regularizes and rounds without
 // leaving the warp - the paper's per-partition "combine" with a
-// warp as the partition's worker. Warps loop over segments (persistent grid).
+// warp as the partition's worker. Warps loop over segments (persistent grid): equal segments
+// in a fixed order, CSR segments in the order they draw them from a ticket word (dynamic
+// balancing of ragged lengths). Equal segments of <= SEG_LANES_MAX elements go to K11
+// (segments_lanes.cu: one lane per segment).
 #include <cuda_runtime.h>
 
 #include "xsum_device.cuh"

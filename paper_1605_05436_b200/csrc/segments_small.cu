@@ -12,7 +12,8 @@
 // summed as if finite; a per-lane max of ep sends a segment that held one to a rescan that
 // cancels them exactly and sets the flags (reading R10). At the segment's end the 32 narrow
 // columns are combined, moved to their digit positions and rounded by finalize_warp (binary64
-// and binary32).
+// and binary32). CSR segments are drawn from a ticket word as in K6; equal
+// segments of <= SEG_LANES_MAX elements go to K11 (one lane per segment).
 #include <cuda_runtime.h>
 
 #include "h16_common.cuh"

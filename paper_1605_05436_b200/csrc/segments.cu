@@ -346,6 +346,11 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     const bool uniform = !offsets && seg_len >= SEG_TILE && seg_len % ((uint64_t)SEG_TILE * SEG_NB) == 0 &&
                          ((uintptr_t)x & 15) == 0 && seg_len / SEG_TILE < (1u << 31);
+#ifndef XS_SEG_HALF
+#define XS_SEG_HALF 1
+#endif
+    if (XS_SEG_HALF && !offsets && segments_half_ok(x, seg_len))
+        return sum_segments_half(x, nseg, seg_len, o, num_sms, s);
     if (uniform)
         k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
     else {

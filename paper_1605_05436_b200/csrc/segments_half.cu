@@ -1,0 +1,381 @@
+// K6h: equal binary64 segments with HALF a warp per segment (config 5's streaming path, two
+// segments per warp). profiles/r01_c5_diagnosis.txt: the per-segment epilogue (the column
+// combine, carry resolution and rounding) costs ~15% of c5 and the loop is
+// issue-bound. With 16 lanes per segment the combine reads 16 instead of 32 lane columns per
+// segment and the two halves run their epilogues together (16-wide shuffles, ballots split by
+// half): the epilogue instructions per segment halve, the streaming loop is K6's (each half
+// reads its own segment's 256-byte rows).
+#include <cuda_runtime.h>
+
+#include "xsum_device.cuh"
+#include "xsum_kernels.h"
+
+namespace xs {
+
+constexpr int SH_WARPS = 8;
+#ifndef XS_SH_U
+#define XS_SH_U 8
+#endif
+#ifndef XS_SH_NB
+#define XS_SH_NB 2
+#endif
+constexpr int SH_U = XS_SH_U;                  // 16-B vectors per lane per tile
+constexpr int SH_NB = XS_SH_NB;                // rotating tile buffers
+constexpr uint32_t SH_TILE = 16 * SH_U * 2;    // doubles per half-warp tile
+constexpr int SH_FLUSH_TILES = FLUSH_ELEMS / (2 * SH_U);
+constexpr size_t SH_SMEM = (size_t)SH_WARPS * D * 32 * sizeof(int64_t);
+
+__device__ __forceinline__ uint32_t half_bits(uint32_t ballot, int half) { return (ballot >> (16 * half)) & 0xFFFFu; }
+
+// Raw lane sums of one half's 16 columns: lane hl sums rows hl, hl+16, hl+32 (hi / lo words
+// apart, as raw_lane_sums: |raw| < 2^63).
+struct HalfSums {
+    int64_t hs[3], ls[3];
+};
+__device__ __forceinline__ HalfSums half_raw_sums(const int64_t* wb, int hl, int half) {
+    HalfSums t = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll 4
+    for (int c = 0; c < 16; ++c) {
+        const int cc = half * 16 + ((hl + c) & 15);   // rotated: conflict-free within the half
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int row = hl + 16 * k;
+            if (row < D) {
+                const int64_t v = wb[row * 32 + cc];
+                t.hs[k] += v >> 32;
+                t.ls[k] += (int64_t)(uint32_t)v;
+            }
+        }
+    }
+    return t;
+}
+
+// Digits hl + 16k (k = 0..2) of the half's sum, regularized (balanced carry to the next digit;
+// the top digit 41 is not split).
+__device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[3], int hl) {
+    int64_t c[3], r[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int row = hl + 16 * k;
+        if (row < D - 1) {
+            c[k] = (d.hs[k] + ((d.ls[k] + (1ll << 51)) >> 32)) >> 20;
+            r[k] = (int64_t)((uint64_t)(d.hs[k] - (c[k] << 20)) << 32) + d.ls[k];
+        } else if (row == D - 1) {
+            c[k] = 0;
+            r[k] = (int64_t)((uint64_t)d.hs[k] << 32) + d.ls[k];
+        } else {
+            c[k] = 0;
+            r[k] = 0;
+        }
+    }
+    // the carry into digit j comes from digit j-1: lane hl-1 of the same row group, or lane 15
+    // of the group below (for hl == 0)
+    const int64_t up0 = __shfl_up_sync(FULL, c[0], 1, 16), up1 = __shfl_up_sync(FULL, c[1], 1, 16),
+                  up2 = __shfl_up_sync(FULL, c[2], 1, 16);
+    const int64_t t0 = __shfl_sync(FULL, c[0], 15, 16), t1 = __shfl_sync(FULL, c[1], 15, 16);
+    a[0] = r[0] + (hl == 0 ? 0 : up0);
+    a[1] = r[1] + (hl == 0 ? t0 : up1);
+    a[2] = hl + 32 < D ? r[2] + (hl == 0 ? t1 : up2) : 0;
+}
+
+// finalize_warp for a half warp: digits hl + 16k in a[k] (regularized); lane hl == 0 of each half
+// returns the record (binary64 and binary32 roundings, RN-even).
+__device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[3], uint32_t flags, uint64_t count, uint64_t* canon,
+                                                     int64_t* su, int hl, int half) {
+    xsum_result res = {};
+    auto mask48 = [&](bool p0, bool p1, bool p2) -> uint64_t {
+        return (uint64_t)half_bits(__ballot_sync(FULL, p0), half) |
+               ((uint64_t)half_bits(__ballot_sync(FULL, p1), half) << 16) |
+               ((uint64_t)half_bits(__ballot_sync(FULL, p2), half) << 32);
+    };
+    auto digit_at = [&](const int64_t (&v)[3], int j) -> int64_t {   // digit j of this half (j per half)
+        const int src = j & 15, k = j >> 4;
+        const int64_t v0 = __shfl_sync(FULL, v[0], src, 16), v1 = __shfl_sync(FULL, v[1], src, 16),
+                      v2 = __shfl_sync(FULL, v[2], src, 16);
+        return j < 0 ? 0 : (k == 0 ? v0 : (k == 1 ? v1 : v2));
+    };
+    const bool has2 = hl + 32 < D;
+    const uint64_t nz = mask48(a[0] != 0, a[1] != 0, has2 && a[2] != 0);
+    int sign = 0;
+    {
+        const int msd = nz ? 63 - __clzll((long long)nz) : 0;
+        const int64_t top = digit_at(a, msd);
+        sign = nz && top < 0;
+    }
+    if (sign) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a[k] = -a[k];
+    }
+    int64_t b[3], r[3], t[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        b[k] = a[k] >> W;
+        r[k] = a[k] & (int64_t)MASK;
+        if (hl + 16 * k == D - 1) { r[k] = a[k]; b[k] = 0; }
+    }
+    {
+        const int64_t up0 = __shfl_up_sync(FULL, b[0], 1, 16), up1 = __shfl_up_sync(FULL, b[1], 1, 16),
+                      up2 = __shfl_up_sync(FULL, b[2], 1, 16);
+        const int64_t t0 = __shfl_sync(FULL, b[0], 15, 16), t1 = __shfl_sync(FULL, b[1], 15, 16);
+        t[0] = r[0] + (hl == 0 ? 0 : up0);
+        t[1] = r[1] + (hl == 0 ? t0 : up1);
+        t[2] = has2 ? r[2] + (hl == 0 ? t1 : up2) : 0;
+    }
+    const uint64_t G = mask48(t[0] == -1, t[1] == -1, has2 && t[2] == -1);
+    const uint64_t P = mask48(t[0] == 0, t[1] == 0, has2 && t[2] == 0);
+    const uint64_t CI = ((G | P) + G) ^ P;
+    int64_t u[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int j = hl + 16 * k;
+        u[k] = t[k] - (int64_t)((CI >> j) & 1);
+        if (j < D - 1) u[k] &= (int64_t)MASK;
+        if (j >= D) u[k] = 0;
+    }
+    const uint64_t nzu = mask48(u[0] != 0, u[1] != 0, has2 && u[2] != 0);
+
+    if (canon) {                                   // rare: digits to shared memory, limbs per lane
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (hl + 16 * k < D) su[hl + 16 * k] = u[k];
+        __syncwarp();
+        for (int l = hl; l < XSUM_CANON_LIMBS; l += 16) {
+            uint64_t v = 0;
+            const int pos = 64 * l, j0 = pos / 52, j1 = (pos + 63) / 52;
+            for (int j = j0; j <= j1 && j < D; ++j) {
+                const uint64_t dj = (uint64_t)su[j];
+                const int sh = 52 * j - pos;
+                if (sh >= 0) { if (sh < 64) v |= dj << sh; }
+                else v |= dj >> (-sh);
+            }
+            canon[l] = v;                          // magnitude limbs; negated below if needed
+        }
+        __syncwarp();
+        if (sign && hl == 0) {                     // two's complement: ~|A| + 1 (sequential, rare)
+            uint64_t carry = 1;
+            for (int l = 0; l < XSUM_CANON_LIMBS; ++l) {
+                const uint64_t w = ~canon[l] + carry;
+                carry = (carry && w == 0) ? 1 : 0;
+                canon[l] = w;
+            }
+        }
+        __syncwarp();
+    }
+
+    const bool is64 = hl == 0;
+    const int prec = is64 ? 53 : 24, emin = is64 ? 0 : 925, emax = is64 ? 2047 : 255;
+    uint64_t bits = 0;
+    uint32_t rf = 0;
+    int dir = 0, msb = INT32_MIN, sh_out = 0;
+    uint64_t q_out = 0;
+    const int m = nzu ? 63 - __clzll((long long)nzu) : 0;
+    const uint64_t dm = (uint64_t)digit_at(u, m), dm1 = (uint64_t)digit_at(u, m - 1),
+                   dm2 = (uint64_t)digit_at(u, m - 2);
+    if (nzu && hl < 2) {
+        const int p = 52 * m + (63 - __clzll((long long)dm));
+        msb = p - 1074;
+        int sh = p - (prec - 1) > emin ? p - (prec - 1) : emin;
+        const unsigned __int128 Wp = ((unsigned __int128)dm << 53) | ((unsigned __int128)dm1 << 1) | (dm2 >> 51);
+        const int s = sh - 52 * m + 53;
+        uint64_t q = 0;
+        int g = 0;
+        bool sticky;
+        if (s < 128) {
+            q = (uint64_t)(Wp >> s);
+            g = (int)((uint64_t)(Wp >> (s - 1)) & 1);
+            sticky = (Wp & (((unsigned __int128)1 << (s - 1)) - 1)) != 0;
+        } else {
+            sticky = Wp != 0;
+        }
+        sticky = sticky || (dm2 & ((1ull << 51) - 1)) || (m >= 3 && (nzu & ((1ull << (m - 2)) - 1)));
+        const int up = g && (sticky || (q & 1));
+        if (g || sticky) dir = up ? 1 : -1;
+        q += (uint64_t)up;
+        if (sh == emin) {
+            bits = q;
+        } else {
+            if (q == (1ull << prec)) { q >>= 1; sh += 1; }
+            const int Eb = sh - emin + 1;
+            if (Eb >= emax) { bits = (uint64_t)emax << (prec - 1); rf |= is64 ? XSUM_F_OVERFLOW : XSUM_F_OVERFLOW32; dir = 1; }
+            else bits = ((uint64_t)Eb << (prec - 1)) | (q - (1ull << (prec - 1)));
+        }
+        q_out = q;
+        sh_out = sh;
+        if (dir) rf |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
+        if (sign) { bits |= is64 ? (1ull << 63) : 0x80000000ull; dir = -dir; }
+    }
+    const uint64_t b32 = __shfl_sync(FULL, bits, 1, 16);
+    const uint32_t rf32 = __shfl_sync(FULL, rf, 1, 16);
+    if (hl == 0) {
+        res.count = count;
+        const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf | rf32;
+        uint32_t v32 = (uint32_t)b32;
+        if (!nzu) {
+            res.msb_exp = INT32_MIN; res.sign = 0; res.sig53 = 0; res.exp2 = 0;
+        } else {
+            res.msb_exp = msb; res.sign = sign; res.sig53 = q_out; res.exp2 = sh_out - 1074;
+        }
+        if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
+            bits = 0x7FF8000000000000ull; dir = 0; v32 = 0x7FC00000u;
+        } else if (fl & XSUM_F_PINF) {
+            bits = 0x7FF0000000000000ull; dir = 0; v32 = 0x7F800000u;
+        } else if (fl & XSUM_F_NINF) {
+            bits = 0xFFF0000000000000ull; dir = 0; v32 = 0xFF800000u;
+        }
+        res.value = __longlong_as_double((long long)bits);
+        res.value_f32 = v32;
+        res.direction = dir;
+        res.flags = fl;
+    }
+    return res;
+}
+
+__device__ __noinline__ void half_rescan(int64_t* col, const uint4* seg, uint32_t t0, uint32_t t1, int hl,
+                                         uint32_t& flags, uint32_t one) {
+    for (uint32_t t = t0; t <= t1; ++t) {
+#pragma unroll
+        for (int u = 0; u < SH_U; ++u) {
+            uint4 v = ldg_stream(seg + (uint64_t)t * (16 * SH_U) + u * 16 + hl);
+            column_fix_special(col, v.x, v.y, flags, one);
+            column_fix_special(col, v.z, v.w, flags, one);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(SH_WARPS * 32, 2)
+k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t su[SH_WARPS][2][48];
+    __shared__ uint64_t canon_sink[SH_WARPS][XSUM_CANON_LIMBS];   // the odd last pair's idle half
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & 15, half = lane >> 4;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t nw = (uint64_t)gridDim.x * SH_WARPS;
+    const uint64_t npairs = (nseg + 1) / 2;
+    const uint64_t gw = (uint64_t)blockIdx.x * SH_WARPS + warp;
+    if (gw >= npairs) return;                                  // warp-uniform
+    const uint32_t TPS = (uint32_t)(seg_len / SH_TILE);        // half tiles per segment
+    const uint64_t seg_vecs = seg_len / 2;
+    const uint4* xv = reinterpret_cast<const uint4*>(x);
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    // this half's segments: 2p + half for the warp's pairs p = gw, gw + nw, ...; the second half
+    // of a last, odd pair re-reads its partner's segment and writes nothing
+    auto seg_of = [&](uint64_t p) -> uint64_t {
+        const uint64_t s = 2 * p + half;
+        return s < nseg ? s : 2 * p;
+    };
+    constexpr uint32_t TV = 16 * SH_U;
+    const uint4* lp = xv + seg_of(gw) * seg_vecs + hl;
+    uint64_t lpair = gw;
+    uint32_t lt = 0;
+    auto advance_load = [&]() {
+        lp += SH_NB * TV;
+        lt += SH_NB;
+        if (lt == TPS) {
+            lt = 0;
+            lpair += nw;
+            lp = xv + seg_of(lpair < npairs ? lpair : gw) * seg_vecs + hl;
+        }
+    };
+    uint64_t pp = gw;
+    uint32_t pt = 0, wstart = 0, flags = 0, nspec = 0;
+    int groups = 0;
+    HalfSums prev = {{0, 0, 0}, {0, 0, 0}};
+    constexpr int GROUPS_PER_WINDOW = SH_FLUSH_TILES / SH_NB;
+    uint4 buf[SH_NB][SH_U];
+#pragma unroll
+    for (int bb = 0; bb < SH_NB; ++bb)
+#pragma unroll
+        for (int u = 0; u < SH_U; ++u) buf[bb][u] = ldg_stream(lp + bb * TV + u * 16);
+    advance_load();
+    while (pp < npairs) {
+        const bool ld = lpair < npairs;
+#pragma unroll
+        for (int bb = 0; bb < SH_NB; ++bb) {
+#pragma unroll
+            for (int u = 0; u < SH_U; ++u) {
+                Chunks a = decompose(buf[bb][u].x, buf[bb][u].y, one, mone);
+                nspec = spec_fold(nspec, a);
+                column_add(col, a, one);
+                Chunks c = decompose(buf[bb][u].z, buf[bb][u].w, one, mone);
+                nspec = spec_fold(nspec, c);
+                column_add(col, c, one);
+            }
+            if (ld) {
+#pragma unroll
+                for (int u = 0; u < SH_U; ++u) buf[bb][u] = ldg_stream(lp + bb * TV + u * 16);
+            }
+        }
+        if (ld) advance_load();
+        pt += SH_NB;
+        ++groups;
+        const uint64_t ps = seg_of(pp);
+        if (pt == TPS) {                                       // both halves' segments complete
+            if (__any_sync(FULL, spec_hit(nspec))) {
+                if (spec_hit(nspec)) {
+                    regularize_column(col);
+                    half_rescan(col, xv + ps * seg_vecs, wstart, pt - 1, hl, flags, one);
+                    regularize_column(col);
+                }
+                nspec = 0;
+                groups = 0;
+            }
+            const int64_t* wb = win + warp * (D * 32);
+            __syncwarp();
+            const HalfSums now = half_raw_sums(wb, hl, half);
+            HalfSums d;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                d.hs[k] = now.hs[k] - prev.hs[k];
+                d.ls[k] = now.ls[k] - prev.ls[k];
+            }
+            prev = now;
+            int64_t a[3];
+            half_digits(d, a, hl);
+            uint32_t fl = flags;
+#pragma unroll
+            for (int off = 8; off > 0; off >>= 1) fl |= __shfl_xor_sync(FULL, fl, off, 16);
+            const bool mine = 2 * pp + half < nseg;
+            // canon pointer non-null for both halves or neither (finalize_half syncs the warp in it)
+            uint64_t* cp = o.canon ? (mine ? o.canon + ps * XSUM_CANON_LIMBS : canon_sink[warp]) : nullptr;
+            xsum_result r = finalize_half(a, fl, seg_len, cp, su[warp][half], hl, half);
+            if (hl == 0 && mine) o.write(ps, r);
+            flags = 0;
+            wstart = 0;
+            pt = 0;
+            pp += nw;
+        }
+        if (groups == GROUPS_PER_WINDOW) {
+            regularize_column_inl(col);
+            if (__any_sync(FULL, spec_hit(nspec))) {
+                if (spec_hit(nspec)) {
+                    half_rescan(col, xv + seg_of(pp) * seg_vecs, wstart, pt - 1, hl, flags, one);
+                    regularize_column(col);
+                }
+            }
+            nspec = 0;
+            groups = 0;
+            wstart = pt;
+        }
+    }
+}
+
+bool segments_half_ok(const double* x, uint64_t seg_len) {
+    return seg_len >= SH_TILE && seg_len % ((uint64_t)SH_TILE * SH_NB) == 0 && ((uintptr_t)x & 15) == 0 &&
+           seg_len / SH_TILE < (1u << 31);
+}
+
+cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
+                              cudaStream_t s) {
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_segments_half, SH_SMEM, smem_set)) return e;
+    const uint64_t npairs = (nseg + 1) / 2;
+    const uint64_t want = (npairs + SH_WARPS - 1) / SH_WARPS;
+    const uint64_t cap = (uint64_t)num_sms * 2;
+    const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    k_segments_half<<<g, SH_WARPS * 32, SH_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace xs

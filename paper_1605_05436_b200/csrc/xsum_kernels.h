@@ -136,6 +136,10 @@ struct SegOut {
 // it (dynamic balancing of ragged lengths), else the static order s, s + nw, ...
 cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets, const SegOut& o,
                          int num_sms, cudaStream_t s, unsigned long long* ticket = nullptr);
+// equal binary64 segments, half a warp per segment (K6h, segments_half.cu)
+bool segments_half_ok(const double* x, uint64_t seg_len);
+cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
+                              cudaStream_t s);
 // short equal segments, one lane per segment (K11, segments_lanes.cu); sum_segments and
 // sum_segments_small route equal segments of length <= SEG_LANES_MAX here
 #ifndef XS_SEG_LANES_MAX

@@ -588,3 +588,24 @@ def test_every_exponent_and_digit_boundary(xs):
     res, canon = xs.exact_sum(d)                          # and all of them at once (fused path)
     r, limbs = oracle.exact_sum(x)
     assert res.bits == r.bits and (canon == limbs).all()
+
+
+@pytest.mark.parametrize("seg_len,nseg", [(512, 1), (512, 301), (1024, 77), (8192, 5), (4096, 2049)])
+def test_segments_half_warp_path(xs, seg_len, nseg):
+    """K6h (half a warp per segment, equal 16-B-aligned segments of a multiple of 512): odd
+    segment counts (the last pair's second half idles and writes nothing), NaN / Inf planted in
+    the last segment and in a segment the other half of its warp does not see, canonical images
+    and flags of every segment vs the oracle."""
+    x = synth.gen.generate("c5", 11, nseg * seg_len)
+    xb = x.view(np.uint64)
+    xb[x.size - 3] = 0x7FF0000000000000                        # +Inf in the last segment
+    if nseg > 2:
+        xb[seg_len + 5] = 0x7FF8000000000001                   # NaN in segment 1
+        xb[2 * seg_len + 9] = 0xFFF0000000000000               # -Inf in segment 2
+    vals, canon, flags = xs.sum_segments(to_dev(x, 0), seg_len, canon=True, flags=True)
+    vals = vals.cpu().numpy().view(np.uint64)
+    canon = canon.cpu().numpy().view(np.uint64)
+    flags = flags.cpu().numpy()
+    for s in range(nseg):
+        r, limbs = oracle.exact_sum(x[s * seg_len:(s + 1) * seg_len], nthreads=1)
+        assert int(vals[s]) == r.bits and int(flags[s]) == r.flags and (canon[s] == limbs).all(), s

@@ -19,27 +19,37 @@ constexpr int SH_WARPS = 8;
 #ifndef XS_SH_NB
 #define XS_SH_NB 2
 #endif
+#ifndef XS_SH_LPS
+#define XS_SH_LPS 16
+#endif
 constexpr int SH_U = XS_SH_U;                  // 16-B vectors per lane per tile
 constexpr int SH_NB = XS_SH_NB;                // rotating tile buffers
-constexpr uint32_t SH_TILE = 16 * SH_U * 2;    // doubles per half-warp tile
+constexpr int LPS = XS_SH_LPS;                 // lanes per segment (16: half warps; 8: quarters)
+constexpr int SEGS = 32 / LPS;                 // segments per warp at a time
+constexpr int KD = (D + LPS - 1) / LPS;        // digits per lane: lane sl holds sl + LPS k
+constexpr uint32_t SH_TILE = LPS * SH_U * 2;   // doubles per segment tile
 constexpr int SH_FLUSH_TILES = FLUSH_ELEMS / (2 * SH_U);
 constexpr size_t SH_SMEM = (size_t)SH_WARPS * D * 32 * sizeof(int64_t);
 
-__device__ __forceinline__ uint32_t half_bits(uint32_t ballot, int half) { return (ballot >> (16 * half)) & 0xFFFFu; }
+__device__ __forceinline__ uint32_t half_bits(uint32_t ballot, int half) {
+    return (ballot >> (LPS * half)) & ((1u << LPS) - 1);
+}
 
 // Raw lane sums of one half's 16 columns: lane hl sums rows hl, hl+16, hl+32 (hi / lo words
 // apart, as raw_lane_sums: |raw| < 2^63).
 struct HalfSums {
-    int64_t hs[3], ls[3];
+    int64_t hs[KD], ls[KD];
 };
 __device__ __forceinline__ HalfSums half_raw_sums(const int64_t* wb, int hl, int half) {
-    HalfSums t = {{0, 0, 0}, {0, 0, 0}};
-#pragma unroll 4
-    for (int c = 0; c < 16; ++c) {
-        const int cc = half * 16 + ((hl + c) & 15);   // rotated: conflict-free within the half
+    HalfSums t;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const int row = hl + 16 * k;
+    for (int k = 0; k < KD; ++k) t.hs[k] = t.ls[k] = 0;
+#pragma unroll 4
+    for (int c = 0; c < LPS; ++c) {
+        const int cc = half * LPS + ((hl + c) & (LPS - 1));   // rotated: conflict-free within the slot
+#pragma unroll
+        for (int k = 0; k < KD; ++k) {
+            const int row = hl + LPS * k;
             if (row < D) {
                 const int64_t v = wb[row * 32 + cc];
                 t.hs[k] += v >> 32;
@@ -50,13 +60,23 @@ __device__ __forceinline__ HalfSums half_raw_sums(const int64_t* wb, int hl, int
     return t;
 }
 
-// Digits hl + 16k (k = 0..2) of the half's sum, regularized (balanced carry to the next digit;
-// the top digit 41 is not split).
-__device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[3], int hl) {
-    int64_t c[3], r[3];
+// Digits hl + LPS k of the slot's sum, regularized (balanced carry to the next digit; the top
+// digit 41 is not split).
+__device__ __forceinline__ void carry_in(const int64_t (&c)[KD], int64_t (&in)[KD], int hl) {
+    // the carry into digit j comes from digit j-1: lane hl-1 of the same row group, or the
+    // slot's last lane of the group below (for hl == 0)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int row = hl + 16 * k;
+    for (int k = 0; k < KD; ++k) {
+        const int64_t up = __shfl_up_sync(FULL, c[k], 1, LPS);
+        const int64_t lo = k > 0 ? __shfl_sync(FULL, c[k > 0 ? k - 1 : 0], LPS - 1, LPS) : 0;
+        in[k] = hl == 0 ? lo : up;
+    }
+}
+__device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[KD], int hl) {
+    int64_t c[KD], r[KD], in[KD];
+#pragma unroll
+    for (int k = 0; k < KD; ++k) {
+        const int row = hl + LPS * k;
         if (row < D - 1) {
             c[k] = (d.hs[k] + ((d.ls[k] + (1ll << 51)) >> 32)) >> 20;
             r[k] = (int64_t)((uint64_t)(d.hs[k] - (c[k] << 20)) << 32) + d.ls[k];
@@ -68,34 +88,34 @@ __device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[3], 
             r[k] = 0;
         }
     }
-    // the carry into digit j comes from digit j-1: lane hl-1 of the same row group, or lane 15
-    // of the group below (for hl == 0)
-    const int64_t up0 = __shfl_up_sync(FULL, c[0], 1, 16), up1 = __shfl_up_sync(FULL, c[1], 1, 16),
-                  up2 = __shfl_up_sync(FULL, c[2], 1, 16);
-    const int64_t t0 = __shfl_sync(FULL, c[0], 15, 16), t1 = __shfl_sync(FULL, c[1], 15, 16);
-    a[0] = r[0] + (hl == 0 ? 0 : up0);
-    a[1] = r[1] + (hl == 0 ? t0 : up1);
-    a[2] = hl + 32 < D ? r[2] + (hl == 0 ? t1 : up2) : 0;
+    carry_in(c, in, hl);
+#pragma unroll
+    for (int k = 0; k < KD; ++k) a[k] = hl + LPS * k < D ? r[k] + in[k] : 0;
 }
 
 // finalize_warp for a half warp: digits hl + 16k in a[k] (regularized); lane hl == 0 of each half
 // returns the record (binary64 and binary32 roundings, RN-even).
-__device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[3], uint32_t flags, uint64_t count, uint64_t* canon,
+__device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[KD], uint32_t flags, uint64_t count, uint64_t* canon,
                                                      int64_t* su, int hl, int half) {
     xsum_result res = {};
-    auto mask48 = [&](bool p0, bool p1, bool p2) -> uint64_t {
-        return (uint64_t)half_bits(__ballot_sync(FULL, p0), half) |
-               ((uint64_t)half_bits(__ballot_sync(FULL, p1), half) << 16) |
-               ((uint64_t)half_bits(__ballot_sync(FULL, p2), half) << 32);
+    auto valid = [&](int k) { return hl + LPS * k < D; };
+    auto mask = [&](auto pred) -> uint64_t {          // bit j of the slot's 42 digits: pred(k) of lane j % LPS
+        uint64_t m = 0;
+#pragma unroll
+        for (int k = 0; k < KD; ++k) m |= (uint64_t)half_bits(__ballot_sync(FULL, valid(k) && pred(k)), half) << (LPS * k);
+        return m;
     };
-    auto digit_at = [&](const int64_t (&v)[3], int j) -> int64_t {   // digit j of this half (j per half)
-        const int src = j & 15, k = j >> 4;
-        const int64_t v0 = __shfl_sync(FULL, v[0], src, 16), v1 = __shfl_sync(FULL, v[1], src, 16),
-                      v2 = __shfl_sync(FULL, v[2], src, 16);
-        return j < 0 ? 0 : (k == 0 ? v0 : (k == 1 ? v1 : v2));
+    auto digit_at = [&](const int64_t (&v)[KD], int j) -> int64_t {   // digit j of this slot (j per slot)
+        const int src = j & (LPS - 1), kk = j / LPS;
+        int64_t out = 0;
+#pragma unroll
+        for (int k = 0; k < KD; ++k) {
+            const int64_t w = __shfl_sync(FULL, v[k], src, LPS);
+            if (k == kk) out = w;
+        }
+        return j < 0 ? 0 : out;
     };
-    const bool has2 = hl + 32 < D;
-    const uint64_t nz = mask48(a[0] != 0, a[1] != 0, has2 && a[2] != 0);
+    const uint64_t nz = mask([&](int k) { return a[k] != 0; });
     int sign = 0;
     {
         const int msd = nz ? 63 - __clzll((long long)nz) : 0;
@@ -104,42 +124,37 @@ __device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[3], uint32_t f
     }
     if (sign) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) a[k] = -a[k];
+        for (int k = 0; k < KD; ++k) a[k] = -a[k];
     }
-    int64_t b[3], r[3], t[3];
+    int64_t b[KD], r[KD], t[KD], in[KD];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < KD; ++k) {
         b[k] = a[k] >> W;
         r[k] = a[k] & (int64_t)MASK;
-        if (hl + 16 * k == D - 1) { r[k] = a[k]; b[k] = 0; }
+        if (hl + LPS * k == D - 1) { r[k] = a[k]; b[k] = 0; }
     }
-    {
-        const int64_t up0 = __shfl_up_sync(FULL, b[0], 1, 16), up1 = __shfl_up_sync(FULL, b[1], 1, 16),
-                      up2 = __shfl_up_sync(FULL, b[2], 1, 16);
-        const int64_t t0 = __shfl_sync(FULL, b[0], 15, 16), t1 = __shfl_sync(FULL, b[1], 15, 16);
-        t[0] = r[0] + (hl == 0 ? 0 : up0);
-        t[1] = r[1] + (hl == 0 ? t0 : up1);
-        t[2] = has2 ? r[2] + (hl == 0 ? t1 : up2) : 0;
-    }
-    const uint64_t G = mask48(t[0] == -1, t[1] == -1, has2 && t[2] == -1);
-    const uint64_t P = mask48(t[0] == 0, t[1] == 0, has2 && t[2] == 0);
-    const uint64_t CI = ((G | P) + G) ^ P;
-    int64_t u[3];
+    carry_in(b, in, hl);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int j = hl + 16 * k;
+    for (int k = 0; k < KD; ++k) t[k] = valid(k) ? r[k] + in[k] : 0;
+    const uint64_t G = mask([&](int k) { return t[k] == -1; });
+    const uint64_t P = mask([&](int k) { return t[k] == 0; });
+    const uint64_t CI = ((G | P) + G) ^ P;
+    int64_t u[KD];
+#pragma unroll
+    for (int k = 0; k < KD; ++k) {
+        const int j = hl + LPS * k;
         u[k] = t[k] - (int64_t)((CI >> j) & 1);
         if (j < D - 1) u[k] &= (int64_t)MASK;
         if (j >= D) u[k] = 0;
     }
-    const uint64_t nzu = mask48(u[0] != 0, u[1] != 0, has2 && u[2] != 0);
+    const uint64_t nzu = mask([&](int k) { return u[k] != 0; });
 
     if (canon) {                                   // rare: digits to shared memory, limbs per lane
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-            if (hl + 16 * k < D) su[hl + 16 * k] = u[k];
+        for (int k = 0; k < KD; ++k)
+            if (hl + LPS * k < D) su[hl + LPS * k] = u[k];
         __syncwarp();
-        for (int l = hl; l < XSUM_CANON_LIMBS; l += 16) {
+        for (int l = hl; l < XSUM_CANON_LIMBS; l += LPS) {
             uint64_t v = 0;
             const int pos = 64 * l, j0 = pos / 52, j1 = (pos + 63) / 52;
             for (int j = j0; j <= j1 && j < D; ++j) {
@@ -204,8 +219,8 @@ __device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[3], uint32_t f
         if (dir) rf |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
         if (sign) { bits |= is64 ? (1ull << 63) : 0x80000000ull; dir = -dir; }
     }
-    const uint64_t b32 = __shfl_sync(FULL, bits, 1, 16);
-    const uint32_t rf32 = __shfl_sync(FULL, rf, 1, 16);
+    const uint64_t b32 = __shfl_sync(FULL, bits, 1, LPS);
+    const uint32_t rf32 = __shfl_sync(FULL, rf, 1, LPS);
     if (hl == 0) {
         res.count = count;
         const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf | rf32;
@@ -235,7 +250,7 @@ __device__ __noinline__ void half_rescan(int64_t* col, const uint4* seg, uint32_
     for (uint32_t t = t0; t <= t1; ++t) {
 #pragma unroll
         for (int u = 0; u < SH_U; ++u) {
-            uint4 v = ldg_stream(seg + (uint64_t)t * (16 * SH_U) + u * 16 + hl);
+            uint4 v = ldg_stream(seg + (uint64_t)t * (LPS * SH_U) + u * LPS + hl);
             column_fix_special(col, v.x, v.y, flags, one);
             column_fix_special(col, v.z, v.w, flags, one);
         }
@@ -245,12 +260,12 @@ __device__ __noinline__ void half_rescan(int64_t* col, const uint4* seg, uint32_
 __global__ void __launch_bounds__(SH_WARPS * 32, 2)
 k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one, uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
-    __shared__ int64_t su[SH_WARPS][2][48];
+    __shared__ int64_t su[SH_WARPS][SEGS][48];
     __shared__ uint64_t canon_sink[SH_WARPS][XSUM_CANON_LIMBS];   // the odd last pair's idle half
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & 15, half = lane >> 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & (LPS - 1), half = lane / LPS;
     int64_t* col = win + warp * (D * 32) + lane;
     const uint64_t nw = (uint64_t)gridDim.x * SH_WARPS;
-    const uint64_t npairs = (nseg + 1) / 2;
+    const uint64_t npairs = (nseg + SEGS - 1) / SEGS;          // groups of SEGS segments
     const uint64_t gw = (uint64_t)blockIdx.x * SH_WARPS + warp;
     if (gw >= npairs) return;                                  // warp-uniform
     const uint32_t TPS = (uint32_t)(seg_len / SH_TILE);        // half tiles per segment
@@ -261,10 +276,10 @@ k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, S
     // this half's segments: 2p + half for the warp's pairs p = gw, gw + nw, ...; the second half
     // of a last, odd pair re-reads its partner's segment and writes nothing
     auto seg_of = [&](uint64_t p) -> uint64_t {
-        const uint64_t s = 2 * p + half;
-        return s < nseg ? s : 2 * p;
+        const uint64_t s = SEGS * p + half;
+        return s < nseg ? s : SEGS * p;
     };
-    constexpr uint32_t TV = 16 * SH_U;
+    constexpr uint32_t TV = LPS * SH_U;
     const uint4* lp = xv + seg_of(gw) * seg_vecs + hl;
     uint64_t lpair = gw;
     uint32_t lt = 0;
@@ -280,13 +295,15 @@ k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, S
     uint64_t pp = gw;
     uint32_t pt = 0, wstart = 0, flags = 0, nspec = 0;
     int groups = 0;
-    HalfSums prev = {{0, 0, 0}, {0, 0, 0}};
+    HalfSums prev;
+#pragma unroll
+    for (int k = 0; k < KD; ++k) prev.hs[k] = prev.ls[k] = 0;
     constexpr int GROUPS_PER_WINDOW = SH_FLUSH_TILES / SH_NB;
     uint4 buf[SH_NB][SH_U];
 #pragma unroll
     for (int bb = 0; bb < SH_NB; ++bb)
 #pragma unroll
-        for (int u = 0; u < SH_U; ++u) buf[bb][u] = ldg_stream(lp + bb * TV + u * 16);
+        for (int u = 0; u < SH_U; ++u) buf[bb][u] = ldg_stream(lp + bb * TV + u * LPS);
     advance_load();
     while (pp < npairs) {
         const bool ld = lpair < npairs;
@@ -303,7 +320,7 @@ k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, S
             }
             if (ld) {
 #pragma unroll
-                for (int u = 0; u < SH_U; ++u) buf[bb][u] = ldg_stream(lp + bb * TV + u * 16);
+                for (int u = 0; u < SH_U; ++u) buf[bb][u] = ldg_stream(lp + bb * TV + u * LPS);
             }
         }
         if (ld) advance_load();
@@ -325,17 +342,17 @@ k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, S
             const HalfSums now = half_raw_sums(wb, hl, half);
             HalfSums d;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
+            for (int k = 0; k < KD; ++k) {
                 d.hs[k] = now.hs[k] - prev.hs[k];
                 d.ls[k] = now.ls[k] - prev.ls[k];
             }
             prev = now;
-            int64_t a[3];
+            int64_t a[KD];
             half_digits(d, a, hl);
             uint32_t fl = flags;
 #pragma unroll
-            for (int off = 8; off > 0; off >>= 1) fl |= __shfl_xor_sync(FULL, fl, off, 16);
-            const bool mine = 2 * pp + half < nseg;
+            for (int off = LPS / 2; off > 0; off >>= 1) fl |= __shfl_xor_sync(FULL, fl, off, LPS);
+            const bool mine = SEGS * pp + half < nseg;
             // canon pointer non-null for both halves or neither (finalize_half syncs the warp in it)
             uint64_t* cp = o.canon ? (mine ? o.canon + ps * XSUM_CANON_LIMBS : canon_sink[warp]) : nullptr;
             xsum_result r = finalize_half(a, fl, seg_len, cp, su[warp][half], hl, half);
@@ -369,7 +386,7 @@ cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, 
                               cudaStream_t s) {
     static unsigned long long smem_set = 0;
     if (cudaError_t e = ensure_smem(k_segments_half, SH_SMEM, smem_set)) return e;
-    const uint64_t npairs = (nseg + 1) / 2;
+    const uint64_t npairs = (nseg + SEGS - 1) / SEGS;          // groups of SEGS segments
     const uint64_t want = (npairs + SH_WARPS - 1) / SH_WARPS;
     const uint64_t cap = (uint64_t)num_sms * 2;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);

@@ -28,9 +28,7 @@ VARIANTS = {
     "seg_u1nb16": ["-DXS_SEG_U=1", "-DXS_SEG_NB=16"],
     "lanes0": ["-DXS_SEG_LANES_MAX=0"],
     "seg_whole": ["-DXS_SEG_HALF=0"],
-    "sh_nb4": ["-DXS_SH_NB=4"],
-    "sh_u2nb4": ["-DXS_SH_U=2", "-DXS_SH_NB=4"],
-    "sh_u8nb2": ["-DXS_SH_U=8", "-DXS_SH_NB=2"],
+    "sh_q8u4": ["-DXS_SH_LPS=8", "-DXS_SH_U=4"],
     "sl_full": ["-DXS_SL_FULL"],
     "str_nb3": ["-DXS_STR_NB=3"],
     "str_nb6": ["-DXS_STR_NB=6"],

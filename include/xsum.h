@@ -311,7 +311,8 @@ XSUM_API uint64_t xsum_count(const xsum_ctx *h);
  * exact sum of d_x[s*seg_len .. (s+1)*seg_len). Optional outputs: d_canon[s*34 .. s*34+34)
  * canonical images, d_flags[s] XSUM_F_* flags. d_x 8-B aligned, any seg_len >= 0.
  * Each segment is reduced by one warp (the paper's per-block "combine");
- * equal segments of length <= 256 by one lane each (its own superaccumulator and rounding).
+ * equal segments of length <= 256 by one lane each (its own superaccumulator and rounding), and
+ * equal 16-B-aligned segments whose length is a multiple of 512 by half a warp each.
  * Errors: XSUM_EINVAL, XSUM_ECUDA. */
 XSUM_API xsum_status xsum_sum_segments(const double *d_x, uint64_t nseg, uint64_t seg_len, double *d_out,
                               uint64_t *d_canon, uint32_t *d_flags, void *stream);

@@ -466,7 +466,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
                          "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
-                                    "c2bf16": "k_accumulate_h16", "c5": "k_segments_uniform",
+                                    "c2bf16": "k_accumulate_h16", "c5": "k_segments_half",
                                     "c5csr": "k_segments", "c5s16": "k_segments_lanes",
                                     "c2dim0": "k_sum_strided"}.get(args.config, "k_accumulate"),
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local,

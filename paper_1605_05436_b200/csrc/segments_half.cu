@@ -4,7 +4,8 @@
 // issue-bound. With 16 lanes per segment the combine reads 16 instead of 32 lane columns per
 // segment and the two halves run their epilogues together (16-wide shuffles, ballots split by
 // half): the epilogue instructions per segment halve, the streaming loop is K6's (each half
-// reads its own segment's 256-byte rows).
+// reads its own segment's rows). The code is generic in the lanes per segment (LPS = 16 kept;
+// 8, quarter warps, measured slower: its 6-digit-per-lane epilogue spills).
 #include <cuda_runtime.h>
 
 #include "xsum_device.cuh"

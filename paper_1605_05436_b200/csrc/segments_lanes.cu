@@ -81,8 +81,10 @@ __device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags,
                                                    int hi) {
     const LaneTop t = lane_canonical_top(col, lo, hi);
     uint32_t rf = 0;
-    uint64_t b64 = lane_round(t, 53, 0, 2047, true, rf);
-    uint32_t b32 = (uint32_t)lane_round(t, 24, 925, 255, false, rf);
+    // the binary32 rounding only when its value or the flags (which carry its bits) are wanted
+    const bool want32 = o.out32 || o.flags;
+    uint64_t b64 = (o.out || o.flags) ? lane_round(t, 53, 0, 2047, true, rf) : 0;
+    uint32_t b32 = want32 ? (uint32_t)lane_round(t, 24, 925, 255, false, rf) : 0;
     const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf;
     if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
         b64 = 0x7FF8000000000000ull; b32 = 0x7FC00000u;

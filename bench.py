@@ -48,6 +48,9 @@ def parse():
                                                          "c2bf16", "c2dim0", "c5s16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sustained-s", type=float, default=2.0,
+                    help="after the timed region, run the step back to back this long and report the "
+                         "power-capped rate as `sustained` (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     # testing the N>1 host path with several ranks on ONE GPU (gloo, no fused exchange: no kernel
@@ -427,6 +430,25 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     except Exception:  # noqa: BLE001
         probe_gbs = None
 
+    # context: the same step back to back for a few seconds, after the timed region (the board's
+    # power cap engages after ~0.1 s; profiles/r01_sustained_power.txt)
+    sustained = None
+    if world == 1 and args.sustained_s > 0:
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k_s = max(1, int(args.sustained_s / max(total_ms / K / 1e3, 1e-6)))
+        with ClockSampler(local_rank, period_s=0.01) as clk_s:
+            a_ev.record(stream)
+            for _ in range(k_s):
+                step()
+            b_ev.record(stream)
+            torch.cuda.synchronize()
+        ms_s = a_ev.elapsed_time(b_ev)
+        cs = clk_s.summary()
+        sustained = {"value": n_local * k_s / (ms_s / 1e3), "unit": unit, "steps": k_s, "seconds": ms_s / 1e3,
+                     "sm_mhz": cs.get("sm_mhz"), "reasons": cs.get("reasons"),
+                     "note": "context only (value is the timed region's): the same step back to back; "
+                             "the 1000 W cap lowers SM clocks after ~0.1 s"}
+
     # check the result once (device result vs nothing host-side: the parity tests do that)
     e2e = None
     if not args.no_e2e and not seg and esz * n_local <= (16 << 30):
@@ -475,6 +497,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "clocks": dict(clk.summary(), **({"remeasured_after": first_clocks} if first_clocks else {})),
             "gpu_launches": launches,
             "e2e": e2e,
+            "sustained": sustained,
             "cpu_baseline": cpu,
             "result": result,
         }

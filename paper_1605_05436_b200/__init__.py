@@ -533,9 +533,10 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
     """Exact reduction of a CUDA tensor along one dimension: every output
     element is the correctly rounded (RN-even) sum of its fibre, independent of order - a
     reproducible torch.sum(x, dim). float64 input gives float64, float32 / float16 / bfloat16
-    input the float32 rounding of the exact sum. A contiguous tensor reduced over a non-last
-    dimension goes to xsum_sum_strided (no copy); otherwise the fibres are laid out as equal
-    contiguous segments (a movedim + contiguous copy for non-contiguous inputs) and summed by
+    input the float32 rounding of the exact sum. A contiguous tensor (or a permuted view of one,
+    e.g. a transpose) reduced over a non-last dimension goes to xsum_sum_strided (no copy);
+    otherwise the fibres are laid out as equal contiguous segments (a movedim + contiguous copy
+    for other non-contiguous inputs) and summed by
     xsum_sum_segments_ex (one warp per fibre; one lane per fibre for fibres of <= 256)."""
     torch = _torch()
     if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype not in (torch.float64, torch.float32,
@@ -545,6 +546,18 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
         raise ValueError("exact_sum_dim needs a tensor with at least one dimension")
     d = dim % x.dim()
     f64 = x.dtype == torch.float64
+    if not x.is_contiguous() and x.dim() > 1:
+        # a permuted view of a contiguous tensor (e.g. a transpose): reduce the matching dimension
+        # of the underlying contiguous layout (no copy of the input), then put the output's
+        # dimensions back in the view's order
+        perm = sorted(range(x.dim()), key=lambda i: -x.stride(i))
+        base = x.permute(perm)
+        if base.is_contiguous():
+            p = perm.index(d)
+            out_b = exact_sum_dim(base, p)
+            rem = [perm[i] for i in range(x.dim()) if i != p]        # view dims in out_b's order
+            out = out_b.permute([rem.index(k) for k in sorted(rem)]).contiguous()
+            return out.unsqueeze(d) if keepdim else out
     outer = 1
     for s_ in x.shape[:d]:
         outer *= s_

@@ -165,3 +165,25 @@ def test_strided_argument_errors(xs):
     assert L.xsum_sum_strided(x.data_ptr() + 4, 0, 1, 8, 8, o.data_ptr(), None, None, None, 0, st) == xs.EINVAL
     assert L.xsum_sum_strided(x.data_ptr(), 0, 0, 8, 8, o.data_ptr(), None, None, None, 0, st) == 0
     assert L.xsum_sum_strided(x.data_ptr(), 0, 1 << 62, 8, 8, o.data_ptr(), None, None, None, 0, st) == xs.EINVAL
+
+
+@pytest.mark.parametrize("shape,perm,dim", [((300, 70), (1, 0), 1), ((300, 70), (1, 0), 0), ((6, 50, 70), (2, 0, 1), 2),
+                                            ((6, 50, 70), (1, 2, 0), 0), ((4, 1, 90), (2, 1, 0), 2)])
+def test_exact_sum_dim_permuted_views(xs, shape, perm, dim):
+    """exact_sum_dim of a permuted (e.g. transposed) view of a contiguous tensor: the matching
+    dimension of the underlying layout is reduced in place and the output put back in the view's
+    order; every fibre vs the oracle."""
+    import torch
+    n = int(np.prod(shape))
+    x = synth.gen.generate("c2", 31, n).reshape(shape)
+    t = torch.from_numpy(x).cuda().permute(perm)
+    assert not t.is_contiguous() or shape[1] == 1
+    out = xs.exact_sum_dim(t, dim).cpu().numpy()
+    xv = np.transpose(x, perm)
+    assert out.shape == np.sum(xv, axis=dim).shape
+    fib = np.moveaxis(xv, dim, -1).reshape(-1, xv.shape[dim])
+    for k in range(fib.shape[0]):
+        r, _ = oracle.exact_sum(np.ascontiguousarray(fib[k]))
+        assert out.reshape(-1)[k].view(np.uint64) == np.uint64(r.bits), (shape, perm, dim, k)
+    kd = xs.exact_sum_dim(t, dim, keepdim=True)
+    assert tuple(kd.shape) == tuple(np.sum(xv, axis=dim, keepdims=True).shape)

@@ -529,7 +529,7 @@ def sum_segments_csr(x, offsets, canon: bool = False, flags: bool = False):
     return _segments(x, offsets.numel() - 1, 0, offsets, canon, flags)
 
 
-def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
+def exact_sum_dim(x, dim=-1, keepdim: bool = False):
     """Exact reduction of a CUDA tensor along one dimension: every output
     element is the correctly rounded (RN-even) sum of its fibre, independent of order - a
     reproducible torch.sum(x, dim). float64 input gives float64, float32 / float16 / bfloat16
@@ -537,15 +537,44 @@ def exact_sum_dim(x, dim: int = -1, keepdim: bool = False):
     e.g. a transpose) reduced over a non-last dimension goes to xsum_sum_strided (no copy);
     otherwise the fibres are laid out as equal contiguous segments (a movedim + contiguous copy
     for other non-contiguous inputs) and summed by
-    xsum_sum_segments_ex (one warp per fibre; one lane per fibre for fibres of <= 256)."""
+    xsum_sum_segments_ex (one warp per fibre; one lane per fibre for fibres of <= 256).
+    `dim` may also be a tuple of dimensions (adjacent ones of a contiguous tensor are merged
+    without a copy) or None (the exact sum of everything, a 0-d tensor, no host synchronization)."""
     torch = _torch()
     if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype not in (torch.float64, torch.float32,
                                                                            torch.float16, torch.bfloat16):
         raise TypeError("expected a float64 / float32 / float16 / bfloat16 CUDA tensor")
+    f64 = x.dtype == torch.float64
+    if dim is None:                              # everything: one fused sum, result stays on the device
+        res, _ = _acc_for(x.device).sum(x.contiguous().reshape(-1))
+        val = res[0:8].clone().view(torch.float64) if f64 else res[44:48].clone().view(torch.float32)
+        out = val.reshape(())
+        return out.reshape((1,) * x.dim()) if keepdim else out
+    if isinstance(dim, (tuple, list)):
+        if x.dim() == 0:
+            raise ValueError("exact_sum_dim needs a tensor with at least one dimension")
+        dims = sorted({int(k) % x.dim() for k in dim})
+        if not dims:
+            raise ValueError("empty dim tuple")
+        if len(dims) == 1:
+            return exact_sum_dim(x, dims[0], keepdim)
+        red = 1
+        for k in dims:
+            red *= x.shape[k]
+        if x.is_contiguous() and dims == list(range(dims[0], dims[-1] + 1)):
+            y = x.reshape(tuple(x.shape[:dims[0]]) + (red,) + tuple(x.shape[dims[-1] + 1:]))   # a view
+            out = exact_sum_dim(y, dims[0])
+        else:
+            keep = [k for k in range(x.dim()) if k not in dims]
+            y = x.permute(keep + dims).contiguous().reshape(tuple(x.shape[k] for k in keep) + (red,))
+            out = exact_sum_dim(y, -1)
+        if keepdim:
+            for k in dims:
+                out = out.unsqueeze(k)
+        return out
     if x.dim() == 0:
         raise ValueError("exact_sum_dim needs a tensor with at least one dimension")
     d = dim % x.dim()
-    f64 = x.dtype == torch.float64
     if not x.is_contiguous() and x.dim() > 1:
         # a permuted view of a contiguous tensor (e.g. a transpose): reduce the matching dimension
         # of the underlying contiguous layout (no copy of the input), then put the output's

@@ -187,3 +187,35 @@ def test_exact_sum_dim_permuted_views(xs, shape, perm, dim):
         assert out.reshape(-1)[k].view(np.uint64) == np.uint64(r.bits), (shape, perm, dim, k)
     kd = xs.exact_sum_dim(t, dim, keepdim=True)
     assert tuple(kd.shape) == tuple(np.sum(xv, axis=dim, keepdims=True).shape)
+
+
+@pytest.mark.parametrize("shape,dim", [((6, 50, 70), (1, 2)), ((6, 50, 70), (0, 1)), ((6, 50, 70), (0, 2)),
+                                       ((6, 50, 70), (-1, 0, 1)), ((6, 50, 70), None), ((5,), None)])
+def test_exact_sum_dim_tuples_and_none(xs, shape, dim):
+    """exact_sum_dim with a tuple of dimensions (adjacent: merged without a copy; otherwise moved
+    last) or None (everything; a 0-d device tensor): the oracle's exact sums, keepdim shapes."""
+    import torch
+    n = int(np.prod(shape))
+    x = synth.gen.generate("c2", 41, n).reshape(shape)
+    t = torch.from_numpy(x).cuda()
+    out = xs.exact_sum_dim(t, dim)
+    ref_shape = np.sum(x, axis=None if dim is None else tuple(dim)).shape
+    assert tuple(out.shape) == tuple(ref_shape)
+    o = out.cpu().numpy().reshape(-1)
+    if dim is None:
+        r, _ = oracle.exact_sum(x.reshape(-1))
+        assert o[0:1].view(np.uint64)[0] == np.uint64(r.bits)
+    else:
+        dims = sorted({k % len(shape) for k in dim})
+        keep = [k for k in range(len(shape)) if k not in dims]
+        fib = np.transpose(x, keep + dims).reshape(o.size, -1)
+        for k in range(o.size):
+            r, _ = oracle.exact_sum(np.ascontiguousarray(fib[k]))
+            assert o[k:k + 1].view(np.uint64)[0] == np.uint64(r.bits), (dim, k)
+    kd = xs.exact_sum_dim(t, dim, keepdim=True)
+    assert tuple(kd.shape) == tuple(np.sum(x, axis=None if dim is None else tuple(dim), keepdims=True).shape)
+    # a narrow format with dim=None gives the binary32 rounding of the exact sum
+    b = synth.gen.bits("c2bf16", 0, 1001)
+    tb = torch.from_numpy(b.view(np.int16)).cuda().view(torch.bfloat16)
+    r, _ = oracle.exact_sum(b, fmt="bf16")
+    assert xs.exact_sum_dim(tb, None).cpu().numpy().reshape(1).view(np.uint32)[0] == r.bits_f32

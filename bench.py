@@ -433,7 +433,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # context: the same step back to back for a few seconds, after the timed region (the board's
     # power cap engages after ~0.1 s; profiles/r01_sustained_power.txt)
     sustained = None
-    if world == 1 and args.sustained_s > 0:
+    if world == 1 and args.sustained_s > 0 and flush is None:      # (an L2-resident input would mislead)
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k_s = max(1, int(args.sustained_s / max(total_ms / K / 1e3, 1e-6)))
         with ClockSampler(local_rank, period_s=0.01) as clk_s:

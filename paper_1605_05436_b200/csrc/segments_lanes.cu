@@ -6,7 +6,8 @@
 // its own column (one thread; lane_round.cuh) - 32 segments per warp, no
 // cross-lane step at all. The lanes of a warp read 32 consecutive segments, so a warp's loads
 // cover one contiguous span of 32*len elements; loads allocate in L1, where the neighbouring
-// bytes of a sector wait for the lane's next load.
+// bytes of a sector wait for the lane's next load. K11c (below) does the same for CSR segments
+// that are mostly short, handing a group's longer segments to the whole warp.
 #include <cuda_runtime.h>
 
 #include "lane_round.cuh"

@@ -105,3 +105,19 @@ def test_csr_workload_offsets():
     lens = np.diff(offs)
     assert offs[0] == 0 and offs.size == cfg["nseg"] + 1 and offs[-1] == cfg["n"]
     assert lens.min() >= 1 and lens.max() <= cfg["maxlen"] and abs(lens.mean() - 4096) < 100
+
+
+def test_f1_measurement_workloads():
+    """c2dim0 is c2's element stream (viewed as [4096, 65536]); c5s16 draws like c5 with its own
+    seed (exponents in [-200, 200], 2^24 segments of 16)."""
+    import synth.gen as g
+    a = g.generate("c2dim0", 12345, 1000)
+    b = g.generate("c2", 12345, 1000)
+    assert (a.view(np.uint64) == b.view(np.uint64)).all()
+    assert g.CONFIGS["c2dim0"]["shape"][0] * g.CONFIGS["c2dim0"]["shape"][1] == g.CONFIGS["c2dim0"]["n"]
+    c = g.CONFIGS["c5s16"]
+    assert c["nseg"] * c["seg_len"] == c["n"]
+    x = g.generate("c5s16", 0, 100_000)
+    e = ((x.view(np.uint64) >> np.uint64(52)) & np.uint64(0x7FF)).astype(np.int64) - 1023
+    assert e.min() >= -200 and e.max() <= 200 and e.min() < -190 and e.max() > 190
+    assert not (x.view(np.uint64) == g.generate("c5", 0, 100_000).view(np.uint64)).all()

@@ -12,13 +12,51 @@ namespace xs {
 // Element loaders: every binary32 / binary16 / bfloat16 value is exactly a binary64 value, so
 // the narrow formats are widened on load (cvt is exact, keeps subnormals, NaN and Inf) and
 // summed by the binary64 decomposition.
+// Native decomposition of a binary32 / binary16 / bfloat16 pattern (t fraction bits, l exponent
+// bits, least subnormal at bit OFF of the 2^-1074 window: 925 / 1050 / 941): |x| = M 2^(k+OFF),
+// M = m | [e != 0] 2^t, k = max(e,1) - 1 (reading R1), chunks of +-M 2^o at
+// digit i = (k+OFF) / 52 as in decompose(); NaN/Inf patterns are marked (spec = 2046) and summed
+// like finite ones, to be cancelled by fix_narrow on the rare path.
+template <int TB, int LB, int OFF>
+__device__ __forceinline__ Chunks dec_narrow(uint32_t b) {
+    constexpr uint32_t EM = (1u << LB) - 1;
+    const uint32_t e = (b >> TB) & EM;
+    const uint32_t m = b & ((1u << TB) - 1);
+    const uint32_t k = (e > 1u ? e : 1u) - 1u;
+    const uint32_t sh = k + OFF;
+    Chunks c;
+    c.i = mulhi_u32(sh, K52);
+    const uint32_t o = sh - 52u * c.i;
+    const int64_t M = (int64_t)(m | ((e != 0u ? 1u : 0u) << TB));
+    const int64_t sM = ((b >> (TB + LB)) & 1u) ? -M : M;
+    c.c0 = (int64_t)(((uint64_t)sM << o) & MASK);
+    c.c1 = sM >> (52u - o);
+    c.spec = e == EM ? 2046u : k;
+    return c;
+}
+template <int TB, int LB, int OFF>
+__device__ __forceinline__ void fix_narrow(int64_t* col, uint32_t b, uint32_t& flags, uint32_t one) {
+    constexpr uint32_t EM = (1u << LB) - 1;
+    if (((b >> TB) & EM) != EM) return;
+    flags |= (b & ((1u << TB) - 1)) ? XSUM_F_NAN : (((b >> (TB + LB)) & 1u) ? XSUM_F_NINF : XSUM_F_PINF);
+    column_add(col, dec_narrow<TB, LB, OFF>(b ^ (1u << (TB + LB))), one);   // the negated pattern cancels it
+}
+
+// K10's loaders: raw(p) loads an element's bits, dec() decomposes them, fix() cancels a NaN/Inf
+// pattern that was added unchecked (rescan). load() widens to binary64 words (exact).
 template <int DT> struct StrLd;
 template <> struct StrLd<XSUM_DT_F64> {
     using T = double;
+    using R = uint2;
     __device__ static __forceinline__ uint2 load(const T* p) {
         uint2 v;
         asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
         return v;
+    }
+    __device__ static __forceinline__ R raw(const T* p) { return load(p); }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t one, uint32_t mone) { return decompose(r.x, r.y, one, mone); }
+    __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
+        column_fix_special(col, r.x, r.y, flags, one);
     }
 };
 __device__ __forceinline__ uint2 widen(float f) {
@@ -27,26 +65,46 @@ __device__ __forceinline__ uint2 widen(float f) {
 }
 template <> struct StrLd<XSUM_DT_F32> {
     using T = float;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint32_t;
+    __device__ static __forceinline__ R raw(const T* p) {
         uint32_t b;
         asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(b) : "l"(p));
-        return widen(__uint_as_float(b));
+        return b;
+    }
+    __device__ static __forceinline__ uint2 load(const T* p) { return widen(__uint_as_float(raw(p))); }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t, uint32_t) { return dec_narrow<23, 8, 925>(r); }
+    __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
+        fix_narrow<23, 8, 925>(col, r, flags, one);
     }
 };
 template <> struct StrLd<XSUM_DT_F16> {
     using T = uint16_t;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint32_t;
+    __device__ static __forceinline__ R raw(const T* p) {
         unsigned short b;
         asm volatile("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(b) : "l"(p));
-        return widen(__half2float(__ushort_as_half(b)));
+        return b;
+    }
+    __device__ static __forceinline__ uint2 load(const T* p) {
+        return widen(__half2float(__ushort_as_half((unsigned short)raw(p))));
+    }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t, uint32_t) { return dec_narrow<10, 5, 1050>(r); }
+    __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
+        fix_narrow<10, 5, 1050>(col, r, flags, one);
     }
 };
 template <> struct StrLd<XSUM_DT_BF16> {
     using T = uint16_t;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint32_t;
+    __device__ static __forceinline__ R raw(const T* p) {
         unsigned short b;
         asm volatile("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(b) : "l"(p));
-        return widen(__uint_as_float((uint32_t)b << 16));
+        return b;
+    }
+    __device__ static __forceinline__ uint2 load(const T* p) { return widen(__uint_as_float(raw(p) << 16)); }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t, uint32_t) { return dec_narrow<7, 8, 941>(r); }
+    __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
+        fix_narrow<7, 8, 941>(col, r, flags, one);
     }
 };
 

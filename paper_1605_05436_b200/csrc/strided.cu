@@ -86,8 +86,7 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
                     regularize_column(col);
                     const typename L::T* qq = qw;
                     for (uint64_t rr = rw; rr < r; ++rr, qq += inner) {
-                        uint2 v = L::load(qq);
-                        column_fix_special(col, v.x, v.y, flags, one);
+                        L::fix(col, L::raw(qq), flags, one);
                     }
                 }
                 regularize_column_inl(col);
@@ -99,14 +98,14 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
             // groups of STR_UNR rows through STR_NB rotating register buffers: STR_NB-1 groups
             // in flight while one is added (K2's scheme; one batch at a time measured 3 TB/s)
             const uint64_t ngroups = (r1 - r0) / STR_UNR;
-            uint2 buf[STR_NB][STR_UNR];
+            typename L::R buf[STR_NB][STR_UNR];
             const typename L::T* lq = q;
             uint64_t lg = 0;
 #pragma unroll
             for (int b = 0; b < STR_NB - 1; ++b) {
                 if (lg < ngroups) {
 #pragma unroll
-                    for (int u = 0; u < STR_UNR; ++u) buf[b][u] = L::load(lq + u * inner);
+                    for (int u = 0; u < STR_UNR; ++u) buf[b][u] = L::raw(lq + u * inner);
                     lq += STR_UNR * inner;
                     ++lg;
                 }
@@ -117,13 +116,13 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
                     if (g >= ngroups) break;
                     if (lg < ngroups) {
 #pragma unroll
-                        for (int u = 0; u < STR_UNR; ++u) buf[(b + STR_NB - 1) % STR_NB][u] = L::load(lq + u * inner);
+                        for (int u = 0; u < STR_UNR; ++u) buf[(b + STR_NB - 1) % STR_NB][u] = L::raw(lq + u * inner);
                         lq += STR_UNR * inner;
                         ++lg;
                     }
 #pragma unroll
                     for (int u = 0; u < STR_UNR; ++u) {
-                        Chunks c = decompose(buf[b][u].x, buf[b][u].y, one, mone);
+                        Chunks c = L::dec(buf[b][u], one, mone);
                         nspec = spec_fold(nspec, c);
                         column_add(col, c, one);
                     }
@@ -135,10 +134,10 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
                 }
             }
             for (; r < r1;) {
-                uint2 v = L::load(q);
+                const typename L::R v = L::raw(q);
                 q += inner;
                 ++r;
-                Chunks c = decompose(v.x, v.y, one, mone);
+                Chunks c = L::dec(v, one, mone);
                 nspec = spec_fold(nspec, c);
                 column_add(col, c, one);
             }

@@ -25,38 +25,56 @@ __device__ __forceinline__ uint4 ld_v4_ca(const uint4* p) {
     asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
+// Loaders: raw(p) the element's bits (L1-allocating), dec() its chunks (binary64 decompose, or
+// the native narrow decode dec_narrow of lane_round.cuh), sflags() the flags of a NaN/Inf pattern.
 template <int DT> struct SlLd;
 template <> struct SlLd<XSUM_DT_F64> {
     using T = double;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint2;
+    __device__ static __forceinline__ R raw(const T* p) {
         uint2 v;
         asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
         return v;
     }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t one) { return decompose(r.x, r.y, one); }
+    __device__ static __forceinline__ uint32_t sflags(R r) { return special_flags(r.x, r.y); }
 };
+template <int TB, int LB>
+__device__ __forceinline__ uint32_t narrow_special_flags(uint32_t b) {
+    return (b & ((1u << TB) - 1)) ? XSUM_F_NAN : (((b >> (TB + LB)) & 1u) ? XSUM_F_NINF : XSUM_F_PINF);
+}
 template <> struct SlLd<XSUM_DT_F32> {
     using T = float;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint32_t;
+    __device__ static __forceinline__ R raw(const T* p) {
         uint32_t b;
         asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(b) : "l"(p));
-        return widen(__uint_as_float(b));
+        return b;
     }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t) { return dec_narrow<23, 8, 925>(r); }
+    __device__ static __forceinline__ uint32_t sflags(R r) { return narrow_special_flags<23, 8>(r); }
 };
 template <> struct SlLd<XSUM_DT_F16> {
     using T = uint16_t;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint32_t;
+    __device__ static __forceinline__ R raw(const T* p) {
         unsigned short b;
         asm volatile("ld.global.nc.b16 %0, [%1];" : "=h"(b) : "l"(p));
-        return widen(__half2float(__ushort_as_half(b)));
+        return b;
     }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t) { return dec_narrow<10, 5, 1050>(r); }
+    __device__ static __forceinline__ uint32_t sflags(R r) { return narrow_special_flags<10, 5>(r); }
 };
 template <> struct SlLd<XSUM_DT_BF16> {
     using T = uint16_t;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    using R = uint32_t;
+    __device__ static __forceinline__ R raw(const T* p) {
         unsigned short b;
         asm volatile("ld.global.nc.b16 %0, [%1];" : "=h"(b) : "l"(p));
-        return widen(__uint_as_float((uint32_t)b << 16));
+        return b;
     }
+    __device__ static __forceinline__ Chunks dec(R r, uint32_t) { return dec_narrow<7, 8, 941>(r); }
+    __device__ static __forceinline__ uint32_t sflags(R r) { return narrow_special_flags<7, 8>(r); }
 };
 
 // Regularize digits [lo, hi] of a lane column (the only ones this segment touched; digits
@@ -119,9 +137,9 @@ k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint
 #else
         int lo = D, hi = -1;                         // touched digit range of this segment
 #endif
-        auto add = [&](uint32_t xlo, uint32_t xhi) {
-            Chunks c = decompose(xlo, xhi, one);
-            if (spec_hit(c.spec)) { flags |= special_flags(xlo, xhi); return; }
+        auto addr = [&](typename L::R rv) {
+            Chunks c = L::dec(rv, one);
+            if (spec_hit(c.spec)) { flags |= L::sflags(rv); return; }
             column_add(col, c, one);
 #ifndef XS_SL_FULL
             lo = min(lo, (int)c.i);
@@ -143,27 +161,26 @@ k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint
                 for (int u = 0; u < 4; ++u) v[u] = ld_v4_ca(pv + r / 2 + u);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    add(v[u].x, v[u].y);
-                    add(v[u].z, v[u].w);
+                    if constexpr (VEC) {
+                        addr(typename L::R{v[u].x, v[u].y});
+                        addr(typename L::R{v[u].z, v[u].w});
+                    }
                 }
                 since += 8;
                 if (since > FLUSH_ELEMS - 8) flush();
             }
         } else {
             for (; r + 8 <= len; r += 8) {
-                uint2 v[8];
+                typename L::R v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = L::load(p + r + u);
+                for (int u = 0; u < 8; ++u) v[u] = L::raw(p + r + u);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) add(v[u].x, v[u].y);
+                for (int u = 0; u < 8; ++u) addr(v[u]);
                 since += 8;
                 if (since > FLUSH_ELEMS - 8) flush();
             }
         }
-        for (; r < len; ++r) {                       // < 8 left: within the window
-            uint2 v = L::load(p + r);
-            add(v.x, v.y);
-        }
+        for (; r < len; ++r) addr(L::raw(p + r));   // < 8 left: within the window
         flush();
         if (hi < 0) lo = hi = 0;
         lane_store_segment(col, flags, o, s, lo, hi);
@@ -202,9 +219,9 @@ k_segments_lanes_csr(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, 
         if (small) {                                             // one lane, one segment
             uint32_t flags = 0;
             int lo = D, hi = -1;
-            auto add = [&](uint32_t xlo, uint32_t xhi) {
-                Chunks c = decompose(xlo, xhi, one);
-                if (spec_hit(c.spec)) { flags |= special_flags(xlo, xhi); return; }
+            auto addr = [&](typename L::R rv) {
+                Chunks c = L::dec(rv, one);
+                if (spec_hit(c.spec)) { flags |= L::sflags(rv); return; }
                 column_add(col, c, one);
                 lo = min(lo, (int)c.i);
                 hi = max(hi, (int)c.i + 1);
@@ -212,16 +229,13 @@ k_segments_lanes_csr(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, 
             const typename L::T* p = x + b;
             uint64_t r = 0;
             for (; r + 8 <= len; r += 8) {                       // len <= 256 < FLUSH_ELEMS: one window
-                uint2 v[8];
+                typename L::R v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = L::load(p + r + u);
+                for (int u = 0; u < 8; ++u) v[u] = L::raw(p + r + u);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) add(v[u].x, v[u].y);
+                for (int u = 0; u < 8; ++u) addr(v[u]);
             }
-            for (; r < len; ++r) {
-                uint2 v = L::load(p + r);
-                add(v.x, v.y);
-            }
+            for (; r < len; ++r) addr(L::raw(p + r));
             if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
             if (hi < 0) lo = hi = 0;
             lane_store_segment(col, flags, o, s, lo, hi);
@@ -237,11 +251,15 @@ k_segments_lanes_csr(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, 
             int since = 0;
             uint64_t r = bj + lane;
             for (; r + 7 * 32 < ej; r += 8 * 32) {
-                uint2 v[8];
+                typename L::R v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = L::load(x + r + u * 32);
+                for (int u = 0; u < 8; ++u) v[u] = L::raw(x + r + u * 32);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) column_add_checked(col, v[u].x, v[u].y, flags, one);
+                for (int u = 0; u < 8; ++u) {
+                    Chunks c = L::dec(v[u], one);
+                    if (spec_hit(c.spec)) flags |= L::sflags(v[u]);
+                    else column_add(col, c, one);
+                }
                 since += 8;
                 if (since > FLUSH_ELEMS - 8) {
                     regularize_column(col);
@@ -249,8 +267,10 @@ k_segments_lanes_csr(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, 
                 }
             }
             for (; r < ej; r += 32) {                            // < 8 per lane left: in the window
-                uint2 v = L::load(x + r);
-                column_add_checked(col, v.x, v.y, flags, one);
+                const typename L::R v = L::raw(x + r);
+                Chunks c = L::dec(v, one);
+                if (spec_hit(c.spec)) flags |= L::sflags(v);
+                else column_add(col, c, one);
             }
             __syncwarp();
             int64_t a0, a1;

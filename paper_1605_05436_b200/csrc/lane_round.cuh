@@ -1,6 +1,7 @@
 // Per-lane (one thread) pieces shared by the kernels whose lanes own independent sums (K10
-// strided reductions, K11 short segments): widening element loaders, canonicalization of one
-// lane column and RN-even rounding from its top three digits, the canonical image.
+// strided reductions, K11 short segments): the native decomposition of narrow-format elements,
+// K10's element loaders, canonicalization of one lane column and RN-even rounding from its top
+// three digits, the canonical image.
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -9,9 +10,6 @@
 
 namespace xs {
 
-// Element loaders: every binary32 / binary16 / bfloat16 value is exactly a binary64 value, so
-// the narrow formats are widened on load (cvt is exact, keeps subnormals, NaN and Inf) and
-// summed by the binary64 decomposition.
 // Native decomposition of a binary32 / binary16 / bfloat16 pattern (t fraction bits, l exponent
 // bits, least subnormal at bit OFF of the 2^-1074 window: 925 / 1050 / 941): |x| = M 2^(k+OFF),
 // M = m | [e != 0] 2^t, k = max(e,1) - 1 (reading R1), chunks of +-M 2^o at
@@ -43,26 +41,21 @@ __device__ __forceinline__ void fix_narrow(int64_t* col, uint32_t b, uint32_t& f
 }
 
 // K10's loaders: raw(p) loads an element's bits, dec() decomposes them, fix() cancels a NaN/Inf
-// pattern that was added unchecked (rescan). load() widens to binary64 words (exact).
+// pattern that was added unchecked (rescan).
 template <int DT> struct StrLd;
 template <> struct StrLd<XSUM_DT_F64> {
     using T = double;
     using R = uint2;
-    __device__ static __forceinline__ uint2 load(const T* p) {
+    __device__ static __forceinline__ R raw(const T* p) {
         uint2 v;
         asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
         return v;
     }
-    __device__ static __forceinline__ R raw(const T* p) { return load(p); }
     __device__ static __forceinline__ Chunks dec(R r, uint32_t one, uint32_t mone) { return decompose(r.x, r.y, one, mone); }
     __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
         column_fix_special(col, r.x, r.y, flags, one);
     }
 };
-__device__ __forceinline__ uint2 widen(float f) {
-    const double d = (double)f;
-    return make_uint2((uint32_t)__double2loint(d), (uint32_t)__double2hiint(d));
-}
 template <> struct StrLd<XSUM_DT_F32> {
     using T = float;
     using R = uint32_t;
@@ -71,7 +64,6 @@ template <> struct StrLd<XSUM_DT_F32> {
         asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(b) : "l"(p));
         return b;
     }
-    __device__ static __forceinline__ uint2 load(const T* p) { return widen(__uint_as_float(raw(p))); }
     __device__ static __forceinline__ Chunks dec(R r, uint32_t, uint32_t) { return dec_narrow<23, 8, 925>(r); }
     __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
         fix_narrow<23, 8, 925>(col, r, flags, one);
@@ -84,9 +76,6 @@ template <> struct StrLd<XSUM_DT_F16> {
         unsigned short b;
         asm volatile("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(b) : "l"(p));
         return b;
-    }
-    __device__ static __forceinline__ uint2 load(const T* p) {
-        return widen(__half2float(__ushort_as_half((unsigned short)raw(p))));
     }
     __device__ static __forceinline__ Chunks dec(R r, uint32_t, uint32_t) { return dec_narrow<10, 5, 1050>(r); }
     __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
@@ -101,7 +90,6 @@ template <> struct StrLd<XSUM_DT_BF16> {
         asm volatile("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(b) : "l"(p));
         return b;
     }
-    __device__ static __forceinline__ uint2 load(const T* p) { return widen(__uint_as_float(raw(p) << 16)); }
     __device__ static __forceinline__ Chunks dec(R r, uint32_t, uint32_t) { return dec_narrow<7, 8, 941>(r); }
     __device__ static __forceinline__ void fix(int64_t* col, R r, uint32_t& flags, uint32_t one) {
         fix_narrow<7, 8, 941>(col, r, flags, one);

@@ -468,8 +468,11 @@ _default_acc: dict = {}
 
 
 def _acc_for(device) -> Accumulator:
+    """The one-shot helpers' accumulator for (device, current stream): a handle is used by one
+    stream at a time (include/xsum.h), so calls on different streams never share scratch/state."""
     torch = _torch()
-    key = (torch.cuda.current_device() if device is None else torch.device(device).index)
+    idx = torch.cuda.current_device() if device is None else torch.device(device).index
+    key = (idx, _stream_ptr(idx))
     acc = _default_acc.get(key)
     if acc is None:
         acc = _default_acc[key] = Accumulator(device)

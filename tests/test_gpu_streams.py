@@ -81,3 +81,25 @@ def test_cuda_graph_capture_of_fused_sum(xs):
         ref, limbs = oracle.exact_sum(x)
         r = xs.Result.from_bytes(res.cpu().numpy().tobytes())
         assert r.bits == ref.bits and (canon.cpu().numpy().view(np.uint64) == limbs).all(), seed
+
+
+def test_one_shot_helpers_per_stream(xs):
+    """exact_sum_dim(dim=None) / fsum on two streams back to back: each stream has its own default
+    handle (no shared scratch/state), so both device results are the oracle's."""
+    import numpy as np
+    import torch
+
+    import oracle
+    import synth
+    a = synth.gen.generate("c2", 51, 3_000_001)
+    b = synth.gen.generate("c2", 52, 2_000_003)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        ra = xs.exact_sum_dim(da, None)
+    with torch.cuda.stream(s2):
+        rb = xs.exact_sum_dim(db, None)
+    torch.cuda.synchronize()
+    assert ra.cpu().numpy().reshape(1).view(np.uint64)[0] == oracle.exact_sum(a)[0].bits
+    assert rb.cpu().numpy().reshape(1).view(np.uint64)[0] == oracle.exact_sum(b)[0].bits

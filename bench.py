@@ -1,15 +1,21 @@
 #!/usr/bin/env python3
 """Benchmark: exactly summed doubles/s on B200 (BASELINE.json metric), one JSON line.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c5|...] [--impl ours|reference]
 
-A step is one pass of the whole hot path over one batch:
+Default workload: BASELINE.json config c4, the one its metric ("at 1/2/4/8 B200") is quoted
+on: n = 2^33 doubles (64 GiB), seed 4, exponent U[-1022,1023], split into N contiguous shards,
+one per GPU (strong scaling). A step is one pass of the whole hot path (SURVEY.md §8(a) rows
+a1-a8) over the whole input:
   N = 1: one fused launch of xsum_sum (decompose + lane-column accumulate + regularize +
-         block/grid merge + canonicalize + round) over the config's input in HBM.
-  N > 1: (torchrun, one process per GPU, NCCL) each rank sums its own shard of the same
-         size (weak scaling), then all-gathers the 384-byte states, merges and rounds.
-Inputs are synthetic (synth/, the recipe in DESIGN.md) and 2 GiB per GPU (> 126 MB L2:
-no flush needed between steps). `--impl reference` times the CPU oracle instead.
+         block/grid merge + canonicalize + round) over the 64 GiB in HBM.
+  N > 1: (torchrun, one process per GPU) every rank sums its shard and the 384-byte states are
+         exchanged and merged: ONE launch per rank with the exchange over
+         NVLink peer memory (xsum_sum_allreduce), or, if that is unavailable or fails its checks
+         (probe before timing; every timed step's flags after it), the shard sums + an NCCL
+         all-gather + xsum_merge_round.
+Inputs are synthetic (synth/, the recipe in DESIGN.md) and larger than the 126 MB L2 (c1 flushes
+it between steps). `--impl reference` times the CPU oracle instead (rank 0 only).
 """
 from __future__ import annotations
 
@@ -40,11 +46,11 @@ def metric_unit(cfg_name: str):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     # c1..c5: BASELINE.json configs; c5csr / c2f32 / c2f16 / c2bf16: measurement workloads of the
     # NEXT rows (CSR segments, other input formats; synth/gen.py)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5csr", "c2f32", "c2f16",
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "c5csr", "c2f32", "c2f16",
                                                          "c2bf16", "c2dim0", "c5s16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -264,6 +270,48 @@ def run_reference(args, rank: int, world: int):
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
+def steps_verdict(xsum, rows, world: int, device) -> str | None:
+    """Check every timed step's result record (rows: K x RESULT_BYTES uint8, host): the same bits
+    and flags in every step and on every rank, and no XSUM_F_PEER_TIMEOUT in ANY step (a timed-out
+    fused step spins ~2 s and returns a value that is not the group's sum). The decision is
+    all-reduced so every rank agrees. Returns None if the steps are valid, else the reason."""
+    import numpy as np
+    import torch
+
+    rs = [xsum.Result.from_bytes(np.asarray(r, dtype=np.uint8).tobytes()) for r in rows]
+    flags_or = 0
+    for r in rs:
+        flags_or |= r.flags
+    bits = {r.bits for r in rs}
+    local_bad = 0
+    if flags_or & xsum.F_PEER_TIMEOUT:
+        local_bad |= 1
+    if len(bits) != 1 or len({r.flags for r in rs}) != 1:
+        local_bad |= 2
+    b0 = rs[0].bits
+    t = torch.tensor([b0 - (1 << 64) if b0 >> 63 else b0, rs[0].flags, local_bad], dtype=torch.int64, device=device)
+    if world > 1:
+        lo, hi = t.clone(), t.clone()
+        allreduce_(lo, torch.distributed.ReduceOp.MIN)
+        allreduce_(hi, torch.distributed.ReduceOp.MAX)
+    else:
+        lo = hi = t
+    bad = int(hi[2])
+    if bad & 1:
+        steps = [i for i, r in enumerate(rs) if r.flags & xsum.F_PEER_TIMEOUT]
+        return f"peer timeout in timed step(s) {steps[:8]} on this rank" if steps else \
+            "peer timeout in a timed step on another rank"
+    if bad & 2:
+        return "results differ between timed steps"
+    if int(lo[0]) != int(hi[0]) or int(lo[1]) != int(hi[1]):
+        return "ranks disagree on the result"
+    return None
+
+
+def step_stats(ms: list[float]) -> dict:
+    return {"median_ms": statistics.median(ms), "min_ms": min(ms), "max_ms": max(ms)}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
@@ -298,7 +346,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         x = synth.device_generate("c5csr", device=dev)
         csr = synth.csr_offsets("c5csr", device=dev)
     elif args.config == "c4":
-        start, stop = dist.shard_range(cfg["n"], rank, world)
+        start, stop = dist.shard_range(cfg["n"], rank, world)   # strong scaling: contiguous shards
         x = synth.device_generate("c4", start, stop - start, device=dev)
     elif args.config == "c3":
         x = synth.device_generate("c3", device=dev)
@@ -310,6 +358,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     acc = xsum.Accumulator(dev)
     tot = xsum.Accumulator(dev) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
+    K = args.steps
+    # one result record per timed step (no extra stream operation between the steps): every
+    # step's bits and flags are checked after the region, not only the last one's
+    res_rows = torch.zeros((max(K, 1), xsum.RESULT_BYTES), dtype=torch.uint8, device=dev)
     # multi-GPU exchange: the fused one-launch step over NVLink peer memory (symmetric memory),
     # or, if the peer buffers cannot be set up on this machine, local sum + NCCL all-gather +
     # merge_round
@@ -328,7 +380,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     elif world > 1 and not seg:
         exchange = f"{args.dist_backend} all-gather of 384-B states + xsum_merge_round"
 
-    def step():
+    def step(i=0):
+        out = res_rows[i]
         if csr is not None:
             xsum.sum_segments_csr(x, csr)
         elif cfg.get("op") == "dim0":
@@ -336,43 +389,49 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         elif seg:
             xsum.sum_segments(x, cfg["seg_len"])
         elif world == 1:
-            acc.sum(x)                                   # one fused launch
+            acc.sum(x, out=out)                          # one fused launch
         elif pe is not None:
-            pe.sum(x, acc)                               # one fused launch incl. the cross-GPU merge
+            pe.sum(x, acc, out=out)                      # one fused launch incl. the cross-GPU merge
         else:
-            dist.exact_sum_distributed(x, acc, tot)     # 2 launches + one NCCL all-gather
+            dist.exact_sum_distributed(x, acc, tot, out=out)   # 2 launches + one NCCL all-gather
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
 
-    K = args.steps
     # inputs smaller than 256 MiB (c1) would be served from the 126 MB L2 on every step after
     # the first: flush L2 by writing a 256 MiB buffer before each timed step (outside its events)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if x.numel() * x.element_size() < (256 << 20) \
         else None
 
     def timed_region():
+        res_rows.zero_()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         l0 = xsum.launch_count()
-        # events bracket the K steps; per-step events only when L2 flushes sit between the steps
-        # (otherwise they would add a stream operation between consecutive kernels)
+        # an event at every step boundary (per-step median / min / max); with L2 flushes the flush
+        # sits between a step's end event and the next step's start event
         with ClockSampler(local_rank) as clk:
             for i in range(K):
                 if flush is not None:
                     flush.zero_()
                 if flush is not None or i == 0:
                     ev[i][0].record(stream)
-                step()
-                if flush is not None or i == K - 1:
-                    ev[i][1].record(stream)
+                step(i)
+                ev[i][1].record(stream)
             torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         return ev, clk, xsum.launch_count() - l0
+
+    def step_ms(ev):
+        out = []
+        for i in range(K):
+            a = ev[i][0] if (flush is not None or i == 0) else ev[i - 1][1]
+            out.append(a.elapsed_time(ev[i][1]))
+        return out
 
     ev, clk, launches = timed_region()
     # a region that saw a hardware / thermal slowdown, or SM clocks far below max with no reason
@@ -384,21 +443,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if float(bad.item()):
         first_clocks = clk.summary()
         ev, clk, launches = timed_region()
-    if world > 1 and not seg:                              # every rank holds the same exact result
-        res_dev = acc._res if pe is not None else tot._res
-        rr = xsum.Result.from_bytes(res_dev.cpu().numpy().tobytes())
-        bits = torch.tensor([rr.bits - (1 << 64) if rr.bits >> 63 else rr.bits, rr.flags], dtype=torch.int64,
-                            device=dev)
-        lo, hi = bits.clone(), bits.clone()
-        allreduce_(lo, torch.distributed.ReduceOp.MIN)
-        allreduce_(hi, torch.distributed.ReduceOp.MAX)
-        if not torch.equal(lo, hi) or int(hi[1]) & xsum.F_PEER_TIMEOUT:
-            raise RuntimeError(f"ranks disagree or the peer exchange timed out: {lo.tolist()} {hi.tolist()}")
+    # every timed step's result: identical bits on every step and rank, no peer timeout in ANY
+    # step; a fused region that fails this is re-timed on the NCCL path
+    fused_rejected = None
+    if not seg:
+        why = steps_verdict(xsum, res_rows.cpu().numpy(), world, dev)
+        if why and pe is not None:
+            fused_rejected = why
+            pe = None
+            exchange = f"NCCL all-gather of 384-B states + xsum_merge_round (fused step re-timed after: {why})"
+            for _ in range(max(3, args.warmup)):
+                step()
+            ev, clk, launches = timed_region()
+            why = steps_verdict(xsum, res_rows.cpu().numpy(), world, dev)
+        if why:
+            raise RuntimeError(f"timed steps invalid: {why}")
+    per_step = step_ms(ev)
     # span of the K steps; with L2 flushes in between, the sum of the steps' own times
-    if flush is not None:
-        total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    else:
-        total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    total_ms = sum(per_step) if flush is not None else ev[0][0].elapsed_time(ev[-1][1])
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         allreduce_(t, torch.distributed.ReduceOp.MAX)
@@ -406,18 +468,33 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     n_all = n_local * world
     value = n_all * K / (total_ms / 1e3)
 
-    # dominant kernel: the accumulate launch (N=1 the step is exactly that one launch: its
-    # average duration is the rank's span / K, launch gaps included)
-    if world == 1:
+    # dominant kernel: the accumulate launch. N=1: the step is exactly that one launch, so its
+    # average duration is the span / K (launch gaps included). N>1: the fused step's local part,
+    # i.e. the same kernel without the exchange (xsum_sum on the shard, one launch), timed with
+    # events on its stream; exchange_us = step - local part.
+    scaling = None
+    if world == 1 or seg:
         kern_ms = total_ms / K
-    else:   # time the local accumulate alone with events on its stream
-        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
-        for a, b in kev:
-            a.record(stream)
-            acc.reset().add(x)
-            b.record(stream)
+    else:
+        nk = 10
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        acc.sum(x)
+        a_ev.record(stream)
+        for _ in range(nk):
+            acc.sum(x)
+        b_ev.record(stream)
         torch.cuda.synchronize()
-        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+        kern_ms = a_ev.elapsed_time(b_ev) / nk
+        km = torch.tensor([kern_ms], dtype=torch.float64, device=dev)
+        allreduce_(km, torch.distributed.ReduceOp.MAX)
+        local_max = float(km.item())
+        step_avg = total_ms / K
+        scaling = {"local_sum_ms": local_max, "step_ms": step_avg,
+                   "exchange_us": 1e3 * (step_avg - local_max),
+                   "efficiency_est": local_max / step_avg,
+                   "note": "efficiency_est = t_local / t_step, i.e. t_1 / (p t_p) with t_1 estimated as p x this "
+                           "GPU count's slowest local shard scan (the scan is HBM-bound, linear in n); the driver "
+                           "computes the measured efficiency from its own per-N runs"}
     peak, peak_src = measured_peak_hbm()
     esz = x.element_size()                                   # algorithmic bytes per summand
     achieved = esz * n_local / (kern_ms / 1e3) / 1e9
@@ -444,47 +521,69 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             torch.cuda.synchronize()
         ms_s = a_ev.elapsed_time(b_ev)
         cs = clk_s.summary()
+        sus_gbs = esz * n_local * k_s / (ms_s / 1e3) / 1e9
         sustained = {"value": n_local * k_s / (ms_s / 1e3), "unit": unit, "steps": k_s, "seconds": ms_s / 1e3,
+                     "achieved_gbs": sus_gbs, "frac": sus_gbs / peak,
                      "sm_mhz": cs.get("sm_mhz"), "reasons": cs.get("reasons"),
                      "note": "context only (value is the timed region's): the same step back to back; "
-                             "the 1000 W cap lowers SM clocks after ~0.1 s"}
+                             "the 1000 W cap lowers SM clocks after ~0.1 s; frac against the same peak as roofline"}
 
-    # check the result once (device result vs nothing host-side: the parity tests do that)
     e2e = None
-    if not args.no_e2e and not seg and esz * n_local <= (16 << 30):
+    if not args.no_e2e and not seg:
         if world == 1:
-            e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev, unit)
+            e2e = measure_e2e(xsum, torch, x, args.e2e_steps, dev, unit,
+                              want_bits=xsum.Result.from_bytes(res_rows[K - 1].cpu().numpy().tobytes()).bits)
         else:
             e2e = measure_e2e_multi(xsum, torch, dist, x, args.e2e_steps, dev, pe, acc, tot, world)
     # the timed step's exact result (the state the last step left), for the record
     result = None
-    if world == 1 and not seg:
+    if not seg:
         import hashlib
-        r_gpu, canon_gpu = acc.exact()
-        result = {"value_hex": f"{r_gpu.bits:016x}", "flags": r_gpu.flags,
-                  "image_sha256": hashlib.sha256(np.asarray(canon_gpu, dtype="<u8").tobytes()).hexdigest()}
+        r_gpu = xsum.Result.from_bytes(res_rows[K - 1].cpu().numpy().tobytes())
+        _, canon_gpu = acc.exact() if world == 1 else (None, None)
+        result = {"value_hex": f"{r_gpu.bits:016x}", "flags": r_gpu.flags, "count": r_gpu.count}
+        if canon_gpu is not None:
+            result["image_sha256"] = hashlib.sha256(np.asarray(canon_gpu, dtype="<u8").tobytes()).hexdigest()
+        if world == 1:
+            result["sig53_exp2"] = [r_gpu.sig53, r_gpu.exp2]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, m, passes, dt, gen_name, (r_cpu, limbs_cpu) = oracle_rate(args.config)
         cpu = {"value": rate, "unit": unit, "cores": cores, "kind": "oracle",
                "sample": f"{gen_name} elements [0, {m}) summed {passes}x by the oracle in {dt:.2f} s "
                          f"on {cores} host threads = {dt * cores:.1f} CPU-s ({cpu_model()})"}
-        if result is not None and gen_name == args.config and m == n_local:
-            # the sample is the whole workload: the oracle's exact sum vs the timed GPU result
-            cpu["matches_gpu"] = bool(r_cpu.bits == r_gpu.bits and r_cpu.flags == r_gpu.flags and
-                                      (np.asarray(limbs_cpu) == np.asarray(canon_gpu)).all())
+        st = oracle_single_thread(gen_name)
+        if st is not None:
+            cpu["single_thread"] = st
+        if result is not None and gen_name == args.config:
+            if m == n_local:
+                # the sample is the whole workload: the oracle's exact sum vs the timed GPU result
+                cpu["matches_gpu"] = bool(r_cpu.bits == r_gpu.bits and r_cpu.flags == r_gpu.flags and
+                                          (np.asarray(limbs_cpu) == np.asarray(canon_gpu)).all())
+            elif cfg["kind"] != "bits" and m < n_local:
+                # the sample is a prefix of the workload: the same prefix summed on the GPU
+                rs, cs_ = xsum.Accumulator(dev).sum(x[:m], canon=True)
+                rs = xsum.Result.from_bytes(rs.cpu().numpy().tobytes())
+                cpu["matches_gpu_on_sample"] = bool(rs.bits == r_cpu.bits and rs.flags == r_cpu.flags and
+                                                    (cs_.cpu().numpy().view(np.uint64) ==
+                                                     np.asarray(limbs_cpu)).all())
     if rank == 0:
+        cfg_out = {"workload": wl["desc"], "n_per_gpu": n_local, "n_total": n_all,
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": ("L2 flushed (256 MiB write) before every timed step; steps timed individually"
+                          if flush is not None else
+                          f"inputs {x.numel() * x.element_size() / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)"),
+                   "step": ("xsum_sum_segments_csr" if csr is not None else "xsum_sum_segments" if seg else
+                            "xsum_sum fused launch" if world == 1 else exchange)}
+        if fused_rejected:
+            cfg_out["fused_rejected"] = fused_rejected
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": K,
             "warmup": max(3, args.warmup), "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": wl["desc"], "n_per_gpu": n_local, "n_total": n_all,
-                       "parallelism": f"dp{world}" if world > 1 else "single",
-                       "l2": ("L2 flushed (256 MiB write) before every timed step; steps timed individually"
-                              if flush is not None else
-                              f"inputs {x.numel() * x.element_size() / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)"),
-                       "step": ("xsum_sum_segments_csr" if csr is not None else "xsum_sum_segments" if seg else
-                                "xsum_sum fused launch" if world == 1 else exchange)},
+            "config": cfg_out,
+            "step_times": dict(step_stats(per_step), note="this rank's device time per timed step (CUDA events at "
+                                                          "every step boundary)"),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
                          "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
@@ -493,7 +592,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                     "c2dim0": "k_sum_strided"}.get(args.config, "k_accumulate"),
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local,
                          "peak_source": peak_src, "read_probe_gbs": probe_gbs,
-                         "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None},
+                         "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None,
+                         "sustained_frac": sustained["frac"] if sustained else None},
             "clocks": dict(clk.summary(), **({"remeasured_after": first_clocks} if first_clocks else {})),
             "gpu_launches": launches,
             "e2e": e2e,
@@ -501,18 +601,42 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "cpu_baseline": cpu,
             "result": result,
         }
+        if scaling is not None:
+            line["multi_gpu"] = scaling
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def measure_e2e(xsum, torch, x_dev, steps: int, dev, unit: str = UNIT):
+def oracle_single_thread(gen_name: str, m: int = 1 << 24):
+    """The oracle's single-thread rate on a 2^24-element prefix."""
+    import numpy as np
+
+    import oracle
+    import synth
+    cfg = synth.CONFIGS[gen_name]
+    if cfg.get("fmt") is not None or cfg["kind"] == "csr":
+        return None
+    m = min(m, cfg["n"])
+    x = synth.host_generate(gen_name, 0, m) if cfg["kind"] != "cancel" else synth.host_generate(gen_name, 0, m)
+    oracle.exact_sum(x[:4096], nthreads=1)
+    t0 = time.perf_counter()
+    oracle.exact_sum(x, nthreads=1)
+    dt = time.perf_counter() - t0
+    del x
+    return {"value": m / dt, "cores": 1, "sample": f"{gen_name} elements [0, {m}) once on one thread ({dt:.2f} s)"}
+
+
+def measure_e2e(xsum, torch, x_dev, steps: int, dev, unit: str = UNIT, want_bits: int | None = None):
     """Same metric through the C-ABI with a HOST buffer: per step the pinned-host -> device copy
     of the whole input (overlapped chunk by chunk, xsum_accumulate_host), the sum, the rounding
-    and the 48-byte device -> host read of the result."""
+    and the 48-byte device -> host read of the result. The host copy of the input is pinned once
+    (64 GiB for c4; the box has ~196 GB of host memory), outside the timed steps."""
     n = x_dev.numel()
+    t0 = time.perf_counter()
     host = torch.empty(n, dtype=x_dev.dtype, pin_memory=True)
     host.copy_(x_dev)
+    setup_s = time.perf_counter() - t0
     acc = xsum.Accumulator(dev)
     out = torch.empty(xsum.RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
 
@@ -529,9 +653,16 @@ def measure_e2e(xsum, torch, x_dev, steps: int, dev, unit: str = UNIT):
         one()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    return {"value": n / dt, "unit": unit, "h2d_bytes_per_step": x_dev.element_size() * n,
-            "d2h_bytes_per_step": xsum.RESULT_BYTES,
-            "ms_per_step": dt * 1e3, "api": "xsum_reset + xsum_accumulate_host + xsum_finalize_round + D2H"}
+    got = xsum.Result.from_bytes(out.numpy().tobytes())
+    del host
+    line = {"value": n / dt, "unit": unit, "h2d_bytes_per_step": x_dev.element_size() * n,
+            "d2h_bytes_per_step": xsum.RESULT_BYTES, "steps": steps,
+            "ms_per_step": dt * 1e3, "h2d_gbs": x_dev.element_size() * n / dt / 1e9,
+            "setup_s": setup_s, "api": "xsum_reset + xsum_accumulate_host + xsum_finalize_round + D2H",
+            "timing": "host wall clock around the steps, after torch.cuda.synchronize"}
+    if want_bits is not None:
+        line["matches_device_result"] = got.bits == want_bits
+    return line
 
 
 def allreduce_(t, op):

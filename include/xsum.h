@@ -30,13 +30,12 @@
  *   - NaN / +-Inf inputs are not errors: they set sticky flags (R10).
  *   - No CPU fallback exists: every arithmetic step runs in CUDA kernels built
  *     for sm_100a.
- *   - The accumulate launches (xsum_accumulate*, xsum_sum*, xsum_sum_allreduce) use
- *     programmatic dependent launch: one may start reading its input while the previous
- *     xsum accumulate launch in the stream is still finishing (it waits for that launch
- *     before touching the handle's scratch or state). Data written by any other preceding
- *     stream operation is complete, as with ordinary stream order; an input must therefore
- *     not be written by the immediately preceding xsum accumulate launch (none of them write
- *     their input). XSUM_NO_PDL=1 in the environment disables it.
+ *   - The accumulate launches (xsum_accumulate*, xsum_sum*, xsum_sum_allreduce) of less than
+ *     1 GiB of input use programmatic dependent launch: their blocks may become resident while
+ *     the previous kernel in the stream is finishing, but every block waits for that kernel's
+ *     completion (griddepcontrol.wait) before its first input load, so data written by any
+ *     preceding stream operation is complete and visible, as with ordinary stream order.
+ *     XSUM_NO_PDL=1 in the environment disables it.
  */
 #ifndef XSUM_H
 #define XSUM_H
@@ -87,14 +86,22 @@ typedef enum xsum_status {
 #define XSUM_F_INEXACT32 128u /* the binary32 rounding differs from the exact finite sum */
 #define XSUM_F_PEER_TIMEOUT 256u /* fused multi-GPU step: a peer's state did not arrive within ~2 s;
                                    the value is NOT the group's sum (xsum_sum_allreduce) */
+#define XSUM_F_CAPACITY 512u /* a merge (or an accumulate after a merge whose count the host had not
+                                yet seen) took the summand count past 2^63-1: the count saturates at
+                                2^63-1 and the state is no longer a valid checkpoint image; the
+                                digits stay exact (int64 top digit) */
+#define XSUM_TOP_DIGIT_MAX (1ll << 29) /* |digit[41]| bound: |A| < 2^(1074+1024+63) = 2^2161 and
+                                          R^41 = 2^2132 (R7) */
 
 /* Packed state image (XSUM_STATE_BYTES, little-endian). Exactly mergeable in any
  * order; it is also the checkpoint format and what ranks exchange.
  *   offset 0  u32 magic = XSUM_MAGIC      offset 4  u16 version = XSUM_VERSION
  *   offset 6  u8  w = 52                  offset 7  u8  ndigits = 42
- *   offset 8  u32 flags (XSUM_F_NAN|PINF|NINF|MISMATCH)
+ *   offset 8  u32 flags (XSUM_F_NAN|PINF|NINF|MISMATCH; CAPACITY / PEER_TIMEOUT make the image
+ *             invalid as a checkpoint)
  *   offset 12 u32 reserved (0)            offset 16 u64 count (summands so far)
- *   offset 24 i64 digit[42], digit j worth R^j * 2^-1074, |digit| <= R-1
+ *   offset 24 i64 digit[42], digit j worth R^j * 2^-1074, |digit| <= R-1 (j < 41),
+ *             |digit[41]| <= XSUM_TOP_DIGIT_MAX (merges reject images outside these bounds)
  *   offset 360..383 zero padding */
 typedef struct xsum_state_image {
     uint32_t magic;
@@ -228,8 +235,9 @@ XSUM_API xsum_status xsum_accumulate_host_ex(xsum_ctx *h, const void *h_x, uint6
 /* State += sum of `count` packed state images at d_states (count * XSUM_STATE_BYTES bytes,
  * 8-B aligned): the MapReduce post-process / all-gather merge (§6.1),
  * a Lemma-1 pairwise tree of carry-free additions. Images with a bad
- * header are skipped and set XSUM_F_MISMATCH in the state (reported by finalize).
- * Errors: XSUM_EINVAL, XSUM_ECAPACITY, XSUM_ECUDA. */
+ * header are skipped and set XSUM_F_MISMATCH in the state (reported by finalize). A merged
+ * summand count beyond 2^63-1 saturates and sets XSUM_F_CAPACITY (known only on the device, so
+ * no status code reports it). Errors: XSUM_EINVAL, XSUM_ECUDA. */
 XSUM_API xsum_status xsum_merge(xsum_ctx *h, const void *d_states, uint32_t count, void *stream);
 
 /* Fused post-process ("reads back the p sparse superaccumulators ...
@@ -304,7 +312,11 @@ XSUM_API xsum_status xsum_set_grid_limit(xsum_ctx *h, uint32_t max_blocks);
 /* Release the host handle (never frees caller memory). */
 XSUM_API xsum_status xsum_destroy(xsum_ctx *h);
 
-/* Elements accumulated into the handle so far (host-side counter). */
+/* Summands in the handle's state: the host-side counter of what was accumulated through the
+ * handle since the last reset / sum / load, plus, after a merge, the merged state's count (the
+ * merge enqueues a copy of it; the first xsum_count after a merge waits for that copy, i.e. for
+ * the stream to pass the merge). Saturates at 2^63-1 (then the state carries XSUM_F_CAPACITY).
+ * UINT64_MAX if that wait fails; 0 for a null handle. */
 XSUM_API uint64_t xsum_count(const xsum_ctx *h);
 
 /* Segmented exact sums (BASELINE.json config 5): for s < nseg, d_out[s] = RN-even of the

@@ -19,8 +19,11 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libxsum.so")
-# development only: benchmark an alternative build of the same C-ABI (tools/variants.py)
-SO_PATH = os.environ.get("XSUM_LIBRARY", SO_PATH)
+# development only: an alternative build of the same C-ABI (tools/variants.py, the checked build of
+# tools/checked_build.py) is loaded only when XSUM_DEV=1 is set as well, so a stray XSUM_LIBRARY
+# cannot silently swap the library under test
+if os.environ.get("XSUM_DEV") == "1" and os.environ.get("XSUM_LIBRARY"):
+    SO_PATH = os.environ["XSUM_LIBRARY"]
 
 STATE_BYTES = 384
 RESULT_BYTES = 48
@@ -32,6 +35,8 @@ VERSION = 1
 F_NAN, F_PINF, F_NINF, F_OVERFLOW, F_INEXACT, F_MISMATCH = 1, 2, 4, 8, 16, 32
 F_OVERFLOW32, F_INEXACT32 = 64, 128
 F_PEER_TIMEOUT = 256
+F_CAPACITY = 512
+TOP_DIGIT_MAX = 1 << 29
 
 OK, EINVAL, ECAPACITY, ECUDA, EMISMATCH, ENOMEM = range(6)
 
@@ -253,6 +258,7 @@ class Accumulator:
         self._idx = self.device.index
         self._res_ptr, self._canon_ptr = self._res.data_ptr(), self._canon.data_ptr()
         self._stage = None
+        self._host_refs = []
         h = ctypes.c_void_p()
         _check("xsum_create", L.xsum_create(ctypes.byref(h), self.device.index, self.state.data_ptr(),
                                             self.scratch.data_ptr(), nscr, _stream_ptr(self.device)))
@@ -273,7 +279,16 @@ class Accumulator:
 
     @property
     def count(self) -> int:
-        return int(lib().xsum_count(self._h))
+        """Summands in the state (xsum_count; after a merge it waits for the merged count)."""
+        c = int(lib().xsum_count(self._h))
+        if c == (1 << 64) - 1:
+            raise XsumError("xsum_count", ECUDA)
+        return c
+
+    def _on_device(self, t, what: str = "tensor"):
+        if t.device.index != self._idx:
+            raise ValueError(f"{what} is on {t.device}, the accumulator on {self.device}")
+        return t
 
     def set_grid_limit(self, max_blocks: int) -> "Accumulator":
         """Cap the blocks of an accumulate launch (0 = one per SM)."""
@@ -287,6 +302,8 @@ class Accumulator:
     def add(self, x) -> "Accumulator":
         """Sum a float64 / float32 / float16 / bfloat16 CUDA tensor into the state, exactly."""
         fa, _, name, _ = _fns_for(x)
+        if x.device.index != self._idx:
+            self._on_device(x)
         rc = fa(self._h, x.data_ptr(), x.numel(), _stream_ptr(self._idx))
         if rc:
             raise XsumError(name, rc)
@@ -308,7 +325,12 @@ class Accumulator:
         _check("xsum_accumulate_host_ex", lib().xsum_accumulate_host_ex(
             self._h, x.data_ptr(), x.numel(), _DT[str(x.dtype).replace("torch.", "")], self._stage.data_ptr(),
             self._stage.numel(), _stream_ptr(self.device)))
-        self._host_ref = x          # keep alive until the stream passes the copies
+        # keep every source alive until its copies are done: the stream waited for each chunk's
+        # copy before accumulating it, so an event recorded on it now passes after the last copy
+        # (torch's pinned-memory cache cannot see the library's raw copies)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._host_refs = [(e, t) for e, t in self._host_refs if not e.query()] + [(ev, x)]
         return self
 
     def merge(self, states) -> "Accumulator":
@@ -319,6 +341,7 @@ class Accumulator:
         if not (isinstance(states, torch.Tensor) and states.is_cuda and states.dtype == torch.uint8
                 and states.is_contiguous() and states.numel() % STATE_BYTES == 0):
             raise TypeError("expected a contiguous uint8 CUDA tensor of k*384 bytes")
+        self._on_device(states, "states")
         k = states.numel() // STATE_BYTES
         _check("xsum_merge", lib().xsum_merge(self._h, states.data_ptr(), k, _stream_ptr(self.device)))
         return self
@@ -355,27 +378,39 @@ class Accumulator:
             data = f.read()
         return cls(device).load_state(data)
 
-    def merge_round(self, states, canon: bool = False):
+    def merge_round(self, states, canon: bool = False, out=None):
         """state := sum of the packed state images, then round (one launch; xsum_merge_round).
-        Returns the device (result, canon) like finalize_async."""
+        Returns the device (result, canon) like finalize_async; `out` (optional uint8 CUDA tensor
+        of RESULT_BYTES) receives the result record instead of the accumulator's own buffer."""
         torch = _torch()
         if not (isinstance(states, torch.Tensor) and states.is_cuda and states.dtype == torch.uint8
                 and states.is_contiguous() and states.numel() % STATE_BYTES == 0):
             raise TypeError("expected a contiguous uint8 CUDA tensor of k*384 bytes")
+        self._on_device(states, "states")
+        res = self._res if out is None else self._out(out)
         _check("xsum_merge_round", lib().xsum_merge_round(
-            self._h, states.data_ptr(), states.numel() // STATE_BYTES, self._res.data_ptr(),
+            self._h, states.data_ptr(), states.numel() // STATE_BYTES, res.data_ptr(),
             self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
-        return self._res, (self._canon if canon else None)
+        return res, (self._canon if canon else None)
 
-    def sum_allreduce(self, x, bufs_dev: int, rank: int, world: int, epoch: int, canon: bool = False):
+    def _out(self, out):
+        torch = _torch()
+        if not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.uint8 and out.is_contiguous()
+                and out.numel() == RESULT_BYTES and out.data_ptr() % 8 == 0):
+            raise TypeError("out must be a contiguous, 8-B aligned uint8 CUDA tensor of RESULT_BYTES")
+        return self._on_device(out, "out")
+
+    def sum_allreduce(self, x, bufs_dev: int, rank: int, world: int, epoch: int, canon: bool = False, out=None):
         """Fused multi-GPU step (xsum_sum_allreduce): state := exact sum of every rank's shard, in
         one launch per rank; `bufs_dev` is the device address of the array of the world exchange
-        buffer pointers (dist.PeerExchange sets it up). Returns the device (result, canon)."""
-        x = _as_f64_cuda(x)
+        buffer pointers (dist.PeerExchange sets it up). Returns the device (result, canon); `out`
+        as in merge_round."""
+        x = self._on_device(_as_f64_cuda(x))
+        res = self._res if out is None else self._out(out)
         _check("xsum_sum_allreduce", lib().xsum_sum_allreduce(
-            self._h, x.data_ptr(), x.numel(), bufs_dev, rank, world, epoch, self._res.data_ptr(),
+            self._h, x.data_ptr(), x.numel(), bufs_dev, rank, world, epoch, res.data_ptr(),
             self._canon.data_ptr() if canon else None, _stream_ptr(self.device)))
-        return self._res, (self._canon if canon else None)
+        return res, (self._canon if canon else None)
 
     def to_sparse(self):
         """Sparse image of the state (xsum_to_sparse): (uint8 CUDA tensor of SPARSE_MAX_BYTES,
@@ -398,6 +433,8 @@ class Accumulator:
         if not (isinstance(offsets, torch.Tensor) and offsets.is_cuda and offsets.dtype == torch.int64 and
                 offsets.is_contiguous()):
             raise TypeError("offsets must be a contiguous int64 CUDA tensor")
+        self._on_device(images, "images")
+        self._on_device(offsets, "offsets")
         base = images if images.numel() else torch.zeros(8, dtype=torch.uint8, device=self.device)
         _check("xsum_merge_sparse", lib().xsum_merge_sparse(self._h, base.data_ptr(), offsets.data_ptr(),
                                                             offsets.numel(), _stream_ptr(self.device)))
@@ -419,15 +456,18 @@ class Accumulator:
         res, canon = self.finalize_async(canon=True)
         return Result.from_bytes(res.cpu().numpy().tobytes()), canon.cpu().numpy().view(np.uint64).copy()
 
-    def sum(self, x, canon: bool = False):
+    def sum(self, x, canon: bool = False, out=None):
         """One-shot fused path (xsum_sum / xsum_sum_f32): state := sum(x); returns device
-        (result, canon)."""
+        (result, canon); `out` as in merge_round."""
         _, fs, _, name = _fns_for(x)
-        rc = fs(self._h, x.data_ptr(), x.numel(), self._res_ptr, self._canon_ptr if canon else None,
+        if x.device.index != self._idx:
+            self._on_device(x)
+        res = self._res if out is None else self._out(out)
+        rc = fs(self._h, x.data_ptr(), x.numel(), res.data_ptr(), self._canon_ptr if canon else None,
                 _stream_ptr(self._idx))
         if rc:
             raise XsumError(name, rc)
-        return self._res, (self._canon if canon else None)
+        return res, (self._canon if canon else None)
 
 
 def peer_buffer_bytes(world: int) -> int:
@@ -465,18 +505,27 @@ def decode_sparse(b: bytes) -> dict:
 
 
 _default_acc: dict = {}
+_DEFAULT_ACC_MAX = 16
 
 
 def _acc_for(device) -> Accumulator:
     """The one-shot helpers' accumulator for (device, current stream): a handle is used by one
-    stream at a time (include/xsum.h), so calls on different streams never share scratch/state."""
+    stream at a time (include/xsum.h), so calls on different streams never share scratch/state.
+    The entry holds the torch Stream object (so the stream outlives the entry) and the cache is
+    LRU-bounded: an evicted entry's stream is synchronized before its buffers are released, so a
+    later stream at a reused address never inherits a handle with work in flight."""
     torch = _torch()
     idx = torch.cuda.current_device() if device is None else torch.device(device).index
     key = (idx, _stream_ptr(idx))
-    acc = _default_acc.get(key)
-    if acc is None:
-        acc = _default_acc[key] = Accumulator(device)
-    return acc
+    ent = _default_acc.pop(key, None)
+    if ent is None:
+        ent = (Accumulator(torch.device("cuda", idx)), torch.cuda.current_stream(idx))
+        while len(_default_acc) >= _DEFAULT_ACC_MAX:
+            old_key = next(iter(_default_acc))
+            _, old_stream = _default_acc.pop(old_key)
+            old_stream.synchronize()
+    _default_acc[key] = ent                     # most recently used last
+    return ent[0]
 
 
 def exact_sum(x) -> tuple[Result, np.ndarray]:

@@ -60,6 +60,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
+    pdl_wait_predecessor();      // inputs are read only after the preceding launch completed
 
     // peel up to PV-1 head elements to reach 16-B alignment; <= PV-1 tail elements remain
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / sizeof(E);

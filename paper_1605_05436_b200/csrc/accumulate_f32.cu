@@ -159,6 +159,7 @@ k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
     for (int g = 0; g < F32B_NBIN; ++g) bins[g * 32] = 0;
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
+    pdl_wait_predecessor();      // inputs are read only after the preceding launch completed
     const uint32_t one = p.one;
 
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 4;

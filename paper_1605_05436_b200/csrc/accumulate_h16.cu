@@ -84,6 +84,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
     for (int j = 0; j < C::COLS; ++j) col[j * 32] = 0;
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
+    pdl_wait_predecessor();      // inputs are read only after the preceding launch completed
 
     // peel up to 7 head elements to reach 16-B alignment; <= 7 tail elements remain
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / 2;

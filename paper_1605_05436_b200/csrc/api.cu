@@ -29,7 +29,12 @@ struct xsum_ctx {
     int num_sms;
     xsum_state_image* state;
     uint8_t* scratch;
-    uint64_t count;                 // host-side mirror of the summand count (capacity check)
+    uint64_t count;                 // host-side mirror of the summand count (capacity check); while
+                                    // count_pending: the summands added since the last merge
+    bool count_pending;             // a merge changed the device count; *count_pinned holds it once
+                                    // ev_count completes
+    uint64_t* count_pinned;         // pinned host word (lazily allocated at the first merge)
+    cudaEvent_t ev_count;
     uint32_t grid_limit;            // 0 = one block per SM
     cudaStream_t copy_stream;       // host-buffer path only (lazily created)
     cudaEvent_t ev_ready[2], ev_done[2];
@@ -87,6 +92,33 @@ int sms_of(int dev) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// After a merge the device state's count is the merged total, unknown to the host until the
+// stream gets there: enqueue a copy of it into a pinned word and remember the event; later
+// accumulates add to h->count (the summands since the merge), which xsum_count adds to the
+// copied word. Until then the host capacity check sees only a lower bound; the kernels saturate
+// the count and set XSUM_F_CAPACITY if the true total passes 2^63-1 (count_add).
+xsum_status note_merge(xsum_ctx* h, cudaStream_t s) {
+    if (!h->count_pinned) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&h->count_pinned), sizeof(uint64_t), cudaHostAllocDefault) !=
+            cudaSuccess) {
+            h->count_pinned = nullptr;
+            return XSUM_ECUDA;
+        }
+        if (cudaEventCreateWithFlags(&h->ev_count, cudaEventDisableTiming) != cudaSuccess) {
+            cudaFreeHost(h->count_pinned);
+            h->count_pinned = nullptr;
+            return XSUM_ECUDA;
+        }
+    }
+    if (cudaMemcpyAsync(h->count_pinned, &h->state->count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaEventRecord(h->ev_count, s) != cudaSuccess)
+        return XSUM_ECUDA;
+    h->count_pending = true;
+    h->count = 0;
+    return XSUM_OK;
+}
+
 // 16-bit inputs: one launch per 2^40 summands (the kernel's int64 bin totals stay < 2^63).
 xsum_status run_h16(xsum_ctx* h, const uint16_t* d_x, uint64_t n, int bf16, int overwrite, xsum_result* res,
                     uint64_t* canon, cudaStream_t s) {
@@ -127,7 +159,10 @@ xsum_status sum_h16_api(xsum_ctx* h, const uint16_t* d_x, uint64_t n, int bf16, 
     if (!g.ok) return XSUM_ECUDA;
     xsum_status st = run_h16(h, d_x, n, bf16, 1, static_cast<xsum_result*>(d_res), d_canon,
                              static_cast<cudaStream_t>(stream));
-    if (st == XSUM_OK) h->count = n;
+    if (st == XSUM_OK) {
+        h->count = n;
+        h->count_pending = false;
+    }
     return st;
 }
 
@@ -186,6 +221,7 @@ xsum_status xsum_reset(xsum_ctx* h, void* stream) {
     if (!g.ok) return XSUM_ECUDA;
     if (xs::init_state(h->state, static_cast<cudaStream_t>(stream)) != cudaSuccess) return XSUM_ECUDA;
     h->count = 0;
+    h->count_pending = false;
     return XSUM_OK;
 }
 
@@ -215,7 +251,8 @@ xsum_status xsum_check_state_image(const void* host_image) {
     for (int j = 0; j < XSUM_NDIGITS - 1; ++j)
         if (im.digit[j] > rmax || im.digit[j] < -rmax) return XSUM_EMISMATCH;
     // top digit (R^41 = 2^2132): |A| < 2^(1024+1074+63) bounds it by 2^29
-    if (im.digit[XSUM_NDIGITS - 1] > (1ll << 29) || im.digit[XSUM_NDIGITS - 1] < -(1ll << 29)) return XSUM_EMISMATCH;
+    if (im.digit[XSUM_NDIGITS - 1] > XSUM_TOP_DIGIT_MAX || im.digit[XSUM_NDIGITS - 1] < -XSUM_TOP_DIGIT_MAX)
+        return XSUM_EMISMATCH;
     return XSUM_OK;
 }
 
@@ -231,6 +268,7 @@ xsum_status xsum_load_state(xsum_ctx* h, const void* host_image, void* stream) {
     uint64_t cnt;
     std::memcpy(&cnt, static_cast<const uint8_t*>(host_image) + 16, sizeof cnt);
     h->count = cnt;
+    h->count_pending = false;
     return XSUM_OK;
 }
 
@@ -258,6 +296,7 @@ xsum_status xsum_sum(xsum_ctx* h, const double* d_x, uint64_t n, void* d_res, ui
                        static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
     h->count = n;
+    h->count_pending = false;
     return XSUM_OK;
 }
 
@@ -277,7 +316,8 @@ xsum_status xsum_sum_allreduce(xsum_ctx* h, const double* d_x, uint64_t n, void*
     p.peer.world = world;
     p.peer.epoch = epoch;
     if (xs::accumulate(d_x, n, p, grid_of(h), static_cast<cudaStream_t>(stream)) != cudaSuccess) return XSUM_ECUDA;
-    h->count = n;                                   // host mirror: this rank's shard
+    h->count = n;                                   // host mirror: this rank's shard (the merged
+    h->count_pending = false;                       // group total is in the result record)
     return XSUM_OK;
 }
 
@@ -317,6 +357,7 @@ xsum_status xsum_sum_f32(xsum_ctx* h, const float* d_x, uint64_t n, void* d_res,
                            static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
     h->count = n;
+    h->count_pending = false;
     return XSUM_OK;
 }
 
@@ -407,7 +448,7 @@ xsum_status xsum_merge(xsum_ctx* h, const void* d_states, uint32_t count, void* 
     if (xs::merge_states(h->state, d_states, count, 0, nullptr, nullptr, static_cast<cudaStream_t>(stream)) !=
         cudaSuccess)
         return XSUM_ECUDA;
-    return XSUM_OK;
+    return note_merge(h, static_cast<cudaStream_t>(stream));
 }
 
 xsum_status xsum_to_sparse(xsum_ctx* h, void* d_out, uint32_t* d_nbytes, void* stream) {
@@ -427,7 +468,7 @@ xsum_status xsum_merge_sparse(xsum_ctx* h, const void* d_images, const uint64_t*
     if (!g.ok) return XSUM_ECUDA;
     if (xs::merge_sparse(h->state, d_images, d_offsets, count, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
-    return XSUM_OK;
+    return note_merge(h, static_cast<cudaStream_t>(stream));
 }
 
 xsum_status xsum_merge_round(xsum_ctx* h, const void* d_states, uint32_t count, void* d_res, uint64_t* d_canon,
@@ -439,7 +480,7 @@ xsum_status xsum_merge_round(xsum_ctx* h, const void* d_states, uint32_t count, 
     if (xs::merge_states(h->state, d_states, count, 1, static_cast<xsum_result*>(d_res), d_canon,
                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return XSUM_ECUDA;
-    return XSUM_OK;
+    return note_merge(h, static_cast<cudaStream_t>(stream));
 }
 
 xsum_status xsum_finalize_round(xsum_ctx* h, void* d_res, uint64_t* d_canon, void* stream) {
@@ -464,12 +505,28 @@ xsum_status xsum_destroy(xsum_ctx* h) {
             }
             cudaStreamDestroy(h->copy_stream);
         }
+        if (h->count_pinned) {
+            cudaEventSynchronize(h->ev_count);
+            cudaEventDestroy(h->ev_count);
+            cudaFreeHost(h->count_pinned);
+        }
     }
     delete h;
     return XSUM_OK;
 }
 
-uint64_t xsum_count(const xsum_ctx* h) { return h ? h->count : 0; }
+uint64_t xsum_count(const xsum_ctx* ch) {
+    if (!ch) return 0;
+    xsum_ctx* h = const_cast<xsum_ctx*>(ch);
+    if (h->count_pending) {             // resolve the merged count (waits for the merge's copy)
+        DeviceGuard g(h->device);
+        if (!g.ok || cudaEventSynchronize(h->ev_count) != cudaSuccess) return UINT64_MAX;
+        const uint64_t base = *h->count_pinned;
+        h->count = (base > kMaxCount - h->count) ? kMaxCount : base + h->count;
+        h->count_pending = false;
+    }
+    return h->count;
+}
 
 xsum_status xsum_set_grid_limit(xsum_ctx* h, uint32_t max_blocks) {
     if (!h) return XSUM_EINVAL;

@@ -76,8 +76,8 @@ __device__ __forceinline__ bool peer_exchange_merge(int64_t& b0, int64_t& b1, ui
         const int64_t d0 = slot->digit[lane];
         const int64_t d1 = (lane + 32 < D) ? slot->digit[lane + 32] : 0;
         lemma1_add(a0, a1, d0, d1, lane);
-        c += slot->count;
         f |= slot->flags;
+        c = count_add(c, slot->count, f);
     }
     b0 = a0;
     b1 = a1;
@@ -141,7 +141,7 @@ __device__ __forceinline__ void grid_tail(int64_t a0, int64_t a1, uint32_t bflag
         uint64_t cnt = n;
         if (!p.overwrite) {
             fl |= p.state->flags;
-            cnt += p.state->count;
+            cnt = count_add(cnt, p.state->count, fl);
         }
         regularize_warp(b0, b1, lane);
         if (p.peer.bufs) peer_exchange_merge(b0, b1, fl, cnt, p.peer, lane);   // fused multi-GPU step

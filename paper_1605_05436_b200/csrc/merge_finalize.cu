@@ -34,8 +34,9 @@ __device__ __forceinline__ bool image_ok(const xsum_state_image* im, int64_t d0,
     bool hdr = im->magic == XSUM_MAGIC && im->version == XSUM_VERSION && im->w == W && im->ndigits == D;
     bool ok0 = d0 >= -(R - 1) && d0 <= R - 1;
     bool ok1 = (lane + 32 < D - 1) ? (d1 >= -(R - 1) && d1 <= R - 1)
-                                   : ((lane + 32 == D - 1) ? (d1 >= -(1ll << 40) && d1 <= (1ll << 40)) : true);
-    return hdr && __all_sync(FULL, ok0 && ok1);
+                                   : ((lane + 32 == D - 1) ? (d1 >= -XSUM_TOP_DIGIT_MAX && d1 <= XSUM_TOP_DIGIT_MAX)
+                                                           : true);
+    return hdr && im->count <= COUNT_MAX && __all_sync(FULL, ok0 && ok1);
 }
 
 constexpr int MERGE_WARPS = 16;
@@ -90,7 +91,7 @@ struct SparseImages {
             if (lane == 0) prev = prev_last;
             prev_last = __shfl_sync(FULL, idx, 31);
             if (has) {
-                const int64_t lim = idx < D - 1 ? R - 1 : (1ll << 40);
+                const int64_t lim = idx < D - 1 ? R - 1 : XSUM_TOP_DIGIT_MAX;
                 ok = ok && idx < D && idx > prev && dg != 0 && dg >= -lim && dg <= lim;
                 if (idx < D) scratch[idx] = dg;
             }
@@ -100,7 +101,7 @@ struct SparseImages {
         d1 = (lane + 32 < D) ? scratch[lane + 32] : 0;
         cnt = hd->count;
         fl = hd->flags;
-        return __all_sync(FULL, ok);
+        return __all_sync(FULL, ok) && cnt <= COUNT_MAX;
     }
 };
 
@@ -122,8 +123,9 @@ k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_resul
         uint32_t f;
         if (src.load(s, lane, scr[warp], d0, d1, c, f)) {
             lemma1_add(a0, a1, d0, d1, lane);
-            cnt += c;
-            fl |= f & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT);
+            cnt = count_add(cnt, c, fl);
+            fl |= f & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT |
+                       XSUM_F_CAPACITY);
         } else {
             fl |= XSUM_F_MISMATCH;
         }
@@ -139,7 +141,11 @@ k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_resul
             lemma1_add(a0, a1, b0, b1, lane);
             acc[warp][lane] = a0;
             acc[warp][lane + 32] = a1;
-            if (lane == 0) { cnts[warp] += cnts[warp + stride]; fls[warp] |= fls[warp + stride]; }
+            if (lane == 0) {
+                uint32_t f2 = fls[warp] | fls[warp + stride];
+                cnts[warp] = count_add(cnts[warp], cnts[warp + stride], f2);
+                fls[warp] = f2;
+            }
         }
         __syncthreads();
     }
@@ -149,8 +155,8 @@ k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_resul
         if (!overwrite) {
             int64_t s0 = st->digit[lane], s1 = (lane + 32 < D) ? st->digit[lane + 32] : 0;
             lemma1_add(a0, a1, s0, s1, lane);
-            cnt_all += st->count;
             fl_all |= st->flags;
+            cnt_all = count_add(cnt_all, st->count, fl_all);
         }
         st->digit[lane] = a0;
         if (lane + 32 < D) st->digit[lane + 32] = a1;

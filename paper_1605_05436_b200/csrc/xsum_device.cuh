@@ -42,6 +42,18 @@ constexpr unsigned FULL = 0xffffffffu;
 // 11 bits of headroom per int64 digit here. 2016 is a multiple of 8 and 16 (whole tiles).
 constexpr int FLUSH_ELEMS = 2016;
 
+// Summand counts of merged states: each is <= 2^63-1, so a + b fits in u64; a total beyond
+// 2^63-1 saturates and sets XSUM_F_CAPACITY (include/xsum.h).
+constexpr uint64_t COUNT_MAX = 0x7FFFFFFFFFFFFFFFull;
+__device__ __forceinline__ uint64_t count_add(uint64_t a, uint64_t b, uint32_t& fl) {
+    uint64_t r = a + b;
+    if (r > COUNT_MAX || r < a) {
+        r = COUNT_MAX;
+        fl |= XSUM_F_CAPACITY;
+    }
+    return r;
+}
+
 // ---------------------------------------------------------------------------------
 // Step 2 of the PRAM algorithm: split x into O(1) components whose
 // exponents are multiples of the radix exponent. For binary64 (IEEE, reading R1/R2):
@@ -442,7 +454,8 @@ __device__ __forceinline__ xsum_result finalize_warp_inl(int64_t a0, int64_t a1,
     const uint32_t rf32 = __shfl_sync(FULL, rf, 1);
     if (lane == 0) {
         r.count = count;
-        uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT)) | rf | rf32;
+        uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT |
+                                 XSUM_F_CAPACITY)) | rf | rf32;
         uint32_t v32 = (uint32_t)b32;
         if (!nzu) {                               // exact zero -> +0.0 (reading R9)
             r.msb_exp = INT32_MIN; r.sign = 0; r.sig53 = 0; r.exp2 = 0;

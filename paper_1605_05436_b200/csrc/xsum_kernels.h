@@ -50,15 +50,15 @@ constexpr size_t SCRATCH_BYTES = SCRATCH_STAMP_OFF + (XS_TIMING ? sizeof(int64_t
 
 void note_launch();
 
-// Programmatic dependent launch (sm_90+): an accumulate launch may start its blocks while the
-// previous kernel in the stream is still finishing (its last block merging and rounding, slower
-// SMs streaming their last tiles); the kernel waits for the predecessor's completion
-// (griddepcontrol.wait in grid_tail) before it touches the scratch table or the state, and it
-// only reads its input before that point. A predecessor that is not an xsum accumulate kernel
-// releases its dependents at completion, so inputs produced by earlier kernels are complete.
-// XSUM_NO_PDL=1 in the environment launches normally (A/B measurements). Only launches of less
-// than PDL_MAX_BYTES of input use it: back to back, 2^24-2^26 doubles gain 6-12%, while at 2^28
-// the early blocks' reads slow the previous grid's stragglers (-1..2%, profiles/r01_pdl_ab.txt).
+// Programmatic dependent launch (sm_90+): an accumulate launch may place its blocks on SMs while
+// the previous kernel in the stream is still finishing (its last block merging and rounding,
+// slower SMs streaming their last tiles); each block zeroes its lane columns and then waits for
+// the predecessor's completion (griddepcontrol.wait) BEFORE its first input load. A predecessor
+// may signal its dependents early (e.g. GEMM kernels before their epilogue stores) and its
+// writes are only guaranteed visible after griddepcontrol.wait, so reading the input earlier
+// would be unsafe for arbitrary producers; the overlap kept is the launch and the
+// block prologue. XSUM_NO_PDL=1 in the environment launches normally (A/B measurements). Only
+// launches of less than PDL_MAX_BYTES of input use it.
 bool pdl_enabled();
 constexpr uint64_t PDL_MAX_BYTES = 1ull << 30;
 

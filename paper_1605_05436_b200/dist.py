@@ -52,13 +52,13 @@ def allreduce_exact(acc: Accumulator, group=None) -> Accumulator:
     return acc
 
 
-def exact_sum_distributed(x, acc: Accumulator, total: Accumulator, group=None):
+def exact_sum_distributed(x, acc: Accumulator, total: Accumulator, group=None, out=None):
     """The whole multi-GPU step on this rank's shard x: local fused sum (one launch), NCCL
     all-gather of the 384-byte states, fused merge + round (one launch). Returns the device
-    result record; every rank gets the identical bits."""
+    result record (in `out` if given); every rank gets the identical bits."""
     acc.sum(x)                                   # state := sum(x) (its local rounding is unused)
     states = gather_states(acc.state, group)
-    res, _ = total.merge_round(states)
+    res, _ = total.merge_round(states, out=out)
     return res
 
 
@@ -88,8 +88,8 @@ class PeerExchange:
         self.epoch = 0
         dist.barrier(group=self.group)
 
-    def sum(self, x, acc: Accumulator, canon: bool = False):
+    def sum(self, x, acc: Accumulator, canon: bool = False, out=None):
         """State of `acc` := exact sum over all ranks' shards x (one launch); returns the device
-        (result, canon), bit-identical on every rank."""
+        (result, canon), bit-identical on every rank (the result record in `out` if given)."""
         self.epoch += 1
-        return acc.sum_allreduce(x, self.bufs_dev, self.rank, self.world, self.epoch, canon=canon)
+        return acc.sum_allreduce(x, self.bufs_dev, self.rank, self.world, self.epoch, canon=canon, out=out)

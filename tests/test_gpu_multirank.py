@@ -174,3 +174,90 @@ def test_peer_exchange_symmetric_memory_nccl_world1():
     p.join(timeout=60)
     assert kind == "ok", val
     assert all(val), val
+
+
+# ------------------------------------------------------------------------------------------
+# full-size sharded c4: exactly the arithmetic of the N = 2/4/8 bench run
+# (contiguous shards of dist.shard_range, one fused xsum_sum per shard, the 384-byte states
+# merged by xsum_merge_round) at 2^33 doubles, on one GPU; the fused-exchange
+# protocol runs on the same p states with p virtual ranks.
+# ------------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def c4_oracle_eighths():
+    """The oracle's exact sums of the 8 contiguous eighths of c4 (streamed from the host
+    generator); coarser shards are their exact merges (oracle limb addition)."""
+    import oracle
+    import synth
+    from paper_1605_05436_b200 import dist
+    n = synth.CONFIGS["c4"]["n"]
+    chunk = 1 << 26
+    buf = np.empty(chunk, dtype=np.float64)
+    parts = []
+    for r in range(8):
+        a, b = dist.shard_range(n, r, 8)
+        acc = oracle.Accumulator()
+        for s in range(a, b, chunk):
+            c = min(chunk, b - s)
+            acc.add(synth.host_generate("c4", s, c, out=buf[:c]))
+        parts.append(acc)
+    return parts
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_full_c4_sharded_merge(c4_oracle_eighths, p):
+    import torch
+
+    import oracle
+    import paper_1605_05436_b200 as xsum
+    import synth
+    from paper_1605_05436_b200 import dist
+    xsum.build()
+    cfg = synth.CONFIGS["c4"]
+    n = cfg["n"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * 8 // p + (4 << 30):
+        pytest.skip("not enough device memory for one shard")
+    # the oracle of each of the p shards (merged eighths) and of the whole
+    per = 8 // p
+    shard_ref = []
+    for r in range(p):
+        o = oracle.Accumulator()
+        for k in range(r * per, (r + 1) * per):
+            o.merge(c4_oracle_eighths[k])
+        shard_ref.append(o)
+    whole = oracle.Accumulator()
+    for o in shard_ref:
+        whole.merge(o)
+    ref, limbs = whole.result(), whole.limbs.copy()
+    states = []
+    buf = torch.empty(n // p + 1, dtype=torch.float64, device="cuda")
+    for r in range(p):
+        a, b = dist.shard_range(n, r, p)
+        x = synth.device_generate("c4", a, b - a, device="cuda", out=buf[: b - a])
+        acc = xsum.Accumulator()
+        res, canon = acc.sum(x, canon=True)                 # the bench's per-rank fused launch
+        rr = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+        sr = shard_ref[r].result()
+        assert rr.bits == sr.bits and rr.flags == sr.flags and rr.count == b - a, (p, r)
+        assert (canon.cpu().numpy().view(np.uint64) == shard_ref[r].limbs).all(), (p, r)
+        states.append(acc.state.clone())
+    del buf
+    torch.cuda.empty_cache()
+    st = torch.cat(states)
+    tot = xsum.Accumulator()
+    res, canon = tot.merge_round(st, canon=True)           # the NCCL path's post-process
+    rr = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
+    assert rr.bits == ref.bits and rr.flags == ref.flags and rr.count == n and rr.sig53 == ref.sig53 \
+        and rr.exp2 == ref.exp2
+    assert (canon.cpu().numpy().view(np.uint64) == limbs).all()
+    assert tot.count == n
+    # the fused exchange protocol on the same p states (p virtual ranks, one cooperative launch)
+    results, out, _ = xsum.peer_selftest(st, p, 1)
+    imgs = out.cpu().numpy().reshape(p, -1)
+    for r in range(p):
+        assert results[r].bits == ref.bits and results[r].flags == ref.flags and results[r].count == n, (p, r)
+        assert (imgs[r] == imgs[0]).all()
+    m = xsum.Accumulator().merge(out[:384].clone())
+    _, canon2 = m.exact()
+    assert (canon2 == limbs).all()

@@ -376,3 +376,72 @@ def test_bench_fused_check_two_ranks(mode):
         assert got[0] is not None and got[1] is not None
         if mode == "one_rank_wrong":
             assert got[0] == "another rank disagreed" and got[1].startswith("rank result")
+
+
+def _rows(bits_flags):
+    return np.stack([_result_bytes(b, f).numpy() for b, f in bits_flags])
+
+
+def _steps_verdict_worker(rank: int, world: int, port: int, mode: str, q):
+    """bench.steps_verdict over gloo on CPU: every rank checks its K timed results; the decision
+    is all-reduced."""
+    import torch
+    import torch.distributed as tdist
+    sys.path.insert(0, ROOT)
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        good = 0x3FF0000000000001
+        steps = [(good, 0)] * 4
+        if mode == "timeout_mid" and rank == 1:
+            steps = [(good, 0), (good ^ 8, xsum.F_PEER_TIMEOUT), (good, 0), (good, 0)]   # not the last step
+        elif mode == "drift" and rank == 0:
+            steps = [(good, 0), (good, 0), (good ^ 1, 0), (good, 0)]
+        elif mode == "disagree" and rank == 1:
+            steps = [(good ^ 2, 0)] * 4
+        q.put((rank, bench.steps_verdict(xsum, _rows(steps), world, torch.device("cpu"))))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["ok", "timeout_mid", "drift", "disagree"])
+def test_bench_steps_verdict_two_ranks(mode):
+    """bench.py checks EVERY timed step's result record on every rank: a
+    peer timeout in a middle step, results that change between steps, or ranks that disagree
+    invalidate the region on all ranks (the fused region is then re-timed on the NCCL path)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    modes = ["ok", "timeout_mid", "drift", "disagree"]
+    port = 33600 + (os.getpid() % 2000) + modes.index(mode) * 7
+    procs = [ctx.Process(target=_steps_verdict_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if mode == "ok":
+        assert got == {0: None, 1: None}
+    elif mode == "timeout_mid":
+        assert got[1].startswith("peer timeout in timed step(s) [1]")
+        assert got[0] == "peer timeout in a timed step on another rank"
+    elif mode == "drift":
+        assert got[0] == got[1] == "results differ between timed steps"
+    else:
+        assert got[0] == got[1] == "ranks disagree on the result"
+
+
+def test_xsum_library_override_needs_dev_flag():
+    """A stray XSUM_LIBRARY must not swap the library under test."""
+    code = ("import paper_1605_05436_b200 as x, os; "
+            "print(os.path.basename(os.path.dirname(x.SO_PATH)) + '/' + os.path.basename(x.SO_PATH))")
+    env = dict(os.environ, XSUM_LIBRARY="/nonexistent/libother.so")
+    env.pop("XSUM_DEV", None)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert out.stdout.strip() == "paper_1605_05436_b200/libxsum.so", out.stderr
+    env["XSUM_DEV"] = "1"
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert out.stdout.strip() == "nonexistent/libother.so", out.stderr

@@ -1,7 +1,7 @@
 """Build libxsum with device asserts (XS_CHECKED=1) into build/checked/, for running the GPU
 test-suite as a bounds / int64-headroom check:
 
-    python tools/checked_build.py && XSUM_LIBRARY=build/checked/libxsum.so pytest tests -m gpu
+    python tools/checked_build.py && XSUM_DEV=1 XSUM_LIBRARY=build/checked/libxsum.so pytest tests -m gpu
 """
 import os
 import subprocess

@@ -22,6 +22,7 @@ if sys.argv[1] == "build":
     print(SO)
     sys.exit(0)
 
+os.environ["XSUM_DEV"] = "1"
 os.environ["XSUM_LIBRARY"] = SO
 import numpy as np  # noqa: E402
 import torch  # noqa: E402

@@ -57,7 +57,8 @@ def run_one(so: str, cfg: str, steps: int):
     code = f"""
 import os, sys, json, statistics
 sys.path.insert(0, {ROOT!r})
-os.environ['XSUM_LIBRARY'] = {so!r}
+os.environ["XSUM_DEV"] = "1"
+os.environ["XSUM_LIBRARY"] = {so!r}
 import torch, synth, paper_1605_05436_b200 as xsum
 if {cfg!r}.startswith("n"):
     x = synth.device_generate("c2")[: 1 << int({cfg!r}[1:])].clone()

@@ -149,6 +149,18 @@ typedef struct xsum_result {
                             double rounding; a negative sum that rounds to 0 gives -0.0f) */
 } xsum_result;
 
+/* Outcome of the condition-number-sensitive sum (xsum_sum_condsens), device memory, 152 bytes. */
+typedef struct xsum_condsens_info {
+    uint32_t r;          /* truncation parameter of the last iteration: 2, 4, 16, or 256 (the exact pass) */
+    uint32_t iterations; /* 1..4 (r = 2, 4, 16, 256) */
+    int32_t e_cut;       /* largest truncation index of the last iteration; -1 if nothing was truncated */
+    uint32_t exact;      /* 1: the last iteration truncated nothing, value = RN-even of the exact sum */
+    uint32_t rule;       /* stopping condition used: 1 or 2 */
+    uint32_t nnz;        /* entries of the root (truncated iterations; 0 for the exact pass) */
+    uint64_t root[16];   /* the root's r-truncated sparse superaccumulator, records (digit << 6) | index in
+                            descending index order (the sparse image record format), zero-padded */
+} xsum_condsens_info;
+
 typedef struct xsum_ctx xsum_ctx;
 
 /* Sizes of the caller-provided device buffers. */
@@ -344,6 +356,27 @@ XSUM_API xsum_status xsum_sum_segments_ex(const void *d_x, int dtype, uint64_t n
  * Outputs as xsum_sum_segments. Errors: XSUM_EINVAL, XSUM_ECUDA. */
 XSUM_API xsum_status xsum_sum_segments_csr(const double *d_x, const uint64_t *d_offsets, uint64_t nseg,
                                   double *d_out, uint64_t *d_canon, uint32_t *d_flags, void *stream);
+
+/* Condition-number-sensitive exact-or-faithful sum (§4):
+ * the paper's iteration r = 2, 4, 16 (r <- r^2) over the complete binary
+ * summation tree of d_x[0..n) in index order (reading C2), every internal node the
+ * r-truncated Lemma-1 sum (Lemma 2 :859-872) of its children;
+ * after each iteration the root is rounded to nearest even (y) and the iteration stops when the
+ * stopping condition `rule` holds - 1: y = y (+) n eps_min = y (+) -n eps_min,
+ * 2: the least significant bit of y is >= ceil(log2 n) + 2 binary orders above eps_min
+ * (reading C4) - with eps_min = R^E_cut 2^-1074 from the largest truncation
+ * index over all nodes (reading C3), or when nothing was truncated. If r = 16 does not stop, the
+ * exact dense sum (r = 256 truncates nothing) runs. Then *d_res holds y (a FAITHFUL rounding of
+ * the exact sum, the RN-even rounding when info.exact; direction / INEXACT refer to the
+ * truncated root T), *d_info the iteration record, d_canon (optional, 34 limbs) the canonical
+ * image of T. NaN / +-Inf inputs set flags and the value per R10. Stream-ordered, no host
+ * synchronization: every iteration is enqueued and an iteration after a stop exits at entry.
+ * d_work: device scratch of xsum_condsens_work_bytes(n) bytes, 256-B aligned, no initialization,
+ * not shared by concurrent calls. d_x 8-B aligned. Errors: XSUM_EINVAL (null / misaligned
+ * pointers, rule not 1 or 2, d_work too small), XSUM_ECUDA. */
+XSUM_API size_t xsum_condsens_work_bytes(uint64_t n);
+XSUM_API xsum_status xsum_sum_condsens(const double *d_x, uint64_t n, int rule, void *d_work, size_t work_bytes,
+                                       void *d_res, void *d_info, uint64_t *d_canon, void *stream);
 
 /* Static string for a status code. */
 XSUM_API const char *xsum_status_str(xsum_status s);

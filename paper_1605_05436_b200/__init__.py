@@ -55,7 +55,7 @@ EXPORTS = ("xsum_state_bytes", "xsum_scratch_bytes", "xsum_result_bytes", "xsum_
            "xsum_to_sparse", "xsum_merge_sparse", "xsum_peer_buffer_bytes", "xsum_sum_allreduce",
            "xsum_peer_selftest", "xsum_sum_segments_ex", "xsum_accumulate_host_ex", "xsum_save_state",
            "xsum_check_state_image", "xsum_load_state", "xsum_sum_strided_work_bytes", "xsum_sum_strided",
-           "xsum_sum_segments_ws", "xsum_sum_segments_csr_lanes")
+           "xsum_sum_segments_ws", "xsum_sum_segments_csr_lanes", "xsum_condsens_work_bytes", "xsum_sum_condsens")
 
 
 class XsumError(RuntimeError):
@@ -108,6 +108,8 @@ def lib() -> ctypes.CDLL:
             "xsum_sum_strided": ([p, i32, u64, u64, u64, p, p, p, p, sz, p], i32),
             "xsum_sum_segments_ws": ([p, i32, u64, u64, p, p, p, p, p, p, p], i32),
             "xsum_sum_segments_csr_lanes": ([p, i32, u64, p, p, p, p, p, p, p], i32),
+            "xsum_condsens_work_bytes": ([u64], sz),
+            "xsum_sum_condsens": ([p, u64, i32, p, sz, p, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -468,6 +470,60 @@ class Accumulator:
         if rc:
             raise XsumError(name, rc)
         return res, (self._canon if canon else None)
+
+
+CONDSENS_INFO_BYTES = 152
+
+
+@dataclass(frozen=True)
+class CondSensInfo:
+    """Host copy of ``xsum_condsens_info`` (include/xsum.h): the last iteration of the
+    condition-number-sensitive sum."""
+    r: int
+    iterations: int
+    e_cut: int | None            # None: nothing was truncated
+    exact: bool
+    rule: int
+    root: dict                   # {index: digit} of the root's r-truncated sparse superaccumulator
+
+    @staticmethod
+    def from_bytes(b) -> "CondSensInfo":
+        a = np.frombuffer(bytes(b), dtype=np.uint8)
+        assert a.size == CONDSENS_INFO_BYTES
+        r, it = (int(v) for v in a[0:8].view(np.uint32))
+        e_cut = int(a[8:12].view(np.int32)[0])
+        exact, rule, nnz = (int(v) for v in a[12:24].view(np.uint32))
+        rec = a[24:24 + 8 * 16].view(np.int64)[:nnz]
+        return CondSensInfo(r=r, iterations=it, e_cut=None if e_cut < 0 else e_cut, exact=bool(exact), rule=rule,
+                            root={int(v & 63): int(v >> 6) for v in rec})
+
+
+def sum_condsens(x, rule: int = 1, canon: bool = False, work=None):
+    """Condition-number-sensitive sum of a float64 CUDA tensor (xsum_sum_condsens):
+    the r = 2, 4, 16 truncated iterations with a stopping condition (rule 1 or 2), then the exact
+    pass if needed. Returns device tensors (result record, info record, canonical image of the
+    truncated root or None); no host synchronization."""
+    torch = _torch()
+    x = _as_f64_cuda(x)
+    nb = int(lib().xsum_condsens_work_bytes(x.numel()))
+    if work is None or work.numel() < nb:
+        work = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    res = torch.empty(RESULT_BYTES, dtype=torch.uint8, device=x.device)
+    info = torch.empty(CONDSENS_INFO_BYTES, dtype=torch.uint8, device=x.device)
+    cn = torch.empty(CANON_LIMBS, dtype=torch.int64, device=x.device) if canon else None
+    xp = x if x.numel() else torch.zeros(1, dtype=torch.float64, device=x.device)
+    with torch.cuda.device(x.device):
+        _check("xsum_sum_condsens", lib().xsum_sum_condsens(
+            xp.data_ptr(), x.numel(), rule, work.data_ptr(), work.numel(), res.data_ptr(), info.data_ptr(),
+            cn.data_ptr() if cn is not None else None, _stream_ptr(x.device)))
+    return res, info, cn
+
+
+def condsens_sum(x, rule: int = 1):
+    """Host view of sum_condsens: (Result, CondSensInfo, canonical image of the truncated root)."""
+    res, info, cn = sum_condsens(x, rule, canon=True)
+    return (Result.from_bytes(res.cpu().numpy().tobytes()), CondSensInfo.from_bytes(info.cpu().numpy().tobytes()),
+            cn.cpu().numpy().view(np.uint64).copy())
 
 
 def peer_buffer_bytes(world: int) -> int:

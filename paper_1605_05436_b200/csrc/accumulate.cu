@@ -61,6 +61,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     if (tid == 0) blk_flags = 0;
     uint32_t flags = 0;
     pdl_wait_predecessor();      // inputs are read only after the preceding launch completed
+    if (p.skip && *(volatile const uint32_t*)p.skip) return;     // K12: an earlier iteration stopped
 
     // peel up to PV-1 head elements to reach 16-B alignment; <= PV-1 tail elements remain
     uint64_t head = ((16 - ((uintptr_t)x & 15)) & 15) / sizeof(E);

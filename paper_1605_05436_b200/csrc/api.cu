@@ -72,6 +72,7 @@ xs::AccParams acc_params(xsum_ctx* h, int overwrite, xsum_result* res, uint64_t*
     p.peer.bufs = nullptr;
     p.peer.rank = p.peer.world = 0;
     p.peer.epoch = 0;
+    p.skip = nullptr;
     return p;
 }
 
@@ -614,6 +615,23 @@ xsum_status xsum_sum_segments_csr_lanes(const void* d_x, int dtype, uint64_t nse
     return xs::sum_segments_lanes_csr(d_x, dtype, nseg, d_offsets, o, static_cast<unsigned long long*>(d_ticket),
                                       sms_of(dev), static_cast<cudaStream_t>(stream)) == cudaSuccess ? XSUM_OK
                                                                                                      : XSUM_ECUDA;
+}
+
+size_t xsum_condsens_work_bytes(uint64_t n) { return xs::condsens_work_bytes(n); }
+
+xsum_status xsum_sum_condsens(const double* d_x, uint64_t n, int rule, void* d_work, size_t work_bytes, void* d_res,
+                              void* d_info, uint64_t* d_canon, void* stream) {
+    if (rule != 1 && rule != 2) return XSUM_EINVAL;
+    if (!d_res || !aligned(d_res, 8) || !d_info || !aligned(d_info, 8) || (d_canon && !aligned(d_canon, 8)))
+        return XSUM_EINVAL;
+    if (!d_work || !aligned(d_work, 256) || work_bytes < xs::condsens_work_bytes(n)) return XSUM_EINVAL;
+    if (n && (!d_x || !aligned(d_x, 8))) return XSUM_EINVAL;
+    if (n > kMaxCount) return XSUM_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XSUM_ECUDA;
+    return xs::condsens_sum(d_x, n, rule, d_work, work_bytes, static_cast<xsum_result*>(d_res),
+                            static_cast<xsum_condsens_info*>(d_info), d_canon, sms_of(dev),
+                            static_cast<cudaStream_t>(stream)) == cudaSuccess ? XSUM_OK : XSUM_ECUDA;
 }
 
 size_t xsum_sum_strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int device) {

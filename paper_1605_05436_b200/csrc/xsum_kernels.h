@@ -34,6 +34,8 @@ struct AccParams {
     uint32_t one;              // = 1  } opaque to the compiler: keeps selected integer ops as IMADs
     uint32_t mone;             // = -1 } on the FMA pipe instead of ALU-pipe IADD3s
     PeerParams peer;           // fused cross-GPU exchange after the grid merge (bufs null: none)
+    const uint32_t* skip;      // non-null: the launch does nothing if *skip != 0 when it starts (read
+                               // after the predecessor completed; K12's exact pass)
 };
 
 // XS_TIMING=1: diagnostic builds (tools/timing_probe.py) stamp %globaltimer per block; 0 in the product
@@ -119,6 +121,10 @@ cudaError_t to_sparse(const xsum_state_image* st, void* out, uint32_t* nbytes, c
 cudaError_t peer_selftest(const xsum_state_image* states, uint8_t* const* bufs, uint32_t world, uint64_t epoch,
                           xsum_result* res, xsum_state_image* out, cudaStream_t s);
 cudaError_t finalize(const xsum_state_image* st, xsum_result* res, uint64_t* canon, cudaStream_t s);
+// K12 (condsens.cu): the condition-number-sensitive iteration of PAPER.md:895-918
+size_t condsens_work_bytes(uint64_t n);
+cudaError_t condsens_sum(const double* x, uint64_t n, int rule, void* work, size_t work_bytes, xsum_result* res,
+                         xsum_condsens_info* info, uint64_t* canon, int num_sms, cudaStream_t s);
 // Per-segment outputs (any may be null): binary64 / binary32 roundings, canonical images, flags.
 struct SegOut {
     double* out;

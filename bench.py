@@ -51,7 +51,7 @@ def parse():
     # c1..c5: BASELINE.json configs; c5csr / c2f32 / c2f16 / c2bf16: measurement workloads of the
     # NEXT rows (CSR segments, other input formats; synth/gen.py)
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "c5csr", "c2f32", "c2f16",
-                                                         "c2bf16", "c2dim0", "c5s16"])
+                                                         "c2bf16", "c2dim0", "c5s16", "c2cs", "c3cs"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sustained-s", type=float, default=2.0,
@@ -81,6 +81,8 @@ def workload(cfg_name: str, world: int) -> dict:
         "c2bf16": "c2bf16: n=2^28 bfloat16, seed 8, uniform over the finite bit patterns",
         "c2dim0": "c2dim0: c2's 2^28 doubles as a [4096, 65536] matrix, exact_sum_dim over dim 0 (65536 sums)",
         "c5s16": "c5s16: 2^24 segments x 16 doubles, seed 10, exponent U[-200,200]",
+        "c2cs": "c2cs: c2's 2^28 doubles, condition-number-sensitive sum (xsum_sum_condsens, rule 1)",
+        "c3cs": "c3cs: c3's 2^28 + 2^20 doubles (ill-conditioned), condition-number-sensitive sum (rule 1)",
     }[cfg_name]
     if cfg_name == "c4":
         n_total = cfg["n"]
@@ -180,6 +182,25 @@ def profiled_traffic(cfg_name: str):
 # ------------------------------------------------------------------------------------------
 # CPU oracle arm (cpu_baseline and --impl reference)
 # ------------------------------------------------------------------------------------------
+SEG_CFGS = ("c5", "c5csr", "c5s16", "c2dim0")
+
+
+def oracle_segments_input(cfg_name: str):
+    """The host input of a segmented workload in segment order: (x, offsets or None, seg_len)."""
+    import numpy as np
+
+    import synth
+    cfg = synth.CONFIGS[cfg_name]
+    if cfg_name == "c2dim0":                     # fibre i of the [4096, 65536] matrix = column i
+        rows, cols = cfg["shape"]
+        x = np.ascontiguousarray(synth.host_generate("c2").reshape(rows, cols).T)
+        return x.reshape(-1), None, rows
+    x = synth.host_generate(cfg_name)
+    if cfg["kind"] == "csr":
+        return x, synth.gen.csr_offsets(cfg).astype(np.uint64), None
+    return x, None, cfg["seg_len"]
+
+
 def oracle_rate(cfg_name: str, target_s: float = 1.5, max_n: int = 1 << 28):
     import numpy as np
     """Time the oracle (as it stands) on a bounded prefix of the workload on all host cores:
@@ -188,8 +209,26 @@ def oracle_rate(cfg_name: str, target_s: float = 1.5, max_n: int = 1 << 28):
     import oracle
     import synth
     cores = oracle.host_threads()
+    if cfg_name in SEG_CFGS:
+        # the workload's own computation: every segment (fibre) summed and rounded on its own
+        # (oracle.sum_segments), the whole input (input preparation untimed)
+        x, off, L = oracle_segments_input(cfg_name)
+        oracle.sum_segments(x[:L or 64], seg_len=L or 64, nthreads=cores)
+        passes, t0 = 0, time.perf_counter()
+        while True:
+            ref = oracle.sum_segments(x, off, seg_len=L, nthreads=cores)
+            passes += 1
+            dt = time.perf_counter() - t0
+            if dt >= target_s:
+                break
+        m = x.size
+        del x
+        return m * passes / dt, cores, m, passes, dt, cfg_name, ref
     gen_name = "c2" if cfg_name in ("c1",) else cfg_name
     m = min(max_n, synth.CONFIGS[gen_name]["n"])
+    if synth.CONFIGS[gen_name]["kind"] == "cancel":
+        # c3's device input is permuted: only the whole input has the same exact sum on the host
+        m = synth.CONFIGS[gen_name]["n"]
     fmt = synth.CONFIGS[gen_name].get("fmt")
     if fmt is None:
         x = synth.host_generate(gen_name, 0, m)
@@ -234,6 +273,8 @@ def run_reference(args, rank: int, world: int):
     import synth
     wl = workload(args.config, world)
     cores = oracle.host_threads()
+    if args.config in SEG_CFGS:
+        return run_reference_segments(args, wl, cores)
     rate, _, _, _, _, gen_name, _ = oracle_rate(args.config, target_s=0.5, max_n=1 << 24)
     budget = 90.0
     m = int(max(1 << 14, min(1 << 26, rate * budget / max(1, args.steps + args.warmup))))
@@ -261,6 +302,44 @@ def run_reference(args, rank: int, world: int):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": {"workload": wl["desc"], "sample_n": m},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_segments(args, wl, cores):
+    """--impl reference for a segmented workload: each step sums and rounds a bounded prefix of
+    whole segments with the oracle (oracle.sum_segments)."""
+    import numpy as np
+
+    import oracle
+    x, off, L = oracle_segments_input(args.config)
+    nseg_all = (off.size - 1) if off is not None else x.size // L
+    budget_elems = int(max(1 << 16, min(x.size, 1.2e9 * 90 / max(1, args.steps + args.warmup))))
+    if off is not None:
+        k = int(np.searchsorted(off, budget_elems, side="right")) - 1
+        k = max(1, min(nseg_all, k))
+        xs, offs, m = x[: int(off[k])], off[: k + 1], int(off[k])
+    else:
+        k = max(1, min(nseg_all, budget_elems // L))
+        xs, offs, m = x[: k * L], None, k * L
+    for _ in range(args.warmup):
+        oracle.sum_segments(xs, offs, seg_len=L, nthreads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sum_segments(xs, offs, seg_len=L, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = m * args.steps / tot
+    metric, unit = metric_unit(args.config)
+    sample = f"{args.config}: the first {k} segments ({m} elements) per step, each summed and rounded, {cpu_model()}"
+    line = {
+        "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": wl["desc"], "sample_n": m, "sample_segments": k},
         "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -333,7 +412,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     synth.build()
     wl = workload(args.config, world)
     cfg = wl["cfg"]
-    if world > 1 and (cfg["kind"] in ("bits", "csr") or args.config in ("c2dim0", "c5s16")):
+    if world > 1 and (cfg["kind"] in ("bits", "csr") or args.config in ("c2dim0", "c5s16", "c2cs", "c3cs")):
         raise SystemExit(f"--config {args.config} is a one-GPU measurement workload")
     seg = args.config in ("c5", "c5csr", "c5s16", "c2dim0")      # many results per step
     csr = None
@@ -348,8 +427,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     elif args.config == "c4":
         start, stop = dist.shard_range(cfg["n"], rank, world)   # strong scaling: contiguous shards
         x = synth.device_generate("c4", start, stop - start, device=dev)
-    elif args.config == "c3":
-        x = synth.device_generate("c3", device=dev)
+    elif args.config in ("c3", "c3cs"):
+        x = synth.device_generate(args.config, device=dev)
     else:
         x = synth.device_generate(args.config, device=dev)   # same c-config per rank (weak scaling)
     n_local = x.numel()
@@ -380,14 +459,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     elif world > 1 and not seg:
         exchange = f"{args.dist_backend} all-gather of 384-B states + xsum_merge_round"
 
+    condsens = cfg.get("op") == "condsens"
+    if condsens:
+        cs_work = torch.empty(xsum.condsens_work_bytes(x.numel()), dtype=torch.uint8, device=dev)
+        cs_info = torch.empty(xsum.CONDSENS_INFO_BYTES, dtype=torch.uint8, device=dev)
+
     def step(i=0):
         out = res_rows[i]
-        if csr is not None:
-            xsum.sum_segments_csr(x, csr)
+        if condsens:
+            xsum.sum_condsens(x, 1, work=cs_work, res=out, info=cs_info)
+        elif csr is not None:
+            return xsum.sum_segments_csr(x, csr)[0]
         elif cfg.get("op") == "dim0":
-            xsum.exact_sum_dim(x.view(cfg["shape"]), 0)
+            return xsum.exact_sum_dim(x.view(cfg["shape"]), 0)
         elif seg:
-            xsum.sum_segments(x, cfg["seg_len"])
+            return xsum.sum_segments(x, cfg["seg_len"])[0]
         elif world == 1:
             acc.sum(x, out=out)                          # one fused launch
         elif pe is not None:
@@ -497,7 +583,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                            "computes the measured efficiency from its own per-N runs"}
     peak, peak_src = measured_peak_hbm()
     esz = x.element_size()                                   # algorithmic bytes per summand
-    achieved = esz * n_local / (kern_ms / 1e3) / 1e9
+    cs_line = None
+    passes = 1
+    if condsens:
+        # every iteration that ran reads the input once (K12 passes over the doubles; the exact pass)
+        inf = xsum.CondSensInfo.from_bytes(cs_info.cpu().numpy().tobytes())
+        passes = inf.iterations
+        cs_line = {"r": inf.r, "iterations": inf.iterations, "exact": inf.exact, "e_cut": inf.e_cut,
+                   "root_entries": len(inf.root), "rule": inf.rule}
+    achieved = esz * n_local * passes / (kern_ms / 1e3) / 1e9
     # context for the roofline: a pure streaming read of the same input in the same run (the
     # best read-only probe configuration of profiles/r01_microbench.txt: 296 blocks x 512 threads,
     # 8 x 16-B loads in flight per thread), untimed by the step
@@ -548,14 +642,30 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             result["sig53_exp2"] = [r_gpu.sig53, r_gpu.exp2]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, m, passes, dt, gen_name, (r_cpu, limbs_cpu) = oracle_rate(args.config)
+        import oracle                      # the cpu_baseline leg (test infrastructure)
+        rate, cores, m, passes, dt, gen_name, ref = oracle_rate(args.config)
+        what = "every segment of" if seg else "elements [0, %d) of" % m
         cpu = {"value": rate, "unit": unit, "cores": cores, "kind": "oracle",
-               "sample": f"{gen_name} elements [0, {m}) summed {passes}x by the oracle in {dt:.2f} s "
+               "sample": f"{what} {gen_name} ({m} elements) summed {passes}x by the oracle in {dt:.2f} s "
                          f"on {cores} host threads = {dt * cores:.1f} CPU-s ({cpu_model()})"}
-        st = oracle_single_thread(gen_name)
+        if seg:
+            # the oracle's per-segment roundings vs the GPU's outputs of the same step, all of them
+            gpu_vals = step().reshape(-1).cpu().numpy().view(np.uint64)
+            cpu["matches_gpu"] = bool(gpu_vals.size == ref[0].size and (gpu_vals == ref[0]).all())
+            cpu["compared"] = f"{gpu_vals.size} binary64 segment sums, bit for bit"
+            r_cpu = limbs_cpu = None
+        else:
+            r_cpu, limbs_cpu = ref
+        st = oracle_single_thread("c2" if args.config == "c2dim0" else gen_name)
         if st is not None:
             cpu["single_thread"] = st
-        if result is not None and gen_name == args.config:
+        if result is not None and condsens:
+            # a faithful rounding, not a unique one: the timed result must be
+            # one of the two binary64 neighbours of the oracle's exact sum
+            cpu["faithful_gpu"] = faithful(r_gpu.value, oracle.limbs_to_int(limbs_cpu))
+            if cs_line is not None and cs_line["exact"]:
+                cpu["matches_gpu"] = bool(r_cpu.bits == r_gpu.bits)
+        elif result is not None and gen_name == args.config:
             if m == n_local:
                 # the sample is the whole workload: the oracle's exact sum vs the timed GPU result
                 cpu["matches_gpu"] = bool(r_cpu.bits == r_gpu.bits and r_cpu.flags == r_gpu.flags and
@@ -589,8 +699,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
                                     "c2bf16": "k_accumulate_h16", "c5": "k_segments_half",
                                     "c5csr": "k_segments", "c5s16": "k_segments_lanes",
-                                    "c2dim0": "k_sum_strided"}.get(args.config, "k_accumulate"),
-                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local,
+                                    "c2dim0": "k_sum_strided", "c2cs": "xsum_sum_condsens step (all passes)",
+                                    "c3cs": "xsum_sum_condsens step (all passes)"}.get(args.config, "k_accumulate"),
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local * passes,
                          "peak_source": peak_src, "read_probe_gbs": probe_gbs,
                          "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None,
                          "sustained_frac": sustained["frac"] if sustained else None},
@@ -603,9 +714,28 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         }
         if scaling is not None:
             line["multi_gpu"] = scaling
+        if cs_line is not None:
+            line["condsens"] = cs_line
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def faithful(y: float, A: int) -> bool:
+    """y is RD or RU of the exact sum A * 2^-1074."""
+    import math
+    from fractions import Fraction
+    if math.isinf(y) or math.isnan(y):
+        return False
+    S = Fraction(A, 1 << 1074)
+    fy = Fraction(y)
+    if fy == S:
+        return True
+    if fy < S:
+        nxt = math.nextafter(y, math.inf)
+        return math.isinf(nxt) or Fraction(nxt) > S
+    prv = math.nextafter(y, -math.inf)
+    return math.isinf(prv) or Fraction(prv) < S
 
 
 def oracle_single_thread(gen_name: str, m: int = 1 << 24):
@@ -615,10 +745,10 @@ def oracle_single_thread(gen_name: str, m: int = 1 << 24):
     import oracle
     import synth
     cfg = synth.CONFIGS[gen_name]
-    if cfg.get("fmt") is not None or cfg["kind"] == "csr":
+    if cfg.get("fmt") is not None:
         return None
     m = min(m, cfg["n"])
-    x = synth.host_generate(gen_name, 0, m) if cfg["kind"] != "cancel" else synth.host_generate(gen_name, 0, m)
+    x = synth.host_generate(gen_name, 0, m)
     oracle.exact_sum(x[:4096], nthreads=1)
     t0 = time.perf_counter()
     oracle.exact_sum(x, nthreads=1)

@@ -9,6 +9,10 @@ Two independent implementations of one definition (§2
 fixed-point view: the exact sum is an integer multiple of 2^-1074):
   * O1  ``xsum_oracle.c``  big-integer limbs, threaded, any n   (this module)
   * O2  ``oracle.pytwin``  Python ints / fractions, small n     (pins O1)
+and, for the condition-number-sensitive algorithm of PAPER.md:851-965 (r-truncated sparse
+superaccumulators, r <- r^2, stopping conditions; a faithful, not a unique, result):
+  * O3  ``oracle.condsens`` Python ints / fractions, step by step in the paper's order,
+        pinned by tests/test_condsens_pins.py
 Rounding: round-to-nearest ties-to-even of the exact sum (PAPER.md:172-179
 faithful; §5 PAPER.md:1066-1069 "correctly rounded").
 
@@ -77,6 +81,8 @@ def _L():
         lib.oracle_round.restype = None
         lib.oracle_limbs_add.argtypes = [p, p]
         lib.oracle_limbs_add.restype = None
+        lib.oracle_sum_segments.argtypes = [p, i32, p, u64, p, p, p, p, i32]
+        lib.oracle_sum_segments.restype = None
         _lib = lib
     return _lib
 
@@ -170,3 +176,34 @@ def limbs_to_int(limbs: np.ndarray) -> int:
 def int_to_limbs(v: int) -> np.ndarray:
     v &= (1 << (64 * NLIMB)) - 1
     return np.array([(v >> (64 * L)) & 0xFFFFFFFFFFFFFFFF for L in range(NLIMB)], dtype=np.uint64)
+
+
+_FMT = {None: 0, "f64": 0, "f32": 1, "f16": 2, "bf16": 3}
+
+
+def sum_segments(x, offsets=None, seg_len: int | None = None, fmt: str | None = None, canon: bool = False,
+                 nthreads: int | None = None):
+    """Per-segment exact sums, each rounded like exact_sum (segment s = x[offsets[s]:offsets[s+1]], or
+    equal segments of seg_len): returns (binary64 bits uint64[nseg], binary32 bits uint32[nseg],
+    flags uint32[nseg], canonical images uint64[nseg, 34] or None). float32 arrays are binary32;
+    uint16 bit patterns need fmt "f16" / "bf16"."""
+    x = np.ascontiguousarray(x)
+    if fmt is None and x.dtype == np.float32:
+        fmt = "f32"
+    if fmt is None and x.dtype == np.float16:
+        fmt, x = "f16", x.view(np.uint16)
+    if offsets is None:
+        if not seg_len or x.size % seg_len:
+            raise ValueError("x.size must be a multiple of seg_len")
+        offsets = np.arange(0, x.size + 1, seg_len, dtype=np.uint64)
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    nseg = off.size - 1
+    b64 = np.zeros(nseg, dtype=np.uint64)
+    b32 = np.zeros(nseg, dtype=np.uint32)
+    fl = np.zeros(nseg, dtype=np.uint32)
+    cn = np.zeros((nseg, NLIMB), dtype=np.uint64) if canon else None
+    if nseg:
+        _L().oracle_sum_segments(x.ctypes.data if x.size else None, _FMT[fmt], off.ctypes.data, nseg,
+                                 b64.ctypes.data, b32.ctypes.data, fl.ctypes.data,
+                                 cn.ctypes.data if cn is not None else None, nthreads or host_threads())
+    return b64, b32, fl, cn

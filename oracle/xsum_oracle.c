@@ -353,3 +353,59 @@ void oracle_round(const uint64_t *A, uint32_t flags_in, uint64_t count, oracle_r
     r->direction = direction;
     r->flags = flags;
 }
+
+/* Segmented sums (the per-segment definition of BASELINE config 5 and SURVEY.md §8(f) f1): segment
+ * s is x[off[s] .. off[s+1]) of format fmt (0 binary64, 1 binary32, 2 binary16, 3 bfloat16); each
+ * segment is summed exactly on its own (oracle_accumulate*) and rounded by oracle_round. Outputs
+ * per segment: bits64[s] (binary64 bits), bits32[s] (binary32 bits), flags[s], and, if canon is not
+ * NULL, the 34-limb image at canon[34 s]. Segments are spread over nthreads threads (segment s on
+ * thread s mod nthreads); nothing is shared between segments. */
+typedef struct {
+    const void *x;
+    int fmt;
+    const uint64_t *off;
+    uint64_t nseg;
+    int t, nt;
+    uint64_t *bits64;
+    uint32_t *bits32, *flags;
+    uint64_t *canon;
+} segs_t;
+
+static void *segs_run(void *arg) {
+    segs_t *a = (segs_t *)arg;
+    size_t esz = a->fmt == FMT_F64 ? 8 : (a->fmt == FMT_F32 ? 4 : 2);
+    for (uint64_t s = (uint64_t)a->t; s < a->nseg; s += (uint64_t)a->nt) {
+        part_t p;
+        memset(&p, 0, sizeof p);
+        p.x = (const char *)a->x + a->off[s] * esz;
+        p.n = a->off[s + 1] - a->off[s];
+        p.fmt = a->fmt;
+        part_run(&p);
+        uint64_t A[NLIMB];
+        memset(A, 0, sizeof A);
+        oracle_limbs_add(A, p.P);
+        oracle_limbs_sub(A, p.N);
+        oracle_result r;
+        oracle_round(A, p.flags, p.n, &r);
+        memcpy(&a->bits64[s], &r.value, 8);
+        a->bits32[s] = r.value_f32;
+        a->flags[s] = r.flags;
+        if (a->canon) memcpy(a->canon + s * NLIMB, A, sizeof A);
+    }
+    return NULL;
+}
+
+void oracle_sum_segments(const void *x, int fmt, const uint64_t *off, uint64_t nseg, uint64_t *bits64,
+                         uint32_t *bits32, uint32_t *flags, uint64_t *canon, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if ((uint64_t)nthreads > nseg) nthreads = nseg ? (int)nseg : 1;
+    segs_t *args = (segs_t *)calloc((size_t)nthreads, sizeof(segs_t));
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int t = 0; t < nthreads; ++t) {
+        segs_t a = {x, fmt, off, nseg, t, nthreads, bits64, bits32, flags, canon};
+        args[t] = a;
+        pthread_create(&th[t], NULL, segs_run, &args[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(args); free(th);
+}

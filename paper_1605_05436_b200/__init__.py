@@ -498,18 +498,29 @@ class CondSensInfo:
                             root={int(v & 63): int(v >> 6) for v in rec})
 
 
-def sum_condsens(x, rule: int = 1, canon: bool = False, work=None):
+def condsens_work_bytes(n: int) -> int:
+    return int(lib().xsum_condsens_work_bytes(n))
+
+
+def sum_condsens(x, rule: int = 1, canon: bool = False, work=None, res=None, info=None):
     """Condition-number-sensitive sum of a float64 CUDA tensor (xsum_sum_condsens):
     the r = 2, 4, 16 truncated iterations with a stopping condition (rule 1 or 2), then the exact
     pass if needed. Returns device tensors (result record, info record, canonical image of the
-    truncated root or None); no host synchronization."""
+    truncated root or None); no host synchronization. `work` (uint8, >= condsens_work_bytes(n),
+    256-B aligned), `res` and `info` may be passed in to reuse buffers."""
     torch = _torch()
     x = _as_f64_cuda(x)
-    nb = int(lib().xsum_condsens_work_bytes(x.numel()))
+    nb = condsens_work_bytes(x.numel())
     if work is None or work.numel() < nb:
         work = torch.empty(nb, dtype=torch.uint8, device=x.device)
-    res = torch.empty(RESULT_BYTES, dtype=torch.uint8, device=x.device)
-    info = torch.empty(CONDSENS_INFO_BYTES, dtype=torch.uint8, device=x.device)
+    if res is None:
+        res = torch.empty(RESULT_BYTES, dtype=torch.uint8, device=x.device)
+    if info is None:
+        info = torch.empty(CONDSENS_INFO_BYTES, dtype=torch.uint8, device=x.device)
+    for t, nbytes in ((res, RESULT_BYTES), (info, CONDSENS_INFO_BYTES)):
+        if not (t.is_cuda and t.dtype == torch.uint8 and t.numel() == nbytes and t.is_contiguous()
+                and t.data_ptr() % 8 == 0 and t.device == x.device):
+            raise TypeError("res / info must be 8-B aligned uint8 CUDA tensors of their record size")
     cn = torch.empty(CANON_LIMBS, dtype=torch.int64, device=x.device) if canon else None
     xp = x if x.numel() else torch.zeros(1, dtype=torch.float64, device=x.device)
     with torch.cuda.device(x.device):

@@ -154,7 +154,8 @@ __device__ __forceinline__ void ssa_merge(SSA<RC>& a, const SSA<RC>& b, int& cut
     }
     // keep the RC most significant non-zero entries
     int cnt = 0;
-    if constexpr (RC <= 4) {
+    static_assert(RC <= 4, "r = 16 uses the warp-dense kernel");
+    {
         ssa_clear(a);
 #pragma unroll
         for (int t = 0; t < 2 * U; ++t) {
@@ -167,22 +168,18 @@ __device__ __forceinline__ void ssa_merge(SSA<RC>& a, const SSA<RC>& b, int& cut
             }
             cnt += nz;
         }
-    } else {
-        int ok[RC];
-        int64_t ov[RC];
-#pragma unroll
-        for (int q = 0; q < RC; ++q) { ok[q] = -1; ov[q] = 0; }
-#pragma unroll
-        for (int t = 0; t < 2 * U; ++t) {
-            if (ck[t] >= 0) {
-                if (cnt < RC) { ok[cnt] = ck[t]; ov[cnt] = cv[t]; }
-                ++cnt;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < RC; ++q) { a.k[q] = ok[q]; a.v[q] = ov[q]; }
     }
     if (cnt > RC) cut = max(cut, a.k[RC - 1]);
+}
+
+// Code size: the first version inlined a merge at every node of a static recursion over the 2^G
+// leaves (~64 KB of SASS per kernel; ncu: no_instruction stalls 3.4 per issue, the L1.5 I-cache is
+// 32 KB). The binary counter below has G merge sites in its loop body; an out-of-line merge
+// measured no faster (r = 2: 5.73 vs 5.54 ms, r = 4: 13.9 vs 14.0 ms for 2^28 leaves;
+// profiles/r02_condsens.txt).
+template <int RC>
+__device__ __forceinline__ void merge_into(SSA<RC>& a, const SSA<RC>& b, int& cut) {
+    ssa_merge(a, b, cut);
 }
 
 // records: (digit << 6) | index, 0 = unused slot (the sparse image record format, include/xsum.h)
@@ -209,51 +206,17 @@ __device__ __forceinline__ void ssa_shfl_down(SSA<RC>& o, const SSA<RC>& a, int 
     }
 }
 
-// The subtree of 2^L leaves starting at leaf p0 of this thread's 2^G: present iff its first leaf
-// exists; the right child is summed in only if present (reading C2).
-template <int RC, int L, typename Leaf>
-struct Sub {
-    __device__ static __forceinline__ void run(SSA<RC>& a, const Leaf& lf, int p0, int nleft, int& cut,
-                                               uint32_t& flags) {
-        Sub<RC, L - 1, Leaf>::run(a, lf, p0, nleft, cut, flags);
-        if (p0 + (1 << (L - 1)) < nleft) {
-            SSA<RC> b;
-            Sub<RC, L - 1, Leaf>::run(b, lf, p0 + (1 << (L - 1)), nleft, cut, flags);
-            ssa_merge(a, b, cut);
-        }
-    }
-};
-template <int RC, typename Leaf>
-struct Sub<RC, 0, Leaf> {
-    __device__ static __forceinline__ void run(SSA<RC>& a, const Leaf& lf, int p0, int nleft, int& cut,
-                                               uint32_t& flags) {
-        (void)nleft; (void)cut;
-        lf.get(a, p0, flags);
-    }
-};
-
-// leaves of pass 1: doubles held in registers
-template <int RC, int NL>
-struct DoubleLeaves {
-    uint64_t b[NL];
-    __device__ __forceinline__ void get(SSA<RC>& a, int p, uint32_t& flags) const { ssa_leaf(a, b[p], flags); }
-};
-// leaves of later passes: the previous pass's block roots (records)
-template <int RC>
-struct RecLeaves {
-    const int64_t* rec;      // this thread's first leaf
-    __device__ __forceinline__ void get(SSA<RC>& a, int p, uint32_t& flags) const {
-        (void)flags;
-        ssa_load(a, rec + (size_t)p * RC);
-    }
-};
-
 template <int RC> struct Shape;
 template <> struct Shape<2> { static constexpr int G = 4, T = 256, MINB = 2; };
 template <> struct Shape<4> { static constexpr int G = 3, T = 256, MINB = 1; };
-template <> struct Shape<16> { static constexpr int G = 1, T = 128, MINB = 1; };
+// r = 16: a sorted 16-entry list per thread does not fit in registers (spills, ~0.9 us per
+// node); that iteration keeps the superaccumulator dense across a warp instead (k_cs_tree_w16)
+constexpr int W16_WARPS = 8, W16_LOG = 10;      // 2^10 consecutive leaves per warp chunk
 template <int RC>
-constexpr int chunk_log2() { return Shape<RC>::G + (Shape<RC>::T == 256 ? 8 : 7); }
+constexpr int chunk_log2() {
+    if constexpr (RC == 16) return W16_LOG;
+    else return Shape<RC>::G + (Shape<RC>::T == 256 ? 8 : 7);
+}
 
 // One pass: chunk c (2^B consecutive leaves, B = G + log2 T) -> its subtree root, recs_out[c].
 template <int RC, bool DOUBLES>
@@ -270,37 +233,55 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
     for (uint64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const uint64_t first = (chunk << B) + ((uint64_t)tid << G);
         const int nleft = first < nleaf ? (int)min((uint64_t)NL, nleaf - first) : 0;
+        // this thread's 2^G leaves: the complete subtree by a binary counter (reading C2): after
+        // leaf p, the subtrees of sizes 2^L that end at p are summed with their left siblings
+        // (stack[L]) while bit L of p is set; a partial last group folds the pending stack
+        // entries from the smallest subtree up (a missing right child passes its left child up)
         SSA<RC> a;
         ssa_clear(a);
         if (nleft > 0) {
-            if constexpr (DOUBLES) {
-                DoubleLeaves<RC, NL> lf;
-                const uint64_t* x = static_cast<const uint64_t*>(src) + first;
-                if (nleft == NL && ((uintptr_t)x & 15) == 0) {
+            SSA<RC> stack[G];
+#pragma unroll 1
+            for (int p = 0; p < nleft; ++p) {
+                SSA<RC> cur;
+                if constexpr (DOUBLES)
+                    ssa_leaf(cur, static_cast<const uint64_t*>(src)[first + p], flags);
+                else
+                    ssa_load(cur, static_cast<const int64_t*>(src) + (first + p) * RC);
+                bool carry = true;
 #pragma unroll
-                    for (int q = 0; q < NL / 2; ++q) {
-                        const uint4 v = *reinterpret_cast<const uint4*>(x + 2 * q);
-                        lf.b[2 * q] = ((uint64_t)v.y << 32) | v.x;
-                        lf.b[2 * q + 1] = ((uint64_t)v.w << 32) | v.z;
+                for (int L = 0; L < G; ++L) {
+                    if (carry) {
+                        if ((p >> L) & 1) {
+                            merge_into(cur, stack[L], cut);
+                        } else {
+                            stack[L] = cur;
+                            carry = false;
+                        }
                     }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < NL; ++q) lf.b[q] = q < nleft ? x[q] : 0;
                 }
-                Sub<RC, G, DoubleLeaves<RC, NL>>::run(a, lf, 0, nleft, cut, flags);
-            } else {
-                RecLeaves<RC> lf{static_cast<const int64_t*>(src) + first * RC};
-                Sub<RC, G, RecLeaves<RC>>::run(a, lf, 0, nleft, cut, flags);
+                if (carry) a = cur;                 // p = 2^G - 1: the whole group
+            }
+            if (nleft < NL) {
+                bool have = false;
+#pragma unroll
+                for (int L = 0; L < G; ++L) {
+                    if ((nleft >> L) & 1) {
+                        if (have) merge_into(a, stack[L], cut);
+                        else a = stack[L];
+                        have = true;
+                    }
+                }
             }
         }
         bool pres = nleft > 0;
         // warp levels G .. G+4 (lane pairs by shuffles)
-#pragma unroll
+#pragma unroll 1
         for (int d = 1; d < 32; d <<= 1) {
             SSA<RC> b;
             ssa_shfl_down(b, a, d);
             const bool bpres = __shfl_down_sync(FULL, pres, d);
-            if ((lane & (2 * d - 1)) == 0 && bpres) ssa_merge(a, b, cut);
+            if ((lane & (2 * d - 1)) == 0 && bpres) merge_into(a, b, cut);
         }
         if (lane == 0) {
             ssa_store(a, wroot[warp]);
@@ -316,12 +297,12 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
                 ssa_load(w, wroot[lane]);
                 wp = wpres[lane];
             }
-#pragma unroll
+#pragma unroll 1
             for (int d = 1; d < WARPS; d <<= 1) {
                 SSA<RC> b;
                 ssa_shfl_down(b, w, d);
                 const bool bpres = __shfl_down_sync(FULL, wp, d);
-                if ((lane & (2 * d - 1)) == 0 && bpres) ssa_merge(w, b, cut);
+                if ((lane & (2 * d - 1)) == 0 && bpres) merge_into(w, b, cut);
             }
             if (lane == 0) ssa_store(w, recs_out + chunk * RC);
         }
@@ -330,6 +311,151 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
     // this iteration's E_cut and the special-value flags
 #pragma unroll
     for (int d = 16; d; d >>= 1) cut = max(cut, __shfl_xor_sync(FULL, cut, d));
+    const uint32_t f = __reduce_or_sync(FULL, flags);
+    if (lane == 0) {
+        if (cut >= 0) atomicMax(&ctl->e_cut, cut);
+        if (f) atomicOr(&ctl->flags, f);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// r = 16: the same tree with the superaccumulator dense across a warp - lane l holds digits l and
+// l + 32, as in the exact path (a0, a1). The r-truncated Lemma-1 sum is lemma1_add (PAPER.md:
+// 578-628; identical to the sparse sum: an absent index is a zero digit, which only a carry
+// makes non-zero) followed by keeping the 16 most significant non-zero digits (two ballots). Each
+// warp walks its chunk of 2^W16_LOG leaves in order with a binary counter whose pending subtree
+// roots live in shared memory; one node costs ~30 warp instructions instead of a 16-entry sorted
+// merge per thread.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void trunc_dense(int64_t& a0, int64_t& a1, int r, int& cut, int lane) {
+    const uint32_t lo = __ballot_sync(FULL, a0 != 0);
+    const uint32_t hi = __ballot_sync(FULL, a1 != 0);
+    const uint64_t m = ((uint64_t)hi << 32) | lo;
+    if (__popcll(m) > r) {                               // warp-uniform
+        uint64_t mm = m;
+        for (int q = 1; q < r; ++q) mm &= ~(1ull << (63 - __clzll(mm)));   // drop the top r-1
+        const int j = 63 - __clzll(mm);                  // the r-th most significant non-zero digit
+        if (lane < j) a0 = 0;
+        if (lane + 32 < j) a1 = 0;
+        cut = max(cut, j);
+    }
+}
+
+// dense digits of one leaf x (bit pattern b, the same value in every lane)
+__device__ __forceinline__ void dense_leaf(uint64_t b, int64_t& a0, int64_t& a1, uint32_t& flags, int lane) {
+    a0 = a1 = 0;
+    const uint32_t e = (uint32_t)(b >> 52) & 0x7FF;
+    const uint64_t m = b & MASK;
+    if (e == 0x7FF) {
+        flags |= m ? XSUM_F_NAN : ((b >> 63) ? XSUM_F_NINF : XSUM_F_PINF);
+        return;
+    }
+    const uint64_t M = m | ((uint64_t)(e != 0) << 52);
+    const uint32_t k = (e ? e : 1) - 1;
+    const int i = (int)(k / 52), o = (int)(k % 52);
+    const uint64_t lo = (M << o) & MASK;
+    const uint64_t hi = o ? (M >> (52 - o)) : (M >> 52);
+    const bool neg = b >> 63;
+    const int64_t slo = neg ? -(int64_t)lo : (int64_t)lo, shi = neg ? -(int64_t)hi : (int64_t)hi;
+    a0 = lane == i ? slo : (lane == i + 1 ? shi : 0);
+    a1 = lane + 32 == i ? slo : (lane + 32 == i + 1 ? shi : 0);
+}
+
+// a 16-record leaf (a previous pass's chunk root) to dense digits
+__device__ __forceinline__ void dense_from_records(const int64_t* rec, int64_t& a0, int64_t& a1, int lane) {
+    const int64_t mine = lane < 16 ? rec[lane] : 0;
+    a0 = a1 = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int64_t r = __shfl_sync(FULL, mine, q);
+        const int k = r ? (int)(r & 63) : -1;
+        if (k == lane) a0 = r >> 6;
+        if (k == lane + 32) a1 = r >> 6;
+    }
+}
+
+// dense digits (at most 16 non-zero) to 16 records in descending index order, zero padded
+__device__ __forceinline__ void dense_to_records(int64_t a0, int64_t a1, int64_t* rec, int lane) {
+    const uint32_t lo = __ballot_sync(FULL, a0 != 0);
+    const uint32_t hi = __ballot_sync(FULL, a1 != 0);
+    const uint64_t m = ((uint64_t)hi << 32) | lo;
+    const int nnz = __popcll(m);
+    if (a0 != 0) {
+        const int rank = __popcll(m >> (lane + 1));
+        if (rank < 16) rec[rank] = (int64_t)(((uint64_t)a0 << 6) | (uint64_t)lane);
+    }
+    if (a1 != 0) {
+        const int pos = lane + 32;
+        const int rank = __popcll(m >> (pos + 1));
+        if (rank < 16) rec[rank] = (int64_t)(((uint64_t)a1 << 6) | (uint64_t)pos);
+    }
+    if (lane >= nnz && lane < 16) rec[lane] = 0;
+}
+
+template <bool DOUBLES>
+__global__ void __launch_bounds__(W16_WARPS * 32)
+k_cs_tree_w16(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ recs_out, uint64_t nchunks,
+              Ctl* ctl) {
+    constexpr int R16 = 16, NLW = 1 << W16_LOG;
+    __shared__ int64_t stk[W16_WARPS][W16_LOG][64];      // pending subtree roots (dense digits)
+    if (*(volatile uint32_t*)&ctl->done) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* const st = &stk[warp][0][0];
+    int cut = -1;
+    uint32_t flags = 0;
+    const uint64_t nw = (uint64_t)gridDim.x * W16_WARPS;
+    for (uint64_t chunk = (uint64_t)blockIdx.x * W16_WARPS + warp; chunk < nchunks; chunk += nw) {
+        const uint64_t first = chunk << W16_LOG;
+        const int nleft = (int)min((uint64_t)NLW, nleaf - first);
+        int64_t a0 = 0, a1 = 0;                          // the chunk root
+        for (int base = 0; base < nleft; base += 32) {
+            uint64_t xb = 0;
+            if constexpr (DOUBLES) {
+                if (base + lane < nleft) xb = static_cast<const uint64_t*>(src)[first + base + lane];
+            }
+            const int cnt = min(32, nleft - base);
+            for (int j = 0; j < cnt; ++j) {
+                const int p = base + j;
+                int64_t c0, c1;
+                if constexpr (DOUBLES)
+                    dense_leaf(__shfl_sync(FULL, xb, j), c0, c1, flags, lane);
+                else
+                    dense_from_records(static_cast<const int64_t*>(src) + (first + p) * R16, c0, c1, lane);
+                // binary counter (reading C2): sum with the left siblings while bit L of p is set
+                int L = 0;
+                while (L < W16_LOG && ((p >> L) & 1)) {
+                    lemma1_add(c0, c1, st[L * 64 + lane], st[L * 64 + 32 + lane], lane);
+                    trunc_dense(c0, c1, R16, cut, lane);
+                    ++L;
+                }
+                if (L < W16_LOG) {
+                    st[L * 64 + lane] = c0;
+                    st[L * 64 + 32 + lane] = c1;
+                } else {
+                    a0 = c0;
+                    a1 = c1;
+                }
+            }
+        }
+        if (nleft < NLW) {                                // fold the pending roots, smallest first
+            bool have = false;
+            for (int L = 0; L < W16_LOG; ++L) {
+                if ((nleft >> L) & 1) {
+                    const int64_t s0 = st[L * 64 + lane], s1 = st[L * 64 + 32 + lane];
+                    if (have) {
+                        lemma1_add(a0, a1, s0, s1, lane);
+                        trunc_dense(a0, a1, R16, cut, lane);
+                    } else {
+                        a0 = s0;
+                        a1 = s1;
+                    }
+                    have = true;
+                }
+            }
+        }
+        dense_to_records(a0, a1, recs_out + chunk * R16, lane);
+        __syncwarp();
+    }
     const uint32_t f = __reduce_or_sync(FULL, flags);
     if (lane == 0) {
         if (cut >= 0) atomicMax(&ctl->e_cut, cut);
@@ -459,7 +585,6 @@ cudaError_t iteration(const double* x, uint64_t n, int iter, int rule, uint8_t* 
     Ctl* ctl = reinterpret_cast<Ctl*>(work);
     int64_t* bufA = reinterpret_cast<int64_t*>(work + RECS_OFF);
     int64_t* bufB = reinterpret_cast<int64_t*>(work + RECS_OFF + first_bytes);
-    constexpr int T = Shape<RC>::T;
     const unsigned max_grid = (unsigned)num_sms * 8u;
     uint64_t m = n;
     const void* src = x;
@@ -467,11 +592,21 @@ cudaError_t iteration(const double* x, uint64_t n, int iter, int rule, uint8_t* 
     int64_t* out = bufA;
     while (true) {
         const uint64_t chunks = pass_count<RC>(m);
-        const unsigned grid = (unsigned)(chunks < max_grid ? chunks : max_grid);
-        if (doubles)
-            k_cs_tree<RC, true><<<grid, T, 0, s>>>(src, m, out, chunks, ctl);
-        else
-            k_cs_tree<RC, false><<<grid, T, 0, s>>>(src, m, out, chunks, ctl);
+        if constexpr (RC == 16) {
+            const uint64_t blocks = (chunks + W16_WARPS - 1) / W16_WARPS;
+            const unsigned grid = (unsigned)(blocks < max_grid ? blocks : max_grid);
+            if (doubles)
+                k_cs_tree_w16<true><<<grid, W16_WARPS * 32, 0, s>>>(src, m, out, chunks, ctl);
+            else
+                k_cs_tree_w16<false><<<grid, W16_WARPS * 32, 0, s>>>(src, m, out, chunks, ctl);
+        } else {
+            constexpr int T = Shape<RC>::T;
+            const unsigned grid = (unsigned)(chunks < max_grid ? chunks : max_grid);
+            if (doubles)
+                k_cs_tree<RC, true><<<grid, T, 0, s>>>(src, m, out, chunks, ctl);
+            else
+                k_cs_tree<RC, false><<<grid, T, 0, s>>>(src, m, out, chunks, ctl);
+        }
         note_launch();
         if (cudaError_t e = cudaGetLastError()) return e;
         if (chunks == 1) break;

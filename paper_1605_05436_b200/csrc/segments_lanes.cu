@@ -313,6 +313,116 @@ cudaError_t sum_segments_lanes_csr(const void* x, int dtype, uint64_t nseg, cons
     }
 }
 
+// K11 for binary64 rows that are 16-B aligned with an even length <= SEG_LANES_MAX (c5s16): the
+// next segment's first SLP elements are loaded before this segment is summed and rounded, so they
+// are in flight through its adds and epilogue (the per-segment epilogue otherwise leaves the load
+// pipe idle: ncu r01, 26% of stall samples on the first use of a load); NaN/Inf patterns are summed
+// unchecked like finite values and, if the lane saw one, cancelled by a rescan of its segment
+// (K2's scheme; <= 2 x 256 adds stay far inside the int64 headroom, so no flush is needed).
+constexpr int SLP = 16;                     // elements prefetched per lane (8 x 16 B)
+#ifndef XS_SL_PF
+#define XS_SL_PF 1
+#endif
+__global__ void __launch_bounds__(SL_WARPS * 32, 1)
+k_segments_lanes64(const double* __restrict__ x, uint64_t nseg, uint64_t len, SegOut o, uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t groups = (nseg + 31) / 32;
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    const uint64_t gstride = (uint64_t)gridDim.x * SL_WARPS;
+    const int npf = (int)(len < (uint64_t)SLP ? len : (uint64_t)SLP) / 2;     // vectors prefetched
+    uint4 pf[SLP / 2];
+    auto prefetch = [&](uint64_t gg) {
+        const uint64_t s = gg * 32 + lane;
+        if (gg < groups && s < nseg) {
+            const uint4* pv = reinterpret_cast<const uint4*>(x + s * len);
+#pragma unroll
+            for (int u = 0; u < SLP / 2; ++u)
+                if (u < npf) pf[u] = ld_v4_ca(pv + u);
+        }
+    };
+    uint64_t g = (uint64_t)blockIdx.x * SL_WARPS + warp;
+    prefetch(g);
+    for (; g < groups; g += gstride) {
+        const uint64_t s = g * 32 + lane;
+        uint4 cur[SLP / 2];
+#pragma unroll
+        for (int u = 0; u < SLP / 2; ++u) cur[u] = pf[u];
+#if XS_SL_PF
+        prefetch(g + gstride);
+#endif
+        if (s >= nseg) continue;
+        int lo = D, hi = -1;                          // touched digit range of this segment
+        uint32_t nspec = 0, flags = 0;
+        auto addc = [&](uint32_t xl, uint32_t xh) {
+            const Chunks c = decompose(xl, xh, one, mone);
+            nspec = spec_fold(nspec, c);
+            column_add(col, c, one);
+            lo = min(lo, (int)c.i);
+            hi = max(hi, (int)c.i + 1);
+        };
+#if !XS_SL_PF
+        {
+            const uint4* pv0 = reinterpret_cast<const uint4*>(x + s * len);
+#pragma unroll
+            for (int u = 0; u < SLP / 2; ++u)
+                if (u < npf) cur[u] = ld_v4_ca(pv0 + u);
+        }
+#endif
+#pragma unroll
+        for (int u = 0; u < SLP / 2; ++u) {
+            if (u < npf) {
+                addc(cur[u].x, cur[u].y);
+                addc(cur[u].z, cur[u].w);
+            }
+        }
+        const uint4* pv = reinterpret_cast<const uint4*>(x + s * len);
+        uint64_t r = 2 * (uint64_t)npf;
+        for (; r + 8 <= len; r += 8) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = ld_v4_ca(pv + r / 2 + u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                addc(v[u].x, v[u].y);
+                addc(v[u].z, v[u].w);
+            }
+        }
+        for (; r < len; r += 2) {
+            const uint4 v = ld_v4_ca(pv + r / 2);
+            addc(v.x, v.y);
+            addc(v.z, v.w);
+        }
+        if (spec_hit(nspec)) {                        // rare: cancel the NaN/Inf patterns (R10)
+            for (uint64_t q = 0; q < len; q += 2) {
+                const uint4 v = ld_v4_ca(pv + q / 2);
+                column_fix_special(col, v.x, v.y, flags, one);
+                column_fix_special(col, v.z, v.w, flags, one);
+            }
+        }
+        if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
+        if (hi < 0) lo = hi = 0;
+        lane_store_segment(col, flags, o, s, lo, hi);
+#pragma unroll 4
+        for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+    }
+}
+
+static cudaError_t launch_lanes64(const void* x, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
+                                  cudaStream_t s) {
+    static unsigned long long done = 0;
+    if (cudaError_t e = ensure_smem(k_segments_lanes64, SL_SMEM, done)) return e;
+    const uint64_t groups = (nseg + 31) / 32;
+    const uint64_t want = (groups + SL_WARPS - 1) / SL_WARPS;
+    const unsigned g = (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
+    k_segments_lanes64<<<g, SL_WARPS * 32, SL_SMEM, s>>>(static_cast<const double*>(x), nseg, len, o, 1u,
+                                                         0xFFFFFFFFu);
+    note_launch();
+    return cudaGetLastError();
+}
+
 template <int DT, bool VEC>
 static cudaError_t launch_lanes(const void* x, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
                                 cudaStream_t s) {
@@ -333,7 +443,8 @@ cudaError_t sum_segments_lanes(const void* x, int dtype, uint64_t nseg, uint64_t
     switch (dtype) {
         case XSUM_DT_F64:
             if (len % 2 == 0 && ((uintptr_t)x & 15) == 0)
-                return launch_lanes<XSUM_DT_F64, true>(x, nseg, len, o, num_sms, s);
+                return len <= SEG_LANES_MAX ? launch_lanes64(x, nseg, len, o, num_sms, s)
+                                            : launch_lanes<XSUM_DT_F64, true>(x, nseg, len, o, num_sms, s);
             return launch_lanes<XSUM_DT_F64, false>(x, nseg, len, o, num_sms, s);
         case XSUM_DT_F32: return launch_lanes<XSUM_DT_F32, false>(x, nseg, len, o, num_sms, s);
         case XSUM_DT_F16: return launch_lanes<XSUM_DT_F16, false>(x, nseg, len, o, num_sms, s);

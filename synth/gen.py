@@ -57,6 +57,11 @@ CONFIGS.update({
     # strided), and 2^24 segments of 16 doubles drawn like c5 with seed 10 (K11, one lane each)
     "c2dim0": dict(kind="uniform", n=1 << 28, seed=2, st=0, lo=-1000, hi=1000, op="dim0", shape=(4096, 65536)),
     "c5s16": dict(kind="segments", n=1 << 28, seed=10, st=0, lo=-200, hi=200, nseg=1 << 24, seg_len=16),
+    # f4 measurement workloads: the condition-number-sensitive sum (K12) over c2 (well conditioned)
+    # and c3 (ill conditioned, C(X) ~ 2^1413) - the same elements as those configs
+    "c2cs": dict(kind="uniform", n=1 << 28, seed=2, st=0, lo=-1000, hi=1000, op="condsens"),
+    "c3cs": dict(kind="cancel", n=(1 << 28) + (1 << 20), seed=3, npairs=1 << 27,
+                 pair_lo=0, pair_hi=600, ntiny=1 << 20, tiny_lo=-900, tiny_hi=-800, op="condsens"),
 })
 
 

@@ -504,3 +504,40 @@ def test_h16_all_binary16_finite_values_sum_to_zero():
     nor = sum(Fraction(sum(range(1024, 2048)) * 2 ** e, 1 << 25) for e in range(1, 31))
     _, lp = oracle.exact_sum(pos, fmt="f16")
     assert oracle.limbs_to_int(lp) == (sub + nor) * (1 << 1074)
+
+
+# ------------------------------------------------------------------------------------------
+# segmented sums (oracle.sum_segments: the per-segment definition of config 5 / f1)
+# ------------------------------------------------------------------------------------------
+def test_sum_segments_vs_o2_every_format():
+    """Each segment of oracle.sum_segments against the independent Python twin O2 (exact Python
+    ints, library rounding): ragged CSR bounds with empty segments, specials, every format."""
+    import synth
+    x64 = synth.gen.generate("c2", 5, 6000)
+    x64[17] = np.inf
+    x64[4000] = np.nan
+    lens = [0, 1, 2, 3, 0, 17, 100, 1000, 0, 2000, 2877]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    assert off[-1] == x64.size
+    b64, b32, fl, cn = oracle.sum_segments(x64, off, canon=True, nthreads=3)
+    for s in range(len(lens)):
+        seg = x64[int(off[s]):int(off[s + 1])]
+        A, f = pytwin.exact_int(seg)
+        v, _, f2 = pytwin.round_int(A, f)
+        assert int(b64[s]) == pytwin.bits_of(v) and int(fl[s]) & 0xFF & ~0xC0 == f2 & ~0xC0
+        assert [int(c) for c in cn[s]] == pytwin.limbs(A)
+        want32, _ = pytwin.round_int_f32(A, f)
+        assert int(b32[s]) == want32
+    # binary32 and 16-bit inputs, equal segments
+    bits32 = synth.gen.bits("c2f32", 3, 64 * 37)
+    b64, b32, fl, _ = oracle.sum_segments(bits32.view(np.float32), seg_len=37)
+    for s in range(64):
+        A, f = pytwin.exact_int_f32(bits32[s * 37:(s + 1) * 37])
+        assert int(b64[s]) == pytwin.bits_of(pytwin.round_int(A, f)[0])
+        assert int(b32[s]) == pytwin.round_int_f32(A, f)[0]
+    for fmt in ("f16", "bf16"):
+        bits16 = synth.gen.bits("c2" + fmt, 3, 50 * 41)
+        b64, b32, fl, _ = oracle.sum_segments(bits16, seg_len=41, fmt=fmt)
+        for s in range(50):
+            A, f = pytwin.exact_int_h16(bits16[s * 41:(s + 1) * 41], fmt)
+            assert int(b64[s]) == pytwin.bits_of(pytwin.round_int(A, f)[0]), (fmt, s)

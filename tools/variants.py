@@ -30,6 +30,7 @@ VARIANTS = {
     "seg_whole": ["-DXS_SEG_HALF=0"],
     "sh_q8u4": ["-DXS_SH_LPS=8", "-DXS_SH_U=4"],
     "sl_full": ["-DXS_SL_FULL"],
+    "sl_nopf": ["-DXS_SL_PF=0"],
     "str_nb3": ["-DXS_STR_NB=3"],
     "str_nb6": ["-DXS_STR_NB=6"],
     "str_u4nb8": ["-DXS_STR_UNR=4", "-DXS_STR_NB=8"],
@@ -97,11 +98,12 @@ if {cfg!r} == "c5csr":
             return xsum_res, None
     xsum_res = acc.sum(x)[0]
     acc = _C()
-if {cfg!r}.endswith("seg"):
+if {cfg!r}.endswith("seg") or {cfg!r} == "c5s16":
+    SEGL = 16 if {cfg!r} == "c5s16" else 4096
     class _S:
         def sum(self, x):
             global seg_v
-            seg_v, _, _ = xsum.sum_segments(x, 4096)
+            seg_v, _, _ = xsum.sum_segments(x, SEGL)
             return xsum_res, None
     xsum_res = acc.sum(x)[0]
     acc = _S()
@@ -114,7 +116,7 @@ torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
 import hashlib
-check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr")) or {cfg!r}.startswith("str") else hex(r.bits)
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16")) or {cfg!r}.startswith("str") else hex(r.bits)
 print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)

@@ -134,6 +134,54 @@ __device__ __forceinline__ LaneTop lane_canonical_top(int64_t* col, int first = 
     return t;
 }
 
+// A lane's RAW column digits [lo, hi] (|y| < 2^62, unregularized; digits outside are zero) to the
+// LaneTop of their sum A, zeroing them, in one carry chain instead of regularize +
+// lane_canonical_top (two read-write passes and scans; ncu r02: K11 issue-bound): t = y + c,
+// d = t mod R, c = floor(t / R) gives the two's complement digits d_j of A (c settles to 0 or -1,
+// the sign). For A >= 0 the magnitude digits are d_j; for A < 0 they are e_j = R-1-d_j above the
+// lowest non-zero digit lz, R-d_lz at lz and 0 below (|A| = ~A + 1). So the chain only records the
+// highest index with d != 0, the highest with d != R-1 and lz, and the window digits are read back.
+__device__ __forceinline__ LaneTop lane_top_chain(int64_t* col, int lo, int hi) {
+    int64_t c = 0;
+    int mpos = -1, mneg = -1, lz = -1;
+    int j = lo;
+    for (; j < D; ++j) {
+        int64_t y = 0;
+        if (j <= hi) y = col[j * 32];
+        else if (c == 0 || c == -1) break;             // the carry has settled: sign extension above
+        const int64_t t = y + c;
+        const uint64_t d = (uint64_t)t & MASK;
+        c = t >> W;
+        col[j * 32] = (int64_t)d;
+        mpos = d ? j : mpos;
+        mneg = d != MASK ? j : mneg;
+        lz = (lz < 0 && d) ? j : lz;
+    }
+    const int top = j - 1;                             // highest digit written
+    LaneTop t = {-1, 0, 0, 0, 0, false};
+    const bool neg = c < 0;
+    if (neg && lz < 0) lz = top + 1;                   // all written digits 0: the first sign digit
+    const int m = neg ? (mneg > lz ? mneg : lz) : mpos;
+    if (m >= 0) {
+        auto dig = [&](int k) -> uint64_t {            // magnitude digit k (k <= m)
+            if (k < 0) return 0;
+            // digits below lo were never written (zero); above top they are sign digits (R-1)
+            const uint64_t d = k <= top ? (uint64_t)col[k * 32] : MASK;
+            if (!neg) return d;
+            return k < lz ? 0 : (k == lz ? (uint64_t)R - d : MASK - d);
+        };
+        t.m = m;
+        t.sign = neg;
+        t.dm = dig(m);
+        t.dm1 = dig(m - 1);
+        t.dm2 = dig(m - 2);
+        t.below = lz < m - 2;
+    }
+#pragma unroll 4
+    for (int k = lo; k <= top; ++k) col[k * 32] = 0;
+    return t;
+}
+
 // RN-even rounding of the magnitude described by `t` to a format (prec, emin, emax as in
 // finalize_warp: binary64 53 / 0 / 2047, binary32 24 / 925 / 255); the same three-digit window.
 __device__ __forceinline__ uint64_t lane_round(const LaneTop& t, int prec, int emin, int emax, bool is64,

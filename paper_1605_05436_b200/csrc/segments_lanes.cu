@@ -96,9 +96,9 @@ __device__ __forceinline__ int lane_regularize_range(int64_t* col, int lo, int h
 
 // Round the lane's regularized column (segment s of `count` elements) into the segment outputs:
 // both roundings and the flags exactly as finalize_warp reports them, and the canonical image.
-__device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
-                                                   int hi) {
-    const LaneTop t = lane_canonical_top(col, lo, hi);
+// the outputs from a segment's canonical top (col: its canonical digits, read only for the image)
+__device__ __forceinline__ void lane_store_top(const LaneTop& t, const int64_t* col, uint32_t flags, const SegOut& o,
+                                               uint64_t s) {
     uint32_t rf = 0;
     // the binary32 rounding only when its value or the flags (which carry its bits) are wanted
     const bool want32 = o.out32 || o.flags;
@@ -116,6 +116,11 @@ __device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags,
     if (o.out32) o.out32[s] = __uint_as_float(b32);
     if (o.flags) o.flags[s] = fl;
     if (o.canon) lane_canon_image(col, t.m, t.sign, o.canon + s * XSUM_CANON_LIMBS);
+}
+
+__device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
+                                                   int hi) {
+    lane_store_top(lane_canonical_top(col, lo, hi), col, flags, o, s);
 }
 
 template <int DT, bool VEC>
@@ -319,9 +324,27 @@ cudaError_t sum_segments_lanes_csr(const void* x, int dtype, uint64_t nseg, cons
 // pipe idle: ncu r01, 26% of stall samples on the first use of a load); NaN/Inf patterns are summed
 // unchecked like finite values and, if the lane saw one, cancelled by a rescan of its segment
 // (K2's scheme; <= 2 x 256 adds stay far inside the int64 headroom, so no flush is needed).
+// End of a segment in the binary64 K11 kernels: the raw digits [lo, hi] (hi < 0: nothing added)
+// rounded and zeroed by one carry chain (lane_top_chain); the generic path when the image is wanted.
+__device__ __forceinline__ void lane_epilogue64(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
+                                                int hi) {
+    if (hi < 0) lo = hi = 0;
+    if (o.canon) {
+        hi = lane_regularize_range(col, lo, hi);
+        lane_store_segment(col, flags, o, s, lo, hi);
+#pragma unroll 4
+        for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+        return;
+    }
+    lane_store_top(lane_top_chain(col, lo, hi), col, flags, o, s);
+}
+
 constexpr int SLP = 16;                     // elements prefetched per lane (8 x 16 B)
 #ifndef XS_SL_PF
 #define XS_SL_PF 1
+#endif
+#ifndef XS_SL_TMA
+#define XS_SL_TMA 1          // short rows through the bulk-copy staging kernel (k_segments_lanes64s)
 #endif
 __global__ void __launch_bounds__(SL_WARPS * 32, 1)
 k_segments_lanes64(const double* __restrict__ x, uint64_t nseg, uint64_t len, SegOut o, uint32_t one, uint32_t mone) {
@@ -402,12 +425,127 @@ k_segments_lanes64(const double* __restrict__ x, uint64_t nseg, uint64_t len, Se
                 column_fix_special(col, v.z, v.w, flags, one);
             }
         }
-        if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
-        if (hi < 0) lo = hi = 0;
-        lane_store_segment(col, flags, o, s, lo, hi);
-#pragma unroll 4
-        for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+        lane_epilogue64(col, flags, o, s, lo, hi);
     }
+}
+
+// K11 for SHORT binary64 rows (even length <= SLS_MAX, 16-B aligned; c5s16): a warp's 32 segments are
+// one contiguous span of 32 * len doubles, fetched by ONE bulk copy (cp.async.bulk, the TMA engine)
+// into a shared-memory staging buffer - double-buffered per warp, the next group's copy in flight
+// while this group is summed - and each lane reads its own segment from shared memory, in a
+// rotated vector order that keeps a quarter warp on distinct banks (the sum is order-free). The
+// per-lane 16-B global loads of k_segments_lanes64 touch 32 lines per warp instruction: ncu (r02)
+// showed the L1 data pipe 84% busy, half of it global-load wavefronts.
+#ifndef XS_SLS_NBUF
+#define XS_SLS_NBUF 1            // staging buffers per warp (tools/variants.py: 1 -> 15 warps, 2 -> 12 warps)
+#endif
+constexpr int SLS_NBUF = XS_SLS_NBUF;
+// lane columns 10.5 KB + NBUF x 4 KB staging per warp: 15 x 14.5 KB / 12 x 18.5 KB <= 227 KB
+constexpr int SLS_WARPS = SLS_NBUF == 1 ? 15 : 12;
+constexpr int SLS_MAX = 16;                    // doubles per segment (4 KB per group of 32 segments)
+constexpr size_t SLS_STAGE = 32 * SLS_MAX * 8;
+constexpr size_t SLS_SMEM = (size_t)SLS_WARPS * (D * 32 * 8 + SLS_NBUF * SLS_STAGE) + SLS_WARPS * 2 * 8;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(SLS_WARPS * 32, 1)
+k_segments_lanes64s(const double* __restrict__ x, uint64_t nseg, uint32_t len, SegOut o, uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(128) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    uint8_t* stage = reinterpret_cast<uint8_t*>(win + SLS_WARPS * D * 32) + (size_t)warp * SLS_NBUF * SLS_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(win + SLS_WARPS * D * 32) +
+                                                 (size_t)SLS_WARPS * SLS_NBUF * SLS_STAGE) + warp * 2;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
+    const uint64_t groups = (nseg + 31) / 32;
+    const uint64_t gstride = (uint64_t)gridDim.x * SLS_WARPS;
+    const uint32_t nv = len / 2;                                 // 16-B vectors per segment
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    if (lane == 0) {
+        mbar_init(bar_s);
+        mbar_init(bar_s + 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](uint64_t gg, int b) {
+        if (lane == 0 && gg < groups) {
+            const uint64_t s0 = gg * 32;
+            const uint64_t ns = nseg - s0 < 32 ? nseg - s0 : 32;
+            bulk_load(stage_s + b * (uint32_t)SLS_STAGE, x + s0 * len, (uint32_t)(ns * len * 8), bar_s + 8 * b);
+        }
+    };
+    uint64_t g = (uint64_t)blockIdx.x * SLS_WARPS + warp;
+    issue(g, 0);
+    uint32_t phases = 0;                                         // bit b: the parity buffer b waits for
+    int b = 0;
+    for (; g < groups; g += gstride) {
+        if (SLS_NBUF == 2) issue(g + gstride, b ^ 1);            // in flight while this group is summed
+        mbar_wait(bar_s + 8 * b, (phases >> b) & 1u);
+        phases ^= 1u << b;
+        const uint64_t s = g * 32 + lane;
+        const bool mine = s < nseg;
+        int lo = D, hi = -1;
+        uint32_t flags = 0;
+        if (mine) {
+            const uint4* sv = reinterpret_cast<const uint4*>(stage + b * SLS_STAGE + (size_t)lane * len * 8);
+            uint32_t nspec = 0;
+            auto addc = [&](uint32_t xl, uint32_t xh) {
+                const Chunks c = decompose(xl, xh, one, mone);
+                nspec = spec_fold(nspec, c);
+                column_add(col, c, one);
+                lo = min(lo, (int)c.i);
+                hi = max(hi, (int)c.i + 1);
+            };
+            uint32_t u = (uint32_t)lane % nv;                    // rotated start: distinct banks
+#pragma unroll 4
+            for (uint32_t q = 0; q < nv; ++q) {
+                const uint4 v = sv[u];
+                addc(v.x, v.y);
+                addc(v.z, v.w);
+                u = u + 1 == nv ? 0 : u + 1;
+            }
+            if (spec_hit(nspec)) {                               // rare: cancel NaN/Inf patterns (R10)
+                for (uint32_t q = 0; q < nv; ++q) {
+                    const uint4 v = sv[q];
+                    column_fix_special(col, v.x, v.y, flags, one);
+                    column_fix_special(col, v.z, v.w, flags, one);
+                }
+            }
+        }
+        __syncwarp();                                            // this group's staging is consumed
+        if (SLS_NBUF == 1) issue(g + gstride, 0);                // the next copy overlaps the epilogue
+        if (mine) lane_epilogue64(col, flags, o, s, lo, hi);
+        if (SLS_NBUF == 2) b ^= 1;
+    }
+}
+
+static cudaError_t launch_lanes64s(const void* x, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
+                                   cudaStream_t s) {
+    static unsigned long long done = 0;
+    if (cudaError_t e = ensure_smem(k_segments_lanes64s, SLS_SMEM, done)) return e;
+    const uint64_t groups = (nseg + 31) / 32;
+    const uint64_t want = (groups + SLS_WARPS - 1) / SLS_WARPS;
+    const unsigned g = (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
+    k_segments_lanes64s<<<g, SLS_WARPS * 32, SLS_SMEM, s>>>(static_cast<const double*>(x), nseg, (uint32_t)len, o, 1u,
+                                                            0xFFFFFFFFu);
+    note_launch();
+    return cudaGetLastError();
 }
 
 static cudaError_t launch_lanes64(const void* x, uint64_t nseg, uint64_t len, const SegOut& o, int num_sms,
@@ -443,8 +581,9 @@ cudaError_t sum_segments_lanes(const void* x, int dtype, uint64_t nseg, uint64_t
     switch (dtype) {
         case XSUM_DT_F64:
             if (len % 2 == 0 && ((uintptr_t)x & 15) == 0)
-                return len <= SEG_LANES_MAX ? launch_lanes64(x, nseg, len, o, num_sms, s)
-                                            : launch_lanes<XSUM_DT_F64, true>(x, nseg, len, o, num_sms, s);
+                return len <= (uint64_t)SLS_MAX && XS_SL_TMA ? launch_lanes64s(x, nseg, len, o, num_sms, s)
+                       : len <= SEG_LANES_MAX ? launch_lanes64(x, nseg, len, o, num_sms, s)
+                                              : launch_lanes<XSUM_DT_F64, true>(x, nseg, len, o, num_sms, s);
             return launch_lanes<XSUM_DT_F64, false>(x, nseg, len, o, num_sms, s);
         case XSUM_DT_F32: return launch_lanes<XSUM_DT_F32, false>(x, nseg, len, o, num_sms, s);
         case XSUM_DT_F16: return launch_lanes<XSUM_DT_F16, false>(x, nseg, len, o, num_sms, s);

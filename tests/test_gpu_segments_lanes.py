@@ -188,3 +188,34 @@ def test_csr_lanes_vs_oracle(xs, fmt, mix):
             want = r.bits if fmt == "f64" else r.bits_f32
             assert int(v[s]) == want and int(fl[s]) == r.flags, (fmt, mix, s, lens[s])
             assert (cn[s] == limbs).all(), (fmt, mix, s)
+
+
+@pytest.mark.parametrize("L", [2, 4, 6, 16, 18, 64, 256])
+@pytest.mark.parametrize("narrow", [False, True])
+def test_lanes_f64_values_only_paths(xs, L, narrow):
+    """binary64 equal segments WITHOUT canonical images: the one-pass rounding of the raw digits
+    (lane_top_fused) in both the bulk-copy kernel (L <= 16) and the prefetching one, values alone
+    and values + flags, vs the oracle's per-segment sums; with exact-zero, negative, borrow-chain
+    (a large term cancelled down to a tiny remainder) and special-value segments."""
+    import torch
+    nseg = 3001
+    b = data("f64", nseg * L, 40 + L, narrow)
+    x = b.view(np.float64).copy()
+    # crafted segments: exact zero, a cancellation leaving a tiny negative remainder, a tie
+    x[0:L] = 0.0
+    x[L:2 * L] = 0.0
+    x[L] = 2.0 ** 900
+    x[L + 1] = -(2.0 ** 900)
+    if L >= 4:
+        x[L + 2] = 2.0 ** -1000
+        x[L + 3] = -(2.0 ** -999)
+    x[2 * L:3 * L] = 0.0
+    x[2 * L] = 1.0
+    x[2 * L + 1] = 2.0 ** -53
+    d = torch.from_numpy(x).cuda()
+    b64, _, fl, _ = oracle.sum_segments(x, seg_len=L)
+    v, _, _ = xs.sum_segments(d, L)
+    assert (v.cpu().numpy().view(np.uint64) == b64).all()
+    v2, _, f2 = xs.sum_segments(d, L, flags=True)
+    assert (v2.cpu().numpy().view(np.uint64) == b64).all()
+    assert (f2.cpu().numpy().astype(np.uint32) == fl).all()

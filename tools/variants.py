@@ -31,6 +31,8 @@ VARIANTS = {
     "sh_q8u4": ["-DXS_SH_LPS=8", "-DXS_SH_U=4"],
     "sl_full": ["-DXS_SL_FULL"],
     "sl_nopf": ["-DXS_SL_PF=0"],
+    "sl_notma": ["-DXS_SL_TMA=0"],
+    "sls_nbuf2": ["-DXS_SLS_NBUF=2"],
     "str_nb3": ["-DXS_STR_NB=3"],
     "str_nb6": ["-DXS_STR_NB=6"],
     "str_u4nb8": ["-DXS_STR_UNR=4", "-DXS_STR_NB=8"],

@@ -31,12 +31,16 @@ using FmtBF16 = H16Fmt<7, 8, 3, 131071, 941>;
 // Segments empty their bins at every segment's end, so fewer bins beat longer windows there:
 // bfloat16 groups of 16 exponents (17 groups; 511 * 255 * 2^15 < 2^32).
 using FmtBF16Seg = H16Fmt<7, 8, 4, 511, 941>;
+// The quarter-warp segments kernel empties its bins once per 16 steps of 32 elements per lane: the
+// longest window that still fits, 514 * 255 * 2^15 < 2^32, covers one 4096-element segment.
+using FmtBF16Q = H16Fmt<7, 8, 4, 514, 941>;
 // a window of FLUSH adds of the largest M 2^o cannot wrap an unsigned 32-bit bin
 template <class F>
 constexpr bool flush_fits() {
     return (unsigned long long)F::FLUSH * ((2ull << F::t) - 1) * (1ull << ((1 << F::SB) - 1)) < (1ull << 32);
 }
-static_assert(flush_fits<FmtF16>() && flush_fits<FmtBF16>() && flush_fits<FmtBF16Seg>(), "bin window too long");
+static_assert(flush_fits<FmtF16>() && flush_fits<FmtBF16>() && flush_fits<FmtBF16Seg>() && flush_fits<FmtBF16Q>(),
+              "bin window too long");
 
 // One summand (checked paths): h = |x| bit pattern (15 bits), s = sign bit; bins = this lane's
 // bin column (bin b at word b*32).

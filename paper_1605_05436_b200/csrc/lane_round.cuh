@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "xsum_device.cuh"
+#include "xsum_kernels.h"
 
 namespace xs {
 
@@ -141,18 +142,19 @@ __device__ __forceinline__ LaneTop lane_canonical_top(int64_t* col, int first = 
 // the sign). For A >= 0 the magnitude digits are d_j; for A < 0 they are e_j = R-1-d_j above the
 // lowest non-zero digit lz, R-d_lz at lz and 0 below (|A| = ~A + 1). So the chain only records the
 // highest index with d != 0, the highest with d != R-1 and lz, and the window digits are read back.
+template <int STRIDE = 32>
 __device__ __forceinline__ LaneTop lane_top_chain(int64_t* col, int lo, int hi) {
     int64_t c = 0;
     int mpos = -1, mneg = -1, lz = -1;
     int j = lo;
     for (; j < D; ++j) {
         int64_t y = 0;
-        if (j <= hi) y = col[j * 32];
+        if (j <= hi) y = col[j * STRIDE];
         else if (c == 0 || c == -1) break;             // the carry has settled: sign extension above
         const int64_t t = y + c;
         const uint64_t d = (uint64_t)t & MASK;
         c = t >> W;
-        col[j * 32] = (int64_t)d;
+        col[j * STRIDE] = (int64_t)d;
         mpos = d ? j : mpos;
         mneg = d != MASK ? j : mneg;
         lz = (lz < 0 && d) ? j : lz;
@@ -166,7 +168,7 @@ __device__ __forceinline__ LaneTop lane_top_chain(int64_t* col, int lo, int hi) 
         auto dig = [&](int k) -> uint64_t {            // magnitude digit k (k <= m)
             if (k < 0) return 0;
             // digits below lo were never written (zero); above top they are sign digits (R-1)
-            const uint64_t d = k <= top ? (uint64_t)col[k * 32] : MASK;
+            const uint64_t d = k <= top ? (uint64_t)col[k * STRIDE] : MASK;
             if (!neg) return d;
             return k < lz ? 0 : (k == lz ? (uint64_t)R - d : MASK - d);
         };
@@ -178,7 +180,7 @@ __device__ __forceinline__ LaneTop lane_top_chain(int64_t* col, int lo, int hi) 
         t.below = lz < m - 2;
     }
 #pragma unroll 4
-    for (int k = lo; k <= top; ++k) col[k * 32] = 0;
+    for (int k = lo; k <= top; ++k) col[k * STRIDE] = 0;
     return t;
 }
 
@@ -247,6 +249,29 @@ __device__ __forceinline__ void lane_canon_image(const int64_t* col, int top, in
         }
         out[limb++] = v;
     }
+}
+
+// (SegOut: xsum_kernels.h)
+// the outputs from a segment's canonical top (col: its canonical digits, read only for the image)
+__device__ __forceinline__ void lane_store_top(const LaneTop& t, const int64_t* col, uint32_t flags, const SegOut& o,
+                                               uint64_t s) {
+    uint32_t rf = 0;
+    // the binary32 rounding only when its value or the flags (which carry its bits) are wanted
+    const bool want32 = o.out32 || o.flags;
+    uint64_t b64 = (o.out || o.flags) ? lane_round(t, 53, 0, 2047, true, rf) : 0;
+    uint32_t b32 = want32 ? (uint32_t)lane_round(t, 24, 925, 255, false, rf) : 0;
+    const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf;
+    if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
+        b64 = 0x7FF8000000000000ull; b32 = 0x7FC00000u;
+    } else if (fl & XSUM_F_PINF) {
+        b64 = 0x7FF0000000000000ull; b32 = 0x7F800000u;
+    } else if (fl & XSUM_F_NINF) {
+        b64 = 0xFFF0000000000000ull; b32 = 0xFF800000u;
+    }
+    if (o.out) o.out[s] = __longlong_as_double((long long)b64);
+    if (o.out32) o.out32[s] = __uint_as_float(b32);
+    if (o.flags) o.flags[s] = fl;
+    if (o.canon) lane_canon_image(col, t.m, t.sign, o.canon + s * XSUM_CANON_LIMBS);
 }
 
 }  // namespace xs

@@ -96,27 +96,6 @@ __device__ __forceinline__ int lane_regularize_range(int64_t* col, int lo, int h
 
 // Round the lane's regularized column (segment s of `count` elements) into the segment outputs:
 // both roundings and the flags exactly as finalize_warp reports them, and the canonical image.
-// the outputs from a segment's canonical top (col: its canonical digits, read only for the image)
-__device__ __forceinline__ void lane_store_top(const LaneTop& t, const int64_t* col, uint32_t flags, const SegOut& o,
-                                               uint64_t s) {
-    uint32_t rf = 0;
-    // the binary32 rounding only when its value or the flags (which carry its bits) are wanted
-    const bool want32 = o.out32 || o.flags;
-    uint64_t b64 = (o.out || o.flags) ? lane_round(t, 53, 0, 2047, true, rf) : 0;
-    uint32_t b32 = want32 ? (uint32_t)lane_round(t, 24, 925, 255, false, rf) : 0;
-    const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf;
-    if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
-        b64 = 0x7FF8000000000000ull; b32 = 0x7FC00000u;
-    } else if (fl & XSUM_F_PINF) {
-        b64 = 0x7FF0000000000000ull; b32 = 0x7F800000u;
-    } else if (fl & XSUM_F_NINF) {
-        b64 = 0xFFF0000000000000ull; b32 = 0xFF800000u;
-    }
-    if (o.out) o.out[s] = __longlong_as_double((long long)b64);
-    if (o.out32) o.out32[s] = __uint_as_float(b32);
-    if (o.flags) o.flags[s] = fl;
-    if (o.canon) lane_canon_image(col, t.m, t.sign, o.canon + s * XSUM_CANON_LIMBS);
-}
 
 __device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
                                                    int hi) {

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "h16_common.cuh"
+#include "lane_round.cuh"
 #include "xsum_device.cuh"
 #include "xsum_kernels.h"
 
@@ -459,6 +460,136 @@ k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Equal 16-bit segments (16-B aligned, length a multiple of 8): a QUARTER warp per segment, four
+// segments per warp at a time. The whole-warp kernel pays its epilogue (bins -> column, the
+// combine of 32 lane columns, finalize_warp: ~550 warp instructions) for every 4096-element
+// (8 KB) segment - 44% of its instructions (ncu r02: issue 74%, ALU 75%). Here the 8 lanes of a
+// group stream their segment (128 B per load instruction, coalesced), empty their bins into their
+// narrow columns, sum the group's 8 columns row by row into a shared row vector (raw digits), and
+// ONE lane rounds it with the carry chain of K11 (lane_top_chain) - the four groups' leaders in
+// parallel. Canonical images are not produced here (the whole-warp kernel serves those calls).
+// ---------------------------------------------------------------------------------------
+#ifndef XS_HQ_LPS
+#define XS_HQ_LPS 8           // lanes per segment (tools/variants.py)
+#endif
+constexpr int HQ_LPS = XS_HQ_LPS, HQ_SEGS = 32 / HQ_LPS;
+
+template <class F>
+__device__ __noinline__ uint32_t h16q_classify(const uint16_t* xs, uint64_t len, int hl) {
+    uint32_t f = 0;
+    for (uint64_t i = hl; i < len; i += HQ_LPS) f |= h16_special_flags<F>(__ldg(xs + i));
+    return f;
+}
+
+template <class F>
+__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+k_segments_h16q(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one,
+                uint32_t mone) {
+    using S = H16Col<F>;
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t gsum[SSEG_WARPS][HQ_SEGS][S::COLS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & (HQ_LPS - 1), grp = lane / HQ_LPS;
+    int64_t* col = win + warp * (S::COLS * 32) + lane;
+    const int64_t* wb = win + warp * (S::COLS * 32);
+    uint32_t* bins = reinterpret_cast<uint32_t*>(win + SSEG_WARPS * S::COLS * 32) + warp * (F::NBIN * 32) + lane;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bins);
+    const uint32_t sbase2 = sbase * 0x00010001u;
+    constexpr int SU = SSEG_U;
+    constexpr uint32_t WIN_STEPS = F::FLUSH / (SU * 8);           // steps of SU vectors (8 elements each) per bin window
+    static_assert(WIN_STEPS >= 1, "window shorter than one step");
+#pragma unroll
+    for (int j = 0; j < S::COLS; ++j) col[j * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < F::NBIN; ++j) bins[j * 32] = 0;
+    const uint64_t nvec = seg_len / 8;
+    const uint64_t nquads = (nseg + HQ_SEGS - 1) / HQ_SEGS;
+    const uint64_t nw = (uint64_t)gridDim.x * SSEG_WARPS;
+    for (uint64_t qd = (uint64_t)blockIdx.x * SSEG_WARPS + warp; qd < nquads; qd += nw) {
+        const uint64_t s = qd * HQ_SEGS + grp;
+        const bool mine = s < nseg;
+        const uint64_t nv = mine ? nvec : 0;
+        const uint4* body = reinterpret_cast<const uint4*>(x + (mine ? s : 0) * seg_len);
+        uint32_t steps = 0, flushes = 0, nflush = 0;
+        bool special = false;
+        uint4 cur[SU], nxt[SU];
+        auto load = [&](uint4 (&b)[SU], uint64_t v0) {
+            const uint4* p = body + v0 + hl;
+            if (v0 + (uint64_t)SU * HQ_LPS <= nv) {                // a whole step: no per-vector guards
+#pragma unroll
+                for (int u = 0; u < SU; ++u) b[u] = ldg_stream(p + u * HQ_LPS);
+            } else {
+#pragma unroll
+                for (int u = 0; u < SU; ++u)
+                    b[u] = v0 + (uint64_t)u * HQ_LPS + hl < nv ? ldg_stream(p + u * HQ_LPS) : make_uint4(0, 0, 0, 0);
+            }
+        };
+        // zero words decode to +0 (bin of group 0, value 0): padding vectors add nothing
+        constexpr uint64_t STEP = (uint64_t)SU * HQ_LPS;
+        if (nv) load(cur, 0);
+        for (uint64_t v0 = 0; v0 < nv; v0 += STEP) {
+            if (v0 + STEP < nv) load(nxt, v0 + STEP);
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                h16_add_word<F>(sbase, sbase2, cur[u].x, one, mone);
+                h16_add_word<F>(sbase, sbase2, cur[u].y, one, mone);
+                h16_add_word<F>(sbase, sbase2, cur[u].z, one, mone);
+                h16_add_word<F>(sbase, sbase2, cur[u].w, one, mone);
+            }
+            if (++steps == WIN_STEPS) {
+                special |= h16_flush_col<F>(bins, col);
+                steps = 0;
+                ++nflush;
+                if (++flushes == S::REG_FLUSHES) { h16_col_regularize<F>(col); flushes = 0; }
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u) cur[u] = nxt[u];
+        }
+        special |= h16_flush_col<F>(bins, col);
+        // more than one flush: regularize so that the sum of 8 columns stays far inside int64
+        if (__any_sync(FULL, nflush > 0)) h16_col_regularize<F>(col);
+        uint32_t flags = 0;
+        const uint32_t sp = __ballot_sync(FULL, special);
+        if (sp) {                                                  // rare: classify NaN / +-Inf (R10)
+            if ((sp >> (grp * HQ_LPS)) & ((1u << HQ_LPS) - 1u)) flags = h16q_classify<F>(x + s * seg_len, seg_len, hl);
+#pragma unroll
+            for (int d = 1; d < HQ_LPS; d <<= 1) flags |= __shfl_xor_sync(FULL, flags, d);   // within the group
+        }
+        __syncwarp();
+        // the group's 8 columns, row by row (raw digits; rows are digits COL0 + r)
+        for (int r = hl; r < S::COLS; r += HQ_LPS) {
+            int64_t acc = 0;
+#pragma unroll
+            for (int c = 0; c < HQ_LPS; ++c) acc += wb[r * 32 + grp * HQ_LPS + ((c + hl) & (HQ_LPS - 1))];
+            gsum[warp][grp][r] = acc;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < S::COLS; ++j) col[j * 32] = 0;
+        if (hl == 0 && mine) {
+            LaneTop t = lane_top_chain<1>(gsum[warp][grp], 0, S::COLS - 1);
+            if (t.m >= 0) t.m += S::COL0;
+            lane_store_top(t, nullptr, flags, o, s);
+        }
+        __syncwarp();
+    }
+}
+
+template <class F>
+static cudaError_t launch_h16q(const void* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
+                               cudaStream_t s) {
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_segments_h16q<F>, h16seg_smem<F>(), smem_set)) return e;
+    const uint64_t nquads = (nseg + HQ_SEGS - 1) / HQ_SEGS;
+    const uint64_t want = (nquads + SSEG_WARPS - 1) / SSEG_WARPS;
+    const uint64_t cap = (uint64_t)num_sms * 2;
+    const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    k_segments_h16q<F><<<g, SSEG_WARPS * 32, h16seg_smem<F>(), s>>>(static_cast<const uint16_t*>(x), nseg, seg_len, o,
+                                                                     1u, 0xFFFFFFFFu);
+    note_launch();
+    return cudaGetLastError();
+}
+
 template <class F>
 static cudaError_t launch_h16seg(const void* x, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                  const SegOut& o, int num_sms, cudaStream_t s, unsigned long long* ticket) {
@@ -488,14 +619,25 @@ static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, 
     return cudaGetLastError();
 }
 
+#ifndef XS_H16Q
+#define XS_H16Q 1             // quarter-warp 16-bit segments (tools/variants.py: 0 = whole warps)
+#endif
+static bool h16q_ok(const void* x, uint64_t seg_len, const uint64_t* offsets, const SegOut& o) {
+    return XS_H16Q && !offsets && !o.canon && seg_len >= 8 && seg_len % 8 == 0 && ((uintptr_t)x & 15) == 0;
+}
+
 cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t seg_len, const uint64_t* offsets,
                                const SegOut& o, int num_sms, cudaStream_t s, unsigned long long* ticket) {
     if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
         return sum_segments_lanes(x, dtype, nseg, seg_len, o, num_sms, s);
     switch (dtype) {
         case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
-        case XSUM_DT_F16: return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
-        case XSUM_DT_BF16: return launch_h16seg<FmtBF16Seg>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
+        case XSUM_DT_F16:
+            if (h16q_ok(x, seg_len, offsets, o)) return launch_h16q<FmtF16>(x, nseg, seg_len, o, num_sms, s);
+            return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
+        case XSUM_DT_BF16:
+            if (h16q_ok(x, seg_len, offsets, o)) return launch_h16q<FmtBF16Q>(x, nseg, seg_len, o, num_sms, s);
+            return launch_h16seg<FmtBF16Seg>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -33,6 +33,8 @@ VARIANTS = {
     "sl_nopf": ["-DXS_SL_PF=0"],
     "sl_notma": ["-DXS_SL_TMA=0"],
     "sls_nbuf2": ["-DXS_SLS_NBUF=2"],
+    "h16q0": ["-DXS_H16Q=0"],
+    "hq_lps4": ["-DXS_HQ_LPS=4"],
     "str_nb3": ["-DXS_STR_NB=3"],
     "str_nb6": ["-DXS_STR_NB=6"],
     "str_u4nb8": ["-DXS_STR_UNR=4", "-DXS_STR_NB=8"],
@@ -89,6 +91,8 @@ elif {cfg!r}.startswith("str"):
 elif {cfg!r} == "c5csr":
     x = synth.device_generate("c5csr")
     csr = synth.csr_offsets("c5csr", device="cuda")
+elif {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
+    pass
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = _D() if {cfg!r}.startswith("str") else xsum.Accumulator()
@@ -100,6 +104,8 @@ if {cfg!r} == "c5csr":
             return xsum_res, None
     xsum_res = acc.sum(x)[0]
     acc = _C()
+if {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
+    x = synth.device_bits({{"f16seg": "c2f16", "bf16seg": "c2bf16", "f32seg": "c2f32"}}[{cfg!r}])
 if {cfg!r}.endswith("seg") or {cfg!r} == "c5s16":
     SEGL = 16 if {cfg!r} == "c5s16" else 4096
     class _S:

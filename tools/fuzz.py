@@ -5,8 +5,9 @@
 Each case draws an input format, a size (log-uniform up to 2^22), a base misalignment, a content
 mix (uniform bit patterns, a narrow exponent band, cancelling pairs, sprinkled NaN/Inf, zeros and
 subnormals) and an API (fused sum, chunked accumulate, host streaming, shard merge, sparse image
-round trip, equal / CSR segments, checkpoint / resume, strided reductions), and compares value bits, binary32 bits, flags and the canonical
-image with the oracle. Prints one line per failure (with the case seed) and a summary."""
+round trip, equal segments with or without images / CSR segments, checkpoint / resume, strided
+reductions, the condition-number-sensitive sum vs oracle/condsens.py), and compares value bits,
+binary32 bits, flags and the canonical image with the oracle. Prints one line per failure (with the case seed) and a summary."""
 from __future__ import annotations
 
 import os
@@ -81,7 +82,21 @@ def one_case(seed: int) -> str | None:
     off = int(rng.integers(0, 8))
     b = content(rng, fmt, n)
     d = to_dev(b, fmt, off)
-    api = rng.integers(0, 8)
+    api = rng.integers(0, 9)
+    if api == 8:                                          # condition-number-sensitive sum (binary64)
+        if fmt != "f64" or n > 6000:
+            return None
+        from oracle import condsens as cs
+        rule = int(rng.integers(1, 3))
+        res, info, canon = xs.condsens_sum(d, rule)
+        vals = b.view(np.float64).tolist()
+        o = cs.condsens_sum(vals, rule=rule)
+        ok = info.r == o.r and info.iterations == o.iterations and info.exact == o.exact
+        if o.r <= 16:
+            ok = ok and info.e_cut == o.e_cut and info.root == o.root
+        ob = int(np.array([o.value], dtype=np.float64).view(np.uint64)[0])
+        ok = ok and (res.bits == ob or (np.isnan(o.value) and np.isnan(res.value)))
+        return None if ok else f"f64 n={n} condsens rule {rule}"
     if api == 7 and n:                                    # strided reduction [outer][len][inner]
         inner = int(rng.integers(2, 80))
         outer = int(rng.integers(1, 4))
@@ -155,7 +170,8 @@ def one_case(seed: int) -> str | None:
         if nseg == 0:
             return None
         bounds = [(s * L, (s + 1) * L) for s in range(nseg)]
-        vals, canon, flags = xs.sum_segments(d[:nseg * L], L, canon=True, flags=True)
+        want_canon = bool(rng.integers(0, 2))         # values-only calls take other kernels (K11s, K9q)
+        vals, canon, flags = xs.sum_segments(d[:nseg * L], L, canon=want_canon, flags=True)
     else:
         nseg = int(rng.integers(1, 40))
         cuts = np.sort(rng.integers(0, n + 1, size=nseg - 1))
@@ -163,13 +179,13 @@ def one_case(seed: int) -> str | None:
         bounds = list(zip(offs[:-1], offs[1:]))
         vals, canon, flags = xs.sum_segments_csr(d, torch.from_numpy(offs).cuda(), canon=True, flags=True)
     v = vals.cpu().numpy()
-    cn = canon.cpu().numpy().view(np.uint64)
+    cn = canon.cpu().numpy().view(np.uint64) if canon is not None else None
     fl = flags.cpu().numpy().view(np.uint32)
     for s, (a, e) in enumerate(bounds):
         r, limbs = ref(fmt, b[a:e])
         want = r.bits if fmt == "f64" else r.bits_f32
         got = int(v[s:s + 1].view(np.uint64 if fmt == "f64" else np.uint32)[0])
-        if got != want or fl[s] != r.flags or not (cn[s] == limbs).all():
+        if got != want or fl[s] != r.flags or (cn is not None and not (cn[s] == limbs).all()):
             return f"{fmt} n={n} segments api={api} seg {s} [{a},{e})"
     return None
 

@@ -21,6 +21,9 @@ VARIANTS = {
     "base": [],        # build this one from another checkout of the sources for same-box A/B
     # examples of compile-time knobs (see the kernels): register-buffer depth of each kernel
     "acc_nb4": ["-DXS_ACC_NB=4"],
+    "acc_nb3": ["-DXS_ACC_NB=3"],
+    "acc_u2nb8": ["-DXS_ACC_U=2", "-DXS_ACC_NB=8"],
+    "acc_w12": ["-DXS_ACC_WARPS=12"],
     "seg_nb4": ["-DXS_SEG_NB=4"],
     "seg_u2nb4": ["-DXS_SEG_U=2", "-DXS_SEG_NB=4"],
     "seg_u2nb8": ["-DXS_SEG_U=2", "-DXS_SEG_NB=8"],
@@ -117,6 +120,11 @@ if {cfg!r}.endswith("seg") or {cfg!r} == "c5s16":
     acc = _S()
 for _ in range(5): acc.sum(x)
 torch.cuda.synchronize()
+import time as _t
+_t0 = _t.perf_counter()
+while _t.perf_counter() - _t0 < float(os.environ.get("VARIANT_SUSTAIN", "0")):   # power-capped steady state
+    for _ in range(20): acc.sum(x)
+    torch.cuda.synchronize()
 ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range({steps})]
 for a, b in ev:
     a.record(); acc.sum(x); b.record()

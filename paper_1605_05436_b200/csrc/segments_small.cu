@@ -575,6 +575,133 @@ k_segments_h16q(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len,
     }
 }
 
+// Equal binary32 segments (16-B aligned, length a multiple of 4), a quarter warp per segment: the
+// same structure as k_segments_h16q with K9's 64-bit exponent-group bins (one read-modify-write per
+// element, emptied every SSEG_FLUSH adds). NaN/Inf patterns are summed as finite and a group that
+// saw one rescans its segment, cancelling them in its lanes' bins.
+template <class F>
+__device__ __noinline__ void smallq_rescan(uint64_t* bins, int64_t* col, const uint4* body, uint64_t nvec, int hl,
+                                           uint32_t& flags, uint32_t one) {
+    uint32_t dummy = 0, adds = 0, flushes = 0;
+    scol_regularize<F>(col);                            // fresh headroom for the flushes below
+    for (uint64_t v = hl; v < nvec; v += HQ_LPS) {
+        const uint4 q = ldg_stream(body + v);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t f = sspecial_flags<F>(w[i]);
+            if (f) {
+                flags |= f;
+                sbin_add<F>(bins, w[i] ^ (1u << (F::t + F::l)), dummy, one);
+                if (++adds == SSEG_FLUSH) {
+                    sbin_flush<F>(bins, col);
+                    adds = 0;
+                    if (++flushes == SSEG_REG_FLUSHES) { scol_regularize<F>(col); flushes = 0; }
+                }
+            }
+        }
+    }
+    sbin_flush<F>(bins, col);
+}
+
+template <class F>
+__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+k_segments_smallq(const float* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one) {
+    extern __shared__ __align__(16) int64_t win[];
+    __shared__ int64_t gsum[SSEG_WARPS][HQ_SEGS][F::COLS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & (HQ_LPS - 1), grp = lane / HQ_LPS;
+    int64_t* col = win + warp * (F::COLS * 32) + lane;
+    const int64_t* wb = win + warp * (F::COLS * 32);
+    uint64_t* bins = reinterpret_cast<uint64_t*>(win + SSEG_WARPS * F::COLS * 32) + warp * (F::NBIN * 32) + lane;
+    constexpr int SU = SSEG_U;
+    constexpr uint32_t WIN_STEPS = SSEG_FLUSH / (SU * 4);        // steps of SU vectors (4 elements each)
+#pragma unroll
+    for (int j = 0; j < F::COLS; ++j) col[j * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < F::NBIN; ++j) bins[j * 32] = 0;
+    const uint64_t nvec = seg_len / 4;
+    const uint64_t nquads = (nseg + HQ_SEGS - 1) / HQ_SEGS;
+    const uint64_t nw = (uint64_t)gridDim.x * SSEG_WARPS;
+    for (uint64_t qd = (uint64_t)blockIdx.x * SSEG_WARPS + warp; qd < nquads; qd += nw) {
+        const uint64_t s = qd * HQ_SEGS + grp;
+        const bool mine = s < nseg;
+        const uint64_t nv = mine ? nvec : 0;
+        const uint4* body = reinterpret_cast<const uint4*>(x + (mine ? s : 0) * seg_len);
+        uint32_t steps = 0, flushes = 0, nflush = 0, spec = 0;
+        uint4 cur[SU], nxt[SU];
+        auto load = [&](uint4 (&b)[SU], uint64_t v0) {
+            const uint4* p = body + v0 + hl;
+            if (v0 + (uint64_t)SU * HQ_LPS <= nv) {
+#pragma unroll
+                for (int u = 0; u < SU; ++u) b[u] = ldg_stream(p + u * HQ_LPS);
+            } else {
+#pragma unroll
+                for (int u = 0; u < SU; ++u)
+                    b[u] = v0 + (uint64_t)u * HQ_LPS + hl < nv ? ldg_stream(p + u * HQ_LPS) : make_uint4(0, 0, 0, 0);
+            }
+        };
+        constexpr uint64_t STEP = (uint64_t)SU * HQ_LPS;
+        if (nv) load(cur, 0);
+        for (uint64_t v0 = 0; v0 < nv; v0 += STEP) {
+            if (v0 + STEP < nv) load(nxt, v0 + STEP);
+#pragma unroll
+            for (int u = 0; u < SU; ++u) sbin_add_vec<F>(bins, cur[u], spec, one);   // +0 patterns add 0
+            if (++steps == WIN_STEPS) {
+                sbin_flush<F>(bins, col);
+                steps = 0;
+                ++nflush;
+                if (++flushes == SSEG_REG_FLUSHES) { scol_regularize<F>(col); flushes = 0; }
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u) cur[u] = nxt[u];
+        }
+        sbin_flush<F>(bins, col);
+        uint32_t flags = 0;
+        const uint32_t sp = __ballot_sync(FULL, spec == F::EM);
+        if (sp) {                                                  // rare: NaN/Inf patterns (R10)
+            if ((sp >> (grp * HQ_LPS)) & ((1u << HQ_LPS) - 1u)) {
+                smallq_rescan<F>(bins, col, body, nv, hl, flags, one);
+                ++nflush;
+            }
+#pragma unroll
+            for (int d = 1; d < HQ_LPS; d <<= 1) flags |= __shfl_xor_sync(FULL, flags, d);   // within the group
+        }
+        // after more than one flush, regularize: the sum of the group's columns stays far inside int64
+        if (__any_sync(FULL, nflush > 0)) scol_regularize<F>(col);
+        __syncwarp();
+        for (int r = hl; r < F::COLS; r += HQ_LPS) {
+            int64_t acc = 0;
+#pragma unroll
+            for (int c = 0; c < HQ_LPS; ++c) acc += wb[r * 32 + grp * HQ_LPS + ((c + hl) & (HQ_LPS - 1))];
+            gsum[warp][grp][r] = acc;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < F::COLS; ++j) col[j * 32] = 0;
+        if (hl == 0 && mine) {
+            LaneTop t = lane_top_chain<1>(gsum[warp][grp], 0, F::COLS - 1);
+            if (t.m >= 0) t.m += F::COL0;
+            lane_store_top(t, nullptr, flags, o, s);
+        }
+        __syncwarp();
+    }
+}
+
+template <class F>
+static cudaError_t launch_smallq(const void* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
+                                 cudaStream_t s) {
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_segments_smallq<F>, sseg_smem<F>(), smem_set)) return e;
+    const uint64_t nquads = (nseg + HQ_SEGS - 1) / HQ_SEGS;
+    const uint64_t want = (nquads + SSEG_WARPS - 1) / SSEG_WARPS;
+    const uint64_t cap = (uint64_t)num_sms * 2;
+    const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    k_segments_smallq<F><<<g, SSEG_WARPS * 32, sseg_smem<F>(), s>>>(static_cast<const float*>(x), nseg, seg_len, o,
+                                                                     1u);
+    note_launch();
+    return cudaGetLastError();
+}
+
 template <class F>
 static cudaError_t launch_h16q(const void* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
                                cudaStream_t s) {
@@ -631,7 +758,10 @@ cudaError_t sum_segments_small(const void* x, int dtype, uint64_t nseg, uint64_t
     if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
         return sum_segments_lanes(x, dtype, nseg, seg_len, o, num_sms, s);
     switch (dtype) {
-        case XSUM_DT_F32: return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
+        case XSUM_DT_F32:
+            if (XS_H16Q && !offsets && !o.canon && seg_len >= 4 && seg_len % 4 == 0 && ((uintptr_t)x & 15) == 0)
+                return launch_smallq<SF32>(x, nseg, seg_len, o, num_sms, s);
+            return launch_small<SF32>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);
         case XSUM_DT_F16:
             if (h16q_ok(x, seg_len, offsets, o)) return launch_h16q<FmtF16>(x, nseg, seg_len, o, num_sms, s);
             return launch_h16seg<FmtF16>(x, nseg, seg_len, offsets, o, num_sms, s, ticket);

@@ -183,24 +183,25 @@ def test_every_exponent_each_format(xs, fmt):
     assert res.bits == r.bits and res.bits_f32 == r.bits_f32 and (cn == limbs).all()
 
 
-@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+@pytest.mark.parametrize("fmt", ["f32", "f16", "bf16"])
 @pytest.mark.parametrize("seg_len,nseg", [(264, 37), (512, 101), (4096, 203), (8200, 9), (70_000, 5)])
 def test_h16_equal_segments_values_only(xs, fmt, seg_len, nseg):
-    """16-bit equal segments without canonical images (the quarter-warp kernel when the base is
-    16-B aligned and the length a multiple of 8): binary32 values, binary64 values and flags of
+    """binary32 / 16-bit equal segments without canonical images (the quarter-warp kernels when the
+    base is 16-B aligned and the length a multiple of 4 / 8): binary32 values, binary64 values and flags of
     every segment vs the oracle's per-segment sums - segments longer than a bin window (bfloat16:
     511 adds per lane), a partial last group of four, specials, and the fallback for a
     misaligned base."""
     import torch
     b = bits_data(fmt, seg_len * nseg, 700 + seg_len)
-    b64, b32, fl, _ = oracle.sum_segments(b, seg_len=seg_len, fmt=fmt)
+    b64, b32, fl, _ = oracle.sum_segments(b.view(np.float32) if fmt == "f32" else b, seg_len=seg_len,
+                                          fmt=None if fmt == "f32" else fmt)
     for off in (0, 1):
         d = to_dev(b, fmt, off)
         v32, _, f = xs.sum_segments(d, seg_len, flags=True)
         assert (v32.cpu().numpy().view(np.uint32) == b32).all(), (fmt, seg_len, off)
         assert (f.cpu().numpy().view(np.uint32) == fl).all(), (fmt, seg_len, off)
         out = torch.empty(nseg, dtype=torch.float64, device="cuda")
-        rc = xs.lib().xsum_sum_segments_ex(d.data_ptr(), 2 if fmt == "f16" else 3, nseg, seg_len, None,
+        rc = xs.lib().xsum_sum_segments_ex(d.data_ptr(), {"f32": 1, "f16": 2, "bf16": 3}[fmt], nseg, seg_len, None,
                                            out.data_ptr(), None, None, None, xs._stream_ptr(d.device))
         assert rc == 0
         assert (out.cpu().numpy().view(np.uint64) == b64).all(), (fmt, seg_len, off)

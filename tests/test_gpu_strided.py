@@ -219,3 +219,47 @@ def test_exact_sum_dim_tuples_and_none(xs, shape, dim):
     tb = torch.from_numpy(b.view(np.int16)).cuda().view(torch.bfloat16)
     r, _ = oracle.exact_sum(b, fmt="bf16")
     assert xs.exact_sum_dim(tb, None).cpu().numpy().reshape(1).view(np.uint32)[0] == r.bits_f32
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+@pytest.mark.parametrize("outer,length,inner", [(2, 5000, 96), (1, 1537, 130), (3, 513, 2), (1, 70_001, 64)])
+def test_strided_h16_two_fibres_per_lane(xs, fmt, outer, length, inner):
+    """K10h (16-bit, even inner, 4-B aligned base: two fibres per lane, packed decode into bins):
+    reductions longer than a bin window (bfloat16: 512 rows), inner sizes that end mid-warp, the
+    split path (with and without the work buffer) - every fibre vs the oracle."""
+    b = patterns(fmt, outer * length * inner, 900 + length + inner)
+    v64, v32, f, wb = check(xs, fmt, b, outer, length, inner, work=True)
+    u64, u32, g, _ = check(xs, fmt, b, outer, length, inner, work=False, sample=range(min(40, outer * inner)))
+    assert (v64[:40] == u64[:40]).all() and (v32[:40] == u32[:40]).all()
+
+
+def test_strided_h16_misaligned_base_falls_back(xs):
+    """A base that is not 4-B aligned takes the one-fibre-per-lane kernel: same bits."""
+    import torch
+    b = patterns("bf16", 1 + 700 * 64, 31)
+    x = dev(b, "bf16")[1:].view(700, 64)
+    assert x.data_ptr() % 4 == 2
+    out = xs.exact_sum_dim(x, 0).cpu().numpy().view(np.uint32)
+    a = b[1:].reshape(700, 64)
+    for i in range(64):
+        r, _ = ref("bf16", np.ascontiguousarray(a[:, i]))
+        assert int(out[i]) == r.bits_f32
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32", "bf16"])
+def test_strided_split_many_fibres(xs, fmt):
+    """Many fibres that still under-fill the GPU: the rows are split into parts and the parts are
+    merged one lane per fibre (k_strided_merge_lanes); every fibre vs the oracle's per-fibre sums."""
+    import torch
+    length, inner = 1536, 40_000
+    b = patterns(fmt, length * inner, 4242)
+    wb = int(xs.lib().xsum_sum_strided_work_bytes(1, length, inner, 0))
+    assert wb > 0                                           # the split path is taken
+    x = dev(b, fmt).view(length, inner)
+    out = xs.exact_sum_dim(x, 0)
+    got = out.cpu().numpy().view(np.uint64 if fmt == "f64" else np.uint32)
+    host_t = np.ascontiguousarray(b.reshape(length, inner).T).reshape(-1)
+    if fmt == "f32":
+        host_t = host_t.view(np.float32)
+    b64, b32, _, _ = oracle.sum_segments(host_t, seg_len=length, fmt=fmt if fmt in ("f16", "bf16") else None)
+    assert (got == (b64 if fmt == "f64" else b32)).all()

@@ -12,6 +12,7 @@ targets (kernel captured):
   merge1024   merge of 1024 state images              (k_merge)
   finalize    finalize_round of a state               (k_finalize)
   c5csr       c5csr CSR segments (bench workload)     (k_segments)
+  str_bf16 / str_f16 / str_f32  [4096, 65536] over dim 0 (k_sum_strided_h16 / _f32)
 """
 from __future__ import annotations
 
@@ -44,6 +45,10 @@ def main(t: str):
             xsum.sum_segments_csr(x, off)
     elif t == "strided_split":
         x = synth.device_generate("c2").view(1 << 20, 256)
+        for _ in range(3):
+            xsum.exact_sum_dim(x, 0)
+    elif t in ("str_bf16", "str_f32", "str_f16"):
+        x = synth.device_bits({"str_bf16": "c2bf16", "str_f32": "c2f32", "str_f16": "c2f16"}[t]).view(4096, 65536)
         for _ in range(3):
             xsum.exact_sum_dim(x, 0)
     elif t == "merge1024":

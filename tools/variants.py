@@ -39,6 +39,8 @@ VARIANTS = {
     "h16q0": ["-DXS_H16Q=0"],
     "hq_lps4": ["-DXS_HQ_LPS=4"],
     "str_nb3": ["-DXS_STR_NB=3"],
+    "strh0": ["-DXS_STRH=0"],
+    "strh_unr8": ["-DXS_STRH_UNR=8"],
     "str_nb6": ["-DXS_STR_NB=6"],
     "str_u4nb8": ["-DXS_STR_UNR=4", "-DXS_STR_NB=8"],
     "exp_seg_noepi": ["-DXS_EXP_SEG_NOEPI"],
@@ -83,8 +85,8 @@ elif {cfg!r}.startswith("str"):
     base = synth.device_generate("c2")
     shp = {{"str64": (4096, 65536), "str1m": (1 << 20, 256), "str3d": (64, 4096, 1024)}}.get({cfg!r}, (4096, 65536))
     x = base.reshape(shp)
-    if {cfg!r} == "strbf16":
-        x = synth.device_bits("c2bf16").reshape(shp)
+    if {cfg!r} in ("strbf16", "strf16", "strf32"):
+        x = synth.device_bits({{"strbf16": "c2bf16", "strf16": "c2f16", "strf32": "c2f32"}}[{cfg!r}]).reshape(shp)
     class _D:
         def sum(self, x):
             global seg_v

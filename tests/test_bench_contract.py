@@ -93,3 +93,19 @@ def test_our_arm_two_ranks_host_path_on_one_gpu():
     d = _json_line(out.stdout)
     assert d["n_gpus"] == 2 and d["config"]["n_total"] == 2 * d["config"]["n_per_gpu"]
     assert d["gpu_launches"] == 6 and d["e2e"]["h2d_bytes_per_step"] == 2 * 8 * d["config"]["n_per_gpu"]
+
+
+def test_bench_faithful_check():
+    """bench.faithful (the c2cs / c3cs line's check): y is RD or RU of the exact A * 2^-1074."""
+    import math
+    sys.path.insert(0, ROOT)
+    import bench
+    one = 1 << 1074                                        # 1.0 in units of 2^-1074
+    ulp = 1 << (1074 - 52)
+    assert bench.faithful(1.0, one)
+    assert bench.faithful(1.0, one + ulp // 3) and bench.faithful(1.0, one + ulp - 1)
+    assert not bench.faithful(1.0, one + ulp)              # S = succ(1.0): only succ is faithful
+    assert bench.faithful(math.nextafter(1.0, 2.0), one + ulp // 3)
+    assert bench.faithful(1.0, one - ulp // 4) and not bench.faithful(1.0, one - ulp // 2)   # gap below is ulp/2
+    assert not bench.faithful(math.inf, one) and not bench.faithful(math.nan, one)
+    assert bench.faithful(-1.0, -one - 1) and not bench.faithful(-1.0, one)

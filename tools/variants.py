@@ -32,6 +32,10 @@ VARIANTS = {
     "lanes0": ["-DXS_SEG_LANES_MAX=0"],
     "seg_whole": ["-DXS_SEG_HALF=0"],
     "sh_q8u4": ["-DXS_SH_LPS=8", "-DXS_SH_U=4"],
+    "sh_u4nb4": ["-DXS_SH_U=4", "-DXS_SH_NB=4"],
+    "sh_u4nb3": ["-DXS_SH_U=4", "-DXS_SH_NB=3"],
+    "sh_u8nb3": ["-DXS_SH_U=8", "-DXS_SH_NB=3"],
+    "sh_u2nb8": ["-DXS_SH_U=2", "-DXS_SH_NB=8"],
     "sl_full": ["-DXS_SL_FULL"],
     "sl_nopf": ["-DXS_SL_PF=0"],
     "sl_notma": ["-DXS_SL_TMA=0"],

@@ -13,7 +13,10 @@
 
 namespace xs {
 
-constexpr int SH_WARPS = 8;
+#ifndef XS_SH_WARPS
+#define XS_SH_WARPS 8
+#endif
+constexpr int SH_WARPS = XS_SH_WARPS;
 #ifndef XS_SH_U
 #define XS_SH_U 8
 #endif

@@ -33,7 +33,7 @@ __device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint
     for (uint64_t tt = t0; tt <= t1; tt += G) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
+            uint4 v = ld_stream(body + tt * TV + (uint64_t)u * T + tid);
             Elem<E>::fix_vec(col, v, flags, one);
         }
     }
@@ -41,7 +41,7 @@ __device__ __noinline__ void rescan_window(int64_t* col, const uint4* body, uint
 
 template <int WARPS, int U, int NB, typename E>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
+k_accumulate(const E* x, uint64_t n, AccParams p) {
     using C = AccCfg<WARPS, U, NB, E>;
     using EL = Elem<E>;
     constexpr int PV = EL::PER_VEC;
@@ -80,7 +80,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
     auto load_tile = [&](uint4 (&buf)[U], uint64_t tt) {
         if (tt < ntiles) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) buf[u] = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
+            for (int u = 0; u < U; ++u) buf[u] = ld_stream(body + tt * TV + (uint64_t)u * T + tid);
         }
     };
     // NB register buffers of U vectors rotate without moves (the unrolled b loop indexes them
@@ -131,7 +131,7 @@ k_accumulate(const E* __restrict__ x, uint64_t n, AccParams p) {
         for (int u = 0; u < U; ++u) {
             uint64_t v = v0 + (uint64_t)u * T + tid;
             if (v < nvec) {
-                EL::add_vec_checked(col, ldg_stream(body + v), flags, one);
+                EL::add_vec_checked(col, ld_stream(body + v), flags, one);
                 touched = true;
             }
         }

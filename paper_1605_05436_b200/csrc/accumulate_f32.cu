@@ -115,7 +115,7 @@ __device__ __noinline__ void f32b_rescan(uint64_t* bins, int64_t* col, const uin
     uint32_t dummy = 0;
     for (uint64_t tt = t0; tt <= t1; tt += G) {
         for (int u = 0; u < F32B_U; ++u) {
-            uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * (F32B_WARPS * 32) + tid);
+            uint4 v = ld_stream(body + tt * TV + (uint64_t)u * (F32B_WARPS * 32) + tid);
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
             for (int i = 0; i < 4; ++i) {
                 const uint32_t f = f32b_special_flags(w[i]);
@@ -137,7 +137,7 @@ __device__ __forceinline__ void f32b_add_checked(uint64_t* bins, uint32_t b, uin
 }
 
 __global__ void __launch_bounds__(F32B_WARPS * 32, 1)
-k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
+k_accumulate_f32b(const float* x, uint64_t n, AccParams p) {
     constexpr int T = F32B_WARPS * 32;
     constexpr int PV = 4;
     constexpr int FLUSH_TILES = F32B_FLUSH / (PV * F32B_U);           // 31 tiles
@@ -178,7 +178,7 @@ k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
     auto load_tile = [&](uint4 (&buf)[F32B_U], uint64_t tt) {
         if (tt < ntiles) {
 #pragma unroll
-            for (int u = 0; u < F32B_U; ++u) buf[u] = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
+            for (int u = 0; u < F32B_U; ++u) buf[u] = ld_stream(body + tt * TV + (uint64_t)u * T + tid);
         }
     };
     uint4 buf[F32B_NB][F32B_U];
@@ -229,7 +229,7 @@ k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
         for (int u = 0; u < F32B_U; ++u) {
             const uint64_t v = v0 + (uint64_t)u * T + tid;
             if (v < nvec) {
-                const uint4 q = ldg_stream(body + v);
+                const uint4 q = ld_stream(body + v);
                 f32b_add_checked(bins, q.x, flags, one);
                 f32b_add_checked(bins, q.y, flags, one);
                 f32b_add_checked(bins, q.z, flags, one);
@@ -237,9 +237,9 @@ k_accumulate_f32b(const float* __restrict__ x, uint64_t n, AccParams p) {
             }
         }
         const uint64_t tail = nbody - nvec * PV;
-        if ((uint64_t)tid < head) f32b_add_checked(bins, __float_as_uint(__ldg(x + tid)), flags, one);
+        if ((uint64_t)tid < head) f32b_add_checked(bins, __float_as_uint(ld_coherent(x + tid)), flags, one);
         if (tid >= 4 && (uint64_t)(tid - 4) < tail)
-            f32b_add_checked(bins, __float_as_uint(__ldg(x + head + nvec * PV + (tid - 4))), flags, one);
+            f32b_add_checked(bins, __float_as_uint(ld_coherent(x + head + nvec * PV + (tid - 4))), flags, one);
         f32b_flush(bins, col);
     }
     __syncwarp();

@@ -37,7 +37,7 @@ __device__ __noinline__ void h16_rescan(const uint4* body, uint64_t t0, uint64_t
     // the special group, which is never summed)
     for (uint64_t tt = t0; tt <= t1; tt += G) {
         for (int u = 0; u < H16_U; ++u) {
-            uint4 v = ldg_stream(body + tt * TV + (uint64_t)u * (H16_WARPS * 32) + tid);
+            uint4 v = ld_stream(body + tt * TV + (uint64_t)u * (H16_WARPS * 32) + tid);
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
             for (int i = 0; i < 4; ++i) flags |= h16_special_flags<F>(w[i] & 0xFFFFu) | h16_special_flags<F>(w[i] >> 16);
         }
@@ -54,7 +54,7 @@ __device__ __forceinline__ void h16_add_checked(uint32_t* bins, uint32_t b16, ui
 
 template <class F>
 __global__ void __launch_bounds__(H16_WARPS * 32, 1)
-k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
+k_accumulate_h16(const uint16_t* x, uint64_t n, AccParams p) {
     using C = H16Col<F>;
     constexpr int T = H16_WARPS * 32;
     constexpr int PV = 8;                                   // summands per 16-B vector
@@ -102,7 +102,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
     auto load_tile = [&](uint4 (&buf)[H16_U], uint64_t tt) {
         if (tt < ntiles) {
 #pragma unroll
-            for (int u = 0; u < H16_U; ++u) buf[u] = ldg_stream(body + tt * TV + (uint64_t)u * T + tid);
+            for (int u = 0; u < H16_U; ++u) buf[u] = ld_stream(body + tt * TV + (uint64_t)u * T + tid);
         }
     };
     uint4 buf[H16_NB][H16_U];
@@ -146,7 +146,7 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
         for (int u = 0; u < H16_U; ++u) {
             uint64_t v = v0 + (uint64_t)u * T + tid;
             if (v < nvec) {
-                uint4 q = ldg_stream(body + v);
+                uint4 q = ld_stream(body + v);
                 const uint32_t w[4] = {q.x, q.y, q.z, q.w};
                 for (int i = 0; i < 4; ++i) {
                     h16_add_checked<F>(bins, w[i] & 0xFFFFu, flags);
@@ -155,8 +155,8 @@ k_accumulate_h16(const uint16_t* __restrict__ x, uint64_t n, AccParams p) {
             }
         }
         const uint64_t tail = nbody - nvec * PV;
-        if ((uint64_t)tid < head) h16_add_checked<F>(bins, __ldg(x + tid), flags);
-        if (tid >= 8 && (uint64_t)(tid - 8) < tail) h16_add_checked<F>(bins, __ldg(x + head + nvec * PV + (tid - 8)), flags);
+        if ((uint64_t)tid < head) h16_add_checked<F>(bins, ld_coherent(x + tid), flags);
+        if (tid >= 8 && (uint64_t)(tid - 8) < tail) h16_add_checked<F>(bins, ld_coherent(x + head + nvec * PV + (tid - 8)), flags);
     }
     h16_flush_col<F>(bins, col);
     __syncwarp();

@@ -190,7 +190,7 @@ template <> struct Elem<double> {
     __device__ static __forceinline__ void add_one_checked(int64_t* col, const double* p, uint32_t& flags,
                                                            uint32_t one) {
         uint2 q;
-        asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(q.x), "=r"(q.y) : "l"(p));
+        asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(q.x), "=r"(q.y) : "l"(p));   // coherent: see ld_stream
         column_add_checked(col, q.x, q.y, flags, one);
     }
 };
@@ -501,6 +501,28 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+// The same load without .nc, for kernels launched with programmatic dependent launch (the
+// accumulate kernels K2/K2f/K2h): .nc declares the data read-only for the kernel's lifetime, and
+// ptxas does schedule ld.global.nc above griddepcontrol.wait (the SASS of k_accumulate_f32b had its
+// first LDG.CONSTANT tiles ahead of ACQBULK, and tests/test_gpu_api_r02.py's early-triggering
+// producer caught the stale reads). With PDL the input may still be being written before the wait.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_coherent(const float* p) {
+    float v;
+    asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint16_t ld_coherent(const uint16_t* p) {
+    uint16_t v;
+    asm volatile("ld.global.u16 %0, [%1];" : "=h"(v) : "l"(p));
     return v;
 }
 

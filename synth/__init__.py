@@ -73,6 +73,8 @@ def cuda_lib():
         lib.synth_gpu_cancel_unpermuted.argtypes = [p, u64, u64, u64, u64, i32, i32, i32, i32, p]
         lib.synth_gpu_keys_signed.argtypes = [p, u64, u64, u64, u64, p]
         lib.synth_probe_read.argtypes = [p, u64, p, i32, i32, i32, p]
+        lib.synth_gpu_fill_after_trigger.argtypes = [p, u64, ctypes.c_double, ctypes.c_longlong, p]
+        lib.synth_gpu_fill_after_trigger.restype = ctypes.c_int
         lib.synth_probe_read.restype = ctypes.c_int
         for f in (lib.synth_gpu_uniform, lib.synth_gpu_cancel_unpermuted, lib.synth_gpu_keys_signed):
             f.restype = ctypes.c_int

@@ -56,6 +56,19 @@ __global__ void k_keys_signed(int64_t* __restrict__ out, uint64_t start, uint64_
         out[t] = (int64_t)(s_mix64(key + SYNTH_G * (start + t + 1)) ^ 0x8000000000000000ull);
 }
 
+// Test helper (tests/test_gpu_api_r02.py): a producer that releases its programmatic dependents at
+// entry (griddepcontrol.launch_dependents), waits ~spin cycles, then fills x[0..n) with v - like a
+// GEMM that triggers its dependents before its epilogue stores. A PDL-launched consumer that read
+// its input before griddepcontrol.wait would see the old contents.
+__global__ void k_fill_after_trigger(double* x, uint64_t n, double v, long long spin) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    const long long t0 = clock64();
+    while (clock64() - t0 < spin) {
+    }
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) x[t] = v;
+}
+
 static unsigned grid_for(uint64_t count) {
     uint64_t b = (count + 255) / 256;
     return (unsigned)(b < 148ull * 64 ? (b ? b : 1) : 148ull * 64);
@@ -84,6 +97,14 @@ int synth_gpu_keys_signed(void* out, uint64_t start, uint64_t count, uint64_t se
     if (!count) return 0;
     k_keys_signed<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>((int64_t*)out, start, count,
                                                                        h_key(seed, st));
+    return (int)cudaGetLastError();
+}
+
+int synth_gpu_fill_after_trigger(void* x, uint64_t n, double v, long long spin, void* stream) {
+    if (!n) return 0;
+    // a few small blocks: the producer must leave the other SMs free, or the consumer's blocks
+    // could not become resident before it exits and the race would be hidden
+    k_fill_after_trigger<<<4, 256, 0, (cudaStream_t)stream>>>((double*)x, n, v, spin);
     return (int)cudaGetLastError();
 }
 

@@ -201,3 +201,29 @@ def test_one_shot_cache_bounded(xs):
         with torch.cuda.stream(s):
             assert xs.fsum(x) == want
     assert len(xs._default_acc) <= xs._DEFAULT_ACC_MAX
+
+
+def test_pdl_consumer_waits_for_an_early_triggering_producer(xs):
+    """a producer that releases its programmatic dependents BEFORE writing the
+    input (synth's k_fill_after_trigger: 4 blocks, launch_dependents, ~100 us spin, then the stores)
+    directly followed by PDL-launched accumulate kernels on the same stream: every sum must be of
+    the written values (the consumers wait for the producer before their first input load).
+    Narrow formats: the producer stores 64-bit words holding 2 (f32) / 4 (f16, bf16) copies of v."""
+    import torch
+    lib = synth.cuda_lib()
+    st = torch.cuda.current_stream().cuda_stream
+    for n, dt in ((1 << 20, torch.float64), (1 << 19, torch.float32), (1 << 21, torch.float16),
+                  (1 << 21, torch.bfloat16), ((1 << 22) + 8, torch.float64)):
+        y = torch.zeros(n, dtype=dt, device="cuda")
+        words = y.view(torch.float64)
+        per = 8 // y.element_size()
+        acc = xs.Accumulator()
+        for k in range(5):
+            v = float(k + 1)
+            word = float(torch.full((per,), v, dtype=dt).view(torch.float64).item())
+            y.zero_()
+            torch.cuda.synchronize()
+            assert lib.synth_gpu_fill_after_trigger(words.data_ptr(), words.numel(), word, 200000, st) == 0
+            res, _ = acc.sum(y)                      # launched right behind the producer
+            got = xs.Result.from_bytes(res.cpu().numpy().tobytes()).value
+            assert got == v * n, (n, dt, k, got)

@@ -48,6 +48,27 @@ def test_library_exports_every_header_symbol(built):
     assert {s for s in exported if s.startswith("xsum_")} == set(header_functions())
 
 
+def test_pdl_kernels_load_no_input_before_griddepcontrol_wait(built):
+    """Every kernel that waits on its programmatic predecessor (griddepcontrol.wait = SASS ACQBULK)
+    issues no global load ahead of the first wait in its SASS and uses no non-coherent
+    (LDG.CONSTANT) loads: ptxas schedules ld.global.nc above the wait (ADVICE r01 PDL finding;
+    the GPU counterpart is test_pdl_consumer_waits_for_an_early_triggering_producer)."""
+    sass = subprocess.run(["cuobjdump", "-sass", xsum.SO_PATH], capture_output=True, text=True).stdout
+    if not sass:
+        pytest.skip("cuobjdump unavailable")
+    funcs = re.split(r"\n\s*Function : ", sass)[1:]
+    waiting = 0
+    for f in funcs:
+        name, body = f.split("\n", 1)
+        if "ACQBULK" not in body:
+            continue
+        waiting += 1
+        before = body.split("ACQBULK", 1)[0]
+        assert not re.search(r"\bLDG", before), f"{name}: global load before griddepcontrol.wait"
+        assert not re.search(r"LDG[^;]*CONSTANT", body), f"{name}: non-coherent input load"
+    assert waiting >= 4            # K2, K2f, K2h (binary16, bfloat16)
+
+
 def test_library_sizes_match_header(built):
     L = built
     assert L.xsum_state_bytes() == xsum.STATE_BYTES == 384

@@ -591,7 +591,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         passes = inf.iterations
         cs_line = {"r": inf.r, "iterations": inf.iterations, "exact": inf.exact, "e_cut": inf.e_cut,
                    "root_entries": len(inf.root), "rule": inf.rule}
-    achieved = esz * n_local * passes / (kern_ms / 1e3) / 1e9
+    alg_bytes = esz * n_local * passes                      # algorithmic bytes per launch
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     # context for the roofline: a pure streaming read of the same input in the same run (the
     # best read-only probe configuration of profiles/r01_microbench.txt: 296 blocks x 512 threads,
     # 8 x 16-B loads in flight per thread), untimed by the step
@@ -645,10 +646,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle                      # the cpu_baseline leg (test infrastructure)
-        rate, cores, m, passes, dt, gen_name, ref = oracle_rate(args.config)
+        rate, cores, m, o_passes, dt, gen_name, ref = oracle_rate(args.config)
         what = "every segment of" if seg else "elements [0, %d) of" % m
         cpu = {"value": rate, "unit": unit, "cores": cores, "kind": "oracle",
-               "sample": f"{what} {gen_name} ({m} elements) summed {passes}x by the oracle in {dt:.2f} s "
+               "sample": f"{what} {gen_name} ({m} elements) summed {o_passes}x by the oracle in {dt:.2f} s "
                          f"on {cores} host threads = {dt * cores:.1f} CPU-s ({cpu_model()})"}
         if seg:
             # the oracle's per-segment roundings vs the GPU's outputs of the same step, all of them
@@ -703,7 +704,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                     "c5csr": "k_segments", "c5s16": "k_segments_lanes64s",
                                     "c2dim0": "k_sum_strided", "c2cs": "xsum_sum_condsens step (all passes)",
                                     "c3cs": "xsum_sum_condsens step (all passes)"}.get(args.config, "k_accumulate"),
-                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": esz * n_local * passes,
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peak_src, "read_probe_gbs": probe_gbs,
                          "frac_of_read_probe": (achieved / probe_gbs) if probe_gbs else None,
                          "sustained_frac": sustained["frac"] if sustained else None,

@@ -75,6 +75,9 @@ def test_our_arm_one_gpu_contract():
     assert d["gpu_launches"] == 5                       # one fused launch per step
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    # achieved = algorithmic bytes per launch (8 per summand) / the kernel's average duration
+    assert r["algorithmic_bytes_per_launch"] == 8 * d["config"]["n_per_gpu"]
+    assert abs(r["achieved"] - r["algorithmic_bytes_per_launch"] / (r["kernel_ms"] * 1e6)) < 1e-6 * r["achieved"]
     assert d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["n_per_gpu"] and d["e2e"]["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["clocks"]["sm_max_mhz"]
     assert len(d["result"]["value_hex"]) == 16 and len(d["result"]["image_sha256"]) == 64

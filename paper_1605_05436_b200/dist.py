@@ -80,8 +80,19 @@ class PeerExchange:
         self.world = dist.get_world_size(self.group)
         self.rank = dist.get_rank(self.group)
         nbytes = peer_buffer_bytes(self.world)
-        self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
-        self.buf.zero_()
+        # a rank that cannot allocate its buffer must not leave the others blocked in the
+        # (collective) rendezvous: agree first, then every rank raises or every rank proceeds
+        ok = torch.ones(1, dtype=torch.int32, device=device)
+        err = None
+        try:
+            self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+            self.buf.zero_()
+        except Exception as e:  # noqa: BLE001
+            err = e
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if not int(ok.item()):
+            raise RuntimeError(f"symmetric peer buffers unavailable on some rank (this rank: {err!r})")
         torch.cuda.synchronize(device)
         self.handle = symm_mem.rendezvous(self.buf, self.group.group_name)
         self.bufs_dev = int(self.handle.buffer_ptrs_dev)

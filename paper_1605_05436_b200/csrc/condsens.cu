@@ -206,9 +206,18 @@ __device__ __forceinline__ void ssa_shfl_down(SSA<RC>& o, const SSA<RC>& a, int 
     }
 }
 
+#ifndef XS_CS2_G
+#define XS_CS2_G 6
+#endif
+#ifndef XS_CS4_G
+#define XS_CS4_G 4
+#endif
+#ifndef XS_CS4_MINB
+#define XS_CS4_MINB 2
+#endif
 template <int RC> struct Shape;
-template <> struct Shape<2> { static constexpr int G = 4, T = 256, MINB = 2; };
-template <> struct Shape<4> { static constexpr int G = 3, T = 256, MINB = 1; };
+template <> struct Shape<2> { static constexpr int G = XS_CS2_G, T = 256, MINB = 2; };
+template <> struct Shape<4> { static constexpr int G = XS_CS4_G, T = 256, MINB = XS_CS4_MINB; };
 // r = 16: a sorted 16-entry list per thread does not fit in registers (spills, ~0.9 us per
 // node); that iteration keeps the superaccumulator dense across a warp instead (k_cs_tree_w16)
 constexpr int W16_WARPS = 8, W16_LOG = 10;      // 2^10 consecutive leaves per warp chunk

@@ -108,7 +108,8 @@ def _families(rng, n):
     yield "cancel", c[:n] if len(c) >= n else c
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 257, 4095, 4096, 4097, 9000])
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 257, 1023, 1025, 4095, 4096, 4097, 9000,
+                               16383, 16384, 16385])
 def test_condsens_matches_oracle_sizes(xs, n):
     rng = random.Random(1000 + n)
     for kind, vals in _families(rng, n):
@@ -117,8 +118,8 @@ def test_condsens_matches_oracle_sizes(xs, n):
 
 @pytest.mark.parametrize("rule", [1, 2])
 def test_condsens_multi_pass(xs, rule):
-    """Sizes past one chunk of every r (r = 2: 4096 leaves, r = 4: 2048, r = 16: 256) and past
-    two passes of r = 16 (65536 leaves), misaligned base."""
+    """Sizes past one chunk of every r (r = 2: 16384 leaves, r = 4: 4096, r = 16: 1024 per warp)
+    and so through a second pass of every r, misaligned base."""
     rng = random.Random(7 + rule)
     for kind, vals in _families(rng, 70_001):
         if kind in ("wide", "cancel"):

@@ -37,6 +37,13 @@ VARIANTS = {
     "sh_u8nb3": ["-DXS_SH_U=8", "-DXS_SH_NB=3"],
     "sh_u2nb8": ["-DXS_SH_U=2", "-DXS_SH_NB=8"],
     "sl_full": ["-DXS_SL_FULL"],
+    "cs2g5": ["-DXS_CS2_G=5"],
+    "cs4g4": ["-DXS_CS4_G=4"],
+    "cs4g4m2": ["-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],
+    "cs4g5": ["-DXS_CS4_G=5"],
+    "cs2g5_4g4m2": ["-DXS_CS2_G=5", "-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],
+    "cs2g6_4g4m2": ["-DXS_CS2_G=6", "-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],
+    "cs2g5_4g5m2": ["-DXS_CS2_G=5", "-DXS_CS4_G=5", "-DXS_CS4_MINB=2"],
     "sl_nopf": ["-DXS_SL_PF=0"],
     "sl_notma": ["-DXS_SL_TMA=0"],
     "sls_nbuf2": ["-DXS_SLS_NBUF=2"],
@@ -97,6 +104,12 @@ elif {cfg!r}.startswith("str"):
             seg_v = xsum.exact_sum_dim(x, 1 if x.dim() == 3 else 0)
             return xsum_res, None
     xsum_res = xsum.Accumulator().sum(base[:1024])[0]
+elif {cfg!r} in ("cs2", "cs3"):
+    x = synth.device_generate("c2" if {cfg!r} == "cs2" else "c3")
+    class _K:
+        def sum(self, x):
+            r, _, _ = xsum.sum_condsens(x, 1)
+            return r, None
 elif {cfg!r} == "c5csr":
     x = synth.device_generate("c5csr")
     csr = synth.csr_offsets("c5csr", device="cuda")
@@ -104,7 +117,7 @@ elif {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
     pass
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
-acc = _D() if {cfg!r}.startswith("str") else xsum.Accumulator()
+acc = _D() if {cfg!r}.startswith("str") else _K() if {cfg!r} in ("cs2", "cs3") else xsum.Accumulator()
 if {cfg!r} == "c5csr":
     class _C:
         def sum(self, x):

@@ -333,8 +333,10 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
 // 578-628; identical to the sparse sum: an absent index is a zero digit, which only a carry
 // makes non-zero) followed by keeping the 16 most significant non-zero digits (two ballots). Each
 // warp walks its chunk of 2^W16_LOG leaves in order with a binary counter whose pending subtree
-// roots live in shared memory; one node costs ~30 warp instructions instead of a 16-entry sorted
-// merge per thread.
+// roots live in shared memory; a merge costs ~60 warp instructions (lemma1_add ~35, the truncation
+// test, the stack) instead of a 16-entry sorted merge per thread. The leaves of a 32-leaf step are
+// decomposed once, lane j taking leaf j, and broadcast by shuffles (ncu: every lane decoding every
+// leaf was ~60 of ~150 warp instructions per leaf; c3 step 63.6 -> 50.0 ms).
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ void trunc_dense(int64_t& a0, int64_t& a1, int r, int& cut, int lane) {
     const uint32_t lo = __ballot_sync(FULL, a0 != 0);
@@ -350,9 +352,11 @@ __device__ __forceinline__ void trunc_dense(int64_t& a0, int64_t& a1, int r, int
     }
 }
 
-// dense digits of one leaf x (bit pattern b, the same value in every lane)
-__device__ __forceinline__ void dense_leaf(uint64_t b, int64_t& a0, int64_t& a1, uint32_t& flags, int lane) {
-    a0 = a1 = 0;
+// the two entries of one leaf x (bit pattern b): +-lo at digit i, +-hi at i+1;
+// i = -1 for NaN / Inf (flagged, summed as zero)
+__device__ __forceinline__ void leaf_parts(uint64_t b, int& i, int64_t& slo, int64_t& shi, uint32_t& flags) {
+    i = -1;
+    slo = shi = 0;
     const uint32_t e = (uint32_t)(b >> 52) & 0x7FF;
     const uint64_t m = b & MASK;
     if (e == 0x7FF) {
@@ -361,11 +365,20 @@ __device__ __forceinline__ void dense_leaf(uint64_t b, int64_t& a0, int64_t& a1,
     }
     const uint64_t M = m | ((uint64_t)(e != 0) << 52);
     const uint32_t k = (e ? e : 1) - 1;
-    const int i = (int)(k / 52), o = (int)(k % 52);
+    i = (int)(k / 52);
+    const int o = (int)(k % 52);
     const uint64_t lo = (M << o) & MASK;
     const uint64_t hi = o ? (M >> (52 - o)) : (M >> 52);
     const bool neg = b >> 63;
-    const int64_t slo = neg ? -(int64_t)lo : (int64_t)lo, shi = neg ? -(int64_t)hi : (int64_t)hi;
+    slo = neg ? -(int64_t)lo : (int64_t)lo;
+    shi = neg ? -(int64_t)hi : (int64_t)hi;
+}
+
+// dense digits of leaf j of the warp's 32 (lane j decomposed it: li / llo / lhi), in every lane
+__device__ __forceinline__ void dense_leaf_from(int li, int64_t llo, int64_t lhi, int j, int64_t& a0, int64_t& a1,
+                                                int lane) {
+    const int i = __shfl_sync(FULL, li, j);
+    const int64_t slo = __shfl_sync(FULL, llo, j), shi = __shfl_sync(FULL, lhi, j);
     a0 = lane == i ? slo : (lane == i + 1 ? shi : 0);
     a1 = lane + 32 == i ? slo : (lane + 32 == i + 1 ? shi : 0);
 }
@@ -418,16 +431,19 @@ k_cs_tree_w16(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict_
         const int nleft = (int)min((uint64_t)NLW, nleaf - first);
         int64_t a0 = 0, a1 = 0;                          // the chunk root
         for (int base = 0; base < nleft; base += 32) {
-            uint64_t xb = 0;
+            // lane j decomposes leaf base + j once (instead of every lane redoing each leaf)
+            int li = -1;
+            int64_t llo = 0, lhi = 0;
             if constexpr (DOUBLES) {
-                if (base + lane < nleft) xb = static_cast<const uint64_t*>(src)[first + base + lane];
+                if (base + lane < nleft)
+                    leaf_parts(static_cast<const uint64_t*>(src)[first + base + lane], li, llo, lhi, flags);
             }
             const int cnt = min(32, nleft - base);
             for (int j = 0; j < cnt; ++j) {
                 const int p = base + j;
                 int64_t c0, c1;
                 if constexpr (DOUBLES)
-                    dense_leaf(__shfl_sync(FULL, xb, j), c0, c1, flags, lane);
+                    dense_leaf_from(li, llo, lhi, j, c0, c1, lane);
                 else
                     dense_from_records(static_cast<const int64_t*>(src) + (first + p) * R16, c0, c1, lane);
                 // binary counter (reading C2): sum with the left siblings while bit L of p is set

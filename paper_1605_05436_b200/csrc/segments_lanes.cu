@@ -443,7 +443,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 
 __global__ void __launch_bounds__(SLS_WARPS * 32, 1)
 k_segments_lanes64s(const double* __restrict__ x, uint64_t nseg, uint32_t len, SegOut o, uint32_t one, uint32_t mone) {
-    extern __shared__ __align__(128) int64_t win[];
+    extern __shared__ __align__(16) int64_t win[];   // bulk copies need 16-B aligned destinations
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t* col = win + warp * (D * 32) + lane;
     uint8_t* stage = reinterpret_cast<uint8_t*>(win + SLS_WARPS * D * 32) + (size_t)warp * SLS_NBUF * SLS_STAGE;

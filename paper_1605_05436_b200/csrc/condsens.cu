@@ -92,8 +92,14 @@ __device__ __forceinline__ void ce_desc(int& ka, int64_t& va, int& kb, int64_t& 
 
 // The r-truncated Lemma-1 sum of two sparse superaccumulators (PAPER.md:703-711, :559-628,
 // :721-725). cut := max(cut, index of the least significant kept entry) if entries were dropped.
+// r >= XS_CS_SLOTS: the selection of the RC most significant entries scatters the candidates by
+// rank into per-thread shared-memory slots instead of an RC x 2U select network (r = 4: c2 step
+// 16.38 -> 15.29 ms; r = 2 is faster with the selects; profiles/r02_condsens.txt)
+#ifndef XS_CS_SLOTS
+#define XS_CS_SLOTS 4
+#endif
 template <int RC>
-__device__ __forceinline__ void ssa_merge(SSA<RC>& a, const SSA<RC>& b, int& cut) {
+__device__ __forceinline__ void ssa_merge(SSA<RC>& a, const SSA<RC>& b, int& cut, int64_t* slot, int sstride) {
     constexpr int U = 2 * RC;
     int k[U];
     int64_t p[U];
@@ -155,6 +161,25 @@ __device__ __forceinline__ void ssa_merge(SSA<RC>& a, const SSA<RC>& b, int& cut
     // keep the RC most significant non-zero entries
     int cnt = 0;
     static_assert(RC <= 4, "r = 16 uses the warp-dense kernel");
+#if XS_CS_SLOTS
+    if (slot) {            // scatter the first RC by rank into this thread's shared slots
+        uint32_t nzm = 0;
+#pragma unroll
+        for (int t = 0; t < 2 * U; ++t) nzm |= (uint32_t)(ck[t] >= 0) << t;
+        cnt = __popc(nzm);
+#pragma unroll
+        for (int t = 0; t < 2 * U; ++t) {
+            const int rank = __popc(nzm & ((1u << t) - 1));
+            if (ck[t] >= 0 && rank < RC) slot[rank * sstride] = (int64_t)(((uint64_t)cv[t] << 6) | (uint64_t)ck[t]);
+        }
+#pragma unroll
+        for (int q = 0; q < RC; ++q) {
+            const int64_t r = q < cnt ? slot[q * sstride] : 0;
+            a.k[q] = r ? (int)(r & 63) : -1;
+            a.v[q] = r >> 6;
+        }
+    } else
+#endif
     {
         ssa_clear(a);
 #pragma unroll
@@ -178,8 +203,9 @@ __device__ __forceinline__ void ssa_merge(SSA<RC>& a, const SSA<RC>& b, int& cut
 // measured no faster (r = 2: 5.73 vs 5.54 ms, r = 4: 13.9 vs 14.0 ms for 2^28 leaves;
 // profiles/r02_condsens.txt).
 template <int RC>
-__device__ __forceinline__ void merge_into(SSA<RC>& a, const SSA<RC>& b, int& cut) {
-    ssa_merge(a, b, cut);
+__device__ __forceinline__ void merge_into(SSA<RC>& a, const SSA<RC>& b, int& cut, int64_t* slot = nullptr,
+                                           int sstride = 0) {
+    ssa_merge(a, b, cut, slot, sstride);
 }
 
 // records: (digit << 6) | index, 0 = unused slot (the sparse image record format, include/xsum.h)
@@ -235,8 +261,16 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
     constexpr int B = chunk_log2<RC>();
     __shared__ int64_t wroot[WARPS][RC];
     __shared__ int wpres[WARPS];
+#if XS_CS_SLOTS
+    __shared__ int64_t cslot[RC * T];                 // per-thread compaction slots, stride T
+#endif
     if (*(volatile uint32_t*)&ctl->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if XS_CS_SLOTS
+    int64_t* const slot = (RC >= XS_CS_SLOTS) ? cslot + tid : nullptr;
+#else
+    int64_t* const slot = nullptr;
+#endif
     int cut = -1;
     uint32_t flags = 0;
     for (uint64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
@@ -262,7 +296,7 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
                 for (int L = 0; L < G; ++L) {
                     if (carry) {
                         if ((p >> L) & 1) {
-                            merge_into(cur, stack[L], cut);
+                            merge_into(cur, stack[L], cut, slot, T);
                         } else {
                             stack[L] = cur;
                             carry = false;
@@ -276,7 +310,7 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
 #pragma unroll
                 for (int L = 0; L < G; ++L) {
                     if ((nleft >> L) & 1) {
-                        if (have) merge_into(a, stack[L], cut);
+                        if (have) merge_into(a, stack[L], cut, slot, T);
                         else a = stack[L];
                         have = true;
                     }
@@ -290,7 +324,7 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
             SSA<RC> b;
             ssa_shfl_down(b, a, d);
             const bool bpres = __shfl_down_sync(FULL, pres, d);
-            if ((lane & (2 * d - 1)) == 0 && bpres) merge_into(a, b, cut);
+            if ((lane & (2 * d - 1)) == 0 && bpres) merge_into(a, b, cut, slot, T);
         }
         if (lane == 0) {
             ssa_store(a, wroot[warp]);
@@ -311,7 +345,7 @@ k_cs_tree(const void* __restrict__ src, uint64_t nleaf, int64_t* __restrict__ re
                 SSA<RC> b;
                 ssa_shfl_down(b, w, d);
                 const bool bpres = __shfl_down_sync(FULL, wp, d);
-                if ((lane & (2 * d - 1)) == 0 && bpres) merge_into(w, b, cut);
+                if ((lane & (2 * d - 1)) == 0 && bpres) merge_into(w, b, cut, slot, T);
             }
             if (lane == 0) ssa_store(w, recs_out + chunk * RC);
         }

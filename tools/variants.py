@@ -41,6 +41,8 @@ VARIANTS = {
     "cs4g4": ["-DXS_CS4_G=4"],
     "cs4g4m2": ["-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],
     "cs4g5": ["-DXS_CS4_G=5"],
+    "csslots4": ["-DXS_CS_SLOTS=4"],
+    "csslots2": ["-DXS_CS_SLOTS=2"],
     "cs2g5_4g4m2": ["-DXS_CS2_G=5", "-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],
     "cs2g6_4g4m2": ["-DXS_CS2_G=6", "-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],
     "cs2g5_4g5m2": ["-DXS_CS2_G=5", "-DXS_CS4_G=5", "-DXS_CS4_MINB=2"],

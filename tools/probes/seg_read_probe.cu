@@ -48,6 +48,27 @@ __global__ void __launch_bounds__(256, 2) k_seg(const uint4* x, uint64_t nseg, u
     if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// LPS lanes per segment (16: K6h's half warps, 8: quarters), 32/LPS segments per warp at a time
+template <int DEPTH, int LPS>
+__global__ void __launch_bounds__(256, 2) k_seg_part(const uint4* x, uint64_t nseg, uint64_t seg_vecs, unsigned* sink) {
+    const int lane = threadIdx.x & 31, sl = lane % LPS, grp = lane / LPS;
+    constexpr int G = 32 / LPS;
+    const uint64_t nw = (uint64_t)gridDim.x * 8, gw = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    unsigned acc = 0;
+    for (uint64_t s0 = gw * G; s0 < nseg; s0 += nw * G) {
+        const uint64_t s = s0 + grp < nseg ? s0 + grp : s0;
+        const uint4* p = x + s * seg_vecs + sl;
+        for (uint64_t j = 0; j < seg_vecs; j += LPS * DEPTH) {
+            uint4 v[DEPTH];
+#pragma unroll
+            for (int d = 0; d < DEPTH; ++d) v[d] = ld(p + j + d * LPS);
+#pragma unroll
+            for (int d = 0; d < DEPTH; ++d) acc ^= v[d].x ^ v[d].y ^ v[d].z ^ v[d].w;
+        }
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b;
@@ -78,6 +99,14 @@ int main() {
         rep(buf, timeit([&] { k_seg<4><<<g, 256>>>(x, nseg, sv, sink); }));
         snprintf(buf, 64, "warp/segment L=%llu depth 8", (unsigned long long)L);
         rep(buf, timeit([&] { k_seg<8><<<g, 256>>>(x, nseg, sv, sink); }));
+        unsigned g2 = (unsigned)((nseg + 15) / 16 < (uint64_t)2 * sms ? (nseg + 15) / 16 : 2 * sms);
+        snprintf(buf, 64, "half-warp/segment L=%llu depth 8", (unsigned long long)L);
+        rep(buf, timeit([&] { k_seg_part<8, 16><<<g2, 256>>>(x, nseg, sv, sink); }));
+        snprintf(buf, 64, "half-warp/segment L=%llu depth 16", (unsigned long long)L);
+        rep(buf, timeit([&] { k_seg_part<16, 16><<<g2, 256>>>(x, nseg, sv, sink); }));
+        unsigned g4 = (unsigned)((nseg + 31) / 32 < (uint64_t)2 * sms ? (nseg + 31) / 32 : 2 * sms);
+        snprintf(buf, 64, "quarter-warp/segment L=%llu depth 16", (unsigned long long)L);
+        rep(buf, timeit([&] { k_seg_part<16, 8><<<g4, 256>>>(x, nseg, sv, sink); }));
         if (L >= 4096) {
             snprintf(buf, 64, "warp/segment L=%llu depth 16", (unsigned long long)L);
             rep(buf, timeit([&] { k_seg<16><<<g, 256>>>(x, nseg, sv, sink); }));

@@ -513,6 +513,9 @@ def sum_condsens(x, rule: int = 1, canon: bool = False, work=None, res=None, inf
     nb = condsens_work_bytes(x.numel())
     if work is None or work.numel() < nb:
         work = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    elif not (work.is_cuda and work.dtype == torch.uint8 and work.is_contiguous() and work.device == x.device
+              and work.data_ptr() % 256 == 0):
+        raise TypeError("work must be a contiguous, 256-B aligned uint8 CUDA tensor on x's device")
     if res is None:
         res = torch.empty(RESULT_BYTES, dtype=torch.uint8, device=x.device)
     if info is None:

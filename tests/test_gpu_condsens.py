@@ -191,3 +191,20 @@ def test_condsens_full_config_faithful(xs, cfg):
     else:
         assert info.iterations >= 2
 
+
+
+def test_condsens_buffer_checks(xs):
+    """Caller-provided buffers: a work buffer that is not a 256-B aligned uint8 CUDA tensor is
+    refused before the call; a reused buffer gives the same result as a fresh one."""
+    import torch
+    d = to_dev([1.0, 2.0 ** -60, -3.5] * 1000)
+    nb = xs.condsens_work_bytes(d.numel())
+    for bad in (torch.empty(nb, dtype=torch.float32, device="cuda"),
+                torch.empty(nb + 1, dtype=torch.uint8, device="cuda")[1:],
+                torch.empty(nb, dtype=torch.uint8)):
+        with pytest.raises(TypeError):
+            xs.sum_condsens(d, 1, work=bad)
+    work = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    r1, i1, _ = xs.sum_condsens(d, 1, work=work)
+    r2, i2, _ = xs.sum_condsens(d, 1)
+    assert bytes(r1.cpu().numpy()) == bytes(r2.cpu().numpy()) and bytes(i1.cpu().numpy()) == bytes(i2.cpu().numpy())

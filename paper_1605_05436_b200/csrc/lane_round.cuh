@@ -252,6 +252,97 @@ __device__ __forceinline__ void lane_canon_image(const int64_t* col, int top, in
 }
 
 // (SegOut: xsum_kernels.h)
+// the outputs of one segment from its roundings (b64 / b32 and their flags rf) and the NaN / Inf
+// flags of its elements
+__device__ __forceinline__ void lane_store_bits(uint64_t b64, uint32_t b32, uint32_t rf, uint32_t flags,
+                                                const SegOut& o, uint64_t s) {
+    const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf;
+    if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
+        b64 = 0x7FF8000000000000ull; b32 = 0x7FC00000u;
+    } else if (fl & XSUM_F_PINF) {
+        b64 = 0x7FF0000000000000ull; b32 = 0x7F800000u;
+    } else if (fl & XSUM_F_NINF) {
+        b64 = 0xFFF0000000000000ull; b32 = 0xFF800000u;
+    }
+    if (o.out) o.out[s] = __longlong_as_double((long long)b64);
+    if (o.out32) o.out32[s] = __uint_as_float(b32);
+    if (o.flags) o.flags[s] = fl;
+}
+
+// Values-only rounding of a lane's RAW digits [lo, hi] without the carry chain, when the top
+// digits decide it (a Ziv-style test; round 2, for K11's short segments whose chain and rounding
+// cost as much as their adds). T = y_hi R + y_(hi-1) (exact in 128 bits: |y_j| < len 2^52), or
+// three digits when that is short, and the digits below add delta in (-len, len) units of T's
+// last digit (|sum_{j<k} y_j R^j| < len R^k).
+// With |T| >= 2^62 the sign and binade of A = (T + delta) R^(hi-1) are T's unless T mod 2^s lies
+// within len of a multiple of 2^(s-1), s the rounding position (>= 10 here), and away from those
+// points RN-even(A) = RN-even of any value within delta of T: the result is T's rounding and it is
+// inexact. Returns false (the caller runs the exact chain) when the test fails or hi < 1.
+__device__ __forceinline__ bool lane_fast_round(const int64_t* col, int lo, int hi, int64_t len, bool want64,
+                                                bool want32, uint64_t& b64, uint32_t& b32, uint32_t& rf) {
+    if (hi < 1 || hi < lo) return false;
+    const int64_t yh = col[hi * 32], yl = hi - 1 >= lo ? col[(hi - 1) * 32] : 0;
+    __int128 T = (__int128)yh * (__int128)R + (__int128)yl;
+    int base = 52 * (hi - 1);
+    // a short top (|T| < 2^74: the largest terms' upper chunks are small) takes the next digit too,
+    // so that the rounding position sits far above delta and the test fails only ~2^-15 of the
+    // time - a warp runs the chain if ANY lane needs it (|T R| < 2^126 + 2^56: still exact)
+    const __int128 lim = (__int128)1 << 74;
+    if (T < lim && T > -lim && hi >= 2 && hi - 2 >= lo) {
+        T = T * (__int128)R + (__int128)col[(hi - 2) * 32];
+        base -= 52;
+    }
+    const bool neg = T < 0;
+    const unsigned __int128 mag = neg ? (unsigned __int128)(-T) : (unsigned __int128)T;
+    const uint64_t mh = (uint64_t)(mag >> 64);
+    if (!mh && ((uint64_t)mag >> 62) == 0) return false;           // |T| < 2^62
+    const int pT = mh ? 127 - __clzll((long long)mh) : 63 - __clzll((long long)(uint64_t)mag);
+    const unsigned __int128 dl = (unsigned __int128)len;
+    bool ok = true;
+    uint32_t r = 0;
+    auto one = [&](int prec, int emin, int emax, bool is64) -> uint64_t {
+        const int P = pT + base;                                   // msb of |A| (binade fixed by the test)
+        int sh = P - (prec - 1) > emin ? P - (prec - 1) : emin;    // lsb kept (absolute)
+        const int sp = sh - base;                                  // ... in units of T: >= 10
+        unsigned __int128 q, rem, half;
+        if (sp >= 120) {                                           // |A| < 2^(sh-1): rounds to zero
+            q = 0; rem = mag; half = (unsigned __int128)1 << 119;
+        } else {
+            q = mag >> sp;
+            rem = mag & (((unsigned __int128)1 << sp) - 1);
+            half = (unsigned __int128)1 << (sp - 1);
+        }
+        if (rem < dl || (rem + dl > half && rem < half + dl) || (sp < 120 && rem + dl > 2 * half)) {
+            ok = false;
+            return 0;
+        }
+        uint64_t qq = (uint64_t)q + (rem > half ? 1u : 0u);
+        uint64_t bits;
+        if (sh == emin) {
+            bits = qq;
+        } else {
+            if (qq == (1ull << prec)) { qq >>= 1; sh += 1; }
+            const int Eb = sh - emin + 1;
+            if (Eb >= emax) {
+                bits = (uint64_t)emax << (prec - 1);
+                r |= is64 ? XSUM_F_OVERFLOW : XSUM_F_OVERFLOW32;
+            } else {
+                bits = ((uint64_t)Eb << (prec - 1)) | (qq - (1ull << (prec - 1)));
+            }
+        }
+        r |= is64 ? XSUM_F_INEXACT : XSUM_F_INEXACT32;
+        if (neg) bits |= is64 ? (1ull << 63) : 0x80000000ull;
+        return bits;
+    };
+    const uint64_t f64 = want64 ? one(53, 0, 2047, true) : 0;
+    const uint32_t f32 = want32 ? (uint32_t)one(24, 925, 255, false) : 0;
+    if (!ok) return false;
+    b64 = f64;
+    b32 = f32;
+    rf |= r;
+    return true;
+}
+
 // the outputs from a segment's canonical top (col: its canonical digits, read only for the image)
 __device__ __forceinline__ void lane_store_top(const LaneTop& t, const int64_t* col, uint32_t flags, const SegOut& o,
                                                uint64_t s) {

@@ -317,6 +317,26 @@ __device__ __forceinline__ void lane_epilogue64(int64_t* col, uint32_t flags, co
     }
     lane_store_top(lane_top_chain(col, lo, hi), col, flags, o, s);
 }
+#ifndef XS_SL_FAST
+#define XS_SL_FAST 1
+#endif
+// K11s: the same, trying the two-digit rounding first (lane_fast_round; values only, len <= 16)
+__device__ __forceinline__ void lane_epilogue64_fast(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s,
+                                                     int lo, int hi, uint32_t len) {
+#if XS_SL_FAST
+    if (!o.canon) {
+        uint64_t b64 = 0;
+        uint32_t b32 = 0, rf = 0;
+        if (lane_fast_round(col, lo, hi, (int64_t)len, o.out || o.flags, o.out32 || o.flags, b64, b32, rf)) {
+#pragma unroll 4
+            for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+            lane_store_bits(b64, b32, rf, flags, o, s);
+            return;
+        }
+    }
+#endif
+    lane_epilogue64(col, flags, o, s, lo, hi);
+}
 
 constexpr int SLP = 16;                     // elements prefetched per lane (8 x 16 B)
 #ifndef XS_SL_PF
@@ -509,7 +529,7 @@ k_segments_lanes64s(const double* __restrict__ x, uint64_t nseg, uint32_t len, S
         }
         __syncwarp();                                            // this group's staging is consumed
         if (SLS_NBUF == 1) issue(g + gstride, 0);                // the next copy overlaps the epilogue
-        if (mine) lane_epilogue64(col, flags, o, s, lo, hi);
+        if (mine) lane_epilogue64_fast(col, flags, o, s, lo, hi, len);
         if (SLS_NBUF == 2) b ^= 1;
     }
 }

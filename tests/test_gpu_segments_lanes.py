@@ -219,3 +219,40 @@ def test_lanes_f64_values_only_paths(xs, L, narrow):
     v2, _, f2 = xs.sum_segments(d, L, flags=True)
     assert (v2.cpu().numpy().view(np.uint64) == b64).all()
     assert (f2.cpu().numpy().astype(np.uint32) == fl).all()
+
+
+@pytest.mark.parametrize("L", [2, 8, 16])
+def test_lanes_f64_two_digit_rounding_boundaries(xs, L):
+    """The values-only K11s epilogue rounds from the two top raw digits when they decide it
+    (lane_fast_round) and otherwise runs the exact chain. Segments built at its decision
+    boundaries: a binary64 / binary32 tie or a result one unit from a rounding or binade boundary
+    in the top digits, tipped either way (or not) by tiny terms in the lower digits, with both
+    signs, at exponents spread over the whole range (near overflow and where binary32 is
+    subnormal or zero); values and flags (both roundings) vs the oracle."""
+    import torch
+    rng = np.random.default_rng(700 + L)
+    nseg = 4096
+    x = np.zeros((nseg, L))
+    for s in range(nseg):
+        e = int(rng.integers(-900, 1000))
+        sg = 1.0 if rng.random() < 0.5 else -1.0
+        prec = 53 if rng.random() < 0.5 else 24
+        m = float(rng.integers(1 << 20, 1 << 21))             # a few significant bits at the top
+        top = sg * m * 2.0 ** e
+        half = 2.0 ** (e + 20 - prec) * (1 if rng.random() < 0.7 else 2)   # half an ulp (or an ulp) of top
+        x[s, 0] = top
+        if L >= 2:
+            x[s, 1] = sg * half * (1 if rng.random() < 0.8 else -1)
+        tiny_e = e - int(rng.integers(60, 300))
+        for k in range(2, L):
+            r = rng.random()
+            x[s, k] = 0.0 if r < 0.3 else (1.0 if r < 0.65 else -1.0) * 2.0 ** (tiny_e - int(rng.integers(0, 40)))
+    x = x.reshape(-1)
+    x[~np.isfinite(x)] = 0.0
+    d = torch.from_numpy(x).cuda()
+    b64, b32, fl, _ = oracle.sum_segments(x, seg_len=L)
+    v, _, f = xs.sum_segments(d, L, flags=True)
+    assert (v.cpu().numpy().view(np.uint64) == b64).all()
+    assert (f.cpu().numpy().astype(np.uint32) == fl).all()
+    v2, _, _ = xs.sum_segments(d, L)                        # values alone (binary64 rounding only)
+    assert (v2.cpu().numpy().view(np.uint64) == b64).all()

@@ -37,6 +37,9 @@ VARIANTS = {
     "sh_u8nb3": ["-DXS_SH_U=8", "-DXS_SH_NB=3"],
     "sh_u2nb8": ["-DXS_SH_U=2", "-DXS_SH_NB=8"],
     "sl_full": ["-DXS_SL_FULL"],
+    "slfast0": ["-DXS_SL_FAST=0"],
+    "slnb2": ["-DXS_SLS_NBUF=2"],
+    "slnb2fast0": ["-DXS_SLS_NBUF=2", "-DXS_SL_FAST=0"],
     "cs2g5": ["-DXS_CS2_G=5"],
     "cs4g4": ["-DXS_CS4_G=4"],
     "cs4g4m2": ["-DXS_CS4_G=4", "-DXS_CS4_MINB=2"],

@@ -103,3 +103,68 @@ def test_one_shot_helpers_per_stream(xs):
     torch.cuda.synchronize()
     assert ra.cpu().numpy().reshape(1).view(np.uint64)[0] == oracle.exact_sum(a)[0].bits
     assert rb.cpu().numpy().reshape(1).view(np.uint64)[0] == oracle.exact_sum(b)[0].bits
+
+
+def test_cuda_graph_capture_of_segment_strided_condsens_paths(xs):
+    """One CUDA graph holding the other hot paths - equal segments (values + flags), a strided
+    reduction over dim 0 (row-split parts + merge), the condition-number-sensitive sum and a
+    binary16 fused sum - replayed on new input contents; every output vs the oracle. No call in
+    these paths synchronizes with the host, so all of them are capturable."""
+    import torch
+
+    from oracle import condsens as cs
+    nseg, L = 777, 1000
+    rows, cols = 5000, 96
+    d_seg = torch.empty(nseg * L, dtype=torch.float64, device="cuda")
+    d_mat = torch.empty(rows * cols, dtype=torch.float64, device="cuda")
+    d_cs = torch.empty(20_001, dtype=torch.float64, device="cuda")
+    d_h = torch.empty(300_007, dtype=torch.int16, device="cuda")
+
+    def fill(seed):
+        xs_ = synth.gen.generate("c2", seed, nseg * L)
+        xm = synth.gen.generate("c5", seed, rows * cols)
+        xc = synth.gen.generate("c3", 2 * seed, 20_001, permute=False)
+        rng = np.random.default_rng(seed)
+        hb = rng.integers(-32768, 32767, size=300_007, dtype=np.int64).astype(np.int16)
+        hb = np.where((hb & 0x7C00) == 0x7C00, hb ^ 0x400, hb).astype(np.int16)
+        d_seg.copy_(torch.from_numpy(xs_))
+        d_mat.copy_(torch.from_numpy(xm))
+        d_cs.copy_(torch.from_numpy(xc))
+        d_h.copy_(torch.from_numpy(hb))
+        return xs_, xm, xc, hb
+
+    s = torch.cuda.Stream()
+    acc = xs.Accumulator()
+    fill(60)
+    torch.cuda.synchronize()
+
+    def step():
+        v, _, f = xs.sum_segments(d_seg, L, flags=True)
+        m = xs.exact_sum_dim(d_mat.view(rows, cols), 0)
+        r, info, _ = xs.sum_condsens(d_cs, 1)
+        h, _ = acc.sum(d_h.view(torch.float16))
+        return v, f, m, r, info, h
+
+    with torch.cuda.stream(s):
+        step()                                           # warm: kernel attributes, allocator
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        outs = step()
+    for seed in (61, 62):
+        xs_, xm, xc, hb = fill(seed)
+        g.replay()
+        torch.cuda.synchronize()
+        v, f, m, r, info, h = outs
+        b64, _, fl, _ = oracle.sum_segments(xs_, seg_len=L)
+        assert (v.cpu().numpy().view(np.uint64) == b64).all() and (f.cpu().numpy().astype(np.uint32) == fl).all()
+        mt = np.ascontiguousarray(xm.reshape(rows, cols).T).reshape(-1)
+        bm, _, _, _ = oracle.sum_segments(mt, seg_len=rows)
+        assert (m.cpu().numpy().view(np.uint64) == bm).all()
+        o = cs.condsens_sum(list(xc), rule=1)
+        res = xs.Result.from_bytes(r.cpu().numpy().tobytes())
+        inf = xs.CondSensInfo.from_bytes(info.cpu().numpy().tobytes())
+        assert inf.r == o.r and inf.iterations == o.iterations
+        assert res.bits == np.float64(o.value).view(np.uint64)
+        rh, _ = oracle.exact_sum(hb.view(np.uint16), fmt="f16")
+        assert xs.Result.from_bytes(h.cpu().numpy().tobytes()).bits == rh.bits

@@ -66,22 +66,29 @@ __device__ __forceinline__ HalfSums half_raw_sums(const int64_t* wb, int hl, int
 
 // Digits hl + LPS k of the slot's sum, regularized (balanced carry to the next digit; the top
 // digit 41 is not split).
+template <int NK = KD>
 __device__ __forceinline__ void carry_in(const int64_t (&c)[KD], int64_t (&in)[KD], int hl) {
     // the carry into digit j comes from digit j-1: lane hl-1 of the same row group, or the
     // slot's last lane of the group below (for hl == 0)
 #pragma unroll
     for (int k = 0; k < KD; ++k) {
+        if (k >= NK) { in[k] = 0; continue; }
         const int64_t up = __shfl_up_sync(FULL, c[k], 1, LPS);
         const int64_t lo = k > 0 ? __shfl_sync(FULL, c[k > 0 ? k - 1 : 0], LPS - 1, LPS) : 0;
         in[k] = hl == 0 ? lo : up;
     }
 }
-__device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[KD], int hl) {
+// (base, NK: the slot's digits base + hl + LPS k for k < NK; the rest are zero)
+template <int NK = KD>
+__device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[KD], int hl, int base = 0) {
     int64_t c[KD], r[KD], in[KD];
 #pragma unroll
     for (int k = 0; k < KD; ++k) {
-        const int row = hl + LPS * k;
-        if (row < D - 1) {
+        const int row = base + hl + LPS * k;
+        if (k >= NK) {
+            c[k] = 0;
+            r[k] = 0;
+        } else if (row < D - 1) {
             c[k] = (d.hs[k] + ((d.ls[k] + (1ll << 51)) >> 32)) >> 20;
             r[k] = (int64_t)((uint64_t)(d.hs[k] - (c[k] << 20)) << 32) + d.ls[k];
         } else if (row == D - 1) {
@@ -92,28 +99,34 @@ __device__ __forceinline__ void half_digits(const HalfSums& d, int64_t (&a)[KD],
             r[k] = 0;
         }
     }
-    carry_in(c, in, hl);
+    carry_in<NK>(c, in, hl);
 #pragma unroll
-    for (int k = 0; k < KD; ++k) a[k] = hl + LPS * k < D ? r[k] + in[k] : 0;
+    for (int k = 0; k < KD; ++k) a[k] = k < NK && base + hl + LPS * k < D ? r[k] + in[k] : 0;
 }
 
 // finalize_warp for a half warp: digits hl + 16k in a[k] (regularized); lane hl == 0 of each half
 // returns the record (binary64 and binary32 roundings, RN-even).
+// Positions are relative to the slot's base digit (bit j of a mask and digit_at(j): digit base + j);
+// base > 0 or NK < KD need zero digits below base and above base + LPS NK (the banded kernel) and no
+// canonical image (canon == nullptr unless base == 0 and NK == KD).
+template <int NK = KD>
 __device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[KD], uint32_t flags, uint64_t count, uint64_t* canon,
-                                                     int64_t* su, int hl, int half) {
+                                                     int64_t* su, int hl, int half, int base = 0) {
     xsum_result res = {};
-    auto valid = [&](int k) { return hl + LPS * k < D; };
-    auto mask = [&](auto pred) -> uint64_t {          // bit j of the slot's 42 digits: pred(k) of lane j % LPS
+    auto valid = [&](int k) { return k < NK && base + hl + LPS * k < D; };
+    auto mask = [&](auto pred) -> uint64_t {          // bit j: pred(k) of lane j % LPS, k = j / LPS (relative)
         uint64_t m = 0;
 #pragma unroll
-        for (int k = 0; k < KD; ++k) m |= (uint64_t)half_bits(__ballot_sync(FULL, valid(k) && pred(k)), half) << (LPS * k);
+        for (int k = 0; k < KD; ++k)
+            if (k < NK) m |= (uint64_t)half_bits(__ballot_sync(FULL, valid(k) && pred(k)), half) << (LPS * k);
         return m;
     };
-    auto digit_at = [&](const int64_t (&v)[KD], int j) -> int64_t {   // digit j of this slot (j per slot)
+    auto digit_at = [&](const int64_t (&v)[KD], int j) -> int64_t {   // relative digit j of this slot
         const int src = j & (LPS - 1), kk = j / LPS;
         int64_t out = 0;
 #pragma unroll
         for (int k = 0; k < KD; ++k) {
+            if (k >= NK) break;
             const int64_t w = __shfl_sync(FULL, v[k], src, LPS);
             if (k == kk) out = w;
         }
@@ -135,9 +148,9 @@ __device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[KD], uint32_t 
     for (int k = 0; k < KD; ++k) {
         b[k] = a[k] >> W;
         r[k] = a[k] & (int64_t)MASK;
-        if (hl + LPS * k == D - 1) { r[k] = a[k]; b[k] = 0; }
+        if (base + hl + LPS * k == D - 1) { r[k] = a[k]; b[k] = 0; }
     }
-    carry_in(b, in, hl);
+    carry_in<NK>(b, in, hl);
 #pragma unroll
     for (int k = 0; k < KD; ++k) t[k] = valid(k) ? r[k] + in[k] : 0;
     const uint64_t G = mask([&](int k) { return t[k] == -1; });
@@ -146,10 +159,10 @@ __device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[KD], uint32_t 
     int64_t u[KD];
 #pragma unroll
     for (int k = 0; k < KD; ++k) {
-        const int j = hl + LPS * k;
-        u[k] = t[k] - (int64_t)((CI >> j) & 1);
+        const int j = base + hl + LPS * k;
+        u[k] = t[k] - (int64_t)((CI >> (hl + LPS * k)) & 1);
         if (j < D - 1) u[k] &= (int64_t)MASK;
-        if (j >= D) u[k] = 0;
+        if (j >= D || k >= NK) u[k] = 0;
     }
     const uint64_t nzu = mask([&](int k) { return u[k] != 0; });
 
@@ -191,11 +204,11 @@ __device__ __forceinline__ xsum_result finalize_half(int64_t (&a)[KD], uint32_t 
     const uint64_t dm = (uint64_t)digit_at(u, m), dm1 = (uint64_t)digit_at(u, m - 1),
                    dm2 = (uint64_t)digit_at(u, m - 2);
     if (nzu && hl < 2) {
-        const int p = 52 * m + (63 - __clzll((long long)dm));
+        const int p = 52 * (m + base) + (63 - __clzll((long long)dm));
         msb = p - 1074;
         int sh = p - (prec - 1) > emin ? p - (prec - 1) : emin;
         const unsigned __int128 Wp = ((unsigned __int128)dm << 53) | ((unsigned __int128)dm1 << 1) | (dm2 >> 51);
-        const int s = sh - 52 * m + 53;
+        const int s = sh - 52 * (m + base) + 53;
         uint64_t q = 0;
         int g = 0;
         bool sticky;
@@ -381,19 +394,217 @@ k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, S
     }
 }
 
+// ---------------------------------------------------------------------------------
+// K6z: the same half-warp streaming loop for segments of at most SZ_MAX_LANE summands per lane
+// (c5: 256). Each segment starts from ZEROED lane columns, so no summand count ever needs a
+// regularization inside the loop and no raw-sum snapshot of the previous segment is kept (12 fewer
+// live registers than K6h: the epilogue reads the columns and zeroes them behind itself). The loop
+// tracks the band of exponents the lane saw with ONE packed 16x2 max (lo: max k, hi: 0xFFFF - min k;
+// the max also serves as K2's NaN/Inf detector); at the segment's end the half's digit band
+// [k_min / 52, k_max / 52 + 1] is the only part of its 16 columns that is combined, zeroed,
+// regularized, canonicalized and rounded (positions relative to the band's lowest digit): c5's
+// exponents span ~10 of the 42 digits, one row group per lane instead of three.
+#ifndef XS_SZ_U
+#define XS_SZ_U 8
+#endif
+#ifndef XS_SZ_NB
+#define XS_SZ_NB 2
+#endif
+constexpr int SZ_U = XS_SZ_U, SZ_NB = XS_SZ_NB;
+constexpr uint32_t SZ_TILE = LPS * SZ_U * 2;                  // doubles per segment tile
+// per-lane summands per segment: every digit of a zeroed column receives at most one chunk
+// (|chunk| <= 2^52) per summand and one per NaN/Inf cancellation: 2 * 1008 chunks < 2^11
+constexpr uint64_t SZ_MAX_LANE = FLUSH_ELEMS / 2;
+
+__device__ __forceinline__ uint32_t band_key(uint32_t k, uint32_t) {
+    return mad_u32(k, 0xFFFF0001u, 0xFFFF0000u);              // lo16: k, hi16: 0xFFFF - k (k <= 2046)
+}
+
+__device__ __noinline__ void halfz_rescan(int64_t* col, const uint4* seg, uint64_t seg_vecs, int hl, uint32_t& flags,
+                                          uint32_t one) {
+    for (uint64_t v = hl; v < seg_vecs; v += LPS) {            // every vector this lane summed
+        const uint4 q = ldg_stream(seg + v);
+        column_fix_special(col, q.x, q.y, flags, one);
+        column_fix_special(col, q.z, q.w, flags, one);
+    }
+}
+
+// K6z's per-segment epilogue over NK row groups of the band (NK = 1: straight-line code)
+template <int NK>
+__device__ __forceinline__ void halfz_epilogue(int64_t* wb, const SegOut& o, int64_t* su, uint64_t* sink, uint64_t ps,
+                                               uint64_t pp, uint64_t nseg, uint64_t seg_len, uint32_t flags, int base,
+                                               int dlo, int dhi, int hl, int half) {
+    __syncwarp();
+    HalfSums d;
+#pragma unroll
+    for (int k = 0; k < KD; ++k) d.hs[k] = d.ls[k] = 0;
+    // lane hl sums row base + hl + LPS k of its half's 16 columns, reading column hl ^ c at step c
+    // (a permutation across the half: conflict-free). The columns are 128-B aligned, so the address
+    // of column hl ^ c is one XOR of the lane's column-hl address. Rows above dhi hold zeros.
+    const uint32_t sw = (uint32_t)__cvta_generic_to_shared(wb) + half * (LPS * 8) + hl * 8;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const int row = base + hl + LPS * k;
+        if (row <= dhi) {
+            const uint32_t A = sw + (uint32_t)row * 256u;
+#pragma unroll
+            for (int c0 = 0; c0 < LPS; c0 += 4) {      // groups of 4 loads in flight (register budget)
+                int64_t v[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v[c]) : "r"(A ^ (uint32_t)((c0 + c) * 8)) : "memory");
+#pragma unroll
+                for (int c = 0; c < 4; ++c)   // the next segment starts from zero
+                    asm volatile("st.shared.b64 [%0], %1;" :: "r"(A ^ (uint32_t)((c0 + c) * 8)), "l"(0ll) : "memory");
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    d.hs[k] += v[c] >> 32;
+                    d.ls[k] += (int64_t)(uint32_t)v[c];
+                }
+            }
+        }
+    }
+    __syncwarp();
+    int64_t a[KD];
+    half_digits<NK>(d, a, hl, base);
+    uint32_t fl = flags;
+#pragma unroll
+    for (int off = LPS / 2; off > 0; off >>= 1) fl |= __shfl_xor_sync(FULL, fl, off, LPS);
+    const bool mine = SEGS * pp + half < nseg;
+    uint64_t* cp = o.canon ? (mine ? o.canon + ps * XSUM_CANON_LIMBS : sink) : nullptr;
+    xsum_result r = finalize_half<NK>(a, fl, seg_len, cp, su, hl, half, base);
+    if (hl == 0 && mine) o.write(ps, r);
+}
+
+#ifndef XS_SZ_WARPS
+#define XS_SZ_WARPS 16    // one block of 16 warps per SM: 658 vs 626 G/s for two blocks of 8 (c5)
+#endif
+#ifndef XS_SZ_MINB
+#define XS_SZ_MINB 1
+#endif
+constexpr int SZ_WARPS = XS_SZ_WARPS;
+constexpr size_t SZ_SMEM = (size_t)SZ_WARPS * D * 32 * sizeof(int64_t);
+#ifndef XS_SZ_COH
+#define XS_SZ_COH 0       // development: coherent (non-.nc) input loads
+#endif
+__device__ __forceinline__ uint4 sz_load(const uint4* p) { return XS_SZ_COH ? ld_stream(p) : ldg_stream(p); }
+
+__global__ void __launch_bounds__(SZ_WARPS * 32, XS_SZ_MINB)
+k_segments_halfz(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(128) int64_t winz[];           // 128-B aligned columns (the epilogue's XOR)
+    __shared__ int64_t su[SZ_WARPS][SEGS][48];
+    __shared__ uint64_t canon_sink[SZ_WARPS][XSUM_CANON_LIMBS];   // the odd last pair's idle half
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & (LPS - 1), half = lane / LPS;
+    int64_t* col = winz + warp * (D * 32) + lane;
+    const uint64_t nw = (uint64_t)gridDim.x * SZ_WARPS;
+    const uint64_t npairs = (nseg + SEGS - 1) / SEGS;
+    const uint64_t gw = (uint64_t)blockIdx.x * SZ_WARPS + warp;
+    if (gw >= npairs) return;                                  // warp-uniform
+    const uint32_t TPS = (uint32_t)(seg_len / SZ_TILE);
+    const uint64_t seg_vecs = seg_len / 2;
+    const uint4* xv = reinterpret_cast<const uint4*>(x);
+#pragma unroll
+    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    auto seg_of = [&](uint64_t p) -> uint64_t {
+        const uint64_t s = SEGS * p + half;
+        return s < nseg ? s : SEGS * p;
+    };
+    constexpr uint32_t TV = LPS * SZ_U;
+    const uint4* lp = xv + seg_of(gw) * seg_vecs + hl;
+    uint64_t lpair = gw;
+    uint32_t lt = 0;
+    auto advance_load = [&]() {
+        lp += SZ_NB * TV;
+        lt += SZ_NB;
+        if (lt == TPS) {
+            lt = 0;
+            lpair += nw;
+            lp = xv + seg_of(lpair < npairs ? lpair : gw) * seg_vecs + hl;
+        }
+    };
+    uint64_t pp = gw;
+    uint32_t pt = 0, band = 0;
+    uint4 buf[SZ_NB][SZ_U];
+#pragma unroll
+    for (int bb = 0; bb < SZ_NB; ++bb)
+#pragma unroll
+        for (int u = 0; u < SZ_U; ++u) buf[bb][u] = sz_load(lp + bb * TV + u * LPS);
+    advance_load();
+    while (pp < npairs) {
+        const bool ld = lpair < npairs;
+#pragma unroll
+        for (int bb = 0; bb < SZ_NB; ++bb) {
+#pragma unroll
+            for (int u = 0; u < SZ_U; ++u) {
+                Chunks a = decompose(buf[bb][u].x, buf[bb][u].y, one, mone);
+                column_add(col, a, one);
+                Chunks c = decompose(buf[bb][u].z, buf[bb][u].w, one, mone);
+                column_add(col, c, one);
+                band = __vmaxu2(__vmaxu2(band, band_key(a.spec, one)), band_key(c.spec, one));
+            }
+            if (ld) {
+#pragma unroll
+                for (int u = 0; u < SZ_U; ++u) buf[bb][u] = sz_load(lp + bb * TV + u * LPS);
+            }
+        }
+        if (ld) advance_load();
+        pt += SZ_NB;
+#ifdef XS_EXP_SZ_NOEPI
+        if (pt == TPS) { pt = 0; pp += nw; band = 0; continue; }   // diagnostic: WRONG sums
+#endif
+        if (pt == TPS) {                                       // both halves' segments complete
+            const uint64_t ps = seg_of(pp);
+            uint32_t flags = 0;
+            if (__any_sync(FULL, (band & 0xFFFFu) >= 2046u)) {  // rare: cancel NaN/Inf patterns
+                if ((band & 0xFFFFu) >= 2046u) halfz_rescan(col, xv + ps * seg_vecs, seg_vecs, hl, flags, one);
+            }
+#pragma unroll
+            for (int off = LPS / 2; off > 0; off >>= 1) band = __vmaxu2(band, __shfl_xor_sync(FULL, band, off, LPS));
+            const int kmax = (int)(band & 0xFFFFu), kmin = 0xFFFF - (int)(band >> 16);
+            const int dlo = kmin / 52, dhi = kmax / 52 + 1;    // the digits this half's chunks touched
+            const int base = o.canon ? 0 : dlo;
+            int nk = (dhi + 2 - base + LPS - 1) / LPS;         // rows base .. dhi + 1 (the top carry)
+            nk = max(nk, __shfl_xor_sync(FULL, nk, LPS));
+            nk = o.canon || nk > KD ? KD : nk;
+            if (nk == 1)                                       // warp-uniform
+                halfz_epilogue<1>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
+                                  flags, base, dlo, dhi, hl, half);
+            else
+                halfz_epilogue<KD>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
+                                   flags, base, dlo, dhi, hl, half);
+            band = 0;
+            pt = 0;
+            pp += nw;
+        }
+    }
+}
+
 bool segments_half_ok(const double* x, uint64_t seg_len) {
     return seg_len >= SH_TILE && seg_len % ((uint64_t)SH_TILE * SH_NB) == 0 && ((uintptr_t)x & 15) == 0 &&
            seg_len / SH_TILE < (1u << 31);
 }
 
+#ifndef XS_SH_Z
+#define XS_SH_Z 1
+#endif
 cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
                               cudaStream_t s) {
-    static unsigned long long smem_set = 0;
-    if (cudaError_t e = ensure_smem(k_segments_half, SH_SMEM, smem_set)) return e;
     const uint64_t npairs = (nseg + SEGS - 1) / SEGS;          // groups of SEGS segments
     const uint64_t want = (npairs + SH_WARPS - 1) / SH_WARPS;
     const uint64_t cap = (uint64_t)num_sms * 2;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    const uint64_t wantz = (npairs + SZ_WARPS - 1) / SZ_WARPS;
+    const uint64_t capz = (uint64_t)num_sms * XS_SZ_MINB;
+    const unsigned gz = (unsigned)(wantz < capz ? (wantz ? wantz : 1) : capz);
+    if (XS_SH_Z && seg_len / LPS <= SZ_MAX_LANE && seg_len % ((uint64_t)SZ_TILE * SZ_NB) == 0) {
+        static unsigned long long smem_z = 0;
+        if (cudaError_t e = ensure_smem(k_segments_halfz, SZ_SMEM, smem_z)) return e;
+        k_segments_halfz<<<gz, SZ_WARPS * 32, SZ_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
+        note_launch();
+        return cudaGetLastError();
+    }
+    static unsigned long long smem_set = 0;
+    if (cudaError_t e = ensure_smem(k_segments_half, SH_SMEM, smem_set)) return e;
     k_segments_half<<<g, SH_WARPS * 32, SH_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
     note_launch();
     return cudaGetLastError();

@@ -609,3 +609,77 @@ def test_segments_half_warp_path(xs, seg_len, nseg):
     for s in range(nseg):
         r, limbs = oracle.exact_sum(x[s * seg_len:(s + 1) * seg_len], nthreads=1)
         assert int(vals[s]) == r.bits and int(flags[s]) == r.flags and (canon[s] == limbs).all(), s
+
+
+def _band_segments(rng, nseg: int, seg_len: int) -> np.ndarray:
+    """Segments whose exponent bands differ (K6z combines only the digits a half-warp's segment
+    touched, positions relative to the band's lowest digit): narrow bands anywhere in the range,
+    bands straddling the 16-digit row groups, the full range, cancellation to a tiny or subnormal
+    sum, zeros and subnormal inputs (band from digit 0), specials, exact ties, overflow."""
+    out = np.empty((nseg, seg_len), dtype=np.uint64)
+
+    def field(lo, hi, n):
+        e = rng.integers(max(lo, 0), min(hi, 2046) + 1, n, dtype=np.uint64)
+        m = rng.integers(0, 1 << 52, n, dtype=np.uint64)
+        s = rng.integers(0, 2, n, dtype=np.uint64)
+        return (s << np.uint64(63)) | (e << np.uint64(52)) | m
+
+    for s in range(nseg):
+        kind = s % 11
+        if kind == 0:
+            c = int(rng.integers(1, 2047))
+            v = field(c - 30, c + 30, seg_len)
+        elif kind == 1:
+            v = field(1, 2046, seg_len)
+        elif kind == 2:                                 # pairs a, -a and a few tiny terms
+            h = field(600, 1400, seg_len // 2)
+            v = np.concatenate([h, h ^ np.uint64(1 << 63)])
+            v[:4] = field(1, 40, 4)
+            rng.shuffle(v)
+        elif kind == 3:                                 # zeros, subnormals and normals
+            v = field(900, 1100, seg_len)
+            idx = rng.integers(0, seg_len, seg_len // 8)
+            v[idx] = rng.integers(0, 1 << 52, idx.size, dtype=np.uint64)            # subnormal / zero
+            v[idx[: idx.size // 2]] = np.uint64(0)
+        elif kind == 4:                                 # a special
+            v = field(500, 700, seg_len)
+            v[int(rng.integers(0, seg_len))] = rng.choice(np.array([0x7FF0000000000000, 0xFFF0000000000000,
+                                                                    0x7FF8000000000123], dtype=np.uint64))
+        elif kind == 5:                                 # all (signed) zeros
+            v = (rng.integers(0, 2, seg_len, dtype=np.uint64) << np.uint64(63))
+        elif kind == 6:                                 # an exact tie: 2^53 + 1 (+ even/odd neighbours)
+            v = np.zeros(seg_len, dtype=np.uint64)
+            v[0] = np.float64(2.0 ** 53).view(np.uint64)
+            v[seg_len // 2] = np.float64(1.0).view(np.uint64)
+            v[seg_len - 1] = np.float64(2.0 * (s % 2)).view(np.uint64)
+        elif kind == 7:                                 # around the digit-16 row boundary (k ~ 832)
+            v = field(800, 870, seg_len)
+        elif kind == 8:                                 # around the digit-32 row boundary (k ~ 1664)
+            v = field(1630, 1700, seg_len)
+        elif kind == 9:                                 # overflow of the rounded sum
+            v = field(2046, 2046, seg_len) & np.uint64((1 << 63) - 1)
+        else:                                           # cancellation to a subnormal sum
+            h = field(1, 3, seg_len // 2)
+            v = np.concatenate([h, h ^ np.uint64(1 << 63)])
+            v[0] = np.uint64(5)
+            rng.shuffle(v)
+        out[s] = v
+    return out.reshape(-1).view(np.float64)
+
+
+@pytest.mark.parametrize("seg_len,nseg", [(512, 45), (1024, 23), (4096, 33), (8192, 11), (15872, 11), (16384, 5)])
+def test_segments_half_band_values_only(xs, seg_len, nseg):
+    """Values-only equal segments (K6z's banded epilogue: no canonical image requested) with a
+    different exponent band in every segment and both halves of a warp on different bands: value
+    and flags of every segment vs the oracle; 16384 (1024 summands per lane) takes K6h."""
+    rng = np.random.default_rng(1605 + seg_len)
+    x = _band_segments(rng, nseg, seg_len)
+    vals, _, flags = xs.sum_segments(to_dev(x, 0), seg_len, flags=True)
+    vals = vals.cpu().numpy().view(np.uint64)
+    flags = flags.cpu().numpy()
+    for s in range(nseg):
+        r, _ = oracle.exact_sum(x[s * seg_len:(s + 1) * seg_len], nthreads=1)
+        assert int(vals[s]) == r.bits and int(flags[s]) == r.flags, (s, s % 11, hex(int(vals[s])), hex(r.bits))
+    # the same segments with images requested (the full-width epilogue) agree as well
+    vals2, canon, _ = xs.sum_segments(to_dev(x, 0), seg_len, canon=True)
+    assert (vals2.cpu().numpy().view(np.uint64) == vals).all()

@@ -66,6 +66,10 @@ def main(t: str):
         a = xsum.Accumulator().add(synth.device_generate("c2", 0, 1 << 20))
         for _ in range(3):
             a.finalize_async(canon=True)
+    elif t == "c5":
+        x = synth.device_generate("c5")
+        for _ in range(3):
+            xsum.sum_segments(x, 4096)
     elif t == "c5csr":
         x = synth.device_generate("c5csr")
         off = synth.csr_offsets("c5csr", device="cuda")

@@ -64,6 +64,12 @@ VARIANTS = {
     "h16_nb2": ["-DXS_H16_NB=2"],
     "h16_ldsts": ["-DXS_H16_LDSTS"],
     "f32b_nb4": ["-DXS_F32B_NB=4"],
+    "sz0": ["-DXS_SH_Z=0"],
+    "sz_u4nb4": ["-DXS_SZ_U=4", "-DXS_SZ_NB=4"],
+    "sz_u2nb8": ["-DXS_SZ_U=2", "-DXS_SZ_NB=8"],
+    "sz_coh": ["-DXS_SZ_COH=1"],
+    "sz_w8": ["-DXS_SZ_WARPS=8", "-DXS_SZ_MINB=2"],
+    "exp_sz_noepi": ["-DXS_EXP_SZ_NOEPI"],
 }
 
 

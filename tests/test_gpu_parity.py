@@ -683,3 +683,41 @@ def test_segments_half_band_values_only(xs, seg_len, nseg):
     # the same segments with images requested (the full-width epilogue) agree as well
     vals2, canon, _ = xs.sum_segments(to_dev(x, 0), seg_len, canon=True)
     assert (vals2.cpu().numpy().view(np.uint64) == vals).all()
+
+
+@pytest.mark.parametrize("fill", ["pairs", "zeros"])
+def test_segments_half_fast_rounding_boundaries(xs, fill):
+    """K6z's banded rounding at its boundaries: segments of 512 whose sum is a binary64 / binary32
+    tie or an ulp from a rounding boundary in the top digits, tipped either way (or not) by tiny
+    terms several digits lower, both signs, exponents over the whole range; the rest of each
+    segment cancelling pairs near the top (a narrow band: one row group) or zeros (the band starts
+    at digit 0: three row groups). Values and flags (both roundings) vs the oracle."""
+    import torch
+    rng = np.random.default_rng(811 if fill == "pairs" else 812)
+    nseg, L = 2048, 512
+    x = np.zeros((nseg, L))
+    for s in range(nseg):
+        e = int(rng.integers(-900, 960))
+        sg = 1.0 if rng.random() < 0.5 else -1.0
+        prec = 53 if rng.random() < 0.5 else 24
+        m = float(rng.integers(1 << 20, 1 << 21))
+        top = sg * m * 2.0 ** e
+        half = 2.0 ** (e + 20 - prec) * (1 if rng.random() < 0.7 else 2)
+        x[s, 0] = top
+        x[s, 1] = sg * half * (1 if rng.random() < 0.8 else -1)
+        tiny_e = e - int(rng.integers(60, 300))
+        for k in range(2, 10):
+            r = rng.random()
+            x[s, k] = 0.0 if r < 0.3 else (1.0 if r < 0.65 else -1.0) * 2.0 ** (tiny_e - int(rng.integers(0, 40)))
+        if fill == "pairs":
+            p = rng.standard_normal((L - 10) // 2) * 2.0 ** (e - 5)
+            x[s, 10:] = np.concatenate([p, -p])
+    x = x.reshape(-1)
+    x[~np.isfinite(x)] = 0.0
+    d = torch.from_numpy(x).cuda()
+    b64, b32, fl, _ = oracle.sum_segments(x, seg_len=L)
+    v, _, f = xs.sum_segments(d, L, flags=True)
+    assert (v.cpu().numpy().view(np.uint64) == b64).all()
+    assert (f.cpu().numpy().astype(np.uint32) == fl).all()
+    v2, _, _ = xs.sum_segments(d, L)
+    assert (v2.cpu().numpy().view(np.uint64) == b64).all()

@@ -700,7 +700,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config),
                          "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
-                                    "c2bf16": "k_accumulate_h16", "c5": "k_segments_half",
+                                    "c2bf16": "k_accumulate_h16", "c5": "k_segments_halfz",
                                     "c5csr": "k_segments", "c5s16": "k_segments_lanes64s",
                                     "c2dim0": "k_sum_strided", "c2cs": "xsum_sum_condsens step (all passes)",
                                     "c3cs": "xsum_sum_condsens step (all passes)"}.get(args.config, "k_accumulate"),

@@ -34,31 +34,62 @@ __device__ __noinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_
     }
 }
 
-// Per-segment epilogue (one warp): combine the 32 lane columns (|sum| <= 32 (2^51 + 2^11)
-// < 2^57), regularize, canonicalize and round, write
-// the outputs, and zero the lane column for the next segment.
-__device__ __forceinline__ void segment_epilogue(int64_t* col, const int64_t* wb, int64_t* su, uint32_t flags,
-                                              uint64_t len, uint64_t s, const SegOut& o, int lane) {
+// Per-segment epilogue of K6's CSR loop (one warp): combine the 32 lane columns (|sum| <= 32 (2^51 +
+// 2^11) < 2^57), regularize, canonicalize and round and write
+// the outputs, reading (and zeroing behind itself) only the rows the segment can
+// have touched: every chunk of a summand with exponent index k lands in digits <= k / 52 + 1, and
+// a column that was regularized inside the segment (long segments only) may hold carries up to
+// digit D-1, so rows 32..41 are read when top = max over the warp of those bounds reaches 32
+// (c5csr's exponents reach digit 25: one row per lane). The rest of the column is zero.
+__device__ __forceinline__ void segment_epilogue_top(const int64_t* wb, int64_t* su, uint32_t flags, int top,
+                                                     uint64_t len, uint64_t s, const SegOut& o, int lane) {
+    __syncwarp();
+    int64_t* wz = const_cast<int64_t*>(wb);
+    LaneSums t = {0, 0, 0, 0};
+    const bool hi_rows = top >= 32;                  // warp-uniform
+#pragma unroll 8
+    for (int c = 0; c < 32; ++c) {
+        const int cc = (lane + c) & 31;              // rotated: conflict-free columns
+        const int64_t v0 = wb[lane * 32 + cc];
+        wz[lane * 32 + cc] = 0;
+        t.hs0 += v0 >> 32;
+        t.ls0 += (int64_t)(uint32_t)v0;
+        if (hi_rows && lane + 32 < D) {
+            const int64_t v1 = wb[(lane + 32) * 32 + cc];
+            wz[(lane + 32) * 32 + cc] = 0;
+            t.hs1 += v1 >> 32;
+            t.ls1 += (int64_t)(uint32_t)v1;
+        }
+    }
     __syncwarp();
     int64_t a0, a1;
-    combine_raw_columns(wb, a0, a1, lane);           // lane columns need no regularization
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < D; ++j) col[j * 32] = 0;
+    sums_to_digits(t, a0, a1, lane);
     flags = __reduce_or_sync(FULL, flags);
     // inline (finalize_warp_inl): an out-of-line call would wait for the next segment's loads
     xsum_result r = finalize_warp_inl(a0, a1, flags, len, o.canon ? o.canon + s * XSUM_CANON_LIMBS : nullptr, su, lane);
     if (lane == 0) o.write(s, r);
 }
 
-__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
+// exponent index k = max(e, 1) - 1 of a binary64 high word (its chunks land in digits <= k / 52 + 1)
+__device__ __forceinline__ uint32_t kidx(uint32_t hi) { return max((hi >> 20) & 0x7FFu, 1u) - 1u; }
+
+#ifndef XS_SEGC_WARPS
+#define XS_SEGC_WARPS 16  // one 16-warp block per SM (c5csr 549 vs 544 G/s for two 8-warp blocks)
+#endif
+#ifndef XS_SEGC_MINB
+#define XS_SEGC_MINB 1
+#endif
+constexpr int SEGC_WARPS = XS_SEGC_WARPS;
+constexpr size_t SEGC_SMEM = (size_t)SEGC_WARPS * D * 32 * sizeof(int64_t);
+
+__global__ void __launch_bounds__(SEGC_WARPS * 32, XS_SEGC_MINB)
 k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
            SegOut o, unsigned long long* __restrict__ ticket, uint32_t one, uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
-    __shared__ int64_t su[SEG_WARPS][64];
+    __shared__ int64_t su[SEGC_WARPS][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t* col = win + warp * (D * 32) + lane;
-    const uint64_t nw = (uint64_t)gridDim.x * SEG_WARPS;
+    const uint64_t nw = (uint64_t)gridDim.x * SEGC_WARPS;
 
     // A warp's segments s, s + nw, ...: the next segment's bounds and first tile are fetched
     // before the current segment's epilogue, so its DRAM latency hides behind the epilogue.
@@ -88,7 +119,7 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
     // Segment order: with a ticket counter, warps take the next unclaimed segment (dynamic
     // balancing: ragged CSR lengths made the static round-robin's busiest warp do 1.36x the mean
     // work on c5csr); without one, segments s, s + nw, ... (static).
-    uint64_t s = ticket ? seg_next(ticket, 0, nw, lane) : (uint64_t)blockIdx.x * SEG_WARPS + warp;
+    uint64_t s = ticket ? seg_next(ticket, 0, nw, lane) : (uint64_t)blockIdx.x * SEGC_WARPS + warp;
     if (s >= nseg) return;                                           // warp-uniform
 #pragma unroll
     for (int j = 0; j < D; ++j) col[j * 32] = 0;
@@ -103,7 +134,8 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
     while (true) {
         const uint64_t sn = seg_next(ticket, s, nw, lane);
         bounds(sn, ob, oe);                                          // next segment's bounds, early
-        uint32_t flags = 0, nspec = 0;
+        uint32_t flags = 0, nspec = 0, kmax = 0;
+        bool flushed = false;
         const uint64_t nit = g.nit, nvec = g.nvec;
         const uint4* body = g.body;
         uint64_t wstart = 0;
@@ -123,12 +155,14 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
             }
             if (++since == SEG_FLUSH_ITERS) {
                 regularize_column(col);
+                flushed = true;
                 if (__any_sync(FULL, spec_hit(nspec))) {
                     if (spec_hit(nspec)) {
                         seg_rescan(col, body, wstart, it, lane, flags, one);
                         regularize_column(col);
                     }
                 }
+                kmax = max(kmax, nspec);
                 nspec = 0;
                 since = 0;
                 wstart = it + 1;
@@ -159,15 +193,18 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
             if (nit * (32 * SEG_U) + u * 32 + lane < nvec) {
                 column_add_checked(col, lv[u].x, lv[u].y, flags, one);
                 column_add_checked(col, lv[u].z, lv[u].w, flags, one);
+                kmax = max(kmax, max(kidx(lv[u].y), kidx(lv[u].w)));
             }
         }
         if (lane == 0 && g.head) {
             uint2 q = ldg_one(g.xs);
             column_add_checked(col, q.x, q.y, flags, one);
+            kmax = max(kmax, kidx(q.y));
         }
         if (lane == 1 && (g.nbody & 1)) {
             uint2 q = ldg_one(g.xs + g.head + 2 * nvec);
             column_add_checked(col, q.x, q.y, flags, one);
+            kmax = max(kmax, kidx(q.y));
         }
         if (__any_sync(FULL, spec_hit(nspec))) {        // raw columns go to the epilogue
             if (spec_hit(nspec) && since) {
@@ -185,7 +222,10 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
                 for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
             }
         }
-        segment_epilogue(col, win + warp * (D * 32), su[warp], flags, len, s, o, lane);
+        // checked adds of the head / tail / leftovers may reach any digit: include them
+        int top = flushed ? D : (int)(max(kmax, nspec) / 52u) + 1;
+        top = __reduce_max_sync(FULL, top);
+        segment_epilogue_top(win + warp * (D * 32), su[warp], flags, top, len, s, o, lane);
         if (!more) break;
         s = sn;
     }
@@ -339,7 +379,7 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     if (!offsets && seg_len > 0 && seg_len <= SEG_LANES_MAX)
         return sum_segments_lanes(x, XSUM_DT_F64, nseg, seg_len, o, num_sms, s);
     static unsigned long long smem_set = 0, smem_set_u = 0;
-    if (cudaError_t e = ensure_smem(k_segments, SEG_SMEM, smem_set)) return e;
+    if (cudaError_t e = ensure_smem(k_segments, SEGC_SMEM, smem_set)) return e;
     if (cudaError_t e = ensure_smem(k_segments_uniform, SEG_SMEM, smem_set_u)) return e;
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
     uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (84 KiB smem each)
@@ -354,8 +394,10 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     if (uniform)
         k_segments_uniform<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
     else {
-        k_segments<<<g, SEG_WARPS * 32, SEG_SMEM, s>>>(x, nseg, seg_len, offsets, o, offsets ? ticket : nullptr, 1u,
-                                                       0xFFFFFFFFu);
+        const uint64_t wantc = (nseg + SEGC_WARPS - 1) / SEGC_WARPS, capc = (uint64_t)num_sms * XS_SEGC_MINB;
+        const unsigned gc = (unsigned)(wantc < capc ? (wantc ? wantc : 1) : capc);
+        k_segments<<<gc, SEGC_WARPS * 32, SEGC_SMEM, s>>>(x, nseg, seg_len, offsets, o, offsets ? ticket : nullptr, 1u,
+                                                          0xFFFFFFFFu);
     }
     note_launch();
     return cudaGetLastError();

@@ -30,7 +30,13 @@ __device__ __forceinline__ uint32_t sload_one(const uint8_t* p) {
     return __ldg(reinterpret_cast<const uint16_t*>(p));
 }
 
-constexpr int SSEG_WARPS = 8;
+#ifndef XS_SSEG_WARPS
+#define XS_SSEG_WARPS 16   // one 16-warp block per SM: segments of 4096 binary32 1030 -> 1100, binary16 1949 -> 2011-2039, bfloat16 1655 -> 1676 G/s
+#endif
+#ifndef XS_SSEG_MINB
+#define XS_SSEG_MINB 1
+#endif
+constexpr int SSEG_WARPS = XS_SSEG_WARPS;
 constexpr int SSEG_U = 4;                  // vectors per lane per tile
 
 template <class F>
@@ -75,7 +81,7 @@ __device__ __noinline__ void sseg_rescan(uint64_t* bins, int64_t* col, const uin
 }
 
 template <class F>
-__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+__global__ void __launch_bounds__(SSEG_WARPS * 32, XS_SSEG_MINB)
 k_segments_small(const uint8_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
                  SegOut o, unsigned long long* __restrict__ ticket, uint32_t one) {
     extern __shared__ __align__(16) int64_t win[];
@@ -237,7 +243,7 @@ constexpr size_t h16seg_smem() {
 }
 
 template <class F>
-__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+__global__ void __launch_bounds__(SSEG_WARPS * 32, XS_SSEG_MINB)
 k_segments_h16(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, const uint64_t* __restrict__ offsets,
                SegOut o, unsigned long long* __restrict__ ticket, uint32_t one, uint32_t mone) {
     using S = H16Col<F>;
@@ -384,7 +390,7 @@ __device__ __noinline__ uint32_t h16q_classify(const uint16_t* xs, uint64_t len,
 }
 
 template <class F>
-__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+__global__ void __launch_bounds__(SSEG_WARPS * 32, XS_SSEG_MINB)
 k_segments_h16q(const uint16_t* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one,
                 uint32_t mone) {
     using S = H16Col<F>;
@@ -506,7 +512,7 @@ __device__ __noinline__ void smallq_rescan(uint64_t* bins, int64_t* col, const u
 }
 
 template <class F>
-__global__ void __launch_bounds__(SSEG_WARPS * 32, 2)
+__global__ void __launch_bounds__(SSEG_WARPS * 32, XS_SSEG_MINB)
 k_segments_smallq(const float* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t gsum[SSEG_WARPS][HQ_SEGS][F::COLS];
@@ -595,7 +601,7 @@ static cudaError_t launch_smallq(const void* x, uint64_t nseg, uint64_t seg_len,
     if (cudaError_t e = ensure_smem(k_segments_smallq<F>, sseg_smem<F>(), smem_set)) return e;
     const uint64_t nquads = (nseg + HQ_SEGS - 1) / HQ_SEGS;
     const uint64_t want = (nquads + SSEG_WARPS - 1) / SSEG_WARPS;
-    const uint64_t cap = (uint64_t)num_sms * 2;
+    const uint64_t cap = (uint64_t)num_sms * XS_SSEG_MINB;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     k_segments_smallq<F><<<g, SSEG_WARPS * 32, sseg_smem<F>(), s>>>(static_cast<const float*>(x), nseg, seg_len, o,
                                                                      1u);
@@ -610,7 +616,7 @@ static cudaError_t launch_h16q(const void* x, uint64_t nseg, uint64_t seg_len, c
     if (cudaError_t e = ensure_smem(k_segments_h16q<F>, h16seg_smem<F>(), smem_set)) return e;
     const uint64_t nquads = (nseg + HQ_SEGS - 1) / HQ_SEGS;
     const uint64_t want = (nquads + SSEG_WARPS - 1) / SSEG_WARPS;
-    const uint64_t cap = (uint64_t)num_sms * 2;
+    const uint64_t cap = (uint64_t)num_sms * XS_SSEG_MINB;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     k_segments_h16q<F><<<g, SSEG_WARPS * 32, h16seg_smem<F>(), s>>>(static_cast<const uint16_t*>(x), nseg, seg_len, o,
                                                                      1u, 0xFFFFFFFFu);
@@ -624,7 +630,7 @@ static cudaError_t launch_h16seg(const void* x, uint64_t nseg, uint64_t seg_len,
     static unsigned long long smem_set = 0;
     if (cudaError_t e = ensure_smem(k_segments_h16<F>, h16seg_smem<F>(), smem_set)) return e;
     const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
-    const uint64_t cap = (uint64_t)num_sms * 2;
+    const uint64_t cap = (uint64_t)num_sms * XS_SSEG_MINB;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     k_segments_h16<F><<<g, SSEG_WARPS * 32, h16seg_smem<F>(), s>>>(static_cast<const uint16_t*>(x), nseg, seg_len,
                                                                     offsets, o, offsets ? ticket : nullptr, 1u,
@@ -639,7 +645,7 @@ static cudaError_t launch_small(const void* x, uint64_t nseg, uint64_t seg_len, 
     static unsigned long long smem_set = 0;
     if (cudaError_t e = ensure_smem(k_segments_small<F>, sseg_smem<F>(), smem_set)) return e;
     const uint64_t want = (nseg + SSEG_WARPS - 1) / SSEG_WARPS;
-    const uint64_t cap = (uint64_t)num_sms * 2;
+    const uint64_t cap = (uint64_t)num_sms * XS_SSEG_MINB;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     k_segments_small<F><<<g, SSEG_WARPS * 32, sseg_smem<F>(), s>>>(static_cast<const uint8_t*>(x), nseg, seg_len,
                                                                     offsets, o, offsets ? ticket : nullptr, 1u);

@@ -70,6 +70,7 @@ VARIANTS = {
     "sz_coh": ["-DXS_SZ_COH=1"],
     "sz_w8": ["-DXS_SZ_WARPS=8", "-DXS_SZ_MINB=2"],
     "segc_w16": ["-DXS_SEGC_WARPS=16", "-DXS_SEGC_MINB=1"],
+    "sseg_w16": ["-DXS_SSEG_WARPS=16", "-DXS_SSEG_MINB=1"],
     "exp_sz_noepi": ["-DXS_EXP_SZ_NOEPI"],
 }
 

@@ -569,6 +569,9 @@ k_segments_halfz(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
             if (nk == 1)                                       // warp-uniform
                 halfz_epilogue<1>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
                                   flags, base, dlo, dhi, hl, half);
+            else if (LPS < 16 && nk == 2)                      // quarter warps: c5's band is two groups
+                halfz_epilogue<2>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
+                                  flags, base, dlo, dhi, hl, half);
             else
                 halfz_epilogue<KD>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
                                    flags, base, dlo, dhi, hl, half);

@@ -416,9 +416,11 @@ XSUM_API xsum_status xsum_sum_segments_csr_lanes(const void *d_x, int dtype, uin
  * requested). Specials follow R10 (NaN, +Inf, -Inf). Each lane sums one fibre in its own shared
  * superaccumulator and rounds it itself. When the fibres
  * cannot fill the GPU the rows are split into parts whose exact partial superaccumulators are
- * merged by a second launch; that needs d_work of xsum_sum_strided_work_bytes(...) bytes
- * (8-B aligned, caller-owned, no initialization); with a smaller or NULL d_work the split is not
- * used (same results, fewer SMs busy). inner = 1 is served by the segment kernels
+ * merged by a second launch, or (binary64, when the fibre groups fill the resident warps unevenly)
+ * every warp takes an equal share of all rows and the pieces of a fibre meet in a per-fibre
+ * accumulator (stream-K; the call clears it first); either needs d_work of
+ * xsum_sum_strided_work_bytes(...) bytes (8-B aligned, caller-owned, no initialization); with a
+ * smaller or NULL d_work neither is used (same results, fewer SMs busy). inner = 1 is served by the segment kernels
  * (xsum_sum_segments_ex; its flags carry both roundings' bits). At least one of d_out64 /
  * d_out32. Stream-ordered, no host synchronization. Errors: XSUM_EINVAL (bad dtype, no output,
  * misalignment, sizes overflowing 2^63), XSUM_ECUDA. */

@@ -35,6 +35,9 @@ constexpr int STR_UNR = XS_STR_UNR;       // rows loaded together per lane (one 
 #endif
 constexpr int STR_NB = XS_STR_NB;         // rotating group buffers
 constexpr size_t STR_SMEM = (size_t)STR_WARPS * D * 32 * sizeof(int64_t);
+#ifndef XS_STR_SK
+#define XS_STR_SK 1                       // binary64 strided reductions through K10s when it balances better
+#endif
 
 // Round the lane's regularized column and store fibre f's outputs (specials per R10).
 __device__ __forceinline__ void lane_store(int64_t* col, uint32_t flags, const StrOut& o, uint64_t f) {
@@ -55,29 +58,14 @@ __device__ __forceinline__ void lane_store(int64_t* col, uint32_t flags, const S
     if (o.flags) o.flags[f] = fl;
 }
 
+// Rows [r0, r1) of fibre (ob, i) into the lane's (zeroed) column, leaving it regularized; NaN / Inf
+// flags into `flags`.
 template <int DT>
-__global__ void __launch_bounds__(STR_WARPS * 32, 1)
-k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner,
-              uint32_t parts, StrOut o, int64_t* __restrict__ work, uint32_t* __restrict__ wflags, uint32_t one,
-              uint32_t mone) {
+__device__ __forceinline__ void strided_rows(const typename StrLd<DT>::T* __restrict__ x, uint64_t ob, uint64_t i,
+                                             uint64_t len, uint64_t inner, uint64_t r0, uint64_t r1, int64_t* col,
+                                             uint32_t& flags, uint32_t one, uint32_t mone) {
     using L = StrLd<DT>;
-    extern __shared__ __align__(16) int64_t win[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t* col = win + warp * (D * 32) + lane;
-    const uint64_t gpr = (inner + 31) / 32;                    // warps per outer row
-    const uint64_t items = outer * gpr * parts;
-    const uint64_t plen = (len + parts - 1) / parts;           // rows per part
-    const uint64_t F = outer * inner;
-    for (uint64_t it = (uint64_t)blockIdx.x * STR_WARPS + warp; it < items; it += (uint64_t)gridDim.x * STR_WARPS) {
-        const uint64_t p = it / (items / parts), grp = it % (items / parts);   // neighbouring warps: neighbouring fibres
-        const uint64_t ob = grp / gpr, i = (grp % gpr) * 32 + lane;
-        const bool act = i < inner;
-        const uint64_t r0 = p * plen < len ? p * plen : len;
-        const uint64_t r1 = r0 + plen < len ? r0 + plen : len;
-#pragma unroll
-        for (int j = 0; j < D; ++j) col[j * 32] = 0;
-        uint32_t flags = 0;
-        if (act) {
+    {
             const typename L::T* q = x + (ob * len + r0) * inner + i;
             const typename L::T* qw = q;                       // window start (rows rw..r)
             uint64_t r = r0, rw = r0;
@@ -147,6 +135,33 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
                 column_add(col, c, one);
             }
             close_window();
+    }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(STR_WARPS * 32, 1)
+k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner,
+              uint32_t parts, StrOut o, int64_t* __restrict__ work, uint32_t* __restrict__ wflags, uint32_t one,
+              uint32_t mone) {
+    using L = StrLd<DT>;
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t gpr = (inner + 31) / 32;                    // warps per outer row
+    const uint64_t items = outer * gpr * parts;
+    const uint64_t plen = (len + parts - 1) / parts;           // rows per part
+    const uint64_t F = outer * inner;
+    for (uint64_t it = (uint64_t)blockIdx.x * STR_WARPS + warp; it < items; it += (uint64_t)gridDim.x * STR_WARPS) {
+        const uint64_t p = it / (items / parts), grp = it % (items / parts);   // neighbouring warps: neighbouring fibres
+        const uint64_t ob = grp / gpr, i = (grp % gpr) * 32 + lane;
+        const bool act = i < inner;
+        const uint64_t r0 = p * plen < len ? p * plen : len;
+        const uint64_t r1 = r0 + plen < len ? r0 + plen : len;
+#pragma unroll
+        for (int j = 0; j < D; ++j) col[j * 32] = 0;
+        uint32_t flags = 0;
+        if (act) {
+            strided_rows<DT>(x, ob, i, len, inner, r0, r1, col, flags, one, mone);
             const uint64_t f = ob * inner + i;
             if (parts == 1) {
                 lane_store(col, flags, o, f);
@@ -157,6 +172,84 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
             }
         }
     }
+}
+
+// K10s: the same lane-per-fibre reduction, stream-K ordered (round 2). When outer * ceil(inner/32)
+// warp items do not fill the resident warps evenly (c2dim0: 2048 items on 148 x 16 = 2368 slots,
+// 20 SMs idle for the whole launch), every resident warp takes an equal share of the rows of all
+// fibre groups in order, [u0, u1) of outer * ceil(inner/32) * len row units: a warp finishes at most
+// one group it started elsewhere and starts at most one it does not finish. A group summed by one
+// warp is rounded at once; the pieces of a split group add their regularized columns into a
+// per-fibre accumulator (acc[j][f], L2-resident red.add; |digit| stays below 2^55 for the <= len
+// pieces a group can have) and count their rows; the piece whose rows complete the group reads the
+// accumulator back, regularizes and rounds. acc, the flag words and the counters are zero on entry
+// (the launch clears them first).
+template <int DT>
+__global__ void __launch_bounds__(STR_WARPS * 32, 1)
+k_sum_strided_sk(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner,
+                 StrOut o, int64_t* __restrict__ acc, uint32_t* __restrict__ aflags, uint32_t* __restrict__ cnt,
+                 uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t gpr = (inner + 31) / 32;
+    const uint64_t U = outer * gpr * len;                       // row units
+    const uint64_t nw = (uint64_t)gridDim.x * STR_WARPS, w = (uint64_t)blockIdx.x * STR_WARPS + warp;
+    uint64_t u0 = (uint64_t)(((unsigned __int128)U * w) / nw);
+    const uint64_t u1 = (uint64_t)(((unsigned __int128)U * (w + 1)) / nw);
+    const uint64_t F = outer * inner;
+    while (u0 < u1) {
+        const uint64_t grp = u0 / len, r0 = u0 - grp * len;
+        const uint64_t r1 = r0 + (u1 - u0) < len ? r0 + (u1 - u0) : len;
+        const uint64_t ob = grp / gpr, i = (grp % gpr) * 32 + lane;
+        const bool act = i < inner;
+        const uint64_t f = ob * inner + i;
+#pragma unroll
+        for (int j = 0; j < D; ++j) col[j * 32] = 0;
+        uint32_t flags = 0;
+        if (act) strided_rows<DT>(x, ob, i, len, inner, r0, r1, col, flags, one, mone);
+        if (r0 == 0 && r1 == len) {
+            if (act) lane_store(col, flags, o, f);
+        } else {
+            if (act) {
+#pragma unroll 6
+                for (int j = 0; j < D; ++j)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(acc + (uint64_t)j * F + f),
+                              (unsigned long long)col[j * 32]);
+                if (flags) atomicOr(aflags + f, flags);
+            }
+            __threadfence();
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) last = atomicAdd(cnt + grp, (uint32_t)(r1 - r0)) + (uint32_t)(r1 - r0) == (uint32_t)len;
+            last = __shfl_sync(FULL, last, 0);
+            if (last) {                                        // this piece completes the group
+                __threadfence();
+                if (act) {
+#pragma unroll 6
+                    for (int j = 0; j < D; ++j)
+                        col[j * 32] = __ldcg(reinterpret_cast<const long long*>(acc + (uint64_t)j * F + f));
+                    flags = __ldcg(aflags + f);
+                    regularize_column(col);
+                    lane_store(col, flags, o, f);
+                }
+            }
+        }
+        u0 += r1 - r0;
+    }
+}
+
+// Stream-K pays off when the warp items leave resident warp slots idle (a wave-quantization loss
+// above 4%) and len fits the 32-bit row counters; its work: acc [D][F] int64 + flags [F] + counters.
+static bool strided_sk_wanted(uint64_t outer, uint64_t len, uint64_t inner, int num_sms) {
+    const uint64_t items = outer * ((inner + 31) / 32), slots = (uint64_t)num_sms * STR_WARPS;
+    if (items == 0 || len < 64 || len >= (1ull << 31)) return false;
+    const uint64_t waves = (items + slots - 1) / slots;
+    return (double)(waves * slots - items) > 0.04 * (double)(waves * slots);
+}
+static size_t strided_sk_bytes(uint64_t outer, uint64_t inner) {
+    const uint64_t F = outer * inner, groups = outer * ((inner + 31) / 32);
+    return (size_t)F * (D * sizeof(int64_t) + sizeof(uint32_t)) + (size_t)groups * sizeof(uint32_t);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -585,7 +678,10 @@ size_t strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int num_
     uint32_t p = strided_parts(outer, len, inner, num_sms);
     const uint32_t ph = strided_parts_h16(outer, len, inner, num_sms);
     if (ph > p) p = ph;
-    return p > 1 ? (size_t)p * outer * inner * (D * sizeof(int64_t) + sizeof(uint32_t)) : 0;
+    size_t b = p > 1 ? (size_t)p * outer * inner * (D * sizeof(int64_t) + sizeof(uint32_t)) : 0;
+    if (XS_STR_SK && strided_sk_wanted(outer, len, inner, num_sms) && strided_sk_bytes(outer, inner) > b)
+        b = strided_sk_bytes(outer, inner);                     // K10s (binary64, one part)
+    return b;
 }
 
 template <int DT>
@@ -618,7 +714,22 @@ cudaError_t sum_strided(const void* x, int dtype, uint64_t outer, uint64_t len, 
         e = dtype == XSUM_DT_F16 ? launch_strided_h16<FmtF16>(x, outer, len, inner, parts, o, wk, wf, num_sms, s)
                                  : launch_strided_h16<FmtBF16Q>(x, outer, len, inner, parts, o, wk, wf, num_sms, s);
     } else switch (dtype) {
-        case XSUM_DT_F64: e = launch_strided<XSUM_DT_F64>(x, outer, len, inner, parts, o, wk, wf, num_sms, s); break;
+        case XSUM_DT_F64:
+            if (XS_STR_SK && parts == 1 && work && strided_sk_wanted(outer, len, inner, num_sms) &&
+                work_bytes >= strided_sk_bytes(outer, inner)) {
+                const size_t nb = strided_sk_bytes(outer, inner);
+                if ((e = cudaMemsetAsync(work, 0, nb, s))) return e;
+                static unsigned long long done_sk = 0;
+                if ((e = ensure_smem(k_sum_strided_sk<XSUM_DT_F64>, STR_SMEM, done_sk))) return e;
+                int64_t* acc = static_cast<int64_t*>(work);
+                uint32_t* af = reinterpret_cast<uint32_t*>(acc + (size_t)D * F);
+                k_sum_strided_sk<XSUM_DT_F64><<<num_sms, STR_WARPS * 32, STR_SMEM, s>>>(
+                    static_cast<const double*>(x), outer, len, inner, o, acc, af, af + F, 1u, 0xFFFFFFFFu);
+                note_launch();
+                return cudaGetLastError();
+            }
+            e = launch_strided<XSUM_DT_F64>(x, outer, len, inner, parts, o, wk, wf, num_sms, s);
+            break;
         case XSUM_DT_F32:
             e = XS_STRH ? launch_strided_f32<SF32>(x, outer, len, inner, parts, o, wk, wf, num_sms, s)
                         : launch_strided<XSUM_DT_F32>(x, outer, len, inner, parts, o, wk, wf, num_sms, s);

@@ -69,8 +69,7 @@ VARIANTS = {
     "sz_u2nb8": ["-DXS_SZ_U=2", "-DXS_SZ_NB=8"],
     "sz_coh": ["-DXS_SZ_COH=1"],
     "sz_w8": ["-DXS_SZ_WARPS=8", "-DXS_SZ_MINB=2"],
-    "sz_q": ["-DXS_SH_LPS=8"],
-    "sz_q_u4nb4": ["-DXS_SH_LPS=8", "-DXS_SZ_U=4", "-DXS_SZ_NB=4"],
+    "strsk0": ["-DXS_STR_SK=0"],
     "segc_w16": ["-DXS_SEGC_WARPS=16", "-DXS_SEGC_MINB=1"],
     "sseg_w16": ["-DXS_SSEG_WARPS=16", "-DXS_SSEG_MINB=1"],
     "exp_sz_noepi": ["-DXS_EXP_SZ_NOEPI"],

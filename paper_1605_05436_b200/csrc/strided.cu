@@ -241,8 +241,8 @@ k_sum_strided_sk(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, ui
 
 // Stream-K pays off when the warp items leave resident warp slots idle (a wave-quantization loss
 // above 4%) and len fits the 32-bit row counters; its work: acc [D][F] int64 + flags [F] + counters.
-static bool strided_sk_wanted(uint64_t outer, uint64_t len, uint64_t inner, int num_sms) {
-    const uint64_t items = outer * ((inner + 31) / 32), slots = (uint64_t)num_sms * STR_WARPS;
+static bool strided_sk_wanted(uint64_t outer, uint64_t len, uint64_t inner, int num_sms, uint64_t fpw = 32) {
+    const uint64_t items = outer * ((inner + fpw - 1) / fpw), slots = (uint64_t)num_sms * STR_WARPS;
     if (items == 0 || len < 64 || len >= (1ull << 31)) return false;
     const uint64_t waves = (items + slots - 1) / slots;
     return (double)(waves * slots - items) > 0.04 * (double)(waves * slots);
@@ -250,6 +250,45 @@ static bool strided_sk_wanted(uint64_t outer, uint64_t len, uint64_t inner, int 
 static size_t strided_sk_bytes(uint64_t outer, uint64_t inner) {
     const uint64_t F = outer * inner, groups = outer * ((inner + 31) / 32);
     return (size_t)F * (D * sizeof(int64_t) + sizeof(uint32_t)) + (size_t)groups * sizeof(uint32_t);
+}
+
+// K10s bookkeeping shared by the narrow-format kernels: a piece's rows join its group's count after
+// its accumulator adds (fence first); true on every lane for the piece that completes the group.
+__device__ __forceinline__ bool sk_piece_done(uint32_t* cnt, uint64_t rows, uint64_t len, int lane) {
+    __threadfence();
+    __syncwarp();
+    uint32_t last = 0;
+    if (lane == 0) last = atomicAdd(cnt, (uint32_t)rows) + (uint32_t)rows == (uint32_t)len;
+    last = __shfl_sync(FULL, last, 0);
+    if (last) __threadfence();
+    return last != 0;
+}
+// The item loop: SK = stream-K (every resident warp an equal share of groups x len row units, in
+// order; whole groups mode 0, pieces mode 2), else (part, group) items (mode 0 for one part, 1 for
+// a part of several).
+template <bool SK, int WARPS, class Fn>
+__device__ __forceinline__ void sk_or_parts(uint64_t groups, uint64_t len, uint32_t parts, uint64_t plen,
+                                            uint64_t items, int lane, int warp, Fn&& range) {
+    (void)lane;
+    if constexpr (SK) {
+        const uint64_t U = groups * len;
+        const uint64_t nw = (uint64_t)gridDim.x * WARPS, w = (uint64_t)blockIdx.x * WARPS + warp;
+        uint64_t u0 = (uint64_t)(((unsigned __int128)U * w) / nw);
+        const uint64_t u1 = (uint64_t)(((unsigned __int128)U * (w + 1)) / nw);
+        while (u0 < u1) {
+            const uint64_t grp = u0 / len, r0 = u0 - grp * len;
+            const uint64_t r1 = r0 + (u1 - u0) < len ? r0 + (u1 - u0) : len;
+            range(grp, r0, r1, 0, (r0 == 0 && r1 == len) ? 0 : 2);
+            u0 += r1 - r0;
+        }
+    } else {
+    for (uint64_t it = (uint64_t)blockIdx.x * WARPS + warp; it < items; it += (uint64_t)gridDim.x * WARPS) {
+        const uint64_t p = it / (items / parts), grp = it % (items / parts);   // neighbouring warps: neighbouring fibres
+        const uint64_t r0 = p * plen < len ? p * plen : len;
+        const uint64_t r1 = r0 + plen < len ? r0 + plen : len;
+        range(grp, r0, r1, p, parts == 1 ? 0 : 1);
+    }
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -417,6 +456,148 @@ k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, 
     }
 }
 
+// K10s for K10h: the kernel above as stream-K pieces (sk_or_parts<true>: modes 0 and 2 only)
+template <class F>
+__global__ void __launch_bounds__(STRH_WARPS * 32, 1)
+k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,
+                  StrOut o, int64_t* __restrict__ work, uint32_t* __restrict__ wflags, uint32_t* __restrict__ cnt,
+                  uint32_t one, uint32_t mone) {
+    using C = H16Col<F>;
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* const colw = win + warp * (2 * C::COLS * 32);
+    int64_t* col[2] = {colw + lane, colw + C::COLS * 32 + lane};
+    uint32_t* const binw = reinterpret_cast<uint32_t*>(win + STRH_WARPS * 2 * C::COLS * 32) + warp * (2 * F::NBIN * 32);
+    uint32_t* bins[2] = {binw + lane, binw + F::NBIN * 32 + lane};
+    const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(bins[0]);
+    const uint32_t sb1 = (uint32_t)__cvta_generic_to_shared(bins[1]);
+    const uint32_t sb2 = sb0 + (sb1 << 16);                     // low half -> fibre i, high half -> i + 1
+    constexpr uint32_t WIN = (uint32_t)(F::FLUSH / STRH_UNR) * STRH_UNR;   // rows per bin window
+    const uint64_t gpr = (inner + 63) / 64;
+    const uint64_t items = outer * gpr * parts;
+    const uint64_t plen = (len + parts - 1) / parts;
+    const uint64_t Fn = outer * inner;
+    const uint64_t wstride = inner / 2;                           // 32-bit words per row
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int j = 0; j < C::COLS; ++j) col[h][j * 32] = 0;
+#pragma unroll
+        for (int j = 0; j < F::NBIN; ++j) bins[h][j * 32] = 0;
+    }
+    // mode 0: whole fibres (round and store); 1: a row part -> work[p]; 2: a stream-K piece (K10s).
+    // (the pointer arrays by copy: a by-reference capture put them in local memory, 230 B of spills)
+    auto range = [&, col, bins](uint64_t grp, uint64_t r0, uint64_t r1, uint64_t p, int mode) {
+        const uint64_t ob = grp / gpr, i = (grp % gpr) * 64 + 2 * (uint64_t)lane;
+        const bool act = i < inner;                                // inner is even: both fibres or none
+        bool special = false;
+        uint32_t flushes = 0;
+        if (act) {
+            const uint32_t* q = reinterpret_cast<const uint32_t*>(x + (ob * len + r0) * inner + i);
+            const uint64_t ngroups = (r1 - r0) / STRH_UNR;
+            uint32_t buf[STRH_NB][STRH_UNR];
+            const uint32_t* lq = q;
+            uint64_t lg = 0;
+#pragma unroll
+            for (int b = 0; b < STRH_NB - 1; ++b) {
+                if (lg < ngroups) {
+#pragma unroll
+                    for (int u = 0; u < STRH_UNR; ++u) buf[b][u] = __ldcs(lq + u * wstride);
+                    lq += STRH_UNR * wstride;
+                    ++lg;
+                }
+            }
+            uint32_t since = 0;
+            for (uint64_t g = 0; g < ngroups;) {
+#pragma unroll
+                for (int b = 0; b < STRH_NB; ++b) {
+                    if (g >= ngroups) break;
+                    if (lg < ngroups) {
+#pragma unroll
+                        for (int u = 0; u < STRH_UNR; ++u)
+                            buf[(b + STRH_NB - 1) % STRH_NB][u] = __ldcs(lq + u * wstride);
+                        lq += STRH_UNR * wstride;
+                        ++lg;
+                    }
+#pragma unroll
+                    for (int u = 0; u < STRH_UNR; ++u) h16_add_word<F>(sb1, sb2, buf[b][u], one, mone);
+                    ++g;
+                    since += STRH_UNR;
+                    if (since == WIN) {                          // bin window full: empty into the columns
+                        special |= h16_flush_col<F>(bins[0], col[0]);
+                        special |= h16_flush_col<F>(bins[1], col[1]);
+                        since = 0;
+                        if (++flushes == C::REG_FLUSHES) {
+                            h16_col_regularize<F>(col[0]);
+                            h16_col_regularize<F>(col[1]);
+                            flushes = 0;
+                        }
+                    }
+                }
+            }
+            for (uint64_t r = r0 + ngroups * STRH_UNR; r < r1; ++r) {   // < STRH_UNR rows left: in the window
+                h16_add_word<F>(sb1, sb2, __ldcs(q + (r - r0) * wstride), one, mone);
+            }
+            special |= h16_flush_col<F>(bins[0], col[0]);
+            special |= h16_flush_col<F>(bins[1], col[1]);
+        }
+        uint32_t fl[2] = {0, 0};
+        if (special) {                                             // rare: classify this lane's fibres
+            const uint16_t* q16 = x + (ob * len + r0) * inner + i;
+            fl[0] = strh_classify<F>(q16, r1 - r0, inner);
+            fl[1] = strh_classify<F>(q16 + 1, r1 - r0, inner);
+        }
+        if (mode == 2) {                                           // stream-K piece: add into acc[r][f]
+            if (act) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t f = ob * inner + i + h;
+                    h16_col_regularize<F>(col[h]);
+                    for (int r = 0; r < C::COLS; ++r) {
+                        atomicAdd(reinterpret_cast<unsigned long long*>(work + (uint64_t)r * Fn + f),
+                                  (unsigned long long)col[h][r * 32]);
+                        col[h][r * 32] = 0;
+                    }
+                    if (fl[h]) atomicOr(wflags + f, fl[h]);
+                }
+            }
+            if (!sk_piece_done(cnt + grp, r1 - r0, len, lane)) return;
+            if (act) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t f = ob * inner + i + h;
+                    for (int r = 0; r < C::COLS; ++r)
+                        col[h][r * 32] = __ldcg(reinterpret_cast<const long long*>(work + (uint64_t)r * Fn + f));
+                    fl[h] = __ldcg(wflags + f);
+                }
+            }
+            mode = 0;
+        }
+        if (act) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint64_t f = ob * inner + i + h;
+                if (mode == 0) {
+                    strh_store<F>(col[h], fl[h], o, f);
+                } else {                                  // partial -> work[p][j][f], 42 digits
+                    h16_col_regularize<F>(col[h]);
+                    for (int j = 0; j < D; ++j) {
+                        const int r = j - C::COL0;
+                        int64_t v = 0;
+                        if (r >= 0 && r < C::COLS) {
+                            v = col[h][r * 32];
+                            col[h][r * 32] = 0;
+                        }
+                        work[(p * D + j) * Fn + f] = v;
+                    }
+                    wflags[p * Fn + f] = fl[h];
+                }
+            }
+        }
+    };
+    sk_or_parts<true, STRH_WARPS>(outer * gpr, len, parts, plen, items, lane, warp, range);
+}
+
 // ---------------------------------------------------------------------------------------------
 // K10f: binary32 strided reductions with K9's 64-bit exponent-group bins (f32_bins.cuh): one 64-bit
 // read-modify-write per element instead of K10's two (the element's two 52-bit digit chunks),
@@ -549,30 +730,165 @@ k_sum_strided_f32(const uint32_t* __restrict__ x, uint64_t outer, uint64_t len, 
     }
 }
 
+// K10s for K10f: the kernel above as stream-K pieces (sk_or_parts<true>: modes 0 and 2 only)
+template <class F>
+__global__ void __launch_bounds__(STR_WARPS * 32, 1)
+k_sum_strided_f32_sk(const uint32_t* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,
+                  StrOut o, int64_t* __restrict__ work, uint32_t* __restrict__ wflags, uint32_t* __restrict__ cnt,
+                  uint32_t one) {
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (F::COLS * 32) + lane;
+    uint64_t* bins = reinterpret_cast<uint64_t*>(win + STR_WARPS * F::COLS * 32) + warp * (F::NBIN * 32) + lane;
+    constexpr uint32_t WIN = (uint32_t)(SSEG_FLUSH / STRH_UNR) * STRH_UNR;    // rows per bin window
+    const uint64_t gpr = (inner + 31) / 32;
+    const uint64_t items = outer * gpr * parts;
+    const uint64_t plen = (len + parts - 1) / parts;
+    const uint64_t Fn = outer * inner;
+#pragma unroll
+    for (int j = 0; j < F::COLS; ++j) col[j * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < F::NBIN; ++j) bins[j * 32] = 0;
+    // mode 0: the whole fibre (round and store); 1: a row part -> work[p]; 2: a stream-K piece (K10s)
+    auto range = [&](uint64_t grp, uint64_t r0, uint64_t r1, uint64_t p, int mode) {
+        const uint64_t ob = grp / gpr, i = (grp % gpr) * 32 + lane;
+        const bool act = i < inner;
+        uint32_t flags = 0;
+        if (act) {
+            const uint32_t* q = x + (ob * len + r0) * inner + i;
+            const uint64_t ngroups = (r1 - r0) / STRH_UNR;
+            uint32_t buf[STRH_NB][STRH_UNR];
+            const uint32_t* lq = q;
+            uint64_t lg = 0;
+            uint32_t spec = 0, since = 0, flushes = 0;
+#pragma unroll
+            for (int b = 0; b < STRH_NB - 1; ++b) {
+                if (lg < ngroups) {
+#pragma unroll
+                    for (int u = 0; u < STRH_UNR; ++u) buf[b][u] = __ldcs(lq + u * inner);
+                    lq += STRH_UNR * inner;
+                    ++lg;
+                }
+            }
+            for (uint64_t g = 0; g < ngroups;) {
+#pragma unroll
+                for (int b = 0; b < STRH_NB; ++b) {
+                    if (g >= ngroups) break;
+                    if (lg < ngroups) {
+#pragma unroll
+                        for (int u = 0; u < STRH_UNR; ++u) buf[(b + STRH_NB - 1) % STRH_NB][u] = __ldcs(lq + u * inner);
+                        lq += STRH_UNR * inner;
+                        ++lg;
+                    }
+#pragma unroll
+                    for (int u = 0; u < STRH_UNR; ++u) sbin_add<F>(bins, buf[b][u], spec, one);
+                    ++g;
+                    since += STRH_UNR;
+                    if (since == WIN) {
+                        sbin_flush<F>(bins, col);
+                        since = 0;
+                        if (++flushes == SSEG_REG_FLUSHES) { scol_regularize<F>(col); flushes = 0; }
+                    }
+                }
+            }
+            for (uint64_t r = r0 + ngroups * STRH_UNR; r < r1; ++r) sbin_add<F>(bins, __ldcs(q + (r - r0) * inner), spec, one);
+            sbin_flush<F>(bins, col);
+            if (spec == F::EM) strf_rescan<F>(bins, col, q, r1 - r0, inner, flags, one);   // rare
+        }
+        const uint64_t f = ob * inner + i;
+        if (mode == 2) {                                         // stream-K piece: add into acc[r][f]
+            if (act) {
+                scol_regularize<F>(col);
+                for (int r = 0; r < F::COLS; ++r) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(work + (uint64_t)r * Fn + f),
+                              (unsigned long long)col[r * 32]);
+                    col[r * 32] = 0;
+                }
+                if (flags) atomicOr(wflags + f, flags);
+            }
+            if (!sk_piece_done(cnt + grp, r1 - r0, len, lane)) return;
+            if (act) {
+                for (int r = 0; r < F::COLS; ++r) col[r * 32] = __ldcg(reinterpret_cast<const long long*>(work + (uint64_t)r * Fn + f));
+                flags = __ldcg(wflags + f);
+            }
+            mode = 0;
+        }
+        if (act) {
+            if (mode == 0) {
+                LaneTop t = lane_top_chain<32>(col, 0, F::COLS - 1);    // zeroes the column
+                if (t.m >= 0) t.m += F::COL0;
+                uint32_t rf = 0;
+                uint64_t b64 = o.out64 ? lane_round(t, 53, 0, 2047, true, rf) : 0;
+                uint32_t b32 = o.out32 ? (uint32_t)lane_round(t, 24, 925, 255, false, rf) : 0;
+                const uint32_t fl = (flags & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF)) | rf;
+                if ((fl & XSUM_F_NAN) || ((fl & XSUM_F_PINF) && (fl & XSUM_F_NINF))) {
+                    b64 = 0x7FF8000000000000ull; b32 = 0x7FC00000u;
+                } else if (fl & XSUM_F_PINF) {
+                    b64 = 0x7FF0000000000000ull; b32 = 0x7F800000u;
+                } else if (fl & XSUM_F_NINF) {
+                    b64 = 0xFFF0000000000000ull; b32 = 0xFF800000u;
+                }
+                if (o.out64) o.out64[f] = __longlong_as_double((long long)b64);
+                if (o.out32) o.out32[f] = __uint_as_float(b32);
+                if (o.flags) o.flags[f] = fl;
+            } else {                                    // partial -> work[p][j][f], 42 digits
+                scol_regularize<F>(col);
+                for (int j = 0; j < D; ++j) {
+                    const int r = j - F::COL0;
+                    int64_t v = 0;
+                    if (r >= 0 && r < F::COLS) {
+                        v = col[r * 32];
+                        col[r * 32] = 0;
+                    }
+                    work[(p * D + j) * Fn + f] = v;
+                }
+                wflags[p * Fn + f] = flags;
+            }
+        }
+    };
+    sk_or_parts<true, STR_WARPS>(outer * gpr, len, parts, plen, items, lane, warp, range);
+}
+
+// sk: K10s (stream-K pieces meeting in work = acc [COLS][F], wflags [F], cnt [groups], cleared by the
+// caller); else row parts (parts == 1: one item per fibre group).
 template <class F>
 static cudaError_t launch_strided_f32(const void* x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,
-                                      const StrOut& o, int64_t* work, uint32_t* wflags, int num_sms, cudaStream_t s) {
-    static unsigned long long done = 0;
+                                      const StrOut& o, int64_t* work, uint32_t* wflags, uint32_t* cnt, bool sk,
+                                      int num_sms, cudaStream_t s) {
+    static unsigned long long done = 0, done_sk = 0;
     if (cudaError_t e = ensure_smem(k_sum_strided_f32<F>, strf_smem<F>(), done)) return e;
+    if (cudaError_t e = ensure_smem(k_sum_strided_f32_sk<F>, strf_smem<F>(), done_sk)) return e;
     const uint64_t items = outer * ((inner + 31) / 32) * parts;
     const uint64_t want = (items + STR_WARPS - 1) / STR_WARPS;
-    const unsigned g = (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
-    k_sum_strided_f32<F><<<g, STR_WARPS * 32, strf_smem<F>(), s>>>(static_cast<const uint32_t*>(x), outer, len, inner,
-                                                                   parts, o, work, wflags, 1u);
+    const unsigned g = sk ? (unsigned)num_sms : (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
+    if (sk)
+        k_sum_strided_f32_sk<F><<<g, STR_WARPS * 32, strf_smem<F>(), s>>>(static_cast<const uint32_t*>(x), outer, len,
+                                                                          inner, 1, o, work, wflags, cnt, 1u);
+    else
+        k_sum_strided_f32<F><<<g, STR_WARPS * 32, strf_smem<F>(), s>>>(static_cast<const uint32_t*>(x), outer, len,
+                                                                       inner, parts, o, work, wflags, 1u);
     note_launch();
     return cudaGetLastError();
 }
 
 template <class F>
 static cudaError_t launch_strided_h16(const void* x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,
-                                      const StrOut& o, int64_t* work, uint32_t* wflags, int num_sms, cudaStream_t s) {
-    static unsigned long long done = 0;
+                                      const StrOut& o, int64_t* work, uint32_t* wflags, uint32_t* cnt, bool sk,
+                                      int num_sms, cudaStream_t s) {
+    static unsigned long long done = 0, done_sk = 0;
     if (cudaError_t e = ensure_smem(k_sum_strided_h16<F>, strh_smem<F>(), done)) return e;
+    if (cudaError_t e = ensure_smem(k_sum_strided_h16_sk<F>, strh_smem<F>(), done_sk)) return e;
     const uint64_t items = outer * ((inner + 63) / 64) * parts;
     const uint64_t want = (items + STRH_WARPS - 1) / STRH_WARPS;
-    const unsigned g = (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
-    k_sum_strided_h16<F><<<g, STRH_WARPS * 32, strh_smem<F>(), s>>>(static_cast<const uint16_t*>(x), outer, len, inner,
-                                                                    parts, o, work, wflags, 1u, 0xFFFFFFFFu);
+    const unsigned g = sk ? (unsigned)num_sms : (unsigned)(want < (uint64_t)num_sms ? want : num_sms);
+    if (sk)
+        k_sum_strided_h16_sk<F><<<g, STRH_WARPS * 32, strh_smem<F>(), s>>>(static_cast<const uint16_t*>(x), outer,
+                                                                           len, inner, 1, o, work, wflags, cnt, 1u,
+                                                                           0xFFFFFFFFu);
+    else
+        k_sum_strided_h16<F><<<g, STRH_WARPS * 32, strh_smem<F>(), s>>>(static_cast<const uint16_t*>(x), outer, len,
+                                                                        inner, parts, o, work, wflags, 1u,
+                                                                        0xFFFFFFFFu);
     note_launch();
     return cudaGetLastError();
 }
@@ -679,8 +995,9 @@ size_t strided_work_bytes(uint64_t outer, uint64_t len, uint64_t inner, int num_
     const uint32_t ph = strided_parts_h16(outer, len, inner, num_sms);
     if (ph > p) p = ph;
     size_t b = p > 1 ? (size_t)p * outer * inner * (D * sizeof(int64_t) + sizeof(uint32_t)) : 0;
-    if (XS_STR_SK && strided_sk_wanted(outer, len, inner, num_sms) && strided_sk_bytes(outer, inner) > b)
-        b = strided_sk_bytes(outer, inner);                     // K10s (binary64, one part)
+    if (XS_STR_SK && (strided_sk_wanted(outer, len, inner, num_sms) || strided_sk_wanted(outer, len, inner, num_sms, 64)) &&
+        strided_sk_bytes(outer, inner) > b)
+        b = strided_sk_bytes(outer, inner);                     // K10s
     return b;
 }
 
@@ -707,12 +1024,29 @@ cudaError_t sum_strided(const void* x, int dtype, uint64_t outer, uint64_t len, 
     uint32_t parts = h16 ? strided_parts_h16(outer, len, inner, num_sms) : strided_parts(outer, len, inner, num_sms);
     if (parts > 1 && (!work || work_bytes < strided_work_bytes(outer, len, inner, num_sms))) parts = 1;
     const uint64_t F = outer * inner;
+    // K10s for the narrow formats (K10h / K10f) whenever their items fill the resident warps unevenly
+    const bool narrow = h16 || (dtype == XSUM_DT_F32 && XS_STRH);
+    const bool skn = XS_STR_SK && narrow && work && strided_sk_wanted(outer, len, inner, num_sms, h16 ? 64 : 32) &&
+                     work_bytes >= strided_sk_bytes(outer, inner);
+    if (skn) parts = 1;
     int64_t* wk = parts > 1 ? static_cast<int64_t*>(work) : nullptr;
     uint32_t* wf = parts > 1 ? reinterpret_cast<uint32_t*>(wk + (size_t)parts * D * F) : nullptr;
+    uint32_t* cnt = nullptr;
     cudaError_t e;
+    if (skn) {
+        const size_t nb = strided_sk_bytes(outer, inner);
+        if ((e = cudaMemsetAsync(work, 0, nb, s))) return e;
+        wk = static_cast<int64_t*>(work);
+        wf = reinterpret_cast<uint32_t*>(wk + (size_t)D * F);
+        cnt = wf + F;
+    }
     if (h16) {
-        e = dtype == XSUM_DT_F16 ? launch_strided_h16<FmtF16>(x, outer, len, inner, parts, o, wk, wf, num_sms, s)
-                                 : launch_strided_h16<FmtBF16Q>(x, outer, len, inner, parts, o, wk, wf, num_sms, s);
+        e = dtype == XSUM_DT_F16
+                ? launch_strided_h16<FmtF16>(x, outer, len, inner, parts, o, wk, wf, cnt, skn, num_sms, s)
+                : launch_strided_h16<FmtBF16Q>(x, outer, len, inner, parts, o, wk, wf, cnt, skn, num_sms, s);
+        if (skn) return e;
+    } else if (skn) {
+        return launch_strided_f32<SF32>(x, outer, len, inner, parts, o, wk, wf, cnt, true, num_sms, s);
     } else switch (dtype) {
         case XSUM_DT_F64:
             if (XS_STR_SK && parts == 1 && work && strided_sk_wanted(outer, len, inner, num_sms) &&
@@ -731,7 +1065,7 @@ cudaError_t sum_strided(const void* x, int dtype, uint64_t outer, uint64_t len, 
             e = launch_strided<XSUM_DT_F64>(x, outer, len, inner, parts, o, wk, wf, num_sms, s);
             break;
         case XSUM_DT_F32:
-            e = XS_STRH ? launch_strided_f32<SF32>(x, outer, len, inner, parts, o, wk, wf, num_sms, s)
+            e = XS_STRH ? launch_strided_f32<SF32>(x, outer, len, inner, parts, o, wk, wf, nullptr, false, num_sms, s)
                         : launch_strided<XSUM_DT_F32>(x, outer, len, inner, parts, o, wk, wf, num_sms, s);
             break;
         case XSUM_DT_F16: e = launch_strided<XSUM_DT_F16>(x, outer, len, inner, parts, o, wk, wf, num_sms, s); break;

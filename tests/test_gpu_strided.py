@@ -265,15 +265,16 @@ def test_strided_split_many_fibres(xs, fmt):
     assert (got == (b64 if fmt == "f64" else b32)).all()
 
 
+@pytest.mark.parametrize("fmt", ["f64", "f32", "f16", "bf16"])
 @pytest.mark.parametrize("outer,length,inner", [(1, 2048, 4096), (3, 777, 1000), (1, 100_003, 32)])
-def test_strided_stream_k(xs, outer, length, inner):
-    """K10s (binary64, fibre groups that fill the resident warps unevenly): every warp takes an equal
-    share of all rows, so fibres are split across 1-3 warps (or, for few long fibres, across many)
-    whose pieces meet in the per-fibre accumulator; NaN / Inf planted in split fibres. Every fibre
-    vs the oracle, and the same bits without a work buffer (the plain per-fibre kernel)."""
-    b = patterns("f64", outer * length * inner, 31 + length)
-    v64, v32, f, wb = check(xs, "f64", b, outer, length, inner, work=True)
+def test_strided_stream_k(xs, fmt, outer, length, inner):
+    """K10s (fibre groups that fill the resident warps unevenly; K10 / K10f / K10h pieces): every warp
+    takes an equal share of all rows, so fibres are split across 1-3 warps (or, for few long fibres,
+    across many) whose pieces meet in the per-fibre accumulator; NaN / Inf planted in split fibres.
+    Every fibre vs the oracle, and the same bits without a work buffer (the plain per-fibre kernel)."""
+    b = patterns(fmt, outer * length * inner, 31 + length)
+    v64, v32, f, wb = check(xs, fmt, b, outer, length, inner, work=True)
     assert wb > 0
-    u64, u32, g, _ = check(xs, "f64", b, outer, length, inner, work=False,
+    u64, u32, g, _ = check(xs, fmt, b, outer, length, inner, work=False,
                            sample=list(range(0, outer * inner, 97)))
     assert (v64 == u64).all() and (v32 == u32).all() and (f == g).all()

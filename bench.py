@@ -702,7 +702,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "kernel": {"c2f32": "k_accumulate_f32b", "c2f16": "k_accumulate_h16",
                                     "c2bf16": "k_accumulate_h16", "c5": "k_segments_halfz",
                                     "c5csr": "k_segments", "c5s16": "k_segments_lanes64s",
-                                    "c2dim0": "k_sum_strided", "c2cs": "xsum_sum_condsens step (all passes)",
+                                    "c2dim0": "k_sum_strided_sk", "c2cs": "xsum_sum_condsens step (all passes)",
                                     "c3cs": "xsum_sum_condsens step (all passes)"}.get(args.config, "k_accumulate"),
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peak_src, "read_probe_gbs": probe_gbs,

@@ -41,22 +41,21 @@ __device__ __noinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_
 // a column that was regularized inside the segment (long segments only) may hold carries up to
 // digit D-1, so rows 32..41 are read when top = max over the warp of those bounds reaches 32
 // (c5csr's exponents reach digit 25: one row per lane). The rest of the column is zero.
-__device__ __forceinline__ void segment_epilogue_top(const int64_t* wb, int64_t* su, uint32_t flags, int top,
+__device__ __forceinline__ void segment_epilogue_top(int64_t* wb, int64_t* su, uint32_t flags, int top,
                                                      uint64_t len, uint64_t s, const SegOut& o, int lane) {
     __syncwarp();
-    int64_t* wz = const_cast<int64_t*>(wb);
     LaneSums t = {0, 0, 0, 0};
     const bool hi_rows = top >= 32;                  // warp-uniform
 #pragma unroll 8
     for (int c = 0; c < 32; ++c) {
         const int cc = (lane + c) & 31;              // rotated: conflict-free columns
         const int64_t v0 = wb[lane * 32 + cc];
-        wz[lane * 32 + cc] = 0;
+        wb[lane * 32 + cc] = 0;
         t.hs0 += v0 >> 32;
         t.ls0 += (int64_t)(uint32_t)v0;
         if (hi_rows && lane + 32 < D) {
             const int64_t v1 = wb[(lane + 32) * 32 + cc];
-            wz[(lane + 32) * 32 + cc] = 0;
+            wb[(lane + 32) * 32 + cc] = 0;
             t.hs1 += v1 >> 32;
             t.ls1 += (int64_t)(uint32_t)v1;
         }

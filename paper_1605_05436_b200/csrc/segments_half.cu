@@ -433,7 +433,7 @@ __device__ __noinline__ void halfz_rescan(int64_t* col, const uint4* seg, uint64
 template <int NK>
 __device__ __forceinline__ void halfz_epilogue(int64_t* wb, const SegOut& o, int64_t* su, uint64_t* sink, uint64_t ps,
                                                uint64_t pp, uint64_t nseg, uint64_t seg_len, uint32_t flags, int base,
-                                               int dlo, int dhi, int hl, int half) {
+                                               int dhi, int hl, int half) {
     __syncwarp();
     HalfSums d;
 #pragma unroll
@@ -568,13 +568,13 @@ k_segments_halfz(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
             nk = o.canon || nk > KD ? KD : nk;
             if (nk == 1)                                       // warp-uniform
                 halfz_epilogue<1>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
-                                  flags, base, dlo, dhi, hl, half);
+                                  flags, base, dhi, hl, half);
             else if (LPS < 16 && nk == 2)                      // quarter warps: c5's band is two groups
                 halfz_epilogue<2>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
-                                  flags, base, dlo, dhi, hl, half);
+                                  flags, base, dhi, hl, half);
             else
                 halfz_epilogue<KD>(winz + warp * (D * 32), o, su[warp][half], canon_sink[warp], ps, pp, nseg, seg_len,
-                                   flags, base, dlo, dhi, hl, half);
+                                   flags, base, dhi, hl, half);
             band = 0;
             pt = 0;
             pp += nw;

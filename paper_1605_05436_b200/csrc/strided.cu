@@ -174,85 +174,7 @@ k_sum_strided(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint6
     }
 }
 
-// K10s: the same lane-per-fibre reduction, stream-K ordered (round 2). When outer * ceil(inner/32)
-// warp items do not fill the resident warps evenly (c2dim0: 2048 items on 148 x 16 = 2368 slots,
-// 20 SMs idle for the whole launch), every resident warp takes an equal share of the rows of all
-// fibre groups in order, [u0, u1) of outer * ceil(inner/32) * len row units: a warp finishes at most
-// one group it started elsewhere and starts at most one it does not finish. A group summed by one
-// warp is rounded at once; the pieces of a split group add their regularized columns into a
-// per-fibre accumulator (acc[j][f], L2-resident red.add; |digit| stays below 2^55 for the <= len
-// pieces a group can have) and count their rows; the piece whose rows complete the group reads the
-// accumulator back, regularizes and rounds. acc, the flag words and the counters are zero on entry
-// (the launch clears them first).
-template <int DT>
-__global__ void __launch_bounds__(STR_WARPS * 32, 1)
-k_sum_strided_sk(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner,
-                 StrOut o, int64_t* __restrict__ acc, uint32_t* __restrict__ aflags, uint32_t* __restrict__ cnt,
-                 uint32_t one, uint32_t mone) {
-    extern __shared__ __align__(16) int64_t win[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t* col = win + warp * (D * 32) + lane;
-    const uint64_t gpr = (inner + 31) / 32;
-    const uint64_t U = outer * gpr * len;                       // row units
-    const uint64_t nw = (uint64_t)gridDim.x * STR_WARPS, w = (uint64_t)blockIdx.x * STR_WARPS + warp;
-    uint64_t u0 = (uint64_t)(((unsigned __int128)U * w) / nw);
-    const uint64_t u1 = (uint64_t)(((unsigned __int128)U * (w + 1)) / nw);
-    const uint64_t F = outer * inner;
-    while (u0 < u1) {
-        const uint64_t grp = u0 / len, r0 = u0 - grp * len;
-        const uint64_t r1 = r0 + (u1 - u0) < len ? r0 + (u1 - u0) : len;
-        const uint64_t ob = grp / gpr, i = (grp % gpr) * 32 + lane;
-        const bool act = i < inner;
-        const uint64_t f = ob * inner + i;
-#pragma unroll
-        for (int j = 0; j < D; ++j) col[j * 32] = 0;
-        uint32_t flags = 0;
-        if (act) strided_rows<DT>(x, ob, i, len, inner, r0, r1, col, flags, one, mone);
-        if (r0 == 0 && r1 == len) {
-            if (act) lane_store(col, flags, o, f);
-        } else {
-            if (act) {
-#pragma unroll 6
-                for (int j = 0; j < D; ++j)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(acc + (uint64_t)j * F + f),
-                              (unsigned long long)col[j * 32]);
-                if (flags) atomicOr(aflags + f, flags);
-            }
-            __threadfence();
-            __syncwarp();
-            uint32_t last = 0;
-            if (lane == 0) last = atomicAdd(cnt + grp, (uint32_t)(r1 - r0)) + (uint32_t)(r1 - r0) == (uint32_t)len;
-            last = __shfl_sync(FULL, last, 0);
-            if (last) {                                        // this piece completes the group
-                __threadfence();
-                if (act) {
-#pragma unroll 6
-                    for (int j = 0; j < D; ++j)
-                        col[j * 32] = __ldcg(reinterpret_cast<const long long*>(acc + (uint64_t)j * F + f));
-                    flags = __ldcg(aflags + f);
-                    regularize_column(col);
-                    lane_store(col, flags, o, f);
-                }
-            }
-        }
-        u0 += r1 - r0;
-    }
-}
-
-// Stream-K pays off when the warp items leave resident warp slots idle (a wave-quantization loss
-// above 4%) and len fits the 32-bit row counters; its work: acc [D][F] int64 + flags [F] + counters.
-static bool strided_sk_wanted(uint64_t outer, uint64_t len, uint64_t inner, int num_sms, uint64_t fpw = 32) {
-    const uint64_t items = outer * ((inner + fpw - 1) / fpw), slots = (uint64_t)num_sms * STR_WARPS;
-    if (items == 0 || len < 64 || len >= (1ull << 31)) return false;
-    const uint64_t waves = (items + slots - 1) / slots;
-    return (double)(waves * slots - items) > 0.04 * (double)(waves * slots);
-}
-static size_t strided_sk_bytes(uint64_t outer, uint64_t inner) {
-    const uint64_t F = outer * inner, groups = outer * ((inner + 31) / 32);
-    return (size_t)F * (D * sizeof(int64_t) + sizeof(uint32_t)) + (size_t)groups * sizeof(uint32_t);
-}
-
-// K10s bookkeeping shared by the narrow-format kernels: a piece's rows join its group's count after
+// K10s bookkeeping (K10s and its narrow-format kernels): a piece's rows join its group's count after
 // its accumulator adds (fence first); true on every lane for the piece that completes the group.
 __device__ __forceinline__ bool sk_piece_done(uint32_t* cnt, uint64_t rows, uint64_t len, int lane) {
     __threadfence();
@@ -289,6 +211,69 @@ __device__ __forceinline__ void sk_or_parts(uint64_t groups, uint64_t len, uint3
         range(grp, r0, r1, p, parts == 1 ? 0 : 1);
     }
     }
+}
+
+// K10s: the same lane-per-fibre reduction, stream-K ordered (round 2). When outer * ceil(inner/32)
+// warp items do not fill the resident warps evenly (c2dim0: 2048 items on 148 x 16 = 2368 slots,
+// 20 SMs idle for the whole launch), every resident warp takes an equal share of the rows of all
+// fibre groups in order, [u0, u1) of outer * ceil(inner/32) * len row units: a warp finishes at most
+// one group it started elsewhere and starts at most one it does not finish. A group summed by one
+// warp is rounded at once; the pieces of a split group add their regularized columns into a
+// per-fibre accumulator (acc[j][f], L2-resident red.add; |digit| stays below 2^55 for the <= len
+// pieces a group can have) and count their rows; the piece whose rows complete the group reads the
+// accumulator back, regularizes and rounds. acc, the flag words and the counters are zero on entry
+// (the launch clears them first).
+template <int DT>
+__global__ void __launch_bounds__(STR_WARPS * 32, 1)
+k_sum_strided_sk(const typename StrLd<DT>::T* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner,
+                 StrOut o, int64_t* __restrict__ acc, uint32_t* __restrict__ aflags, uint32_t* __restrict__ cnt,
+                 uint32_t one, uint32_t mone) {
+    extern __shared__ __align__(16) int64_t win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t* col = win + warp * (D * 32) + lane;
+    const uint64_t gpr = (inner + 31) / 32;
+    const uint64_t F = outer * inner;
+    auto range = [&](uint64_t grp, uint64_t r0, uint64_t r1, uint64_t, int mode) {
+        const uint64_t ob = grp / gpr, i = (grp % gpr) * 32 + lane;
+        const bool act = i < inner;
+        const uint64_t f = ob * inner + i;
+#pragma unroll
+        for (int j = 0; j < D; ++j) col[j * 32] = 0;
+        uint32_t flags = 0;
+        if (act) strided_rows<DT>(x, ob, i, len, inner, r0, r1, col, flags, one, mone);
+        if (mode == 2) {                                       // a piece: add into acc[j][f]
+            if (act) {
+#pragma unroll 6
+                for (int j = 0; j < D; ++j)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(acc + (uint64_t)j * F + f),
+                              (unsigned long long)col[j * 32]);
+                if (flags) atomicOr(aflags + f, flags);
+            }
+            if (!sk_piece_done(cnt + grp, r1 - r0, len, lane)) return;
+            if (act) {                                         // this piece completes the group
+#pragma unroll 6
+                for (int j = 0; j < D; ++j)
+                    col[j * 32] = __ldcg(reinterpret_cast<const long long*>(acc + (uint64_t)j * F + f));
+                flags = __ldcg(aflags + f);
+                regularize_column(col);
+            }
+        }
+        if (act) lane_store(col, flags, o, f);
+    };
+    sk_or_parts<true, STR_WARPS>(outer * gpr, len, 1, len, outer * gpr, lane, warp, range);
+}
+
+// Stream-K pays off when the warp items leave resident warp slots idle (a wave-quantization loss
+// above 4%) and len fits the 32-bit row counters; its work: acc [D][F] int64 + flags [F] + counters.
+static bool strided_sk_wanted(uint64_t outer, uint64_t len, uint64_t inner, int num_sms, uint64_t fpw = 32) {
+    const uint64_t items = outer * ((inner + fpw - 1) / fpw), slots = (uint64_t)num_sms * STR_WARPS;
+    if (items == 0 || len < 64 || len >= (1ull << 31)) return false;
+    const uint64_t waves = (items + slots - 1) / slots;
+    return (double)(waves * slots - items) > 0.04 * (double)(waves * slots);
+}
+static size_t strided_sk_bytes(uint64_t outer, uint64_t inner) {
+    const uint64_t F = outer * inner, groups = outer * ((inner + 31) / 32);
+    return (size_t)F * (D * sizeof(int64_t) + sizeof(uint32_t)) + (size_t)groups * sizeof(uint32_t);
 }
 
 // ---------------------------------------------------------------------------------------------

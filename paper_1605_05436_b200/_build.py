@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 SO = os.path.join(HERE, "libxsum.so")
 SOURCES = ["api.cu", "accumulate.cu", "accumulate_h16.cu", "accumulate_f32.cu", "merge_finalize.cu", "segments.cu", "segments_small.cu", "strided.cu", "segments_lanes.cu", "segments_half.cu", "condsens.cu"]
-HEADERS = ["xsum_device.cuh", "xsum_kernels.h", "grid_tail.cuh", "h16_common.cuh", "lane_round.cuh",
+HEADERS = ["band_round.cuh", "xsum_device.cuh", "xsum_kernels.h", "grid_tail.cuh", "h16_common.cuh", "lane_round.cuh",
            "f32_bins.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -9,6 +9,7 @@
 // (segments_lanes.cu: one lane per segment).
 #include <cuda_runtime.h>
 
+#include "band_round.cuh"
 #include "xsum_device.cuh"
 #include "xsum_kernels.h"
 
@@ -44,6 +45,37 @@ __device__ __noinline__ void seg_rescan(int64_t* col, const uint4* body, uint64_
 __device__ __forceinline__ void segment_epilogue_top(int64_t* wb, int64_t* su, uint32_t flags, int top,
                                                      uint64_t len, uint64_t s, const SegOut& o, int lane) {
     __syncwarp();
+    if (!o.canon && top < 31) {
+        // values only, every chunk in rows <= top < 31 (the top carry lands in row top + 1 <= 31):
+        // one row per lane, read straight-line (column lane ^ c at step c: a conflict-free
+        // permutation) and zeroed, then the per-slot regularization / canonicalization / rounding
+        // of band_round.cuh with the whole warp as one slot of 32 digits (LPS = 32, NK = 1).
+        SlotSums<32> d;
+        d.hs[0] = d.ls[0] = d.hs[1] = d.ls[1] = 0;
+        if (lane <= top) {
+            int64_t* row = wb + lane * 32;
+#pragma unroll
+            for (int c0 = 0; c0 < 32; c0 += 8) {
+                int64_t v[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) v[c] = row[lane ^ (c0 + c)];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) row[lane ^ (c0 + c)] = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    d.hs[0] += v[c] >> 32;
+                    d.ls[0] += (int64_t)(uint32_t)v[c];
+                }
+            }
+        }
+        __syncwarp();
+        int64_t a[SlotSums<32>::KD];
+        slot_digits<32, 1>(d, a, lane, 0);
+        flags = __reduce_or_sync(FULL, flags);
+        xsum_result r = slot_finalize<32, 1>(a, flags, len, nullptr, su, lane, 0, 0);
+        if (lane == 0) o.write(s, r);
+        return;
+    }
     LaneSums t = {0, 0, 0, 0};
     const bool hi_rows = top >= 32;                  // warp-uniform
 #pragma unroll 8

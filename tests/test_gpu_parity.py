@@ -721,3 +721,26 @@ def test_segments_half_fast_rounding_boundaries(xs, fill):
     assert (f.cpu().numpy().astype(np.uint32) == fl).all()
     v2, _, _ = xs.sum_segments(d, L)
     assert (v2.cpu().numpy().view(np.uint64) == b64).all()
+
+
+def test_csr_segments_values_only_bands(xs):
+    """K6's values-only CSR epilogue (one row per lane, the whole warp as one slot of band_round.cuh)
+    and its fallbacks (exponents reaching row 31, NaN / Inf rescans, canonical images): ragged CSR
+    segments (empty, single elements, partial tiles, > 8K) with a different exponent band in each;
+    value and flags of every segment vs the oracle, and the same values with images requested."""
+    import torch
+    rng = np.random.default_rng(4242)
+    lens = np.concatenate([[0, 1, 2, 255, 256, 257, 9000], rng.integers(0, 3000, 150)])
+    rng.shuffle(lens)
+    full = _band_segments(rng, lens.size, 9000).reshape(lens.size, 9000)   # every kind, cut to length
+    x = np.concatenate([full[s, :int(L)] for s, L in enumerate(lens)])
+    off = np.zeros(lens.size + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    d = to_dev(x, 0)
+    o = torch.from_numpy(off).cuda()
+    vals, _, flags = xs.sum_segments_csr(d, o, flags=True)
+    b64, _, fl, _ = oracle.sum_segments(x, offsets=off)
+    assert (vals.cpu().numpy().view(np.uint64) == b64).all()
+    assert (flags.cpu().numpy().astype(np.uint32) == fl).all()
+    vals2, _, _ = xs.sum_segments_csr(d, o, canon=True)
+    assert (vals2.cpu().numpy().view(np.uint64) == b64).all()

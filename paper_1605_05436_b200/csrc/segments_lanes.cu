@@ -327,7 +327,8 @@ __device__ __forceinline__ void lane_epilogue64_fast(int64_t* col, uint32_t flag
     if (!o.canon) {
         uint64_t b64 = 0;
         uint32_t b32 = 0, rf = 0;
-        if (lane_fast_round(col, lo, hi, (int64_t)len, o.out || o.flags, o.out32 || o.flags, b64, b32, rf)) {
+        if (lane_fast_round(col, lo, hi, (int64_t)len, o.out || o.flags, o.out32 || o.flags, o.flags != nullptr, b64,
+                            b32, rf)) {
 #pragma unroll 4
             for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
             lane_store_bits(b64, b32, rf, flags, o, s);

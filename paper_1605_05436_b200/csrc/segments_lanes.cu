@@ -504,23 +504,26 @@ k_segments_lanes64s(const double* __restrict__ x, uint64_t nseg, uint32_t len, S
         uint32_t flags = 0;
         if (mine) {
             const uint4* sv = reinterpret_cast<const uint4*>(stage + b * SLS_STAGE + (size_t)lane * len * 8);
-            uint32_t nspec = 0;
-            auto addc = [&](uint32_t xl, uint32_t xh) {
-                const Chunks c = decompose(xl, xh, one, mone);
-                nspec = spec_fold(nspec, c);
-                column_add(col, c, one);
-                lo = min(lo, (int)c.i);
-                hi = max(hi, (int)c.i + 1);
-            };
+            // the exponent band of the segment in ONE packed 16x2 max per two summands (lo16: max k,
+            // also the NaN/Inf detector; hi16: 0xFFFF - min k), as K6z: chunks land in digits
+            // [k_min / 52, k_max / 52 + 1]
+            uint32_t band = 0;
+            auto key = [&](const Chunks& c) { return mad_u32(c.spec, 0xFFFF0001u, 0xFFFF0000u); };
             uint32_t u = (uint32_t)lane % nv;                    // rotated start: distinct banks
 #pragma unroll 4
             for (uint32_t q = 0; q < nv; ++q) {
                 const uint4 v = sv[u];
-                addc(v.x, v.y);
-                addc(v.z, v.w);
+                const Chunks ca = decompose(v.x, v.y, one, mone);
+                column_add(col, ca, one);
+                const Chunks cb = decompose(v.z, v.w, one, mone);
+                column_add(col, cb, one);
+                band = __vmaxu2(__vmaxu2(band, key(ca)), key(cb));
                 u = u + 1 == nv ? 0 : u + 1;
             }
-            if (spec_hit(nspec)) {                               // rare: cancel NaN/Inf patterns (R10)
+            const int kmax = (int)(band & 0xFFFFu), kmin = 0xFFFF - (int)(band >> 16);
+            lo = kmin / 52;
+            hi = kmax / 52 + 1;
+            if (spec_hit((uint32_t)kmax)) {                      // rare: cancel NaN/Inf patterns (R10)
                 for (uint32_t q = 0; q < nv; ++q) {
                     const uint4 v = sv[q];
                     column_fix_special(col, v.x, v.y, flags, one);

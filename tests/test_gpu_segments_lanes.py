@@ -256,3 +256,47 @@ def test_lanes_f64_two_digit_rounding_boundaries(xs, L):
     assert (f.cpu().numpy().astype(np.uint32) == fl).all()
     v2, _, _ = xs.sum_segments(d, L)                        # values alone (binary64 rounding only)
     assert (v2.cpu().numpy().view(np.uint64) == b64).all()
+
+
+@pytest.mark.parametrize("L", [2, 8, 16])
+def test_lanes_f64_values_only_representable_tops(xs, L):
+    """K11s without flags decides the rounding next to representable values from the top digits
+    (lane_fast_round, need_flags false): a segment's largest element isolated 60-900 binades above
+    the rest (its sum is representable up to a tail far below half an ulp), at powers of two (a
+    negative tail moves the exact sum into the lower binade), at the largest mantissa, next to
+    DBL_MAX (finite) and at the overflow midpoint, both signs; values alone and with flags (the
+    strict test) vs the oracle."""
+    import torch
+    rng = np.random.default_rng(900 + L)
+    nseg = 4096
+    x = np.zeros((nseg, L))
+    for s in range(nseg):
+        kind = s % 4
+        e = int(rng.integers(-800, 1000))
+        sg = 1.0 if rng.random() < 0.5 else -1.0
+        if kind == 0:
+            top = 2.0 ** e
+        elif kind == 1:
+            top = (2.0 - 2.0 ** -52) * 2.0 ** min(e, 1022)
+        elif kind == 2:
+            top = float(rng.integers(1 << 52, 1 << 53)) * 2.0 ** (min(e, 960) - 52)
+        else:
+            top = np.finfo(np.float64).max
+        x[s, 0] = sg * top
+        if L >= 2:
+            if kind == 3 and rng.random() < 0.5:
+                x[s, 1] = sg * 2.0 ** 970                        # the overflow midpoint (ties to even: Inf)
+            else:
+                te = int(np.log2(abs(top))) - int(rng.integers(60, 900))
+                for k in range(1, L):
+                    r = rng.random()
+                    x[s, k] = 0.0 if r < 0.2 else (1.0 if r < 0.6 else -1.0) * 2.0 ** max(te - int(rng.integers(0, 60)), -1074)
+    x = x.reshape(-1)
+    x[~np.isfinite(x)] = 0.0
+    d = torch.from_numpy(x).cuda()
+    b64, b32, fl, _ = oracle.sum_segments(x, seg_len=L)
+    v, _, _ = xs.sum_segments(d, L)
+    assert (v.cpu().numpy().view(np.uint64) == b64).all()
+    v2, _, f = xs.sum_segments(d, L, flags=True)
+    assert (v2.cpu().numpy().view(np.uint64) == b64).all()
+    assert (f.cpu().numpy().astype(np.uint32) == fl).all()

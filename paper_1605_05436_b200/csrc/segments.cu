@@ -110,7 +110,11 @@ __device__ __forceinline__ uint32_t kidx(uint32_t hi) { return max((hi >> 20) & 
 #ifndef XS_SEGC_MINB
 #define XS_SEGC_MINB 1
 #endif
+#ifndef XS_SEGC_NB
+#define XS_SEGC_NB 2      // rotating tile buffers of the CSR loop
+#endif
 constexpr int SEGC_WARPS = XS_SEGC_WARPS;
+constexpr int SEGC_NB = XS_SEGC_NB;
 constexpr size_t SEGC_SMEM = (size_t)SEGC_WARPS * D * 32 * sizeof(int64_t);
 
 __global__ void __launch_bounds__(SEGC_WARPS * 32, XS_SEGC_MINB)
@@ -157,11 +161,17 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
     uint64_t cb = 0, ce = 0, ob = 0, oe = 0;
     bounds(s, cb, ce);
     Seg g = open_seg(cb, ce);
-    uint4 cur[SEG_U];
-    if (g.nit) {
+    // SEGC_NB register buffers rotate without moves (tile t of a segment in buf[t % SEGC_NB]): while
+    // one tile is decoded the next SEGC_NB - 1 are in flight; the first SEGC_NB - 1 tiles of the next
+    // segment are fetched before the current segment's epilogue
+    uint4 buf[SEGC_NB][SEG_U];
+    auto load_tile = [&](uint4 (&bf)[SEG_U], const uint4* body, uint64_t t) {
 #pragma unroll
-        for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
-    }
+        for (int u = 0; u < SEG_U; ++u) bf[u] = ldg_stream(body + t * (32 * SEG_U) + u * 32 + lane);
+    };
+#pragma unroll
+    for (int b = 0; b < SEGC_NB - 1; ++b)
+        if ((uint64_t)b < g.nit) load_tile(buf[b], g.body, b);
     while (true) {
         const uint64_t sn = seg_next(ticket, s, nw, lane);
         bounds(sn, ob, oe);                                          // next segment's bounds, early
@@ -171,9 +181,6 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         const uint4* body = g.body;
         uint64_t wstart = 0;
         int since = 0;
-        // two register buffers alternate without copies (a copy would wait for the loads in
-        // flight): tile it+1 loads while tile it is decoded
-        uint4 alt[SEG_U];
         auto process = [&](const uint4 (&bf)[SEG_U], uint64_t it) {
 #pragma unroll
             for (int u = 0; u < SEG_U; ++u) {
@@ -199,18 +206,13 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
                 wstart = it + 1;
             }
         };
-        for (uint64_t it = 0; it < nit; it += 2) {
-            if (it + 1 < nit) {
+        for (uint64_t it = 0; it < nit; it += SEGC_NB) {
 #pragma unroll
-                for (int u = 0; u < SEG_U; ++u) alt[u] = ldg_stream(body + (it + 1) * (32 * SEG_U) + u * 32 + lane);
+            for (int b = 0; b < SEGC_NB; ++b) {
+                if (it + b >= nit) break;                            // warp-uniform
+                if (it + b + SEGC_NB - 1 < nit) load_tile(buf[(b + SEGC_NB - 1) % SEGC_NB], body, it + b + SEGC_NB - 1);
+                process(buf[b], it + b);
             }
-            process(cur, it);
-            if (it + 1 >= nit) break;
-            if (it + 2 < nit) {
-#pragma unroll
-                for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(body + (it + 2) * (32 * SEG_U) + u * 32 + lane);
-            }
-            process(alt, it + 1);
         }
         // leftover vectors (issued together before use), head and tail: checked adds
         uint4 lv[SEG_U];
@@ -248,10 +250,9 @@ k_segments(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, const 
         const uint64_t len = g.len;
         if (more) {
             g = open_seg(ob, oe);
-            if (g.nit) {
 #pragma unroll
-                for (int u = 0; u < SEG_U; ++u) cur[u] = ldg_stream(g.body + u * 32 + lane);
-            }
+            for (int b = 0; b < SEGC_NB - 1; ++b)
+                if ((uint64_t)b < g.nit) load_tile(buf[b], g.body, b);
         }
         // checked adds of the head / tail / leftovers may reach any digit: include them
         int top = flushed ? D : (int)(max(kmax, nspec) / 52u) + 1;

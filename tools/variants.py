@@ -72,6 +72,7 @@ VARIANTS = {
     "strsk0": ["-DXS_STR_SK=0"],
     "segc_w16": ["-DXS_SEGC_WARPS=16", "-DXS_SEGC_MINB=1"],
     "sseg_w16": ["-DXS_SSEG_WARPS=16", "-DXS_SSEG_MINB=1"],
+    "segc_nb3": ["-DXS_SEGC_NB=3"],
     "exp_sz_noepi": ["-DXS_EXP_SZ_NOEPI"],
 }
 

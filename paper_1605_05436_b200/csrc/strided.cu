@@ -441,7 +441,9 @@ k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, 
     }
 }
 
-// K10s for K10h: the kernel above as stream-K pieces (sk_or_parts<true>: modes 0 and 2 only)
+// K10s for K10h: the kernel above as stream-K pieces (sk_or_parts<true>: modes 0 and 2 only). One
+// templated body for both made ptxas spill 230-370 B in the row-parts instantiation (the lambda's
+// captures), so the stream-K form is a separate kernel.
 template <class F>
 __global__ void __launch_bounds__(STRH_WARPS * 32, 1)
 k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,
@@ -715,7 +717,8 @@ k_sum_strided_f32(const uint32_t* __restrict__ x, uint64_t outer, uint64_t len, 
     }
 }
 
-// K10s for K10f: the kernel above as stream-K pieces (sk_or_parts<true>: modes 0 and 2 only)
+// K10s for K10f: the kernel above as stream-K pieces (sk_or_parts<true>: modes 0 and 2 only; a
+// separate kernel for the same reason as k_sum_strided_h16_sk).
 template <class F>
 __global__ void __launch_bounds__(STR_WARPS * 32, 1)
 k_sum_strided_f32_sk(const uint32_t* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,

@@ -294,6 +294,10 @@ constexpr int STRH_WARPS = 16;
 #define XS_STRH_NB 4
 #endif
 constexpr int STRH_UNR = XS_STRH_UNR, STRH_NB = XS_STRH_NB;
+// K10h rows per group: bfloat16 8 (its kernel is large enough for instruction-cache stalls at 16:
+// 1477 vs 1430 G/s on [4096, 65536] over dim 0), binary16 16 (1755 vs 1586 at 8)
+template <class F>
+constexpr int strh_unr() { return F::t == 7 ? 8 : STRH_UNR; }
 template <class F>
 constexpr size_t strh_smem() {
     return (size_t)STRH_WARPS * 32 * 2 * (H16Col<F>::COLS * 8 + F::NBIN * 4);
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(STRH_WARPS * 32, 1)
 k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, uint64_t inner, uint32_t parts,
                   StrOut o, int64_t* __restrict__ work, uint32_t* __restrict__ wflags, uint32_t one, uint32_t mone) {
     using C = H16Col<F>;
+    constexpr int HU = strh_unr<F>();                          // rows per group
     extern __shared__ __align__(16) int64_t win[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t* const colw = win + warp * (2 * C::COLS * 32);
@@ -341,7 +346,7 @@ k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, 
     const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(bins[0]);
     const uint32_t sb1 = (uint32_t)__cvta_generic_to_shared(bins[1]);
     const uint32_t sb2 = sb0 + (sb1 << 16);                     // low half -> fibre i, high half -> i + 1
-    constexpr uint32_t WIN = (uint32_t)(F::FLUSH / STRH_UNR) * STRH_UNR;   // rows per bin window
+    constexpr uint32_t WIN = (uint32_t)(F::FLUSH / HU) * HU;   // rows per bin window
     const uint64_t gpr = (inner + 63) / 64;
     const uint64_t items = outer * gpr * parts;
     const uint64_t plen = (len + parts - 1) / parts;
@@ -364,16 +369,16 @@ k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, 
         uint32_t flushes = 0;
         if (act) {
             const uint32_t* q = reinterpret_cast<const uint32_t*>(x + (ob * len + r0) * inner + i);
-            const uint64_t ngroups = (r1 - r0) / STRH_UNR;
-            uint32_t buf[STRH_NB][STRH_UNR];
+            const uint64_t ngroups = (r1 - r0) / HU;
+            uint32_t buf[STRH_NB][HU];
             const uint32_t* lq = q;
             uint64_t lg = 0;
 #pragma unroll
             for (int b = 0; b < STRH_NB - 1; ++b) {
                 if (lg < ngroups) {
 #pragma unroll
-                    for (int u = 0; u < STRH_UNR; ++u) buf[b][u] = __ldcs(lq + u * wstride);
-                    lq += STRH_UNR * wstride;
+                    for (int u = 0; u < HU; ++u) buf[b][u] = __ldcs(lq + u * wstride);
+                    lq += HU * wstride;
                     ++lg;
                 }
             }
@@ -384,15 +389,15 @@ k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, 
                     if (g >= ngroups) break;
                     if (lg < ngroups) {
 #pragma unroll
-                        for (int u = 0; u < STRH_UNR; ++u)
+                        for (int u = 0; u < HU; ++u)
                             buf[(b + STRH_NB - 1) % STRH_NB][u] = __ldcs(lq + u * wstride);
-                        lq += STRH_UNR * wstride;
+                        lq += HU * wstride;
                         ++lg;
                     }
 #pragma unroll
-                    for (int u = 0; u < STRH_UNR; ++u) h16_add_word<F>(sb1, sb2, buf[b][u], one, mone);
+                    for (int u = 0; u < HU; ++u) h16_add_word<F>(sb1, sb2, buf[b][u], one, mone);
                     ++g;
-                    since += STRH_UNR;
+                    since += HU;
                     if (since == WIN) {                          // bin window full: empty into the columns
                         special |= h16_flush_col<F>(bins[0], col[0]);
                         special |= h16_flush_col<F>(bins[1], col[1]);
@@ -405,7 +410,7 @@ k_sum_strided_h16(const uint16_t* __restrict__ x, uint64_t outer, uint64_t len, 
                     }
                 }
             }
-            for (uint64_t r = r0 + ngroups * STRH_UNR; r < r1; ++r) {   // < STRH_UNR rows left: in the window
+            for (uint64_t r = r0 + ngroups * HU; r < r1; ++r) {   // < HU rows left: in the window
                 h16_add_word<F>(sb1, sb2, __ldcs(q + (r - r0) * wstride), one, mone);
             }
             special |= h16_flush_col<F>(bins[0], col[0]);
@@ -450,6 +455,7 @@ k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t le
                   StrOut o, int64_t* __restrict__ work, uint32_t* __restrict__ wflags, uint32_t* __restrict__ cnt,
                   uint32_t one, uint32_t mone) {
     using C = H16Col<F>;
+    constexpr int HU = strh_unr<F>();                          // rows per group
     extern __shared__ __align__(16) int64_t win[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t* const colw = win + warp * (2 * C::COLS * 32);
@@ -459,7 +465,7 @@ k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t le
     const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(bins[0]);
     const uint32_t sb1 = (uint32_t)__cvta_generic_to_shared(bins[1]);
     const uint32_t sb2 = sb0 + (sb1 << 16);                     // low half -> fibre i, high half -> i + 1
-    constexpr uint32_t WIN = (uint32_t)(F::FLUSH / STRH_UNR) * STRH_UNR;   // rows per bin window
+    constexpr uint32_t WIN = (uint32_t)(F::FLUSH / HU) * HU;   // rows per bin window
     const uint64_t gpr = (inner + 63) / 64;
     const uint64_t items = outer * gpr * parts;
     const uint64_t plen = (len + parts - 1) / parts;
@@ -481,16 +487,16 @@ k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t le
         uint32_t flushes = 0;
         if (act) {
             const uint32_t* q = reinterpret_cast<const uint32_t*>(x + (ob * len + r0) * inner + i);
-            const uint64_t ngroups = (r1 - r0) / STRH_UNR;
-            uint32_t buf[STRH_NB][STRH_UNR];
+            const uint64_t ngroups = (r1 - r0) / HU;
+            uint32_t buf[STRH_NB][HU];
             const uint32_t* lq = q;
             uint64_t lg = 0;
 #pragma unroll
             for (int b = 0; b < STRH_NB - 1; ++b) {
                 if (lg < ngroups) {
 #pragma unroll
-                    for (int u = 0; u < STRH_UNR; ++u) buf[b][u] = __ldcs(lq + u * wstride);
-                    lq += STRH_UNR * wstride;
+                    for (int u = 0; u < HU; ++u) buf[b][u] = __ldcs(lq + u * wstride);
+                    lq += HU * wstride;
                     ++lg;
                 }
             }
@@ -501,15 +507,15 @@ k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t le
                     if (g >= ngroups) break;
                     if (lg < ngroups) {
 #pragma unroll
-                        for (int u = 0; u < STRH_UNR; ++u)
+                        for (int u = 0; u < HU; ++u)
                             buf[(b + STRH_NB - 1) % STRH_NB][u] = __ldcs(lq + u * wstride);
-                        lq += STRH_UNR * wstride;
+                        lq += HU * wstride;
                         ++lg;
                     }
 #pragma unroll
-                    for (int u = 0; u < STRH_UNR; ++u) h16_add_word<F>(sb1, sb2, buf[b][u], one, mone);
+                    for (int u = 0; u < HU; ++u) h16_add_word<F>(sb1, sb2, buf[b][u], one, mone);
                     ++g;
-                    since += STRH_UNR;
+                    since += HU;
                     if (since == WIN) {                          // bin window full: empty into the columns
                         special |= h16_flush_col<F>(bins[0], col[0]);
                         special |= h16_flush_col<F>(bins[1], col[1]);
@@ -522,7 +528,7 @@ k_sum_strided_h16_sk(const uint16_t* __restrict__ x, uint64_t outer, uint64_t le
                     }
                 }
             }
-            for (uint64_t r = r0 + ngroups * STRH_UNR; r < r1; ++r) {   // < STRH_UNR rows left: in the window
+            for (uint64_t r = r0 + ngroups * HU; r < r1; ++r) {   // < HU rows left: in the window
                 h16_add_word<F>(sb1, sb2, __ldcs(q + (r - r0) * wstride), one, mone);
             }
             special |= h16_flush_col<F>(bins[0], col[0]);

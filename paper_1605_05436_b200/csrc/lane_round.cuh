@@ -301,6 +301,9 @@ __device__ __forceinline__ bool lane_fast_round(const int64_t* col, int lo, int 
     const uint64_t mh = (uint64_t)(mag >> 64);
     if (!mh && ((uint64_t)mag >> 62) == 0) return false;           // |T| < 2^62
     const int pT = mh ? 127 - __clzll((long long)mh) : 63 - __clzll((long long)(uint64_t)mag);
+    // the value test below needs 2 len < 2^(s-2) with s >= pT - 52: pT >= 57 + log2(len) (len <= 16:
+    // any |T| >= 2^62; K11's rows of up to 256: 2^65)
+    if (pT < 57 + (32 - __clz((int)(len - 1 > 0 ? len - 1 : 1)))) return false;
     const unsigned __int128 dl = (unsigned __int128)len;
     bool ok = true;
     uint32_t r = 0;

@@ -320,7 +320,7 @@ __device__ __forceinline__ void lane_epilogue64(int64_t* col, uint32_t flags, co
 #ifndef XS_SL_FAST
 #define XS_SL_FAST 1
 #endif
-// K11s: the same, trying the two-digit rounding first (lane_fast_round; values only, len <= 16)
+// K11s / K11 binary64: the same, trying the top-digit rounding first (lane_fast_round; values only, len <= 256)
 __device__ __forceinline__ void lane_epilogue64_fast(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s,
                                                      int lo, int hi, uint32_t len) {
 #if XS_SL_FAST
@@ -377,14 +377,12 @@ k_segments_lanes64(const double* __restrict__ x, uint64_t nseg, uint64_t len, Se
         prefetch(g + gstride);
 #endif
         if (s >= nseg) continue;
-        int lo = D, hi = -1;                          // touched digit range of this segment
-        uint32_t nspec = 0, flags = 0;
+        // the segment's exponent band in one packed 16x2 max (lo16: max k, hi16: 0xFFFF - min k; K6z)
+        uint32_t band = 0, flags = 0;
         auto addc = [&](uint32_t xl, uint32_t xh) {
             const Chunks c = decompose(xl, xh, one, mone);
-            nspec = spec_fold(nspec, c);
             column_add(col, c, one);
-            lo = min(lo, (int)c.i);
-            hi = max(hi, (int)c.i + 1);
+            band = __vmaxu2(band, mad_u32(c.spec, 0xFFFF0001u, 0xFFFF0000u));
         };
 #if !XS_SL_PF
         {
@@ -418,14 +416,15 @@ k_segments_lanes64(const double* __restrict__ x, uint64_t nseg, uint64_t len, Se
             addc(v.x, v.y);
             addc(v.z, v.w);
         }
-        if (spec_hit(nspec)) {                        // rare: cancel the NaN/Inf patterns (R10)
+        const int lo = (0xFFFF - (int)(band >> 16)) / 52, hi = (int)(band & 0xFFFFu) / 52 + 1;
+        if (spec_hit(band & 0xFFFFu)) {               // rare: cancel the NaN/Inf patterns (R10)
             for (uint64_t q = 0; q < len; q += 2) {
                 const uint4 v = ld_v4_ca(pv + q / 2);
                 column_fix_special(col, v.x, v.y, flags, one);
                 column_fix_special(col, v.z, v.w, flags, one);
             }
         }
-        lane_epilogue64(col, flags, o, s, lo, hi);
+        lane_epilogue64_fast(col, flags, o, s, lo, hi, (uint32_t)len);
     }
 }
 

@@ -221,7 +221,7 @@ def test_lanes_f64_values_only_paths(xs, L, narrow):
     assert (f2.cpu().numpy().astype(np.uint32) == fl).all()
 
 
-@pytest.mark.parametrize("L", [2, 8, 16])
+@pytest.mark.parametrize("L", [2, 8, 16, 18, 64, 256])
 def test_lanes_f64_two_digit_rounding_boundaries(xs, L):
     """The values-only K11s epilogue rounds from the two top raw digits when they decide it
     (lane_fast_round) and otherwise runs the exact chain. Segments built at its decision
@@ -258,7 +258,7 @@ def test_lanes_f64_two_digit_rounding_boundaries(xs, L):
     assert (v2.cpu().numpy().view(np.uint64) == b64).all()
 
 
-@pytest.mark.parametrize("L", [2, 8, 16])
+@pytest.mark.parametrize("L", [2, 8, 16, 18, 64, 256])
 def test_lanes_f64_values_only_representable_tops(xs, L):
     """K11s without flags decides the rounding next to representable values from the top digits
     (lane_fast_round, need_flags false): a segment's largest element isolated 60-900 binades above

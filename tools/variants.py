@@ -130,6 +130,8 @@ elif {cfg!r} == "c5csr":
     csr = synth.csr_offsets("c5csr", device="cuda")
 elif {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
     pass
+elif {cfg!r} in ("c2s64", "c2s256"):
+    x = synth.device_generate("c2")
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = _D() if {cfg!r}.startswith("str") else _K() if {cfg!r} in ("cs2", "cs3") else xsum.Accumulator()
@@ -143,8 +145,8 @@ if {cfg!r} == "c5csr":
     acc = _C()
 if {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
     x = synth.device_bits({{"f16seg": "c2f16", "bf16seg": "c2bf16", "f32seg": "c2f32"}}[{cfg!r}])
-if {cfg!r}.endswith("seg") or {cfg!r} == "c5s16":
-    SEGL = 16 if {cfg!r} == "c5s16" else 4096
+if {cfg!r}.endswith("seg") or {cfg!r} in ("c5s16", "c2s64", "c2s256"):
+    SEGL = {{"c5s16": 16, "c2s64": 64, "c2s256": 256}}.get({cfg!r}, 4096)
     class _S:
         def sum(self, x):
             global seg_v
@@ -166,7 +168,7 @@ torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
 import hashlib
-check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16")) or {cfg!r}.startswith("str") else hex(r.bits)
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16", "s64", "s256")) or {cfg!r}.startswith("str") else hex(r.bits)
 print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)

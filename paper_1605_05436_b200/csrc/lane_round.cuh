@@ -312,8 +312,11 @@ __device__ __forceinline__ bool lane_fast_round(const int64_t* col, int lo, int 
         int sh = P - (prec - 1) > emin ? P - (prec - 1) : emin;    // lsb kept (absolute)
         const int sp = sh - base;                                  // ... in units of T: >= 10
         unsigned __int128 q, rem, half;
-        if (sp >= 120) {                                           // |A| < 2^(sh-1): rounds to zero
-            q = 0; rem = mag; half = (unsigned __int128)1 << 119;
+        if (sp >= 128) {                                           // |A| < 2^(sh-1): rounds to zero
+            // (mag < 2^127 <= 2^(sp-1); the bound was 120 until round 2, which sent a three-digit T of
+            // 2^119..2^126 with a binary32 rounding position 120..127 digits up into this branch
+            // against a wrong half of 2^119: a sum of ~2^-276 rounded to the smallest subnormal)
+            q = 0; rem = mag; half = (unsigned __int128)1 << 127;
         } else {
             q = mag >> sp;
             rem = mag & (((unsigned __int128)1 << sp) - 1);
@@ -323,7 +326,7 @@ __device__ __forceinline__ bool lane_fast_round(const int64_t* col, int lo, int 
         // 0 or of 2 half) the value is decided - every point within 2 dl << half rounds to it, in the
         // lower binade too (dl < 2^(sp-2)) - and only INEXACT needs the tail: decided unless the
         // caller wants the flags
-        if ((rem + dl > half && rem < half + dl) || (need_flags && (rem < dl || (sp < 120 && rem + dl > 2 * half)))) {
+        if ((rem + dl > half && rem < half + dl) || (need_flags && (rem < dl || (sp < 128 && rem + dl > 2 * half)))) {
             ok = false;
             return 0;
         }

@@ -102,6 +102,42 @@ __device__ __forceinline__ void lane_store_segment(int64_t* col, uint32_t flags,
     lane_store_top(lane_canonical_top(col, lo, hi), col, flags, o, s);
 }
 
+// End of a segment in the K11 kernels (any input format): the raw digits [lo, hi] (hi < 0: nothing added)
+// rounded and zeroed by one carry chain (lane_top_chain); the generic path when the image is wanted.
+__device__ __forceinline__ void lane_epilogue64(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
+                                                int hi) {
+    if (hi < 0) lo = hi = 0;
+    if (o.canon) {
+        hi = lane_regularize_range(col, lo, hi);
+        lane_store_segment(col, flags, o, s, lo, hi);
+#pragma unroll 4
+        for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+        return;
+    }
+    lane_store_top(lane_top_chain(col, lo, hi), col, flags, o, s);
+}
+#ifndef XS_SL_FAST
+#define XS_SL_FAST 1
+#endif
+// K11s / K11 binary64: the same, trying the top-digit rounding first (lane_fast_round; values only, len <= 256)
+__device__ __forceinline__ void lane_epilogue64_fast(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s,
+                                                     int lo, int hi, uint32_t len) {
+#if XS_SL_FAST
+    if (!o.canon) {
+        uint64_t b64 = 0;
+        uint32_t b32 = 0, rf = 0;
+        if (lane_fast_round(col, lo, hi, (int64_t)len, o.out || o.flags, o.out32 || o.flags, o.flags != nullptr, b64,
+                            b32, rf)) {
+#pragma unroll 4
+            for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+            lane_store_bits(b64, b32, rf, flags, o, s);
+            return;
+        }
+    }
+#endif
+    lane_epilogue64(col, flags, o, s, lo, hi);
+}
+
 template <int DT, bool VEC>
 __global__ void __launch_bounds__(SL_WARPS * 32, 1)
 k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint64_t len, SegOut o, uint32_t one) {
@@ -133,9 +169,11 @@ k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint
         const typename L::T* p = x + s * len;
         uint64_t r = 0;
         int since = 0;
+        bool regd = false;                           // a flush regularized the column
         auto flush = [&]() {
             if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
             since = 0;
+            regd = true;
         };
         if (VEC) {                                   // binary64, even length, 16-B aligned rows
             const uint4* pv = reinterpret_cast<const uint4*>(p);
@@ -165,6 +203,10 @@ k_segments_lanes(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, uint
             }
         }
         for (; r < len; ++r) addr(L::raw(p + r));   // < 8 left: within the window
+        if (!regd) {                                 // no regularization ran: raw digits, |y| <= len 2^52
+            lane_epilogue64_fast(col, flags, o, s, lo, hi, (uint32_t)len);
+            continue;
+        }
         flush();
         if (hi < 0) lo = hi = 0;
         lane_store_segment(col, flags, o, s, lo, hi);
@@ -220,11 +262,7 @@ k_segments_lanes_csr(const typename SlLd<DT>::T* __restrict__ x, uint64_t nseg, 
                 for (int u = 0; u < 8; ++u) addr(v[u]);
             }
             for (; r < len; ++r) addr(L::raw(p + r));
-            if (hi >= 0) hi = lane_regularize_range(col, lo, hi);
-            if (hi < 0) lo = hi = 0;
-            lane_store_segment(col, flags, o, s, lo, hi);
-#pragma unroll 4
-            for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
+            lane_epilogue64_fast(col, flags, o, s, lo, hi, (uint32_t)len);   // raw digits (<= 256 adds)
         }
         unsigned long long big = __ballot_sync(FULL, act && !small);
         while (big) {                                            // long segments: the whole warp
@@ -303,42 +341,6 @@ cudaError_t sum_segments_lanes_csr(const void* x, int dtype, uint64_t nseg, cons
 // pipe idle: ncu r01, 26% of stall samples on the first use of a load); NaN/Inf patterns are summed
 // unchecked like finite values and, if the lane saw one, cancelled by a rescan of its segment
 // (K2's scheme; <= 2 x 256 adds stay far inside the int64 headroom, so no flush is needed).
-// End of a segment in the binary64 K11 kernels: the raw digits [lo, hi] (hi < 0: nothing added)
-// rounded and zeroed by one carry chain (lane_top_chain); the generic path when the image is wanted.
-__device__ __forceinline__ void lane_epilogue64(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s, int lo,
-                                                int hi) {
-    if (hi < 0) lo = hi = 0;
-    if (o.canon) {
-        hi = lane_regularize_range(col, lo, hi);
-        lane_store_segment(col, flags, o, s, lo, hi);
-#pragma unroll 4
-        for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
-        return;
-    }
-    lane_store_top(lane_top_chain(col, lo, hi), col, flags, o, s);
-}
-#ifndef XS_SL_FAST
-#define XS_SL_FAST 1
-#endif
-// K11s / K11 binary64: the same, trying the top-digit rounding first (lane_fast_round; values only, len <= 256)
-__device__ __forceinline__ void lane_epilogue64_fast(int64_t* col, uint32_t flags, const SegOut& o, uint64_t s,
-                                                     int lo, int hi, uint32_t len) {
-#if XS_SL_FAST
-    if (!o.canon) {
-        uint64_t b64 = 0;
-        uint32_t b32 = 0, rf = 0;
-        if (lane_fast_round(col, lo, hi, (int64_t)len, o.out || o.flags, o.out32 || o.flags, o.flags != nullptr, b64,
-                            b32, rf)) {
-#pragma unroll 4
-            for (int j = lo; j <= hi; ++j) col[j * 32] = 0;
-            lane_store_bits(b64, b32, rf, flags, o, s);
-            return;
-        }
-    }
-#endif
-    lane_epilogue64(col, flags, o, s, lo, hi);
-}
-
 constexpr int SLP = 16;                     // elements prefetched per lane (8 x 16 B)
 #ifndef XS_SL_PF
 #define XS_SL_PF 1

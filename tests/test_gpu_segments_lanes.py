@@ -86,6 +86,12 @@ def test_short_segments_vs_oracle(xs, fmt, L, narrow):
         want = r.bits if fmt == "f64" else r.bits_f32
         assert int(v[s]) == want and int(fl[s]) == r.flags, (fmt, L, narrow, s)
         assert (cn[s] == limbs).all(), (fmt, L, narrow, s)
+    # without images: the top-digit rounding (values with flags: the strict test; values alone)
+    vals2, _, flags2 = xs.sum_segments(to_dev(b, fmt, off), L, flags=True)
+    vals3, _, _ = xs.sum_segments(to_dev(b, fmt, off), L)
+    assert vals2.cpu().numpy().tobytes() == vals.cpu().numpy().tobytes()
+    assert flags2.cpu().numpy().tobytes() == flags.cpu().numpy().tobytes()
+    assert vals3.cpu().numpy().tobytes() == vals.cpu().numpy().tobytes()
 
 
 def test_short_segments_both_roundings(xs):
@@ -178,6 +184,11 @@ def test_csr_lanes_vs_oracle(xs, fmt, mix):
                                                  torch.cuda.current_stream().cuda_stream)
         assert rc == 0
         runs.append((out.clone(), cnt.clone(), flt.clone()))
+    vo, _, fo = xs.sum_segments_csr(d, o, flags=True)                   # no images: top-digit rounding
+    va, _, _ = xs.sum_segments_csr(d, o)
+    assert vo.cpu().numpy().tobytes() == runs[0][0].cpu().numpy().tobytes()
+    assert fo.cpu().numpy().tobytes() == runs[0][2].cpu().numpy().tobytes()
+    assert va.cpu().numpy().tobytes() == runs[0][0].cpu().numpy().tobytes()
     for vals, canon, flags in runs:
         v = vals.cpu().numpy()
         v = v.view(np.uint64) if fmt == "f64" else v.view(np.uint32)
@@ -300,3 +311,29 @@ def test_lanes_f64_values_only_representable_tops(xs, L):
     v2, _, f = xs.sum_segments(d, L, flags=True)
     assert (v2.cpu().numpy().view(np.uint64) == b64).all()
     assert (f.cpu().numpy().astype(np.uint32) == fl).all()
+
+
+@pytest.mark.parametrize("L", [5, 6, 16, 64])
+def test_short_segments_tiny_sum_binary32(xs, L):
+    """Regression (round 2): a segment whose exact sum is ~2^-276 with a three-digit top T of ~2^122 -
+    far below binary32's least subnormal, so its binary32 rounding is -0 - rounded to the smallest
+    subnormal in lane_fast_round's rounds-to-zero branch (its bound on the rounding position was 120
+    where T reaches 2^126). The case came from test_short_segments_both_roundings' data (segment 383);
+    it is placed in every slot of a batch of segments, zero-padded to L (K11 generic / K11s / K11)."""
+    import torch
+    b = data("f64", 5 * 1000, 5, False)
+    base = b[383 * 5:384 * 5]
+    seg = np.zeros(L, dtype=b.dtype)                               # bit patterns; zeros pad
+    seg[:5] = base
+    nseg = 64
+    x = np.tile(seg, nseg)
+    d = to_dev(x, "f64", 0)
+    o64 = torch.empty(nseg, dtype=torch.float64, device="cuda")
+    o32 = torch.empty(nseg, dtype=torch.float32, device="cuda")
+    rc = xs.lib().xsum_sum_segments_ex(d.data_ptr(), 0, nseg, L, None, o64.data_ptr(), o32.data_ptr(), None, None,
+                                       torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    r, _ = ref("f64", seg)
+    assert r.bits_f32 == 0x80000000                                 # the oracle: -0 in binary32
+    assert (o64.cpu().numpy().view(np.uint64) == r.bits).all()
+    assert (o32.cpu().numpy().view(np.uint32) == r.bits_f32).all()

@@ -128,6 +128,12 @@ elif {cfg!r} in ("cs2", "cs3"):
 elif {cfg!r} == "c5csr":
     x = synth.device_generate("c5csr")
     csr = synth.csr_offsets("c5csr", device="cuda")
+elif {cfg!r} == "csrl32":                       # sparse-matrix-like rows: U[0, 32] doubles (K11c)
+    g = torch.Generator(device="cuda"); g.manual_seed(5)
+    lens = torch.randint(0, 33, (1 << 23,), device="cuda", generator=g)
+    csr = torch.zeros(lens.numel() + 1, dtype=torch.int64, device="cuda")
+    csr[1:] = torch.cumsum(lens, 0)
+    x = synth.device_generate("c2", 0, int(csr[-1].item()))
 elif {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
     pass
 elif {cfg!r} in ("c2s64", "c2s256"):
@@ -135,7 +141,7 @@ elif {cfg!r} in ("c2s64", "c2s256"):
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = _D() if {cfg!r}.startswith("str") else _K() if {cfg!r} in ("cs2", "cs3") else xsum.Accumulator()
-if {cfg!r} == "c5csr":
+if {cfg!r} in ("c5csr", "csrl32"):
     class _C:
         def sum(self, x):
             global seg_v
@@ -168,7 +174,7 @@ torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
 import hashlib
-check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16", "s64", "s256")) or {cfg!r}.startswith("str") else hex(r.bits)
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16", "s64", "s256", "l32")) or {cfg!r}.startswith("str") else hex(r.bits)
 print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)

@@ -14,8 +14,11 @@
 
 namespace xs {
 
+#ifndef XS_SH_MINB
+#define XS_SH_MINB 1
+#endif
 #ifndef XS_SH_WARPS
-#define XS_SH_WARPS 8
+#define XS_SH_WARPS 16     // K6h (segments of > 1008 summands per lane): one 16-warp block per SM (65536-long: 586 -> 606 G/s)
 #endif
 constexpr int SH_WARPS = XS_SH_WARPS;
 #ifndef XS_SH_U
@@ -82,7 +85,7 @@ __device__ __noinline__ void half_rescan(int64_t* col, const uint4* seg, uint32_
     }
 }
 
-__global__ void __launch_bounds__(SH_WARPS * 32, 2)
+__global__ void __launch_bounds__(SH_WARPS * 32, XS_SH_MINB)
 k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one, uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
     __shared__ int64_t su[SH_WARPS][SEGS][48];
@@ -402,7 +405,7 @@ cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, 
                               cudaStream_t s) {
     const uint64_t npairs = (nseg + SEGS - 1) / SEGS;          // groups of SEGS segments
     const uint64_t want = (npairs + SH_WARPS - 1) / SH_WARPS;
-    const uint64_t cap = (uint64_t)num_sms * 2;
+    const uint64_t cap = (uint64_t)num_sms * XS_SH_MINB;
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     const uint64_t wantz = (npairs + SZ_WARPS - 1) / SZ_WARPS;
     const uint64_t capz = (uint64_t)num_sms * XS_SZ_MINB;

@@ -15,7 +15,13 @@
 
 namespace xs {
 
-constexpr int SEG_WARPS = 8;
+#ifndef XS_SEGU_WARPS
+#define XS_SEGU_WARPS 8   // k_segments_uniform: warps per block, XS_SEGU_MINB blocks per SM
+#endif
+#ifndef XS_SEGU_MINB
+#define XS_SEGU_MINB 2
+#endif
+constexpr int SEG_WARPS = XS_SEGU_WARPS;
 #ifndef XS_SEG_U
 #define XS_SEG_U 4
 #endif
@@ -288,7 +294,7 @@ __device__ __noinline__ void seg_rescan_uniform(int64_t* col, const uint4* seg, 
     }
 }
 
-__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
+__global__ void __launch_bounds__(SEG_WARPS * 32, XS_SEGU_MINB)
 k_segments_uniform(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one,
                    uint32_t mone) {
     extern __shared__ __align__(16) int64_t win[];
@@ -414,7 +420,7 @@ cudaError_t sum_segments(const double* x, uint64_t nseg, uint64_t seg_len, const
     if (cudaError_t e = ensure_smem(k_segments, SEGC_SMEM, smem_set)) return e;
     if (cudaError_t e = ensure_smem(k_segments_uniform, SEG_SMEM, smem_set_u)) return e;
     uint64_t want = (nseg + SEG_WARPS - 1) / SEG_WARPS;
-    uint64_t cap = (uint64_t)num_sms * 2;   // two 8-warp blocks per SM (84 KiB smem each)
+    uint64_t cap = (uint64_t)num_sms * XS_SEGU_MINB;
     unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     const bool uniform = !offsets && seg_len >= SEG_TILE && seg_len % ((uint64_t)SEG_TILE * SEG_NB) == 0 &&
                          ((uintptr_t)x & 15) == 0 && seg_len / SEG_TILE < (1u << 31);

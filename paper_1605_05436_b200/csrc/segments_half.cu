@@ -221,8 +221,10 @@ k_segments_half(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, S
 #ifndef XS_SZ_NB
 #define XS_SZ_NB 2
 #endif
-constexpr int SZ_U = XS_SZ_U, SZ_NB = XS_SZ_NB;
-constexpr uint32_t SZ_TILE = LPS * SZ_U * 2;                  // doubles per segment tile
+// two shapes: U = XS_SZ_U (8) vectors per lane per tile for lengths that are multiples of 2 tiles of
+// 256 doubles (c5), U = 4 for the other multiples of 256 (e.g. rows of 768)
+constexpr int SZ_U1 = XS_SZ_U, SZ_NB1 = XS_SZ_NB, SZ_U2 = 4;
+constexpr uint32_t SZ_GRAN1 = LPS * SZ_U1 * 2 * SZ_NB1, SZ_GRAN2 = LPS * SZ_U2 * 2 * 2;
 // per-lane summands per segment: every digit of a zeroed column receives at most one chunk
 // (|chunk| <= 2^52) per summand and one per NaN/Inf cancellation: 2 * 1008 chunks < 2^11
 constexpr uint64_t SZ_MAX_LANE = FLUSH_ELEMS / 2;
@@ -300,6 +302,7 @@ constexpr size_t SZ_SMEM = (size_t)SZ_WARPS * D * 32 * sizeof(int64_t);
 #endif
 __device__ __forceinline__ uint4 sz_load(const uint4* p) { return XS_SZ_COH ? ld_stream(p) : ldg_stream(p); }
 
+template <int SZ_U, int SZ_NB>
 __global__ void __launch_bounds__(SZ_WARPS * 32, XS_SZ_MINB)
 k_segments_halfz(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, SegOut o, uint32_t one, uint32_t mone) {
     extern __shared__ __align__(128) int64_t winz[];           // 128-B aligned columns (the epilogue's XOR)
@@ -311,6 +314,7 @@ k_segments_halfz(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
     const uint64_t npairs = (nseg + SEGS - 1) / SEGS;
     const uint64_t gw = (uint64_t)blockIdx.x * SZ_WARPS + warp;
     if (gw >= npairs) return;                                  // warp-uniform
+    constexpr uint32_t SZ_TILE = LPS * SZ_U * 2;                // doubles per segment tile
     const uint32_t TPS = (uint32_t)(seg_len / SZ_TILE);
     const uint64_t seg_vecs = seg_len / 2;
     const uint4* xv = reinterpret_cast<const uint4*>(x);
@@ -393,14 +397,15 @@ k_segments_halfz(const double* __restrict__ x, uint64_t nseg, uint64_t seg_len, 
     }
 }
 
-bool segments_half_ok(const double* x, uint64_t seg_len) {
-    return seg_len >= SH_TILE && seg_len % ((uint64_t)SH_TILE * SH_NB) == 0 && ((uintptr_t)x & 15) == 0 &&
-           seg_len / SH_TILE < (1u << 31);
-}
-
 #ifndef XS_SH_Z
 #define XS_SH_Z 1
 #endif
+bool segments_half_ok(const double* x, uint64_t seg_len) {
+    if (((uintptr_t)x & 15) != 0) return false;
+    if (XS_SH_Z && seg_len >= SZ_GRAN2 && seg_len % SZ_GRAN2 == 0 && seg_len / LPS <= SZ_MAX_LANE) return true;
+    return seg_len >= SH_TILE && seg_len % ((uint64_t)SH_TILE * SH_NB) == 0 && seg_len / SH_TILE < (1u << 31);
+}
+
 cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, const SegOut& o, int num_sms,
                               cudaStream_t s) {
     const uint64_t npairs = (nseg + SEGS - 1) / SEGS;          // groups of SEGS segments
@@ -410,10 +415,17 @@ cudaError_t sum_segments_half(const double* x, uint64_t nseg, uint64_t seg_len, 
     const uint64_t wantz = (npairs + SZ_WARPS - 1) / SZ_WARPS;
     const uint64_t capz = (uint64_t)num_sms * XS_SZ_MINB;
     const unsigned gz = (unsigned)(wantz < capz ? (wantz ? wantz : 1) : capz);
-    if (XS_SH_Z && seg_len / LPS <= SZ_MAX_LANE && seg_len % ((uint64_t)SZ_TILE * SZ_NB) == 0) {
+    if (XS_SH_Z && seg_len / LPS <= SZ_MAX_LANE && seg_len % SZ_GRAN1 == 0) {
         static unsigned long long smem_z = 0;
-        if (cudaError_t e = ensure_smem(k_segments_halfz, SZ_SMEM, smem_z)) return e;
-        k_segments_halfz<<<gz, SZ_WARPS * 32, SZ_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
+        if (cudaError_t e = ensure_smem(k_segments_halfz<SZ_U1, SZ_NB1>, SZ_SMEM, smem_z)) return e;
+        k_segments_halfz<SZ_U1, SZ_NB1><<<gz, SZ_WARPS * 32, SZ_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (XS_SH_Z && seg_len / LPS <= SZ_MAX_LANE && seg_len % SZ_GRAN2 == 0) {
+        static unsigned long long smem_z2 = 0;
+        if (cudaError_t e = ensure_smem(k_segments_halfz<SZ_U2, 2>, SZ_SMEM, smem_z2)) return e;
+        k_segments_halfz<SZ_U2, 2><<<gz, SZ_WARPS * 32, SZ_SMEM, s>>>(x, nseg, seg_len, o, 1u, 0xFFFFFFFFu);
         note_launch();
         return cudaGetLastError();
     }

@@ -667,7 +667,8 @@ def _band_segments(rng, nseg: int, seg_len: int) -> np.ndarray:
     return out.reshape(-1).view(np.float64)
 
 
-@pytest.mark.parametrize("seg_len,nseg", [(512, 45), (1024, 23), (4096, 33), (8192, 11), (15872, 11), (16384, 5)])
+@pytest.mark.parametrize("seg_len,nseg", [(512, 45), (768, 21), (1024, 23), (1280, 15), (4096, 33), (8192, 11), (15872, 11),
+                                         (16128, 3), (16384, 5)])
 def test_segments_half_band_values_only(xs, seg_len, nseg):
     """Values-only equal segments (K6z's banded epilogue: no canonical image requested) with a
     different exponent band in every segment and both halves of a warp on different bands: value

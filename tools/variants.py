@@ -73,7 +73,7 @@ VARIANTS = {
     "segc_w16": ["-DXS_SEGC_WARPS=16", "-DXS_SEGC_MINB=1"],
     "sseg_w16": ["-DXS_SSEG_WARPS=16", "-DXS_SSEG_MINB=1"],
     "segc_nb3": ["-DXS_SEGC_NB=3"],
-    "sh_w16": ["-DXS_SH_WARPS=16", "-DXS_SH_MINB=1"],
+    "segu_w16": ["-DXS_SEGU_WARPS=16", "-DXS_SEGU_MINB=1"],
     "exp_sz_noepi": ["-DXS_EXP_SZ_NOEPI"],
 }
 
@@ -137,8 +137,9 @@ elif {cfg!r} == "csrl32":                       # sparse-matrix-like rows: U[0, 
     x = synth.device_generate("c2", 0, int(csr[-1].item()))
 elif {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
     pass
-elif {cfg!r} in ("c2s64", "c2s256", "c2s64k"):
+elif {cfg!r} in ("c2s64", "c2s256", "c2s64k", "c2s768"):
     x = synth.device_generate("c2")
+    x = x[: x.numel() // 768 * 768] if {cfg!r} == "c2s768" else x
 else:
     x = synth.device_generate({cfg!r}.replace("seg", ""))
 acc = _D() if {cfg!r}.startswith("str") else _K() if {cfg!r} in ("cs2", "cs3") else xsum.Accumulator()
@@ -152,8 +153,8 @@ if {cfg!r} in ("c5csr", "csrl32"):
     acc = _C()
 if {cfg!r} in ("f16seg", "bf16seg", "f32seg"):
     x = synth.device_bits({{"f16seg": "c2f16", "bf16seg": "c2bf16", "f32seg": "c2f32"}}[{cfg!r}])
-if {cfg!r}.endswith("seg") or {cfg!r} in ("c5s16", "c2s64", "c2s256", "c2s64k"):
-    SEGL = {{"c5s16": 16, "c2s64": 64, "c2s256": 256, "c2s64k": 65536}}.get({cfg!r}, 4096)
+if {cfg!r}.endswith("seg") or {cfg!r} in ("c5s16", "c2s64", "c2s256", "c2s64k", "c2s768"):
+    SEGL = {{"c5s16": 16, "c2s64": 64, "c2s256": 256, "c2s64k": 65536, "c2s768": 768}}.get({cfg!r}, 4096)
     class _S:
         def sum(self, x):
             global seg_v
@@ -175,7 +176,7 @@ torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 res, _ = acc.sum(x); r = xsum.Result.from_bytes(res.cpu().numpy().tobytes())
 import hashlib
-check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16", "s64", "s256", "l32", "s64k")) or {cfg!r}.startswith("str") else hex(r.bits)
+check = hashlib.sha256(seg_v.cpu().numpy().tobytes()).hexdigest()[:16] if {cfg!r}.endswith(("seg", "csr", "s16", "s64", "s256", "l32", "s64k", "s768")) or {cfg!r}.startswith("str") else hex(r.bits)
 print(json.dumps(dict(so=os.path.basename({so!r}), cfg={cfg!r}, ms=ms, gdps=x.numel()/ms/1e6, gbs=x.element_size()*x.numel()/ms/1e6, check=check)))
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)

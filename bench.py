@@ -503,7 +503,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             # ~0.1 ms of device-side delay ahead of the first start event, so the host enqueues the
             # first steps while the stream is still busy: the region then holds device work only,
             # not the host's launch latency for step 0 (a 0.48 ms first step among 0.388 ms ones on c5)
-            torch.cuda._sleep(200_000)
+            if hasattr(torch.cuda, "_sleep"):
+                torch.cuda._sleep(200_000)
             for i in range(K):
                 if flush is not None:
                     flush.zero_()

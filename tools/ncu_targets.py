@@ -12,7 +12,7 @@ targets (kernel captured):
   merge1024   merge of 1024 state images              (k_merge)
   finalize    finalize_round of a state               (k_finalize)
   c5csr       c5csr CSR segments (bench workload)     (k_segments)
-  str_bf16 / str_f16 / str_f32  [4096, 65536] over dim 0 (k_sum_strided_h16 / _f32)
+  str_f64 / str_bf16 / str_f16 / str_f32  [4096, 65536] over dim 0 (K10s; k_sum_strided_h16 / _f32)
 """
 from __future__ import annotations
 
@@ -45,6 +45,10 @@ def main(t: str):
             xsum.sum_segments_csr(x, off)
     elif t == "strided_split":
         x = synth.device_generate("c2").view(1 << 20, 256)
+        for _ in range(3):
+            xsum.exact_sum_dim(x, 0)
+    elif t == "str_f64":
+        x = synth.device_generate("c2").view(4096, 65536)
         for _ in range(3):
             xsum.exact_sum_dim(x, 0)
     elif t in ("str_bf16", "str_f32", "str_f16"):

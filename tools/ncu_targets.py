@@ -11,6 +11,7 @@ targets (kernel captured):
   strided_split  [2^20, 256] doubles over dim 0       (k_sum_strided split + k_strided_merge)
   merge1024   merge of 1024 state images              (k_merge)
   finalize    finalize_round of a state               (k_finalize)
+  sparse      to_sparse of a state, then a merge of 1024 sparse images (k_to_sparse, k_merge)
   c5csr       c5csr CSR segments (bench workload)     (k_segments)
   str_f64 / str_bf16 / str_f16 / str_f32  [4096, 65536] over dim 0 (K10s; k_sum_strided_h16 / _f32)
 """
@@ -70,6 +71,19 @@ def main(t: str):
         a = xsum.Accumulator().add(synth.device_generate("c2", 0, 1 << 20))
         for _ in range(3):
             a.finalize_async(canon=True)
+    elif t == "sparse":
+        x = synth.device_generate("c2", 0, 1 << 22)
+        imgs, offs, pos = [], [], 0
+        for k in range(1024):
+            img, n = xsum.Accumulator().add(x[k * 4096:(k + 1) * 4096]).to_sparse()
+            imgs.append(img.clone())
+            offs.append(pos)
+            pos += n
+        images = torch.cat(imgs)
+        offsets = torch.tensor(offs, dtype=torch.int64, device="cuda")
+        m = xsum.Accumulator()
+        for _ in range(3):
+            m.reset().merge_sparse(images, offsets)
     elif t == "c5":
         x = synth.device_generate("c5")
         for _ in range(3):

@@ -5,6 +5,7 @@
 // digit-parallel with signed carries C in {-1,0,1} that move at most one digit.
 // Finalize: steps 6-7 of the PRAM algorithm, see finalize_warp.
 #include <cuda_runtime.h>
+#include <cstddef>
 
 #include "grid_tail.cuh"
 #include "xsum_device.cuh"
@@ -45,6 +46,7 @@ constexpr int MERGE_WARPS = 16;
 // (a0 = digit lane, a1 = digit lane+32). Returns false (image rejected) on a bad header or
 // digits that are not regularized.
 struct DenseImages {
+    static constexpr bool kPipelined = false;
     const xsum_state_image* ims;
     __device__ __forceinline__ bool load(uint32_t s, int lane, int64_t* /*scratch*/, int64_t& d0, int64_t& d1,
                                          uint64_t& cnt, uint32_t& fl) const {
@@ -61,28 +63,44 @@ struct DenseImages {
 // only the active indices are kept): a 24-byte header and nnz records (digit << 6) | index in
 // ascending index order (include/xsum.h). Image s starts at base + offs[s].
 struct SparseImages {
+    static constexpr bool kPipelined = true;
     const uint8_t* base;
     const uint64_t* offs;
-    __device__ __forceinline__ bool load(uint32_t s, int lane, int64_t* scratch, int64_t& d0, int64_t& d1,
-                                         uint64_t& cnt, uint32_t& fl) const {
-        const uint64_t off = offs[s];
+    // The three dependent loads of an image (offset -> header -> records) are software-pipelined by
+    // k_merge: offsets two images ahead, headers one ahead (ncu r02f: 1024 images in 117 us, stalls
+    // on long_scoreboard 14 per issued instruction, with the chain serialised per image).
+    struct Hdr {
+        uint64_t off, w0, w1, w2;      // w0: magic | version | w | nnz, w1: flags | reserved, w2: count
+    };
+    __device__ __forceinline__ uint64_t off_of(uint32_t s, uint32_t count) const { return s < count ? offs[s] : 0; }
+    __device__ __forceinline__ Hdr hdr_of(uint64_t off, bool valid) const {
+        Hdr h{off, 0, 0, 0};
+        if (valid && !(off & 7)) {
+            const uint64_t* p = reinterpret_cast<const uint64_t*>(base + off);
+            h.w0 = p[0];
+            h.w1 = p[1];
+            h.w2 = p[2];
+        }
+        return h;
+    }
+    __device__ __forceinline__ bool load_from(const Hdr& h, int lane, int64_t* scratch, int64_t& d0, int64_t& d1,
+                                              uint64_t& cnt, uint32_t& fl) const {
         d0 = d1 = 0;
         cnt = 0;
         fl = 0;
-        if (off & 7) return false;                                     // warp-uniform
-        const xsum_sparse_header* hd = reinterpret_cast<const xsum_sparse_header*>(base + off);
-        const uint32_t nnz = hd->nnz;
-        if (hd->magic != XSUM_SPARSE_MAGIC || hd->version != XSUM_VERSION || hd->w != W || nnz > (uint32_t)D)
-            return false;
-        const uint64_t* rec = reinterpret_cast<const uint64_t*>(base + off + sizeof(xsum_sparse_header));
+        if (h.off & 7) return false;                                   // warp-uniform
+        const uint32_t magic = (uint32_t)h.w0, version = (uint32_t)(h.w0 >> 32) & 0xFFFFu;
+        const uint32_t w = (uint32_t)(h.w0 >> 48) & 0xFFu, nnz = (uint32_t)(h.w0 >> 56);
+        if (magic != XSUM_SPARSE_MAGIC || version != XSUM_VERSION || w != W || nnz > (uint32_t)D) return false;
+        const uint64_t* rec = reinterpret_cast<const uint64_t*>(base + h.off + sizeof(xsum_sparse_header));
         scratch[lane] = 0;
         scratch[lane + 32] = 0;
         __syncwarp();
         bool ok = true;
         int prev_last = -1;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t r = (uint32_t)lane + 32u * h;
+        for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t r = (uint32_t)lane + 32u * hh;
             const bool has = r < nnz;
             const uint64_t v = has ? rec[r] : 0;
             const int idx = has ? (int)(v & 63u) : 64;
@@ -99,11 +117,14 @@ struct SparseImages {
         __syncwarp();
         d0 = scratch[lane];
         d1 = (lane + 32 < D) ? scratch[lane + 32] : 0;
-        cnt = hd->count;
-        fl = hd->flags;
+        cnt = h.w2;
+        fl = (uint32_t)h.w1;
         return __all_sync(FULL, ok) && cnt <= COUNT_MAX;
     }
 };
+static_assert(sizeof(xsum_sparse_header) == 24 && offsetof(xsum_sparse_header, nnz) == 7 &&
+              offsetof(xsum_sparse_header, flags) == 8 && offsetof(xsum_sparse_header, count) == 16,
+              "SparseImages::Hdr word layout");
 
 template <class Src>
 __global__ void __launch_bounds__(MERGE_WARPS * 32)
@@ -117,17 +138,37 @@ k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_resul
     uint64_t cnt = 0;
     uint32_t fl = 0;
     // leaves: each warp folds images warp, warp+16, ... (Lemma-1 adds)
-    for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
-        int64_t d0, d1;
-        uint64_t c;
-        uint32_t f;
-        if (src.load(s, lane, scr[warp], d0, d1, c, f)) {
+    auto fold = [&](bool ok, int64_t d0, int64_t d1, uint64_t c, uint32_t f) {
+        if (ok) {
             lemma1_add(a0, a1, d0, d1, lane);
             cnt = count_add(cnt, c, fl);
             fl |= f & (XSUM_F_NAN | XSUM_F_PINF | XSUM_F_NINF | XSUM_F_MISMATCH | XSUM_F_PEER_TIMEOUT |
                        XSUM_F_CAPACITY);
         } else {
             fl |= XSUM_F_MISMATCH;
+        }
+    };
+    if constexpr (Src::kPipelined) {
+        uint64_t off1 = src.off_of(warp + MERGE_WARPS, count);
+        typename Src::Hdr h = src.hdr_of(src.off_of(warp, count), warp < count);
+        for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
+            const uint64_t off2 = src.off_of(s + 2 * MERGE_WARPS, count);          // two images ahead
+            const typename Src::Hdr hn = src.hdr_of(off1, s + MERGE_WARPS < count);  // one ahead
+            int64_t d0, d1;
+            uint64_t c;
+            uint32_t f;
+            const bool ok = src.load_from(h, lane, scr[warp], d0, d1, c, f);
+            fold(ok, d0, d1, c, f);
+            h = hn;
+            off1 = off2;
+        }
+    } else {
+        for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
+            int64_t d0, d1;
+            uint64_t c;
+            uint32_t f;
+            const bool ok = src.load(s, lane, scr[warp], d0, d1, c, f);
+            fold(ok, d0, d1, c, f);
         }
     }
     acc[warp][lane] = a0;

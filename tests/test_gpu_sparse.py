@@ -90,3 +90,45 @@ def test_sparse_rejects_malformed_images(xs):
     r = xs.Accumulator().merge_sparse(blob, torch.tensor([0, len(good) + 4], dtype=torch.int64,
                                                          device="cuda")).result()
     assert r.flags & xs.F_MISMATCH
+
+
+@pytest.mark.parametrize("nimg", [17, 33, 48, 1000])
+def test_sparse_merge_many_images_with_bad_ones(xs, nimg):
+    """More images than the merge kernel's 16 leaf warps: every warp folds several images through
+    its pipelined offset / header / record loads (offsets two images ahead, headers one ahead).
+    Malformed images and a misaligned offset sit at positions the pipeline reaches from the
+    previous iterations; the good images' exact sum and count must match the oracle."""
+    import torch
+    rng = np.random.default_rng(nimg)
+    x = synth.gen.generate("c1", 11, 40 * nimg + 7)
+    cuts = np.sort(rng.integers(0, x.size, nimg - 1))
+    cuts = np.concatenate([[0], cuts, [x.size]])
+    bad_hdr = struct.pack("<IHBBIIQ", 0x41505359, 1, 52, 1, 0, 0, 1) + struct.pack("<q", (5 << 6) | 21)
+    bad_pos = {p for p in (16, 20, 45, 70, 999) if p < nimg}
+    mis_pos = 37 if nimg > 37 else None
+    parts, offs, off, good = [], [], 0, []
+    for i, (a, b) in enumerate(zip(cuts, cuts[1:])):
+        if i in bad_pos:
+            parts.append(np.frombuffer(bad_hdr, dtype=np.uint8))
+            offs.append(off)
+            off += len(bad_hdr)
+            continue
+        img, nb = xs.Accumulator().add(dev(x[a:b])).to_sparse()
+        if i == mis_pos:                                 # a 4-byte gap: this image's offset is misaligned
+            parts.append(np.zeros(4, dtype=np.uint8))
+            off += 4
+        else:
+            good.append(x[a:b])
+        parts.append(img.cpu().numpy())
+        offs.append(off)
+        off += nb
+        if i == mis_pos:                                 # realign the following images
+            parts.append(np.zeros(4, dtype=np.uint8))
+            off += 4
+    blob = torch.from_numpy(np.concatenate(parts)).cuda()
+    acc = xs.Accumulator().merge_sparse(blob, torch.tensor(offs, dtype=torch.int64, device="cuda"))
+    res, canon = acc.exact()
+    g = np.concatenate(good)
+    r, limbs = oracle.exact_sum(g)
+    assert res.bits == r.bits and (canon == limbs).all() and res.count == g.size
+    assert bool(res.flags & xs.F_MISMATCH) == bool(bad_pos or mis_pos is not None)

@@ -29,16 +29,8 @@ __global__ void k_init_state(xsum_state_image* st) {
     }
 }
 
-// A state image is accepted iff its header matches and its digits are regularized
+// A state image is accepted (DenseImages::load_from) iff its header matches and its digits are regularized
 // (|Y_j| <= R-1 below the top digit; top digit bounded by the value).
-__device__ __forceinline__ bool image_ok(const xsum_state_image* im, int64_t d0, int64_t d1, int lane) {
-    bool hdr = im->magic == XSUM_MAGIC && im->version == XSUM_VERSION && im->w == W && im->ndigits == D;
-    bool ok0 = d0 >= -(R - 1) && d0 <= R - 1;
-    bool ok1 = (lane + 32 < D - 1) ? (d1 >= -(R - 1) && d1 <= R - 1)
-                                   : ((lane + 32 == D - 1) ? (d1 >= -XSUM_TOP_DIGIT_MAX && d1 <= XSUM_TOP_DIGIT_MAX)
-                                                           : true);
-    return hdr && im->count <= COUNT_MAX && __all_sync(FULL, ok0 && ok1);
-}
 
 constexpr int MERGE_WARPS = 16;
 
@@ -46,24 +38,50 @@ constexpr int MERGE_WARPS = 16;
 // (a0 = digit lane, a1 = digit lane+32). Returns false (image rejected) on a bad header or
 // digits that are not regularized.
 struct DenseImages {
-    static constexpr bool kPipelined = false;
     const xsum_state_image* ims;
-    __device__ __forceinline__ bool load(uint32_t s, int lane, int64_t* /*scratch*/, int64_t& d0, int64_t& d1,
-                                         uint64_t& cnt, uint32_t& fl) const {
-        const xsum_state_image* im = ims + s;
-        d0 = im->digit[lane];
-        d1 = (lane + 32 < D) ? im->digit[lane + 32] : 0;
-        cnt = im->count;
-        fl = im->flags;
-        return image_ok(im, d0, d1, lane);
+    // k_merge's leaf pipeline (as for sparse images): image s + 16's header and digits are in flight
+    // while image s is validated and folded
+    struct Hdr {
+        uint64_t off, w0, w1, w2;      // off: the image index; w0: magic | version | w | ndigits,
+        int64_t d0, d1;                // w1: flags | reserved, w2: count; digits lane and lane + 32
+    };
+    __device__ __forceinline__ uint64_t off_of(uint32_t s, uint32_t /*count*/) const { return s; }
+    __device__ __forceinline__ Hdr hdr_of(uint64_t s, bool valid, int lane) const {
+        Hdr h{s, 0, 0, 0, 0, 0};
+        if (valid) {
+            const xsum_state_image* im = ims + s;
+            const uint64_t* p = reinterpret_cast<const uint64_t*>(im);
+            h.w0 = p[0];
+            h.w1 = p[1];
+            h.w2 = p[2];
+            h.d0 = im->digit[lane];
+            h.d1 = (lane + 32 < D) ? im->digit[lane + 32] : 0;
+        }
+        return h;
+    }
+    __device__ __forceinline__ bool load_from(const Hdr& h, int lane, int64_t* /*scratch*/, int64_t& d0, int64_t& d1,
+                                              uint64_t& cnt, uint32_t& fl) const {
+        d0 = h.d0;
+        d1 = h.d1;
+        cnt = h.w2;
+        fl = (uint32_t)h.w1;
+        const bool hdr = (uint32_t)h.w0 == XSUM_MAGIC && ((h.w0 >> 32) & 0xFFFFu) == XSUM_VERSION &&
+                         ((h.w0 >> 48) & 0xFFu) == (uint64_t)W && (h.w0 >> 56) == (uint64_t)D;
+        const bool ok0 = d0 >= -(R - 1) && d0 <= R - 1;
+        const bool ok1 = (lane + 32 < D - 1) ? (d1 >= -(R - 1) && d1 <= R - 1)
+                                             : ((lane + 32 == D - 1) ? (d1 >= -XSUM_TOP_DIGIT_MAX && d1 <= XSUM_TOP_DIGIT_MAX)
+                                                                     : true);
+        return hdr && cnt <= COUNT_MAX && __all_sync(FULL, ok0 && ok1);     
     }
 };
+static_assert(offsetof(xsum_state_image, ndigits) == 7 && offsetof(xsum_state_image, flags) == 8 &&
+              offsetof(xsum_state_image, count) == 16 && offsetof(xsum_state_image, digit) == 24,
+              "DenseImages::Hdr word layout");
 
 // Sparse images (the paper's sparse superaccumulator, PAPER.md:682-696:
 // only the active indices are kept): a 24-byte header and nnz records (digit << 6) | index in
 // ascending index order (include/xsum.h). Image s starts at base + offs[s].
 struct SparseImages {
-    static constexpr bool kPipelined = true;
     const uint8_t* base;
     const uint64_t* offs;
     // The three dependent loads of an image (offset -> header -> records) are software-pipelined by
@@ -73,7 +91,7 @@ struct SparseImages {
         uint64_t off, w0, w1, w2;      // w0: magic | version | w | nnz, w1: flags | reserved, w2: count
     };
     __device__ __forceinline__ uint64_t off_of(uint32_t s, uint32_t count) const { return s < count ? offs[s] : 0; }
-    __device__ __forceinline__ Hdr hdr_of(uint64_t off, bool valid) const {
+    __device__ __forceinline__ Hdr hdr_of(uint64_t off, bool valid, int /*lane*/) const {
         Hdr h{off, 0, 0, 0};
         if (valid && !(off & 7)) {
             const uint64_t* p = reinterpret_cast<const uint64_t*>(base + off);
@@ -148,28 +166,18 @@ k_merge(xsum_state_image* st, Src src, uint32_t count, int overwrite, xsum_resul
             fl |= XSUM_F_MISMATCH;
         }
     };
-    if constexpr (Src::kPipelined) {
-        uint64_t off1 = src.off_of(warp + MERGE_WARPS, count);
-        typename Src::Hdr h = src.hdr_of(src.off_of(warp, count), warp < count);
-        for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
-            const uint64_t off2 = src.off_of(s + 2 * MERGE_WARPS, count);          // two images ahead
-            const typename Src::Hdr hn = src.hdr_of(off1, s + MERGE_WARPS < count);  // one ahead
-            int64_t d0, d1;
-            uint64_t c;
-            uint32_t f;
-            const bool ok = src.load_from(h, lane, scr[warp], d0, d1, c, f);
-            fold(ok, d0, d1, c, f);
-            h = hn;
-            off1 = off2;
-        }
-    } else {
-        for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
-            int64_t d0, d1;
-            uint64_t c;
-            uint32_t f;
-            const bool ok = src.load(s, lane, scr[warp], d0, d1, c, f);
-            fold(ok, d0, d1, c, f);
-        }
+    uint64_t off1 = src.off_of(warp + MERGE_WARPS, count);
+    typename Src::Hdr h = src.hdr_of(src.off_of(warp, count), warp < count, lane);
+    for (uint32_t s = warp; s < count; s += MERGE_WARPS) {
+        const uint64_t off2 = src.off_of(s + 2 * MERGE_WARPS, count);          // two images ahead
+        const typename Src::Hdr hn = src.hdr_of(off1, s + MERGE_WARPS < count, lane);  // one ahead
+        int64_t d0, d1;
+        uint64_t c;
+        uint32_t f;
+        const bool ok = src.load_from(h, lane, scr[warp], d0, d1, c, f);
+        fold(ok, d0, d1, c, f);
+        h = hn;
+        off1 = off2;
     }
     acc[warp][lane] = a0;
     acc[warp][lane + 32] = a1;

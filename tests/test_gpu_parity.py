@@ -317,6 +317,25 @@ def test_merge_rejects_bad_images(xs):
     assert res.bits == 1 and res.count == 3            # only the good image counted: 2^-1074
 
 
+@pytest.mark.parametrize("k", [17, 40, 100])
+def test_merge_rejects_bad_images_past_first_leaf_round(xs, k):
+    """k images through the 16 leaf warps' pipelined loads (image s + 16 in flight while s folds):
+    malformed images at positions 16, 20, 33 and 99 (when present) are rejected, the rest counted."""
+    import torch
+    imgs, good_count = [], 0
+    for i in range(k):
+        if i in (16, 33):
+            imgs.append(_image([5] + [0] * 41, magic=0x12345678))
+        elif i in (20, 99):
+            imgs.append(_image([1 << 52] + [0] * 41))
+        else:
+            imgs.append(_image([1] + [0] * 41, count=3))
+            good_count += 1
+    res, canon = xs.Accumulator().merge(torch.from_numpy(np.concatenate(imgs)).cuda()).exact()
+    assert res.flags & xs.F_MISMATCH
+    assert res.bits == good_count and res.count == 3 * good_count       # good_count * 2^-1074
+
+
 def test_launch_counter_counts_kernels(xs):
     n0 = xs.launch_count()
     acc = xs.Accumulator()              # init kernel
